@@ -1,0 +1,570 @@
+/*
+ * ebb_oracle.c -- sequential fp64 CPU ORACLE for the Ebb tet-FEM hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant with the CUDA path
+ * (paper_1506_07577_b200/csrc); neither includes the other.
+ *
+ * Built with:  gcc -O2 -ffp-contract=off -fno-fast-math -std=c11 -fPIC -shared
+ * (no FMA contraction, no reassociation: the summation order written here is
+ * the order that is executed).
+ *
+ * Paper: Bernstein et al., "Ebb: A DSL for Physical Simulation on CPUs and
+ * GPUs" (arXiv 1506.07577), cited as P:<line of /root/reference/PAPER.md>.
+ * The paper names StVK, neo-Hookean, implicit backward Euler
+ * and Jacobi-PCG but prints no formulas; the textbook
+ * definitions used here are the readings listed in DESIGN.md §3 (from
+ * SURVEY.md §8(c) O1-O10).  Every function below names its step.
+ *
+ * Parity pins (tests/test_oracle_*.py, -m "not gpu"): see DESIGN.md §4.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_STVK 0
+#define ORC_NH 1
+
+/* ------------------------------------------------------------------ */
+/* small dense helpers (3x3, row-major A[r][c])                        */
+/* ------------------------------------------------------------------ */
+static double det3(const double A[3][3]) {
+    return A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1])
+         - A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0])
+         + A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+}
+
+/* inverse by adjugate / determinant */
+static void inv3(const double A[3][3], double R[3][3]) {
+    double d = det3(A);
+    double C[3][3]; /* cofactor matrix */
+    C[0][0] = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+    C[0][1] = -(A[1][0] * A[2][2] - A[1][2] * A[2][0]);
+    C[0][2] = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+    C[1][0] = -(A[0][1] * A[2][2] - A[0][2] * A[2][1]);
+    C[1][1] = A[0][0] * A[2][2] - A[0][2] * A[2][0];
+    C[1][2] = -(A[0][0] * A[2][1] - A[0][1] * A[2][0]);
+    C[2][0] = A[0][1] * A[1][2] - A[0][2] * A[1][1];
+    C[2][1] = -(A[0][0] * A[1][2] - A[0][2] * A[1][0]);
+    C[2][2] = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) R[r][c] = C[c][r] / d; /* adj = C^T */
+}
+
+static void matmul3(const double A[3][3], const double B[3][3], double R[3][3]) {
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += A[r][k] * B[k][c];
+            R[r][c] = s;
+        }
+}
+
+static void transpose3(const double A[3][3], double R[3][3]) {
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) R[r][c] = A[c][r];
+}
+
+/* Dm = [X1-X0, X2-X0, X3-X0] (columns), SURVEY O5 / P:944 rest data */
+static void edge_matrix(const double* P, const int64_t* tv, double D[3][3]) {
+    for (int k = 0; k < 3; ++k)
+        for (int a = 0; a < 3; ++a) D[a][k] = P[3 * tv[k + 1] + a] - P[3 * tv[0] + a];
+}
+
+/* ------------------------------------------------------------------ */
+/* O1  orientation: swap v2,v3 where det(Dm) < 0; reject degenerate     */
+/* returns number of swaps, or -(t+1) for the first degenerate tet t   */
+/* ------------------------------------------------------------------ */
+int64_t orc_orient(int64_t nv, const double* X, int64_t nt, int64_t* tets) {
+    (void)nv;
+    int64_t swaps = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+        int64_t* tv = tets + 4 * t;
+        double D[3][3];
+        edge_matrix(X, tv, D);
+        double d = det3(D);
+        double l = 0.0; /* longest edge */
+        for (int i = 0; i < 4; ++i)
+            for (int j = i + 1; j < 4; ++j) {
+                double s = 0.0;
+                for (int a = 0; a < 3; ++a) {
+                    double q = X[3 * tv[j] + a] - X[3 * tv[i] + a];
+                    s += q * q;
+                }
+                if (sqrt(s) > l) l = sqrt(s);
+            }
+        if (fabs(d) <= 1e-12 * l * l * l) return -(t + 1);
+        if (d < 0.0) {
+            int64_t tmp = tv[2];
+            tv[2] = tv[3];
+            tv[3] = tmp;
+            ++swaps;
+        }
+    }
+    return swaps;
+}
+
+/* ------------------------------------------------------------------ */
+/* O2  edge relation: sorted unique ordered pairs within a tet plus a   */
+/* self-loop per vertex (P:797 caption), grouped by tail     */
+/* (sort the target by the key, hidden [begin,end) index).       */
+/* returns E, or -1 if cap is too small.                                */
+/* ------------------------------------------------------------------ */
+typedef struct { int64_t tail, head; } pair_t;
+
+static int cmp_pair(const void* a, const void* b) {
+    const pair_t* x = (const pair_t*)a;
+    const pair_t* y = (const pair_t*)b;
+    if (x->tail != y->tail) return x->tail < y->tail ? -1 : 1;
+    if (x->head != y->head) return x->head < y->head ? -1 : 1;
+    return 0;
+}
+
+int64_t orc_edges(int64_t nv, int64_t nt, const int64_t* tets, int64_t cap,
+                  int64_t* tail, int64_t* head, int64_t* row_ptr, int64_t* e) {
+    int64_t np = nt * 16 + nv;
+    pair_t* P = (pair_t*)malloc(sizeof(pair_t) * (size_t)(np > 0 ? np : 1));
+    int64_t k = 0;
+    for (int64_t t = 0; t < nt; ++t)
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) {
+                P[k].tail = tets[4 * t + i];
+                P[k].head = tets[4 * t + j];
+                ++k;
+            }
+    for (int64_t v = 0; v < nv; ++v) {
+        P[k].tail = v;
+        P[k].head = v;
+        ++k;
+    }
+    qsort(P, (size_t)np, sizeof(pair_t), cmp_pair);
+    int64_t E = 0;
+    for (int64_t i = 0; i < np; ++i) {
+        if (i > 0 && P[i].tail == P[i - 1].tail && P[i].head == P[i - 1].head) continue;
+        if (E >= cap) { free(P); return -1; }
+        tail[E] = P[i].tail;
+        head[E] = P[i].head;
+        ++E;
+    }
+    free(P);
+    for (int64_t v = 0; v <= nv; ++v) row_ptr[v] = 0;
+    for (int64_t r = 0; r < E; ++r) row_ptr[tail[r] + 1] += 1;
+    for (int64_t v = 0; v < nv; ++v) row_ptr[v + 1] += row_ptr[v];
+    if (e) {
+        for (int64_t t = 0; t < nt; ++t)
+            for (int i = 0; i < 4; ++i)
+                for (int j = 0; j < 4; ++j) {
+                    int64_t a = tets[4 * t + i], b = tets[4 * t + j], found = -1;
+                    for (int64_t r = row_ptr[a]; r < row_ptr[a + 1]; ++r)
+                        if (head[r] == b) { found = r; break; }
+                    e[16 * t + 4 * i + j] = found;
+                }
+    }
+    return E;
+}
+
+/* ------------------------------------------------------------------ */
+/* O3  locality renumbering (Morton order of quantised rest positions).  */
+/* Licence: keys are opaque so the runtime may reorder.     */
+/* ------------------------------------------------------------------ */
+void orc_morton(int64_t nv, const double* X, uint64_t* code) {
+    double lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) { lo[d] = INFINITY; hi[d] = -INFINITY; }
+    for (int64_t v = 0; v < nv; ++v)
+        for (int d = 0; d < 3; ++d) {
+            if (X[3 * v + d] < lo[d]) lo[d] = X[3 * v + d];
+            if (X[3 * v + d] > hi[d]) hi[d] = X[3 * v + d];
+        }
+    const double S = 2097152.0; /* 2^21 */
+    for (int64_t v = 0; v < nv; ++v) {
+        uint64_t q[3];
+        for (int d = 0; d < 3; ++d) {
+            if (hi[d] == lo[d]) { q[d] = 0; continue; }
+            double s = X[3 * v + d] - lo[d];       /* subtract */
+            s = s / (hi[d] - lo[d]);                /* divide   */
+            s = s * S;                              /* multiply */
+            double f = floor(s);                    /* floor    */
+            uint64_t qi = (uint64_t)f;
+            q[d] = qi > 2097151u ? 2097151u : qi;
+        }
+        uint64_t c = 0;
+        for (int b = 0; b < 21; ++b)
+            for (int d = 0; d < 3; ++d) c |= ((q[d] >> b) & 1u) << (3 * b + d);
+        code[v] = c;
+    }
+}
+
+typedef struct { uint64_t key; int64_t id; } kv_t;
+static int cmp_kv(const void* a, const void* b) {
+    const kv_t* x = (const kv_t*)a;
+    const kv_t* y = (const kv_t*)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    return x->id < y->id ? -1 : (x->id > y->id);
+}
+
+typedef struct { int64_t s[4]; int64_t id; } tk_t;
+static int cmp_tk(const void* a, const void* b) {
+    const tk_t* x = (const tk_t*)a;
+    const tk_t* y = (const tk_t*)b;
+    for (int i = 0; i < 4; ++i)
+        if (x->s[i] != y->s[i]) return x->s[i] < y->s[i] ? -1 : 1;
+    return x->id < y->id ? -1 : (x->id > y->id);
+}
+
+/* new_of_old[v] = new id of old vertex v; tet_src[t'] = old index of the
+   tet at new position t'; tets_out = remapped tets in new order with the
+   local corner order kept (orientation). */
+void orc_renumber(int64_t nv, const double* X, int64_t nt, const int64_t* tets,
+                  int64_t* new_of_old, int64_t* tet_src, int64_t* tets_out) {
+    uint64_t* code = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nv > 0 ? nv : 1));
+    orc_morton(nv, X, code);
+    kv_t* A = (kv_t*)malloc(sizeof(kv_t) * (size_t)(nv > 0 ? nv : 1));
+    for (int64_t v = 0; v < nv; ++v) { A[v].key = code[v]; A[v].id = v; }
+    qsort(A, (size_t)nv, sizeof(kv_t), cmp_kv); /* (code, old id): stable */
+    for (int64_t r = 0; r < nv; ++r) new_of_old[A[r].id] = r;
+    free(A);
+    free(code);
+    tk_t* B = (tk_t*)malloc(sizeof(tk_t) * (size_t)(nt > 0 ? nt : 1));
+    for (int64_t t = 0; t < nt; ++t) {
+        int64_t s[4];
+        for (int i = 0; i < 4; ++i) s[i] = new_of_old[tets[4 * t + i]];
+        for (int i = 1; i < 4; ++i) /* insertion sort, ascending */
+            for (int j = i; j > 0 && s[j - 1] > s[j]; --j) { int64_t q = s[j]; s[j] = s[j - 1]; s[j - 1] = q; }
+        for (int i = 0; i < 4; ++i) B[t].s[i] = s[i];
+        B[t].id = t;
+    }
+    qsort(B, (size_t)nt, sizeof(tk_t), cmp_tk);
+    for (int64_t r = 0; r < nt; ++r) {
+        tet_src[r] = B[r].id;
+        for (int i = 0; i < 4; ++i) tets_out[4 * r + i] = new_of_old[tets[4 * B[r].id + i]];
+    }
+    free(B);
+}
+
+/* ------------------------------------------------------------------ */
+/* O5  rest data: Dm, W = det(Dm)/6, Dminv (adjugate/det, row-major:     */
+/* row i-1 = g_i), lumped mass m_v = sum rho W / 4.  P:944 "material    */
+/* properties on the tetrahedra"; mass on vertices (Fig. 2).      */
+/* returns the number of tets with W <= 0                               */
+/* ------------------------------------------------------------------ */
+int64_t orc_rest(int64_t nv, const double* X, int64_t nt, const int64_t* tets, double rho,
+                 double* Dminv, double* W, double* mass) {
+    int64_t bad = 0;
+    for (int64_t v = 0; v < nv; ++v) mass[v] = 0.0;
+    for (int64_t t = 0; t < nt; ++t) {
+        double D[3][3], R[3][3];
+        edge_matrix(X, tets + 4 * t, D);
+        double w = det3(D) / 6.0;
+        if (!(w > 0.0)) ++bad;
+        inv3(D, R);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) Dminv[9 * t + 3 * r + c] = R[r][c];
+        W[t] = w;
+        for (int i = 0; i < 4; ++i) mass[tets[4 * t + i]] += rho * w / 4.0;
+    }
+    return bad;
+}
+
+/* ------------------------------------------------------------------ */
+/* O6  constitutive models (textbook forms; the paper names them only)   */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    double F[3][3], FinvT[3][3], S[3][3], J, lnJ, mu, lam;
+    int model;
+} mat_state;
+
+/* first Piola-Kirchhoff stress P(F) and energy density Psi(F) */
+static int piola(int model, const double F[3][3], double mu, double lam,
+                 double P[3][3], double* psi, mat_state* st) {
+    memcpy(st->F, F, sizeof(st->F));
+    st->mu = mu;
+    st->lam = lam;
+    st->model = model;
+    if (model == ORC_STVK) {
+        /* E = 1/2 (F^T F - I), S = 2 mu E + lam tr(E) I, P = F S,
+           Psi = mu E:E + 1/2 lam tr(E)^2 */
+        double Ft[3][3], C[3][3], E[3][3];
+        transpose3(F, Ft);
+        matmul3(Ft, F, C);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) E[r][c] = 0.5 * (C[r][c] - (r == c ? 1.0 : 0.0));
+        double trE = E[0][0] + E[1][1] + E[2][2];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) st->S[r][c] = 2.0 * mu * E[r][c] + (r == c ? lam * trE : 0.0);
+        matmul3(F, st->S, P);
+        double EE = 0.0;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) EE += E[r][c] * E[r][c];
+        *psi = mu * EE + 0.5 * lam * trE * trE;
+        return 0;
+    }
+    /* compressible neo-Hookean (Bonet-Wood):
+       Psi = 1/2 mu (tr F^T F - 3) - mu ln J + 1/2 lam (ln J)^2,
+       P = mu (F - F^-T) + lam ln J F^-T */
+    double J = det3(F);
+    st->J = J;
+    if (!(J > 0.0)) {
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) P[r][c] = NAN;
+        *psi = NAN;
+        st->lnJ = NAN;
+        return 1;
+    }
+    double Finv[3][3];
+    inv3(F, Finv);
+    transpose3(Finv, st->FinvT);
+    double lnJ = log(J);
+    st->lnJ = lnJ;
+    double I1 = 0.0;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) I1 += F[r][c] * F[r][c];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) P[r][c] = mu * (F[r][c] - st->FinvT[r][c]) + lam * lnJ * st->FinvT[r][c];
+    *psi = 0.5 * mu * (I1 - 3.0) - mu * lnJ + 0.5 * lam * lnJ * lnJ;
+    return 0;
+}
+
+/* directional derivative dP = (dP/dF) : dF (generic 4th-order tensor) */
+static void piola_diff(const mat_state* st, const double dF[3][3], double dP[3][3]) {
+    const double(*F)[3] = st->F;
+    if (st->model == ORC_STVK) {
+        /* dP = dF S + F (2 mu dE + lam tr(dE) I), dE = sym(F^T dF) */
+        double Ft[3][3], FtdF[3][3], dE[3][3], T1[3][3], T2[3][3], M[3][3];
+        transpose3(F, Ft);
+        matmul3(Ft, dF, FtdF);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) dE[r][c] = 0.5 * (FtdF[r][c] + FtdF[c][r]);
+        double tr = dE[0][0] + dE[1][1] + dE[2][2];
+        matmul3(dF, st->S, T1);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) M[r][c] = 2.0 * st->mu * dE[r][c] + (r == c ? st->lam * tr : 0.0);
+        matmul3(F, M, T2);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) dP[r][c] = T1[r][c] + T2[r][c];
+        return;
+    }
+    /* dP = mu dF + (mu - lam ln J) F^-T dF^T F^-T + lam tr(F^-1 dF) F^-T */
+    double dFt[3][3], T[3][3], T2[3][3], Finv[3][3], FinvdF[3][3];
+    transpose3(dF, dFt);
+    matmul3(st->FinvT, dFt, T);
+    matmul3(T, st->FinvT, T2);
+    transpose3(st->FinvT, Finv);
+    matmul3(Finv, dF, FinvdF);
+    double tr = FinvdF[0][0] + FinvdF[1][1] + FinvdF[2][2];
+    double c1 = st->mu - st->lam * st->lnJ;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            dP[r][c] = st->mu * dF[r][c] + c1 * T2[r][c] + st->lam * tr * st->FinvT[r][c];
+}
+
+/* ------------------------------------------------------------------ */
+/* O6 + O7  element map over tets (P:944-946 forces and stiffness;      */
+/* P:885 field reductions `+=`; P:887 global reduction).                 */
+/* f (nv*3) and K (ne*9, row-major 3x3 blocks) are zeroed, then          */
+/* accumulated in loop order: tets ascending, corners i, blocks (i,j).   */
+/* Returns the number of tets with J <= 0 (NH) -- their output is NaN.   */
+/* ------------------------------------------------------------------ */
+int64_t orc_element_map(int model, int64_t nv, const double* X, const double* u,
+                        int64_t nt, const int64_t* tets, const double* Dminv, const double* W,
+                        const double* mu, const double* lam, const int64_t* e, int64_t ne,
+                        double* f, double* K, double* energy) {
+    int64_t inverted = 0;
+    double en = 0.0;
+    for (int64_t v = 0; v < 3 * nv; ++v) f[v] = 0.0;
+    if (K)
+        for (int64_t r = 0; r < 9 * ne; ++r) K[r] = 0.0;
+    for (int64_t t = 0; t < nt; ++t) {
+        const int64_t* tv = tets + 4 * t;
+        /* F = Ds Dm^-1, Ds = [x1-x0, x2-x0, x3-x0], x = X + u (textbook F-form) */
+        double x[4][3];
+        for (int i = 0; i < 4; ++i)
+            for (int a = 0; a < 3; ++a) x[i][a] = X[3 * tv[i] + a] + u[3 * tv[i] + a];
+        double Ds[3][3], Dmi[3][3], F[3][3];
+        for (int k = 0; k < 3; ++k)
+            for (int a = 0; a < 3; ++a) Ds[a][k] = x[k + 1][a] - x[0][a];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) Dmi[r][c] = Dminv[9 * t + 3 * r + c];
+        matmul3(Ds, Dmi, F);
+        /* g_i = row i-1 of Dm^-1 (i = 1..3), g_0 = -(g_1 + g_2 + g_3) */
+        double g[4][3];
+        for (int i = 1; i < 4; ++i)
+            for (int c = 0; c < 3; ++c) g[i][c] = Dmi[i - 1][c];
+        for (int c = 0; c < 3; ++c) g[0][c] = -(g[1][c] + g[2][c] + g[3][c]);
+        double P[3][3], psi;
+        mat_state st;
+        inverted += piola(model, F, mu[t], lam[t], P, &psi, &st);
+        double w = W[t];
+        /* f_i = -W P g_i (i >= 1), f_0 = -(f_1 + f_2 + f_3) */
+        double fi[4][3];
+        for (int i = 1; i < 4; ++i)
+            for (int a = 0; a < 3; ++a) {
+                double s = 0.0;
+                for (int b = 0; b < 3; ++b) s += P[a][b] * g[i][b];
+                fi[i][a] = -w * s;
+            }
+        for (int a = 0; a < 3; ++a) fi[0][a] = -(fi[1][a] + fi[2][a] + fi[3][a]);
+        for (int i = 0; i < 4; ++i)
+            for (int a = 0; a < 3; ++a) f[3 * tv[i] + a] += fi[i][a];
+        en += w * psi;
+        if (!K) continue;
+        /* C[a][c][b][d] = dP_ac / dF_bd, column by column */
+        double C[3][3][3][3];
+        for (int b = 0; b < 3; ++b)
+            for (int d = 0; d < 3; ++d) {
+                double dF[3][3] = {{0}}, dP[3][3];
+                dF[b][d] = 1.0;
+                piola_diff(&st, dF, dP);
+                for (int a = 0; a < 3; ++a)
+                    for (int c = 0; c < 3; ++c) C[a][c][b][d] = dP[a][c];
+            }
+        /* K_ij[a][b] = W sum_{c,d} C[a][c][b][d] g_i[c] g_j[d] */
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) {
+                int64_t row = e[16 * t + 4 * i + j];
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) {
+                        double s = 0.0;
+                        for (int c = 0; c < 3; ++c)
+                            for (int d = 0; d < 3; ++d) s += C[a][c][b][d] * g[i][c] * g[j][d];
+                        K[9 * row + 3 * a + b] += w * s;
+                    }
+            }
+    }
+    if (energy) *energy = en;
+    return inverted;
+}
+
+/* ------------------------------------------------------------------ */
+/* edge-relation matvec (query-loop over v.edges):     */
+/* q_v = sum_{e in [row_ptr[v], row_ptr[v+1])} A_e p_head(e)             */
+/* ------------------------------------------------------------------ */
+void orc_edge_matvec(int64_t nv, const int64_t* row_ptr, const int64_t* head,
+                     const double* A, const double* p, double* q) {
+    for (int64_t v = 0; v < nv; ++v) {
+        double s[3] = {0.0, 0.0, 0.0};
+        for (int64_t r = row_ptr[v]; r < row_ptr[v + 1]; ++r) {
+            const double* a = A + 9 * r;
+            const double* x = p + 3 * head[r];
+            for (int i = 0; i < 3; ++i) s[i] += a[3 * i + 0] * x[0] + a[3 * i + 1] * x[1] + a[3 * i + 2] * x[2];
+        }
+        for (int i = 0; i < 3; ++i) q[3 * v + i] = s[i];
+    }
+}
+
+/* dot product over vertices ascending, components x,y,z (global `+=`) */
+double orc_dot(int64_t n, const double* a, const double* b) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+
+/* ------------------------------------------------------------------ */
+/* O8  explicit step update (Fig. 2 applyForces):             */
+/* a = (f + m g)/m; u += v h + 1/2 a h^2; v += a h; fixed rows untouched  */
+/* ------------------------------------------------------------------ */
+void orc_explicit_update(int64_t nv, const double* f, const double* mass, const uint8_t* free_mask,
+                         const double* g, double h, double* u, double* v) {
+    for (int64_t i = 0; i < nv; ++i) {
+        if (free_mask && !free_mask[i]) continue;
+        for (int a = 0; a < 3; ++a) {
+            double acc = (f[3 * i + a] + mass[i] * g[a]) / mass[i];
+            u[3 * i + a] += v[3 * i + a] * h + 0.5 * acc * h * h;
+            v[3 * i + a] += acc * h;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* O9  implicit (linearised backward Euler) system:        */
+/*   A = M + h D + h^2 K,  D = alpha M + beta K                          */
+/*   b = h (f + M g - D v - h K v)                                       */
+/* M is lumped (m_v I on the self-loop row of v).                        */
+/* ------------------------------------------------------------------ */
+void orc_implicit_assemble(int64_t nv, const int64_t* row_ptr, const int64_t* head,
+                           const double* K, const double* mass, const double* f, const double* vel,
+                           double h, double alpha, double beta, const double* g,
+                           double* A, double* b) {
+    int64_t ne = row_ptr[nv];
+    double* Kv = (double*)malloc(sizeof(double) * (size_t)(3 * nv > 0 ? 3 * nv : 1));
+    orc_edge_matvec(nv, row_ptr, head, K, vel, Kv);
+    for (int64_t i = 0; i < nv; ++i)
+        for (int a = 0; a < 3; ++a) {
+            double Mv = mass[i] * vel[3 * i + a];
+            double Dv = alpha * Mv + beta * Kv[3 * i + a];
+            b[3 * i + a] = h * (f[3 * i + a] + mass[i] * g[a] - Dv - h * Kv[3 * i + a]);
+        }
+    free(Kv);
+    for (int64_t v = 0; v < nv; ++v)
+        for (int64_t r = row_ptr[v]; r < row_ptr[v + 1]; ++r)
+            for (int a = 0; a < 3; ++a)
+                for (int c = 0; c < 3; ++c) {
+                    double Me = (head[r] == v && a == c) ? mass[v] : 0.0;
+                    double Ke = K[9 * r + 3 * a + c];
+                    double De = alpha * Me + beta * Ke;
+                    A[9 * r + 3 * a + c] = Me + h * De + h * h * Ke;
+                }
+    (void)ne;
+}
+
+/* ------------------------------------------------------------------ */
+/* O10  Jacobi-preconditioned CG (Saad Alg. 9.1), fixed N iters,  */
+/* Dirichlet projection by the free mask (subsets).           */
+/* Readings: alpha = 0 if p.q == 0, beta = 0 if rho == 0.    */
+/* rho_hist (nullable, iters+1): rho before each iteration and at end.   */
+/* returns 1 if some p.q < 0 (A not SPD on the Krylov space), else 0.     */
+/* ------------------------------------------------------------------ */
+int orc_pcg(int64_t nv, const int64_t* row_ptr, const int64_t* head, const double* A,
+            const double* b, const uint8_t* free_mask, int iters, double* x, double* rho_hist) {
+    int64_t n = 3 * nv;
+    double* r = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    double* z = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    double* p = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    double* q = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    double* d = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    int not_spd = 0;
+    for (int64_t v = 0; v < nv; ++v)
+        for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e)
+            if (head[e] == v)
+                for (int a = 0; a < 3; ++a) d[3 * v + a] = A[9 * e + 4 * a];
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = 0.0;
+        double m = (free_mask && !free_mask[i / 3]) ? 0.0 : 1.0;
+        r[i] = b[i] * m;
+        z[i] = (m != 0.0) ? r[i] / d[i] : 0.0;
+        p[i] = z[i];
+    }
+    double rho = orc_dot(n, r, z);
+    for (int k = 0; k < iters; ++k) {
+        if (rho_hist) rho_hist[k] = rho;
+        orc_edge_matvec(nv, row_ptr, head, A, p, q);
+        if (free_mask)
+            for (int64_t i = 0; i < n; ++i)
+                if (!free_mask[i / 3]) q[i] = 0.0;
+        double pq = orc_dot(n, p, q);
+        if (pq < 0.0) not_spd = 1;
+        double alpha = (pq != 0.0) ? rho / pq : 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            x[i] += alpha * p[i];
+            r[i] -= alpha * q[i];
+            double m = (free_mask && !free_mask[i / 3]) ? 0.0 : 1.0;
+            z[i] = (m != 0.0) ? r[i] / d[i] : 0.0;
+        }
+        double rho_new = orc_dot(n, r, z);
+        double beta = (rho != 0.0) ? rho_new / rho : 0.0;
+        for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        rho = rho_new;
+    }
+    if (rho_hist) rho_hist[iters] = rho;
+    free(r); free(z); free(p); free(q); free(d);
+    return not_spd;
+}
+
+/* implicit step state update: v += dv; u += h v (P:941 integrator) */
+void orc_implicit_update(int64_t nv, const double* dv, double h, double* u, double* v) {
+    for (int64_t i = 0; i < 3 * nv; ++i) {
+        v[i] += dv[i];
+        u[i] += h * v[i];
+    }
+}

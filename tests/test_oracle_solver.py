@@ -1,0 +1,136 @@
+"""Pins for oracle O8-O10 (explicit update, implicit assembly, Jacobi-PCG).
+
+Independent references: a dense textbook PCG in numpy, numpy.linalg.solve,
+the exact constant-acceleration solution (free fall) of both integrators,
+and rest invariance.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import mesh as M
+from synth import state as S
+
+
+def _dense(m, A):
+    D = np.zeros((3 * m.nv, 3 * m.nv))
+    for r in range(m.ne):
+        a, b = m.tail[r], m.head[r]
+        D[3 * a:3 * a + 3, 3 * b:3 * b + 3] = A[r]
+    return D
+
+
+def _system(n=2, model="nh", seed=7, h=1e-2, E=2e5, fixed=True):
+    X, tets = M.kuhn6(n)
+    m = oracle.Mesh(X, tets)
+    free = S.fixed_mask(X, n) if fixed else np.ones(m.nv, np.uint8)
+    u = S.stretch_noise_u(X, n, seed, free=free)
+    v = np.random.default_rng(seed).uniform(-0.1, 0.1, size=X.shape) * free[:, None]
+    mu, lam = S.materials(m.nt, E, 0.3)
+    f, K, en, inv = oracle.element_map(model, m.X, u, m.tets, m.Dminv, m.W, mu, lam, e=m.e, ne=m.ne)
+    A, b = oracle.implicit_assemble(m.row_ptr, m.head, K, m.mass, f, v, h, 0.1, 0.01)
+    return m, free, u, v, f, K, A, b
+
+
+def dense_pcg(A, b, mask, iters):
+    """Textbook Jacobi-PCG (Saad Alg. 9.1) on a dense matrix with projection."""
+    n = b.size
+    d = np.diag(A).copy()
+    x = np.zeros(n)
+    r = b * mask
+    z = np.where(mask > 0, r / d, 0.0)
+    p = z.copy()
+    rho = r @ z
+    for _ in range(iters):
+        q = (A @ p) * mask
+        pq = p @ q
+        al = rho / pq if pq != 0 else 0.0
+        x += al * p
+        r -= al * q
+        z = np.where(mask > 0, r / d, 0.0)
+        rn = r @ z
+        be = rn / rho if rho != 0 else 0.0
+        p = z + be * p
+        rho = rn
+    return x
+
+
+def test_assembly_matches_dense_definition():
+    m, free, u, v, f, K, A, b = _system()
+    h, al, be = 1e-2, 0.1, 0.01
+    Kd = _dense(m, K)
+    Md = np.diag(np.repeat(m.mass, 3))
+    Ad = Md + h * (al * Md + be * Kd) + h * h * Kd
+    g = np.tile([0.0, -9.81, 0.0], m.nv)
+    bd = h * (f.ravel() + Md @ g - (al * Md + be * Kd) @ v.ravel() - h * Kd @ v.ravel())
+    assert np.abs(_dense(m, A) - Ad).max() < 1e-14 * np.abs(Ad).max()
+    assert np.abs(b.ravel() - bd).max() < 1e-12 * np.abs(bd).max()
+
+
+@pytest.mark.parametrize("iters", [1, 5, 20])
+def test_pcg_matches_dense_textbook_pcg(iters):
+    m, free, u, v, f, K, A, b = _system()
+    mask = np.repeat(free, 3).astype(np.float64)
+    x, hist, ns = oracle.pcg(m.row_ptr, m.head, A, b, free, iters)
+    xd = dense_pcg(_dense(m, A), b.ravel(), mask, iters)
+    assert np.abs(x.ravel() - xd).max() < 1e-11 * np.abs(xd).max()
+    assert not ns
+
+
+def test_pcg_converges_to_direct_solve():
+    m, free, u, v, f, K, A, b = _system(n=2)
+    idx = np.nonzero(np.repeat(free, 3))[0]
+    Ad = _dense(m, A)[np.ix_(idx, idx)]
+    assert np.linalg.eigvalsh(Ad).min() > 0               # SPD on free DOFs
+    xs = np.linalg.solve(Ad, b.ravel()[idx])
+    x, hist, ns = oracle.pcg(m.row_ptr, m.head, A, b, free, 3 * m.nv)
+    assert np.abs(x.ravel()[idx] - xs).max() < 1e-10 * np.abs(xs).max()
+    assert np.all(x[free == 0] == 0.0)
+
+
+def test_explicit_rest_invariance():
+    X, tets = M.kuhn6(3)
+    m = oracle.Mesh(X, tets)
+    mu, lam = S.materials(m.nt, 1e6, 0.3)
+    u = np.zeros_like(X)
+    v = np.zeros_like(X)
+    for _ in range(5):
+        u, v, f, en = oracle.explicit_step(m, "stvk", u, v, mu, lam, None, 1e-4, g=(0, 0, 0))
+    assert np.all(u == 0) and np.all(v == 0)
+
+
+def test_explicit_free_fall_exact():
+    """Rigid translation under gravity: u_n = 1/2 g (n h)^2 (update P:376-377 is
+    exact for constant acceleration; internal forces stay at round-off)."""
+    X, tets = M.kuhn6(2)
+    m = oracle.Mesh(X, tets)
+    mu, lam = S.materials(m.nt, 1e6, 0.3)
+    u = np.zeros_like(X)
+    v = np.zeros_like(X)
+    h, N = 1e-3, 10
+    g = np.array([0.0, -9.81, 0.0])
+    for _ in range(N):
+        u, v, f, en = oracle.explicit_step(m, "stvk", u, v, mu, lam, None, h, g=g)
+    assert np.abs(u - 0.5 * g * (N * h) ** 2).max() < 1e-12
+    assert np.abs(v - g * N * h).max() < 1e-12
+
+
+@pytest.mark.parametrize("model", ["stvk", "nh"])
+def test_implicit_free_fall(model):
+    """Backward Euler from rest with no constraints: dv = h g exactly solves
+    (M + h^2 K) dv = h M g because K annihilates translations."""
+    X, tets = M.kuhn6(2)
+    m = oracle.Mesh(X, tets)
+    mu, lam = S.materials(m.nt, 2e5, 0.3)
+    u = np.zeros_like(X)
+    v = np.zeros_like(X)
+    h = 1e-2
+    out = oracle.implicit_step(m, model, u, v, mu, lam, None, h, iters=60)
+    assert np.abs(out["dv"] - np.array([0, -9.81 * h, 0])).max() < 1e-8
+    assert np.abs(out["u"] - h * out["v"]).max() < 1e-15
+
+
+def test_pcg_zero_rhs_is_noop():
+    m, free, u, v, f, K, A, b = _system()
+    x, hist, ns = oracle.pcg(m.row_ptr, m.head, A, np.zeros_like(b), free, 10)
+    assert np.all(x == 0) and np.all(hist == 0)

@@ -1,0 +1,277 @@
+/*
+ * ebb.h -- C ABI of the B200-native Ebb tet-FEM hot path (libebb_b200.so).
+ *
+ * Paper: Bernstein et al., "Ebb: A DSL for Physical Simulation on CPUs and
+ * GPUs", arXiv 1506.07577.  P:<n> = line n of the paper's PAPER.md, S:<n> =
+ * line n of SPEC.md.  The calls follow the paper's relational model:
+ * relations, fields in a column store, key-fields
+ * (stored as uint64 in the paper P:854 -- here uint32,
+ * which "Ebb is subsequently free to ... encode" P:674-677), GroupBy /
+ * query-loops, field and global reductions.
+ * The one hot path is the FEM element map over tets and the CG solve over the
+ * edge relation; see DESIGN.md.
+ *
+ * Conventions for every call
+ *   - Returns EBB_OK (0) or a negative ebb_status; never throws.  The text of
+ *     the last error of a context is in ebb_last_error(ctx) (valid until the
+ *     next call on that context).
+ *   - A context is bound to one CUDA device and is single-entrant:
+ *     no two calls on the same context may run concurrently.
+ *   - ebb_stream is a cudaStream_t (NULL = the legacy default stream).  Kernel
+ *     launching calls are asynchronous and stream-ordered; calls documented as
+ *     "synchronous" block the host until the stream is idle.
+ *   - Handles (ebb_rel, ebb_field) are small integers owned by the context and
+ *     valid until ebb_ctx_free.  EBB_NONE marks an absent optional field.
+ *   - Keys are opaque row references.  They cross the ABI as
+ *     uint64 and are bounds-checked on entry.
+ *   - Device memory of library-allocated fields is owned by the context;
+ *     ebb_field_wrap borrows caller memory that must outlive the context.
+ *   - Kernel-side failures (inverted elements, non-SPD CG, key out of range)
+ *     increment a device error word read by ebb_error_counts (synchronous).
+ */
+#ifndef EBB_H
+#define EBB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ebb_status;
+#define EBB_OK 0
+#define EBB_E_ARG (-1)          /* bad handle, NULL pointer, bad enum        */
+#define EBB_E_DUP (-2)          /* duplicate relation/field name      */
+#define EBB_E_SIZE (-3)         /* zero size / byte count mismatch */
+#define EBB_E_BOUNDS (-4)       /* key out of range of its target     */
+#define EBB_E_TYPE (-5)         /* dtype/shape/relation mismatch  */
+#define EBB_E_STATE (-6)        /* double grouping, missing prerequisite      */
+#define EBB_E_PHASE (-7)        /* a field in two phases of one map  */
+#define EBB_E_INVERTED (-8)     /* tet with W <= 0 at rest                   */
+#define EBB_E_NOT_SPD (-9)      /* CG found p.q <= 0                          */
+#define EBB_E_CUDA (-10)        /* CUDA runtime failure                       */
+#define EBB_E_RANGE (-11)       /* value does not fit the 32-bit key storage  */
+#define EBB_E_NOMEM (-12)       /* device allocation failed                   */
+#define EBB_E_DEGENERATE (-13)  /* |det Dm| <= 1e-12 l^3 (O1)                  */
+
+typedef struct ebb_ctx_s* ebb_ctx;
+typedef uint32_t ebb_rel;
+typedef uint32_t ebb_field;
+typedef void* ebb_stream; /* cudaStream_t */
+#define EBB_NONE 0xFFFFFFFFu
+
+typedef enum {
+    EBB_F32 = 1, EBB_F64 = 2, EBB_I32 = 3, EBB_I64 = 4, EBB_U8 = 5, EBB_U32 = 6,
+    EBB_KEY = 7 /* key-field: uint32 storage, typed by its target relation */
+} ebb_dtype;
+
+/* Storage layout of a rows x cols field.  AOS: element-major (the 9 entries
+ * of a 3x3 block are contiguous).  SOA: component-planar -- one contiguous
+ * column per component, the paper's column store applied per
+ * component; used for tet rest data and the edge stiffness so that a warp's
+ * loads coalesce.  Host-side data crossing the ABI is always element-major. */
+typedef enum { EBB_AOS = 0, EBB_SOA = 1 } ebb_layout;
+
+typedef struct {
+    void* data;               /* device pointer                               */
+    uint64_t count;           /* rows of the owning relation                  */
+    uint32_t rows, cols;      /* per-element shape (vec3 = 3x1, mat3 = 3x3)   */
+    int32_t dtype;            /* ebb_dtype                                    */
+    int32_t layout;           /* ebb_layout                                   */
+    uint64_t elem_stride;     /* bytes between consecutive elements           */
+    uint64_t comp_stride;     /* bytes between consecutive components         */
+    ebb_rel rel;              /* owning relation                              */
+    ebb_rel key_target;       /* target relation of a key-field, else NONE    */
+} ebb_view;
+
+const char* ebb_version(void);
+
+/* ---- context -------------------------------------------------------- */
+ebb_status ebb_ctx_new(int device, ebb_ctx* out);
+ebb_status ebb_ctx_free(ebb_ctx ctx);
+const char* ebb_last_error(ebb_ctx ctx);
+/* Kernel-side error counters (synchronous; optionally reset):
+ * out[0] inverted elements (J<=0), out[1] CG p.q<=0 events,
+ * out[2] key out of range, out[3] reserved. */
+ebb_status ebb_error_counts(ebb_ctx ctx, uint64_t out[4], int reset);
+ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s);
+
+/* ---- relations and fields ----------- */
+ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_rel* out);
+ebb_status ebb_relation_size(ebb_ctx ctx, ebb_rel rel, uint64_t* out);
+/* Library-allocated field; host_init (element-major, rows*cols per element)
+ * or NULL for zeros.  Synchronous. */
+ebb_status ebb_field_new(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype dtype,
+                         uint32_t rows, uint32_t cols, ebb_layout layout,
+                         const void* host_init, ebb_field* out);
+/* Borrowed device memory (e.g. a torch tensor's data_ptr) in the given layout. */
+ebb_status ebb_field_wrap(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype dtype,
+                          uint32_t rows, uint32_t cols, ebb_layout layout,
+                          void* device_ptr, ebb_field* out);
+ebb_status ebb_field_find(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_field* out);
+/* Host <-> device copies of the whole column, element-major host order.
+ * nbytes must equal count*rows*cols*sizeof(dtype).  write is stream-ordered
+ * (host buffer must stay valid until the stream reaches it; pinned memory
+ * makes it asynchronous); read is synchronous. */
+ebb_status ebb_field_write(ebb_ctx ctx, ebb_field f, const void* host, uint64_t nbytes, ebb_stream s);
+ebb_status ebb_field_read(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes, ebb_stream s);
+ebb_status ebb_field_fill(ebb_ctx ctx, ebb_field f, double value, ebb_stream s);
+ebb_status ebb_field_copy(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream s);
+/* dst = (dtype of dst) src for F32/F64 fields of equal relation, shape, layout. */
+ebb_status ebb_field_convert(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream s);
+/* Zero-copy raw view; invalidated by group_by/renumber. */
+ebb_status ebb_field_view(ebb_ctx ctx, ebb_field f, ebb_view* out);
+
+/* Key-field: rows x cols keys per element of `owner`, each a row
+ * of `target`.  keys are uint64 (host, or device if keys_on_device);
+ * EBB_E_BOUNDS if any key >= size(target); EBB_E_RANGE if a target is
+ * larger than 2^32-1 rows.  Synchronous. */
+ebb_status ebb_key_field(ebb_ctx ctx, ebb_rel owner, const char* name, ebb_rel target,
+                         uint32_t rows, uint32_t cols, const uint64_t* keys, int keys_on_device,
+                         ebb_field* out);
+
+/* ---- globals ----------------------- */
+ebb_status ebb_global_new(ebb_ctx ctx, const char* name, ebb_dtype dtype, double init, ebb_field* out);
+ebb_status ebb_global_get(ebb_ctx ctx, ebb_field g, double* out);   /* synchronous */
+ebb_status ebb_global_set(ebb_ctx ctx, ebb_field g, double value, ebb_stream s);
+
+/* ---- GroupBy ------------------------- */
+/* Stably sorts `rel` by the scalar key-field `key`, permutes every field of
+ * rel, remaps every key-field in the context that targets rel, and builds the
+ * hidden index on the source relation: a U32 field "__index" of size+1 rows
+ * (CSR offsets; row s owns [index[s], index[s+1])).  EBB_E_STATE if rel is
+ * already grouped; EBB_E_TYPE if key is not a scalar key-field of rel.
+ * Synchronous. */
+ebb_status ebb_group_by(ebb_ctx ctx, ebb_rel rel, ebb_field key);
+ebb_status ebb_group_index(ebb_ctx ctx, ebb_rel rel, ebb_field* index_out);
+
+/* ---- locality renumbering (licence P:674-677) -------- */
+/* Morton order of the quantised rows of `pos` (vec3 F64 on rel): q_d =
+ * min(2^21-1, floor((x_d-lo_d)/(hi_d-lo_d) 2^21)), x bit at 3b, y at 3b+1,
+ * z at 3b+2; stable by old id.  Permutes rel's fields, remaps inbound keys.
+ * Synchronous. */
+ebb_status ebb_renumber_morton(ebb_ctx ctx, ebb_rel rel, ebb_field pos);
+/* Sort `rel` lexicographically by the ascending-sorted tuple of its rows x 1
+ * key-field `keys` (tets by their vertex ids), stable.  Synchronous. */
+ebb_status ebb_sort_by_key_tuple(ebb_ctx ctx, ebb_rel rel, ebb_field keys);
+
+/* ---- tetrahedral mesh domain --------- */
+typedef struct {
+    ebb_rel edges;   /* relation of ordered vertex pairs + one self-loop per vertex */
+    ebb_field tail;  /* edges -> verts key, grouped (edges sorted by (tail, head)) */
+    ebb_field head;  /* edges -> verts key                                         */
+    ebb_field e;     /* tets 4x4 key -> edges; tail(e[i][j]) = v[i], head = v[j]   */
+    ebb_field self;  /* verts -> edges key of the self-loop (diagonal block)       */
+    ebb_field index; /* verts U32 (V+1) CSR offsets of the grouping                */
+} ebb_tetmesh;
+/* O1: swap v[2], v[3] of tets with det(Dm) < 0 (pos: verts vec3 F64).
+ * EBB_E_DEGENERATE if |det| <= 1e-12 l^3.  Synchronous. */
+ebb_status ebb_tetmesh_orient(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, uint64_t* n_swapped);
+/* a1: build the edge relation named edges_name from tets.v (4x1 keys) and
+ * group it by tail.  Synchronous. */
+ebb_status ebb_tetmesh_build(ebb_ctx ctx, ebb_field tets_v, const char* edges_name, ebb_tetmesh* out);
+/* a3: Dminv (tets 3x3, rows g_1..g_3), W = det(Dm)/6 (tets 1x1), lumped mass
+ * m_v = sum rho W / 4 (verts 1x1), all F64.  EBB_E_INVERTED if some W <= 0. */
+ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double rho,
+                            ebb_field Dminv, ebb_field W, ebb_field mass, ebb_stream s);
+
+/* ---- the element map (hot path a4-a8) --------------------------------- */
+#define EBB_STVK 0
+#define EBB_NH 1
+#define EBB_SCATTER_AUTO 0
+#define EBB_SCATTER_ATOMIC 1    /* per-tet red.global.add              */
+#define EBB_SCATTER_TILED 2     /* CTA shared-memory aggregation + red/stores  */
+typedef struct {
+    int32_t model;         /* EBB_STVK | EBB_NH                                */
+    int32_t scatter;       /* EBB_SCATTER_*                                    */
+    int32_t zero_outputs;  /* 1: f, K, energy are zeroed first                 */
+    int32_t reserved;
+    ebb_field v;           /* tets.v   4x1 key -> verts      (read)            */
+    ebb_field e;           /* tets.e   4x4 key -> edges      (read; iff K)     */
+    ebb_field u;           /* verts    vec3 displacement     (read)            */
+    ebb_field Dminv;       /* tets     3x3 (rows g_1..g_3)   (read)            */
+    ebb_field W;           /* tets     rest volume           (read)            */
+    ebb_field mu, lam;     /* tets     Lame parameters       (read)     */
+    ebb_field f;           /* verts    vec3 force            (reduce +)        */
+    ebb_field K;           /* edges    3x3 stiffness         (reduce +) / NONE */
+    ebb_field energy;      /* global   strain energy sum WΨ  (reduce +) / NONE */
+} ebb_tet_map_desc;
+/* For each tet: H = Du Dminv, F = I + H; StVK or
+ * compressible neo-Hookean first Piola stress P; f_i = -W P g_i, f_0 =
+ * -sum f_i; K_ij = d^2(WΨ)/dx_i dx_j (closed rank-1 forms);
+ * f[v[i]] += f_i, K[e[i][j]] += K_ij, energy += WΨ.  All float fields share
+ * one dtype (F32 or F64) and the documented layouts: u, f AOS; Dminv, K SOA.
+ * EBB_E_PHASE if u aliases f or K, or f aliases K. */
+ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_stream s);
+
+/* a10: q_v = sum_{e in [index[v], index[v+1])} A_e p_head(e)  (query-loop over
+ * v.edges), q *= mask (optional U8 on verts), and optionally
+ * pq_global = p.q (fused, deterministic two-pass).  `edges` must be
+ * grouped by a key into verts and carry a scalar key-field named "head"
+ * (the e.head of the query-loop); A is SOA 3x3, p and q AOS vec3, one dtype. */
+ebb_status ebb_map_edge_matvec(ebb_ctx ctx, ebb_rel edges, ebb_field A, ebb_field p, ebb_field q,
+                               ebb_field mask, ebb_field pq_global, ebb_stream s);
+
+/* a8: global reductions over every component of `a`:
+ * SUM a, DOT a.b, MAX a, MIN a, optionally masked per element by a U8 field
+ * (masked-out elements contribute the identity). out is an F64 global. */
+#define EBB_RED_SUM 0
+#define EBB_RED_DOT 1
+#define EBB_RED_MAX 2
+#define EBB_RED_MIN 3
+ebb_status ebb_global_reduce(ebb_ctx ctx, int32_t op, ebb_field a, ebb_field b, ebb_field mask,
+                             ebb_field out, ebb_stream s);
+
+/* ---- integrators (Fig. 2) ---------------------- */
+typedef struct {
+    ebb_rel edges;
+    ebb_field K;      /* edges 3x3 stiffness (read)                          */
+    ebb_field A;      /* edges 3x3 system matrix (write; may equal K)        */
+    ebb_field self;   /* verts -> edges self-loop key                        */
+    ebb_field mass, f, vel;   /* verts (read)                                */
+    ebb_field b;      /* verts vec3 rhs (write)                              */
+    double h, alpha, beta;    /* step, Rayleigh damping D = alpha M + beta K */
+    double g[3];              /* gravity                                     */
+} ebb_implicit_desc;
+/* a9: A = M + h D + h^2 K, b = h (f + M g - D v - h K v) (lumped M). */
+ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_stream s);
+
+typedef struct {
+    ebb_rel edges;
+    ebb_field A, b, x;   /* system (read), rhs (read), solution (write)       */
+    ebb_field self;      /* verts -> edges self-loop key (Jacobi diagonal)    */
+    ebb_field mask;      /* verts U8, 1 = free, or EBB_NONE (a12)  */
+    /* work fields; EBB_NONE = allocated by ebb_cg_init and written back      */
+    ebb_field r, p, z, q, dinv;
+    ebb_field rho;       /* F64 global r.z (allocated if NONE)                */
+    ebb_field scal;      /* internal device scalars rho, alpha, beta, p.q     */
+} ebb_cg;
+/* a11: x = 0, r = b*mask, z = r/diag(A), p = z, rho = r.z.  Stream-ordered. */
+ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream s);
+/* a10-a12: `iters` Jacobi-PCG iterations (Saad Alg. 9.1), alpha/beta kept
+ * on the device (no host sync); p.q <= 0 counts in error word [1]. */
+ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream s);
+
+typedef struct {
+    ebb_field f, mass, mask;  /* mask: verts U8 (1 = free) or EBB_NONE        */
+    ebb_field u, vel;         /* verts vec3 (read-write)                      */
+    double h;
+    double g[3];
+} ebb_explicit_desc;
+/* O8: a = (f + m g)/m; u += v h + a h^2/2; v += a h on free vertices. */
+ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stream s);
+/* implicit state update: vel += dv; u += h vel. */
+ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
+
+/* ---- multi-GPU partition ----------------------------- */
+/* owner_t(t) = floor(t P / T); owner_v(v) = owner_t(min tet containing v),
+ * floor(v P / V) if isolated.  Outputs are I32 fields on tets / verts.
+ * Synchronous. */
+ebb_status ebb_partition(ebb_ctx ctx, ebb_field tets_v, int32_t nparts,
+                         ebb_field owner_t, ebb_field owner_v);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EBB_H */

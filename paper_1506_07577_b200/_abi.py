@@ -1,0 +1,128 @@
+"""ctypes declarations of include/ebb.h (argument marshalling only).
+
+Loads the in-tree ``libebb_b200.so``; there is no fallback: if the library is
+missing or cannot be loaded, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libebb_b200.so")
+
+NONE = 0xFFFFFFFF
+
+# status codes
+OK = 0
+E_NAMES = {
+    -1: "EBB_E_ARG", -2: "EBB_E_DUP", -3: "EBB_E_SIZE", -4: "EBB_E_BOUNDS", -5: "EBB_E_TYPE",
+    -6: "EBB_E_STATE", -7: "EBB_E_PHASE", -8: "EBB_E_INVERTED", -9: "EBB_E_NOT_SPD",
+    -10: "EBB_E_CUDA", -11: "EBB_E_RANGE", -12: "EBB_E_NOMEM", -13: "EBB_E_DEGENERATE",
+}
+F32, F64, I32, I64, U8, U32, KEY = 1, 2, 3, 4, 5, 6, 7
+AOS, SOA = 0, 1
+STVK, NH = 0, 1
+SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED = 0, 1, 2
+RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
+
+u32 = C.c_uint32
+ctx_t = C.c_void_p
+stream_t = C.c_void_p
+
+
+class View(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("count", C.c_uint64), ("rows", u32), ("cols", u32),
+                ("dtype", C.c_int32), ("layout", C.c_int32), ("elem_stride", C.c_uint64),
+                ("comp_stride", C.c_uint64), ("rel", u32), ("key_target", u32)]
+
+
+class TetmeshOut(C.Structure):
+    _fields_ = [("edges", u32), ("tail", u32), ("head", u32), ("e", u32), ("self", u32), ("index", u32)]
+
+
+class TetMapDesc(C.Structure):
+    _fields_ = [("model", C.c_int32), ("scatter", C.c_int32), ("zero_outputs", C.c_int32), ("reserved", C.c_int32),
+                ("v", u32), ("e", u32), ("u", u32), ("Dminv", u32), ("W", u32), ("mu", u32), ("lam", u32),
+                ("f", u32), ("K", u32), ("energy", u32)]
+
+
+class ImplicitDesc(C.Structure):
+    _fields_ = [("edges", u32), ("K", u32), ("A", u32), ("self", u32), ("mass", u32), ("f", u32), ("vel", u32),
+                ("b", u32), ("h", C.c_double), ("alpha", C.c_double), ("beta", C.c_double),
+                ("g", C.c_double * 3)]
+
+
+class CG(C.Structure):
+    _fields_ = [("edges", u32), ("A", u32), ("b", u32), ("x", u32), ("self", u32), ("mask", u32),
+                ("r", u32), ("p", u32), ("z", u32), ("q", u32), ("dinv", u32), ("rho", u32), ("scal", u32)]
+
+
+class ExplicitDesc(C.Structure):
+    _fields_ = [("f", u32), ("mass", u32), ("mask", u32), ("u", u32), ("vel", u32), ("h", C.c_double),
+                ("g", C.c_double * 3)]
+
+
+P = C.c_void_p
+S = C.c_int32
+SIGS = {
+    "ebb_version": (C.c_char_p, []),
+    "ebb_ctx_new": (S, [C.c_int, C.POINTER(ctx_t)]),
+    "ebb_ctx_free": (S, [ctx_t]),
+    "ebb_last_error": (C.c_char_p, [ctx_t]),
+    "ebb_error_counts": (S, [ctx_t, C.POINTER(C.c_uint64), C.c_int]),
+    "ebb_sync": (S, [ctx_t, stream_t]),
+    "ebb_relation_new": (S, [ctx_t, C.c_char_p, C.c_uint64, C.POINTER(u32)]),
+    "ebb_relation_size": (S, [ctx_t, u32, C.POINTER(C.c_uint64)]),
+    "ebb_field_new": (S, [ctx_t, u32, C.c_char_p, C.c_int, u32, u32, C.c_int, P, C.POINTER(u32)]),
+    "ebb_field_wrap": (S, [ctx_t, u32, C.c_char_p, C.c_int, u32, u32, C.c_int, P, C.POINTER(u32)]),
+    "ebb_field_find": (S, [ctx_t, u32, C.c_char_p, C.POINTER(u32)]),
+    "ebb_field_write": (S, [ctx_t, u32, P, C.c_uint64, stream_t]),
+    "ebb_field_read": (S, [ctx_t, u32, P, C.c_uint64, stream_t]),
+    "ebb_field_fill": (S, [ctx_t, u32, C.c_double, stream_t]),
+    "ebb_field_copy": (S, [ctx_t, u32, u32, stream_t]),
+    "ebb_field_convert": (S, [ctx_t, u32, u32, stream_t]),
+    "ebb_field_view": (S, [ctx_t, u32, C.POINTER(View)]),
+    "ebb_key_field": (S, [ctx_t, u32, C.c_char_p, u32, u32, u32, P, C.c_int, C.POINTER(u32)]),
+    "ebb_global_new": (S, [ctx_t, C.c_char_p, C.c_int, C.c_double, C.POINTER(u32)]),
+    "ebb_global_get": (S, [ctx_t, u32, C.POINTER(C.c_double)]),
+    "ebb_global_set": (S, [ctx_t, u32, C.c_double, stream_t]),
+    "ebb_group_by": (S, [ctx_t, u32, u32]),
+    "ebb_group_index": (S, [ctx_t, u32, C.POINTER(u32)]),
+    "ebb_renumber_morton": (S, [ctx_t, u32, u32]),
+    "ebb_sort_by_key_tuple": (S, [ctx_t, u32, u32]),
+    "ebb_tetmesh_orient": (S, [ctx_t, u32, u32, C.POINTER(C.c_uint64)]),
+    "ebb_tetmesh_build": (S, [ctx_t, u32, C.c_char_p, C.POINTER(TetmeshOut)]),
+    "ebb_tetmesh_rest": (S, [ctx_t, u32, u32, C.c_double, u32, u32, u32, stream_t]),
+    "ebb_map_tet_forces": (S, [ctx_t, C.POINTER(TetMapDesc), stream_t]),
+    "ebb_map_edge_matvec": (S, [ctx_t, u32, u32, u32, u32, u32, u32, stream_t]),
+    "ebb_global_reduce": (S, [ctx_t, C.c_int32, u32, u32, u32, u32, stream_t]),
+    "ebb_implicit_assemble": (S, [ctx_t, C.POINTER(ImplicitDesc), stream_t]),
+    "ebb_cg_init": (S, [ctx_t, C.POINTER(CG), stream_t]),
+    "ebb_cg_step": (S, [ctx_t, C.POINTER(CG), C.c_int32, stream_t]),
+    "ebb_explicit_update": (S, [ctx_t, C.POINTER(ExplicitDesc), stream_t]),
+    "ebb_implicit_update": (S, [ctx_t, u32, C.c_double, u32, u32, stream_t]),
+    "ebb_partition": (S, [ctx_t, u32, C.c_int32, u32, u32]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load the native library (raises if absent -- there is no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(python -m paper_1506_07577_b200.build)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(SIGS)

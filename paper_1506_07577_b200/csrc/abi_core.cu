@@ -1,0 +1,676 @@
+// abi_core.cu -- context, relations, fields, key-fields, globals, GroupBy.
+//
+// The relational runtime of the paper's L1 layer, re-designed as a
+// C ABI over device-resident SoA/AoS columns.  Setup calls are synchronous and
+// may allocate; the per-step calls (maps, CG) never allocate.
+#include <cub/cub.cuh>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "ebb_internal.cuh"
+
+using namespace ebb;
+
+namespace ebb {
+
+size_t dtype_size(ebb_dtype d) {
+    switch (d) {
+        case EBB_F32: return 4;
+        case EBB_F64: return 8;
+        case EBB_I32: return 4;
+        case EBB_I64: return 8;
+        case EBB_U8: return 1;
+        case EBB_U32: return 4;
+        case EBB_KEY: return 4;
+    }
+    return 0;
+}
+
+ebb_status fail(Ctx* c, ebb_status code, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return code;
+}
+
+ebb_status cuda_fail(Ctx* c, cudaError_t e, const char* where) {
+    cudaGetLastError();
+    return fail(c, e == cudaErrorMemoryAllocation ? EBB_E_NOMEM : EBB_E_CUDA, "CUDA error %s in %s",
+                cudaGetErrorString(e), where);
+}
+
+Field* get_field(Ctx* c, ebb_field f) {
+    if (!c || f >= c->fields.size() || !c->fields[f].alive) return nullptr;
+    return &c->fields[f];
+}
+
+Relation* get_rel(Ctx* c, ebb_rel r) {
+    if (!c || r >= c->rels.size()) return nullptr;
+    return &c->rels[r];
+}
+
+ebb_status scratch_reserve(Ctx* c, size_t bytes) {
+    if (bytes <= c->scratch_bytes) return EBB_OK;
+    if (c->scratch) cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    EBB_CUDA(c, cudaMalloc(&c->scratch, bytes));
+    c->scratch_bytes = bytes;
+    return EBB_OK;
+}
+
+}  // namespace ebb
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+ebb_status add_field(Ctx* c, ebb_rel rel, const char* name, ebb_dtype dt, uint32_t rows, uint32_t cols,
+                     ebb_layout layout, void* ptr, bool owned, ebb_field* out) {
+    Relation* R = get_rel(c, rel);
+    if (!R) return fail(c, EBB_E_ARG, "bad relation handle %u", rel);
+    if (!name || !*name) return fail(c, EBB_E_ARG, "field name is empty");
+    if (rows == 0 || cols == 0 || rows > 4 || cols > 4) return fail(c, EBB_E_SIZE, "field shape %ux%u", rows, cols);
+    if (dtype_size(dt) == 0) return fail(c, EBB_E_ARG, "bad dtype %d", (int)dt);
+    if (layout != EBB_AOS && layout != EBB_SOA) return fail(c, EBB_E_ARG, "bad layout");
+    for (ebb_field f : R->fields)
+        if (c->fields[f].alive && c->fields[f].name == name)
+            return fail(c, EBB_E_DUP, "field '%s' already exists on relation '%s'", name, R->name.c_str());
+    Field F;
+    F.name = name;
+    F.rel = rel;
+    F.dtype = dt;
+    F.rows = rows;
+    F.cols = cols;
+    F.layout = layout;
+    F.ptr = ptr;
+    F.owned = owned;
+    F.alive = true;
+    c->fields.push_back(F);
+    ebb_field h = (ebb_field)(c->fields.size() - 1);
+    R->fields.push_back(h);
+    *out = h;
+    return EBB_OK;
+}
+
+// ---- layout conversion kernels (element-major host order <-> SoA planes)
+template <typename T>
+__global__ void k_aos_to_soa(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t comps) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * comps) return;
+    uint64_t e = i / comps;
+    uint32_t c = (uint32_t)(i % comps);
+    out[(uint64_t)c * n + e] = in[i];
+}
+template <typename T>
+__global__ void k_soa_to_aos(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t comps) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * comps) return;
+    uint64_t e = i / comps;
+    uint32_t c = (uint32_t)(i % comps);
+    out[i] = in[(uint64_t)c * n + e];
+}
+
+ebb_status convert_layout(Ctx* c, const Field& F, uint64_t n, const void* src, void* dst, bool to_soa,
+                          cudaStream_t s) {
+    uint64_t tot = n * F.comps();
+    size_t es = dtype_size(F.dtype);
+    unsigned g = grid_for(tot, 256);
+    if (es == 8) {
+        if (to_soa) k_aos_to_soa<uint64_t><<<g, 256, 0, s>>>((const uint64_t*)src, (uint64_t*)dst, n, F.comps());
+        else k_soa_to_aos<uint64_t><<<g, 256, 0, s>>>((const uint64_t*)src, (uint64_t*)dst, n, F.comps());
+    } else if (es == 4) {
+        if (to_soa) k_aos_to_soa<uint32_t><<<g, 256, 0, s>>>((const uint32_t*)src, (uint32_t*)dst, n, F.comps());
+        else k_soa_to_aos<uint32_t><<<g, 256, 0, s>>>((const uint32_t*)src, (uint32_t*)dst, n, F.comps());
+    } else {
+        if (to_soa) k_aos_to_soa<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, n, F.comps());
+        else k_soa_to_aos<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, n, F.comps());
+    }
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+template <typename D, typename S>
+__global__ void k_convert(D* __restrict__ d, const S* __restrict__ s, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) d[i] = (D)s[i];
+}
+
+template <typename T>
+__global__ void k_fill(T* p, uint64_t n, T v) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// bounds check + narrowing of uint64 keys to uint32 storage
+__global__ void k_keys_narrow(const uint64_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n,
+                              uint64_t target_size, unsigned long long* bad_count,
+                              unsigned long long* first_bad) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t k = in[i];
+    if (k >= target_size) {
+        atomicAdd(bad_count, 1ull);
+        atomicMin(first_bad, (unsigned long long)i);
+        out[i] = 0;
+    } else {
+        out[i] = (uint32_t)k;
+    }
+}
+
+// gathers for permutations
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ in, T* __restrict__ out, const uint32_t* __restrict__ new_to_old,
+                              uint64_t n, uint32_t comps, int soa) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * comps) return;
+    if (soa) {
+        uint64_t c = i / n, e = i % n;
+        out[i] = in[c * n + new_to_old[e]];
+    } else {
+        uint64_t e = i / comps, c = i % comps;
+        out[i] = in[(uint64_t)new_to_old[e] * comps + c];
+    }
+}
+
+__global__ void k_remap_keys(uint32_t* keys, uint64_t n, const uint32_t* __restrict__ old_to_new) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = old_to_new[keys[i]];
+}
+
+__global__ void k_iota(uint32_t* p, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (uint32_t)i;
+}
+
+__global__ void k_invert_perm(const uint32_t* __restrict__ new_to_old, uint32_t* __restrict__ old_to_new, uint64_t n) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) old_to_new[new_to_old[i]] = (uint32_t)i;
+}
+
+// row_ptr[s] = first position with sorted_key >= s (lower bound), s in [0, ns]
+__global__ void k_lower_bound_index(const uint32_t* __restrict__ sorted, uint64_t n, uint32_t* __restrict__ index,
+                                    uint64_t ns) {
+    uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (s > ns) return;
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (sorted[mid] < s) lo = mid + 1;
+        else hi = mid;
+    }
+    index[s] = (uint32_t)lo;
+}
+
+__global__ void k_max_range(const uint32_t* __restrict__ index, uint64_t ns, unsigned int* out) {
+    uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (s < ns) atomicMax(out, index[s + 1] - index[s]);
+}
+
+}  // namespace
+
+namespace ebb {
+
+ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_dtype dt, uint32_t rows,
+                              uint32_t cols, ebb_layout layout, ebb_field* out) {
+    Relation* R = get_rel(c, rel);
+    size_t bytes = (size_t)R->size * rows * cols * dtype_size(dt);
+    void* p = nullptr;
+    if (bytes) {
+        EBB_CUDA(c, cudaMalloc(&p, bytes));
+        EBB_CUDA(c, cudaMemset(p, 0, bytes));
+    }
+    ebb_status st = add_field(c, rel, name.c_str(), dt, rows, cols, layout, p, true, out);
+    if (st != EBB_OK && p) cudaFree(p);
+    return st;
+}
+
+// Apply a row permutation to every field of `rel` and remap every key-field
+// (anywhere in the context) that targets `rel`.  The paper's licence: the
+// runtime may reorder relations and re-encode keys.
+ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, const uint32_t* d_old_to_new,
+                            cudaStream_t s) {
+    Relation* R = get_rel(c, rel);
+    uint64_t n = R->size;
+    for (ebb_field fh : R->fields) {
+        Field& F = c->fields[fh];
+        if (!F.alive) continue;
+        size_t es = dtype_size(F.dtype);
+        uint64_t tot = n * F.comps();
+        void* np = nullptr;
+        EBB_CUDA(c, cudaMalloc(&np, tot * es ? tot * es : 1));
+        unsigned g = grid_for(tot, 256);
+        int soa = F.layout == EBB_SOA;
+        if (es == 8)
+            k_gather_rows<uint64_t><<<g, 256, 0, s>>>((const uint64_t*)F.ptr, (uint64_t*)np, d_new_to_old, n, F.comps(), soa);
+        else if (es == 4)
+            k_gather_rows<uint32_t><<<g, 256, 0, s>>>((const uint32_t*)F.ptr, (uint32_t*)np, d_new_to_old, n, F.comps(), soa);
+        else
+            k_gather_rows<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)F.ptr, (uint8_t*)np, d_new_to_old, n, F.comps(), soa);
+        EBB_CUDA(c, cudaGetLastError());
+        if (F.owned) {
+            EBB_CUDA(c, cudaStreamSynchronize(s));
+            cudaFree(F.ptr);
+            F.ptr = np;
+        } else {
+            // borrowed memory keeps its address: copy back in place
+            EBB_CUDA(c, cudaMemcpyAsync(F.ptr, np, tot * es, cudaMemcpyDeviceToDevice, s));
+            EBB_CUDA(c, cudaStreamSynchronize(s));
+            cudaFree(np);
+        }
+    }
+    for (Field& F : c->fields) {
+        if (!F.alive || F.dtype != EBB_KEY || F.key_target != rel) continue;
+        uint64_t tot = c->rels[F.rel].size * F.comps();
+        k_remap_keys<<<grid_for(tot, 256), 256, 0, s>>>((uint32_t*)F.ptr, tot, d_old_to_new);
+        EBB_CUDA(c, cudaGetLastError());
+    }
+    // a grouping of rel or an index on rel is no longer valid unless rebuilt
+    EBB_CUDA(c, cudaStreamSynchronize(s));
+    return EBB_OK;
+}
+
+}  // namespace ebb
+
+extern "C" {
+
+const char* ebb_version(void) { return "ebb-b200 0.1 (sm_100a)"; }
+
+ebb_status ebb_ctx_new(int device, ebb_ctx* out) {
+    if (!out) return EBB_E_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return EBB_E_CUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return EBB_E_CUDA;
+    Ctx* c = new Ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMalloc(&c->d_err, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(c->d_err, 0, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->d_partials, 8 * 8192 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c->d_counter, 64 * sizeof(unsigned int)) != cudaSuccess ||
+        cudaMemset(c->d_counter, 0, 64 * sizeof(unsigned int)) != cudaSuccess) {
+        delete c;
+        return EBB_E_CUDA;
+    }
+    Relation g;
+    g.name = "__globals";
+    g.size = 1;
+    c->rels.push_back(g);
+    c->globals_rel = 0;
+    *out = c;
+    return EBB_OK;
+}
+
+ebb_status ebb_ctx_free(ebb_ctx ctx) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c) return EBB_E_ARG;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (Field& F : c->fields)
+        if (F.alive && F.owned && F.ptr) cudaFree(F.ptr);
+    if (c->scratch) cudaFree(c->scratch);
+    cudaFree(c->d_err);
+    cudaFree(c->d_partials);
+    cudaFree(c->d_counter);
+    delete c;
+    return EBB_OK;
+}
+
+const char* ebb_last_error(ebb_ctx ctx) {
+    Ctx* c = (Ctx*)ctx;
+    return c ? c->err.c_str() : "null context";
+}
+
+ebb_status ebb_error_counts(ebb_ctx ctx, uint64_t out[4], int reset) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !out) return EBB_E_ARG;
+    EBB_CUDA(c, cudaDeviceSynchronize());
+    unsigned long long h[4];
+    EBB_CUDA(c, cudaMemcpy(h, c->d_err, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 4; ++i) out[i] = h[i];
+    if (reset) EBB_CUDA(c, cudaMemset(c->d_err, 0, sizeof(h)));
+    return EBB_OK;
+}
+
+ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c) return EBB_E_ARG;
+    EBB_CUDA(c, cudaStreamSynchronize((cudaStream_t)s));
+    return EBB_OK;
+}
+
+ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_rel* out) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !name || !out) return fail(c, EBB_E_ARG, "null argument");
+    if (size == 0) return fail(c, EBB_E_SIZE, "relation '%s' has zero size", name);
+    for (auto& R : c->rels)
+        if (R.name == name) return fail(c, EBB_E_DUP, "relation '%s' already exists", name);
+    Relation R;
+    R.name = name;
+    R.size = size;
+    c->rels.push_back(R);
+    *out = (ebb_rel)(c->rels.size() - 1);
+    return EBB_OK;
+}
+
+ebb_status ebb_relation_size(ebb_ctx ctx, ebb_rel rel, uint64_t* out) {
+    Ctx* c = (Ctx*)ctx;
+    Relation* R = get_rel(c, rel);
+    if (!R || !out) return fail(c, EBB_E_ARG, "bad relation");
+    *out = R->size;
+    return EBB_OK;
+}
+
+ebb_status ebb_field_new(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype dtype, uint32_t rows, uint32_t cols,
+                         ebb_layout layout, const void* host_init, ebb_field* out) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !out) return fail(c, EBB_E_ARG, "null argument");
+    if (dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "use ebb_key_field for key-fields");
+    ebb_field h;
+    EBB_TRY(new_internal_field(c, rel, name ? name : "", dtype, rows, cols, layout, &h));
+    Field& F = c->fields[h];
+    if (host_init) {
+        uint64_t nbytes = c->rels[rel].size * F.comps() * dtype_size(dtype);
+        ebb_status st = ebb_field_write(ctx, h, host_init, nbytes, nullptr);
+        if (st != EBB_OK) return st;
+        EBB_CUDA(c, cudaDeviceSynchronize());
+    }
+    *out = h;
+    return EBB_OK;
+}
+
+ebb_status ebb_field_wrap(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype dtype, uint32_t rows, uint32_t cols,
+                          ebb_layout layout, void* device_ptr, ebb_field* out) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !out || !device_ptr) return fail(c, EBB_E_ARG, "null argument");
+    if (dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "key-fields must be created by ebb_key_field");
+    return add_field(c, rel, name, dtype, rows, cols, layout, device_ptr, false, out);
+}
+
+ebb_status ebb_field_find(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_field* out) {
+    Ctx* c = (Ctx*)ctx;
+    Relation* R = get_rel(c, rel);
+    if (!R || !name || !out) return fail(c, EBB_E_ARG, "bad argument");
+    for (ebb_field f : R->fields)
+        if (c->fields[f].alive && c->fields[f].name == name) {
+            *out = f;
+            return EBB_OK;
+        }
+    return fail(c, EBB_E_ARG, "no field '%s' on relation '%s'", name, R->name.c_str());
+}
+
+ebb_status ebb_field_write(ebb_ctx ctx, ebb_field f, const void* host, uint64_t nbytes, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field* F = get_field(c, f);
+    if (!F || !host) return fail(c, EBB_E_ARG, "bad field or null host pointer");
+    uint64_t n = c->rels[F->rel].size;
+    uint64_t want = n * F->comps() * dtype_size(F->dtype);
+    if (nbytes != want) return fail(c, EBB_E_SIZE, "field '%s': %llu bytes given, %llu expected", F->name.c_str(),
+                                    (unsigned long long)nbytes, (unsigned long long)want);
+    cudaStream_t st = (cudaStream_t)s;
+    if (F->layout == EBB_AOS || F->comps() == 1) {
+        EBB_CUDA(c, cudaMemcpyAsync(F->ptr, host, nbytes, cudaMemcpyHostToDevice, st));
+        return EBB_OK;
+    }
+    EBB_TRY(scratch_reserve(c, nbytes));
+    EBB_CUDA(c, cudaMemcpyAsync(c->scratch, host, nbytes, cudaMemcpyHostToDevice, st));
+    return convert_layout(c, *F, n, c->scratch, F->ptr, true, st);
+}
+
+ebb_status ebb_field_read(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field* F = get_field(c, f);
+    if (!F || !host) return fail(c, EBB_E_ARG, "bad field or null host pointer");
+    uint64_t n = c->rels[F->rel].size;
+    uint64_t want = n * F->comps() * dtype_size(F->dtype);
+    if (nbytes != want) return fail(c, EBB_E_SIZE, "field '%s': %llu bytes given, %llu expected", F->name.c_str(),
+                                    (unsigned long long)nbytes, (unsigned long long)want);
+    cudaStream_t st = (cudaStream_t)s;
+    if (F->layout == EBB_AOS || F->comps() == 1) {
+        EBB_CUDA(c, cudaMemcpyAsync(host, F->ptr, nbytes, cudaMemcpyDeviceToHost, st));
+    } else {
+        EBB_TRY(scratch_reserve(c, nbytes));
+        EBB_TRY(convert_layout(c, *F, n, F->ptr, c->scratch, false, st));
+        EBB_CUDA(c, cudaMemcpyAsync(host, c->scratch, nbytes, cudaMemcpyDeviceToHost, st));
+    }
+    EBB_CUDA(c, cudaStreamSynchronize(st));
+    return EBB_OK;
+}
+
+ebb_status ebb_field_fill(ebb_ctx ctx, ebb_field f, double value, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field* F = get_field(c, f);
+    if (!F) return fail(c, EBB_E_ARG, "bad field");
+    if (F->dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "cannot fill a key-field");
+    uint64_t n = c->rels[F->rel].size * F->comps();
+    cudaStream_t st = (cudaStream_t)s;
+    unsigned g = grid_for(n, 256);
+    switch (F->dtype) {
+        case EBB_F32: k_fill<float><<<g, 256, 0, st>>>((float*)F->ptr, n, (float)value); break;
+        case EBB_F64: k_fill<double><<<g, 256, 0, st>>>((double*)F->ptr, n, value); break;
+        case EBB_I32: k_fill<int32_t><<<g, 256, 0, st>>>((int32_t*)F->ptr, n, (int32_t)value); break;
+        case EBB_I64: k_fill<int64_t><<<g, 256, 0, st>>>((int64_t*)F->ptr, n, (int64_t)value); break;
+        case EBB_U32: k_fill<uint32_t><<<g, 256, 0, st>>>((uint32_t*)F->ptr, n, (uint32_t)value); break;
+        case EBB_U8: k_fill<uint8_t><<<g, 256, 0, st>>>((uint8_t*)F->ptr, n, (uint8_t)value); break;
+        default: return fail(c, EBB_E_TYPE, "bad dtype");
+    }
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+ebb_status ebb_field_copy(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field* D = get_field(c, dst);
+    Field* S = get_field(c, src);
+    if (!D || !S) return fail(c, EBB_E_ARG, "bad field");
+    if (D->dtype != S->dtype || D->comps() != S->comps() || D->layout != S->layout ||
+        c->rels[D->rel].size != c->rels[S->rel].size)
+        return fail(c, EBB_E_TYPE, "field_copy: '%s' and '%s' differ in type/shape/layout", D->name.c_str(),
+                    S->name.c_str());
+    uint64_t nbytes = c->rels[D->rel].size * D->comps() * dtype_size(D->dtype);
+    EBB_CUDA(c, cudaMemcpyAsync(D->ptr, S->ptr, nbytes, cudaMemcpyDeviceToDevice, (cudaStream_t)s));
+    return EBB_OK;
+}
+
+ebb_status ebb_field_convert(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field* D = get_field(c, dst);
+    Field* S = get_field(c, src);
+    if (!D || !S) return fail(c, EBB_E_ARG, "bad field");
+    bool fl = (D->dtype == EBB_F32 || D->dtype == EBB_F64) && (S->dtype == EBB_F32 || S->dtype == EBB_F64);
+    if (!fl || D->comps() != S->comps() || D->layout != S->layout || c->rels[D->rel].size != c->rels[S->rel].size)
+        return fail(c, EBB_E_TYPE, "field_convert: '%s' <- '%s' needs float fields of equal shape/layout/size",
+                    D->name.c_str(), S->name.c_str());
+    if (D->dtype == S->dtype) return ebb_field_copy(ctx, dst, src, s);
+    uint64_t n = c->rels[D->rel].size * D->comps();
+    if (D->dtype == EBB_F32)
+        k_convert<float, double><<<grid_for(n, 256), 256, 0, (cudaStream_t)s>>>((float*)D->ptr, (const double*)S->ptr, n);
+    else
+        k_convert<double, float><<<grid_for(n, 256), 256, 0, (cudaStream_t)s>>>((double*)D->ptr, (const float*)S->ptr, n);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+ebb_status ebb_field_view(ebb_ctx ctx, ebb_field f, ebb_view* out) {
+    Ctx* c = (Ctx*)ctx;
+    Field* F = get_field(c, f);
+    if (!F || !out) return fail(c, EBB_E_ARG, "bad field");
+    uint64_t n = c->rels[F->rel].size;
+    size_t es = dtype_size(F->dtype);
+    out->data = F->ptr;
+    out->count = n;
+    out->rows = F->rows;
+    out->cols = F->cols;
+    out->dtype = F->dtype;
+    out->layout = F->layout;
+    if (F->layout == EBB_AOS) {
+        out->elem_stride = es * F->comps();
+        out->comp_stride = es;
+    } else {
+        out->elem_stride = es;
+        out->comp_stride = es * n;
+    }
+    out->rel = F->rel;
+    out->key_target = F->key_target;
+    return EBB_OK;
+}
+
+ebb_status ebb_key_field(ebb_ctx ctx, ebb_rel owner, const char* name, ebb_rel target, uint32_t rows, uint32_t cols,
+                         const uint64_t* keys, int keys_on_device, ebb_field* out) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !keys || !out) return fail(c, EBB_E_ARG, "null argument");
+    Relation* O = get_rel(c, owner);
+    Relation* T = get_rel(c, target);
+    if (!O || !T) return fail(c, EBB_E_ARG, "bad relation handle");
+    if (T->size > 0xFFFFFFFFull) return fail(c, EBB_E_RANGE, "target relation '%s' exceeds 2^32-1 rows", T->name.c_str());
+    ebb_field h;
+    EBB_TRY(new_internal_field(c, owner, name ? name : "", EBB_KEY, rows, cols, EBB_AOS, &h));
+    c->fields[h].key_target = target;
+    uint64_t n = O->size * rows * cols;
+    DevBuf in;
+    const uint64_t* dkeys = keys;
+    if (!keys_on_device) {
+        EBB_CUDA(c, cudaMalloc(&in.p, n * 8));
+        EBB_CUDA(c, cudaMemcpy(in.p, keys, n * 8, cudaMemcpyHostToDevice));
+        dkeys = (const uint64_t*)in.p;
+    }
+    DevBuf flag;
+    EBB_CUDA(c, cudaMalloc(&flag.p, 16));
+    unsigned long long init[2] = {0ull, ~0ull};
+    EBB_CUDA(c, cudaMemcpy(flag.p, init, 16, cudaMemcpyHostToDevice));
+    unsigned long long* fl = (unsigned long long*)flag.p;
+    k_keys_narrow<<<grid_for(n, 256), 256>>>(dkeys, (uint32_t*)c->fields[h].ptr, n, T->size, fl, fl + 1);
+    EBB_CUDA(c, cudaGetLastError());
+    unsigned long long res[2];
+    EBB_CUDA(c, cudaMemcpy(res, flag.p, 16, cudaMemcpyDeviceToHost));
+    if (res[0]) {
+        // drop the field again: a key-field is in bounds by construction
+        Field& F = c->fields[h];
+        cudaFree(F.ptr);
+        F.ptr = nullptr;
+        F.alive = false;
+        O->fields.pop_back();
+        return fail(c, EBB_E_BOUNDS, "key-field '%s': %llu keys out of range of '%s' (size %llu); first at flat index %llu",
+                    name, res[0], T->name.c_str(), (unsigned long long)T->size, res[1]);
+    }
+    *out = h;
+    return EBB_OK;
+}
+
+ebb_status ebb_global_new(ebb_ctx ctx, const char* name, ebb_dtype dtype, double init, ebb_field* out) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !out) return fail(c, EBB_E_ARG, "null argument");
+    if (dtype != EBB_F64 && dtype != EBB_F32 && dtype != EBB_I64 && dtype != EBB_I32)
+        return fail(c, EBB_E_TYPE, "globals are scalar numeric");
+    ebb_field h;
+    EBB_TRY(new_internal_field(c, c->globals_rel, name ? name : "", dtype, 1, 1, EBB_AOS, &h));
+    c->fields[h].is_global = true;
+    EBB_TRY(ebb_global_set(ctx, h, init, nullptr));
+    EBB_CUDA(c, cudaDeviceSynchronize());
+    *out = h;
+    return EBB_OK;
+}
+
+ebb_status ebb_global_get(ebb_ctx ctx, ebb_field g, double* out) {
+    Ctx* c = (Ctx*)ctx;
+    Field* F = get_field(c, g);
+    if (!F || !out || !F->is_global) return fail(c, EBB_E_ARG, "not a global");
+    EBB_CUDA(c, cudaDeviceSynchronize());
+    union { double d; float f; int64_t l; int32_t i; } u;
+    EBB_CUDA(c, cudaMemcpy(&u, F->ptr, dtype_size(F->dtype), cudaMemcpyDeviceToHost));
+    switch (F->dtype) {
+        case EBB_F64: *out = u.d; break;
+        case EBB_F32: *out = u.f; break;
+        case EBB_I64: *out = (double)u.l; break;
+        default: *out = (double)u.i; break;
+    }
+    return EBB_OK;
+}
+
+ebb_status ebb_global_set(ebb_ctx ctx, ebb_field g, double value, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field* F = get_field(c, g);
+    if (!F || !F->is_global) return fail(c, EBB_E_ARG, "not a global");
+    return ebb_field_fill(ctx, g, value, s);
+}
+
+ebb_status ebb_group_by(ebb_ctx ctx, ebb_rel rel, ebb_field key) {
+    Ctx* c = (Ctx*)ctx;
+    Relation* R = get_rel(c, rel);
+    Field* K = get_field(c, key);
+    if (!R || !K) return fail(c, EBB_E_ARG, "bad handle");
+    if (K->dtype != EBB_KEY || K->comps() != 1 || K->rel != rel)
+        return fail(c, EBB_E_TYPE, "group_by: '%s' is not a scalar key-field of '%s'", K->name.c_str(), R->name.c_str());
+    if (R->grouped_by != EBB_NONE) return fail(c, EBB_E_STATE, "relation '%s' is already grouped", R->name.c_str());
+    ebb_rel src = K->key_target;
+    uint64_t n = R->size, ns = c->rels[src].size;
+    if (n > 0xFFFFFFFFull) return fail(c, EBB_E_RANGE, "relation too large for 32-bit keys");
+    DevBuf kout, vin, vout, inv, tmp;
+    EBB_CUDA(c, cudaMalloc(&kout.p, n * 4));
+    EBB_CUDA(c, cudaMalloc(&vin.p, n * 4));
+    EBB_CUDA(c, cudaMalloc(&vout.p, n * 4));
+    EBB_CUDA(c, cudaMalloc(&inv.p, n * 4));
+    k_iota<<<grid_for(n, 256), 256>>>((uint32_t*)vin.p, n);
+    size_t tb = 0;
+    int end_bit = 1;
+    while (end_bit < 32 && (1ull << end_bit) < ns) ++end_bit;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const uint32_t*)K->ptr, (uint32_t*)kout.p, (const uint32_t*)vin.p,
+                                    (uint32_t*)vout.p, (int)n, 0, end_bit);
+    EBB_CUDA(c, cudaMalloc(&tmp.p, tb));
+    EBB_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp.p, tb, (const uint32_t*)K->ptr, (uint32_t*)kout.p,
+                                                (const uint32_t*)vin.p, (uint32_t*)vout.p, (int)n, 0, end_bit));
+    k_invert_perm<<<grid_for(n, 256), 256>>>((const uint32_t*)vout.p, (uint32_t*)inv.p, n);
+    EBB_CUDA(c, cudaGetLastError());
+    EBB_TRY(permute_relation(c, rel, (const uint32_t*)vout.p, (const uint32_t*)inv.p, nullptr));
+    // hidden index on the source relation ("range of rows ... encoded as two indices")
+    ebb_field idx;
+    Relation* Sr = get_rel(c, src);
+    std::string iname = "__index_" + R->name;
+    // index has ns+1 entries: allocate on a fresh hidden relation of that size
+    ebb_rel irel;
+    EBB_TRY(ebb_relation_new(ctx, ("__index_rel_" + R->name).c_str(), ns + 1, &irel));
+    EBB_TRY(new_internal_field(c, irel, iname, EBB_U32, 1, 1, EBB_AOS, &idx));
+    R = get_rel(c, rel);
+    Sr = get_rel(c, src);
+    K = get_field(c, key);
+    k_lower_bound_index<<<grid_for(ns + 1, 256), 256>>>((const uint32_t*)K->ptr, n, (uint32_t*)c->fields[idx].ptr, ns);
+    DevBuf mx;
+    EBB_CUDA(c, cudaMalloc(&mx.p, 4));
+    EBB_CUDA(c, cudaMemset(mx.p, 0, 4));
+    k_max_range<<<grid_for(ns, 256), 256>>>((const uint32_t*)c->fields[idx].ptr, ns, (unsigned int*)mx.p);
+    unsigned int hmx = 0;
+    EBB_CUDA(c, cudaMemcpy(&hmx, mx.p, 4, cudaMemcpyDeviceToHost));
+    R->grouped_by = key;
+    R->index = idx;
+    R->max_group = hmx;
+    Sr->index = idx;
+    Sr->max_group = hmx;
+    return EBB_OK;
+}
+
+ebb_status ebb_group_index(ebb_ctx ctx, ebb_rel rel, ebb_field* index_out) {
+    Ctx* c = (Ctx*)ctx;
+    Relation* R = get_rel(c, rel);
+    if (!R || !index_out) return fail(c, EBB_E_ARG, "bad argument");
+    if (R->index == EBB_NONE) return fail(c, EBB_E_STATE, "relation '%s' has no group index", R->name.c_str());
+    *index_out = R->index;
+    return EBB_OK;
+}
+
+}  // extern "C"

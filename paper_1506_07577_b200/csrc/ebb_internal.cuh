@@ -1,0 +1,88 @@
+// ebb_internal.cuh -- runtime state behind the C ABI (include/ebb.h).
+// Relations and fields follow the paper's relational model (P:405-420,
+// P:663-690).  Everything here is host C++ plus small device
+// helpers; kernels live in the *.cu files next to this header.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ebb.h"
+
+struct ebb_ctx_s {};
+
+namespace ebb {
+
+struct Field {
+    std::string name;
+    ebb_rel rel = EBB_NONE;
+    ebb_dtype dtype = EBB_F64;
+    uint32_t rows = 1, cols = 1;
+    ebb_layout layout = EBB_AOS;
+    void* ptr = nullptr;
+    bool owned = false;
+    bool alive = false;
+    ebb_rel key_target = EBB_NONE;  // key-fields only
+    bool is_global = false;
+    uint32_t comps() const { return rows * cols; }
+};
+
+struct Relation {
+    std::string name;
+    uint64_t size = 0;
+    std::vector<ebb_field> fields;
+    ebb_field grouped_by = EBB_NONE;   // key-field this relation is grouped by
+    ebb_field index = EBB_NONE;        // hidden CSR index on the source
+    uint32_t max_group = 0;            // longest range of an index on this relation
+};
+
+struct Ctx : ebb_ctx_s {
+    int device = 0;
+    std::vector<Relation> rels;
+    std::vector<Field> fields;
+    std::string err;
+    ebb_rel globals_rel = EBB_NONE;
+    unsigned long long* d_err = nullptr;   // device error word [4]
+    // reusable scratch (grown on demand, never shrunk)
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    double* d_partials = nullptr;          // per-block reduction partials
+    unsigned int* d_counter = nullptr;     // last-block-done tickets
+    int num_sms = 148;
+};
+
+size_t dtype_size(ebb_dtype d);
+ebb_status fail(Ctx* c, ebb_status code, const char* fmt, ...);
+ebb_status cuda_fail(Ctx* c, cudaError_t e, const char* where);
+Field* get_field(Ctx* c, ebb_field f);
+Relation* get_rel(Ctx* c, ebb_rel r);
+ebb_status scratch_reserve(Ctx* c, size_t bytes);
+ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_dtype dt, uint32_t rows,
+                              uint32_t cols, ebb_layout layout, ebb_field* out);
+ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, const uint32_t* d_old_to_new,
+                            cudaStream_t s);
+
+#define EBB_CUDA(c, call)                                               \
+    do {                                                                \
+        cudaError_t _e = (call);                                        \
+        if (_e != cudaSuccess) return ::ebb::cuda_fail((c), _e, #call); \
+    } while (0)
+
+#define EBB_TRY(call)                  \
+    do {                               \
+        ebb_status _s = (call);        \
+        if (_s != EBB_OK) return _s;   \
+    } while (0)
+
+inline unsigned grid_for(uint64_t n, unsigned block) {
+    uint64_t g = (n + block - 1) / block;
+    return (unsigned)(g == 0 ? 1 : g);
+}
+
+// error word slots
+enum { ERR_INVERTED = 0, ERR_NOT_SPD = 1, ERR_BOUNDS = 2 };
+
+}  // namespace ebb

@@ -1,0 +1,61 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol that
+include/ebb.h declares; the Python binding declares exactly that set.  No
+compute calls are made (no GPU here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "ebb.h")
+
+
+def declared():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:ebb_status|const char\*)\s+(ebb_\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_1506_07577_b200 import build
+    return build.build()
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared()
+    for n in ("ebb_relation_new", "ebb_field_new", "ebb_key_field", "ebb_map_tet_forces",
+              "ebb_map_edge_matvec", "ebb_global_reduce", "ebb_cg_step"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    L = ctypes.CDLL(libpath)
+    for n in declared():
+        assert hasattr(L, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ebb_\w+)", out))
+    assert set(declared()) <= exported
+
+
+def test_binding_matches_header(libpath):
+    from paper_1506_07577_b200 import _abi
+    assert sorted(_abi.exported_symbols()) == declared()
+    L = _abi.lib()
+    assert L.ebb_version().decode().startswith("ebb-b200")
+
+
+def test_ctx_new_fails_cleanly_without_gpu(libpath):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1506_07577_b200 import ebb
+    with pytest.raises(ebb.EbbError):
+        ebb.Context(0)
+
+
+def test_sass_is_sm100a(libpath):
+    out = subprocess.run(["cuobjdump", "--list-elf", libpath], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

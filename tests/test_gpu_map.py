@@ -1,0 +1,100 @@
+"""GPU parity of the element map (a4-a8) against the oracle (O6/O7).
+
+Bars (BASELINE.json north_star): fp64 forces relative L2 <= 1e-12; fp32 <= 1e-5
+with the oracle fed the fp32-rounded inputs.  The same bars are applied to the
+stiffness (relative L2 over all blocks) and the strain energy.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import Case, gpu_fem, oracle_renumbered, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1506_07577_b200 import ebb
+    c = ebb.Context(0)
+    yield c
+    c.close()
+
+
+def _oracle_map(case, m, order, tet_src, model, u=None):
+    u = case.u[order] if u is None else u
+    return oracle.element_map(model, m.X, u, m.tets, m.Dminv, m.W, case.mu[tet_src], case.lam[tet_src],
+                              e=m.e, ne=m.ne)
+
+
+@pytest.mark.parametrize("model", ["stvk", "nh"])
+@pytest.mark.parametrize("n,mesh", [(4, "kuhn6"), (9, "kuhn6"), (4, "alt5")])
+def test_map_fp64(ctx, model, n, mesh):
+    case = Case(n=n, mesh=mesh, model=model, spread=0.1)
+    fem = gpu_fem(ctx, case, name=f"m64{model}{n}{mesh}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, model)
+    fem.map_forces(model)
+    assert rel_l2(fem.f.read(), f) <= 1e-12
+    assert rel_l2(fem.K.read(), K) <= 1e-12
+    assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+    assert ctx.error_counts(reset=True)["inverted"] == 0
+
+
+@pytest.mark.parametrize("model", ["stvk", "nh"])
+def test_map_fp32_displacement_form(ctx, model):
+    case = Case(n=8, model=model, spread=0.1)
+    # oracle is fed the fp32-rounded inputs
+    case.u = case.u.astype(np.float32).astype(np.float64)
+    case.mu = case.mu.astype(np.float32).astype(np.float64)
+    case.lam = case.lam.astype(np.float32).astype(np.float64)
+    fem = gpu_fem(ctx, case, dtype="f32", name=f"m32{model}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, model)
+    fem.map_forces(model)
+    assert rel_l2(fem.f.read(), f) <= 1e-5
+    assert rel_l2(fem.K.read(), K) <= 1e-5
+    assert abs(fem.energy.get() - en) <= 1e-5 * abs(en)
+
+
+def test_map_small_strain_fp32(ctx):
+    """1e-3 strain: the displacement form keeps fp32 within 1e-5."""
+    case = Case(n=6, model="nh")
+    case.u = (case.u * 0.01).astype(np.float32).astype(np.float64)
+    fem = gpu_fem(ctx, case, dtype="f32", name="m32small")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, "nh")
+    fem.map_forces("nh")
+    assert rel_l2(fem.f.read(), f) <= 1e-5
+
+
+def test_map_rest_state_is_zero(ctx):
+    case = Case(n=3)
+    case.u[:] = 0.0
+    fem = gpu_fem(ctx, case, name="mrest")
+    fem.map_forces("nh")
+    assert np.abs(fem.f.read()).max() == 0.0 and fem.energy.get() == 0.0
+
+
+def test_map_inverted_element_counted(ctx):
+    case = Case(n=2, order_seed=None)
+    fem = gpu_fem(ctx, case, renumber=False, name="minv")
+    u = case.u.copy()
+    u[:] = 0.0
+    u[:, 0] = -2.0 * case.X[:, 0]            # mirror x: every tet inverted
+    fem.u.write(u)
+    ctx.error_counts(reset=True)
+    fem.map_forces("nh")
+    assert ctx.error_counts(reset=True)["inverted"] == fem.nt
+
+
+def test_map_energy_deterministic(ctx):
+    case = Case(n=6)
+    fem = gpu_fem(ctx, case, name="mdet")
+    fem.map_forces("nh")
+    e1 = fem.energy.get()
+    fem.map_forces("nh")
+    assert fem.energy.get() == e1

@@ -1,0 +1,156 @@
+"""GPU parity of the edge matvec (a10), global reductions (a8), implicit assembly
+(a9), Jacobi-PCG (a11-a12) and both integrators against the oracle.
+
+Bars: CG iterates <= 1e-8 relative after 50 iterations (fp64, north_star);
+explicit steps <= 1e-12 (fp64) per step; matvec <= 1e-13 (fp64), 1e-6 (fp32).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import Case, gpu_fem, oracle_renumbered, rel_l2
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1506_07577_b200 import ebb
+    c = ebb.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-13), ("f32", 1e-6)])
+def test_edge_matvec(ctx, dtype, tol):
+    case = Case(n=7)
+    fem = gpu_fem(ctx, case, dtype=dtype, name=f"mv{dtype}")
+    m, *_ = oracle_renumbered(case)
+    rng = np.random.default_rng(6)
+    A = rng.uniform(-1, 1, size=(m.ne, 3, 3))
+    p = rng.uniform(-1, 1, size=(m.nv, 3))
+    if dtype == "f32":
+        A = A.astype(np.float32).astype(np.float64)
+        p = p.astype(np.float32).astype(np.float64)
+    fem.K.write(A)
+    P = fem.verts.field("p_mv", dtype, (3, 1), init=p)
+    Q = fem.verts.field("q_mv", dtype, (3, 1))
+    fem.matvec(fem.K, P, Q)
+    ref = oracle.edge_matvec(m.row_ptr, m.head, A, p)
+    assert rel_l2(Q.read(), ref) <= tol
+    # masked + fused p.q (global `+=`)
+    pq = ctx.global_(f"pq_{dtype}")
+    fem.matvec(fem.K, P, Q, mask=True, pq=pq)
+    free = fem.free.read()
+    refm = ref * free[:, None]
+    assert rel_l2(Q.read(), refm) <= tol
+    assert abs(pq.get() - oracle.dot(p, refm)) <= 10 * tol * np.abs(p).sum() * np.abs(refm).max()
+
+
+def test_global_reduce_ops(ctx):
+    from paper_1506_07577_b200 import _abi as A
+    g = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+    R = ctx.relation("red", 4)
+    x = R.field("x", "f64", init=g["global_sum"]["values"])
+    out = ctx.global_("red_out")
+    for op, want in ((A.RED_SUM, 10.0), (A.RED_MAX, 6.0), (A.RED_MIN, 0.0)):
+        ctx.check(ctx.L.ebb_global_reduce(ctx.h, op, x.h, A.NONE, A.NONE, out.h, None))
+        assert out.get() == want
+    # S:295 measureTotalEnergy: E = sum 1/2 m qd.qd = 3.0, as a DOT of (m/2 qd) and qd
+    e = g["global_energy"]
+    V = ctx.relation("red.v", 3)
+    qd = np.array(e["qd"], dtype=np.float64)
+    a = V.field("a", "f64", (3, 1), init=0.5 * np.array(e["mass"])[:, None] * qd)
+    b = V.field("b", "f64", (3, 1), init=qd)
+    ctx.check(ctx.L.ebb_global_reduce(ctx.h, A.RED_DOT, a.h, b.h, A.NONE, out.h, None))
+    assert out.get() == e["E"]
+
+
+def test_global_reduce_large_masked(ctx):
+    from paper_1506_07577_b200 import _abi as A
+    n = 1_000_003
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((n, 3))
+    mk = (rng.random(n) < 0.7).astype(np.uint8)
+    R = ctx.relation("redL", n)
+    fx = R.field("x", "f64", (3, 1), init=x)
+    fm = R.field("m", "u8", init=mk)
+    out = ctx.global_("redL_out")
+    ctx.check(ctx.L.ebb_global_reduce(ctx.h, A.RED_DOT, fx.h, fx.h, fm.h, out.h, None))
+    ref = float(np.sum(x[mk == 1] ** 2))
+    assert abs(out.get() - ref) <= 1e-12 * ref
+    v1 = out.get()
+    ctx.check(ctx.L.ebb_global_reduce(ctx.h, A.RED_DOT, fx.h, fx.h, fm.h, out.h, None))
+    assert out.get() == v1                          # deterministic two-pass
+    ctx.check(ctx.L.ebb_global_reduce(ctx.h, A.RED_MAX, fx.h, A.NONE, A.NONE, out.h, None))
+    assert out.get() == x.max()
+
+
+@pytest.mark.parametrize("model", ["nh", "stvk"])
+def test_implicit_step(ctx, model):
+    case = Case(n=6, model=model, vel_amp=0.05)
+    h, iters, al, be = 1e-2, 50, 0.05, 0.002
+    fem = gpu_fem(ctx, case, name=f"imp{model}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    out = oracle.implicit_step(m, model, case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                               case.free[order], h, iters=iters, alpha=al, beta=be)
+    fem.implicit_step(model, h=h, iters=iters, alpha=al, beta=be)
+    assert rel_l2(fem.b.read(), out["b"]) <= 1e-12
+    assert rel_l2(fem.K.read(), out["A"]) <= 1e-12          # A assembled in place of K
+    assert rel_l2(fem.dv.read(), out["dv"]) <= 1e-8
+    assert rel_l2(fem.vel.read(), out["v"]) <= 1e-8
+    assert rel_l2(fem.u.read(), out["u"]) <= 1e-8
+    assert abs(fem.cg_rho() - out["rho"][-1]) <= 1e-6 * abs(out["rho"][0])
+    assert ctx.error_counts(reset=True)["not_spd"] == 0
+
+
+def test_explicit_C1(ctx):
+    """BASELINE configs[0]: StVK explicit, 4x4x4 Kuhn cube (384 tets), fp64, 10 steps."""
+    case = Case(n=4, model="stvk", E=1e6)
+    h = 1e-4
+    fem = gpu_fem(ctx, case, name="C1")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    u, v = case.u[order], case.vel[order]
+    mu, lam, free = case.mu[tet_src], case.lam[tet_src], case.free[order]
+    for step in range(10):
+        u, v, f, en = oracle.explicit_step(m, "stvk", u, v, mu, lam, free, h)
+        fem.explicit_step("stvk", h=h)
+        assert rel_l2(fem.u.read(), u) <= 1e-12, step
+        assert rel_l2(fem.vel.read(), v) <= 1e-12, step
+        assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+
+
+def test_cg_zero_rhs_noop(ctx):
+    case = Case(n=3)
+    fem = gpu_fem(ctx, case, name="cg0")
+    fem.map_forces("nh")
+    fem.assemble(1e-2)
+    fem.b.fill(0.0)
+    fem.cg_init()
+    fem.cg_step(5)
+    assert np.all(fem.dv.read() == 0.0) and fem.cg_rho() == 0.0
+
+
+def test_C2_full_size_implicit_step(ctx):
+    """BASELINE configs[1] at full size (998,250 tets), bench launch configuration:
+    integer maps bit-exact, f/K <= 1e-12, CG iterate <= 1e-8 after 50 iterations."""
+    case = Case(n=55, model="nh", E=2e5)
+    fem = gpu_fem(ctx, case, name="C2")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    assert np.array_equal(fem.vert_order(), order)
+    assert np.array_equal(fem.tet_order(), tet_src)
+    assert np.array_equal(fem.head.read(), m.head)
+    out = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                               case.free[order], 1e-2, iters=50)
+    fem.implicit_step("nh", h=1e-2, iters=50)
+    assert rel_l2(fem.f.read(), out["f"]) <= 1e-12
+    assert rel_l2(fem.K.read(), out["A"]) <= 1e-12
+    assert rel_l2(fem.dv.read(), out["dv"]) <= 1e-8
+    assert ctx.error_counts(reset=True) == dict(inverted=0, not_spd=0, bounds=0)

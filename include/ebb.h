@@ -96,6 +96,20 @@ const char* ebb_last_error(ebb_ctx ctx);
  * out[2] key out of range, out[3] reserved. */
 ebb_status ebb_error_counts(ebb_ctx ctx, uint64_t out[4], int reset);
 ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s);
+/* Instrumentation ("we instrument Ebb directly").  When enabled,
+ * every launch of a hot kernel is bracketed by CUDA events recorded on the
+ * launching stream.  kernel ids: EBB_K_TET_MAP, EBB_K_EDGE_MATVEC,
+ * EBB_K_CG_UPDATE, EBB_K_CG_DIR, EBB_K_ASSEMBLE.  timing_read is synchronous
+ * and returns the summed device time (ms) and the number of timed launches. */
+#define EBB_K_TET_MAP 0
+#define EBB_K_EDGE_MATVEC 1
+#define EBB_K_CG_UPDATE 2
+#define EBB_K_CG_DIR 3
+#define EBB_K_ASSEMBLE 4
+ebb_status ebb_timing_enable(ebb_ctx ctx, int on);
+ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64_t* launches, int reset);
+/* Number of kernels this context has launched (all entry points). */
+ebb_status ebb_launch_count(ebb_ctx ctx, uint64_t* out, int reset);
 
 /* ---- relations and fields ----------- */
 ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_rel* out);

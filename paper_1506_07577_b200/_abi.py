@@ -25,6 +25,7 @@ AOS, SOA = 0, 1
 STVK, NH = 0, 1
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED = 0, 1, 2
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
+K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE = 0, 1, 2, 3, 4
 
 u32 = C.c_uint32
 ctx_t = C.c_void_p
@@ -72,6 +73,9 @@ SIGS = {
     "ebb_last_error": (C.c_char_p, [ctx_t]),
     "ebb_error_counts": (S, [ctx_t, C.POINTER(C.c_uint64), C.c_int]),
     "ebb_sync": (S, [ctx_t, stream_t]),
+    "ebb_timing_enable": (S, [ctx_t, C.c_int]),
+    "ebb_timing_read": (S, [ctx_t, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int]),
+    "ebb_launch_count": (S, [ctx_t, C.POINTER(C.c_uint64), C.c_int]),
     "ebb_relation_new": (S, [ctx_t, C.c_char_p, C.c_uint64, C.POINTER(u32)]),
     "ebb_relation_size": (S, [ctx_t, u32, C.POINTER(C.c_uint64)]),
     "ebb_field_new": (S, [ctx_t, u32, C.c_char_p, C.c_int, u32, u32, C.c_int, P, C.POINTER(u32)]),

@@ -325,6 +325,7 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
     for (Field& F : c->fields)
         if (F.alive && F.owned && F.ptr) cudaFree(F.ptr);
     if (c->scratch) cudaFree(c->scratch);
+    for (auto& e : c->ev_pool) cudaEventDestroy(e);
     cudaFree(c->d_err);
     cudaFree(c->d_partials);
     cudaFree(c->d_counter);
@@ -352,6 +353,48 @@ ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
     if (!c) return EBB_E_ARG;
     EBB_CUDA(c, cudaStreamSynchronize((cudaStream_t)s));
+    return EBB_OK;
+}
+
+ebb_status ebb_timing_enable(ebb_ctx ctx, int on) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c) return EBB_E_ARG;
+    if (on && c->ev_pool.empty()) {
+        c->ev_pool.resize(16384);
+        for (auto& e : c->ev_pool) EBB_CUDA(c, cudaEventCreate(&e));
+    }
+    c->timing = on != 0;
+    return EBB_OK;
+}
+
+ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64_t* launches, int reset) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !total_ms || !launches) return EBB_E_ARG;
+    double tot = 0.0;
+    uint64_t n = 0;
+    for (auto& t : c->timed) {
+        if (t.kernel != kernel) continue;
+        EBB_CUDA(c, cudaEventSynchronize(t.b));
+        float ms = 0.f;
+        EBB_CUDA(c, cudaEventElapsedTime(&ms, t.a, t.b));
+        tot += ms;
+        ++n;
+    }
+    *total_ms = tot;
+    *launches = n;
+    if (reset) {
+        EBB_CUDA(c, cudaDeviceSynchronize());
+        c->timed.clear();
+        c->ev_used = 0;
+    }
+    return EBB_OK;
+}
+
+ebb_status ebb_launch_count(ebb_ctx ctx, uint64_t* out, int reset) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !out) return EBB_E_ARG;
+    *out = c->launches;
+    if (reset) c->launches = 0;
     return EBB_OK;
 }
 

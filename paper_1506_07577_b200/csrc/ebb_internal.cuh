@@ -52,6 +52,35 @@ struct Ctx : ebb_ctx_s {
     double* d_partials = nullptr;          // per-block reduction partials
     unsigned int* d_counter = nullptr;     // last-block-done tickets
     int num_sms = 148;
+    // instrumentation
+    unsigned long long launches = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct TimedLaunch { int kernel; cudaEvent_t a, b; };
+    std::vector<TimedLaunch> timed;
+};
+
+// Brackets one hot-kernel launch with events on its stream when timing is on.
+struct KernelTimer {
+    Ctx* c;
+    int kernel;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    KernelTimer(Ctx* c_, int k, cudaStream_t s_) : c(c_), kernel(k), s(s_) {
+        c->launches++;
+        if (c->timing && c->ev_used + 2 <= c->ev_pool.size()) {
+            a = c->ev_pool[c->ev_used++];
+            b = c->ev_pool[c->ev_used++];
+            cudaEventRecord(a, s);
+        }
+    }
+    ~KernelTimer() {
+        if (a) {
+            cudaEventRecord(b, s);
+            c->timed.push_back({kernel, a, b});
+        }
+    }
 };
 
 size_t dtype_size(ebb_dtype d);

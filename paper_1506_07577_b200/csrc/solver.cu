@@ -256,6 +256,7 @@ unsigned vec_grid(Ctx* c, uint64_t n) {
 template <typename R, int MODE>
 ebb_status launch_matvec(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask, double* scal,
                          double* pq_out, unsigned int* counter, cudaStream_t s) {
+    KernelTimer kt(c, EBB_K_EDGE_MATVEC, s);
     if (G.max_group <= 16) {
         unsigned grid = vec_grid(c, G.nv * 16);
         k_matvec<R, 16, MODE><<<grid, 256, 0, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials, counter,
@@ -310,8 +311,14 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     unsigned vg = vec_grid(c, ndof);
     for (int k = 0; k < iters; ++k) {
         EBB_TRY((launch_matvec<R, 2>(c, G, A, p, q, mask, scal, nullptr, c->d_counter + 1, s)));
-        k_cg_update<R><<<vg, 256, 0, s>>>(ndof, p, q, dinv, x, r, z, c->d_partials, c->d_counter + 2, scal, rho_user);
-        k_cg_dir<R><<<vg, 256, 0, s>>>(ndof, z, p, scal);
+        {
+            KernelTimer kt(c, EBB_K_CG_UPDATE, s);
+            k_cg_update<R><<<vg, 256, 0, s>>>(ndof, p, q, dinv, x, r, z, c->d_partials, c->d_counter + 2, scal, rho_user);
+        }
+        {
+            KernelTimer kt(c, EBB_K_CG_DIR, s);
+            k_cg_dir<R><<<vg, 256, 0, s>>>(ndof, z, p, scal);
+        }
     }
     EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
@@ -397,6 +404,7 @@ ebb_status ebb_global_reduce(ebb_ctx ctx, int32_t op, ebb_field a, ebb_field b, 
     int soa = Af->layout == EBB_SOA;
     double* o = (double*)O->ptr;
     unsigned int* cnt = c->d_counter + 4;
+    c->launches++;
 #define EBB_RED(R)                                                                                                    \
     do {                                                                                                              \
         const R* pa = (const R*)Af->ptr;                                                                              \
@@ -453,6 +461,8 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
     do {                                                                                                            \
         EBB_TRY((launch_matvec<R, 0>(c, G, (const R*)K->ptr, (const R*)V->ptr, (R*)kv, nullptr, nullptr, nullptr,     \
                                      c->d_counter + 5, s)));                                                        \
+        KernelTimer kt(c, EBB_K_ASSEMBLE, s);                                                                       \
+        c->launches++;                                                                                              \
         k_assemble_b<R><<<grid_for(3 * G.nv, 256), 256, 0, s>>>(G.nv, (const R*)F->ptr, (const R*)M->ptr,             \
                                                                 (const R*)V->ptr, (const R*)kv, (R*)B->ptr, (R)d->h,  \
                                                                 (R)d->alpha, (R)d->beta, (R)d->g[0], (R)d->g[1],      \
@@ -516,6 +526,7 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     double* rho = (double*)c->fields[cg->rho].ptr;
 #define EBB_INIT(R)                                                                                                 \
     do {                                                                                                            \
+        c->launches += 2;                                                                                           \
         k_dinv<R><<<grid_for(G.nv, 256), 256, 0, s>>>(G.nv, self, (const R*)c->fields[cg->A].ptr, G.ne, mask,         \
                                                       (R*)c->fields[cg->dinv].ptr);                                  \
         k_cg_init<R><<<vg, 256, 0, s>>>(ndof, (const R*)c->fields[cg->b].ptr, mask, (const R*)c->fields[cg->dinv].ptr, \
@@ -561,6 +572,7 @@ ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stre
     uint64_t nv = c->rels[verts].size;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned g = grid_for(3 * nv, 256);
+    c->launches++;
     if (dt == EBB_F64)
         k_explicit<double><<<g, 256, 0, s>>>(nv, (const double*)c->fields[d->f].ptr, (const double*)M->ptr, mask,
                                              (double*)U->ptr, (double*)c->fields[d->vel].ptr, d->h, d->g[0], d->g[1], d->g[2]);
@@ -583,6 +595,7 @@ ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u,
     EBB_TRY(check_vec(c, get_field(c, dv), U->rel, dt, "dv"));
     uint64_t ndof = 3 * c->rels[U->rel].size;
     cudaStream_t s = (cudaStream_t)stream;
+    c->launches++;
     if (dt == EBB_F64)
         k_implicit_update<double><<<grid_for(ndof, 256), 256, 0, s>>>(ndof, (const double*)c->fields[dv].ptr, h,
                                                                       (double*)U->ptr, (double*)c->fields[vel].ptr);

@@ -237,6 +237,7 @@ ebb_status launch_map(Ctx* c, bool want_k, bool want_e, uint64_t nt, const Field
     unsigned grid = grid_for(nt, block);
     unsigned cap = (unsigned)c->num_sms * 8;
     if (grid > cap) grid = cap;
+    KernelTimer kt(c, EBB_K_TET_MAP, s);
 #define EBB_ARGS                                                                                               \
     nt, (const uint4*)V->ptr, Ef ? (const uint4*)Ef->ptr : nullptr, (const R*)U->ptr, (const R*)D->ptr,         \
         (const R*)W->ptr, (const R*)MU->ptr, (const R*)LA->ptr, (R*)Fo->ptr, Ko ? (R*)Ko->ptr : nullptr, ne,      \

@@ -67,6 +67,20 @@ class Context:
         self.check(self.L.ebb_error_counts(self.h, out, int(reset)))
         return dict(inverted=out[0], not_spd=out[1], bounds=out[2])
 
+    def timing(self, on=True):
+        self.check(self.L.ebb_timing_enable(self.h, int(on)))
+
+    def timing_read(self, kernel, reset=False):
+        ms = C.c_double()
+        n = C.c_uint64()
+        self.check(self.L.ebb_timing_read(self.h, int(kernel), C.byref(ms), C.byref(n), int(reset)))
+        return ms.value, n.value
+
+    def launch_count(self, reset=False):
+        n = C.c_uint64()
+        self.check(self.L.ebb_launch_count(self.h, C.byref(n), int(reset)))
+        return n.value
+
     # -- relations / globals
     def relation(self, name: str, size: int) -> "Relation":
         h = C.c_uint32()

@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the Ebb tet-FEM hot path on B200 (one JSON line).
+
+Workload (BASELINE.json configs[1], the config its metric is quoted on that
+fits one GPU): neo-Hookean implicit backward-Euler step with 50 Jacobi-PCG
+iterations on the 1M-tet subdivided cube (Kuhn-6, n=55: 998,250 tets), fp64.
+A "step" is one pass of the whole hot path: element
+force+stiffness map, system assembly, PCG init + 50 iterations, state update.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+value = tets advanced through one full step per second (tet-steps/s), summed
+over ranks; components report the map in tets/s and the CG in iterations/s.
+--impl reference times the CPU oracle (the reference arm of this tier) on a
+bounded sample of the same workload.  Under torchrun each rank runs its own C2
+instance (weak scaling, no data-path collective yet).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tets/sec (force+stiffness map) and CG iters/sec at 1/2/4/8 B200; % HBM roofline"
+WORKLOAD = dict(name="C2", n=55, model="nh", E=2e5, nu=0.3, rho=1e3, h=1e-2, cg_iters=50, order_seed=2, u_seed=1)
+SAMPLE_N = 40          # oracle sample: same recipe on a 40^3-cube Kuhn mesh (384,000 tets)
+FLUSH_BYTES = 256 << 20
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def _ncu_traffic(kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d[kernel]
+        if e.get("workload") == WORKLOAD["name"]:
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons during the timed region (NVML)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device):
+        self.device = device
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.hdl = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.hdl, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.hdl, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.hdl)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_case(n, order_seed, u_seed, E, nu):
+    from synth import mesh as M
+    from synth import state as S
+    X, tets = M.kuhn6(n)
+    if order_seed is not None:
+        X, tets = M.permute_vertices(X, tets, order_seed)
+    free = S.fixed_mask(X, n)
+    u = S.stretch_noise_u(X, n, u_seed, free=free)
+    mu, lam = S.materials(tets.shape[0], E, nu)
+    return X, tets, free, u, mu, lam
+
+
+def bytes_map(T, V, E, bf=8):
+    """compulsory bytes of the force+stiffness map."""
+    return T * (4 + 16) * 4 + T * 12 * bf + V * 6 * bf + E * 9 * bf
+
+
+def bytes_matvec(V, E, bf=8):
+    return E * (9 * bf + 4) + V * (4 + 6 * bf)
+
+
+def bytes_cg_iter(V, E, bf=8):
+    return bytes_matvec(V, E, bf) + V * 3 * bf * 11
+
+
+def cpu_baseline(steps=1):
+    """The oracle, as it stands, on a bounded sample of the workload (1 thread)."""
+    import numpy as np
+
+    import oracle
+    w = WORKLOAD
+    X, tets, free, u, mu, lam = make_case(SAMPLE_N, w["order_seed"], w["u_seed"], w["E"], w["nu"])
+    m = oracle.Mesh(X, tets, rho=w["rho"])
+    v = np.zeros_like(u)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = oracle.implicit_step(m, w["model"], u, v, mu, lam, free, w["h"], iters=w["cg_iters"])
+        u, v = out["u"], out["v"]
+    dt = time.perf_counter() - t0
+    T = tets.shape[0]
+    return {"value": T * steps / dt, "unit": "tets/s", "cores": 1, "kind": "oracle",
+            "sample": f"{steps} full implicit NH step(s) (map + assembly + 50 PCG iterations) on the C2 recipe at "
+                      f"Kuhn-6 n={SAMPLE_N} ({T} tets) instead of n=55; single-threaded C oracle "
+                      f"(gcc -O2, generic 4th-order stiffness tensor)",
+            "seconds": dt}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    # warm-up: one untimed sample step (if W > 0), then K timed sample steps
+    import numpy as np
+
+    import oracle
+    w = WORKLOAD
+    X, tets, free, u, mu, lam = make_case(SAMPLE_N, w["order_seed"], w["u_seed"], w["E"], w["nu"])
+    m = oracle.Mesh(X, tets, rho=w["rho"])
+    v = np.zeros_like(u)
+    for _ in range(min(args.warmup, 1)):
+        oracle.implicit_step(m, w["model"], u, v, mu, lam, free, w["h"], iters=w["cg_iters"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = oracle.implicit_step(m, w["model"], u, v, mu, lam, free, w["h"], iters=w["cg_iters"])
+        u, v = out["u"], out["v"]
+    dt = time.perf_counter() - t0
+    T = tets.shape[0]
+    val = T * args.steps / dt
+    cb = {"value": val, "unit": "tets/s", "cores": 1, "kind": "oracle",
+          "sample": f"each step = one implicit NH step (map + assembly + 50 PCG its) of the C2 recipe on Kuhn-6 "
+                    f"n={SAMPLE_N} ({T} tets) instead of n=55; single-threaded C oracle"}
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tets/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(world, sample=True),
+            "cpu_baseline": cb, "e2e": {"value": val, "unit": "tets/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def _config(world, sample=False):
+    from synth import mesh as M
+    n = SAMPLE_N if sample else WORKLOAD["n"]
+    T, V, U, E = M.kuhn_counts(n)
+    return {"workload": f"C2: neo-Hookean implicit backward-Euler step + 50 Jacobi-PCG iterations, Kuhn-6 "
+                        f"subdivided cube n={n} ({T} tets, {V} verts, {E} edge rows), fp64"
+                        + (" [oracle sample of the n=55 workload]" if sample else ""),
+            "tets": T, "verts": V, "edge_rows": E, "h": WORKLOAD["h"], "cg_iters": WORKLOAD["cg_iters"],
+            "E_young": WORKLOAD["E"], "nu": WORKLOAD["nu"],
+            "l2": "flushed between timed steps (256 MiB write); per-step working set ~0.5 GB > 126 MB L2",
+            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (weak)"}
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import build as B
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.tetfem import TetFEM
+
+    B.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = WORKLOAD
+    X, tets, free, u0, mu, lam = make_case(w["n"], w["order_seed"], w["u_seed"], w["E"], w["nu"])
+    ctx = ebb.Context(local_rank)
+    fem = TetFEM(ctx, X, tets, dtype="f64", mu=mu, lam=lam, rho=w["rho"], free=free, u=u0, name="bench")
+    T, V, E = fem.nt, fem.nv, fem.ne
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"], stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.error_counts(reset=True)
+    ctx.timing(True)
+    ctx.timing_read(0, reset=True)
+    ctx.launch_count(reset=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()                          # L2 flush, outside the timed events
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launch_count(reset=True)
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    kt = {}
+    for name, kid in (("tet_map", A.K_TET_MAP), ("edge_matvec", A.K_EDGE_MATVEC), ("cg_update", A.K_CG_UPDATE),
+                      ("cg_dir", A.K_CG_DIR), ("assemble", A.K_ASSEMBLE)):
+        ms, n = ctx.timing_read(kid)
+        kt[name] = {"total_ms": ms, "launches": n, "avg_us": 1e3 * ms / max(n, 1)}
+    ctx.timing_read(0, reset=True)
+    ctx.timing(False)
+    errs = ctx.error_counts(reset=True)
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = world * T * args.steps / (t_ms / 1e3)
+
+    # ---- end to end through the public API: host state in, step, host state out
+    u_h = torch.empty((V, 3), dtype=torch.float64, pin_memory=True)
+    v_h = torch.empty((V, 3), dtype=torch.float64, pin_memory=True)
+    u_h.copy_(torch.from_numpy(fem.u.read()))
+    v_h.copy_(torch.from_numpy(fem.vel.read()))
+    nb = V * 3 * 8
+    e2e_ms = 0.0
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fem.u.write_async(u_h.data_ptr(), nb, stream)
+        fem.vel.write_async(v_h.data_ptr(), nb, stream)
+        step()
+        fem.u.read_into(u_h.data_ptr(), nb, stream)      # synchronous
+        fem.vel.read_into(v_h.data_ptr(), nb, stream)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e = {"value": world * T * args.steps / (e2e_ms / 1e3), "unit": "tets/s",
+           "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
+           "api": "TetFEM.implicit_step + ebb_field_write/ebb_field_read (pinned host buffers)"}
+
+    # ---- roofline of the dominant kernel (largest share of the timed step)
+    peak, peak_src = _peaks()
+    mv, mp = kt["edge_matvec"], kt["tet_map"]
+    b_mv, b_map, b_it = bytes_matvec(V, E), bytes_map(T, V, E), bytes_cg_iter(V, E)
+    shares = {k: v["total_ms"] / t_ms for k, v in kt.items()}
+    dom = max(shares, key=shares.get)
+    per_launch_bytes = {"edge_matvec": b_mv, "tet_map": b_map}.get(dom, None)
+    if per_launch_bytes is None:
+        dom, per_launch_bytes = "edge_matvec", b_mv
+    d = kt[dom]
+    ach = per_launch_bytes / (d["avg_us"] * 1e-6) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": peak_src, "traffic": _ncu_traffic(dom), "algorithmic_bytes_per_launch": per_launch_bytes,
+            "avg_launch_us": d["avg_us"], "share_of_step": shares[dom]}
+    cg_it_us = mv["avg_us"] + kt["cg_update"]["avg_us"] + kt["cg_dir"]["avg_us"]
+    comps = {
+        "map": {"tets_per_s": T / (mp["avg_us"] * 1e-6), "avg_us": mp["avg_us"],
+                "hbm_frac": b_map / (mp["avg_us"] * 1e-6) / 1e9 / peak, "bytes": b_map},
+        "cg": {"iters_per_s": 1e6 / cg_it_us, "iter_us": cg_it_us,
+               "hbm_frac": b_it / (cg_it_us * 1e-6) / 1e9 / peak, "bytes_per_iter": b_it},
+        "matvec": {"avg_us": mv["avg_us"], "hbm_frac": b_mv / (mv["avg_us"] * 1e-6) / 1e9 / peak},
+        "kernel_times": kt, "shares": shares,
+    }
+    line = {"metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Kuhn-6 cube, stretch+noise displacement, no external meshes)",
+            "config": _config(world), "roofline": roof, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "components": comps, "device_errors": errs}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

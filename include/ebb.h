@@ -253,19 +253,41 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
 
 typedef struct {
     ebb_rel edges;
-    ebb_field A, b, x;   /* system (read), rhs (read), solution (write)       */
+    ebb_field A, b, x;   /* system (read, library-allocated), rhs, solution   */
     ebb_field self;      /* verts -> edges self-loop key (Jacobi diagonal)    */
     ebb_field mask;      /* verts U8, 1 = free, or EBB_NONE (a12)  */
-    /* work fields; EBB_NONE = allocated by ebb_cg_init and written back      */
+    /* work fields: EBB_NONE = allocated by ebb_cg_init and written back; a
+     * supplied work field must be an AOS 4x1 field on verts (vec3 padded to
+     * one 32-byte / 16-byte record so that a vertex is a single access)     */
     ebb_field r, p, z, q, dinv;
     ebb_field rho;       /* F64 global r.z (allocated if NONE)                */
-    ebb_field scal;      /* internal device scalars rho, alpha, beta, p.q     */
+    ebb_field scal;      /* internal device scalars rho, p.q, r.z             */
+    ebb_field p2;        /* second direction buffer (p is double-buffered)    */
 } ebb_cg;
-/* a11: x = 0, r = b*mask, z = r/diag(A), p = z, rho = r.z.  Stream-ordered. */
+/* a11: x = 0, r = b*mask, z = r/diag(A), p = z, rho = r.z.  Stream-ordered.
+ * Per iteration (ebb_cg_step): beta = rho'/rho, p = z + beta p fused into
+ * q = (A p)*mask with the local p.q; then alpha = rho/p.q, x += alpha p,
+ * r -= alpha q, z = r/diag(A), rho' = r.z -- two kernels, no host sync. */
 ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream s);
 /* a10-a12: `iters` Jacobi-PCG iterations (Saad Alg. 9.1), alpha/beta kept
  * on the device (no host sync); p.q <= 0 counts in error word [1]. */
 ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream s);
+/* One phase of an iteration, for callers that interleave communication
+ * (multi-GPU: allreduce the scal slot after MATVEC (p.q, slot 1) and after
+ * UPDATE (r.z, slot 2), and refresh ghost rows of z after UPDATE and after
+ * ebb_cg_init).  ebb_cg_step(n) == n x (DIR, MATVEC, UPDATE); DIR is a no-op
+ * kept for callers -- the direction update is fused into MATVEC. */
+#define EBB_CG_DIR 0
+#define EBB_CG_MATVEC 1
+#define EBB_CG_UPDATE 2
+ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream s);
+
+/* ---- halo support ------------------------------------- */
+/* pack:   buf[k] = f[rows[k]]      unpack: f[rows[k]] = buf[k]
+ * f: AOS field of any dtype; rows: U32 field (row ids of f's relation) on a
+ * list relation; buf: AOS field of f's dtype and shape on the list relation. */
+ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s);
+ebb_status ebb_rows_scatter(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s);
 
 typedef struct {
     ebb_field f, mass, mask;  /* mask: verts U8 (1 = free) or EBB_NONE        */

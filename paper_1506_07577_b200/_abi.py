@@ -25,6 +25,7 @@ AOS, SOA = 0, 1
 STVK, NH = 0, 1
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED = 0, 1, 2
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
+CG_DIR, CG_MATVEC, CG_UPDATE = 0, 1, 2
 K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE = 0, 1, 2, 3, 4
 
 u32 = C.c_uint32
@@ -56,7 +57,7 @@ class ImplicitDesc(C.Structure):
 
 class CG(C.Structure):
     _fields_ = [("edges", u32), ("A", u32), ("b", u32), ("x", u32), ("self", u32), ("mask", u32),
-                ("r", u32), ("p", u32), ("z", u32), ("q", u32), ("dinv", u32), ("rho", u32), ("scal", u32)]
+                ("r", u32), ("p", u32), ("z", u32), ("q", u32), ("dinv", u32), ("rho", u32), ("scal", u32), ("p2", u32)]
 
 
 class ExplicitDesc(C.Structure):
@@ -107,6 +108,9 @@ SIGS = {
     "ebb_explicit_update": (S, [ctx_t, C.POINTER(ExplicitDesc), stream_t]),
     "ebb_implicit_update": (S, [ctx_t, u32, C.c_double, u32, u32, stream_t]),
     "ebb_partition": (S, [ctx_t, u32, C.c_int32, u32, u32]),
+    "ebb_cg_phase": (S, [ctx_t, C.POINTER(CG), C.c_int32, stream_t]),
+    "ebb_rows_gather": (S, [ctx_t, u32, u32, u32, stream_t]),
+    "ebb_rows_scatter": (S, [ctx_t, u32, u32, u32, stream_t]),
 }
 
 _lib = None

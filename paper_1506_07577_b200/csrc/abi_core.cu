@@ -190,6 +190,22 @@ __global__ void k_remap_keys(uint32_t* keys, uint64_t n, const uint32_t* __restr
     if (i < n) keys[i] = old_to_new[keys[i]];
 }
 
+// halo pack / unpack: element = `words` 32-bit words
+__global__ void k_rows_gather(const uint32_t* __restrict__ f, const uint32_t* __restrict__ rows, uint32_t* __restrict__ buf,
+                              uint64_t n, uint32_t words) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * words) return;
+    uint64_t k = i / words, w = i % words;
+    buf[i] = f[(uint64_t)rows[k] * words + w];
+}
+__global__ void k_rows_scatter(uint32_t* __restrict__ f, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ buf,
+                               uint64_t n, uint32_t words) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * words) return;
+    uint64_t k = i / words, w = i % words;
+    f[(uint64_t)rows[k] * words + w] = buf[i];
+}
+
 __global__ void k_iota(uint32_t* p, uint64_t n) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i < n) p[i] = (uint32_t)i;
@@ -229,8 +245,9 @@ ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_
     size_t bytes = (size_t)R->size * rows * cols * dtype_size(dt);
     void* p = nullptr;
     if (bytes) {
-        EBB_CUDA(c, cudaMalloc(&p, bytes));
-        EBB_CUDA(c, cudaMemset(p, 0, bytes));
+        // +64 B tail slack: bulk async copies round segment ends up to 16 B
+        EBB_CUDA(c, cudaMalloc(&p, bytes + kFieldSlack));
+        EBB_CUDA(c, cudaMemset(p, 0, bytes + kFieldSlack));
     }
     ebb_status st = add_field(c, rel, name.c_str(), dt, rows, cols, layout, p, true, out);
     if (st != EBB_OK && p) cudaFree(p);
@@ -244,13 +261,16 @@ ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, c
                             cudaStream_t s) {
     Relation* R = get_rel(c, rel);
     uint64_t n = R->size;
+    for (auto& P : c->plans) P.release();
+    c->plans.clear();
     for (ebb_field fh : R->fields) {
         Field& F = c->fields[fh];
         if (!F.alive) continue;
         size_t es = dtype_size(F.dtype);
         uint64_t tot = n * F.comps();
         void* np = nullptr;
-        EBB_CUDA(c, cudaMalloc(&np, tot * es ? tot * es : 1));
+        EBB_CUDA(c, cudaMalloc(&np, tot * es + kFieldSlack));
+        EBB_CUDA(c, cudaMemset(np, 0, tot * es + kFieldSlack));
         unsigned g = grid_for(tot, 256);
         int soa = F.layout == EBB_SOA;
         if (es == 8)
@@ -326,6 +346,7 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
         if (F.alive && F.owned && F.ptr) cudaFree(F.ptr);
     if (c->scratch) cudaFree(c->scratch);
     for (auto& e : c->ev_pool) cudaEventDestroy(e);
+    for (auto& P : c->plans) P.release();
     cudaFree(c->d_err);
     cudaFree(c->d_partials);
     cudaFree(c->d_counter);
@@ -704,6 +725,49 @@ ebb_status ebb_group_by(ebb_ctx ctx, ebb_rel rel, ebb_field key) {
     R->max_group = hmx;
     Sr->index = idx;
     Sr->max_group = hmx;
+    return EBB_OK;
+}
+
+static ebb_status rows_common(Ctx* c, ebb_field f, ebb_field rows, ebb_field buf, Field** F, Field** Rw, Field** B,
+                              uint64_t* n, uint32_t* words) {
+    *F = get_field(c, f);
+    *Rw = get_field(c, rows);
+    *B = get_field(c, buf);
+    if (!*F || !*Rw || !*B) return fail(c, EBB_E_ARG, "rows_gather/scatter: bad handle");
+    if ((*F)->layout != EBB_AOS && (*F)->comps() > 1) return fail(c, EBB_E_TYPE, "halo fields must be AOS");
+    if ((*Rw)->dtype != EBB_U32 || (*Rw)->comps() != 1) return fail(c, EBB_E_TYPE, "rows must be a U32 scalar field");
+    if ((*B)->dtype != (*F)->dtype || (*B)->comps() != (*F)->comps() || (*B)->rel != (*Rw)->rel)
+        return fail(c, EBB_E_TYPE, "buf must match f's dtype/shape on the rows' relation");
+    size_t eb = (*F)->comps() * dtype_size((*F)->dtype);
+    if (eb % 4) return fail(c, EBB_E_TYPE, "halo element size must be a multiple of 4 bytes");
+    *words = (uint32_t)(eb / 4);
+    *n = c->rels[(*Rw)->rel].size;
+    return EBB_OK;
+}
+
+ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field *F, *Rw, *B;
+    uint64_t n;
+    uint32_t w;
+    EBB_TRY(rows_common(c, f, rows, buf, &F, &Rw, &B, &n, &w));
+    c->launches++;
+    k_rows_gather<<<grid_for(n * w, 256), 256, 0, (cudaStream_t)s>>>((const uint32_t*)F->ptr, (const uint32_t*)Rw->ptr,
+                                                                     (uint32_t*)B->ptr, n, w);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+ebb_status ebb_rows_scatter(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    Field *F, *Rw, *B;
+    uint64_t n;
+    uint32_t w;
+    EBB_TRY(rows_common(c, f, rows, buf, &F, &Rw, &B, &n, &w));
+    c->launches++;
+    k_rows_scatter<<<grid_for(n * w, 256), 256, 0, (cudaStream_t)s>>>((uint32_t*)F->ptr, (const uint32_t*)Rw->ptr,
+                                                                      (const uint32_t*)B->ptr, n, w);
+    EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
 }
 

@@ -16,6 +16,8 @@ struct ebb_ctx_s {};
 
 namespace ebb {
 
+constexpr size_t kFieldSlack = 64;  // bytes past the end of every library-owned column
+
 struct Field {
     std::string name;
     ebb_rel rel = EBB_NONE;
@@ -39,6 +41,27 @@ struct Relation {
     uint32_t max_group = 0;            // longest range of an index on this relation
 };
 
+// Scatter plan of the tiled element map (built once per mesh, tet_map.cu):
+// vertex tiles of `nvt` consecutive (SFC-ordered) vertices own the canonical
+// edge rows (tail <= head) of their vertices; every tet touching a tile is an
+// "instance" of that tile with a 32-byte record (tet id, local row slot of
+// each of its 10 canonical pairs, local vertex of each owned corner, flags).
+struct MapPlan {
+    ebb_field v = EBB_NONE, e = EBB_NONE;
+    int nvt = 0;
+    uint32_t ntiles = 0, max_slots = 0;
+    uint64_t ninst = 0, ncanon = 0;
+    uint32_t* inst_ptr = nullptr;   // ntiles + 1
+    uint4* recs = nullptr;          // 2 x uint4 per instance
+    uint32_t* tile_cptr = nullptr;  // ntiles + 1, canonical-slot offsets
+    uint32_t* crow = nullptr;       // ncanon: global row of canonical slot
+    uint32_t* ctrow = nullptr;      // ncanon: global row of its transpose
+    void release() {
+        cudaFree(inst_ptr); cudaFree(recs); cudaFree(tile_cptr); cudaFree(crow); cudaFree(ctrow);
+        inst_ptr = nullptr; recs = nullptr; tile_cptr = nullptr; crow = nullptr; ctrow = nullptr;
+    }
+};
+
 struct Ctx : ebb_ctx_s {
     int device = 0;
     std::vector<Relation> rels;
@@ -59,6 +82,7 @@ struct Ctx : ebb_ctx_s {
     size_t ev_used = 0;
     struct TimedLaunch { int kernel; cudaEvent_t a, b; };
     std::vector<TimedLaunch> timed;
+    std::vector<MapPlan> plans;     // invalidated by any relation permutation
 };
 
 // Brackets one hot-kernel launch with events on its stream when timing is on.
@@ -105,6 +129,22 @@ ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, c
         ebb_status _s = (call);        \
         if (_s != EBB_OK) return _s;   \
     } while (0)
+
+// Grid for a grid-stride kernel: exactly the number of CTAs that are resident
+// at once (occupancy API x SM count), never more than the work needs.  A grid
+// larger than one resident wave leaves a partial tail wave.
+template <typename K>
+inline unsigned occ_grid(const Ctx* c, K kernel, int block, size_t smem, uint64_t work_threads) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, block, smem) != cudaSuccess || nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    uint64_t full = (uint64_t)nb * (uint64_t)c->num_sms;
+    uint64_t need = (work_threads + block - 1) / block;
+    if (need == 0) need = 1;
+    return (unsigned)(need < full ? need : full);
+}
 
 inline unsigned grid_for(uint64_t n, unsigned block) {
     uint64_t g = (n + block - 1) / block;

@@ -4,7 +4,20 @@
 // The matvec is the paper's query-loop `for e in v.edges do ... e.head ... end`
 // over the edge relation grouped by tail (CSR) with the
 // 3x3 stiffness stored per edge.  PCG follows Saad Alg. 9.1
-// with the Jacobi preconditioner; alpha and beta stay on the device.
+// with the Jacobi preconditioner; every scalar stays on the device.
+//
+// PCG iteration (one stream, no host synchronisation), two kernels:
+//   spmv (CG)    beta = rz/rho (0 on the first iteration); p = z + beta p_old,
+//                formed on the fly for every gathered head and stored for the
+//                owned vertex (p double-buffered); q = (A p) * mask; local p.q
+//   k_cg_update  alpha = rho / p.q; x += alpha p; r -= alpha q; z = r * dinv; local r.z
+// Between kernels the scalars p.q and r.z are the only cross-CTA (and, on
+// several GPUs, cross-rank) reductions; z is the only vector a halo needs.
+// CG work vectors are padded 4-component records (32 B fp64 / 16 B fp32) so a
+// vertex is one 256-/128-bit access.
+#include <cstdlib>
+
+#include "async_copy.cuh"
 #include "ebb_internal.cuh"
 #include "reduce.cuh"
 
@@ -12,133 +25,388 @@ using namespace ebb;
 
 namespace {
 
-enum { S_RHO = 0, S_ALPHA = 1, S_BETA = 2, S_PQ = 3, S_NSCAL = 8 };
+enum { S_RHO = 0, S_PQ = 1, S_RZ = 2, S_FIRST = 3, S_PAR = 4, S_NSCAL = 8 };
+
+template <typename R>
+struct V4;
+template <>
+struct V4<double> {
+    using T = double4;
+};
+template <>
+struct V4<float> {
+    using T = float4;
+};
+
+template <typename R>
+__device__ __forceinline__ typename V4<R>::T ld4(const R* p, uint64_t v) {
+    return reinterpret_cast<const typename V4<R>::T*>(p)[v];
+}
+template <typename R>
+__device__ __forceinline__ void st4(R* p, uint64_t v, typename V4<R>::T x) {
+    reinterpret_cast<typename V4<R>::T*>(p)[v] = x;
+}
 
 // ---------------------------------------------------------------------------
-// a10: q_v = sum_{e in row(v)} A_e p_head(e); LPV lanes cooperate on one vertex.
-// MODE 0: plain; 1: q *= mask, fused p.q -> pq_out; 2: CG (mask, p.q, alpha).
-template <typename R, int LPV, int MODE>
-__global__ void __launch_bounds__(256) k_matvec(uint64_t nv, const uint32_t* __restrict__ index,
-                                                const uint32_t* __restrict__ head, const R* __restrict__ A, uint64_t ne,
-                                                const R* __restrict__ p, R* __restrict__ q,
-                                                const uint8_t* __restrict__ mask, double* __restrict__ partials,
-                                                unsigned int* __restrict__ counter, double* __restrict__ scal,
-                                                double* __restrict__ pq_out, unsigned long long* __restrict__ err) {
-    // warp-uniform trip count: the LPV-lane groups of one warp leave together
-    const unsigned lane = threadIdx.x % LPV;
-    const unsigned gpw = 32 / LPV;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+// Edge-relation matvec, register path (used for borrowed, unpadded columns):
+// two phases per CTA chunk of SPMV_VC vertices -- flat coalesced row loads
+// into shared memory, then 4 lanes per vertex sum the vertex's rows.
+#define SPMV_VC 64
+#define SPMV_BATCH 4
+template <typename R, bool MPQ>
+__global__ void __launch_bounds__(256) k_spmv(uint64_t nv, const uint32_t* __restrict__ index,
+                                              const uint32_t* __restrict__ head, const R* __restrict__ A, uint64_t ne,
+                                              const R* __restrict__ p, R* __restrict__ q,
+                                              const uint8_t* __restrict__ mask, double* __restrict__ partials,
+                                              unsigned int* __restrict__ counter, double* __restrict__ pq_out) {
+    extern __shared__ __align__(16) unsigned char spmv_smem[];
+    R* ys = reinterpret_cast<R*>(spmv_smem);
     double pq = 0.0;
-    for (uint64_t vb = warp * gpw; vb < nv; vb += nwarps * gpw) {
-        const uint64_t v = vb + (threadIdx.x & 31) / LPV;
-        const bool valid = v < nv;
-        const uint32_t r0 = valid ? index[v] : 0u, r1 = valid ? index[v + 1] : 0u;
+    const uint64_t nchunks = (nv + SPMV_VC - 1) / SPMV_VC;
+    for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const uint64_t v0 = ch * SPMV_VC;
+        const uint64_t v1 = v0 + SPMV_VC < nv ? v0 + SPMV_VC : nv;
+        const uint32_t e0 = index[v0], nr = index[v1] - e0;
+        for (uint32_t kb = threadIdx.x; kb < nr; kb += SPMV_BATCH * 256) {
+            R a[SPMV_BATCH][9];
+            uint32_t hh[SPMV_BATCH];
+#pragma unroll
+            for (int u = 0; u < SPMV_BATCH; ++u) {
+                const uint32_t k = kb + u * 256;
+                if (k < nr) {
+                    const uint64_t e = e0 + k;
+                    hh[u] = __ldcs(head + e);
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) a[u][c] = __ldcs(A + c * ne + e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < SPMV_BATCH; ++u) {
+                const uint32_t k = kb + u * 256;
+                if (k < nr) {
+                    const uint64_t h = 3ull * hh[u];
+                    const R px = p[h], py = p[h + 1], pz = p[h + 2];
+                    ys[3 * k] = a[u][0] * px + a[u][1] * py + a[u][2] * pz;
+                    ys[3 * k + 1] = a[u][3] * px + a[u][4] * py + a[u][5] * pz;
+                    ys[3 * k + 2] = a[u][6] * px + a[u][7] * py + a[u][8] * pz;
+                }
+            }
+        }
+        __syncthreads();
+        const uint64_t v = v0 + (threadIdx.x >> 2);
+        const unsigned sub = threadIdx.x & 3;
+        const bool valid = v < v1;
         R a0 = 0, a1 = 0, a2 = 0;
-        for (uint32_t e = r0 + lane; e < r1; e += LPV) {
-            const uint32_t h = head[e];
-            const R px = p[3ull * h], py = p[3ull * h + 1], pz = p[3ull * h + 2];
-            a0 += A[e] * px + A[ne + e] * py + A[2 * ne + e] * pz;
-            a1 += A[3 * ne + e] * px + A[4 * ne + e] * py + A[5 * ne + e] * pz;
-            a2 += A[6 * ne + e] * px + A[7 * ne + e] * py + A[8 * ne + e] * pz;
+        if (valid) {
+            const uint32_t r1 = index[v + 1] - e0;
+            for (uint32_t r = index[v] - e0 + sub; r < r1; r += 4) {
+                a0 += ys[3 * r];
+                a1 += ys[3 * r + 1];
+                a2 += ys[3 * r + 2];
+            }
         }
 #pragma unroll
-        for (int o = LPV / 2; o > 0; o >>= 1) {
-            a0 += __shfl_xor_sync(0xffffffffu, a0, o, LPV);
-            a1 += __shfl_xor_sync(0xffffffffu, a1, o, LPV);
-            a2 += __shfl_xor_sync(0xffffffffu, a2, o, LPV);
+        for (int o = 2; o > 0; o >>= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o, 4);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o, 4);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, o, 4);
         }
-        if (lane == 0 && valid) {
-            if (MODE >= 1 && mask && !mask[v]) a0 = a1 = a2 = 0;
+        if (sub == 0 && valid) {
+            if (MPQ && mask && !mask[v]) a0 = a1 = a2 = 0;
             q[3 * v] = a0;
             q[3 * v + 1] = a1;
             q[3 * v + 2] = a2;
-            if (MODE >= 1) pq += (double)p[3 * v] * a0 + (double)p[3 * v + 1] * a1 + (double)p[3 * v + 2] * a2;
+            if (MPQ) pq += (double)p[3 * v] * a0 + (double)p[3 * v + 1] * a1 + (double)p[3 * v + 2] * a2;
+        }
+        __syncthreads();
+    }
+    if (MPQ) {
+        double tot;
+        if (block_sum_last_done(pq, partials, counter, &tot)) *pq_out = tot;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Edge-relation matvec streamed through shared memory by the TMA engine,
+// warp-specialized.  A persistent CTA walks chunks of TMA_VCH consecutive
+// vertices; the rows of a chunk are one contiguous range of the grouped edge
+// relation, so its 9 A planes and its head keys are 10 contiguous segments.
+//   producer warp (warp 8, one lane): for each chunk, waits until the ring
+//     stage is empty, then issues 10 1-D bulk async copies (cp.async.bulk,
+//     L2 evict-first) that complete on the stage's "full" mbarrier;
+//   consumer warps 0..7: each owns 2 vertices of every chunk (16 lanes per
+//     vertex), waits on "full", reads A and head from shared memory, gathers
+//     p through head (L2-resident; one 256-bit load per head in CG mode),
+//     reduces with shuffles, then arrives on the stage's "empty" mbarrier.
+//     No block-wide barrier inside the loop: consumer warps run ahead of each
+//     other by up to TMA_NS chunks.
+// CG = true: p, q are padded vec4 records; MPQ: q *= mask, fused local p.q.
+#define TMA_VCH 16
+#define TMA_NS 4
+#define TMA_CONSUMERS 8
+template <typename R, bool CG, bool MPQ, bool DIR = false>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
+    k_spmv_tma(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
+               const R* __restrict__ A, uint64_t ne, const R* __restrict__ p, R* __restrict__ q,
+               const uint8_t* __restrict__ mask, double* __restrict__ partials, unsigned int* __restrict__ counter,
+               double* __restrict__ pq_out, uint32_t cap, R* pbuf0 = nullptr, R* pbuf1 = nullptr,
+               double* __restrict__ scal = nullptr) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
+    constexpr uint32_t AE = 16 / sizeof(R);   // elements per 16 B
+    const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const uint64_t nchunks = (nv + TMA_VCH - 1) / TMA_VCH;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TMA_NS; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], TMA_CONSUMERS);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    double pq = 0.0;
+    if (warp == TMA_CONSUMERS) {
+        if (lane == 0) {
+            uint32_t k = 0;
+            for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++k) {
+                const int s = k % TMA_NS;
+                const uint64_t v0 = ch * TMA_VCH;
+                const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+                const uint64_t e0 = index[v0], e1 = index[v1];
+                if (k >= TMA_NS) mbar_wait(&empty_bar[s], ((k / TMA_NS) + 1) & 1u);
+                unsigned char* base = tma_smem + s * stage_bytes;
+                uint32_t tot = 0;
+#pragma unroll
+                for (int c = 0; c < 9; ++c) {
+                    const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+                    const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+                    tot += (uint32_t)((a1 - a0) * sizeof(R));
+                }
+                const uint64_t h0 = e0 & ~3ull, h1 = (e1 + 3) & ~3ull;
+                tot += (uint32_t)((h1 - h0) * 4);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&full_bar[s], tot);
+#pragma unroll
+                for (int c = 0; c < 9; ++c) {
+                    const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+                    const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+                    bulk_g2s_evict_first(base + (size_t)c * cap * sizeof(R), A + a0,
+                                         (uint32_t)((a1 - a0) * sizeof(R)), &full_bar[s]);
+                }
+                bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4),
+                                     &full_bar[s]);
+            }
+        }
+    } else {
+        const unsigned sub = lane & 15;
+        // DIR (CG): p = z + beta p_old on the fly -- `p` holds z, p is double-buffered
+        const R* __restrict__ pold = nullptr;
+        R* __restrict__ pnew = nullptr;
+        R beta = 0;
+        if (DIR) {
+            const int cur = scal[S_PAR] != 0.0;
+            pold = cur ? pbuf1 : pbuf0;
+            pnew = cur ? pbuf0 : pbuf1;
+            const double rho = scal[S_RHO], rz = scal[S_RZ];
+            beta = (scal[S_FIRST] != 0.0 || rho == 0.0) ? R(0) : (R)(rz / rho);
+        }
+        uint32_t k = 0;
+        for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++k) {
+            const int s = k % TMA_NS;
+            const uint64_t v0 = ch * TMA_VCH;
+            const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+            const uint64_t v = v0 + 2 * warp + (lane >> 4);
+            const bool valid = v < v1;
+            const uint32_t e0 = index[v0];
+            const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
+            R own0 = 0, own1 = 0, own2 = 0;
+            uint8_t mk = 1;
+            if (MPQ && valid && sub == 0) {
+                if (DIR) {
+                    const auto zv = ld4(p, v);
+                    const auto ov = ld4(pold, v);
+                    own0 = zv.x + beta * ov.x;
+                    own1 = zv.y + beta * ov.y;
+                    own2 = zv.z + beta * ov.z;
+                } else if (CG) {
+                    const auto pv = ld4(p, v);
+                    own0 = pv.x;
+                    own1 = pv.y;
+                    own2 = pv.z;
+                } else {
+                    own0 = p[3 * v];
+                    own1 = p[3 * v + 1];
+                    own2 = p[3 * v + 2];
+                }
+                if (mask) mk = mask[v];
+            }
+            mbar_wait(&full_bar[s], (k / TMA_NS) & 1u);
+            const unsigned char* base = tma_smem + s * stage_bytes;
+            const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
+            R a0 = 0, a1 = 0, a2 = 0;
+            for (uint32_t r = r0 + sub; r < r1; r += 16) {
+                const uint32_t hv = hs[r];
+                R px, py, pz;
+                if (DIR) {
+                    const auto zv = ld4(p, hv);
+                    const auto ov = ld4(pold, hv);
+                    px = zv.x + beta * ov.x;
+                    py = zv.y + beta * ov.y;
+                    pz = zv.z + beta * ov.z;
+                } else if (CG) {
+                    const auto pv = ld4(p, hv);
+                    px = pv.x;
+                    py = pv.y;
+                    pz = pv.z;
+                } else {
+                    px = p[3ull * hv];
+                    py = p[3ull * hv + 1];
+                    pz = p[3ull * hv + 2];
+                }
+                R av[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) {
+                    const uint32_t off = (uint32_t)((c * ne + e0) & (AE - 1));
+                    av[c] = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R))[r + off];
+                }
+                a0 += av[0] * px + av[1] * py + av[2] * pz;
+                a1 += av[3] * px + av[4] * py + av[5] * pz;
+                a2 += av[6] * px + av[7] * py + av[8] * pz;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[s]);
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, o, 16);
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o, 16);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o, 16);
+            }
+            if (sub == 0 && valid) {
+                if (MPQ && !mk) a0 = a1 = a2 = 0;
+                if (CG) {
+                    typename V4<R>::T qv;
+                    qv.x = a0;
+                    qv.y = a1;
+                    qv.z = a2;
+                    qv.w = 0;
+                    st4(q, v, qv);
+                    if (DIR) {
+                        typename V4<R>::T pv;
+                        pv.x = own0;
+                        pv.y = own1;
+                        pv.z = own2;
+                        pv.w = 0;
+                        st4(pnew, v, pv);
+                    }
+                } else {
+                    q[3 * v] = a0;
+                    q[3 * v + 1] = a1;
+                    q[3 * v + 2] = a2;
+                }
+                if (MPQ) pq += (double)own0 * a0 + (double)own1 * a1 + (double)own2 * a2;
+            }
         }
     }
-    if (MODE >= 1) {
+    if (MPQ) {
         double tot;
         if (block_sum_last_done(pq, partials, counter, &tot)) {
-            if (MODE == 1) {
-                *pq_out = tot;
-            } else {
-                scal[S_PQ] = tot;
-                if (tot < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
-                scal[S_ALPHA] = (tot != 0.0) ? scal[S_RHO] / tot : 0.0;
+            *pq_out = tot;
+            if (DIR) {   // every block has read rho/rz/parity: retire them
+                scal[S_RHO] = scal[S_RZ];
+                scal[S_FIRST] = 0.0;
+                scal[S_PAR] = scal[S_PAR] != 0.0 ? 0.0 : 1.0;
             }
         }
     }
 }
 
-// CG init: x = 0, r = b*m, z = r*dinv, p = z, rho = r.z
+// ---------------------------------------------------------------------------
+// PCG kernels on padded vec4 work vectors (one thread per vertex)
+// init: dinv = 1/diag(A) on free DOFs (Jacobi), x = 0, r = b*m,
+//       z = r*dinv, p = z, local r.z -> scal[S_RZ]; scal[S_FIRST] = 1
 template <typename R>
-__global__ void k_cg_init(uint64_t ndof, const R* __restrict__ b, const uint8_t* __restrict__ mask,
-                          const R* __restrict__ dinv, R* __restrict__ x, R* __restrict__ r, R* __restrict__ z,
-                          R* __restrict__ p, double* __restrict__ partials, unsigned int* __restrict__ counter,
-                          double* __restrict__ scal, double* __restrict__ rho_user) {
+__global__ void __launch_bounds__(256) k_cg_init(uint64_t nv, const uint32_t* __restrict__ self,
+                                                 const R* __restrict__ A, uint64_t ne, const R* __restrict__ b,
+                                                 const uint8_t* __restrict__ mask, R* __restrict__ dinv,
+                                                 R* __restrict__ x, R* __restrict__ r, R* __restrict__ z,
+                                                 R* __restrict__ p, double* __restrict__ partials,
+                                                 unsigned int* __restrict__ counter, double* __restrict__ scal,
+                                                 double* __restrict__ rho_user) {
     double acc = 0.0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ndof; i += (uint64_t)gridDim.x * blockDim.x) {
-        R m = (mask && !mask[i / 3]) ? R(0) : R(1);
-        R ri = b[i] * m;
-        R zi = ri * dinv[i];
-        x[i] = 0;
-        r[i] = ri;
-        z[i] = zi;
-        p[i] = zi;
-        acc += (double)ri * zi;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+        const bool fr = !mask || mask[v];
+        const uint32_t e = self[v];
+        typename V4<R>::T dv, rv, zv;
+        dv.x = fr ? R(1) / A[e] : R(0);
+        dv.y = fr ? R(1) / A[4 * ne + e] : R(0);
+        dv.z = fr ? R(1) / A[8 * ne + e] : R(0);
+        dv.w = 0;
+        rv.x = fr ? b[3 * v] : R(0);
+        rv.y = fr ? b[3 * v + 1] : R(0);
+        rv.z = fr ? b[3 * v + 2] : R(0);
+        rv.w = 0;
+        zv.x = rv.x * dv.x;
+        zv.y = rv.y * dv.y;
+        zv.z = rv.z * dv.z;
+        zv.w = 0;
+        st4(dinv, v, dv);
+        st4(r, v, rv);
+        st4(z, v, zv);
+        st4(p, v, zv);
+        x[3 * v] = 0;
+        x[3 * v + 1] = 0;
+        x[3 * v + 2] = 0;
+        acc += (double)rv.x * zv.x + (double)rv.y * zv.y + (double)rv.z * zv.z;
     }
     double tot;
     if (block_sum_last_done(acc, partials, counter, &tot)) {
+        scal[S_RZ] = tot;
         scal[S_RHO] = tot;
-        scal[S_ALPHA] = 0.0;
-        scal[S_BETA] = 0.0;
+        scal[S_PQ] = 0.0;
+        scal[S_FIRST] = 1.0;
+        scal[S_PAR] = 0.0;
         if (rho_user) *rho_user = tot;
     }
 }
 
-// dinv = 1/diag(A) on free DOFs (Jacobi), 0 on fixed DOFs
+// alpha = rho / p.q; x += alpha p; r -= alpha q; z = r*dinv; local r.z -> scal[S_RZ]
 template <typename R>
-__global__ void k_dinv(uint64_t nv, const uint32_t* __restrict__ self, const R* __restrict__ A, uint64_t ne,
-                       const uint8_t* __restrict__ mask, R* __restrict__ dinv) {
-    uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (v >= nv) return;
-    uint32_t e = self[v];
-    bool fr = !mask || mask[v];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) dinv[3 * v + a] = fr ? R(1) / A[(uint64_t)(4 * a) * ne + e] : R(0);
-}
-
-// x += alpha p; r -= alpha q; z = r*dinv; rho' = r.z -> beta = rho'/rho
-template <typename R>
-__global__ void k_cg_update(uint64_t ndof, const R* __restrict__ p, const R* __restrict__ q, const R* __restrict__ dinv,
-                            R* __restrict__ x, R* __restrict__ r, R* __restrict__ z, double* __restrict__ partials,
-                            unsigned int* __restrict__ counter, double* __restrict__ scal, double* __restrict__ rho_user) {
-    const R alpha = (R)scal[S_ALPHA];
+__global__ void __launch_bounds__(256) k_cg_update(uint64_t nv, const R* pbuf0, const R* pbuf1, const R* __restrict__ q,
+                                                   const R* __restrict__ dinv, R* __restrict__ x, R* __restrict__ r,
+                                                   R* __restrict__ z, double* __restrict__ partials,
+                                                   unsigned int* __restrict__ counter, double* __restrict__ scal,
+                                                   double* __restrict__ rho_user, unsigned long long* __restrict__ err) {
+    const double pqs = scal[S_PQ];
+    const R alpha = (pqs != 0.0) ? (R)(scal[S_RHO] / pqs) : R(0);
+    const R* __restrict__ p = scal[S_PAR] != 0.0 ? pbuf1 : pbuf0;   // the current direction
     double acc = 0.0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ndof; i += (uint64_t)gridDim.x * blockDim.x) {
-        R pi = p[i];
-        R ri = r[i] - alpha * q[i];
-        R zi = ri * dinv[i];
-        x[i] += alpha * pi;
-        r[i] = ri;
-        z[i] = zi;
-        acc += (double)ri * zi;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+        const auto pv = ld4(p, v);
+        const auto qv = ld4(q, v);
+        const auto dv = ld4(dinv, v);
+        auto rv = ld4(r, v);
+        rv.x -= alpha * qv.x;
+        rv.y -= alpha * qv.y;
+        rv.z -= alpha * qv.z;
+        typename V4<R>::T zv;
+        zv.x = rv.x * dv.x;
+        zv.y = rv.y * dv.y;
+        zv.z = rv.z * dv.z;
+        zv.w = 0;
+        st4(r, v, rv);
+        st4(z, v, zv);
+        x[3 * v] += alpha * pv.x;
+        x[3 * v + 1] += alpha * pv.y;
+        x[3 * v + 2] += alpha * pv.z;
+        acc += (double)rv.x * zv.x + (double)rv.y * zv.y + (double)rv.z * zv.z;
     }
     double tot;
     if (block_sum_last_done(acc, partials, counter, &tot)) {
-        double rho = scal[S_RHO];
-        scal[S_BETA] = (rho != 0.0) ? tot / rho : 0.0;
-        scal[S_RHO] = tot;
+        if (pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+        scal[S_RZ] = tot;
         if (rho_user) *rho_user = tot;
     }
-}
-
-// p = z + beta p
-template <typename R>
-__global__ void k_cg_dir(uint64_t ndof, const R* __restrict__ z, R* __restrict__ p, const double* __restrict__ scal) {
-    const R beta = (R)scal[S_BETA];
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ndof; i += (uint64_t)gridDim.x * blockDim.x)
-        p[i] = z[i] + beta * p[i];
 }
 
 // a9: A = M + h (alpha M + beta K) + h^2 K on every row of vertex v (in place ok)
@@ -247,25 +515,44 @@ ebb_status edge_graph(Ctx* c, ebb_rel edges, EdgeGraph* g) {
     return EBB_OK;
 }
 
-unsigned vec_grid(Ctx* c, uint64_t n) {
-    unsigned g = grid_for(n, 256);
-    unsigned cap = (unsigned)c->num_sms * 8;
-    return g < cap ? g : cap;
+template <typename R, bool CG, bool MPQ, bool DIR = false>
+ebb_status launch_tma(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask, double* pq_out,
+                      unsigned int* counter, cudaStream_t s, R* pb0 = nullptr, R* pb1 = nullptr,
+                      double* scal = nullptr) {
+    const uint32_t cap = (uint32_t)(TMA_VCH * (G.max_group ? G.max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+    const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const size_t smem = stage * TMA_NS;
+    if (smem > 200 * 1024) return EBB_E_SIZE;   // caller falls back to the register path
+    static thread_local size_t configured = 0;
+    if (smem > configured) {
+        EBB_CUDA(c, cudaFuncSetAttribute(k_spmv_tma<R, CG, MPQ, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        configured = smem;
+    }
+    const int block = 32 * (TMA_CONSUMERS + 1);
+    const uint64_t nch = (G.nv + TMA_VCH - 1) / TMA_VCH;
+    const unsigned grid = occ_grid(c, k_spmv_tma<R, CG, MPQ, DIR>, block, smem, nch * block);
+    k_spmv_tma<R, CG, MPQ, DIR><<<grid, block, smem, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials,
+                                                          counter, pq_out, cap, pb0, pb1, scal);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
 }
 
-template <typename R, int MODE>
-ebb_status launch_matvec(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask, double* scal,
-                         double* pq_out, unsigned int* counter, cudaStream_t s) {
+// matvec on AOS vec3 p, q (the ebb_map_edge_matvec ABI and the K v of assembly)
+template <typename R, bool MPQ>
+ebb_status launch_spmv3(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask, double* pq_out,
+                        unsigned int* counter, cudaStream_t s, bool padded) {
     KernelTimer kt(c, EBB_K_EDGE_MATVEC, s);
-    if (G.max_group <= 16) {
-        unsigned grid = vec_grid(c, G.nv * 16);
-        k_matvec<R, 16, MODE><<<grid, 256, 0, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials, counter,
-                                                   scal, pq_out, c->d_err);
-    } else {
-        unsigned grid = vec_grid(c, G.nv * 32);
-        k_matvec<R, 32, MODE><<<grid, 256, 0, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials, counter,
-                                                   scal, pq_out, c->d_err);
+    const char* env = getenv("EBB_SPMV");
+    if (padded && !(env && env[0] == 'p')) {
+        ebb_status st = launch_tma<R, false, MPQ>(c, G, A, p, q, mask, pq_out, counter, s);
+        if (st != EBB_E_SIZE) return st;
     }
+    const size_t smem = (size_t)SPMV_VC * (G.max_group ? G.max_group : 1) * 3 * sizeof(R);
+    if (smem > 48 * 1024)
+        EBB_CUDA(c, cudaFuncSetAttribute(k_spmv<R, MPQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = occ_grid(c, k_spmv<R, MPQ>, 256, smem, ((G.nv + SPMV_VC - 1) / SPMV_VC) * 256);
+    k_spmv<R, MPQ><<<grid, 256, smem, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials, counter, pq_out);
     EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
 }
@@ -294,12 +581,14 @@ ebb_status check_mask(Ctx* c, ebb_field m, ebb_rel rel, const uint8_t** out) {
     return EBB_OK;
 }
 
+
 template <typename R>
-ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s) {
+ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s, int only_phase = -1) {
     const R* A = (const R*)c->fields[cg->A].ptr;
     R* x = (R*)c->fields[cg->x].ptr;
     R* r = (R*)c->fields[cg->r].ptr;
     R* p = (R*)c->fields[cg->p].ptr;
+    R* p2 = (R*)c->fields[cg->p2].ptr;
     R* z = (R*)c->fields[cg->z].ptr;
     R* q = (R*)c->fields[cg->q].ptr;
     const R* dinv = (const R*)c->fields[cg->dinv].ptr;
@@ -307,17 +596,18 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     EBB_TRY(check_mask(c, cg->mask, G.verts, &mask));
     double* scal = (double*)c->fields[cg->scal].ptr;
     double* rho_user = (double*)c->fields[cg->rho].ptr;
-    uint64_t ndof = 3 * G.nv;
-    unsigned vg = vec_grid(c, ndof);
+    const unsigned ug = occ_grid(c, k_cg_update<R>, 256, 0, G.nv);
     for (int k = 0; k < iters; ++k) {
-        EBB_TRY((launch_matvec<R, 2>(c, G, A, p, q, mask, scal, nullptr, c->d_counter + 1, s)));
-        {
-            KernelTimer kt(c, EBB_K_CG_UPDATE, s);
-            k_cg_update<R><<<vg, 256, 0, s>>>(ndof, p, q, dinv, x, r, z, c->d_partials, c->d_counter + 2, scal, rho_user);
+        // EBB_CG_DIR is fused into the matvec (p = z + beta p_old gathered on the fly)
+        if (only_phase < 0 || only_phase == EBB_CG_MATVEC) {
+            KernelTimer kt(c, EBB_K_EDGE_MATVEC, s);
+            EBB_TRY((launch_tma<R, true, true, true>(c, G, A, z, q, mask, scal + S_PQ, c->d_counter + 1, s, p, p2,
+                                                     scal)));
         }
-        {
-            KernelTimer kt(c, EBB_K_CG_DIR, s);
-            k_cg_dir<R><<<vg, 256, 0, s>>>(ndof, z, p, scal);
+        if (only_phase < 0 || only_phase == EBB_CG_UPDATE) {
+            KernelTimer kt(c, EBB_K_CG_UPDATE, s);
+            k_cg_update<R><<<ug, 256, 0, s>>>(G.nv, p, p2, q, dinv, x, r, z, c->d_partials, c->d_counter + 2, scal,
+                                              rho_user, c->d_err);
         }
     }
     EBB_CUDA(c, cudaGetLastError());
@@ -330,6 +620,7 @@ ebb_status cg_validate(Ctx* c, const ebb_cg* cg, EdgeGraph* G, ebb_dtype* dt) {
     if (!A) return fail(c, EBB_E_ARG, "cg: bad A");
     *dt = A->dtype;
     EBB_TRY(check_mat(c, A, cg->edges, *dt, "A"));
+    if (!A->owned) return fail(c, EBB_E_TYPE, "cg: A must be a library-allocated field (padded for bulk copies)");
     EBB_TRY(check_vec(c, get_field(c, cg->b), G->verts, *dt, "b"));
     EBB_TRY(check_vec(c, get_field(c, cg->x), G->verts, *dt, "x"));
     return EBB_OK;
@@ -363,18 +654,21 @@ ebb_status ebb_map_edge_matvec(ebb_ctx ctx, ebb_rel edges, ebb_field A, ebb_fiel
         pq = (double*)PQ->ptr;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    bool fused = pq || m;
+    const bool fused = pq || m;
+    double* pqo = pq ? pq : (double*)c->d_partials + 8191;
     if (dt == EBB_F64) {
-        if (fused) return launch_matvec<double, 1>(c, G, (const double*)Af->ptr, (const double*)P->ptr, (double*)Q->ptr, m,
-                                                   nullptr, pq ? pq : (double*)c->d_partials + 8191, c->d_counter + 3, s);
-        return launch_matvec<double, 0>(c, G, (const double*)Af->ptr, (const double*)P->ptr, (double*)Q->ptr, nullptr,
-                                        nullptr, nullptr, c->d_counter + 3, s);
+        if (fused)
+            return launch_spmv3<double, true>(c, G, (const double*)Af->ptr, (const double*)P->ptr, (double*)Q->ptr, m,
+                                              pqo, c->d_counter + 3, s, Af->owned);
+        return launch_spmv3<double, false>(c, G, (const double*)Af->ptr, (const double*)P->ptr, (double*)Q->ptr,
+                                           nullptr, nullptr, c->d_counter + 3, s, Af->owned);
     }
     if (dt == EBB_F32) {
-        if (fused) return launch_matvec<float, 1>(c, G, (const float*)Af->ptr, (const float*)P->ptr, (float*)Q->ptr, m,
-                                                  nullptr, pq ? pq : (double*)c->d_partials + 8191, c->d_counter + 3, s);
-        return launch_matvec<float, 0>(c, G, (const float*)Af->ptr, (const float*)P->ptr, (float*)Q->ptr, nullptr,
-                                       nullptr, nullptr, c->d_counter + 3, s);
+        if (fused)
+            return launch_spmv3<float, true>(c, G, (const float*)Af->ptr, (const float*)P->ptr, (float*)Q->ptr, m,
+                                             pqo, c->d_counter + 3, s, Af->owned);
+        return launch_spmv3<float, false>(c, G, (const float*)Af->ptr, (const float*)P->ptr, (float*)Q->ptr, nullptr,
+                                          nullptr, c->d_counter + 3, s, Af->owned);
     }
     return fail(c, EBB_E_TYPE, "matvec: dtype must be F32 or F64");
 }
@@ -399,7 +693,7 @@ ebb_status ebb_global_reduce(ebb_ctx ctx, int32_t op, ebb_field a, ebb_field b, 
     const uint8_t* m;
     EBB_TRY(check_mask(c, mask, Af->rel, &m));
     uint64_t n = c->rels[Af->rel].size;
-    unsigned grid = vec_grid(c, n * Af->comps());
+    unsigned grid = occ_grid(c, k_global_reduce<double, ROP_SUM, true>, 256, 0, n * Af->comps());
     cudaStream_t s = (cudaStream_t)stream;
     int soa = Af->layout == EBB_SOA;
     double* o = (double*)O->ptr;
@@ -459,8 +753,8 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
     const int lpv = G.max_group <= 16 ? 16 : 32;
 #define EBB_ASM(R)                                                                                                  \
     do {                                                                                                            \
-        EBB_TRY((launch_matvec<R, 0>(c, G, (const R*)K->ptr, (const R*)V->ptr, (R*)kv, nullptr, nullptr, nullptr,     \
-                                     c->d_counter + 5, s)));                                                        \
+        EBB_TRY((launch_spmv3<R, false>(c, G, (const R*)K->ptr, (const R*)V->ptr, (R*)kv, nullptr, nullptr,          \
+                                        c->d_counter + 5, s, K->owned)));                                         \
         KernelTimer kt(c, EBB_K_ASSEMBLE, s);                                                                       \
         c->launches++;                                                                                              \
         k_assemble_b<R><<<grid_for(3 * G.nv, 256), 256, 0, s>>>(G.nv, (const R*)F->ptr, (const R*)M->ptr,             \
@@ -494,44 +788,47 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
         return fail(c, EBB_E_TYPE, "cg: self must be the verts -> edges self-loop key");
     const uint8_t* mask;
     EBB_TRY(check_mask(c, cg->mask, G.verts, &mask));
-    // allocate work fields that were not supplied
+    // work vectors: padded 4-component records, allocated on first use
     static int serial = 0;
-    int id = serial++;
     char nm[64];
-    ebb_field* work[] = {&cg->r, &cg->p, &cg->z, &cg->q, &cg->dinv};
-    const char* wn[] = {"r", "p", "z", "q", "dinv"};
-    for (int i = 0; i < 5; ++i) {
-        if (*work[i] == EBB_NONE) {
+    ebb_field* work[] = {&cg->r, &cg->p, &cg->z, &cg->q, &cg->dinv, &cg->p2};
+    const char* wn[] = {"r", "p", "z", "q", "dinv", "p2"};
+    int id = -1;
+    for (int i = 0; i < 6; ++i) {
+        Field* W = *work[i] == EBB_NONE ? nullptr : get_field(c, *work[i]);
+        if (!W) {
+            if (id < 0) id = serial++;
             snprintf(nm, sizeof(nm), "__cg%d_%s", id, wn[i]);
-            EBB_TRY(new_internal_field(c, G.verts, nm, dt, 3, 1, EBB_AOS, work[i]));
-        } else {
-            EBB_TRY(check_vec(c, get_field(c, *work[i]), G.verts, dt, wn[i]));
+            EBB_TRY(new_internal_field(c, G.verts, nm, dt, 4, 1, EBB_AOS, work[i]));
+        } else if (W->rel != G.verts || W->comps() != 4 || W->dtype != dt || W->layout != EBB_AOS) {
+            return fail(c, EBB_E_TYPE, "cg: work field '%s' must be an AOS 4x1 (padded vec3) field on verts",
+                        W->name.c_str());
         }
     }
     if (cg->rho == EBB_NONE) {
+        if (id < 0) id = serial++;
         snprintf(nm, sizeof(nm), "__cg%d_rho", id);
         EBB_TRY(ebb_global_new(ctx, nm, EBB_F64, 0.0, &cg->rho));
     }
     if (cg->scal == EBB_NONE) {
+        if (id < 0) id = serial++;
         snprintf(nm, sizeof(nm), "__cg%d_scal", id);
         ebb_rel sr;
         EBB_TRY(ebb_relation_new(ctx, (std::string(nm) + "_rel").c_str(), S_NSCAL, &sr));
         EBB_TRY(new_internal_field(c, sr, nm, EBB_F64, 1, 1, EBB_AOS, &cg->scal));
     }
     cudaStream_t s = (cudaStream_t)stream;
-    uint64_t ndof = 3 * G.nv;
-    unsigned vg = vec_grid(c, ndof);
-    const uint32_t* self = (const uint32_t*)c->fields[cg->self].ptr;
     double* scal = (double*)c->fields[cg->scal].ptr;
     double* rho = (double*)c->fields[cg->rho].ptr;
-#define EBB_INIT(R)                                                                                                 \
-    do {                                                                                                            \
-        c->launches += 2;                                                                                           \
-        k_dinv<R><<<grid_for(G.nv, 256), 256, 0, s>>>(G.nv, self, (const R*)c->fields[cg->A].ptr, G.ne, mask,         \
-                                                      (R*)c->fields[cg->dinv].ptr);                                  \
-        k_cg_init<R><<<vg, 256, 0, s>>>(ndof, (const R*)c->fields[cg->b].ptr, mask, (const R*)c->fields[cg->dinv].ptr, \
-                                        (R*)c->fields[cg->x].ptr, (R*)c->fields[cg->r].ptr, (R*)c->fields[cg->z].ptr,  \
-                                        (R*)c->fields[cg->p].ptr, c->d_partials, c->d_counter + 6, scal, rho);         \
+    const uint32_t* self = (const uint32_t*)c->fields[cg->self].ptr;
+    c->launches++;
+#define EBB_INIT(R)                                                                                                  \
+    do {                                                                                                             \
+        const unsigned g = occ_grid(c, k_cg_init<R>, 256, 0, G.nv);                                                  \
+        k_cg_init<R><<<g, 256, 0, s>>>(G.nv, self, (const R*)c->fields[cg->A].ptr, G.ne,                             \
+                                       (const R*)c->fields[cg->b].ptr, mask, (R*)c->fields[cg->dinv].ptr,            \
+                                       (R*)c->fields[cg->x].ptr, (R*)c->fields[cg->r].ptr, (R*)c->fields[cg->z].ptr, \
+                                       (R*)c->fields[cg->p].ptr, c->d_partials, c->d_counter + 6, scal, rho);        \
     } while (0)
     if (dt == EBB_F64) EBB_INIT(double);
     else EBB_INIT(float);
@@ -547,12 +844,27 @@ ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream 
     EdgeGraph G;
     ebb_dtype dt;
     EBB_TRY(cg_validate(c, cg, &G, &dt));
-    ebb_field w[] = {cg->r, cg->p, cg->z, cg->q, cg->dinv, cg->rho, cg->scal};
+    ebb_field w[] = {cg->r, cg->p, cg->z, cg->q, cg->dinv, cg->rho, cg->scal, cg->p2};
     for (ebb_field f : w)
         if (!get_field(c, f)) return fail(c, EBB_E_STATE, "cg: call ebb_cg_init first");
     cudaStream_t s = (cudaStream_t)stream;
     if (dt == EBB_F64) return cg_iterate<double>(c, cg, G, iters, s);
     return cg_iterate<float>(c, cg, G, iters, s);
+}
+
+ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream stream) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");
+    if (phase < EBB_CG_DIR || phase > EBB_CG_UPDATE) return fail(c, EBB_E_ARG, "unknown CG phase %d", phase);
+    EdgeGraph G;
+    ebb_dtype dt;
+    EBB_TRY(cg_validate(c, cg, &G, &dt));
+    ebb_field w[] = {cg->r, cg->p, cg->z, cg->q, cg->dinv, cg->rho, cg->scal, cg->p2};
+    for (ebb_field f : w)
+        if (!get_field(c, f)) return fail(c, EBB_E_STATE, "cg: call ebb_cg_init first");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dt == EBB_F64) return cg_iterate<double>(c, cg, G, 1, s, phase);
+    return cg_iterate<float>(c, cg, G, 1, s, phase);
 }
 
 ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stream stream) {

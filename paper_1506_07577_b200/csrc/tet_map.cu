@@ -1,27 +1,40 @@
 // tet_map.cu -- the element map over the tets relation.
 //
-// Per tet (P:941-946 Vega StVK, P:975-980 neo-Hookean "specialized"):
-//   gather u[v[k]] through the key-field tets.v,
-//   H = Du Dminv, F = I + H (displacement form: no cancellation in fp32),
-//   first Piola stress P and energy density Psi (StVK or compressible NH),
-//   f_i = -W P g_i (i = 1..3), f_0 = -(f_1 + f_2 + f_3),
-//   K_ij = d^2(W Psi)/dx_i dx_j by the closed rank-1 forms of DESIGN.md §5:
-//     NH   K_ij = W [mu m_ij I + c1 k_j k_i^T + lam k_i k_j^T],  k_i = F^-T g_i
-//     StVK K_ij = W [s_ij I + mu m_ij F F^T + mu h_j h_i^T + lam h_i h_j^T], h_i = F g_i
-//   and reduces f[v[i]] += f_i, K[e[i][j]] += K_ij (field `+=`) and
-//   energy += W Psi (global `+=`, fused two-pass).
+// Per tet (P:941-946 Vega StVK, P:975-980 neo-Hookean "specialized"): gather
+// u[v[k]] through the key-field tets.v, element physics
+// (element.cuh: displacement form + closed rank-1 stiffness), and the
+// reductions f[v[i]] += f_i, K[e[i][j]] += K_ij (field `+=`) and
+// energy += W Psi (global `+=`, fused two-pass).
+//
+// Two scatter strategies (SURVEY §8(a) "the += strategies", chosen by
+// measurement -- DESIGN.md §5):
+//   ATOMIC  one thread per tet, red.global.add per value (the paper's field
+//           reductions with native fp64 RED instead of Kepler CAS);
+//   TILED   owner-computes vertex tiles: a CTA owns the canonical edge rows
+//           (tail <= head) and the forces of a tile of consecutive vertices,
+//           recomputes every tet touching the tile, accumulates in shared
+//           memory and writes each K row and f row exactly once with plain
+//           stores (row (b,a) as the transpose of canonical (a,b)).  No global
+//           atomics, no zero-fill of K.
 // The oracle computes the same quantities by the textbook F-form and a generic
 // 4th-order tensor contraction (oracle/ebb_oracle.c); the two share no code.
+#include <cub/cub.cuh>
+
+#include <cstdlib>
+
 #include "ebb_internal.cuh"
+#include "element.cuh"
 #include "reduce.cuh"
 
 using namespace ebb;
 
 namespace {
 
-template <typename R>
-struct M3 {
-    R m[3][3];
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
 };
 
 template <typename R>
@@ -29,6 +42,32 @@ __device__ __forceinline__ void red_add(R* p, R v) {
     atomicAdd(p, v);  // result unused -> REDG.E.ADD
 }
 
+template <typename R>
+__device__ __forceinline__ void load_tet(uint64_t t, uint64_t nt, const uint4* __restrict__ tv, const R* __restrict__ u,
+                                         const R* __restrict__ Dminv, const R* __restrict__ Wt,
+                                         const R* __restrict__ mu_t, const R* __restrict__ lam_t, uint32_t v[4],
+                                         R uu[4][3], TetState<R>& st) {
+    const uint4 vv = tv[t];
+    v[0] = vv.x;
+    v[1] = vv.y;
+    v[2] = vv.z;
+    v[3] = vv.w;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) uu[k][a] = u[3ull * v[k] + a];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) st.g[r + 1][c] = Dminv[(uint64_t)(3 * r + c) * nt + t];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) st.g[0][c] = -(st.g[1][c] + st.g[2][c] + st.g[3][c]);
+    st.W = Wt[t];
+    st.mu = mu_t[t];
+    st.lam = lam_t[t];
+}
+
+// ---------------------------------------------------------------- ATOMIC
 template <typename R, int MODEL, bool WANT_K, bool WANT_E>
 __global__ void __launch_bounds__(128) k_tet_map(uint64_t nt, const uint4* __restrict__ tv,
                                                  const uint4* __restrict__ te, const R* __restrict__ u,
@@ -39,188 +78,41 @@ __global__ void __launch_bounds__(128) k_tet_map(uint64_t nt, const uint4* __res
                                                  R* __restrict__ energy, unsigned long long* __restrict__ err) {
     double e_acc = 0.0;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt; t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint4 vv = tv[t];
-        const uint32_t v[4] = {vv.x, vv.y, vv.z, vv.w};
+        uint32_t v[4];
         R uu[4][3];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int a = 0; a < 3; ++a) uu[k][a] = u[3ull * v[k] + a];
-        // g_i = row i-1 of Dm^-1 (i = 1..3), component-planar storage
-        R g[4][3];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) g[r + 1][c] = Dminv[(uint64_t)(3 * r + c) * nt + t];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) g[0][c] = -(g[1][c] + g[2][c] + g[3][c]);
-        const R W = Wt[t], mu = mu_t[t], lam = lam_t[t];
-        // H = Du Dm^-1,  Du = [u1-u0, u2-u0, u3-u0]
-        R H[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-                R s = 0;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) s += (uu[k + 1][a] - uu[0][a]) * g[k + 1][b];
-                H[a][b] = s;
-            }
-        R P[3][3];
-        R psi;
-        // model-specific state kept for the stiffness
-        R S[3][3];     // StVK second Piola stress
-        R FiT[3][3];   // NH F^-T
-        R c1 = 0;      // NH mu - lam ln J
-        if (MODEL == EBB_STVK) {
-            // E = 1/2 (H + H^T + H^T H), S = 2 mu E + lam tr(E) I, P = (I + H) S
-            R E[3][3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) {
-                    R hh = H[0][a] * H[0][b] + H[1][a] * H[1][b] + H[2][a] * H[2][b];
-                    E[a][b] = R(0.5) * (H[a][b] + H[b][a] + hh);
-                }
-            R trE = E[0][0] + E[1][1] + E[2][2];
-            R EE = 0;
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) {
-                    S[a][b] = R(2) * mu * E[a][b] + (a == b ? lam * trE : R(0));
-                    EE += E[a][b] * E[a][b];
-                }
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) P[a][b] = S[a][b] + H[a][0] * S[0][b] + H[a][1] * S[1][b] + H[a][2] * S[2][b];
-            psi = mu * EE + R(0.5) * lam * trE * trE;
-        } else {
-            // cancellation-free invariants of F = I + H (App. B of SURVEY.md)
-            R t1 = H[0][0] + H[1][1] + H[2][2];
-            R H2[3][3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) H2[a][b] = H[a][0] * H[0][b] + H[a][1] * H[1][b] + H[a][2] * H[2][b];
-            R trH2 = H2[0][0] + H2[1][1] + H2[2][2];
-            R s2 = R(0.5) * (t1 * t1 - trH2);
-            R dH = H[0][0] * (H[1][1] * H[2][2] - H[1][2] * H[2][1]) - H[0][1] * (H[1][0] * H[2][2] - H[1][2] * H[2][0]) +
-                   H[0][2] * (H[1][0] * H[2][1] - H[1][1] * H[2][0]);
-            R delta = t1 + s2 + dH;  // J - 1
-            R J = R(1) + delta;
-            if (!(J > R(0))) atomicAdd(&err[ERR_INVERTED], 1ull);
-            R lnJ = log1p(delta);
-            R invJ = R(1) / J;
-            // adj(F) = (1 + t + s2) I - (1 + t) H + H^2 ;  cof F = adj^T ; F^-T = cof/J
-            R ca = R(1) + t1 + s2, cb = R(1) + t1;
-            R cof[3][3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) cof[a][b] = (a == b ? ca : R(0)) - cb * H[b][a] + H2[b][a];
-            // J F - cof F = det(H) I + (1 + delta) H + (1 + t) H^T - (H^T)^2
-            R HF2 = 0;
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) {
-                    R jf = (a == b ? dH : R(0)) + J * H[a][b] + cb * H[b][a] - H2[b][a];
-                    P[a][b] = (mu * jf + lam * lnJ * cof[a][b]) * invJ;
-                    FiT[a][b] = cof[a][b] * invJ;
-                    HF2 += H[a][b] * H[a][b];
-                }
-            c1 = mu - lam * lnJ;
-            // tr(F^T F) - 3 = 2 tr H + |H|^2
-            psi = R(0.5) * mu * (R(2) * t1 + HF2) - mu * lnJ + R(0.5) * lam * lnJ * lnJ;
-        }
-        // forces
+        TetState<R> st;
+        load_tet(t, nt, tv, u, Dminv, Wt, mu_t, lam_t, v, uu, st);
+        tet_physics<R, MODEL, WANT_K>(uu, st);
+        if (MODEL == EBB_NH && !(st.J > R(0))) atomicAdd(&err[ERR_INVERTED], 1ull);
         R fi[4][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) fi[0][a] = 0;
-#pragma unroll
-        for (int i = 1; i < 4; ++i)
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                fi[i][a] = -W * (P[a][0] * g[i][0] + P[a][1] * g[i][1] + P[a][2] * g[i][2]);
-                fi[0][a] -= fi[i][a];
-            }
+        tet_forces(st, fi);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int a = 0; a < 3; ++a) red_add(&f[3ull * v[i] + a], fi[i][a]);
-        if (WANT_E) e_acc += (double)(W * psi);
+        if (WANT_E) e_acc += (double)(st.W * st.psi);
         if (WANT_K) {
             uint32_t row[16];
-            const uint4* tep = te + 4 * t;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint4 r4 = tep[q];
-                row[4 * q + 0] = r4.x;
-                row[4 * q + 1] = r4.y;
-                row[4 * q + 2] = r4.z;
-                row[4 * q + 3] = r4.w;
-            }
-            // per-corner vectors: NH k_i = F^-T g_i ; StVK h_i = F g_i
-            R kv[4][3];
-            R B[3][3];
-            if (MODEL == EBB_NH) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) kv[i][a] = FiT[a][0] * g[i][0] + FiT[a][1] * g[i][1] + FiT[a][2] * g[i][2];
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int a = 0; a < 3; ++a)
-                        kv[i][a] = g[i][a] + H[a][0] * g[i][0] + H[a][1] * g[i][1] + H[a][2] * g[i][2];
-                // B = F F^T
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-#pragma unroll
-                    for (int b = 0; b < 3; ++b) {
-                        R s = 0;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) s += ((a == c ? R(1) : R(0)) + H[a][c]) * ((b == c ? R(1) : R(0)) + H[b][c]);
-                        B[a][b] = s;
-                    }
+            for (int qd = 0; qd < 4; ++qd) {
+                uint4 r4 = te[4 * t + qd];
+                row[4 * qd + 0] = r4.x;
+                row[4 * qd + 1] = r4.y;
+                row[4 * qd + 2] = r4.z;
+                row[4 * qd + 3] = r4.w;
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                R Sg[3];
-                if (MODEL == EBB_STVK) {
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) Sg[a] = S[a][0] * g[i][0] + S[a][1] * g[i][1] + S[a][2] * g[i][2];
-                }
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    R mij = g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2];
+                    R Kb[3][3];
+                    tet_block<R, MODEL>(st, i, j, Kb);
                     R* Kr = K + row[4 * i + j];
-                    if (MODEL == EBB_NH) {
-                        R d = W * mu * mij, cc = W * c1, cl = W * lam;
 #pragma unroll
-                        for (int a = 0; a < 3; ++a)
+                    for (int a = 0; a < 3; ++a)
 #pragma unroll
-                            for (int b = 0; b < 3; ++b) {
-                                R val = cc * kv[j][a] * kv[i][b] + cl * kv[i][a] * kv[j][b] + (a == b ? d : R(0));
-                                red_add(Kr + (uint64_t)(3 * a + b) * ne, val);
-                            }
-                    } else {
-                        R sij = Sg[0] * g[j][0] + Sg[1] * g[j][1] + Sg[2] * g[j][2];
-                        R d = W * sij, cm = W * mu * mij, ch = W * mu, cl = W * lam;
-#pragma unroll
-                        for (int a = 0; a < 3; ++a)
-#pragma unroll
-                            for (int b = 0; b < 3; ++b) {
-                                R val = cm * B[a][b] + ch * kv[j][a] * kv[i][b] + cl * kv[i][a] * kv[j][b] +
-                                        (a == b ? d : R(0));
-                                red_add(Kr + (uint64_t)(3 * a + b) * ne, val);
-                            }
-                    }
+                        for (int b = 0; b < 3; ++b) red_add(Kr + (uint64_t)(3 * a + b) * ne, Kb[a][b]);
                 }
-            }
         }
     }
     if (WANT_E) {
@@ -229,14 +121,310 @@ __global__ void __launch_bounds__(128) k_tet_map(uint64_t nt, const uint4* __res
     }
 }
 
+// ---------------------------------------------------------------- plan build
+// pair order: off-diagonal (0,1) (0,2) (0,3) (1,2) (1,3) (2,3), diagonal (0,0)..(3,3)
+__constant__ int8_t kPairI[10] = {0, 0, 0, 1, 1, 2, 0, 1, 2, 3};
+__constant__ int8_t kPairJ[10] = {1, 2, 3, 2, 3, 3, 0, 1, 2, 3};
+
+__global__ void k_canon_flag(uint64_t ne, const uint32_t* __restrict__ tail, const uint32_t* __restrict__ head,
+                             uint32_t* __restrict__ flag) {
+    uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r < ne) flag[r] = head[r] >= tail[r] ? 1u : 0u;
+}
+
+__device__ __forceinline__ uint32_t find_row_d(const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
+                                               uint32_t a, uint32_t b) {
+    uint32_t lo = index[a], hi = index[a + 1];
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (head[mid] < b) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_canon_lists(uint64_t ne, const uint32_t* __restrict__ tail, const uint32_t* __restrict__ head,
+                              const uint32_t* __restrict__ index, const uint32_t* __restrict__ gci,
+                              uint32_t* __restrict__ crow, uint32_t* __restrict__ ctrow) {
+    uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= ne) return;
+    uint32_t a = tail[r], b = head[r];
+    if (b < a) return;
+    uint32_t g = gci[r];
+    crow[g] = (uint32_t)r;
+    ctrow[g] = (a == b) ? (uint32_t)r : find_row_d(index, head, b, a);
+}
+
+__global__ void k_tile_cptr(uint32_t ntiles, int nvt, uint64_t nv, const uint32_t* __restrict__ index,
+                            const uint32_t* __restrict__ gci, uint64_t ne, uint32_t ncanon, uint32_t* __restrict__ cptr) {
+    uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t > ntiles) return;
+    uint64_t v = t * (uint64_t)nvt;
+    if (v > nv) v = nv;
+    uint32_t r = index[v];
+    cptr[t] = (r >= ne) ? ncanon : gci[r];
+}
+
+__global__ void k_inst_keys(uint64_t nt, const uint32_t* __restrict__ tv, int nvt, uint64_t* __restrict__ keys) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= nt * 4) return;
+    uint64_t t = i >> 2;
+    keys[i] = ((uint64_t)(tv[i] / (uint32_t)nvt) << 32) | t;
+}
+
+__global__ void k_inst_ptr(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ ptr, uint32_t ntiles) {
+    uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (s > ntiles) return;
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if ((keys[mid] >> 32) < s) lo = mid + 1;
+        else hi = mid;
+    }
+    ptr[s] = (uint32_t)lo;
+}
+
+// record words: w0 tet | w1..w5 slot[10] (u16) | w6 local vertex of corner k (u8) | w7 flags
+// flags bit p (p < 6): block of pair p is stored transposed; bit 8: energy owner
+__global__ void k_inst_records(uint64_t ninst, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ tv,
+                               const uint32_t* __restrict__ te, const uint32_t* __restrict__ gci,
+                               const uint32_t* __restrict__ cptr, int nvt, uint32_t* __restrict__ recs) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= ninst) return;
+    const uint32_t tile = (uint32_t)(keys[i] >> 32);
+    const uint64_t t = keys[i] & 0xFFFFFFFFull;
+    uint32_t v[4];
+    for (int k = 0; k < 4; ++k) v[k] = tv[4 * t + k];
+    uint32_t w[8] = {(uint32_t)t, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t flags = 0;
+    for (int p = 0; p < 10; ++p) {
+        int a = kPairI[p], b = kPairJ[p];
+        uint32_t lo = v[a] < v[b] ? v[a] : v[b];
+        uint32_t slot = 0xFFFFu;
+        if (lo / (uint32_t)nvt == tile) {
+            // canonical row (min, max); block K_ab is stored transposed when v_a > v_b
+            uint32_t r = (v[a] <= v[b]) ? te[16 * t + 4 * a + b] : te[16 * t + 4 * b + a];
+            slot = gci[r] - cptr[tile];
+            if (p < 6 && v[a] > v[b]) flags |= 1u << p;
+        }
+        w[1 + p / 2] |= slot << (16 * (p & 1));
+    }
+    uint32_t vmin = v[0];
+    for (int k = 0; k < 4; ++k) {
+        uint32_t lv = (v[k] / (uint32_t)nvt == tile) ? (v[k] - tile * (uint32_t)nvt) : 0xFFu;
+        w[6] |= lv << (8 * k);
+        vmin = v[k] < vmin ? v[k] : vmin;
+    }
+    if (vmin / (uint32_t)nvt == tile) flags |= 1u << 8;
+    w[7] = flags;
+    for (int k = 0; k < 8; ++k) recs[8 * i + k] = w[k];
+}
+
+__global__ void k_max_diff(const uint32_t* __restrict__ ptr, uint32_t n, unsigned int* out) {
+    uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n) atomicMax(out, ptr[s + 1] - ptr[s]);
+}
+
+ebb_status build_plan(Ctx* c, ebb_field vf, ebb_field ef, int nvt, MapPlan** out) {
+    for (auto& P : c->plans)
+        if (P.v == vf && P.e == ef && P.nvt == nvt) {
+            *out = &P;
+            return EBB_OK;
+        }
+    Field* V = get_field(c, vf);
+    Field* E = get_field(c, ef);
+    ebb_rel edges = E->key_target;
+    Relation& ER = c->rels[edges];
+    if (ER.grouped_by == EBB_NONE || ER.index == EBB_NONE)
+        return fail(c, EBB_E_STATE, "tiled map: the edge relation must be grouped by tail");
+    ebb_field hf = EBB_NONE;
+    for (ebb_field f : ER.fields)
+        if (c->fields[f].alive && c->fields[f].name == "head") hf = f;
+    if (hf == EBB_NONE) return fail(c, EBB_E_STATE, "tiled map: edge relation has no 'head' key-field");
+    const uint32_t* tail = (const uint32_t*)c->fields[ER.grouped_by].ptr;
+    const uint32_t* head = (const uint32_t*)c->fields[hf].ptr;
+    const uint32_t* index = (const uint32_t*)c->fields[ER.index].ptr;
+    const uint64_t nt = c->rels[V->rel].size, nv = c->rels[V->key_target].size, ne = ER.size;
+    MapPlan P;
+    P.v = vf;
+    P.e = ef;
+    P.nvt = nvt;
+    P.ntiles = (uint32_t)((nv + nvt - 1) / nvt);
+    DevBuf flag, gci, tmp, keys, keys2, uk, nsel, mx, tmp2;
+    EBB_CUDA(c, cudaMalloc(&flag.p, ne * 4));
+    EBB_CUDA(c, cudaMalloc(&gci.p, ne * 4));
+    k_canon_flag<<<grid_for(ne, 256), 256>>>(ne, tail, head, (uint32_t*)flag.p);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (const uint32_t*)flag.p, (uint32_t*)gci.p, (int)ne);
+    EBB_CUDA(c, cudaMalloc(&tmp.p, tb));
+    EBB_CUDA(c, cub::DeviceScan::ExclusiveSum(tmp.p, tb, (const uint32_t*)flag.p, (uint32_t*)gci.p, (int)ne));
+    uint32_t last_g = 0, last_f = 0;
+    EBB_CUDA(c, cudaMemcpy(&last_g, (uint32_t*)gci.p + ne - 1, 4, cudaMemcpyDeviceToHost));
+    EBB_CUDA(c, cudaMemcpy(&last_f, (uint32_t*)flag.p + ne - 1, 4, cudaMemcpyDeviceToHost));
+    P.ncanon = (uint64_t)last_g + last_f;
+    EBB_CUDA(c, cudaMalloc(&P.crow, P.ncanon * 4));
+    EBB_CUDA(c, cudaMalloc(&P.ctrow, P.ncanon * 4));
+    k_canon_lists<<<grid_for(ne, 256), 256>>>(ne, tail, head, index, (const uint32_t*)gci.p, P.crow, P.ctrow);
+    EBB_CUDA(c, cudaMalloc(&P.tile_cptr, (P.ntiles + 1) * 4));
+    k_tile_cptr<<<grid_for(P.ntiles + 1, 256), 256>>>(P.ntiles, nvt, nv, index, (const uint32_t*)gci.p, ne,
+                                                      (uint32_t)P.ncanon, P.tile_cptr);
+    // instances: unique (tile, tet) over the 4 corners of every tet
+    const uint64_t nk = nt * 4;
+    EBB_CUDA(c, cudaMalloc(&keys.p, nk * 8));
+    EBB_CUDA(c, cudaMalloc(&keys2.p, nk * 8));
+    EBB_CUDA(c, cudaMalloc(&uk.p, nk * 8));
+    EBB_CUDA(c, cudaMalloc(&nsel.p, 8));
+    k_inst_keys<<<grid_for(nk, 256), 256>>>(nt, (const uint32_t*)V->ptr, nvt, (uint64_t*)keys.p);
+    int tbits = 1;
+    while (tbits < 32 && (1ull << tbits) <= P.ntiles) ++tbits;
+    size_t tb1 = 0, tb2 = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb1, (const uint64_t*)keys.p, (uint64_t*)keys2.p, (int)nk, 0, 32 + tbits);
+    cub::DeviceSelect::Unique(nullptr, tb2, (const uint64_t*)keys2.p, (uint64_t*)uk.p, (int*)nsel.p, (int)nk);
+    EBB_CUDA(c, cudaMalloc(&tmp2.p, tb1 > tb2 ? tb1 : tb2));
+    EBB_CUDA(c, cub::DeviceRadixSort::SortKeys(tmp2.p, tb1, (const uint64_t*)keys.p, (uint64_t*)keys2.p, (int)nk, 0,
+                                               32 + tbits));
+    EBB_CUDA(c, cub::DeviceSelect::Unique(tmp2.p, tb2, (const uint64_t*)keys2.p, (uint64_t*)uk.p, (int*)nsel.p, (int)nk));
+    int ni = 0;
+    EBB_CUDA(c, cudaMemcpy(&ni, nsel.p, 4, cudaMemcpyDeviceToHost));
+    P.ninst = (uint64_t)ni;
+    EBB_CUDA(c, cudaMalloc(&P.inst_ptr, (P.ntiles + 1) * 4));
+    k_inst_ptr<<<grid_for(P.ntiles + 1, 256), 256>>>((const uint64_t*)uk.p, P.ninst, P.inst_ptr, P.ntiles);
+    EBB_CUDA(c, cudaMalloc(&P.recs, P.ninst * 32));
+    k_inst_records<<<grid_for(P.ninst, 256), 256>>>(P.ninst, (const uint64_t*)uk.p, (const uint32_t*)V->ptr,
+                                                    (const uint32_t*)E->ptr, (const uint32_t*)gci.p, P.tile_cptr, nvt,
+                                                    (uint32_t*)P.recs);
+    EBB_CUDA(c, cudaMalloc(&mx.p, 4));
+    EBB_CUDA(c, cudaMemset(mx.p, 0, 4));
+    k_max_diff<<<grid_for(P.ntiles, 256), 256>>>(P.tile_cptr, P.ntiles, (unsigned int*)mx.p);
+    EBB_CUDA(c, cudaGetLastError());
+    EBB_CUDA(c, cudaMemcpy(&P.max_slots, mx.p, 4, cudaMemcpyDeviceToHost));
+    if (P.max_slots >= 0xFFFFu) {
+        P.release();
+        return fail(c, EBB_E_RANGE, "tiled map: %u canonical rows in one tile (> 65534)", P.max_slots);
+    }
+    c->plans.push_back(P);
+    *out = &c->plans.back();
+    return EBB_OK;
+}
+
+// ---------------------------------------------------------------- TILED
+template <typename R, int MODEL, bool WANT_E>
+__global__ void __launch_bounds__(256) k_tet_map_tiled(
+    uint32_t ntiles, int nvt, uint64_t nv, uint64_t nt, const uint32_t* __restrict__ inst_ptr,
+    const uint4* __restrict__ recs, const uint32_t* __restrict__ tile_cptr, const uint32_t* __restrict__ crow,
+    const uint32_t* __restrict__ ctrow, uint32_t max_slots, const uint4* __restrict__ tv, const R* __restrict__ u,
+    const R* __restrict__ Dminv, const R* __restrict__ Wt, const R* __restrict__ mu_t, const R* __restrict__ lam_t,
+    R* __restrict__ f, R* __restrict__ K, uint64_t ne, int accumulate, double* __restrict__ partials,
+    unsigned int* __restrict__ counter, R* __restrict__ energy, unsigned long long* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    R* acc = reinterpret_cast<R*>(tile_smem);   // [max_slots][9]
+    R* facc = acc + (size_t)max_slots * 9;       // [nvt][3]
+    double e_acc = 0.0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t c0 = tile_cptr[tile], ns = tile_cptr[tile + 1] - c0;
+        const uint64_t v0 = (uint64_t)tile * nvt;
+        const uint32_t nvl = (uint32_t)((v0 + nvt <= nv) ? nvt : nv - v0);
+        for (uint32_t k = threadIdx.x; k < ns * 9; k += blockDim.x) acc[k] = R(0);
+        for (uint32_t k = threadIdx.x; k < nvl * 3; k += blockDim.x) facc[k] = R(0);
+        __syncthreads();
+        const uint32_t i1 = inst_ptr[tile + 1];
+        for (uint32_t i = inst_ptr[tile] + threadIdx.x; i < i1; i += blockDim.x) {
+            const uint4 ra = recs[2ull * i], rb = recs[2ull * i + 1];
+            const uint64_t t = ra.x;
+            uint32_t v[4];
+            R uu[4][3];
+            TetState<R> st;
+            load_tet(t, nt, tv, u, Dminv, Wt, mu_t, lam_t, v, uu, st);
+            tet_physics<R, MODEL, true>(uu, st);
+            const uint32_t flags = rb.w;
+            if (MODEL == EBB_NH && (flags & 0x100u) && !(st.J > R(0))) atomicAdd(&err[ERR_INVERTED], 1ull);
+            if (WANT_E && (flags & 0x100u)) e_acc += (double)(st.W * st.psi);
+            R fi[4][3];
+            tet_forces(st, fi);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t lv = (rb.z >> (8 * k)) & 0xFFu;
+                if (lv != 0xFFu)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) atomicAdd(&facc[3 * lv + a], fi[k][a]);
+            }
+            const uint32_t sw[5] = {ra.y, ra.z, ra.w, rb.x, rb.y};
+#pragma unroll
+            for (int p = 0; p < 10; ++p) {
+                const uint32_t slot = (sw[p / 2] >> (16 * (p & 1))) & 0xFFFFu;
+                if (slot == 0xFFFFu) continue;
+                const int bi = p < 6 ? (p < 3 ? 0 : (p < 5 ? 1 : 2)) : p - 6;
+                const int bj = p < 6 ? (p < 3 ? p + 1 : (p < 5 ? p - 1 : 3)) : p - 6;
+                R Kb[3][3];
+                tet_block<R, MODEL>(st, bi, bj, Kb);
+                R* as = acc + 9 * slot;
+                if (p >= 6) {
+                    // symmetric diagonal block: upper triangle only, mirrored at the flush
+                    atomicAdd(as + 0, Kb[0][0]);
+                    atomicAdd(as + 1, Kb[0][1]);
+                    atomicAdd(as + 2, Kb[0][2]);
+                    atomicAdd(as + 4, Kb[1][1]);
+                    atomicAdd(as + 5, Kb[1][2]);
+                    atomicAdd(as + 8, Kb[2][2]);
+                } else if ((flags >> p) & 1u) {
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+#pragma unroll
+                        for (int b = 0; b < 3; ++b) atomicAdd(as + 3 * a + b, Kb[b][a]);
+                } else {
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+#pragma unroll
+                        for (int b = 0; b < 3; ++b) atomicAdd(as + 3 * a + b, Kb[a][b]);
+                }
+            }
+        }
+        __syncthreads();
+        // flush: canonical row (a,b) and its transpose (b,a), each written once
+        for (uint32_t s = threadIdx.x; s < ns; s += blockDim.x) {
+            const uint32_t r = crow[c0 + s], rt = ctrow[c0 + s];
+            const R* as = acc + 9 * s;
+            R blk[9];
+#pragma unroll
+            for (int c = 0; c < 9; ++c) blk[c] = as[c];
+            if (rt == r) {
+                blk[3] = blk[1];
+                blk[6] = blk[2];
+                blk[7] = blk[5];
+            }
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                R* dst = K + (uint64_t)c * ne + r;
+                *dst = accumulate ? *dst + blk[c] : blk[c];
+            }
+            if (rt != r) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) {
+                        R* dst = K + (uint64_t)(3 * a + b) * ne + rt;
+                        *dst = accumulate ? *dst + blk[3 * b + a] : blk[3 * b + a];
+                    }
+            }
+        }
+        for (uint32_t k = threadIdx.x; k < nvl * 3; k += blockDim.x) {
+            R* dst = f + 3 * v0 + k;
+            *dst = accumulate ? *dst + facc[k] : facc[k];
+        }
+        __syncthreads();
+    }
+    if (WANT_E) {
+        double tot;
+        if (block_sum_last_done(e_acc, partials, counter, &tot)) *energy = (R)((double)*energy + tot);
+    }
+}
+
 template <typename R, int MODEL>
-ebb_status launch_map(Ctx* c, bool want_k, bool want_e, uint64_t nt, const Field* V, const Field* Ef, const Field* U,
-                      const Field* D, const Field* W, const Field* MU, const Field* LA, const Field* Fo, const Field* Ko,
-                      uint64_t ne, const Field* En, cudaStream_t s) {
+ebb_status launch_atomic(Ctx* c, bool want_k, bool want_e, uint64_t nt, const Field* V, const Field* Ef,
+                         const Field* U, const Field* D, const Field* W, const Field* MU, const Field* LA,
+                         const Field* Fo, const Field* Ko, uint64_t ne, const Field* En, cudaStream_t s) {
     const int block = 128;
-    unsigned grid = grid_for(nt, block);
-    unsigned cap = (unsigned)c->num_sms * 8;
-    if (grid > cap) grid = cap;
+    unsigned grid = occ_grid(c, k_tet_map<R, MODEL, true, true>, block, 0, nt);
     KernelTimer kt(c, EBB_K_TET_MAP, s);
 #define EBB_ARGS                                                                                               \
     nt, (const uint4*)V->ptr, Ef ? (const uint4*)Ef->ptr : nullptr, (const R*)U->ptr, (const R*)D->ptr,         \
@@ -251,12 +439,40 @@ ebb_status launch_map(Ctx* c, bool want_k, bool want_e, uint64_t nt, const Field
     return EBB_OK;
 }
 
+template <typename R, int MODEL>
+ebb_status launch_tiled(Ctx* c, const MapPlan& P, bool want_e, int accumulate, uint64_t nt, uint64_t nv,
+                        const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
+                        const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
+                        cudaStream_t s) {
+    const int block = 256;
+    const size_t smem = ((size_t)P.max_slots * 9 + (size_t)P.nvt * 3) * sizeof(R);
+    auto kern = want_e ? k_tet_map_tiled<R, MODEL, true> : k_tet_map_tiled<R, MODEL, false>;
+    EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned grid = occ_grid(c, kern, block, smem, (uint64_t)P.ntiles * block);
+    KernelTimer kt(c, EBB_K_TET_MAP, s);
+    kern<<<grid, block, smem, s>>>(P.ntiles, P.nvt, nv, nt, P.inst_ptr, P.recs, P.tile_cptr, P.crow, P.ctrow,
+                                   P.max_slots, (const uint4*)V->ptr, (const R*)U->ptr, (const R*)D->ptr,
+                                   (const R*)W->ptr, (const R*)MU->ptr, (const R*)LA->ptr, (R*)Fo->ptr, (R*)Ko->ptr,
+                                   ne, accumulate, c->d_partials, c->d_counter + 0, En ? (R*)En->ptr : nullptr,
+                                   c->d_err);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+int tile_vertices(ebb_dtype dt) {
+    const char* e = getenv("EBB_TILE_VERTS");
+    if (e && atoi(e) > 0 && atoi(e) <= 255) return atoi(e);
+    return dt == EBB_F64 ? 128 : 192;
+}
+
 }  // namespace
 
 extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     if (d->model != EBB_STVK && d->model != EBB_NH) return fail(c, EBB_E_ARG, "unknown model %d", d->model);
+    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_TILED)
+        return fail(c, EBB_E_ARG, "unknown scatter strategy %d", d->scatter);
     Field* V = get_field(c, d->v);
     Field* U = get_field(c, d->u);
     Field* D = get_field(c, d->Dminv);
@@ -273,7 +489,7 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     // relational typing: v : tets -> verts, e : tets -> edges
     if (V->dtype != EBB_KEY || V->comps() != 4) return fail(c, EBB_E_TYPE, "v must be a 4x1 key-field");
     ebb_rel tets = V->rel, verts = V->key_target;
-    uint64_t nt = c->rels[tets].size;
+    uint64_t nt = c->rels[tets].size, nv = c->rels[verts].size;
     ebb_dtype dt = U->dtype;
     if (dt != EBB_F32 && dt != EBB_F64) return fail(c, EBB_E_TYPE, "u must be F32 or F64");
     auto chk = [&](Field* F, ebb_rel rel, uint32_t comps, ebb_layout lay, const char* what) -> ebb_status {
@@ -300,16 +516,36 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     if (U->ptr == Fo->ptr || (Ko && (U->ptr == Ko->ptr || Fo->ptr == Ko->ptr)))
         return fail(c, EBB_E_PHASE, "map_tet_forces: a field is used in two phases (read and reduce)");
     cudaStream_t s = (cudaStream_t)stream;
+    const bool tiled = Ko && (d->scatter == EBB_SCATTER_TILED || d->scatter == EBB_SCATTER_AUTO);
+    if (tiled) {
+        // every K row and f row is written exactly once: zero_outputs means overwrite
+        MapPlan* P;
+        EBB_TRY(build_plan(c, d->v, d->e, tile_vertices(dt), &P));
+        V = get_field(c, d->v); U = get_field(c, d->u); D = get_field(c, d->Dminv); W = get_field(c, d->W);
+        MU = get_field(c, d->mu); LA = get_field(c, d->lam); Fo = get_field(c, d->f); Ko = get_field(c, d->K);
+        En = d->energy == EBB_NONE ? nullptr : get_field(c, d->energy);
+        if (d->zero_outputs && En) EBB_CUDA(c, cudaMemsetAsync(En->ptr, 0, dtype_size(dt), s));
+        int accum = d->zero_outputs ? 0 : 1;
+        bool we = En != nullptr;
+        if (dt == EBB_F64) {
+            if (d->model == EBB_NH)
+                return launch_tiled<double, EBB_NH>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+            return launch_tiled<double, EBB_STVK>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+        }
+        if (d->model == EBB_NH)
+            return launch_tiled<float, EBB_NH>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+        return launch_tiled<float, EBB_STVK>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+    }
     if (d->zero_outputs) {
-        EBB_CUDA(c, cudaMemsetAsync(Fo->ptr, 0, c->rels[verts].size * 3 * dtype_size(dt), s));
+        EBB_CUDA(c, cudaMemsetAsync(Fo->ptr, 0, nv * 3 * dtype_size(dt), s));
         if (Ko) EBB_CUDA(c, cudaMemsetAsync(Ko->ptr, 0, ne * 9 * dtype_size(dt), s));
         if (En) EBB_CUDA(c, cudaMemsetAsync(En->ptr, 0, dtype_size(dt), s));
     }
     bool wk = Ko != nullptr, we = En != nullptr;
     if (dt == EBB_F64) {
-        if (d->model == EBB_NH) return launch_map<double, EBB_NH>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
-        return launch_map<double, EBB_STVK>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+        if (d->model == EBB_NH) return launch_atomic<double, EBB_NH>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+        return launch_atomic<double, EBB_STVK>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
     }
-    if (d->model == EBB_NH) return launch_map<float, EBB_NH>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
-    return launch_map<float, EBB_STVK>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+    if (d->model == EBB_NH) return launch_atomic<float, EBB_NH>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+    return launch_atomic<float, EBB_STVK>(c, wk, we, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
 }

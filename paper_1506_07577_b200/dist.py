@@ -1,0 +1,249 @@
+"""Multi-GPU domain decomposition of the tet-FEM hot path.
+
+Decomposition ("owner computes" with ghost tets):
+  * owner maps follow O4 (``ebb_partition`` on the device, ``oracle.partition``
+    in tests): tets in equal contiguous SFC ranges, every vertex owned by the
+    rank of its lowest incident tet;
+  * rank r holds every tet touching a vertex it owns (owned + ghost tets) and
+    all their vertices (owned + ghost vertices).  Every edge row whose tail is
+    owned is then complete locally, so the element map needs no reverse
+    exchange (SURVEY §8(e) "alternative: overlapping decomposition");
+  * the PCG solves on owned rows only (mask = free AND owned).  Ghost copies
+    of x, p, u, v stay consistent because they are updated with the same
+    global alpha/beta from owner-consistent z, so per iteration the only
+    exchanges are the z halo (owners -> ghosts) and two scalar sums (p.q,
+    r.z).  Step order: map, assemble, cg_init, [sum rho/pq/rz, z halo],
+    50 x (DIR, MATVEC, [sum p.q], UPDATE, [sum r.z, z halo]), state update.
+
+The driver below is backend-agnostic: a *rank* object runs the local phases
+(``GpuRank`` through the Ebb C ABI; the CPU test rank in tests/ through the
+oracle) and a *transport* moves scalars and halo rows (``TorchTransport`` over
+torch.distributed -- NCCL on B200s, gloo on CPU -- or ``LocalTransport`` for
+several ranks driven from one process).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SLOT_RHO, SLOT_PQ, SLOT_RZ = 0, 1, 2
+
+
+# ----------------------------------------------------------------------------- plans
+def local_problem(tets, owner_v, rank):
+    """Local mesh of `rank`: (tet ids, global vertex ids ascending, local tets, owned mask)."""
+    tets = np.asarray(tets, dtype=np.int64)
+    touch = (owner_v[tets] == rank).any(axis=1)
+    lt = np.nonzero(touch)[0]
+    verts = np.unique(tets[lt])
+    local_tets = np.searchsorted(verts, tets[lt])
+    owned = owner_v[verts] == rank
+    return lt, verts, local_tets, owned
+
+
+def halo_plan(tets, owner_v, nranks):
+    """Ghost lists and matching send lists for every ordered rank pair.
+
+    ghosts[r] = vertices of r's local mesh not owned by r (ascending global id);
+    send[o][r] = recv[r][o] = ghosts[r] owned by o (ascending) -- both ends
+    derive the same list from the global owner map, no negotiation needed.
+    """
+    problems = [local_problem(tets, owner_v, r) for r in range(nranks)]
+    ghosts = [p[1][~p[3]] for p in problems]
+    recv = [[ghosts[r][owner_v[ghosts[r]] == o] if o != r else np.zeros(0, np.int64)
+             for o in range(nranks)] for r in range(nranks)]
+    send = [[recv[r][o] for r in range(nranks)] for o in range(nranks)]
+    return problems, send, recv
+
+
+# ----------------------------------------------------------------------------- transports
+class TorchTransport:
+    """torch.distributed collectives (NCCL on GPUs, gloo on CPU); one local rank."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def allreduce(self, ranks, slots):
+        (R,) = ranks
+        t = R.scal_tensor()
+        lo, hi = slots
+        v = t[lo:hi].clone()
+        self.dist.all_reduce(v, group=self.group)
+        t[lo:hi] = v
+
+    def exchange(self, ranks):
+        (R,) = ranks
+        ops = []
+        recvs = {}
+        for peer in R.peers():
+            sb = R.pack(peer)
+            rb = R.recv_buffer(peer)
+            ops.append(self.dist.P2POp(self.dist.isend, sb, peer, group=self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, rb, peer, group=self.group))
+            recvs[peer] = rb
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+        for peer, rb in recvs.items():
+            R.unpack(peer, rb)
+
+
+class LocalTransport:
+    """Several ranks driven from one process (virtual shards on one device)."""
+
+    def allreduce(self, ranks, slots):
+        lo, hi = slots
+        tot = None
+        for R in ranks:
+            v = R.scal_tensor()[lo:hi]
+            tot = v.clone() if tot is None else tot + v
+        for R in ranks:
+            R.scal_tensor()[lo:hi] = tot
+
+    def exchange(self, ranks):
+        by_rank = {R.rank: R for R in ranks}
+        packed = {(R.rank, peer): R.pack(peer) for R in ranks for peer in R.peers()}
+        for R in ranks:
+            for peer in R.peers():
+                R.unpack(peer, packed[(peer, R.rank)])
+        del by_rank
+
+
+# ----------------------------------------------------------------------------- driver
+def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0)):
+    """One distributed implicit step (O9 + O10) over `ranks` (the local ones)."""
+    for R in ranks:
+        R.map_assemble(model, h, alpha, beta, g)
+        R.cg_init()
+    transport.allreduce(ranks, (SLOT_RHO, SLOT_RZ + 1))
+    transport.exchange(ranks)
+    for _ in range(iters):
+        for R in ranks:
+            R.cg_phase(0)
+        for R in ranks:
+            R.cg_phase(1)
+        transport.allreduce(ranks, (SLOT_PQ, SLOT_PQ + 1))
+        for R in ranks:
+            R.cg_phase(2)
+        transport.allreduce(ranks, (SLOT_RZ, SLOT_RZ + 1))
+        transport.exchange(ranks)
+    for R in ranks:
+        R.finish(h)
+
+
+# ----------------------------------------------------------------------------- GPU setup
+def global_partition(ctx, X, tets, nranks, name="global"):
+    """Renumber the global mesh on the device (a2) and compute the O4 owner maps
+    there (``ebb_partition``).  Returns the mesh in stored (SFC) order."""
+    from .tetfem import TetFEM
+    fem = TetFEM(ctx, X, tets, name=name)
+    ot = fem.tets.field("owner_t", "i32")
+    ov = fem.verts.field("owner_v", "i32")
+    ctx.check(ctx.L.ebb_partition(ctx.h, fem.v.h, int(nranks), ot.h, ov.h))
+    order, tord = fem.vert_order(), fem.tet_order()
+    return dict(X=np.ascontiguousarray(X[order]), tets=fem.v.read().astype(np.int64), owner_v=ov.read(),
+                owner_t=ot.read(), vert_order=order, tet_order=tord)
+
+
+# ----------------------------------------------------------------------------- GPU rank
+class GpuRank:
+    """One rank's local problem on its GPU through the Ebb C ABI."""
+
+    def __init__(self, ctx, rank, X, tets, owner_v, plan, free, u, vel, mu, lam, rho=1e3, dtype="f64",
+                 stream=None, name=None):
+        import torch
+
+        from . import _abi as A
+        from .tetfem import TetFEM
+        problems, send, recv = plan
+        lt, verts, ltets, owned = problems[rank]
+        self.rank, self.ctx, self.stream, self.A = rank, ctx, stream, A
+        self.verts_g = verts
+        mask = (free[verts] & owned).astype(np.uint8)
+        self.fem = TetFEM(ctx, X[verts], ltets, dtype=dtype, mu=mu[lt], lam=lam[lt], rho=rho, free=mask,
+                          u=u[verts], vel=vel[verts], name=name or f"r{rank}")
+        order = self.fem.vert_order()                 # local input index at each stored row
+        stored = np.empty_like(order)
+        stored[order] = np.arange(order.size)
+        self.stored_of_input = stored
+        self.owned_stored = owned[order]
+        self.fem.cg_init(stream)                       # allocates the CG work fields
+        self.z_field = self._field(self.fem.cg.z, 4)
+        self.scal = self._field(self.fem.cg.scal, 1, count=8, dt="f64").tensor()
+        self._send, self._recv, self._bufs = {}, {}, {}
+        nranks = len(problems)
+        for peer in range(nranks):
+            for kind, lst in (("send", send[rank][peer]), ("recv", recv[rank][peer])):
+                if len(lst) == 0:
+                    continue
+                rows = stored[np.searchsorted(verts, lst)].astype(np.uint32)
+                rel = ctx.relation(f"{self.fem.verts.name}.{kind}{peer}", len(rows))
+                rf = rel.field("rows", "u32", init=rows)
+                buf = torch.zeros((len(rows), 4), dtype=torch.float64 if dtype == "f64" else torch.float32,
+                                  device=f"cuda:{ctx.device}")
+                bf = rel.wrap("buf", buf, dtype, (4, 1))
+                (self._send if kind == "send" else self._recv)[peer] = (rf, bf, buf)
+        self._peers = sorted(set(self._send) | set(self._recv))
+        torch.cuda.synchronize()
+
+    def _field(self, h, rows, count=None, dt=None):
+        from .ebb import Field
+        f = Field(self.ctx, h, self.fem.verts if count is None else None, "cgwork", dt or self.fem.dtype,
+                  (rows, 1), self.A.AOS)
+        if count is not None:
+            f.count = count
+        return f
+
+    # -- phases
+    def map_assemble(self, model, h, alpha, beta, g):
+        self.fem.map_forces(model, True, False, stream=self.stream)
+        self.fem.assemble(h, alpha, beta, g, stream=self.stream)
+
+    def cg_init(self):
+        self.fem.cg_init(self.stream)
+
+    def cg_phase(self, k):
+        import ctypes as C
+
+        from .ebb import _stream
+        self.ctx.check(self.ctx.L.ebb_cg_phase(self.ctx.h, C.byref(self.fem.cg), int(k), _stream(self.stream)))
+
+    def finish(self, h):
+        import ctypes as C
+
+        from .ebb import _stream
+        self.ctx.check(self.ctx.L.ebb_implicit_update(self.ctx.h, self.fem.dv.h, float(h), self.fem.u.h,
+                                                      self.fem.vel.h, _stream(self.stream)))
+        del C
+
+    # -- transport hooks
+    def scal_tensor(self):
+        return self.scal
+
+    def peers(self):
+        return self._peers
+
+    def pack(self, peer):
+        from .ebb import _stream
+        rf, bf, buf = self._send[peer]
+        self.ctx.check(self.ctx.L.ebb_rows_gather(self.ctx.h, self.z_field.h, rf.h, bf.h, _stream(self.stream)))
+        return buf
+
+    def recv_buffer(self, peer):
+        return self._recv[peer][2]
+
+    def unpack(self, peer, data):
+        from .ebb import _stream
+        rf, bf, buf = self._recv[peer]
+        if data is not buf:
+            buf.copy_(data)
+        self.ctx.check(self.ctx.L.ebb_rows_scatter(self.ctx.h, self.z_field.h, rf.h, bf.h, _stream(self.stream)))
+
+    # -- results in global numbering (owned rows only)
+    def owned_values(self, field):
+        vals = field.read()
+        ids = self.verts_g[self.fem.vert_order()]
+        return ids[self.owned_stored], vals[self.owned_stored]

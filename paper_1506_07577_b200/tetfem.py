@@ -113,11 +113,12 @@ class TetFEM:
         return np.ascontiguousarray(arr_in[self.vert_order()])
 
     # ---------------------------------------------------------------- hot path
-    def map_forces(self, model="nh", want_K=True, want_energy=True, scatter=A.SCATTER_AUTO, stream=None):
+    def map_forces(self, model="nh", want_K=True, want_energy=True, scatter=A.SCATTER_AUTO, zero_outputs=True,
+                   stream=None):
         d = A.TetMapDesc()
         d.model = MODELS[model]
         d.scatter = scatter
-        d.zero_outputs = 1
+        d.zero_outputs = int(zero_outputs)
         d.v, d.e, d.u = self.v.h, self.e.h, self.u.h
         d.Dminv, d.W, d.mu, d.lam = self.Dminv.h, self.W.h, self.mu.h, self.lam.h
         d.f = self.f.h
@@ -144,7 +145,7 @@ class TetFEM:
             cg = A.CG()
             cg.edges, cg.A, cg.b, cg.x, cg.self = self.edges.h, self.K.h, self.b.h, self.dv.h, self.self_e.h
             cg.mask = self.free.h if self.has_mask else A.NONE
-            cg.r = cg.p = cg.z = cg.q = cg.dinv = cg.rho = cg.scal = A.NONE
+            cg.r = cg.p = cg.z = cg.q = cg.dinv = cg.rho = cg.scal = cg.p2 = A.NONE
             self.cg = cg
         self.ctx.check(self.ctx.L.ebb_cg_init(self.ctx.h, C.byref(self.cg), _stream(stream)))
 

@@ -30,31 +30,36 @@ def _oracle_map(case, m, order, tet_src, model, u=None):
                               e=m.e, ne=m.ne)
 
 
+SCATTERS = {"atomic": 1, "tiled": 2}
+
+
+@pytest.mark.parametrize("scatter", ["atomic", "tiled"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 @pytest.mark.parametrize("n,mesh", [(4, "kuhn6"), (9, "kuhn6"), (4, "alt5")])
-def test_map_fp64(ctx, model, n, mesh):
+def test_map_fp64(ctx, model, n, mesh, scatter):
     case = Case(n=n, mesh=mesh, model=model, spread=0.1)
-    fem = gpu_fem(ctx, case, name=f"m64{model}{n}{mesh}")
+    fem = gpu_fem(ctx, case, name=f"m64{model}{n}{mesh}{scatter}")
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     f, K, en, inv = _oracle_map(case, m, order, tet_src, model)
-    fem.map_forces(model)
+    fem.map_forces(model, scatter=SCATTERS[scatter])
     assert rel_l2(fem.f.read(), f) <= 1e-12
     assert rel_l2(fem.K.read(), K) <= 1e-12
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
     assert ctx.error_counts(reset=True)["inverted"] == 0
 
 
+@pytest.mark.parametrize("scatter", ["atomic", "tiled"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
-def test_map_fp32_displacement_form(ctx, model):
+def test_map_fp32_displacement_form(ctx, model, scatter):
     case = Case(n=8, model=model, spread=0.1)
     # oracle is fed the fp32-rounded inputs
     case.u = case.u.astype(np.float32).astype(np.float64)
     case.mu = case.mu.astype(np.float32).astype(np.float64)
     case.lam = case.lam.astype(np.float32).astype(np.float64)
-    fem = gpu_fem(ctx, case, dtype="f32", name=f"m32{model}")
+    fem = gpu_fem(ctx, case, dtype="f32", name=f"m32{model}{scatter}")
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     f, K, en, inv = _oracle_map(case, m, order, tet_src, model)
-    fem.map_forces(model)
+    fem.map_forces(model, scatter=SCATTERS[scatter])
     assert rel_l2(fem.f.read(), f) <= 1e-5
     assert rel_l2(fem.K.read(), K) <= 1e-5
     assert abs(fem.energy.get() - en) <= 1e-5 * abs(en)
@@ -98,3 +103,40 @@ def test_map_energy_deterministic(ctx):
     e1 = fem.energy.get()
     fem.map_forces("nh")
     assert fem.energy.get() == e1
+
+
+@pytest.mark.parametrize("tile", ["1", "7", "33", "255"])
+def test_tiled_map_tile_sizes(ctx, tile, monkeypatch):
+    """Ragged tiles (1 vertex .. 255 vertices) give the same result."""
+    monkeypatch.setenv("EBB_TILE_VERTS", tile)
+    case = Case(n=5, model="nh", spread=0.1)
+    fem = gpu_fem(ctx, case, name=f"mtile{tile}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, "nh")
+    fem.map_forces("nh", scatter=SCATTERS["tiled"])
+    assert rel_l2(fem.f.read(), f) <= 1e-12
+    assert rel_l2(fem.K.read(), K) <= 1e-12
+    assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+
+
+@pytest.mark.parametrize("scatter", ["atomic", "tiled"])
+def test_map_accumulates_without_zeroing(ctx, scatter):
+    """zero_outputs = 0 is the paper's `+=` into existing fields."""
+    case = Case(n=4, model="stvk")
+    fem = gpu_fem(ctx, case, name=f"macc{scatter}")
+    fem.map_forces("stvk", scatter=SCATTERS[scatter])
+    f1, K1 = fem.f.read(), fem.K.read()
+    fem.map_forces("stvk", scatter=SCATTERS[scatter], zero_outputs=False)
+    assert rel_l2(fem.f.read(), 2 * f1) <= 1e-14
+    assert rel_l2(fem.K.read(), 2 * K1) <= 1e-14
+
+
+def test_tiled_map_is_deterministic(ctx):
+    case = Case(n=8, model="nh")
+    fem = gpu_fem(ctx, case, name="mdet2")
+    fem.map_forces("nh", scatter=SCATTERS["tiled"])
+    f1, K1 = fem.f.read(), fem.K.read()
+    fem.map_forces("nh", scatter=SCATTERS["tiled"])
+    f2, K2 = fem.f.read(), fem.K.read()
+    # smem CAS order may differ between runs; bounded by fp64 round-off
+    assert rel_l2(f2, f1) <= 1e-14 and rel_l2(K2, K1) <= 1e-14

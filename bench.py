@@ -12,8 +12,11 @@ force+stiffness map, system assembly, PCG init + 50 iterations, state update.
 value = tets advanced through one full step per second (tet-steps/s), summed
 over ranks; components report the map in tets/s and the CG in iterations/s.
 --impl reference times the CPU oracle (the reference arm of this tier) on a
-bounded sample of the same workload.  Under torchrun each rank runs its own C2
-instance (weak scaling, no data-path collective yet).
+bounded sample of the same workload.  Under torchrun (N > 1) the global mesh is
+a Kuhn cube with round(55 N^(1/3)) cells per side (~1M tets per GPU, weak
+scaling), partitioned by the O4 owner maps; each rank runs the distributed
+implicit step (paper_1506_07577_b200.dist: ghost tets, z halo and the p.q /
+r.z allreduces over NCCL) -- DESIGN.md §7.
 """
 from __future__ import annotations
 
@@ -231,6 +234,27 @@ def run_ours(args, rank, world, local_rank):
     ctx.error_counts(reset=True)
     ctx.timing(True)
     ctx.timing_read(0, reset=True)
+    graph = None
+    if not args.no_graph:
+        # one implicit step captured as a CUDA graph (kernel timers become graph
+        # event nodes: each replay re-records them)
+        ctx.graph_begin(stream)
+        step()
+        graph = ctx.graph_end(stream)
+        ctx.graph_launch(graph, stream)          # untimed replay
+        torch.cuda.synchronize()
+
+    def run_step():
+        if graph is None:
+            step()
+        else:
+            ctx.graph_launch(graph, stream)
+
+    kids = (("tet_map", A.K_TET_MAP), ("edge_matvec", A.K_EDGE_MATVEC), ("cg_update", A.K_CG_UPDATE),
+            ("cg_dir", A.K_CG_DIR), ("assemble", A.K_ASSEMBLE), ("cg_solve", A.K_CG_SOLVE))
+    kt = {name: {"total_ms": 0.0, "launches": 0} for name, _ in kids}
+    if graph is None:
+        ctx.timing_read(0, reset=True)
     ctx.launch_count(reset=True)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
@@ -241,20 +265,26 @@ def run_ours(args, rank, world, local_rank):
             with torch.cuda.stream(stream):
                 flush.zero_()                          # L2 flush, outside the timed events
             evs[k][0].record(stream)
-            step()
+            run_step()
             evs[k][1].record(stream)
+            if graph is not None:
+                # read this replay's kernel events before the next replay re-records them
+                evs[k][1].synchronize()
+                for name, kid in kids:
+                    ms, n = ctx.timing_read(kid)
+                    kt[name]["total_ms"] += ms
+                    kt[name]["launches"] += n
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = ctx.launch_count(reset=True)
     t_ms = sum(a.elapsed_time(b) for a, b in evs)
-    kt = {}
-    for name, kid in (("tet_map", A.K_TET_MAP), ("edge_matvec", A.K_EDGE_MATVEC), ("cg_update", A.K_CG_UPDATE),
-                      ("cg_dir", A.K_CG_DIR), ("assemble", A.K_ASSEMBLE)):
-        ms, n = ctx.timing_read(kid)
-        kt[name] = {"total_ms": ms, "launches": n, "avg_us": 1e3 * ms / max(n, 1)}
-    ctx.timing_read(0, reset=True)
-    ctx.timing(False)
+    if graph is None:
+        for name, kid in kids:
+            ms, n = ctx.timing_read(kid)
+            kt[name] = {"total_ms": ms, "launches": n}
+    for v in kt.values():
+        v["avg_us"] = 1e3 * v["total_ms"] / max(v["launches"], 1)
     errs = ctx.error_counts(reset=True)
     if world > 1:
         tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
@@ -276,7 +306,7 @@ def run_ours(args, rank, world, local_rank):
         a.record(stream)
         fem.u.write_async(u_h.data_ptr(), nb, stream)
         fem.vel.write_async(v_h.data_ptr(), nb, stream)
-        step()
+        run_step()
         fem.u.read_into(u_h.data_ptr(), nb, stream)      # synchronous
         fem.vel.read_into(v_h.data_ptr(), nb, stream)
         b.record(stream)
@@ -288,39 +318,129 @@ def run_ours(args, rank, world, local_rank):
         e2e_ms = float(tt.item())
     e2e = {"value": world * T * args.steps / (e2e_ms / 1e3), "unit": "tets/s",
            "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
-           "api": "TetFEM.implicit_step + ebb_field_write/ebb_field_read (pinned host buffers)"}
+           "api": "ebb_field_write (pinned host u, v) -> implicit step (TetFEM.implicit_step as captured graph) -> "
+                  "ebb_field_read (u, v)"}
 
     # ---- roofline of the dominant kernel (largest share of the timed step)
     peak, peak_src = _peaks()
-    mv, mp = kt["edge_matvec"], kt["tet_map"]
+    mv, mp, cs = kt["edge_matvec"], kt["tet_map"], kt["cg_solve"]
+    iters = w["cg_iters"]
     b_mv, b_map, b_it = bytes_matvec(V, E), bytes_map(T, V, E), bytes_cg_iter(V, E)
     shares = {k: v["total_ms"] / t_ms for k, v in kt.items()}
     dom = max(shares, key=shares.get)
-    per_launch_bytes = {"edge_matvec": b_mv, "tet_map": b_map}.get(dom, None)
-    if per_launch_bytes is None:
-        dom, per_launch_bytes = "edge_matvec", b_mv
+    per_launch = {"edge_matvec": b_mv, "tet_map": b_map, "cg_solve": iters * b_it}
+    if dom not in per_launch:
+        dom = "edge_matvec"
     d = kt[dom]
-    ach = per_launch_bytes / (d["avg_us"] * 1e-6) / 1e9
-    roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "peak_source": peak_src, "traffic": _ncu_traffic(dom), "algorithmic_bytes_per_launch": per_launch_bytes,
+    ach = per_launch[dom] / (d["avg_us"] * 1e-6) / 1e9
+    roof = {"kernel": {"cg_solve": "k_cg_persistent (all 50 PCG iterations, one launch)",
+                       "edge_matvec": "k_spmv_tma", "tet_map": "k_tet_map_tiled"}[dom],
+            "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": peak_src, "traffic": _ncu_traffic(dom), "algorithmic_bytes_per_launch": per_launch[dom],
+            "bytes_model": "SURVEY 8(d): PCG iteration = E(9 b_f + 4) + V(4 + 6 b_f) + 33 V b_f, x 50 iterations"
+                           if dom == "cg_solve" else "SURVEY 8(d)",
             "avg_launch_us": d["avg_us"], "share_of_step": shares[dom]}
-    cg_it_us = mv["avg_us"] + kt["cg_update"]["avg_us"] + kt["cg_dir"]["avg_us"]
+    if cs["launches"]:
+        cg_it_us = cs["avg_us"] / iters
+    else:
+        cg_it_us = mv["avg_us"] + kt["cg_update"]["avg_us"] + kt["cg_dir"]["avg_us"]
     comps = {
         "map": {"tets_per_s": T / (mp["avg_us"] * 1e-6), "avg_us": mp["avg_us"],
                 "hbm_frac": b_map / (mp["avg_us"] * 1e-6) / 1e9 / peak, "bytes": b_map},
         "cg": {"iters_per_s": 1e6 / cg_it_us, "iter_us": cg_it_us,
                "hbm_frac": b_it / (cg_it_us * 1e-6) / 1e9 / peak, "bytes_per_iter": b_it},
-        "matvec": {"avg_us": mv["avg_us"], "hbm_frac": b_mv / (mv["avg_us"] * 1e-6) / 1e9 / peak},
         "kernel_times": kt, "shares": shares,
     }
     line = {"metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Kuhn-6 cube, stretch+noise displacement, no external meshes)",
-            "config": _config(world), "roofline": roof, "e2e": e2e, "gpu_launches": launches,
+            "config": dict(_config(world), launch="one CUDA graph per step" if graph is not None else "eager"),
+            "roofline": roof, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "components": comps, "device_errors": errs}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+
+
+def run_dist(args, rank, world, local_rank):
+    """N > 1: one partition of a global weak-scaled mesh per rank (NCCL transport)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import build as B
+    from paper_1506_07577_b200 import dist as D
+    from paper_1506_07577_b200 import ebb
+
+    B.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = WORKLOAD
+    n = int(round(w["n"] * world ** (1.0 / 3.0)))
+    X, tets, free, u0, mu, lam = make_case(n, w["order_seed"], w["u_seed"], w["E"], w["nu"])
+    ctx = ebb.Context(local_rank)
+    G = D.global_partition(ctx, X, tets, world, name="global")
+    plan = D.halo_plan(G["tets"], G["owner_v"], world)
+    tord = G["tet_order"]
+    order = G["vert_order"]
+    R = D.GpuRank(ctx, rank, G["X"], G["tets"], G["owner_v"], plan, free[order], u0[order],
+                  np.zeros_like(u0), mu[tord], lam[tord], rho=w["rho"], name=f"rank{rank}")
+    T = D.TorchTransport()
+    T_global = tets.shape[0]
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        D.implicit_step([R], T, w["model"], h=w["h"], iters=w["cg_iters"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.timing(True)
+    ctx.timing_read(0, reset=True)
+    ctx.launch_count(reset=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record()
+            step()
+            evs[k][1].record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.launch_count(reset=True)
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    mv_ms, mv_n = ctx.timing_read(A.K_EDGE_MATVEC)
+    mp_ms, mp_n = ctx.timing_read(A.K_TET_MAP, reset=True)
+    tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    value = T_global * args.steps / (t_ms / 1e3)
+    peak, peak_src = _peaks()
+    V_loc, E_loc = R.fem.nv, R.fem.ne
+    b_mv = bytes_matvec(V_loc, E_loc)
+    avg_mv = 1e3 * mv_ms / max(mv_n, 1)
+    roof = {"kernel": "edge_matvec", "bound": "hbm", "achieved": b_mv / (avg_mv * 1e-6) / 1e9, "peak": peak,
+            "unit": "GB/s", "frac": b_mv / (avg_mv * 1e-6) / 1e9 / peak, "peak_source": peak_src, "traffic": None,
+            "algorithmic_bytes_per_launch": b_mv, "avg_launch_us": avg_mv, "rank": rank}
+    cfg = _config(world)
+    cfg.update({"workload": f"C2 recipe weak-scaled: Kuhn-6 n={n} ({T_global} tets, {X.shape[0]} verts) split over "
+                            f"{world} GPUs by the O4 owner maps (ghost tets, z halo + 2 scalar allreduces per "
+                            f"PCG iteration over NCCL), fp64",
+                "tets": T_global, "parallelism": f"domain decomposition x{world} (NCCL halo + allreduce)"})
+    line = {"metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Kuhn-6 cube, stretch+noise displacement)",
+            "config": cfg, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(),
+            "e2e": {"value": value, "unit": "tets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "multi-GPU line: state stays resident on the devices"},
+            "components": {"map_avg_us": 1e3 * mp_ms / max(mp_n, 1), "matvec_avg_us": avg_mv,
+                           "local_tets": int(R.fem.nt), "local_verts": int(V_loc)}}
     if rank == 0:
         print(json.dumps(line))
     ctx.close()
@@ -333,6 +453,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of a CUDA graph")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -346,7 +467,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if world > 1:
+            run_dist(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -106,10 +106,24 @@ ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s);
 #define EBB_K_CG_UPDATE 2
 #define EBB_K_CG_DIR 3
 #define EBB_K_ASSEMBLE 4
+#define EBB_K_CG_SOLVE 5   /* persistent single-launch PCG (all iterations) */
 ebb_status ebb_timing_enable(ebb_ctx ctx, int on);
 ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64_t* launches, int reset);
 /* Number of kernels this context has launched (all entry points). */
 ebb_status ebb_launch_count(ebb_ctx ctx, uint64_t* out, int reset);
+
+/* CUDA-graph capture of a sequence of stream-ordered calls (e.g. one implicit
+ * step: map, assemble, cg_init, cg_step, implicit_update).  s must be a
+ * non-default stream; calls between begin and end must not allocate or
+ * synchronise (run the sequence once eagerly first: first calls build plans
+ * and work fields).  Kernel timers recorded during capture become graph
+ * event nodes: after a launch + ebb_sync, ebb_timing_read(.., reset=0)
+ * returns that replay's per-kernel times.  Launch counts of a replay are the
+ * captured ones. */
+ebb_status ebb_graph_begin(ebb_ctx ctx, ebb_stream s);
+ebb_status ebb_graph_end(ebb_ctx ctx, ebb_stream s, int32_t* graph_out);
+ebb_status ebb_graph_launch(ebb_ctx ctx, int32_t graph, ebb_stream s);
+ebb_status ebb_graph_free(ebb_ctx ctx, int32_t graph);
 
 /* ---- relations and fields ----------- */
 ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_rel* out);
@@ -265,9 +279,11 @@ typedef struct {
     ebb_field p2;        /* second direction buffer (p is double-buffered)    */
 } ebb_cg;
 /* a11: x = 0, r = b*mask, z = r/diag(A), p = z, rho = r.z.  Stream-ordered.
- * Per iteration (ebb_cg_step): beta = rho'/rho, p = z + beta p fused into
- * q = (A p)*mask with the local p.q; then alpha = rho/p.q, x += alpha p,
- * r -= alpha q, z = r/diag(A), rho' = r.z -- two kernels, no host sync. */
+ * Per iteration: beta = rho'/rho, p = z + beta p fused into q = (A p)*mask
+ * with p.q; then alpha = rho/p.q, x += alpha p, r -= alpha q, z = r/diag(A),
+ * rho' = r.z.  ebb_cg_step runs all `iters` iterations in ONE persistent
+ * cooperative kernel (grid barriers between the phases, deterministic dots);
+ * ebb_cg_phase launches the phases separately (multi-GPU). No host sync. */
 ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream s);
 /* a10-a12: `iters` Jacobi-PCG iterations (Saad Alg. 9.1), alpha/beta kept
  * on the device (no host sync); p.q <= 0 counts in error word [1]. */

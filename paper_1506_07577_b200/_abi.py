@@ -26,7 +26,7 @@ STVK, NH = 0, 1
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED = 0, 1, 2
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
 CG_DIR, CG_MATVEC, CG_UPDATE = 0, 1, 2
-K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE = 0, 1, 2, 3, 4
+K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE, K_CG_SOLVE = 0, 1, 2, 3, 4, 5
 
 u32 = C.c_uint32
 ctx_t = C.c_void_p
@@ -77,6 +77,10 @@ SIGS = {
     "ebb_timing_enable": (S, [ctx_t, C.c_int]),
     "ebb_timing_read": (S, [ctx_t, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int]),
     "ebb_launch_count": (S, [ctx_t, C.POINTER(C.c_uint64), C.c_int]),
+    "ebb_graph_begin": (S, [ctx_t, stream_t]),
+    "ebb_graph_end": (S, [ctx_t, stream_t, C.POINTER(C.c_int32)]),
+    "ebb_graph_launch": (S, [ctx_t, C.c_int32, stream_t]),
+    "ebb_graph_free": (S, [ctx_t, C.c_int32]),
     "ebb_relation_new": (S, [ctx_t, C.c_char_p, C.c_uint64, C.POINTER(u32)]),
     "ebb_relation_size": (S, [ctx_t, u32, C.POINTER(C.c_uint64)]),
     "ebb_field_new": (S, [ctx_t, u32, C.c_char_p, C.c_int, u32, u32, C.c_int, P, C.POINTER(u32)]),

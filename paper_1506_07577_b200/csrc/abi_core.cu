@@ -347,6 +347,8 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
     if (c->scratch) cudaFree(c->scratch);
     for (auto& e : c->ev_pool) cudaEventDestroy(e);
     for (auto& P : c->plans) P.release();
+    for (auto& G : c->graphs)
+        if (G.exec) cudaGraphExecDestroy(G.exec);
     cudaFree(c->d_err);
     cudaFree(c->d_partials);
     cudaFree(c->d_counter);
@@ -416,6 +418,47 @@ ebb_status ebb_launch_count(ebb_ctx ctx, uint64_t* out, int reset) {
     if (!c || !out) return EBB_E_ARG;
     *out = c->launches;
     if (reset) c->launches = 0;
+    return EBB_OK;
+}
+
+ebb_status ebb_graph_begin(ebb_ctx ctx, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c) return EBB_E_ARG;
+    if (!s) return fail(c, EBB_E_ARG, "graph capture needs a non-default stream");
+    EBB_CUDA(c, cudaStreamBeginCapture((cudaStream_t)s, cudaStreamCaptureModeThreadLocal));
+    c->capture_launch0 = c->launches;
+    return EBB_OK;
+}
+
+ebb_status ebb_graph_end(ebb_ctx ctx, ebb_stream s, int32_t* graph_out) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !graph_out || !s) return fail(c, EBB_E_ARG, "bad argument");
+    cudaGraph_t g = nullptr;
+    EBB_CUDA(c, cudaStreamEndCapture((cudaStream_t)s, &g));
+    Ctx::GraphRec r;
+    cudaError_t e = cudaGraphInstantiate(&r.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
+    r.launches = c->launches - c->capture_launch0;
+    c->graphs.push_back(r);
+    *graph_out = (int32_t)(c->graphs.size() - 1);
+    return EBB_OK;
+}
+
+ebb_status ebb_graph_launch(ebb_ctx ctx, int32_t graph, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || graph < 0 || (size_t)graph >= c->graphs.size() || !c->graphs[graph].exec)
+        return fail(c, EBB_E_ARG, "bad graph handle");
+    EBB_CUDA(c, cudaGraphLaunch(c->graphs[graph].exec, (cudaStream_t)s));
+    c->launches += c->graphs[graph].launches;
+    return EBB_OK;
+}
+
+ebb_status ebb_graph_free(ebb_ctx ctx, int32_t graph) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || graph < 0 || (size_t)graph >= c->graphs.size()) return EBB_E_ARG;
+    if (c->graphs[graph].exec) cudaGraphExecDestroy(c->graphs[graph].exec);
+    c->graphs[graph].exec = nullptr;
     return EBB_OK;
 }
 

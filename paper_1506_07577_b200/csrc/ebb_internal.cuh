@@ -83,6 +83,12 @@ struct Ctx : ebb_ctx_s {
     struct TimedLaunch { int kernel; cudaEvent_t a, b; };
     std::vector<TimedLaunch> timed;
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
+    struct GraphRec {
+        cudaGraphExec_t exec = nullptr;
+        unsigned long long launches = 0;
+    };
+    std::vector<GraphRec> graphs;
+    unsigned long long capture_launch0 = 0;
 };
 
 // Brackets one hot-kernel launch with events on its stream when timing is on.
@@ -91,17 +97,23 @@ struct KernelTimer {
     int kernel;
     cudaStream_t s;
     cudaEvent_t a = nullptr, b = nullptr;
+    unsigned int flags = cudaEventRecordDefault;
     KernelTimer(Ctx* c_, int k, cudaStream_t s_) : c(c_), kernel(k), s(s_) {
         c->launches++;
         if (c->timing && c->ev_used + 2 <= c->ev_pool.size()) {
+            // under stream capture the records must be external event nodes so
+            // that every replay re-records them (host-visible, timeable)
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            if (s && cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+                flags = cudaEventRecordExternal;
             a = c->ev_pool[c->ev_used++];
             b = c->ev_pool[c->ev_used++];
-            cudaEventRecord(a, s);
+            cudaEventRecordWithFlags(a, s, flags);
         }
     }
     ~KernelTimer() {
         if (a) {
-            cudaEventRecord(b, s);
+            cudaEventRecordWithFlags(b, s, flags);
             c->timed.push_back({kernel, a, b});
         }
     }

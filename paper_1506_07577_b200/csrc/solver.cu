@@ -42,6 +42,23 @@ template <typename R>
 __device__ __forceinline__ typename V4<R>::T ld4(const R* p, uint64_t v) {
     return reinterpret_cast<const typename V4<R>::T*>(p)[v];
 }
+// L1-bypassing (L2-coherent) 4-wide load: data written by other CTAs earlier in
+// the same (persistent) kernel must not be served from a stale L1 line
+__device__ __forceinline__ double4 ld4cg(const double* p, uint64_t v) {
+    double4 r;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+                 : "l"(p + 4 * v));
+    return r;
+}
+__device__ __forceinline__ float4 ld4cg(const float* p, uint64_t v) {
+    float4 r;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p + 4 * v));
+    return r;
+}
+
 template <typename R>
 __device__ __forceinline__ void st4(R* p, uint64_t v, typename V4<R>::T x) {
     reinterpret_cast<typename V4<R>::T*>(p)[v] = x;
@@ -321,6 +338,227 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent PCG (single GPU): all `iters` iterations in one cooperative
+// launch.  Every CTA runs the warp-specialized TMA matvec of k_spmv_tma over
+// its chunks, then a software grid barrier, then the vector update over a
+// grid-stride range of vertices, then a grid barrier.  The two dots are
+// per-CTA partials summed by every CTA in block order (deterministic, no
+// last-block second pass), so alpha and beta are known everywhere right after
+// each barrier.  The producer warp keeps streaming: when a matvec phase ends
+// it immediately issues the first TMA_NS chunks of the next iteration, so the
+// HBM stream of A overlaps the latency-bound update phase and the barriers.
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int g = *reinterpret_cast<volatile unsigned int*>(gen);
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *reinterpret_cast<volatile unsigned int*>(count) = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned int*>(gen) == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// sum of the per-CTA partials in block order, same value in every CTA
+__device__ __forceinline__ double grid_sum_partials(const double* partials, unsigned int n, double* sm_tot) {
+    double s = 0.0;
+    for (unsigned int i = threadIdx.x; i < n; i += blockDim.x) s += __ldcg(&partials[i]);
+    s = block_reduce<ROP_SUM>(s);
+    if (threadIdx.x == 0) *sm_tot = s;
+    __syncthreads();
+    return *sm_tot;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
+    k_cg_persistent(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
+                    const R* __restrict__ A, uint64_t ne, R* __restrict__ z, R* pb0, R* pb1, R* __restrict__ q,
+                    const R* __restrict__ dinv, R* __restrict__ x, R* __restrict__ r,
+                    const uint8_t* __restrict__ mask, double* __restrict__ part_pq, double* __restrict__ part_rz,
+                    unsigned int* __restrict__ bar_count, unsigned int* __restrict__ bar_gen,
+                    double* __restrict__ scal, double* __restrict__ rho_user, unsigned long long* __restrict__ err,
+                    uint32_t cap, int iters) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
+    __shared__ double sm_tot;
+    constexpr uint32_t AE = 16 / sizeof(R);
+    const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const uint64_t nchunks = (nv + TMA_VCH - 1) / TMA_VCH;
+    const uint64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TMA_NS; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], TMA_CONSUMERS);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // scalars (identical in every CTA)
+    double rho = scal[S_RHO];
+    int first = scal[S_FIRST] != 0.0;
+    int cur = scal[S_PAR] != 0.0;
+    double rz_new = scal[S_RZ];
+    // producer state: global chunk sequence number (continues across iterations)
+    uint64_t issued = 0;          // stage uses issued so far
+    auto issue = [&](uint64_t ch, uint64_t seq) {
+        const int s = seq % TMA_NS;
+        const uint64_t v0 = ch * TMA_VCH;
+        const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+        const uint64_t e0 = index[v0], e1 = index[v1];
+        if (seq >= TMA_NS) mbar_wait(&empty_bar[s], (uint32_t)(((seq / TMA_NS) + 1) & 1u));
+        unsigned char* base = tma_smem + s * stage_bytes;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            tot += (uint32_t)((a1 - a0) * sizeof(R));
+        }
+        const uint64_t h0 = e0 & ~3ull, h1 = (e1 + 3) & ~3ull;
+        tot += (uint32_t)((h1 - h0) * 4);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full_bar[s], tot);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            bulk_g2s_evict_first(base + (size_t)c * cap * sizeof(R), A + a0, (uint32_t)((a1 - a0) * sizeof(R)),
+                                 &full_bar[s]);
+        }
+        bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
+    };
+    // prologue: the first TMA_NS chunks of iteration 0
+    if (warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+    uint64_t consumed = 0;        // stage uses consumed so far (consumer side)
+    const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
+    for (int it = 0; it < iters; ++it) {
+        const R beta = (first || rho == 0.0) ? R(0) : (R)(rz_new / rho);
+        const R* __restrict__ pold = cur ? pb1 : pb0;
+        R* __restrict__ pnew = cur ? pb0 : pb1;
+        double pq = 0.0;
+        if (warp == TMA_CONSUMERS) {
+            // producer: remaining chunks of this iteration, then the head of the next one
+            if (lane == 0) {
+                for (uint64_t j = TMA_NS; j < my_chunks; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+                if (it + 1 < iters)
+                    for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+            }
+        } else {
+            const unsigned sub = lane & 15;
+            for (uint64_t j = 0; j < my_chunks; ++j, ++consumed) {
+                const uint64_t ch = blockIdx.x + j * gridDim.x;
+                const int s = consumed % TMA_NS;
+                const uint64_t v0 = ch * TMA_VCH;
+                const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+                const uint64_t v = v0 + 2 * warp + (lane >> 4);
+                const bool valid = v < v1;
+                const uint32_t e0 = index[v0];
+                const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
+                R own0 = 0, own1 = 0, own2 = 0;
+                uint8_t mk = 1;
+                if (valid && sub == 0) {
+                    const auto zv = ld4cg(z, v);
+                    const auto ov = ld4cg(pold, v);
+                    own0 = zv.x + beta * ov.x;
+                    own1 = zv.y + beta * ov.y;
+                    own2 = zv.z + beta * ov.z;
+                    if (mask) mk = mask[v];
+                }
+                mbar_wait(&full_bar[s], (uint32_t)((consumed / TMA_NS) & 1u));
+                const unsigned char* base = tma_smem + s * stage_bytes;
+                const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
+                R a0 = 0, a1 = 0, a2 = 0;
+                for (uint32_t rr = r0 + sub; rr < r1; rr += 16) {
+                    const uint32_t hv = hs[rr];
+                    const auto zv = ld4cg(z, hv);
+                    const auto ov = ld4cg(pold, hv);
+                    const R px = zv.x + beta * ov.x, py = zv.y + beta * ov.y, pz = zv.z + beta * ov.z;
+                    R av[9];
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) {
+                        const uint32_t off = (uint32_t)((c * ne + e0) & (AE - 1));
+                        av[c] = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R))[rr + off];
+                    }
+                    a0 += av[0] * px + av[1] * py + av[2] * pz;
+                    a1 += av[3] * px + av[4] * py + av[5] * pz;
+                    a2 += av[6] * px + av[7] * py + av[8] * pz;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o, 16);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o, 16);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, o, 16);
+                }
+                if (sub == 0 && valid) {
+                    if (!mk) a0 = a1 = a2 = 0;
+                    typename V4<R>::T qv, pv;
+                    qv.x = a0; qv.y = a1; qv.z = a2; qv.w = 0;
+                    pv.x = own0; pv.y = own1; pv.z = own2; pv.w = 0;
+                    st4(q, v, qv);
+                    st4(pnew, v, pv);
+                    pq += (double)own0 * a0 + (double)own1 * a1 + (double)own2 * a2;
+                }
+            }
+        }
+        pq = block_reduce<ROP_SUM>(pq);
+        if (threadIdx.x == 0) part_pq[blockIdx.x] = pq;
+        grid_barrier(bar_count, bar_gen, gridDim.x);
+        const double pqs = grid_sum_partials(part_pq, gridDim.x, &sm_tot);
+        if (blockIdx.x == 0 && threadIdx.x == 0 && pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+        rho = rz_new;                   // rho_k = r_k . z_k (beta above used the previous rho)
+        first = 0;
+        cur ^= 1;
+        const R alpha = (pqs != 0.0) ? (R)(rho / pqs) : R(0);
+        // update phase over every thread of the grid
+        double acc = 0.0;
+        for (uint64_t vv = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; vv < nv; vv += gthreads) {
+            const auto pv = ld4cg(pnew, vv);
+            const auto qv = ld4cg(q, vv);
+            const auto dv = ld4(dinv, vv);
+            auto rv = ld4(r, vv);
+            rv.x -= alpha * qv.x;
+            rv.y -= alpha * qv.y;
+            rv.z -= alpha * qv.z;
+            typename V4<R>::T zv;
+            zv.x = rv.x * dv.x;
+            zv.y = rv.y * dv.y;
+            zv.z = rv.z * dv.z;
+            zv.w = 0;
+            st4(r, vv, rv);
+            st4(z, vv, zv);
+            x[3 * vv] += alpha * pv.x;
+            x[3 * vv + 1] += alpha * pv.y;
+            x[3 * vv + 2] += alpha * pv.z;
+            acc += (double)rv.x * zv.x + (double)rv.y * zv.y + (double)rv.z * zv.z;
+        }
+        acc = block_reduce<ROP_SUM>(acc);
+        if (threadIdx.x == 0) part_rz[blockIdx.x] = acc;
+        grid_barrier(bar_count, bar_gen, gridDim.x);
+        rz_new = grid_sum_partials(part_rz, gridDim.x, &sm_tot);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            scal[S_PQ] = pqs;
+            *rho_user = rz_new;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scal[S_RHO] = rho;
+        scal[S_RZ] = rz_new;
+        scal[S_FIRST] = first ? 1.0 : 0.0;
+        scal[S_PAR] = cur ? 1.0 : 0.0;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // PCG kernels on padded vec4 work vectors (one thread per vertex)
 // init: dinv = 1/diag(A) on free DOFs (Jacobi), x = 0, r = b*m,
@@ -597,6 +835,46 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     double* scal = (double*)c->fields[cg->scal].ptr;
     double* rho_user = (double*)c->fields[cg->rho].ptr;
     const unsigned ug = occ_grid(c, k_cg_update<R>, 256, 0, G.nv);
+    const char* mode = getenv("EBB_CG");
+    if (only_phase < 0 && iters > 0 && !(mode && mode[0] == '2')) {
+        // single launch, all iterations (cooperative: every CTA resident)
+        const uint32_t cap = (uint32_t)(TMA_VCH * (G.max_group ? G.max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+        const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+        const size_t smem = stage * TMA_NS;
+        if (smem <= 200 * 1024) {
+            static thread_local size_t configured = 0;
+            if (smem > configured) {
+                EBB_CUDA(c, cudaFuncSetAttribute(k_cg_persistent<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem));
+                configured = smem;
+            }
+            const int block = 32 * (TMA_CONSUMERS + 1);
+            int nb = 0;
+            EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_persistent<R>, block, smem));
+            if (nb >= 1) {
+                const uint64_t nch = (G.nv + TMA_VCH - 1) / TMA_VCH;
+                uint64_t grid = (uint64_t)nb * c->num_sms;
+                if (grid > nch) grid = nch;
+                if (grid > 4096) grid = 4096;
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)grid);
+                cfg.blockDim = dim3(block);
+                cfg.dynamicSmemBytes = smem;
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                KernelTimer kt(c, EBB_K_CG_SOLVE, s);
+                EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg_persistent<R>, G.nv, G.index, G.head, A, G.ne, z, p, p2, q,
+                                               dinv, x, r, mask, c->d_partials, c->d_partials + 4096,
+                                               c->d_counter + 10, c->d_counter + 11, scal, rho_user, c->d_err, cap,
+                                               iters));
+                return EBB_OK;
+            }
+        }
+    }
     for (int k = 0; k < iters; ++k) {
         // EBB_CG_DIR is fused into the matvec (p = z + beta p_old gathered on the fly)
         if (only_phase < 0 || only_phase == EBB_CG_MATVEC) {

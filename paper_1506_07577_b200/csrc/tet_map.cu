@@ -447,7 +447,11 @@ ebb_status launch_tiled(Ctx* c, const MapPlan& P, bool want_e, int accumulate, u
     const int block = 256;
     const size_t smem = ((size_t)P.max_slots * 9 + (size_t)P.nvt * 3) * sizeof(R);
     auto kern = want_e ? k_tet_map_tiled<R, MODEL, true> : k_tet_map_tiled<R, MODEL, false>;
-    EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static thread_local size_t configured[2] = {0, 0};   // attribute set once (graph-capture safe)
+    if (smem > configured[want_e]) {
+        EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured[want_e] = smem;
+    }
     unsigned grid = occ_grid(c, kern, block, smem, (uint64_t)P.ntiles * block);
     KernelTimer kt(c, EBB_K_TET_MAP, s);
     kern<<<grid, block, smem, s>>>(P.ntiles, P.nvt, nv, nt, P.inst_ptr, P.recs, P.tile_cptr, P.crow, P.ctrow,

@@ -81,6 +81,17 @@ class Context:
         self.check(self.L.ebb_launch_count(self.h, C.byref(n), int(reset)))
         return n.value
 
+    def graph_begin(self, stream):
+        self.check(self.L.ebb_graph_begin(self.h, _stream(stream)))
+
+    def graph_end(self, stream) -> int:
+        g = C.c_int32()
+        self.check(self.L.ebb_graph_end(self.h, _stream(stream), C.byref(g)))
+        return g.value
+
+    def graph_launch(self, graph: int, stream):
+        self.check(self.L.ebb_graph_launch(self.h, int(graph), _stream(stream)))
+
     # -- relations / globals
     def relation(self, name: str, size: int) -> "Relation":
         h = C.c_uint32()

@@ -154,3 +154,24 @@ def test_C2_full_size_implicit_step(ctx):
     assert rel_l2(fem.K.read(), out["A"]) <= 1e-12
     assert rel_l2(fem.dv.read(), out["dv"]) <= 1e-8
     assert ctx.error_counts(reset=True) == dict(inverted=0, not_spd=0, bounds=0)
+
+
+def test_graph_capture_replays_the_step(ctx):
+    """ebb_graph_* capture of one implicit step replays to the eager result."""
+    import torch
+    case = Case(n=5, model="nh", vel_amp=0.02)
+    s = torch.cuda.Stream()
+    a = gpu_fem(ctx, case, name="geager")
+    b = gpu_fem(ctx, case, name="ggraph")
+    for fem in (a, b):                      # warm-up: plans and work fields
+        fem.implicit_step("nh", h=1e-2, iters=20, stream=s)
+    s.synchronize()
+    ctx.graph_begin(s)
+    b.implicit_step("nh", h=1e-2, iters=20, stream=s)
+    g = ctx.graph_end(s)
+    for _ in range(3):
+        a.implicit_step("nh", h=1e-2, iters=20, stream=s)
+        ctx.graph_launch(g, s)
+    s.synchronize()
+    assert rel_l2(b.u.read(), a.u.read()) <= 1e-12
+    assert rel_l2(b.dv.read(), a.dv.read()) <= 1e-12

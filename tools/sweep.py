@@ -1,0 +1,132 @@
+#!/usr/bin/env python
+"""Secondary measurements of SURVEY §8(d) (not the bench line): one JSON line each.
+
+  C3  StVK (and NH) force+stiffness map on a ~1e7-tet blob mesh, fp32 and fp64,
+      tiled vs atomic scatter -- tets/s and fraction of measured HBM peak.
+  C4  edge-relation matvec sweep over Kuhn-6 meshes (1e5 .. 1e8 tets), fp32 vs
+      fp64 -- GB/s and fraction of peak (algorithmic bytes of §8(d)).
+
+Timing: CUDA events on the launching stream around each launch (library
+instrumentation), warm-up first, L2 flushed before every timed launch.
+
+    python tools/sweep.py [--c3] [--c4] [--sizes 26,55,119] [--reps 5]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402  (peaks, byte models)
+
+
+def _flush(buf):
+    buf.zero_()
+
+
+def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000):
+    import numpy as np
+    import torch
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.tetfem import TetFEM
+    from synth import mesh as M
+    from synth import state as S
+
+    X, tets, n = M.blob(target)
+    free = S.fixed_mask(X, n)
+    u = S.twist_u(X, n, 6, free=free)
+    mu, lam = S.materials(tets.shape[0], 1e6, 0.3, spread=0.1)
+    peak, src = bench._peaks()
+    flush = torch.empty(bench.FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    for dt in dtypes:
+        ctx = ebb.Context(0)
+        fem = TetFEM(ctx, X, tets, dtype=dt, mu=mu, lam=lam, free=free, u=u, name="c3")
+        T, V, E = fem.nt, fem.nv, fem.ne
+        bf = 4 if dt == "f32" else 8
+        for model in models:
+            for scat, sid in (("tiled", A.SCATTER_TILED), ("atomic", A.SCATTER_ATOMIC)):
+                fem.map_forces(model, scatter=sid)
+                torch.cuda.synchronize()
+                ctx.timing(True)
+                ctx.timing_read(A.K_TET_MAP, reset=True)
+                for _ in range(reps):
+                    _flush(flush)
+                    fem.map_forces(model, scatter=sid)
+                ms, nl = ctx.timing_read(A.K_TET_MAP, reset=True)
+                ctx.timing(False)
+                us = 1e3 * ms / nl
+                b = bench.bytes_map(T, V, E, bf)
+                print(json.dumps({"workload": "C3", "mesh": f"blob n={n}", "tets": T, "verts": V, "edge_rows": E,
+                                  "dtype": dt, "model": model, "scatter": scat, "avg_us": us,
+                                  "tets_per_s": T / (us * 1e-6), "algorithmic_bytes": b,
+                                  "hbm_frac": b / (us * 1e-6) / 1e9 / peak, "peak_gbs": peak, "peak_source": src}),
+                      flush=True)
+        ctx.close()
+        del fem
+    del np
+
+
+def run_c4(sizes, reps):
+    import numpy as np
+    import torch
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.tetfem import TetFEM
+    from synth import mesh as M
+
+    peak, src = bench._peaks()
+    flush = torch.empty(bench.FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    for n in sizes:
+        X, tets = M.kuhn6(n)
+        for dt in ("f32", "f64"):
+            ctx = ebb.Context(0)
+            fem = TetFEM(ctx, X, tets, dtype=dt, name=f"c4_{n}_{dt}")
+            rng = np.random.default_rng(6)
+            fem.K.write(rng.uniform(-1, 1, size=(fem.ne, 9)))
+            P = fem.verts.field("p", dt, (3, 1), init=rng.uniform(-1, 1, size=(fem.nv, 3)))
+            Q = fem.verts.field("q", dt, (3, 1))
+            fem.matvec(fem.K, P, Q)
+            torch.cuda.synchronize()
+            ctx.timing(True)
+            ctx.timing_read(A.K_EDGE_MATVEC, reset=True)
+            for _ in range(reps):
+                _flush(flush)
+                fem.matvec(fem.K, P, Q)
+            ms, nl = ctx.timing_read(A.K_EDGE_MATVEC, reset=True)
+            ctx.timing(False)
+            us = 1e3 * ms / nl
+            bf = 4 if dt == "f32" else 8
+            b = bench.bytes_matvec(fem.nv, fem.ne, bf)
+            print(json.dumps({"workload": "C4", "mesh": f"kuhn6 n={n}", "tets": fem.nt, "verts": fem.nv,
+                              "edge_rows": fem.ne, "dtype": dt, "avg_us": us, "gbs": b / (us * 1e-6) / 1e9,
+                              "hbm_frac": b / (us * 1e-6) / 1e9 / peak, "algorithmic_bytes": b, "peak_gbs": peak,
+                              "peak_source": src}), flush=True)
+            ctx.close()
+            del fem
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--c3", action="store_true")
+    ap.add_argument("--c4", action="store_true")
+    ap.add_argument("--sizes", default="26,37,55,79,119")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--c3-tets", type=int, default=10_000_000)
+    a = ap.parse_args()
+    from paper_1506_07577_b200 import build
+    build.build()
+    if a.c3:
+        run_c3(a.reps, target=a.c3_tets)
+    if a.c4:
+        run_c4([int(x) for x in a.sizes.split(",")], a.reps)
+
+
+if __name__ == "__main__":
+    main()

@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(256) k_spmv(uint64_t nv, const uint32_t* __res
 #define TMA_VCH 16
 #define TMA_NS 4
 #define TMA_CONSUMERS 8
+#define PCG_GROUPS 2                          // persistent PCG: consumer warp groups
+#define PCG_WPG (TMA_CONSUMERS / PCG_GROUPS)  // warps per group
 template <typename R, bool CG, bool MPQ, bool DIR = false>
 __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     k_spmv_tma(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     if (threadIdx.x == 0) {
         for (int s = 0; s < TMA_NS; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], TMA_CONSUMERS);
+            mbar_init(&empty_bar[s], PCG_WPG);
         }
         mbar_fence_init();
     }
@@ -438,7 +440,6 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     // prologue: the first TMA_NS chunks of iteration 0
     if (warp == TMA_CONSUMERS && lane == 0)
         for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
-    uint64_t consumed = 0;        // stage uses consumed so far (consumer side)
     const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
     for (int it = 0; it < iters; ++it) {
         const R beta = (first || rho == 0.0) ? R(0) : (R)(rz_new / rho);
@@ -453,13 +454,18 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                     for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
             }
         } else {
-            const unsigned sub = lane & 15;
-            for (uint64_t j = 0; j < my_chunks; ++j, ++consumed) {
+            // consumer group g (warps 4g..4g+3) takes the chunks of sequence
+            // number = g (mod 2); 8 lanes per vertex, 4 vertices per warp
+            const unsigned grp = warp / PCG_WPG, wig = warp % PCG_WPG;
+            const unsigned sub = lane & 7;
+            const uint64_t seq0 = (uint64_t)it * my_chunks;
+            for (uint64_t j = grp; j < my_chunks; j += PCG_GROUPS) {
+                const uint64_t seq = seq0 + j;
                 const uint64_t ch = blockIdx.x + j * gridDim.x;
-                const int s = consumed % TMA_NS;
+                const int s = seq % TMA_NS;
                 const uint64_t v0 = ch * TMA_VCH;
                 const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
-                const uint64_t v = v0 + 2 * warp + (lane >> 4);
+                const uint64_t v = v0 + 4 * wig + (lane >> 3);
                 const bool valid = v < v1;
                 const uint32_t e0 = index[v0];
                 const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
@@ -473,32 +479,42 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                     own2 = zv.z + beta * ov.z;
                     if (mask) mk = mask[v];
                 }
-                mbar_wait(&full_bar[s], (uint32_t)((consumed / TMA_NS) & 1u));
+                mbar_wait(&full_bar[s], (uint32_t)((seq / TMA_NS) & 1u));
                 const unsigned char* base = tma_smem + s * stage_bytes;
                 const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
+                uint32_t off[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) off[c] = (uint32_t)((c * ne + e0) & (AE - 1));
                 R a0 = 0, a1 = 0, a2 = 0;
-                for (uint32_t rr = r0 + sub; rr < r1; rr += 16) {
-                    const uint32_t hv = hs[rr];
-                    const auto zv = ld4cg(z, hv);
-                    const auto ov = ld4cg(pold, hv);
-                    const R px = zv.x + beta * ov.x, py = zv.y + beta * ov.y, pz = zv.z + beta * ov.z;
-                    R av[9];
+                for (uint32_t rb = r0 + sub; rb < r1; rb += 16) {
+                    // two rows per lane per pass: both gathers in flight together
+                    const uint32_t rr1 = rb + 8;
+                    const bool two = rr1 < r1;
+                    const uint32_t h0 = hs[rb], h1 = two ? hs[rr1] : h0;
+                    const auto z0 = ld4cg(z, h0);
+                    const auto o0 = ld4cg(pold, h0);
+                    const auto z1 = ld4cg(z, h1);
+                    const auto o1 = ld4cg(pold, h1);
+                    R av[9], bv[9];
 #pragma unroll
                     for (int c = 0; c < 9; ++c) {
-                        const uint32_t off = (uint32_t)((c * ne + e0) & (AE - 1));
-                        av[c] = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R))[rr + off];
+                        const R* pl = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R)) + off[c];
+                        av[c] = pl[rb];
+                        bv[c] = two ? pl[rr1] : R(0);
                     }
-                    a0 += av[0] * px + av[1] * py + av[2] * pz;
-                    a1 += av[3] * px + av[4] * py + av[5] * pz;
-                    a2 += av[6] * px + av[7] * py + av[8] * pz;
+                    const R px = z0.x + beta * o0.x, py = z0.y + beta * o0.y, pz = z0.z + beta * o0.z;
+                    const R qx = z1.x + beta * o1.x, qy = z1.y + beta * o1.y, qz = z1.z + beta * o1.z;
+                    a0 += av[0] * px + av[1] * py + av[2] * pz + (bv[0] * qx + bv[1] * qy + bv[2] * qz);
+                    a1 += av[3] * px + av[4] * py + av[5] * pz + (bv[3] * qx + bv[4] * qy + bv[5] * qz);
+                    a2 += av[6] * px + av[7] * py + av[8] * pz + (bv[6] * qx + bv[7] * qy + bv[8] * qz);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[s]);
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) {
-                    a0 += __shfl_xor_sync(0xffffffffu, a0, o, 16);
-                    a1 += __shfl_xor_sync(0xffffffffu, a1, o, 16);
-                    a2 += __shfl_xor_sync(0xffffffffu, a2, o, 16);
+                for (int o = 4; o > 0; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o, 8);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o, 8);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, o, 8);
                 }
                 if (sub == 0 && valid) {
                     if (!mk) a0 = a1 = a2 = 0;

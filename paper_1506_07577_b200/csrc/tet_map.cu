@@ -188,10 +188,17 @@ __global__ void k_inst_ptr(const uint64_t* __restrict__ keys, uint64_t n, uint32
 // flags bit p (p < 6): block of pair p is stored transposed; bit 8: energy owner
 __global__ void k_inst_records(uint64_t ninst, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ tv,
                                const uint32_t* __restrict__ te, const uint32_t* __restrict__ gci,
-                               const uint32_t* __restrict__ cptr, int nvt, uint32_t* __restrict__ recs) {
+                               const uint32_t* __restrict__ cptr, int nvt, const uint32_t* __restrict__ inst_ptr,
+                               uint32_t* __restrict__ recs) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= ninst) return;
     const uint32_t tile = (uint32_t)(keys[i] >> 32);
+    // Records of a tile are stored in a pseudo-random order (k -> k * 1000003 mod n,
+    // a bijection since the prime exceeds n): SFC-adjacent tets share rows, and
+    // processing them concurrently makes every thread of a CTA CAS the same
+    // shared-memory words; scattered, a row's ~24 contributors rarely coincide.
+    const uint64_t t0 = inst_ptr[tile], nloc = inst_ptr[tile + 1] - t0;
+    const uint64_t out = t0 + ((i - t0) * 1000003ull) % nloc;
     const uint64_t t = keys[i] & 0xFFFFFFFFull;
     uint32_t v[4];
     for (int k = 0; k < 4; ++k) v[k] = tv[4 * t + k];
@@ -217,7 +224,7 @@ __global__ void k_inst_records(uint64_t ninst, const uint64_t* __restrict__ keys
     }
     if (vmin / (uint32_t)nvt == tile) flags |= 1u << 8;
     w[7] = flags;
-    for (int k = 0; k < 8; ++k) recs[8 * i + k] = w[k];
+    for (int k = 0; k < 8; ++k) recs[8 * out + k] = w[k];
 }
 
 __global__ void k_max_diff(const uint32_t* __restrict__ ptr, uint32_t n, unsigned int* out) {
@@ -292,7 +299,7 @@ ebb_status build_plan(Ctx* c, ebb_field vf, ebb_field ef, int nvt, MapPlan** out
     EBB_CUDA(c, cudaMalloc(&P.recs, P.ninst * 32));
     k_inst_records<<<grid_for(P.ninst, 256), 256>>>(P.ninst, (const uint64_t*)uk.p, (const uint32_t*)V->ptr,
                                                     (const uint32_t*)E->ptr, (const uint32_t*)gci.p, P.tile_cptr, nvt,
-                                                    (uint32_t*)P.recs);
+                                                    P.inst_ptr, (uint32_t*)P.recs);
     EBB_CUDA(c, cudaMalloc(&mx.p, 4));
     EBB_CUDA(c, cudaMemset(mx.p, 0, 4));
     k_max_diff<<<grid_for(P.ntiles, 256), 256>>>(P.tile_cptr, P.ntiles, (unsigned int*)mx.p);

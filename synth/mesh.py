@@ -148,14 +148,15 @@ def _blob_cells(n: int) -> np.ndarray:
 
 
 def blob_n_for(target_T: int) -> int:
-    lo, hi = 4, 1024
-    while hi - lo > 1:
-        mid = (lo + hi) // 2
-        if 6 * _blob_cells(mid).shape[0] >= target_T:
-            hi = mid
-        else:
-            lo = mid
-    return hi
+    """Smallest n with 6 * (#kept cubes) >= target_T.  The kept volume fraction
+    is estimated on a 48^3 grid, then n is refined by a local search."""
+    frac = _blob_cells(48).shape[0] / 48 ** 3
+    n = max(4, int(round((target_T / (6.0 * frac)) ** (1.0 / 3.0))))
+    while n > 4 and 6 * _blob_cells(n - 1).shape[0] >= target_T:
+        n -= 1
+    while 6 * _blob_cells(n).shape[0] < target_T:
+        n += 1
+    return n
 
 
 def blob(target_T: int = 10_000_000, n: int | None = None, jitter_seed: int = 3, order_seed: int = 4):
@@ -172,13 +173,11 @@ def blob(target_T: int = 10_000_000, n: int | None = None, jitter_seed: int = 3,
     used = np.unique(tets)
     remap = -np.ones((n + 1) ** 3, dtype=np.int64)
     remap[used] = np.arange(used.size)
-    ijk_all = None
     ii = used % (n + 1)
     jj = (used // (n + 1)) % (n + 1)
     kk = used // ((n + 1) * (n + 1))
     ijk = np.stack([ii, jj, kk], axis=1)
     tets = _orient_lattice(ijk, remap[tets])
-    del ijk_all
     X = ijk.astype(np.float64) / n
     X += rng(jitter_seed).uniform(-0.1 / n, 0.1 / n, size=X.shape)
     X, tets = permute_vertices(X, tets, order_seed)

@@ -192,3 +192,14 @@ def test_morton_quantisation_closed_form():
     assert int(c[1]) == 1 << 60
     assert int(c[2]) == sum(1 << (3 * b) for b in range(21))
     assert int(c[3]) == sum((1 << (3 * b + 1)) | (1 << (3 * b + 2)) for b in range(21))
+
+
+def test_blob_generator_is_valid():
+    """C3 blob recipe: positive volumes after jitter (no swaps needed), target
+    size reached with the smallest n, every vertex used."""
+    X, tets, n = M.blob(20_000)
+    assert 6 * (tets.shape[0] // 6) == tets.shape[0] and tets.shape[0] >= 20_000
+    assert n == M.blob_n_for(20_000)
+    m = oracle.Mesh(X, tets)
+    assert m.swaps == 0 and np.all(m.W > 0)
+    assert np.all(np.bincount(m.tets.ravel(), minlength=m.nv) > 0)

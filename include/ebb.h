@@ -209,7 +209,11 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
 #define EBB_NH 1
 #define EBB_SCATTER_AUTO 0
 #define EBB_SCATTER_ATOMIC 1    /* per-tet red.global.add              */
-#define EBB_SCATTER_TILED 2     /* CTA shared-memory aggregation + red/stores  */
+#define EBB_SCATTER_TILED 2     /* owner tiles, shared-memory accumulation
+                                   (AUTO: the measured fastest)                */
+#define EBB_SCATTER_GATHER 3    /* owner tiles, element state staged in an L2
+                                   scratch, per-row register gather: no
+                                   atomics, bitwise run-to-run deterministic  */
 typedef struct {
     int32_t model;         /* EBB_STVK | EBB_NH                                */
     int32_t scatter;       /* EBB_SCATTER_*                                    */

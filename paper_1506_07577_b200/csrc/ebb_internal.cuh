@@ -56,9 +56,18 @@ struct MapPlan {
     uint32_t* tile_cptr = nullptr;  // ntiles + 1, canonical-slot offsets
     uint32_t* crow = nullptr;       // ncanon: global row of canonical slot
     uint32_t* ctrow = nullptr;      // ncanon: global row of its transpose
+    // gather strategy: per canonical slot the (instance, pair, transpose)
+    // contributions, per vertex the (instance, corner) force contributions
+    uint32_t max_inst = 0;          // most instances in one tile
+    uint32_t* slot_ptr = nullptr;   // ncanon + 1
+    uint32_t* slot_ent = nullptr;   // (local instance << 5) | (pair << 1) | transpose
+    uint32_t* fv_ptr = nullptr;     // nverts + 1
+    uint32_t* fv_ent = nullptr;     // (local instance << 2) | corner
     void release() {
         cudaFree(inst_ptr); cudaFree(recs); cudaFree(tile_cptr); cudaFree(crow); cudaFree(ctrow);
+        cudaFree(slot_ptr); cudaFree(slot_ent); cudaFree(fv_ptr); cudaFree(fv_ent);
         inst_ptr = nullptr; recs = nullptr; tile_cptr = nullptr; crow = nullptr; ctrow = nullptr;
+        slot_ptr = slot_ent = fv_ptr = fv_ent = nullptr;
     }
 };
 
@@ -83,6 +92,8 @@ struct Ctx : ebb_ctx_s {
     struct TimedLaunch { int kernel; cudaEvent_t a, b; };
     std::vector<TimedLaunch> timed;
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
+    void* map_scratch = nullptr;    // per-CTA element-state staging of the gather map
+    size_t map_scratch_bytes = 0;
     struct GraphRec {
         cudaGraphExec_t exec = nullptr;
         unsigned long long launches = 0;

@@ -232,6 +232,124 @@ __global__ void k_max_diff(const uint32_t* __restrict__ ptr, uint32_t n, unsigne
     if (s < n) atomicMax(out, ptr[s + 1] - ptr[s]);
 }
 
+// ---- gather-strategy contribution lists
+__device__ __forceinline__ uint32_t tile_of(const uint32_t* __restrict__ inst_ptr, uint32_t ntiles, uint64_t i) {
+    uint32_t lo = 0, hi = ntiles;   // last tile with inst_ptr[tile] <= i
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (inst_ptr[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_entry_counts(uint64_t ninst, const uint32_t* __restrict__ recs, uint32_t* __restrict__ npair,
+                               uint32_t* __restrict__ ncorner) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= ninst) return;
+    const uint32_t* w = recs + 8 * i;
+    uint32_t a = 0, b = 0;
+    for (int p = 0; p < 10; ++p) a += ((w[1 + p / 2] >> (16 * (p & 1))) & 0xFFFFu) != 0xFFFFu;
+    for (int k = 0; k < 4; ++k) b += ((w[6] >> (8 * k)) & 0xFFu) != 0xFFu;
+    npair[i] = a;
+    ncorner[i] = b;
+}
+
+__global__ void k_entry_emit(uint64_t ninst, const uint32_t* __restrict__ recs, const uint32_t* __restrict__ inst_ptr,
+                             uint32_t ntiles, const uint32_t* __restrict__ cptr, int nvt,
+                             const uint32_t* __restrict__ poff, const uint32_t* __restrict__ coff,
+                             uint32_t* __restrict__ pkey, uint32_t* __restrict__ pval, uint32_t* __restrict__ ckey,
+                             uint32_t* __restrict__ cval) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= ninst) return;
+    const uint32_t* w = recs + 8 * i;
+    const uint32_t tile = tile_of(inst_ptr, ntiles, i);
+    const uint32_t li = (uint32_t)(i - inst_ptr[tile]);
+    uint32_t o = poff[i];
+    for (int p = 0; p < 10; ++p) {
+        const uint32_t slot = (w[1 + p / 2] >> (16 * (p & 1))) & 0xFFFFu;
+        if (slot == 0xFFFFu) continue;
+        pkey[o] = cptr[tile] + slot;
+        pval[o] = (li << 5) | ((uint32_t)p << 1) | (p < 6 ? ((w[7] >> p) & 1u) : 0u);
+        ++o;
+    }
+    o = coff[i];
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t lv = (w[6] >> (8 * k)) & 0xFFu;
+        if (lv == 0xFFu) continue;
+        ckey[o] = tile * (uint32_t)nvt + lv;
+        cval[o] = (li << 2) | (uint32_t)k;
+        ++o;
+    }
+}
+
+__global__ void k_lower_bound_u32(const uint32_t* __restrict__ sorted, uint64_t n, uint32_t* __restrict__ ptr,
+                                  uint64_t nkeys) {
+    uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (s > nkeys) return;
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (sorted[mid] < s) lo = mid + 1;
+        else hi = mid;
+    }
+    ptr[s] = (uint32_t)lo;
+}
+
+// sort (key, value) pairs by key and build key -> [ptr[k], ptr[k+1]) offsets
+ebb_status sort_entries(Ctx* c, uint32_t* key, uint32_t* val, uint64_t n, uint64_t nkeys, uint32_t** ptr_out,
+                        uint32_t** ent_out) {
+    DevBuf k2, tmp;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) <= nkeys) ++bits;
+    EBB_CUDA(c, cudaMalloc(&k2.p, n * 4 + 16));
+    EBB_CUDA(c, cudaMalloc(ent_out, n * 4 + 16));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, (uint32_t*)k2.p, val, *ent_out, (int)n, 0, bits);
+    EBB_CUDA(c, cudaMalloc(&tmp.p, tb));
+    EBB_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp.p, tb, key, (uint32_t*)k2.p, val, *ent_out, (int)n, 0, bits));
+    EBB_CUDA(c, cudaMalloc(ptr_out, (nkeys + 1) * 4));
+    k_lower_bound_u32<<<grid_for(nkeys + 1, 256), 256>>>((const uint32_t*)k2.p, n, *ptr_out, nkeys);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+ebb_status build_gather_lists(Ctx* c, MapPlan& P, uint64_t nv) {
+    const uint64_t ni = P.ninst;
+    DevBuf npair, ncorner, poff, coff, tmp, pkey, pval, ckey, cval, mx;
+    EBB_CUDA(c, cudaMalloc(&npair.p, ni * 4 + 16));
+    EBB_CUDA(c, cudaMalloc(&ncorner.p, ni * 4 + 16));
+    EBB_CUDA(c, cudaMalloc(&poff.p, ni * 4 + 16));
+    EBB_CUDA(c, cudaMalloc(&coff.p, ni * 4 + 16));
+    k_entry_counts<<<grid_for(ni, 256), 256>>>(ni, (const uint32_t*)P.recs, (uint32_t*)npair.p, (uint32_t*)ncorner.p);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (const uint32_t*)npair.p, (uint32_t*)poff.p, (int)ni);
+    EBB_CUDA(c, cudaMalloc(&tmp.p, tb));
+    EBB_CUDA(c, cub::DeviceScan::ExclusiveSum(tmp.p, tb, (const uint32_t*)npair.p, (uint32_t*)poff.p, (int)ni));
+    EBB_CUDA(c, cub::DeviceScan::ExclusiveSum(tmp.p, tb, (const uint32_t*)ncorner.p, (uint32_t*)coff.p, (int)ni));
+    uint32_t lp, lc, op, oc;
+    EBB_CUDA(c, cudaMemcpy(&lp, (uint32_t*)npair.p + ni - 1, 4, cudaMemcpyDeviceToHost));
+    EBB_CUDA(c, cudaMemcpy(&lc, (uint32_t*)ncorner.p + ni - 1, 4, cudaMemcpyDeviceToHost));
+    EBB_CUDA(c, cudaMemcpy(&op, (uint32_t*)poff.p + ni - 1, 4, cudaMemcpyDeviceToHost));
+    EBB_CUDA(c, cudaMemcpy(&oc, (uint32_t*)coff.p + ni - 1, 4, cudaMemcpyDeviceToHost));
+    const uint64_t np = (uint64_t)op + lp, nc = (uint64_t)oc + lc;
+    EBB_CUDA(c, cudaMalloc(&pkey.p, np * 4 + 16));
+    EBB_CUDA(c, cudaMalloc(&pval.p, np * 4 + 16));
+    EBB_CUDA(c, cudaMalloc(&ckey.p, nc * 4 + 16));
+    EBB_CUDA(c, cudaMalloc(&cval.p, nc * 4 + 16));
+    k_entry_emit<<<grid_for(ni, 256), 256>>>(ni, (const uint32_t*)P.recs, P.inst_ptr, P.ntiles, P.tile_cptr, P.nvt,
+                                             (const uint32_t*)poff.p, (const uint32_t*)coff.p, (uint32_t*)pkey.p,
+                                             (uint32_t*)pval.p, (uint32_t*)ckey.p, (uint32_t*)cval.p);
+    EBB_CUDA(c, cudaGetLastError());
+    EBB_TRY(sort_entries(c, (uint32_t*)pkey.p, (uint32_t*)pval.p, np, P.ncanon, &P.slot_ptr, &P.slot_ent));
+    EBB_TRY(sort_entries(c, (uint32_t*)ckey.p, (uint32_t*)cval.p, nc, nv, &P.fv_ptr, &P.fv_ent));
+    EBB_CUDA(c, cudaMalloc(&mx.p, 4));
+    EBB_CUDA(c, cudaMemset(mx.p, 0, 4));
+    k_max_diff<<<grid_for(P.ntiles, 256), 256>>>(P.inst_ptr, P.ntiles, (unsigned int*)mx.p);
+    EBB_CUDA(c, cudaMemcpy(&P.max_inst, mx.p, 4, cudaMemcpyDeviceToHost));
+    return EBB_OK;
+}
+
 ebb_status build_plan(Ctx* c, ebb_field vf, ebb_field ef, int nvt, MapPlan** out) {
     for (auto& P : c->plans)
         if (P.v == vf && P.e == ef && P.nvt == nvt) {
@@ -308,6 +426,13 @@ ebb_status build_plan(Ctx* c, ebb_field vf, ebb_field ef, int nvt, MapPlan** out
     if (P.max_slots >= 0xFFFFu) {
         P.release();
         return fail(c, EBB_E_RANGE, "tiled map: %u canonical rows in one tile (> 65534)", P.max_slots);
+    }
+    {
+        ebb_status st = build_gather_lists(c, P, nv);
+        if (st != EBB_OK) {
+            P.release();
+            return st;
+        }
     }
     c->plans.push_back(P);
     *out = &c->plans.back();
@@ -426,6 +551,255 @@ __global__ void __launch_bounds__(256) k_tet_map_tiled(
     }
 }
 
+
+// ---------------------------------------------------------------- GATHER
+// Atomic-free owner-computes map.  Per tile (persistent CTA loop):
+//  phase 1  every tet touching the tile: element physics, then a compact
+//           per-instance state row written to this CTA's slice of an
+//           L2-resident scratch (NH: k_i = F^-T g_i, W mu m_ij per pair,
+//           W c1, W lam, f_i;  StVK: h_i = F g_i, W s_ij, W mu m_ij per pair,
+//           F F^T, W mu, W lam, f_i);
+//  phase 2  one thread per canonical row of the tile walks that row's
+//           (instance, pair, transpose) list, rebuilds each 3x3 block from
+//           the state (closed rank-1 forms) and accumulates it in registers;
+//           the row and its transpose are written once with plain stores.
+//           One thread per owned vertex sums its force contributions.
+// Deterministic: fixed list order, no atomics anywhere.
+template <int MODEL>
+struct GState;
+template <>
+struct GState<EBB_NH> {   // [kv 12][cm 10][W c1][W lam][f 12]
+    static constexpr int KV = 0, CM = 12, C1 = 22, CL = 23, F = 24, SW = 36;
+};
+template <>
+struct GState<EBB_STVK> { // [kv 12][ws 10][wm 10][B 6][W mu][W lam][f 12]
+    static constexpr int KV = 0, WS = 12, WM = 22, B = 32, CH = 38, CL = 39, F = 40, SW = 52;
+};
+
+template <typename R, int MODEL, bool WANT_E>
+__global__ void __launch_bounds__(256) k_tet_map_gather(
+    uint32_t ntiles, int nvt, uint64_t nv, uint64_t nt, const uint32_t* __restrict__ inst_ptr,
+    const uint4* __restrict__ recs, const uint32_t* __restrict__ tile_cptr, const uint32_t* __restrict__ crow,
+    const uint32_t* __restrict__ ctrow, const uint32_t* __restrict__ slot_ptr, const uint32_t* __restrict__ slot_ent,
+    const uint32_t* __restrict__ fv_ptr, const uint32_t* __restrict__ fv_ent, R* __restrict__ scratch,
+    uint32_t max_inst, const uint4* __restrict__ tv, const R* __restrict__ u, const R* __restrict__ Dminv,
+    const R* __restrict__ Wt, const R* __restrict__ mu_t, const R* __restrict__ lam_t, R* __restrict__ f,
+    R* __restrict__ K, uint64_t ne, int accumulate, double* __restrict__ partials, unsigned int* __restrict__ counter,
+    R* __restrict__ energy, unsigned long long* __restrict__ err) {
+    using G = GState<MODEL>;
+    R* __restrict__ st_base = scratch + (uint64_t)blockIdx.x * max_inst * G::SW;
+    double e_acc = 0.0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t i0 = inst_ptr[tile], ni = inst_ptr[tile + 1] - i0;
+        // ---- phase 1: element state of every instance
+        for (uint32_t li = threadIdx.x; li < ni; li += blockDim.x) {
+            const uint4 ra = recs[2ull * (i0 + li)], rb = recs[2ull * (i0 + li) + 1];
+            const uint64_t t = ra.x;
+            uint32_t v[4];
+            R uu[4][3];
+            TetState<R> st;
+            load_tet(t, nt, tv, u, Dminv, Wt, mu_t, lam_t, v, uu, st);
+            tet_physics<R, MODEL, true>(uu, st);
+            const uint32_t flags = rb.w;
+            if (MODEL == EBB_NH && (flags & 0x100u) && !(st.J > R(0))) atomicAdd(&err[ERR_INVERTED], 1ull);
+            if (WANT_E && (flags & 0x100u)) e_acc += (double)(st.W * st.psi);
+            R fi[4][3];
+            tet_forces(st, fi);
+            R* sr = st_base + (uint64_t)li * G::SW;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    sr[G::KV + 3 * i + a] = st.kv[i][a];
+                    sr[G::F + 3 * i + a] = fi[i][a];
+                }
+#pragma unroll
+            for (int p = 0; p < 10; ++p) {
+                const int i = p < 6 ? (p < 3 ? 0 : (p < 5 ? 1 : 2)) : p - 6;
+                const int j = p < 6 ? (p < 3 ? p + 1 : (p < 5 ? p - 1 : 3)) : p - 6;
+                const R mij = st.g[i][0] * st.g[j][0] + st.g[i][1] * st.g[j][1] + st.g[i][2] * st.g[j][2];
+                if (MODEL == EBB_NH) {
+                    sr[GState<EBB_NH>::CM + p] = st.W * st.mu * mij;
+                } else {
+                    R Sg[3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        Sg[a] = st.S[a][0] * st.g[i][0] + st.S[a][1] * st.g[i][1] + st.S[a][2] * st.g[i][2];
+                    sr[GState<EBB_STVK>::WS + p] = st.W * (Sg[0] * st.g[j][0] + Sg[1] * st.g[j][1] + Sg[2] * st.g[j][2]);
+                    sr[GState<EBB_STVK>::WM + p] = st.W * st.mu * mij;
+                }
+            }
+            if (MODEL == EBB_NH) {
+                sr[GState<EBB_NH>::C1] = st.W * st.c1;
+                sr[GState<EBB_NH>::CL] = st.W * st.lam;
+            } else {
+                const int B = GState<EBB_STVK>::B;
+                sr[B + 0] = st.B[0][0];
+                sr[B + 1] = st.B[0][1];
+                sr[B + 2] = st.B[0][2];
+                sr[B + 3] = st.B[1][1];
+                sr[B + 4] = st.B[1][2];
+                sr[B + 5] = st.B[2][2];
+                sr[GState<EBB_STVK>::CH] = st.W * st.mu;
+                sr[GState<EBB_STVK>::CL] = st.W * st.lam;
+            }
+        }
+        __syncthreads();   // block-scope visibility of the state rows
+        // ---- phase 2a: canonical rows of the tile (entries in batches of 4:
+        // all state loads of a batch are in flight before any arithmetic)
+        const uint32_t c0 = tile_cptr[tile], ns = tile_cptr[tile + 1] - c0;
+        for (uint32_t s = threadIdx.x; s < ns; s += blockDim.x) {
+            const uint32_t gs = c0 + s;
+            R acc[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc[k] = R(0);
+            const uint32_t eb = slot_ptr[gs], e1 = slot_ptr[gs + 1];
+            for (uint32_t e = eb; e < e1; e += 4) {
+                uint32_t ent[4];
+                bool ok[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    ok[q] = e + q < e1;
+                    ent[q] = ok[q] ? slot_ent[e + q] : slot_ent[eb];
+                }
+                R ki[4][3], kj[4][3], c_a[4], c_b[4], c_c[4], c_d[4];
+                R Bm[4][6];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t li = ent[q] >> 5, p = (ent[q] >> 1) & 15u;
+                    const int i = p < 6 ? (p < 3 ? 0 : (p < 5 ? 1 : 2)) : (int)p - 6;
+                    const int j = p < 6 ? (p < 3 ? (int)p + 1 : (p < 5 ? (int)p - 1 : 3)) : (int)p - 6;
+                    const R* sr = st_base + (uint64_t)li * G::SW;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        ki[q][a] = sr[G::KV + 3 * i + a];
+                        kj[q][a] = sr[G::KV + 3 * j + a];
+                    }
+                    if (MODEL == EBB_NH) {
+                        c_a[q] = sr[GState<EBB_NH>::CM + p];
+                        c_b[q] = sr[GState<EBB_NH>::C1];
+                        c_c[q] = sr[GState<EBB_NH>::CL];
+                        c_d[q] = R(0);
+                    } else {
+                        using S = GState<EBB_STVK>;
+                        c_a[q] = sr[S::WS + p];
+                        c_b[q] = sr[S::CH];
+                        c_c[q] = sr[S::CL];
+                        c_d[q] = sr[S::WM + p];
+#pragma unroll
+                        for (int k = 0; k < 6; ++k) Bm[q][k] = sr[S::B + k];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (!ok[q]) continue;
+                    const bool tr = ent[q] & 1u;
+                    R Kb[3][3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+#pragma unroll
+                        for (int b = 0; b < 3; ++b) {
+                            R val = c_b[q] * kj[q][a] * ki[q][b] + c_c[q] * ki[q][a] * kj[q][b] + (a == b ? c_a[q] : R(0));
+                            if (MODEL != EBB_NH) {
+                                const int lo = a < b ? a : b, hi = a < b ? b : a;
+                                const int bi = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+                                val += c_d[q] * Bm[q][bi];
+                            }
+                            Kb[a][b] = val;
+                        }
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+#pragma unroll
+                        for (int b = 0; b < 3; ++b) acc[3 * a + b] += tr ? Kb[b][a] : Kb[a][b];
+                }
+            }
+            const uint32_t r = crow[gs], rt = ctrow[gs];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                R* dst = K + (uint64_t)k * ne + r;
+                __stcs(dst, accumulate ? *dst + acc[k] : acc[k]);   // streaming: keep the state slice in L2
+            }
+            if (rt != r) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) {
+                        R* dst = K + (uint64_t)(3 * a + b) * ne + rt;
+                        __stcs(dst, accumulate ? *dst + acc[3 * b + a] : acc[3 * b + a]);
+                    }
+            }
+        }
+        // ---- phase 2b: forces of the tile's vertices
+        const uint64_t v0 = (uint64_t)tile * nvt;
+        const uint32_t nvl = (uint32_t)((v0 + nvt <= nv) ? nvt : nv - v0);
+        for (uint32_t lv = threadIdx.x; lv < nvl; lv += blockDim.x) {
+            const uint64_t vv = v0 + lv;
+            R f0 = 0, f1 = 0, f2 = 0;
+            const uint32_t e1 = fv_ptr[vv + 1];
+            uint32_t e = fv_ptr[vv];
+            for (; e + 4 <= e1; e += 4) {
+                R a[4][3];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t ent = fv_ent[e + q];
+                    const R* sr = st_base + (uint64_t)(ent >> 2) * G::SW + G::F + 3 * (ent & 3u);
+                    a[q][0] = sr[0];
+                    a[q][1] = sr[1];
+                    a[q][2] = sr[2];
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    f0 += a[q][0];
+                    f1 += a[q][1];
+                    f2 += a[q][2];
+                }
+            }
+            for (; e < e1; ++e) {
+                const uint32_t ent = fv_ent[e];
+                const R* sr = st_base + (uint64_t)(ent >> 2) * G::SW + G::F + 3 * (ent & 3u);
+                f0 += sr[0];
+                f1 += sr[1];
+                f2 += sr[2];
+            }
+            R* dst = f + 3 * vv;
+            dst[0] = accumulate ? dst[0] + f0 : f0;
+            dst[1] = accumulate ? dst[1] + f1 : f1;
+            dst[2] = accumulate ? dst[2] + f2 : f2;
+        }
+        __syncthreads();   // the next tile overwrites the state slice
+    }
+    if (WANT_E) {
+        double tot;
+        if (block_sum_last_done(e_acc, partials, counter, &tot)) *energy = (R)((double)*energy + tot);
+    }
+}
+
+template <typename R, int MODEL>
+ebb_status launch_gather(Ctx* c, const MapPlan& P, bool want_e, int accumulate, uint64_t nt, uint64_t nv,
+                         const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
+                         const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
+                         cudaStream_t s) {
+    const int block = 256;
+    auto kern = want_e ? k_tet_map_gather<R, MODEL, true> : k_tet_map_gather<R, MODEL, false>;
+    unsigned grid = occ_grid(c, kern, block, 0, (uint64_t)P.ntiles * block);
+    const size_t need = (size_t)grid * P.max_inst * GState<MODEL>::SW * sizeof(R);
+    if (need > c->map_scratch_bytes) {
+        if (c->map_scratch) cudaFree(c->map_scratch);
+        c->map_scratch = nullptr;
+        c->map_scratch_bytes = 0;
+        EBB_CUDA(c, cudaMalloc(&c->map_scratch, need));
+        c->map_scratch_bytes = need;
+    }
+    KernelTimer kt(c, EBB_K_TET_MAP, s);
+    kern<<<grid, block, 0, s>>>(P.ntiles, P.nvt, nv, nt, P.inst_ptr, P.recs, P.tile_cptr, P.crow, P.ctrow, P.slot_ptr,
+                                P.slot_ent, P.fv_ptr, P.fv_ent, (R*)c->map_scratch, P.max_inst, (const uint4*)V->ptr,
+                                (const R*)U->ptr, (const R*)D->ptr, (const R*)W->ptr, (const R*)MU->ptr,
+                                (const R*)LA->ptr, (R*)Fo->ptr, (R*)Ko->ptr, ne, accumulate, c->d_partials,
+                                c->d_counter + 0, En ? (R*)En->ptr : nullptr, c->d_err);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
 template <typename R, int MODEL>
 ebb_status launch_atomic(Ctx* c, bool want_k, bool want_e, uint64_t nt, const Field* V, const Field* Ef,
                          const Field* U, const Field* D, const Field* W, const Field* MU, const Field* LA,
@@ -470,9 +844,10 @@ ebb_status launch_tiled(Ctx* c, const MapPlan& P, bool want_e, int accumulate, u
     return EBB_OK;
 }
 
-int tile_vertices(ebb_dtype dt) {
+int tile_vertices(ebb_dtype dt, bool gather) {
     const char* e = getenv("EBB_TILE_VERTS");
     if (e && atoi(e) > 0 && atoi(e) <= 255) return atoi(e);
+    if (gather) return 64;     // bounds the L2-resident state slice per CTA
     return dt == EBB_F64 ? 128 : 192;
 }
 
@@ -482,7 +857,7 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     Ctx* c = (Ctx*)ctx;
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     if (d->model != EBB_STVK && d->model != EBB_NH) return fail(c, EBB_E_ARG, "unknown model %d", d->model);
-    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_TILED)
+    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_GATHER)
         return fail(c, EBB_E_ARG, "unknown scatter strategy %d", d->scatter);
     Field* V = get_field(c, d->v);
     Field* U = get_field(c, d->u);
@@ -527,17 +902,32 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     if (U->ptr == Fo->ptr || (Ko && (U->ptr == Ko->ptr || Fo->ptr == Ko->ptr)))
         return fail(c, EBB_E_PHASE, "map_tet_forces: a field is used in two phases (read and reduce)");
     cudaStream_t s = (cudaStream_t)stream;
-    const bool tiled = Ko && (d->scatter == EBB_SCATTER_TILED || d->scatter == EBB_SCATTER_AUTO);
+    const char* envs = getenv("EBB_SCATTER");
+    int strat = d->scatter;
+    // AUTO = the measured fastest: TILED for f + K
+    if (strat == EBB_SCATTER_AUTO) strat = (envs && atoi(envs) > 0) ? atoi(envs) : EBB_SCATTER_TILED;
+    const bool tiled = Ko && (strat == EBB_SCATTER_TILED || strat == EBB_SCATTER_GATHER);
     if (tiled) {
         // every K row and f row is written exactly once: zero_outputs means overwrite
+        const bool gather = strat == EBB_SCATTER_GATHER;
         MapPlan* P;
-        EBB_TRY(build_plan(c, d->v, d->e, tile_vertices(dt), &P));
+        EBB_TRY(build_plan(c, d->v, d->e, tile_vertices(dt, gather), &P));
         V = get_field(c, d->v); U = get_field(c, d->u); D = get_field(c, d->Dminv); W = get_field(c, d->W);
         MU = get_field(c, d->mu); LA = get_field(c, d->lam); Fo = get_field(c, d->f); Ko = get_field(c, d->K);
         En = d->energy == EBB_NONE ? nullptr : get_field(c, d->energy);
         if (d->zero_outputs && En) EBB_CUDA(c, cudaMemsetAsync(En->ptr, 0, dtype_size(dt), s));
         int accum = d->zero_outputs ? 0 : 1;
         bool we = En != nullptr;
+        if (gather) {
+            if (dt == EBB_F64) {
+                if (d->model == EBB_NH)
+                    return launch_gather<double, EBB_NH>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+                return launch_gather<double, EBB_STVK>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+            }
+            if (d->model == EBB_NH)
+                return launch_gather<float, EBB_NH>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+            return launch_gather<float, EBB_STVK>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);
+        }
         if (dt == EBB_F64) {
             if (d->model == EBB_NH)
                 return launch_tiled<double, EBB_NH>(c, *P, we, accum, nt, nv, V, U, D, W, MU, LA, Fo, Ko, ne, En, s);

@@ -50,7 +50,7 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
         T, V, E = fem.nt, fem.nv, fem.ne
         bf = 4 if dt == "f32" else 8
         for model in models:
-            for scat, sid in (("tiled", A.SCATTER_TILED), ("atomic", A.SCATTER_ATOMIC)):
+            for scat, sid in (("gather", A.SCATTER_GATHER), ("tiled", A.SCATTER_TILED), ("atomic", A.SCATTER_ATOMIC)):
                 fem.map_forces(model, scatter=sid)
                 torch.cuda.synchronize()
                 ctx.timing(True)

@@ -207,13 +207,17 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
 /* ---- the element map (hot path a4-a8) --------------------------------- */
 #define EBB_STVK 0
 #define EBB_NH 1
-#define EBB_SCATTER_AUTO 0
+#define EBB_SCATTER_AUTO 0      /* the measured fastest: GATHER, except StVK in
+                                   F64 -> TILED              */
 #define EBB_SCATTER_ATOMIC 1    /* per-tet red.global.add              */
-#define EBB_SCATTER_TILED 2     /* owner tiles, shared-memory accumulation
-                                   (AUTO: the measured fastest)                */
-#define EBB_SCATTER_GATHER 3    /* owner tiles, element state staged in an L2
-                                   scratch, per-row register gather: no
-                                   atomics, bitwise run-to-run deterministic  */
+#define EBB_SCATTER_TILED 2     /* owner tiles, shared-memory atomic
+                                   accumulation of every block                */
+#define EBB_SCATTER_GATHER 3    /* owner tiles, warp-specialized: producer
+                                   warps stage per-instance element state in
+                                   shared memory, owner threads of each row
+                                   gather it (no atomics, bitwise run-to-run
+                                   deterministic).  EBB_E_RANGE if a forced
+                                   tile size (EBB_TILE_VERTS) does not fit.   */
 typedef struct {
     int32_t model;         /* EBB_STVK | EBB_NH                                */
     int32_t scatter;       /* EBB_SCATTER_*                                    */

@@ -347,7 +347,6 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
     if (c->scratch) cudaFree(c->scratch);
     for (auto& e : c->ev_pool) cudaEventDestroy(e);
     for (auto& P : c->plans) P.release();
-    if (c->map_scratch) cudaFree(c->map_scratch);
     for (auto& G : c->graphs)
         if (G.exec) cudaGraphExecDestroy(G.exec);
     cudaFree(c->d_err);

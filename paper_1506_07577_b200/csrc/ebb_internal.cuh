@@ -49,6 +49,7 @@ struct Relation {
 struct MapPlan {
     ebb_field v = EBB_NONE, e = EBB_NONE;
     int nvt = 0;
+    int round = 0;                  // 0: tiled order; >0: gather rounds of this size (padded)
     uint32_t ntiles = 0, max_slots = 0;
     uint64_t ninst = 0, ncanon = 0;
     uint32_t* inst_ptr = nullptr;   // ntiles + 1
@@ -59,8 +60,10 @@ struct MapPlan {
     // gather strategy: per canonical slot the (instance, pair, transpose)
     // contributions, per vertex the (instance, corner) force contributions
     uint32_t max_inst = 0;          // most instances in one tile
+    uint32_t max_sent = 0;          // most row-contribution entries in one tile
+    uint32_t max_fent = 0;          // most force-contribution entries in one tile
     uint32_t* slot_ptr = nullptr;   // ncanon + 1
-    uint32_t* slot_ent = nullptr;   // (local instance << 5) | (pair << 1) | transpose
+    uint32_t* slot_ent = nullptr;   // (local instance << 8) | (i << 6) | (j << 4) | pair, i/j as stored
     uint32_t* fv_ptr = nullptr;     // nverts + 1
     uint32_t* fv_ent = nullptr;     // (local instance << 2) | corner
     void release() {
@@ -92,8 +95,6 @@ struct Ctx : ebb_ctx_s {
     struct TimedLaunch { int kernel; cudaEvent_t a, b; };
     std::vector<TimedLaunch> timed;
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
-    void* map_scratch = nullptr;    // per-CTA element-state staging of the gather map
-    size_t map_scratch_bytes = 0;
     struct GraphRec {
         cudaGraphExec_t exec = nullptr;
         unsigned long long launches = 0;

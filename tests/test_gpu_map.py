@@ -106,10 +106,18 @@ def test_map_energy_deterministic(ctx):
 
 
 @pytest.mark.parametrize("scatter", ["tiled", "gather"])
-@pytest.mark.parametrize("tile", ["1", "7", "33", "255"])
+@pytest.mark.parametrize("tile", ["1", "7", "33", "64", "255"])
 def test_tiled_map_tile_sizes(ctx, tile, scatter, monkeypatch):
-    """Ragged tiles (1 vertex .. 255 vertices) give the same result."""
+    """Ragged tiles (1 vertex .. 255 vertices) give the same result.  A forced
+    gather tile whose on-chip state does not fit in shared memory is refused
+    with EBB_E_RANGE (never silently shrunk or spilled)."""
     monkeypatch.setenv("EBB_TILE_VERTS", tile)
+    if scatter == "gather" and tile == "255":
+        from paper_1506_07577_b200.ebb import EbbError
+        fem = gpu_fem(ctx, Case(n=5, model="nh"), name="mtilebig")
+        with pytest.raises(EbbError, match="EBB_E_RANGE"):
+            fem.map_forces("nh", scatter=SCATTERS[scatter])
+        return
     case = Case(n=5, model="nh", spread=0.1)
     fem = gpu_fem(ctx, case, name=f"mtile{tile}{scatter}")
     m, new_of_old, tet_src, order = oracle_renumbered(case)

@@ -28,7 +28,7 @@ def _flush(buf):
     buf.zero_()
 
 
-def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000):
+def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000, kuhn_n=0):
     import numpy as np
     import torch
 
@@ -38,7 +38,13 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
     from synth import mesh as M
     from synth import state as S
 
-    X, tets, n = M.blob(target)
+    if kuhn_n:
+        n = kuhn_n
+        X, tets = M.kuhn6(n)
+        wl, mname = "C2", f"kuhn6 n={n}"
+    else:
+        X, tets, n = M.blob(target)
+        wl, mname = "C3", f"blob n={n}"
     free = S.fixed_mask(X, n)
     u = S.twist_u(X, n, 6, free=free)
     mu, lam = S.materials(tets.shape[0], 1e6, 0.3, spread=0.1)
@@ -62,7 +68,7 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
                 ctx.timing(False)
                 us = 1e3 * ms / nl
                 b = bench.bytes_map(T, V, E, bf)
-                print(json.dumps({"workload": "C3", "mesh": f"blob n={n}", "tets": T, "verts": V, "edge_rows": E,
+                print(json.dumps({"workload": wl, "mesh": mname, "tets": T, "verts": V, "edge_rows": E,
                                   "dtype": dt, "model": model, "scatter": scat, "avg_us": us,
                                   "tets_per_s": T / (us * 1e-6), "algorithmic_bytes": b,
                                   "hbm_frac": b / (us * 1e-6) / 1e9 / peak, "peak_gbs": peak, "peak_source": src}),
@@ -119,9 +125,12 @@ def main():
     ap.add_argument("--sizes", default="26,37,55,79,119")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--c3-tets", type=int, default=10_000_000)
+    ap.add_argument("--c2", action="store_true", help="the map sweep on the C2 Kuhn n=55 mesh")
     a = ap.parse_args()
     from paper_1506_07577_b200 import build
     build.build()
+    if a.c2:
+        run_c3(a.reps, kuhn_n=55)
     if a.c3:
         run_c3(a.reps, target=a.c3_tets)
     if a.c4:

@@ -218,6 +218,12 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
                                    gather it (no atomics, bitwise run-to-run
                                    deterministic).  EBB_E_RANGE if a forced
                                    tile size (EBB_TILE_VERTS) does not fit.   */
+#define EBB_SCATTER_SEGMENTED 4 /* single-pass owner tiles (host-built plan):
+                                   every thread computes one instance's
+                                   compact element state, then every owned
+                                   edge row sums its blocks rebuilt from the
+                                   states (segmented reduction, no atomics,
+                                   bitwise run-to-run deterministic).         */
 typedef struct {
     int32_t model;         /* EBB_STVK | EBB_NH                                */
     int32_t scatter;       /* EBB_SCATTER_*                                    */

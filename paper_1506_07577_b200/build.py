@@ -1,6 +1,7 @@
 """Build libebb_b200.so in-tree with nvcc for sm_100a (no JIT cache, no torch ABI)."""
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -13,8 +14,9 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
+OBJ = os.path.join(HERE, "build")
 
 
 def sources():
@@ -38,10 +40,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     if os.path.exists("/usr/local/cuda/bin/nvcc") and nvcc == "nvcc":
         nvcc = "/usr/local/cuda/bin/nvcc"
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *sources()]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+    # one nvcc per translation unit, in parallel, then one link
+    os.makedirs(OBJ, exist_ok=True)
+    hdr_t = max(os.path.getmtime(p) for p in _deps() if not p.endswith(".cu"))
+    objs, cmds = [], []
+    for src in sources():
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr_t):
+            cmds.append([nvcc, *NVCC_FLAGS, "-c", "-o", obj, src])
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, len(cmds))) as ex:
+        for cmd, rc in zip(cmds, ex.map(lambda c: subprocess.call(c), cmds)):
+            if verbose:
+                print(" ".join(cmd))
+            if rc != 0:
+                raise subprocess.CalledProcessError(rc, cmd)
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs]
+    subprocess.check_call(link)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

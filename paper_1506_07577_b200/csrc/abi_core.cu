@@ -254,6 +254,16 @@ ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_
     return st;
 }
 
+void release_plans(Ctx* c) {
+    for (auto& P : c->plans) P.release();
+    c->plans.clear();
+    for (SegPlan* P : c->segplans) {
+        P->release();
+        delete P;
+    }
+    c->segplans.clear();
+}
+
 // Apply a row permutation to every field of `rel` and remap every key-field
 // (anywhere in the context) that targets `rel`.  The paper's licence: the
 // runtime may reorder relations and re-encode keys.
@@ -261,8 +271,7 @@ ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, c
                             cudaStream_t s) {
     Relation* R = get_rel(c, rel);
     uint64_t n = R->size;
-    for (auto& P : c->plans) P.release();
-    c->plans.clear();
+    release_plans(c);
     for (ebb_field fh : R->fields) {
         Field& F = c->fields[fh];
         if (!F.alive) continue;
@@ -346,7 +355,7 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
         if (F.alive && F.owned && F.ptr) cudaFree(F.ptr);
     if (c->scratch) cudaFree(c->scratch);
     for (auto& e : c->ev_pool) cudaEventDestroy(e);
-    for (auto& P : c->plans) P.release();
+    release_plans(c);
     for (auto& G : c->graphs)
         if (G.exec) cudaGraphExecDestroy(G.exec);
     cudaFree(c->d_err);

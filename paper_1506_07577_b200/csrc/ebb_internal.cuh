@@ -74,6 +74,38 @@ struct MapPlan {
     }
 };
 
+// Plan of the SEGMENTED element map (seg_map.cu, built once per mesh on the
+// host): variable vertex tiles (consecutive SFC-ordered vertices) grown until
+// the tets touching them ("instances") reach `ni`, so one tile is one pass of
+// the kernel.  Per tile: its instance tet ids; per canonical edge row (tail <=
+// head) owned by the tile a "slot" (global row and transpose row); its phase-2
+// work as "items" = chunks of at most `chunk` entries of one slot's (or one
+// vertex's force) contribution list, the chunks of a list in consecutive lanes
+// of one warp (combined by shuffles), every tile's items padded to whole warps.
+struct SegPlan {
+    ebb_field v = EBB_NONE, e = EBB_NONE;
+    int ni = 0;                       // instance cap per tile (= threads per CTA)
+    uint32_t ntiles = 0, max_ent = 0, max_items = 0;
+    uint64_t ninst = 0, nslots = 0, nent = 0, nitems = 0;
+    double host_ms = 0;               // plan build time (host)
+    uint32_t* tile_v = nullptr;       // ntiles + 1: first vertex of each tile
+    uint32_t* tile_inst = nullptr;    // ntiles + 1: instance offsets
+    uint32_t* tile_item = nullptr;    // ntiles + 1: item offsets (multiples of 32)
+    uint32_t* tile_ent = nullptr;     // ntiles + 1: entry offsets (multiples of 4)
+    uint32_t* inst_t = nullptr;       // ninst: tet id of each instance (ascending per tile)
+    uint32_t* item_meta = nullptr;    // nitems: begin[0:16) count[16:23) pos[23:26) last[26:29) force[29]
+    uint32_t* item_tgt = nullptr;     // nitems: slot (row items) or vertex (force items); ~0 = padding
+    uint32_t* crow = nullptr;         // nslots: global edge row of the slot
+    uint32_t* ctrow = nullptr;        // nslots: global edge row of its transpose
+    uint32_t* ents = nullptr;         // nent: slot entries (lr << 8 | i << 6 | j << 4 | pair),
+                                      //       force entries (lr << 2 | corner)
+    void release() {
+        cudaFree(tile_v); cudaFree(tile_inst); cudaFree(tile_item); cudaFree(tile_ent); cudaFree(inst_t);
+        cudaFree(item_meta); cudaFree(item_tgt); cudaFree(crow); cudaFree(ctrow); cudaFree(ents);
+        tile_v = tile_inst = tile_item = tile_ent = inst_t = item_meta = item_tgt = crow = ctrow = ents = nullptr;
+    }
+};
+
 struct Ctx : ebb_ctx_s {
     int device = 0;
     std::vector<Relation> rels;
@@ -95,6 +127,7 @@ struct Ctx : ebb_ctx_s {
     struct TimedLaunch { int kernel; cudaEvent_t a, b; };
     std::vector<TimedLaunch> timed;
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
+    std::vector<SegPlan*> segplans; // (same)
     struct GraphRec {
         cudaGraphExec_t exec = nullptr;
         unsigned long long launches = 0;
@@ -139,6 +172,12 @@ Relation* get_rel(Ctx* c, ebb_rel r);
 ebb_status scratch_reserve(Ctx* c, size_t bytes);
 ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_dtype dt, uint32_t rows,
                               uint32_t cols, ebb_layout layout, ebb_field* out);
+void release_plans(Ctx* c);
+// seg_map.cu: the SEGMENTED element map (builds its plan on first use)
+ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
+                          const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
+                          const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
+                          cudaStream_t s);
 ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, const uint32_t* d_old_to_new,
                             cudaStream_t s);
 

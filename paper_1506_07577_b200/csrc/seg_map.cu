@@ -1,0 +1,637 @@
+// seg_map.cu -- the SEGMENTED element map ("+=" strategy
+// (iii): per-tet compact stiffness state, then a per-edge-row segmented sum of
+// the K_ij rebuilt from the states of the row's contributing (tet, i, j)).
+//
+// Per tet (P:941-946 Vega StVK, P:975-980 neo-Hookean): gather u[v[k]] through
+// the key-field tets.v, element physics (element.cuh: displacement
+// form + closed rank-1 stiffness), and the field reductions f[v[i]] += f_i,
+// K[e[i][j]] += K_ij plus energy += W Psi -- without atomics:
+//
+//   plan (host, once per mesh)  vertex tiles = runs of consecutive SFC-ordered
+//        vertices grown until the tets touching them ("instances") reach NT;
+//        a tile owns the canonical rows (tail <= head) of its vertices and
+//        their forces.  Per owned row the list of (instance, i, j) blocks that
+//        add into it, per owned vertex the list of (instance, corner) forces.
+//   kernel (persistent CTA of NT threads, one tile per pass)
+//        phase 1  thread = instance: element physics, compact state -> smem
+//                 (NH: k_i = F^-T g_i, W mu m_ij, W c1, W lam, f_i;
+//                  StVK: h_i = F g_i, W s_ij, W mu m_ij, F F^T, W mu, W lam, f_i);
+//                 then the loads of the next tile's instance inputs are issued
+//                 (they land during phase 2: a register software pipeline)
+//        phase 2  thread = owned row: walk its entries (staged in smem by a
+//                 bulk async copy issued one tile ahead), rebuild each 3x3
+//                 block from the state, sum in registers, store the row and its
+//                 transpose once; thread = owned vertex: sum its forces.
+// Every K row and f row is written exactly once (plain stores, no zero-fill),
+// in a fixed order: bitwise run-to-run deterministic.  The oracle computes the
+// same quantities by the textbook F-form and a generic 4th-order tensor
+// contraction (oracle/ebb_oracle.c); the two share no code.
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <vector>
+
+#include "async_copy.cuh"
+#include "ebb_internal.cuh"
+#include "element.cuh"
+#include "reduce.cuh"
+
+namespace ebb {
+namespace {
+
+// ------------------------------------------------------------------ state
+template <int MODEL>
+struct SegState;
+template <>
+struct SegState<EBB_NH> {   // [k 12][W mu m_p 10][W c1][W lam][f 12]
+    static constexpr int KV = 0, CM = 12, C1 = 22, CL = 23, F = 24, SW = 36;
+};
+template <>
+struct SegState<EBB_STVK> { // [h 12][W s_p 10][W mu m_p 10][B 6][W mu][W lam][f 12]
+    static constexpr int KV = 0, WS = 12, WM = 22, B = 32, CH = 38, CL = 39, F = 40, SW = 52;
+};
+
+// pair order: off-diagonal (0,1) (0,2) (0,3) (1,2) (1,3) (2,3), diagonal (0,0)..(3,3)
+__host__ __device__ constexpr int pair_i(int p) { return p < 3 ? 0 : p < 5 ? 1 : p < 6 ? 2 : p - 6; }
+__host__ __device__ constexpr int pair_j(int p) { return p < 3 ? p + 1 : p < 5 ? p - 1 : p < 6 ? 3 : p - 6; }
+
+template <typename R>
+struct SegIn {
+    R uu[4][3];
+    R g[3][3];
+    R W, mu, lam;
+};
+
+template <typename R>
+__device__ __forceinline__ void seg_load(uint32_t t, uint4 v, uint64_t nt, const R* __restrict__ u,
+                                         const R* __restrict__ Dminv, const R* __restrict__ Wt,
+                                         const R* __restrict__ mu_t, const R* __restrict__ lam_t, SegIn<R>& in) {
+    if (t == 0xFFFFFFFFu) return;
+    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) in.uu[k][a] = __ldg(u + 3ull * vv[k] + a);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) in.g[r][c] = __ldg(Dminv + (uint64_t)(3 * r + c) * nt + t);
+    in.W = __ldg(Wt + t);
+    in.mu = __ldg(mu_t + t);
+    in.lam = __ldg(lam_t + t);
+}
+
+// Adds one stored block (entry = (lr << 8) | (i << 6) | (j << 4) | pair) to acc:
+//   NH   K_ij = W [ mu m_ij I + c1 k_j k_i^T + lam k_i k_j^T ]
+//   StVK K_ij = W [ s_ij I + mu (m_ij F F^T + h_j h_i^T) + lam h_i h_j^T ]
+template <typename R, int MODEL, int NT>
+__device__ __forceinline__ void seg_block(const R* __restrict__ st, uint32_t ent, R acc[9]) {
+    using G = SegState<MODEL>;
+    const uint32_t lr = ent >> 8, i = (ent >> 6) & 3u, j = (ent >> 4) & 3u, p = ent & 15u;
+    const R* si = st + (G::KV + 3 * i) * NT + lr;
+    const R* sj = st + (G::KV + 3 * j) * NT + lr;
+    const R ki[3] = {si[0], si[NT], si[2 * NT]};
+    const R kj[3] = {sj[0], sj[NT], sj[2 * NT]};
+    R ca, cb, cc, cd = R(0), Bm[6];
+    if constexpr (MODEL == EBB_NH) {
+        ca = st[(G::CM + p) * NT + lr];
+        cb = st[G::C1 * NT + lr];
+        cc = st[G::CL * NT + lr];
+    } else {
+        ca = st[(G::WS + p) * NT + lr];
+        cb = st[G::CH * NT + lr];
+        cc = st[G::CL * NT + lr];
+        cd = st[(G::WM + p) * NT + lr];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) Bm[k] = st[(G::B + k) * NT + lr];
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            R val = cb * kj[a] * ki[b] + cc * ki[a] * kj[b];
+            if (a == b) val += ca;
+            if constexpr (MODEL != EBB_NH) {
+                constexpr int bidx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+                val += cd * Bm[bidx[a][b]];
+            }
+            acc[3 * a + b] += val;
+        }
+}
+
+template <typename R, int MODEL, bool WANT_E, int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
+    uint32_t ntiles, const uint32_t* __restrict__ tile_v, const uint32_t* __restrict__ tile_inst,
+    const uint32_t* __restrict__ tile_item, const uint32_t* __restrict__ tile_ent, const uint32_t* __restrict__ inst_t,
+    const uint32_t* __restrict__ item_meta, const uint32_t* __restrict__ item_tgt, const uint32_t* __restrict__ crow,
+    const uint32_t* __restrict__ ctrow, const uint32_t* __restrict__ ents, uint32_t max_ent, uint64_t nt,
+    const uint4* __restrict__ tv, const R* __restrict__ u, const R* __restrict__ Dminv, const R* __restrict__ Wt,
+    const R* __restrict__ mu_t, const R* __restrict__ lam_t, R* __restrict__ f, R* __restrict__ K, uint64_t ne,
+    int accumulate, double* __restrict__ partials, unsigned int* __restrict__ counter, R* __restrict__ energy,
+    unsigned long long* __restrict__ err) {
+    using G = SegState<MODEL>;
+    extern __shared__ __align__(16) unsigned char seg_smem[];
+    R* st = reinterpret_cast<R*>(seg_smem);                                // [SW][NT]
+    uint32_t* ebuf = reinterpret_cast<uint32_t*>(st + (size_t)G::SW * NT);  // [2][max_ent]
+    __shared__ __align__(8) uint64_t bar[2];
+    const uint32_t tid = threadIdx.x, G0 = gridDim.x;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto stage = [&](uint32_t tile, int b) {   // thread 0: bulk copy of a tile's entry lists
+        const uint32_t e0 = __ldg(tile_ent + tile), bytes = (__ldg(tile_ent + tile + 1) - e0) * 4u;
+        mbar_arrive_expect_tx(&bar[b], bytes);
+        if (bytes) bulk_g2s(ebuf + (size_t)b * max_ent, ents + e0, bytes, &bar[b]);
+    };
+    auto inst_of = [&](uint32_t tile) -> uint32_t {
+        if (tile >= ntiles) return 0xFFFFFFFFu;
+        const uint32_t i0 = __ldg(tile_inst + tile), n = __ldg(tile_inst + tile + 1) - i0;
+        return tid < n ? __ldg(inst_t + i0 + tid) : 0xFFFFFFFFu;
+    };
+    auto verts_of = [&](uint32_t t) -> uint4 { return t == 0xFFFFFFFFu ? make_uint4(0, 0, 0, 0) : __ldg(tv + t); };
+
+    // first pass of a tile's phase-2 items, loaded one tile ahead
+    uint32_t it0_n = 0, nit_n = 0, meta_n = 0, tgt_n = 0xFFFFFFFFu;
+    auto item_head = [&](uint32_t tile) {
+        it0_n = 0;
+        nit_n = 0;
+        meta_n = 0;
+        tgt_n = 0xFFFFFFFFu;
+        if (tile >= ntiles) return;
+        it0_n = __ldg(tile_item + tile);
+        nit_n = __ldg(tile_item + tile + 1) - it0_n;
+        if (tid < nit_n) {
+            meta_n = __ldg(item_meta + it0_n + tid);
+            tgt_n = __ldg(item_tgt + it0_n + tid);
+        }
+    };
+    const uint32_t tile0 = blockIdx.x;
+    if (tid == 0 && tile0 < ntiles) stage(tile0, 0);
+    item_head(tile0);
+    // software pipeline: inputs of this tile, keys of the next, tet id of the one after
+    uint32_t tc = inst_of(tile0);
+    uint4 vc = verts_of(tc);
+    SegIn<R> in;
+    seg_load(tc, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
+    uint32_t t1 = inst_of(tile0 + G0);
+    uint4 v1 = verts_of(t1);
+    uint32_t t2 = inst_of(tile0 + 2 * G0);
+    double e_acc = 0.0;
+    uint32_t k = 0;
+    for (uint32_t tile = tile0; tile < ntiles; tile += G0, ++k) {
+        const uint32_t va = __ldg(tile_v + tile), vb = __ldg(tile_v + tile + 1);
+        // ---- phase 1: this thread's instance -> compact state
+        if (tc != 0xFFFFFFFFu) {
+            TetState<R> ts;
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) ts.g[r + 1][c] = in.g[r][c];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ts.g[0][c] = -(ts.g[1][c] + ts.g[2][c] + ts.g[3][c]);
+            ts.W = in.W;
+            ts.mu = in.mu;
+            ts.lam = in.lam;
+            tet_physics<R, MODEL, true>(in.uu, ts);
+            const uint32_t vmin = min(min(vc.x, vc.y), min(vc.z, vc.w));
+            const bool owner = vmin >= va && vmin < vb;   // the tile of the min vertex counts the tet once
+            if (MODEL == EBB_NH && owner && !(ts.J > R(0))) atomicAdd(&err[ERR_INVERTED], 1ull);
+            if (WANT_E && owner) e_acc += (double)(ts.W * ts.psi);
+            R fi[4][3];
+            tet_forces(ts, fi);
+            R* sr = st + tid;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    sr[(G::KV + 3 * i + a) * NT] = ts.kv[i][a];
+                    sr[(G::F + 3 * i + a) * NT] = fi[i][a];
+                }
+#pragma unroll
+            for (int p = 0; p < 10; ++p) {
+                const int i = pair_i(p), j = pair_j(p);
+                const R mij = ts.g[i][0] * ts.g[j][0] + ts.g[i][1] * ts.g[j][1] + ts.g[i][2] * ts.g[j][2];
+                if constexpr (MODEL == EBB_NH) {
+                    sr[(SegState<EBB_NH>::CM + p) * NT] = ts.W * ts.mu * mij;
+                } else {
+                    R Sg[3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        Sg[a] = ts.S[a][0] * ts.g[i][0] + ts.S[a][1] * ts.g[i][1] + ts.S[a][2] * ts.g[i][2];
+                    sr[(SegState<EBB_STVK>::WS + p) * NT] =
+                        ts.W * (Sg[0] * ts.g[j][0] + Sg[1] * ts.g[j][1] + Sg[2] * ts.g[j][2]);
+                    sr[(SegState<EBB_STVK>::WM + p) * NT] = ts.W * ts.mu * mij;
+                }
+            }
+            if constexpr (MODEL == EBB_NH) {
+                sr[SegState<EBB_NH>::C1 * NT] = ts.W * ts.c1;
+                sr[SegState<EBB_NH>::CL * NT] = ts.W * ts.lam;
+            } else {
+                constexpr int B = SegState<EBB_STVK>::B;
+                sr[(B + 0) * NT] = ts.B[0][0];
+                sr[(B + 1) * NT] = ts.B[0][1];
+                sr[(B + 2) * NT] = ts.B[0][2];
+                sr[(B + 3) * NT] = ts.B[1][1];
+                sr[(B + 4) * NT] = ts.B[1][2];
+                sr[(B + 5) * NT] = ts.B[2][2];
+                sr[SegState<EBB_STVK>::CH * NT] = ts.W * ts.mu;
+                sr[SegState<EBB_STVK>::CL * NT] = ts.W * ts.lam;
+            }
+        }
+        // ---- advance the pipeline: these loads land during phase 2
+        tc = t1;
+        vc = v1;
+        seg_load(tc, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
+        t1 = t2;
+        v1 = verts_of(t1);
+        t2 = inst_of(tile + 3 * G0);
+        if (tid == 0 && tile + G0 < ntiles) {
+            fence_proxy_async_smem();
+            stage(tile + G0, (k + 1) & 1);
+        }
+        // phase-2 work list of this tile (its first pass was loaded one tile ahead)
+        const uint32_t it0 = it0_n, nit = nit_n;
+        uint32_t meta = meta_n, tgt = tgt_n;
+        item_head(tile + G0);
+        __syncthreads();   // state complete
+        const int b = k & 1;
+        mbar_wait(&bar[b], (k >> 1) & 1);
+        const uint32_t* E = ebuf + (size_t)b * max_ent;
+        // ---- phase 2: items = chunks of one row's (or one vertex's force) list;
+        // the chunks of a list sit in consecutive lanes and are combined by a
+        // shuffle tree (items are padded to whole warps: the loop is warp-uniform)
+        for (uint32_t base = 0; base < nit; base += NT) {
+            if (base) {
+                meta = 0;
+                tgt = 0xFFFFFFFFu;
+                if (base + tid < nit) {
+                    meta = __ldg(item_meta + it0 + base + tid);
+                    tgt = __ldg(item_tgt + it0 + base + tid);
+                }
+            }
+            const uint32_t e0 = meta & 0xFFFFu, e1 = e0 + ((meta >> 16) & 0x7Fu);
+            const uint32_t pos = (meta >> 23) & 7u, last = (meta >> 26) & 7u;
+            const bool force = (meta >> 29) & 1u;
+            R a9[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) a9[q] = R(0);
+            if (!force) {
+                uint32_t e = e0;
+                for (; e + 1 < e1; e += 2) {
+                    const uint32_t x = E[e], y = E[e + 1];
+                    seg_block<R, MODEL, NT>(st, x, a9);
+                    seg_block<R, MODEL, NT>(st, y, a9);
+                }
+                if (e < e1) seg_block<R, MODEL, NT>(st, E[e], a9);
+            } else {
+                for (uint32_t e = e0; e < e1; ++e) {
+                    const uint32_t en = E[e], lr = en >> 2, kk = en & 3u;
+                    a9[0] += st[(G::F + 3 * kk + 0) * NT + lr];
+                    a9[1] += st[(G::F + 3 * kk + 1) * NT + lr];
+                    a9[2] += st[(G::F + 3 * kk + 2) * NT + lr];
+                }
+            }
+            const bool all_force = __all_sync(0xFFFFFFFFu, force);
+#pragma unroll
+            for (uint32_t step = 1; step < 8; step <<= 1) {
+                if (!__any_sync(0xFFFFFFFFu, last >= step)) break;
+                const bool take = pos + step <= last;
+#pragma unroll
+                for (int q = 0; q < 9; ++q) {
+                    if (all_force && q >= 3) break;
+                    const R o = __shfl_down_sync(0xFFFFFFFFu, a9[q], step);
+                    if (take) a9[q] += o;
+                }
+            }
+            if (pos == 0 && tgt != 0xFFFFFFFFu) {
+                if (!force) {
+                    const uint32_t r = __ldg(crow + tgt), rt = __ldg(ctrow + tgt);
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) {
+                        R* dst = K + (uint64_t)q * ne + r;
+                        *dst = accumulate ? *dst + a9[q] : a9[q];
+                    }
+                    if (rt != r) {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a)
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                R* dst = K + (uint64_t)(3 * a + c) * ne + rt;
+                                *dst = accumulate ? *dst + a9[3 * c + a] : a9[3 * c + a];
+                            }
+                    }
+                } else {
+                    R* dst = f + 3ull * tgt;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) dst[a] = accumulate ? dst[a] + a9[a] : a9[a];
+                }
+            }
+        }
+        __syncthreads();   // state and entry buffer b free for reuse
+    }
+    if (WANT_E) {
+        double tot;
+        if (block_sum_last_done(e_acc, partials, counter, &tot)) *energy = (R)((double)*energy + tot);
+    }
+}
+
+// ------------------------------------------------------------------ plan (host)
+uint32_t lower_bound_u32(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t x) {
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <typename T>
+ebb_status upload(Ctx* c, const std::vector<T>& h, uint32_t** d) {
+    EBB_CUDA(c, cudaMalloc((void**)d, h.size() * sizeof(T) + 16));
+    if (!h.empty()) EBB_CUDA(c, cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return EBB_OK;
+}
+
+ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** out) {
+    for (SegPlan* P : c->segplans)
+        if (P->v == vf && P->e == ef && P->ni == ni) {
+            *out = P;
+            return EBB_OK;
+        }
+    const auto t_start = std::chrono::steady_clock::now();
+    Field* V = get_field(c, vf);
+    Field* E = get_field(c, ef);
+    Relation& ER = c->rels[E->key_target];
+    if (ER.grouped_by == EBB_NONE || ER.index == EBB_NONE)
+        return fail(c, EBB_E_STATE, "segmented map: the edge relation must be grouped by tail");
+    ebb_field hf = EBB_NONE;
+    for (ebb_field fh : ER.fields)
+        if (c->fields[fh].alive && c->fields[fh].name == "head") hf = fh;
+    if (hf == EBB_NONE) return fail(c, EBB_E_STATE, "segmented map: edge relation has no 'head' key-field");
+    const uint64_t nt = c->rels[V->rel].size, nv = c->rels[V->key_target].size, ne = ER.size;
+    std::vector<uint32_t> tv(nt * 4), index(nv + 1), head(ne);
+    EBB_CUDA(c, cudaMemcpy(tv.data(), V->ptr, nt * 16, cudaMemcpyDeviceToHost));
+    EBB_CUDA(c, cudaMemcpy(index.data(), c->fields[ER.index].ptr, (nv + 1) * 4, cudaMemcpyDeviceToHost));
+    EBB_CUDA(c, cudaMemcpy(head.data(), c->fields[hf].ptr, ne * 4, cudaMemcpyDeviceToHost));
+    // vertex -> incident tets (ascending tet id)
+    std::vector<uint32_t> vt_ptr(nv + 1, 0), vt(nt * 4);
+    for (uint64_t i = 0; i < nt * 4; ++i) vt_ptr[tv[i] + 1]++;
+    for (uint64_t v = 0; v < nv; ++v) vt_ptr[v + 1] += vt_ptr[v];
+    {
+        std::vector<uint32_t> cur(vt_ptr.begin(), vt_ptr.end() - 1);
+        for (uint64_t i = 0; i < nt * 4; ++i) vt[cur[tv[i]]++] = (uint32_t)(i >> 2);
+    }
+    // self row of every vertex (canonical rows of v = [self, index[v+1]))
+    std::vector<uint32_t> rself(nv);
+    for (uint64_t v = 0; v < nv; ++v) {
+        rself[v] = lower_bound_u32(head.data(), index[v], index[v + 1], (uint32_t)v);
+        if (rself[v] >= index[v + 1] || head[rself[v]] != v)
+            return fail(c, EBB_E_STATE, "segmented map: vertex %llu has no self-loop edge row", (unsigned long long)v);
+    }
+    // greedy tiles: grow until the next vertex would push the instances past ni
+    std::vector<uint32_t> tile_v{0};
+    {
+        std::vector<int64_t> stamp(nt, -1);
+        int64_t tile = 0;
+        uint32_t ci = 0, cv = 0;
+        for (uint64_t v = 0; v < nv; ++v) {
+            const uint32_t deg = vt_ptr[v + 1] - vt_ptr[v];
+            if (deg > (uint32_t)ni)
+                return fail(c, EBB_E_RANGE, "segmented map: vertex %llu touches %u tets (> %d per tile)",
+                            (unsigned long long)v, deg, ni);
+            uint32_t nw = 0;
+            for (uint32_t q = vt_ptr[v]; q < vt_ptr[v + 1]; ++q) nw += stamp[vt[q]] != tile;
+            if (cv > 0 && (ci + nw > (uint32_t)ni || cv >= 4096)) {
+                tile_v.push_back((uint32_t)v);
+                ++tile;
+                ci = 0;
+                cv = 0;
+                nw = deg;
+            }
+            for (uint32_t q = vt_ptr[v]; q < vt_ptr[v + 1]; ++q) stamp[vt[q]] = tile;
+            ci += nw;
+            ++cv;
+        }
+        if (nv > 0) tile_v.push_back((uint32_t)nv);
+    }
+    const uint32_t ntiles = (uint32_t)tile_v.size() - 1;
+    std::vector<uint32_t> tile_inst{0}, tile_item{0}, tile_ent{0}, inst_t, item_meta, item_tgt, crow, ctrow, ents;
+    inst_t.reserve(nt * 2);
+    ents.reserve(nt * 30);
+    std::vector<uint32_t> lr_of(nt, 0xFFFFFFFFu);
+    std::vector<uint32_t> order, sbase, lbeg;
+    std::vector<std::vector<uint32_t>> lists;
+    uint32_t max_ent = 0, max_items = 0;
+    for (uint32_t T = 0; T < ntiles; ++T) {
+        const uint32_t a = tile_v[T], b = tile_v[T + 1];
+        // instances: tets touching [a, b), ascending
+        const size_t i0 = inst_t.size();
+        for (uint32_t v = a; v < b; ++v)
+            for (uint32_t q = vt_ptr[v]; q < vt_ptr[v + 1]; ++q) {
+                const uint32_t t = vt[q];
+                if (lr_of[t] != T) {   // lr_of doubles as a per-tile stamp here
+                    lr_of[t] = T;
+                    inst_t.push_back(t);
+                }
+            }
+        std::sort(inst_t.begin() + i0, inst_t.end());
+        const uint32_t ninst = (uint32_t)(inst_t.size() - i0);
+        // canonical slots of the tile in row order
+        sbase.assign(b - a + 1, 0);
+        for (uint32_t v = a; v < b; ++v) sbase[v - a + 1] = sbase[v - a] + (index[v + 1] - rself[v]);
+        const uint32_t ns = sbase[b - a], nvl = b - a;
+        lists.assign(ns + nvl, {});   // [0, ns): slot lists; [ns, ns + nvl): force lists
+        for (uint32_t l = 0; l < ninst; ++l) {
+            const uint32_t t = inst_t[i0 + l];
+            const uint32_t* vv = &tv[4ull * t];
+            for (int p = 0; p < 10; ++p) {
+                const int i = pair_i(p), j = pair_j(p);
+                const uint32_t lo = std::min(vv[i], vv[j]), hi = std::max(vv[i], vv[j]);
+                if (lo < a || lo >= b) continue;
+                const uint32_t r = lower_bound_u32(head.data(), rself[lo], index[lo + 1], hi);
+                const uint32_t s = sbase[lo - a] + (r - rself[lo]);
+                // block K_ij lands on row (v_i, v_j): transposed (K_ji) when v_i > v_j
+                const uint32_t bi = vv[i] <= vv[j] ? i : j, bj = vv[i] <= vv[j] ? j : i;
+                lists[s].push_back((l << 8) | (bi << 6) | (bj << 4) | (uint32_t)p);
+            }
+            for (uint32_t kk = 0; kk < 4; ++kk)
+                if (vv[kk] >= a && vv[kk] < b) lists[ns + vv[kk] - a].push_back((l << 2) | kk);
+        }
+        // entries: slot lists (by descending length), then force lists, padded to 16 B
+        order.resize(ns);
+        for (uint32_t s = 0; s < ns; ++s) order[s] = s;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint32_t x, uint32_t y) { return lists[x].size() > lists[y].size(); });
+        for (uint32_t v = 0; v < nvl; ++v) order.push_back(ns + v);
+        const size_t e_base = ents.size();
+        const uint32_t slot_g0 = (uint32_t)crow.size();
+        lbeg.assign(ns + nvl, 0);
+        size_t tot = 0, longest = 0;
+        for (uint32_t q : order) {
+            lbeg[q] = (uint32_t)(ents.size() - e_base);
+            ents.insert(ents.end(), lists[q].begin(), lists[q].end());
+            tot += lists[q].size();
+            longest = std::max(longest, lists[q].size());
+        }
+        while ((ents.size() - e_base) % 4) ents.push_back(0);
+        const uint32_t nent = (uint32_t)(ents.size() - e_base);
+        if (nent >= 65536)
+            return fail(c, EBB_E_RANGE, "segmented map: tile %u has %u entries (> 65535)", T, nent);
+        // slots -> rows (global slot = slot_g0 + position in `order`)
+        for (uint32_t q = 0; q < ns; ++q) {
+            const uint32_t s = order[q];
+            const uint32_t lv = (uint32_t)(std::upper_bound(sbase.begin(), sbase.end(), s) - sbase.begin()) - 1;
+            const uint32_t tail = a + lv, r = rself[tail] + (s - sbase[lv]), hd = head[r];
+            crow.push_back(r);
+            ctrow.push_back(hd == tail ? r : lower_bound_u32(head.data(), index[hd], index[hd + 1], tail));
+        }
+        // items: chunks of <= L entries (L ~ the even share per thread), at most
+        // 8 chunks per list, the chunks of one list never straddle a warp
+        // chunk cap L: the smallest (from the even share per thread) whose
+        // warp-padded item list fits one pass of the CTA; at most 8 chunks a list
+        auto count_items = [&](size_t L) {
+            size_t n = 0;
+            for (uint32_t q : order) {
+                const size_t cnt = lists[q].size(), nc = cnt == 0 ? 1 : (cnt + L - 1) / L;
+                if ((n % 32) + nc > 32) n = (n + 31) / 32 * 32;
+                n += nc;
+            }
+            return (n + 31) / 32 * 32;
+        };
+        size_t L = std::max<size_t>({(size_t)2, (tot + ni - 1) / ni, (longest + 7) / 8});
+        while (L < longest && count_items(L) > (size_t)ni) ++L;
+        if (L > 127) return fail(c, EBB_E_RANGE, "segmented map: a list of %zu entries (> 8 x 127)", longest);
+        const size_t it_base = item_meta.size();
+        for (uint32_t qi = 0; qi < order.size(); ++qi) {
+            const uint32_t q = order[qi];
+            const bool force = q >= ns;
+            const uint32_t cnt = (uint32_t)lists[q].size();
+            const uint32_t nc = cnt == 0 ? 1 : (uint32_t)((cnt + L - 1) / L);
+            if (((item_meta.size() - it_base) % 32) + nc > 32)
+                while ((item_meta.size() - it_base) % 32) {
+                    item_meta.push_back(0);
+                    item_tgt.push_back(0xFFFFFFFFu);
+                }
+            uint32_t beg = lbeg[q];
+            for (uint32_t cc = 0; cc < nc; ++cc) {
+                const uint32_t sz = cnt / nc + (cc < cnt % nc ? 1 : 0);
+                item_meta.push_back(beg | (sz << 16) | (cc << 23) | ((nc - 1) << 26) | ((force ? 1u : 0u) << 29));
+                item_tgt.push_back(force ? a + (q - ns) : slot_g0 + qi);
+                beg += sz;
+            }
+        }
+        while ((item_meta.size() - it_base) % 32) {
+            item_meta.push_back(0);
+            item_tgt.push_back(0xFFFFFFFFu);
+        }
+        for (uint32_t l = 0; l < ninst; ++l) lr_of[inst_t[i0 + l]] = 0xFFFFFFFEu;   // never a tile id
+        max_ent = std::max(max_ent, nent);
+        max_items = std::max(max_items, (uint32_t)(item_meta.size() - it_base));
+        tile_inst.push_back((uint32_t)inst_t.size());
+        tile_item.push_back((uint32_t)item_meta.size());
+        tile_ent.push_back((uint32_t)ents.size());
+    }
+    SegPlan* P = new SegPlan();
+    P->v = vf;
+    P->e = ef;
+    P->ni = ni;
+    P->ntiles = ntiles;
+    P->max_ent = max_ent;
+    P->max_items = max_items;
+    P->ninst = inst_t.size();
+    P->nslots = crow.size();
+    P->nent = ents.size();
+    P->nitems = item_meta.size();
+    ebb_status s = EBB_OK;
+    auto up = [&](const std::vector<uint32_t>& h, uint32_t** d) {
+        if (s == EBB_OK) s = upload(c, h, d);
+    };
+    up(tile_v, &P->tile_v);
+    up(tile_inst, &P->tile_inst);
+    up(tile_item, &P->tile_item);
+    up(tile_ent, &P->tile_ent);
+    up(inst_t, &P->inst_t);
+    up(item_meta, &P->item_meta);
+    up(item_tgt, &P->item_tgt);
+    up(crow, &P->crow);
+    up(ctrow, &P->ctrow);
+    up(ents, &P->ents);
+    if (s != EBB_OK) {
+        P->release();
+        delete P;
+        return s;
+    }
+    P->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    c->segplans.push_back(P);
+    *out = P;
+    return EBB_OK;
+}
+
+template <typename R, int MODEL, int NT>
+ebb_status launch_seg_t(Ctx* c, const SegPlan& P, bool want_e, int accumulate, uint64_t nt, const Field* V,
+                        const Field* U, const Field* D, const Field* W, const Field* MU, const Field* LA,
+                        const Field* Fo, const Field* Ko, uint64_t ne, const Field* En, cudaStream_t s) {
+    const size_t smem = (size_t)SegState<MODEL>::SW * NT * sizeof(R) + 2ull * P.max_ent * 4;
+    if (smem > 227 * 1024)
+        return fail(c, EBB_E_RANGE, "segmented map: %zu B of shared memory needed (> 227 KB)", smem);
+    auto kern = want_e ? k_tet_map_seg<R, MODEL, true, NT> : k_tet_map_seg<R, MODEL, false, NT>;
+    static thread_local size_t configured[2] = {0, 0};   // attribute set once (graph-capture safe)
+    if (smem > configured[want_e]) {
+        EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured[want_e] = smem;
+    }
+    const unsigned grid = occ_grid(c, kern, NT, smem, (uint64_t)P.ntiles * NT);
+    KernelTimer kt(c, EBB_K_TET_MAP, s);
+    kern<<<grid, NT, smem, s>>>(P.ntiles, P.tile_v, P.tile_inst, P.tile_item, P.tile_ent, P.inst_t, P.item_meta,
+                                P.item_tgt, P.crow, P.ctrow, P.ents, P.max_ent, nt, (const uint4*)V->ptr,
+                                (const R*)U->ptr, (const R*)D->ptr, (const R*)W->ptr, (const R*)MU->ptr,
+                                (const R*)LA->ptr, (R*)Fo->ptr, (R*)Ko->ptr, ne, accumulate, c->d_partials,
+                                c->d_counter + 0, En ? (R*)En->ptr : nullptr, c->d_err);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+}  // namespace
+
+// threads per CTA = instance cap per tile: the compact state must fit in
+// shared memory next to two entry buffers (fp64 StVK state is 52 words)
+int seg_threads(ebb_dtype dt, int model) {
+    const char* e = getenv("EBB_SEG_NT");
+    if (e && (atoi(e) == 256 || atoi(e) == 384 || atoi(e) == 512)) {
+        const int v = atoi(e);
+        return (dt == EBB_F64 && model == EBB_STVK && v > 384) ? 384 : v;
+    }
+    return (dt == EBB_F64 && model == EBB_STVK) ? 384 : 256;   // measured
+}
+
+ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
+                          const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
+                          const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
+                          cudaStream_t s) {
+    const ebb_dtype dt = U->dtype;
+    const int NT = seg_threads(dt, model);
+    SegPlan* P;
+    EBB_TRY(build_seg_plan(c, vf, ef, NT, &P));
+#define EBB_SARGS c, *P, want_e, accumulate, nt, V, U, D, W, MU, LA, Fo, Ko, ne, En, s
+#define EBB_SDISPATCH(R, MODEL)                                               \
+    do {                                                                      \
+        if (NT == 256) return launch_seg_t<R, MODEL, 256>(EBB_SARGS);         \
+        if (NT == 384) return launch_seg_t<R, MODEL, 384>(EBB_SARGS);         \
+        if constexpr (!(sizeof(R) == 8 && MODEL == EBB_STVK))                 \
+            return launch_seg_t<R, MODEL, 512>(EBB_SARGS);                    \
+        return fail(c, EBB_E_ARG, "segmented map: bad thread count %d", NT); \
+    } while (0)
+    if (dt == EBB_F64) {
+        if (model == EBB_NH) EBB_SDISPATCH(double, EBB_NH);
+        EBB_SDISPATCH(double, EBB_STVK);
+    }
+    if (model == EBB_NH) EBB_SDISPATCH(float, EBB_NH);
+    EBB_SDISPATCH(float, EBB_STVK);
+#undef EBB_SDISPATCH
+#undef EBB_SARGS
+}
+
+}  // namespace ebb

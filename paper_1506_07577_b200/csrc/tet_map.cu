@@ -1151,7 +1151,7 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     Ctx* c = (Ctx*)ctx;
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     if (d->model != EBB_STVK && d->model != EBB_NH) return fail(c, EBB_E_ARG, "unknown model %d", d->model);
-    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_GATHER)
+    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_SEGMENTED)
         return fail(c, EBB_E_ARG, "unknown scatter strategy %d", d->scatter);
     Field* V = get_field(c, d->v);
     Field* U = get_field(c, d->u);
@@ -1204,6 +1204,12 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     if (strat == EBB_SCATTER_AUTO) {
         if (envs && atoi(envs) > 0) strat = atoi(envs);
         else strat = (dt == EBB_F64 && d->model == EBB_STVK) ? EBB_SCATTER_TILED : EBB_SCATTER_GATHER;
+    }
+    if (Ko && strat == EBB_SCATTER_SEGMENTED) {
+        // every K row and f row is written exactly once: zero_outputs means overwrite
+        if (d->zero_outputs && En) EBB_CUDA(c, cudaMemsetAsync(En->ptr, 0, dtype_size(dt), s));
+        return seg_map_launch(c, d->v, d->e, d->model, En != nullptr, d->zero_outputs ? 0 : 1, nt, V, U, D, W, MU, LA,
+                              Fo, Ko, ne, En, s);
     }
     const bool tiled = Ko && (strat == EBB_SCATTER_TILED || strat == EBB_SCATTER_GATHER);
     if (tiled) {

@@ -30,10 +30,10 @@ def _oracle_map(case, m, order, tet_src, model, u=None):
                               e=m.e, ne=m.ne)
 
 
-SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3}
+SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4}
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 @pytest.mark.parametrize("n,mesh", [(4, "kuhn6"), (9, "kuhn6"), (4, "alt5")])
 def test_map_fp64(ctx, model, n, mesh, scatter):
@@ -48,7 +48,7 @@ def test_map_fp64(ctx, model, n, mesh, scatter):
     assert ctx.error_counts(reset=True)["inverted"] == 0
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 def test_map_fp32_displacement_form(ctx, model, scatter):
     case = Case(n=8, model=model, spread=0.1)
@@ -128,7 +128,7 @@ def test_tiled_map_tile_sizes(ctx, tile, scatter, monkeypatch):
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented"])
 def test_map_accumulates_without_zeroing(ctx, scatter):
     """zero_outputs = 0 is the paper's `+=` into existing fields."""
     case = Case(n=4, model="stvk")
@@ -159,3 +159,34 @@ def test_gather_map_is_bitwise_deterministic(ctx):
     f1, K1 = fem.f.read(), fem.K.read()
     fem.map_forces("nh", scatter=SCATTERS["gather"])
     assert np.array_equal(fem.f.read(), f1) and np.array_equal(fem.K.read(), K1)
+
+
+def test_segmented_map_is_bitwise_deterministic(ctx):
+    """The segmented strategy has no atomics: reruns are bitwise identical."""
+    case = Case(n=8, model="nh")
+    fem = gpu_fem(ctx, case, name="mdet4")
+    fem.map_forces("nh", scatter=SCATTERS["segmented"])
+    f1, K1 = fem.f.read(), fem.K.read()
+    fem.map_forces("nh", scatter=SCATTERS["segmented"])
+    assert np.array_equal(fem.f.read(), f1) and np.array_equal(fem.K.read(), K1)
+
+
+@pytest.mark.parametrize("nt", ["256", "384", "512"])
+@pytest.mark.parametrize("model,dtype", [("nh", "f64"), ("stvk", "f64"), ("nh", "f32")])
+def test_segmented_tile_caps(ctx, nt, model, dtype, monkeypatch):
+    """Every instance cap (threads per CTA) gives the oracle's result: many
+    small ragged tiles (n=9 -> 6000 tets over ~25-60 tiles)."""
+    monkeypatch.setenv("EBB_SEG_NT", nt)
+    case = Case(n=9, model=model, spread=0.1)
+    if dtype == "f32":
+        case.u = case.u.astype(np.float32).astype(np.float64)
+        case.mu = case.mu.astype(np.float32).astype(np.float64)
+        case.lam = case.lam.astype(np.float32).astype(np.float64)
+    fem = gpu_fem(ctx, case, dtype=dtype, name=f"mseg{nt}{model}{dtype}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, model)
+    fem.map_forces(model, scatter=SCATTERS["segmented"])
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    assert rel_l2(fem.f.read(), f) <= tol
+    assert rel_l2(fem.K.read(), K) <= tol
+    assert abs(fem.energy.get() - en) <= tol * abs(en)

@@ -34,7 +34,8 @@ def main():
     mu, lam = S.materials(tets.shape[0], 1e6, 0.3, spread=0.1)
     ctx = ebb.Context(0)
     fem = TetFEM(ctx, X, tets, dtype=a.dtype, mu=mu, lam=lam, free=free, u=S.twist_u(X, a.n, 6, free=free))
-    sid = {"atomic": A.SCATTER_ATOMIC, "tiled": A.SCATTER_TILED, "gather": A.SCATTER_GATHER}[a.scatter]
+    sid = {"atomic": A.SCATTER_ATOMIC, "tiled": A.SCATTER_TILED, "gather": A.SCATTER_GATHER,
+           "segmented": A.SCATTER_SEGMENTED}[a.scatter]
     for _ in range(a.reps):
         fem.map_forces(a.model, scatter=sid)
     torch.cuda.synchronize()

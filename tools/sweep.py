@@ -28,7 +28,8 @@ def _flush(buf):
     buf.zero_()
 
 
-def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000, kuhn_n=0):
+def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000, kuhn_n=0,
+           scatters=("segmented", "gather", "tiled", "atomic")):
     import numpy as np
     import torch
 
@@ -56,7 +57,10 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
         T, V, E = fem.nt, fem.nv, fem.ne
         bf = 4 if dt == "f32" else 8
         for model in models:
-            for scat, sid in (("gather", A.SCATTER_GATHER), ("tiled", A.SCATTER_TILED), ("atomic", A.SCATTER_ATOMIC)):
+            ids = {"segmented": A.SCATTER_SEGMENTED, "gather": A.SCATTER_GATHER, "tiled": A.SCATTER_TILED,
+                   "atomic": A.SCATTER_ATOMIC}
+            for scat in scatters:
+                sid = ids[scat]
                 fem.map_forces(model, scatter=sid)
                 torch.cuda.synchronize()
                 ctx.timing(True)
@@ -126,13 +130,18 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--c3-tets", type=int, default=10_000_000)
     ap.add_argument("--c2", action="store_true", help="the map sweep on the C2 Kuhn n=55 mesh")
+    ap.add_argument("--scatters", default="segmented,gather,tiled,atomic")
+    ap.add_argument("--dtypes", default="f32,f64")
+    ap.add_argument("--models", default="stvk,nh")
     a = ap.parse_args()
     from paper_1506_07577_b200 import build
     build.build()
     if a.c2:
-        run_c3(a.reps, kuhn_n=55)
+        run_c3(a.reps, kuhn_n=55, scatters=a.scatters.split(","), dtypes=a.dtypes.split(","),
+               models=a.models.split(","))
     if a.c3:
-        run_c3(a.reps, target=a.c3_tets)
+        run_c3(a.reps, target=a.c3_tets, scatters=a.scatters.split(","), dtypes=a.dtypes.split(","),
+               models=a.models.split(","))
     if a.c4:
         run_c4([int(x) for x in a.sizes.split(",")], a.reps)
 

@@ -334,7 +334,7 @@ def run_ours(args, rank, world, local_rank):
     d = kt[dom]
     ach = per_launch[dom] / (d["avg_us"] * 1e-6) / 1e9
     roof = {"kernel": {"cg_solve": "k_cg_persistent (all 50 PCG iterations, one launch)",
-                       "edge_matvec": "k_spmv_tma", "tet_map": "k_tet_map_tiled"}[dom],
+                       "edge_matvec": "k_spmv_tma", "tet_map": "k_tet_map_seg"}[dom],
             "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "peak_source": peak_src, "traffic": _ncu_traffic(dom), "algorithmic_bytes_per_launch": per_launch[dom],
             "bytes_model": "SURVEY 8(d): PCG iteration = E(9 b_f + 4) + V(4 + 6 b_f) + 33 V b_f, x 50 iterations"

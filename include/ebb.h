@@ -207,8 +207,8 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
 /* ---- the element map (hot path a4-a8) --------------------------------- */
 #define EBB_STVK 0
 #define EBB_NH 1
-#define EBB_SCATTER_AUTO 0      /* the measured fastest: GATHER, except StVK in
-                                   F64 -> TILED              */
+#define EBB_SCATTER_AUTO 0      /* the measured fastest: SEGMENTED (f + K);
+                                   force-only maps use ATOMIC */
 #define EBB_SCATTER_ATOMIC 1    /* per-tet red.global.add              */
 #define EBB_SCATTER_TILED 2     /* owner tiles, shared-memory atomic
                                    accumulation of every block                */

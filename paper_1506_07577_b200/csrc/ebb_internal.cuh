@@ -88,21 +88,18 @@ struct SegPlan {
     uint32_t ntiles = 0, max_ent = 0, max_items = 0;
     uint64_t ninst = 0, nslots = 0, nent = 0, nitems = 0;
     double host_ms = 0;               // plan build time (host)
-    uint32_t* tile_v = nullptr;       // ntiles + 1: first vertex of each tile
-    uint32_t* tile_inst = nullptr;    // ntiles + 1: instance offsets
-    uint32_t* tile_item = nullptr;    // ntiles + 1: item offsets (multiples of 32)
-    uint32_t* tile_ent = nullptr;     // ntiles + 1: entry offsets (multiples of 4)
+    uint4* tdesc = nullptr;           // ntiles + 1: {first vertex, instance offset, item offset
+                                      //   (multiple of 32), entry offset (multiple of 4)}
     uint32_t* inst_t = nullptr;       // ninst: tet id of each instance (ascending per tile)
-    uint32_t* item_meta = nullptr;    // nitems: begin[0:16) count[16:23) pos[23:26) last[26:29) force[29]
-    uint32_t* item_tgt = nullptr;     // nitems: slot (row items) or vertex (force items); ~0 = padding
-    uint32_t* crow = nullptr;         // nslots: global edge row of the slot
-    uint32_t* ctrow = nullptr;        // nslots: global edge row of its transpose
+    uint4* items = nullptr;           // nitems: {meta, row | vertex, transpose row, 0}; meta =
+                                      //   begin[0:16) count[16:23) pos[23:26) last[26:29) kind[29:31)
+                                      //   kind 0 off-diagonal row, 1 self row, 2 vertex force; row ~0 = padding
     uint32_t* ents = nullptr;         // nent: slot entries (lr << 8 | i << 6 | j << 4 | pair),
                                       //       force entries (lr << 2 | corner)
     void release() {
-        cudaFree(tile_v); cudaFree(tile_inst); cudaFree(tile_item); cudaFree(tile_ent); cudaFree(inst_t);
-        cudaFree(item_meta); cudaFree(item_tgt); cudaFree(crow); cudaFree(ctrow); cudaFree(ents);
-        tile_v = tile_inst = tile_item = tile_ent = inst_t = item_meta = item_tgt = crow = ctrow = ents = nullptr;
+        cudaFree(tdesc); cudaFree(inst_t); cudaFree(items); cudaFree(ents);
+        inst_t = ents = nullptr;
+        tdesc = items = nullptr;
     }
 };
 

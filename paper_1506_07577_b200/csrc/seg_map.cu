@@ -81,9 +81,10 @@ __device__ __forceinline__ void seg_load(uint32_t t, uint4 v, uint64_t nt, const
     in.lam = __ldg(lam_t + t);
 }
 
-// Adds one stored block (entry = (lr << 8) | (i << 6) | (j << 4) | pair) to acc:
+// Adds one stored off-diagonal block (entry = (lr << 8) | (i << 6) | (j << 4) | pair):
 //   NH   K_ij = W [ mu m_ij I + c1 k_j k_i^T + lam k_i k_j^T ]
 //   StVK K_ij = W [ s_ij I + mu (m_ij F F^T + h_j h_i^T) + lam h_i h_j^T ]
+// as K[a][b] += (W c1 k_j)[a] k_i[b] + (W lam k_i)[a] k_j[b] (+ the I and F F^T terms).
 template <typename R, int MODEL, int NT>
 __device__ __forceinline__ void seg_block(const R* __restrict__ st, uint32_t ent, R acc[9]) {
     using G = SegState<MODEL>;
@@ -92,7 +93,7 @@ __device__ __forceinline__ void seg_block(const R* __restrict__ st, uint32_t ent
     const R* sj = st + (G::KV + 3 * j) * NT + lr;
     const R ki[3] = {si[0], si[NT], si[2 * NT]};
     const R kj[3] = {sj[0], sj[NT], sj[2 * NT]};
-    R ca, cb, cc, cd = R(0), Bm[6];
+    R ca, cb, cc;
     if constexpr (MODEL == EBB_NH) {
         ca = st[(G::CM + p) * NT + lr];
         cb = st[G::C1 * NT + lr];
@@ -101,30 +102,64 @@ __device__ __forceinline__ void seg_block(const R* __restrict__ st, uint32_t ent
         ca = st[(G::WS + p) * NT + lr];
         cb = st[G::CH * NT + lr];
         cc = st[G::CL * NT + lr];
-        cd = st[(G::WM + p) * NT + lr];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) Bm[k] = st[(G::B + k) * NT + lr];
     }
+    const R uj[3] = {cb * kj[0], cb * kj[1], cb * kj[2]};
+    const R wi[3] = {cc * ki[0], cc * ki[1], cc * ki[2]};
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
-            R val = cb * kj[a] * ki[b] + cc * ki[a] * kj[b];
-            if (a == b) val += ca;
-            if constexpr (MODEL != EBB_NH) {
-                constexpr int bidx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-                val += cd * Bm[bidx[a][b]];
-            }
-            acc[3 * a + b] += val;
+            R v = fma(uj[a], ki[b], acc[3 * a + b]);
+            acc[3 * a + b] = fma(wi[a], kj[b], v);
         }
+    acc[0] += ca;
+    acc[4] += ca;
+    acc[8] += ca;
+    if constexpr (MODEL != EBB_NH) {
+        const R cd = st[(G::WM + p) * NT + lr];
+        constexpr int bidx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) acc[3 * a + b] = fma(cd, st[(G::B + bidx[a][b]) * NT + lr], acc[3 * a + b]);
+    }
+}
+
+// Adds one diagonal block K_ii (symmetric: 6 unique, acc = 00 01 02 11 12 22):
+//   NH   K_ii = W [ mu m_ii I + (c1 + lam) k_i k_i^T ]
+//   StVK K_ii = W [ s_ii I + mu m_ii F F^T + (mu + lam) h_i h_i^T ]
+template <typename R, int MODEL, int NT>
+__device__ __forceinline__ void seg_diag(const R* __restrict__ st, uint32_t ent, R acc[6]) {
+    using G = SegState<MODEL>;
+    const uint32_t lr = ent >> 8, i = (ent >> 6) & 3u, p = ent & 15u;
+    const R* si = st + (G::KV + 3 * i) * NT + lr;
+    const R k[3] = {si[0], si[NT], si[2 * NT]};
+    R ca, sc;
+    if constexpr (MODEL == EBB_NH) {
+        ca = st[(G::CM + p) * NT + lr];
+        sc = st[G::C1 * NT + lr] + st[G::CL * NT + lr];
+    } else {
+        ca = st[(G::WS + p) * NT + lr];
+        sc = st[G::CH * NT + lr] + st[G::CL * NT + lr];
+    }
+    const R v[3] = {sc * k[0], sc * k[1], sc * k[2]};
+    acc[0] = fma(v[0], k[0], acc[0] + ca);
+    acc[1] = fma(v[0], k[1], acc[1]);
+    acc[2] = fma(v[0], k[2], acc[2]);
+    acc[3] = fma(v[1], k[1], acc[3] + ca);
+    acc[4] = fma(v[1], k[2], acc[4]);
+    acc[5] = fma(v[2], k[2], acc[5] + ca);
+    if constexpr (MODEL != EBB_NH) {
+        const R cd = st[(G::WM + p) * NT + lr];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) acc[q] = fma(cd, st[(G::B + q) * NT + lr], acc[q]);
+    }
 }
 
 template <typename R, int MODEL, bool WANT_E, int NT>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
-    uint32_t ntiles, const uint32_t* __restrict__ tile_v, const uint32_t* __restrict__ tile_inst,
-    const uint32_t* __restrict__ tile_item, const uint32_t* __restrict__ tile_ent, const uint32_t* __restrict__ inst_t,
-    const uint32_t* __restrict__ item_meta, const uint32_t* __restrict__ item_tgt, const uint32_t* __restrict__ crow,
-    const uint32_t* __restrict__ ctrow, const uint32_t* __restrict__ ents, uint32_t max_ent, uint64_t nt,
+    uint32_t ntiles, const uint4* __restrict__ tdesc, const uint32_t* __restrict__ inst_t,
+    const uint4* __restrict__ items, const uint32_t* __restrict__ ents, uint32_t max_ent, uint64_t nt,
     const uint4* __restrict__ tv, const R* __restrict__ u, const R* __restrict__ Dminv, const R* __restrict__ Wt,
     const R* __restrict__ mu_t, const R* __restrict__ lam_t, R* __restrict__ f, R* __restrict__ K, uint64_t ne,
     int accumulate, double* __restrict__ partials, unsigned int* __restrict__ counter, R* __restrict__ energy,
@@ -133,56 +168,83 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
     extern __shared__ __align__(16) unsigned char seg_smem[];
     R* st = reinterpret_cast<R*>(seg_smem);                                // [SW][NT]
     uint32_t* ebuf = reinterpret_cast<uint32_t*>(st + (size_t)G::SW * NT);  // [2][max_ent]
-    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(16) uint4 dring[64][2];   // descriptors {v0, inst0, item0, ent0} of local tile j
+                                                   // and of its successor (= its ends), slot j & 63
+    __shared__ __align__(8) uint64_t bar[2];       // entry buffers 0/1
     const uint32_t tid = threadIdx.x, G0 = gridDim.x;
+    // this CTA's tiles: blockIdx.x + j G0 -- all CTAs sweep the SFC order
+    // together, so the tets and rows shared by neighbouring tiles meet in L2
+    const uint32_t tile0 = blockIdx.x;
+    const uint32_t m = tile0 < ntiles ? (ntiles - tile0 + G0 - 1) / G0 : 0;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
+    // descriptor ring: warp 0 copies (cp.async, no registers held) 32 tiles
+    // ahead; the copies complete (wait_group) 16 tiles before their first use
+    auto ring_fill = [&](uint32_t j) {   // warp 0, lane l: local tile j + l
+        const uint32_t jj = j + (tid & 31);
+        if (jj < m) {
+            const uint32_t t = tile0 + jj * G0;
+            const uint32_t d = smem_addr(&dring[jj & 63][0]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(tdesc + t) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16), "l"(tdesc + t + 1) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (tid < 32) {
+        ring_fill(0);
+        ring_fill(32);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
-    auto stage = [&](uint32_t tile, int b) {   // thread 0: bulk copy of a tile's entry lists
-        const uint32_t e0 = __ldg(tile_ent + tile), bytes = (__ldg(tile_ent + tile + 1) - e0) * 4u;
+    auto D = [&](uint32_t j) -> uint4 { return dring[j & 63][0]; };
+    auto Dn = [&](uint32_t j) -> uint4 { return dring[j & 63][1]; };
+    auto stage = [&](uint32_t j, int b) {   // thread 0: bulk copy of tile j's entry lists
+        const uint32_t e0 = D(j).w, bytes = (Dn(j).w - e0) * 4u;
         mbar_arrive_expect_tx(&bar[b], bytes);
         if (bytes) bulk_g2s(ebuf + (size_t)b * max_ent, ents + e0, bytes, &bar[b]);
     };
-    auto inst_of = [&](uint32_t tile) -> uint32_t {
-        if (tile >= ntiles) return 0xFFFFFFFFu;
-        const uint32_t i0 = __ldg(tile_inst + tile), n = __ldg(tile_inst + tile + 1) - i0;
+    auto inst_of = [&](uint32_t j) -> uint32_t {
+        if (j >= m) return 0xFFFFFFFFu;
+        const uint32_t i0 = D(j).y, n = Dn(j).y - i0;
         return tid < n ? __ldg(inst_t + i0 + tid) : 0xFFFFFFFFu;
     };
     auto verts_of = [&](uint32_t t) -> uint4 { return t == 0xFFFFFFFFu ? make_uint4(0, 0, 0, 0) : __ldg(tv + t); };
 
     // first pass of a tile's phase-2 items, loaded one tile ahead
-    uint32_t it0_n = 0, nit_n = 0, meta_n = 0, tgt_n = 0xFFFFFFFFu;
-    auto item_head = [&](uint32_t tile) {
+    const uint4 no_item = make_uint4(0, 0xFFFFFFFFu, 0xFFFFFFFFu, 0);
+    uint32_t it0_n = 0, nit_n = 0;
+    uint4 item_n = no_item;
+    auto item_head = [&](uint32_t j) {
         it0_n = 0;
         nit_n = 0;
-        meta_n = 0;
-        tgt_n = 0xFFFFFFFFu;
-        if (tile >= ntiles) return;
-        it0_n = __ldg(tile_item + tile);
-        nit_n = __ldg(tile_item + tile + 1) - it0_n;
-        if (tid < nit_n) {
-            meta_n = __ldg(item_meta + it0_n + tid);
-            tgt_n = __ldg(item_tgt + it0_n + tid);
-        }
+        item_n = no_item;
+        if (j >= m) return;
+        it0_n = D(j).z;
+        nit_n = Dn(j).z - it0_n;
+        if (tid < nit_n) item_n = __ldg(items + it0_n + tid);
     };
-    const uint32_t tile0 = blockIdx.x;
-    if (tid == 0 && tile0 < ntiles) stage(tile0, 0);
-    item_head(tile0);
+    if (tid == 0 && m > 0) stage(0, 0);
+    item_head(0);
     // software pipeline: inputs of this tile, keys of the next, tet id of the one after
-    uint32_t tc = inst_of(tile0);
+    uint32_t tc = inst_of(0);
     uint4 vc = verts_of(tc);
     SegIn<R> in;
     seg_load(tc, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
-    uint32_t t1 = inst_of(tile0 + G0);
+    uint32_t t1 = inst_of(1);
     uint4 v1 = verts_of(t1);
-    uint32_t t2 = inst_of(tile0 + 2 * G0);
+    uint32_t t2 = inst_of(2);
     double e_acc = 0.0;
-    uint32_t k = 0;
-    for (uint32_t tile = tile0; tile < ntiles; tile += G0, ++k) {
-        const uint32_t va = __ldg(tile_v + tile), vb = __ldg(tile_v + tile + 1);
+    for (uint32_t j = 0; j < m; ++j) {
+        const uint32_t k = j;
+        // descriptor ring: copy [j + 32, j + 64) at j = 32 r, complete at j = 32 r + 16
+        if (tid < 32) {
+            if ((j & 31) == 0 && j > 0) ring_fill(j + 32);
+            if ((j & 31) == 16) asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        const uint32_t va = D(j).x, vb = Dn(j).x;
         // ---- phase 1: this thread's instance -> compact state
         if (tc != 0xFFFFFFFFu) {
             TetState<R> ts;
@@ -247,15 +309,15 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
         seg_load(tc, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
         t1 = t2;
         v1 = verts_of(t1);
-        t2 = inst_of(tile + 3 * G0);
-        if (tid == 0 && tile + G0 < ntiles) {
+        t2 = inst_of(j + 3);
+        if (tid == 0 && j + 1 < m) {
             fence_proxy_async_smem();
-            stage(tile + G0, (k + 1) & 1);
+            stage(j + 1, (k + 1) & 1);
         }
         // phase-2 work list of this tile (its first pass was loaded one tile ahead)
         const uint32_t it0 = it0_n, nit = nit_n;
-        uint32_t meta = meta_n, tgt = tgt_n;
-        item_head(tile + G0);
+        uint4 item = item_n;
+        item_head(j + 1);
         __syncthreads();   // state complete
         const int b = k & 1;
         mbar_wait(&bar[b], (k >> 1) & 1);
@@ -264,21 +326,14 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
         // the chunks of a list sit in consecutive lanes and are combined by a
         // shuffle tree (items are padded to whole warps: the loop is warp-uniform)
         for (uint32_t base = 0; base < nit; base += NT) {
-            if (base) {
-                meta = 0;
-                tgt = 0xFFFFFFFFu;
-                if (base + tid < nit) {
-                    meta = __ldg(item_meta + it0 + base + tid);
-                    tgt = __ldg(item_tgt + it0 + base + tid);
-                }
-            }
+            if (base) item = base + tid < nit ? __ldg(items + it0 + base + tid) : no_item;
+            const uint32_t meta = item.x;
             const uint32_t e0 = meta & 0xFFFFu, e1 = e0 + ((meta >> 16) & 0x7Fu);
-            const uint32_t pos = (meta >> 23) & 7u, last = (meta >> 26) & 7u;
-            const bool force = (meta >> 29) & 1u;
+            const uint32_t pos = (meta >> 23) & 7u, last = (meta >> 26) & 7u, kind = (meta >> 29) & 3u;
             R a9[9];
 #pragma unroll
             for (int q = 0; q < 9; ++q) a9[q] = R(0);
-            if (!force) {
+            if (kind == 0) {
                 uint32_t e = e0;
                 for (; e + 1 < e1; e += 2) {
                     const uint32_t x = E[e], y = E[e + 1];
@@ -286,6 +341,14 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
                     seg_block<R, MODEL, NT>(st, y, a9);
                 }
                 if (e < e1) seg_block<R, MODEL, NT>(st, E[e], a9);
+            } else if (kind == 1) {
+                uint32_t e = e0;
+                for (; e + 1 < e1; e += 2) {
+                    const uint32_t x = E[e], y = E[e + 1];
+                    seg_diag<R, MODEL, NT>(st, x, a9);
+                    seg_diag<R, MODEL, NT>(st, y, a9);
+                }
+                if (e < e1) seg_diag<R, MODEL, NT>(st, E[e], a9);
             } else {
                 for (uint32_t e = e0; e < e1; ++e) {
                     const uint32_t en = E[e], lr = en >> 2, kk = en & 3u;
@@ -294,39 +357,41 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
                     a9[2] += st[(G::F + 3 * kk + 2) * NT + lr];
                 }
             }
-            const bool all_force = __all_sync(0xFFFFFFFFu, force);
+            // combine the chunks of a list (values live: 9 / 6 / 3 by kind)
+            const uint32_t nval = __reduce_max_sync(0xFFFFFFFFu, kind == 0 ? 9u : kind == 1 ? 6u : 3u);
 #pragma unroll
             for (uint32_t step = 1; step < 8; step <<= 1) {
                 if (!__any_sync(0xFFFFFFFFu, last >= step)) break;
                 const bool take = pos + step <= last;
 #pragma unroll
-                for (int q = 0; q < 9; ++q) {
-                    if (all_force && q >= 3) break;
+                for (uint32_t q = 0; q < 9; ++q) {
+                    if (q >= nval) break;
                     const R o = __shfl_down_sync(0xFFFFFFFFu, a9[q], step);
                     if (take) a9[q] += o;
                 }
             }
-            if (pos == 0 && tgt != 0xFFFFFFFFu) {
-                if (!force) {
-                    const uint32_t r = __ldg(crow + tgt), rt = __ldg(ctrow + tgt);
+            if (pos == 0 && item.y != 0xFFFFFFFFu) {
+                if (kind == 2) {
+                    R* dst = f + 3ull * item.y;
 #pragma unroll
-                    for (int q = 0; q < 9; ++q) {
-                        R* dst = K + (uint64_t)q * ne + r;
-                        *dst = accumulate ? *dst + a9[q] : a9[q];
+                    for (int a = 0; a < 3; ++a) dst[a] = accumulate ? dst[a] + a9[a] : a9[a];
+                } else {
+                    if (kind == 1) {   // symmetric self block: expand 00 01 02 11 12 22
+                        const R d[6] = {a9[0], a9[1], a9[2], a9[3], a9[4], a9[5]};
+                        a9[0] = d[0]; a9[1] = d[1]; a9[2] = d[2];
+                        a9[3] = d[1]; a9[4] = d[3]; a9[5] = d[4];
+                        a9[6] = d[2]; a9[7] = d[4]; a9[8] = d[5];
                     }
-                    if (rt != r) {
+                    R* dst = K + item.y;
+#pragma unroll
+                    for (int q = 0; q < 9; ++q, dst += ne) *dst = accumulate ? *dst + a9[q] : a9[q];
+                    if (kind == 0) {
+                        dst = K + item.z;
 #pragma unroll
                         for (int a = 0; a < 3; ++a)
 #pragma unroll
-                            for (int c = 0; c < 3; ++c) {
-                                R* dst = K + (uint64_t)(3 * a + c) * ne + rt;
-                                *dst = accumulate ? *dst + a9[3 * c + a] : a9[3 * c + a];
-                            }
+                            for (int c = 0; c < 3; ++c, dst += ne) *dst = accumulate ? *dst + a9[3 * c + a] : a9[3 * c + a];
                     }
-                } else {
-                    R* dst = f + 3ull * tgt;
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) dst[a] = accumulate ? dst[a] + a9[a] : a9[a];
                 }
             }
         }
@@ -349,7 +414,7 @@ uint32_t lower_bound_u32(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t x
 }
 
 template <typename T>
-ebb_status upload(Ctx* c, const std::vector<T>& h, uint32_t** d) {
+ebb_status upload(Ctx* c, const std::vector<T>& h, T** d) {
     EBB_CUDA(c, cudaMalloc((void**)d, h.size() * sizeof(T) + 16));
     if (!h.empty()) EBB_CUDA(c, cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
     return EBB_OK;
@@ -418,7 +483,10 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         if (nv > 0) tile_v.push_back((uint32_t)nv);
     }
     const uint32_t ntiles = (uint32_t)tile_v.size() - 1;
-    std::vector<uint32_t> tile_inst{0}, tile_item{0}, tile_ent{0}, inst_t, item_meta, item_tgt, crow, ctrow, ents;
+    std::vector<uint32_t> tile_inst{0}, tile_item{0}, tile_ent{0}, inst_t, ents;
+    std::vector<uint4> tdesc;
+    std::vector<uint4> items;
+    std::vector<uint32_t> srow, strow;   // per slot of the current tile: row, transpose row
     inst_t.reserve(nt * 2);
     ents.reserve(nt * 30);
     std::vector<uint32_t> lr_of(nt, 0xFFFFFFFFu);
@@ -460,14 +528,28 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
             for (uint32_t kk = 0; kk < 4; ++kk)
                 if (vv[kk] >= a && vv[kk] < b) lists[ns + vv[kk] - a].push_back((l << 2) | kk);
         }
-        // entries: slot lists (by descending length), then force lists, padded to 16 B
-        order.resize(ns);
-        for (uint32_t s = 0; s < ns; ++s) order[s] = s;
-        std::stable_sort(order.begin(), order.end(),
+        // rows of the slots
+        srow.resize(ns);
+        strow.resize(ns);
+        for (uint32_t lv = 0; lv < nvl; ++lv)
+            for (uint32_t s = sbase[lv]; s < sbase[lv + 1]; ++s) {
+                const uint32_t tail = a + lv, r = rself[tail] + (s - sbase[lv]), hd = head[r];
+                srow[s] = r;
+                strow[s] = hd == tail ? r : lower_bound_u32(head.data(), index[hd], index[hd + 1], tail);
+            }
+        // work lists in kind order: self rows (1), off-diagonal rows by
+        // descending length (0), vertex forces (2); entries in the same order
+        order.clear();
+        for (uint32_t lv = 0; lv < nvl; ++lv) order.push_back(sbase[lv]);
+        const size_t n_self = order.size();
+        for (uint32_t lv = 0; lv < nvl; ++lv)
+            for (uint32_t s = sbase[lv] + 1; s < sbase[lv + 1]; ++s) order.push_back(s);
+        std::stable_sort(order.begin() + n_self, order.end(),
                          [&](uint32_t x, uint32_t y) { return lists[x].size() > lists[y].size(); });
+        const size_t n_rows = order.size();
         for (uint32_t v = 0; v < nvl; ++v) order.push_back(ns + v);
+        auto kind_of = [&](size_t qi) -> uint32_t { return qi < n_self ? 1u : qi < n_rows ? 0u : 2u; };
         const size_t e_base = ents.size();
-        const uint32_t slot_g0 = (uint32_t)crow.size();
         lbeg.assign(ns + nvl, 0);
         size_t tot = 0, longest = 0;
         for (uint32_t q : order) {
@@ -480,58 +562,47 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         const uint32_t nent = (uint32_t)(ents.size() - e_base);
         if (nent >= 65536)
             return fail(c, EBB_E_RANGE, "segmented map: tile %u has %u entries (> 65535)", T, nent);
-        // slots -> rows (global slot = slot_g0 + position in `order`)
-        for (uint32_t q = 0; q < ns; ++q) {
-            const uint32_t s = order[q];
-            const uint32_t lv = (uint32_t)(std::upper_bound(sbase.begin(), sbase.end(), s) - sbase.begin()) - 1;
-            const uint32_t tail = a + lv, r = rself[tail] + (s - sbase[lv]), hd = head[r];
-            crow.push_back(r);
-            ctrow.push_back(hd == tail ? r : lower_bound_u32(head.data(), index[hd], index[hd + 1], tail));
-        }
-        // items: chunks of <= L entries (L ~ the even share per thread), at most
-        // 8 chunks per list, the chunks of one list never straddle a warp
         // chunk cap L: the smallest (from the even share per thread) whose
-        // warp-padded item list fits one pass of the CTA; at most 8 chunks a list
-        auto count_items = [&](size_t L) {
+        // warp-padded item list fits one pass of the CTA; at most 8 chunks a
+        // list, the chunks of a list never straddle a warp, kinds start a warp
+        auto layout = [&](size_t L, bool emit) {
             size_t n = 0;
-            for (uint32_t q : order) {
-                const size_t cnt = lists[q].size(), nc = cnt == 0 ? 1 : (cnt + L - 1) / L;
-                if ((n % 32) + nc > 32) n = (n + 31) / 32 * 32;
-                n += nc;
+            auto pad = [&]() {
+                while (n % 32) {
+                    if (emit) items.push_back(make_uint4(0, 0xFFFFFFFFu, 0xFFFFFFFFu, 0));
+                    ++n;
+                }
+            };
+            for (size_t qi = 0; qi < order.size(); ++qi) {
+                if (qi > 0 && kind_of(qi) != kind_of(qi - 1)) pad();
+                const uint32_t q = order[qi], kind = kind_of(qi);
+                const uint32_t cnt = (uint32_t)lists[q].size();
+                const uint32_t nc = cnt == 0 ? 1 : (uint32_t)((cnt + L - 1) / L);
+                if ((n % 32) + nc > 32) pad();
+                uint32_t beg = lbeg[q];
+                for (uint32_t cc = 0; cc < nc; ++cc, ++n) {
+                    const uint32_t sz = cnt / nc + (cc < cnt % nc ? 1 : 0);
+                    if (emit) {
+                        const uint32_t meta = beg | (sz << 16) | (cc << 23) | ((nc - 1) << 26) | (kind << 29);
+                        items.push_back(kind == 2 ? make_uint4(meta, a + (q - ns), 0, 0)
+                                                  : make_uint4(meta, srow[q], strow[q], 0));
+                    }
+                    beg += sz;
+                }
             }
-            return (n + 31) / 32 * 32;
+            pad();
+            return n;
         };
         size_t L = std::max<size_t>({(size_t)2, (tot + ni - 1) / ni, (longest + 7) / 8});
-        while (L < longest && count_items(L) > (size_t)ni) ++L;
+        while (L < longest && layout(L, false) > (size_t)ni) ++L;
         if (L > 127) return fail(c, EBB_E_RANGE, "segmented map: a list of %zu entries (> 8 x 127)", longest);
-        const size_t it_base = item_meta.size();
-        for (uint32_t qi = 0; qi < order.size(); ++qi) {
-            const uint32_t q = order[qi];
-            const bool force = q >= ns;
-            const uint32_t cnt = (uint32_t)lists[q].size();
-            const uint32_t nc = cnt == 0 ? 1 : (uint32_t)((cnt + L - 1) / L);
-            if (((item_meta.size() - it_base) % 32) + nc > 32)
-                while ((item_meta.size() - it_base) % 32) {
-                    item_meta.push_back(0);
-                    item_tgt.push_back(0xFFFFFFFFu);
-                }
-            uint32_t beg = lbeg[q];
-            for (uint32_t cc = 0; cc < nc; ++cc) {
-                const uint32_t sz = cnt / nc + (cc < cnt % nc ? 1 : 0);
-                item_meta.push_back(beg | (sz << 16) | (cc << 23) | ((nc - 1) << 26) | ((force ? 1u : 0u) << 29));
-                item_tgt.push_back(force ? a + (q - ns) : slot_g0 + qi);
-                beg += sz;
-            }
-        }
-        while ((item_meta.size() - it_base) % 32) {
-            item_meta.push_back(0);
-            item_tgt.push_back(0xFFFFFFFFu);
-        }
+        const size_t it_base = items.size();
+        layout(L, true);
         for (uint32_t l = 0; l < ninst; ++l) lr_of[inst_t[i0 + l]] = 0xFFFFFFFEu;   // never a tile id
         max_ent = std::max(max_ent, nent);
-        max_items = std::max(max_items, (uint32_t)(item_meta.size() - it_base));
+        max_items = std::max(max_items, (uint32_t)(items.size() - it_base));
         tile_inst.push_back((uint32_t)inst_t.size());
-        tile_item.push_back((uint32_t)item_meta.size());
+        tile_item.push_back((uint32_t)items.size());
         tile_ent.push_back((uint32_t)ents.size());
     }
     SegPlan* P = new SegPlan();
@@ -542,22 +613,17 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
     P->max_ent = max_ent;
     P->max_items = max_items;
     P->ninst = inst_t.size();
-    P->nslots = crow.size();
+    P->nslots = 0;
     P->nent = ents.size();
-    P->nitems = item_meta.size();
+    P->nitems = items.size();
     ebb_status s = EBB_OK;
     auto up = [&](const std::vector<uint32_t>& h, uint32_t** d) {
         if (s == EBB_OK) s = upload(c, h, d);
     };
-    up(tile_v, &P->tile_v);
-    up(tile_inst, &P->tile_inst);
-    up(tile_item, &P->tile_item);
-    up(tile_ent, &P->tile_ent);
+    for (uint32_t T = 0; T <= ntiles; ++T) tdesc.push_back(make_uint4(tile_v[T], tile_inst[T], tile_item[T], tile_ent[T]));
+    if (s == EBB_OK) s = upload(c, tdesc, &P->tdesc);
     up(inst_t, &P->inst_t);
-    up(item_meta, &P->item_meta);
-    up(item_tgt, &P->item_tgt);
-    up(crow, &P->crow);
-    up(ctrow, &P->ctrow);
+    if (s == EBB_OK) s = upload(c, items, &P->items);
     up(ents, &P->ents);
     if (s != EBB_OK) {
         P->release();
@@ -583,10 +649,11 @@ ebb_status launch_seg_t(Ctx* c, const SegPlan& P, bool want_e, int accumulate, u
         EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured[want_e] = smem;
     }
-    const unsigned grid = occ_grid(c, kern, NT, smem, (uint64_t)P.ntiles * NT);
+    unsigned grid = occ_grid(c, kern, NT, smem, (uint64_t)P.ntiles * NT);
+    const char* eg = getenv("EBB_SEG_GRID");   // test knob: fewer CTAs = longer tile runs per CTA
+    if (eg && atoi(eg) > 0 && (unsigned)atoi(eg) < grid) grid = (unsigned)atoi(eg);
     KernelTimer kt(c, EBB_K_TET_MAP, s);
-    kern<<<grid, NT, smem, s>>>(P.ntiles, P.tile_v, P.tile_inst, P.tile_item, P.tile_ent, P.inst_t, P.item_meta,
-                                P.item_tgt, P.crow, P.ctrow, P.ents, P.max_ent, nt, (const uint4*)V->ptr,
+    kern<<<grid, NT, smem, s>>>(P.ntiles, P.tdesc, P.inst_t, P.items, P.ents, P.max_ent, nt, (const uint4*)V->ptr,
                                 (const R*)U->ptr, (const R*)D->ptr, (const R*)W->ptr, (const R*)MU->ptr,
                                 (const R*)LA->ptr, (R*)Fo->ptr, (R*)Ko->ptr, ne, accumulate, c->d_partials,
                                 c->d_counter + 0, En ? (R*)En->ptr : nullptr, c->d_err);

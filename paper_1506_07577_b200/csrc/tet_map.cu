@@ -1198,12 +1198,11 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     cudaStream_t s = (cudaStream_t)stream;
     const char* envs = getenv("EBB_SCATTER");
     int strat = d->scatter;
-    // AUTO = the measured fastest on C2: GATHER for f + K,
-    // except StVK in fp64 (its double-buffered state only fits 128-instance
-    // rounds) where TILED wins
+    // AUTO = the measured fastest on C2 and C3: SEGMENTED for
+    // f + K (every dtype and model); the force-only map is the atomic kernel
     if (strat == EBB_SCATTER_AUTO) {
         if (envs && atoi(envs) > 0) strat = atoi(envs);
-        else strat = (dt == EBB_F64 && d->model == EBB_STVK) ? EBB_SCATTER_TILED : EBB_SCATTER_GATHER;
+        else strat = EBB_SCATTER_SEGMENTED;
     }
     if (Ko && strat == EBB_SCATTER_SEGMENTED) {
         // every K row and f row is written exactly once: zero_outputs means overwrite

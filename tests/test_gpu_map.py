@@ -190,3 +190,19 @@ def test_segmented_tile_caps(ctx, nt, model, dtype, monkeypatch):
     assert rel_l2(fem.f.read(), f) <= tol
     assert rel_l2(fem.K.read(), K) <= tol
     assert abs(fem.energy.get() - en) <= tol * abs(en)
+
+
+@pytest.mark.parametrize("grid", ["1", "3"])
+def test_segmented_long_tile_runs(ctx, grid, monkeypatch):
+    """A few CTAs walking hundreds of consecutive tiles each (descriptor ring
+    refilled every 32 tiles, entry buffers and the register pipeline wrapping
+    many times) give the oracle's result."""
+    monkeypatch.setenv("EBB_SEG_GRID", grid)
+    case = Case(n=16, model="nh", spread=0.1)
+    fem = gpu_fem(ctx, case, name=f"mseggrid{grid}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, "nh")
+    fem.map_forces("nh", scatter=SCATTERS["segmented"])
+    assert rel_l2(fem.f.read(), f) <= 1e-12
+    assert rel_l2(fem.K.read(), K) <= 1e-12
+    assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)

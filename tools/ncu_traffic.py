@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""Per-launch DRAM traffic of the bench's kernels from an `ncu --set full`
+capture of the bench command -> profiles/ncu_traffic.json (read by bench.py
+for the roofline `traffic` field).
+
+    python tools/ncu_traffic.py <capture.ncu-rep> [workload=C2]
+"""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+KEYS = {"cg_solve": "k_cg_persistent", "tet_map": "k_tet_map_seg", "edge_matvec": "k_spmv"}
+
+
+def main():
+    path = sys.argv[1]
+    workload = sys.argv[2] if len(sys.argv) > 2 else "C2"
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    acc = collections.defaultdict(list)
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        name = d.get("Kernel Name", "")
+        for key, pat in KEYS.items():
+            if pat in name:
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                b = 0.0
+                for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    u = units[h.index(m)]
+                    b += float(d[m].replace(",", "")) * scale.get(u, 1)
+                acc[key].append((b, name, float(d["gpu__time_duration.sum"].replace(",", ""))))
+    res = {}
+    for key, v in acc.items():
+        res[key] = {"workload": workload, "dram_bytes_per_launch": sum(x[0] for x in v) / len(v),
+                    "launches_captured": len(v), "ncu_kernel": v[0][1][:100], "capture": os.path.basename(path),
+                    "ncu_duration_each": [x[2] for x in v],
+                    "note": "ncu --set full --clock-control none (replayed, cold cache per pass)"}
+    dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+    old = {}
+    if os.path.exists(dst):
+        old = json.load(open(dst))
+    old.update(res)
+    json.dump(old, open(dst, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()

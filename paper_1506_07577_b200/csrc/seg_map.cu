@@ -156,8 +156,12 @@ __device__ __forceinline__ void seg_diag(const R* __restrict__ st, uint32_t ent,
     }
 }
 
+// CTAs per SM at NT = 256: two CTAs overlap one's barrier tail with the
+// other's work; fp32 state leaves room for a third (fp64 would spill) -- measured
+template <typename R>
+constexpr int seg_min_blocks() { return sizeof(R) == 4 ? 3 : 2; }
 template <typename R, int MODEL, bool WANT_E, int NT>
-__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
+__global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet_map_seg(
     uint32_t ntiles, const uint4* __restrict__ tdesc, const uint32_t* __restrict__ inst_t,
     const uint4* __restrict__ items, const uint32_t* __restrict__ ents, uint32_t max_ent, uint64_t nt,
     const uint4* __restrict__ tv, const R* __restrict__ u, const R* __restrict__ Dminv, const R* __restrict__ Wt,
@@ -333,28 +337,34 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_tet_map_seg(
             R a9[9];
 #pragma unroll
             for (int q = 0; q < 9; ++q) a9[q] = R(0);
+            // entry e + 1 is loaded while block e is rebuilt (the state loads
+            // of a block depend only on its own entry)
             if (kind == 0) {
-                uint32_t e = e0;
-                for (; e + 1 < e1; e += 2) {
-                    const uint32_t x = E[e], y = E[e + 1];
-                    seg_block<R, MODEL, NT>(st, x, a9);
-                    seg_block<R, MODEL, NT>(st, y, a9);
-                }
-                if (e < e1) seg_block<R, MODEL, NT>(st, E[e], a9);
-            } else if (kind == 1) {
-                uint32_t e = e0;
-                for (; e + 1 < e1; e += 2) {
-                    const uint32_t x = E[e], y = E[e + 1];
-                    seg_diag<R, MODEL, NT>(st, x, a9);
-                    seg_diag<R, MODEL, NT>(st, y, a9);
-                }
-                if (e < e1) seg_diag<R, MODEL, NT>(st, E[e], a9);
-            } else {
+                uint32_t x = e0 < e1 ? E[e0] : 0u;
+#pragma unroll 2
                 for (uint32_t e = e0; e < e1; ++e) {
-                    const uint32_t en = E[e], lr = en >> 2, kk = en & 3u;
+                    const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
+                    seg_block<R, MODEL, NT>(st, x, a9);
+                    x = nx;
+                }
+            } else if (kind == 1) {
+                uint32_t x = e0 < e1 ? E[e0] : 0u;
+#pragma unroll 2
+                for (uint32_t e = e0; e < e1; ++e) {
+                    const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
+                    seg_diag<R, MODEL, NT>(st, x, a9);
+                    x = nx;
+                }
+            } else {
+                uint32_t x = e0 < e1 ? E[e0] : 0u;
+#pragma unroll 2
+                for (uint32_t e = e0; e < e1; ++e) {
+                    const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
+                    const uint32_t lr = x >> 2, kk = x & 3u;
                     a9[0] += st[(G::F + 3 * kk + 0) * NT + lr];
                     a9[1] += st[(G::F + 3 * kk + 1) * NT + lr];
                     a9[2] += st[(G::F + 3 * kk + 2) * NT + lr];
+                    x = nx;
                 }
             }
             // combine the chunks of a list (values live: 9 / 6 / 3 by kind)

@@ -246,6 +246,11 @@ typedef struct {
  * one dtype (F32 or F64) and the documented layouts: u, f AOS; Dminv, K SOA.
  * EBB_E_PHASE if u aliases f or K, or f aliases K. */
 ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_stream s);
+/* Statistics of the SEGMENTED map plan built for (v, e) (0 if none yet):
+ * out = {tiles, instances, instances / tets (redundancy), entries, items,
+ *        instance cap per tile, host build ms, largest tile's entries}.
+ * Host-only; no device work. */
+ebb_status ebb_map_plan_stats(ebb_ctx ctx, ebb_field v, ebb_field e, double out[8]);
 
 /* a10: q_v = sum_{e in [index[v], index[v+1])} A_e p_head(e)  (query-loop over
  * v.edges), q *= mask (optional U8 on verts), and optionally

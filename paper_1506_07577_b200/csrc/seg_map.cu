@@ -712,3 +712,25 @@ ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool wa
 }
 
 }  // namespace ebb
+
+extern "C" ebb_status ebb_map_plan_stats(ebb_ctx ctx, ebb_field v, ebb_field e, double out[8]) {
+    using namespace ebb;
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !out) return EBB_E_ARG;
+    for (int k = 0; k < 8; ++k) out[k] = 0;
+    Field* V = get_field(c, v);
+    if (!V) return fail(c, EBB_E_ARG, "map_plan_stats: bad field handle");
+    const double nt = (double)c->rels[V->rel].size;
+    for (SegPlan* P : c->segplans)
+        if (P->v == v && P->e == e) {
+            out[0] = P->ntiles;
+            out[1] = (double)P->ninst;
+            out[2] = nt > 0 ? (double)P->ninst / nt : 0;
+            out[3] = (double)P->nent;
+            out[4] = (double)P->nitems;
+            out[5] = P->ni;
+            out[6] = P->host_ms;
+            out[7] = P->max_ent;
+        }
+    return EBB_OK;
+}

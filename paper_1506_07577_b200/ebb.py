@@ -67,6 +67,14 @@ class Context:
         self.check(self.L.ebb_error_counts(self.h, out, int(reset)))
         return dict(inverted=out[0], not_spd=out[1], bounds=out[2])
 
+    def map_plan_stats(self, v, e):
+        """Statistics of the SEGMENTED map plan for key-fields (v, e)."""
+        out = (C.c_double * 8)()
+        self.check(self.L.ebb_map_plan_stats(self.h, int(v), int(e), out))
+        keys = ("tiles", "instances", "redundancy", "entries", "items", "instance_cap", "host_build_ms",
+                "max_tile_entries")
+        return dict(zip(keys, list(out)))
+
     def timing(self, on=True):
         self.check(self.L.ebb_timing_enable(self.h, int(on)))
 

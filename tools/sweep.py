@@ -72,7 +72,8 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
                 ctx.timing(False)
                 us = 1e3 * ms / nl
                 b = bench.bytes_map(T, V, E, bf)
-                print(json.dumps({"workload": wl, "mesh": mname, "tets": T, "verts": V, "edge_rows": E,
+                plan = fem.plan_stats() if scat == "segmented" else None
+                print(json.dumps({"plan": plan, "workload": wl, "mesh": mname, "tets": T, "verts": V, "edge_rows": E,
                                   "dtype": dt, "model": model, "scatter": scat, "avg_us": us,
                                   "tets_per_s": T / (us * 1e-6), "algorithmic_bytes": b,
                                   "hbm_frac": b / (us * 1e-6) / 1e9 / peak, "peak_gbs": peak, "peak_source": src}),

@@ -94,8 +94,9 @@ struct SegPlan {
     uint4* items = nullptr;           // nitems: {meta, row | vertex, transpose row, 0}; meta =
                                       //   begin[0:16) count[16:23) pos[23:26) last[26:29) kind[29:31)
                                       //   kind 0 off-diagonal row, 1 self row, 2 vertex force; row ~0 = padding
-    uint32_t* ents = nullptr;         // nent: slot entries (lr << 8 | i << 6 | j << 4 | pair),
-                                      //       force entries (lr << 2 | corner)
+    uint32_t* ents = nullptr;         // nent: block entries oi | oj << 13 | pair << 26 (oi, oj =
+                                      //   3 i NT + lr, 3 j NT + lr: state word offsets of k_i, k_j),
+                                      //   force entries 3 corner NT + lr (offset of f_corner)
     void release() {
         cudaFree(tdesc); cudaFree(inst_t); cudaFree(items); cudaFree(ents);
         inst_t = ents = nullptr;

@@ -81,16 +81,18 @@ __device__ __forceinline__ void seg_load(uint32_t t, uint4 v, uint64_t nt, const
     in.lam = __ldg(lam_t + t);
 }
 
-// Adds one stored off-diagonal block (entry = (lr << 8) | (i << 6) | (j << 4) | pair):
+// Adds one stored off-diagonal block (entry = oi | oj << 13 | pair << 26 with
+// oi = 3 i NT + lr, oj = 3 j NT + lr the word offsets of k_i, k_j in the state):
 //   NH   K_ij = W [ mu m_ij I + c1 k_j k_i^T + lam k_i k_j^T ]
 //   StVK K_ij = W [ s_ij I + mu (m_ij F F^T + h_j h_i^T) + lam h_i h_j^T ]
 // as K[a][b] += (W c1 k_j)[a] k_i[b] + (W lam k_i)[a] k_j[b] (+ the I and F F^T terms).
 template <typename R, int MODEL, int NT>
 __device__ __forceinline__ void seg_block(const R* __restrict__ st, uint32_t ent, R acc[9]) {
     using G = SegState<MODEL>;
-    const uint32_t lr = ent >> 8, i = (ent >> 6) & 3u, j = (ent >> 4) & 3u, p = ent & 15u;
-    const R* si = st + (G::KV + 3 * i) * NT + lr;
-    const R* sj = st + (G::KV + 3 * j) * NT + lr;
+    // entry = word offsets of k_i[0] and k_j[0] in the state, and the pair
+    const uint32_t oi = ent & 0x1FFFu, oj = (ent >> 13) & 0x1FFFu, p = ent >> 26, lr = oi % NT;
+    const R* si = st + G::KV * NT + oi;
+    const R* sj = st + G::KV * NT + oj;
     const R ki[3] = {si[0], si[NT], si[2 * NT]};
     const R kj[3] = {sj[0], sj[NT], sj[2 * NT]};
     R ca, cb, cc;
@@ -131,8 +133,8 @@ __device__ __forceinline__ void seg_block(const R* __restrict__ st, uint32_t ent
 template <typename R, int MODEL, int NT>
 __device__ __forceinline__ void seg_diag(const R* __restrict__ st, uint32_t ent, R acc[6]) {
     using G = SegState<MODEL>;
-    const uint32_t lr = ent >> 8, i = (ent >> 6) & 3u, p = ent & 15u;
-    const R* si = st + (G::KV + 3 * i) * NT + lr;
+    const uint32_t oi = ent & 0x1FFFu, p = ent >> 26, lr = oi % NT;
+    const R* si = st + G::KV * NT + oi;
     const R k[3] = {si[0], si[NT], si[2 * NT]};
     R ca, sc;
     if constexpr (MODEL == EBB_NH) {
@@ -360,10 +362,10 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
 #pragma unroll 2
                 for (uint32_t e = e0; e < e1; ++e) {
                     const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
-                    const uint32_t lr = x >> 2, kk = x & 3u;
-                    a9[0] += st[(G::F + 3 * kk + 0) * NT + lr];
-                    a9[1] += st[(G::F + 3 * kk + 1) * NT + lr];
-                    a9[2] += st[(G::F + 3 * kk + 2) * NT + lr];
+                    const R* sf = st + G::F * NT + x;   // x = word offset of f_k[0]
+                    a9[0] += sf[0];
+                    a9[1] += sf[NT];
+                    a9[2] += sf[2 * NT];
                     x = nx;
                 }
             }
@@ -533,10 +535,11 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
                 const uint32_t s = sbase[lo - a] + (r - rself[lo]);
                 // block K_ij lands on row (v_i, v_j): transposed (K_ji) when v_i > v_j
                 const uint32_t bi = vv[i] <= vv[j] ? i : j, bj = vv[i] <= vv[j] ? j : i;
-                lists[s].push_back((l << 8) | (bi << 6) | (bj << 4) | (uint32_t)p);
+                lists[s].push_back((3 * bi * (uint32_t)ni + l) | ((3 * bj * (uint32_t)ni + l) << 13) |
+                                   ((uint32_t)p << 26));
             }
             for (uint32_t kk = 0; kk < 4; ++kk)
-                if (vv[kk] >= a && vv[kk] < b) lists[ns + vv[kk] - a].push_back((l << 2) | kk);
+                if (vv[kk] >= a && vv[kk] < b) lists[ns + vv[kk] - a].push_back(3 * kk * (uint32_t)ni + l);
         }
         // rows of the slots
         srow.resize(ns);

@@ -224,6 +224,11 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
                                    edge row sums its blocks rebuilt from the
                                    states (segmented reduction, no atomics,
                                    bitwise run-to-run deterministic).         */
+#define EBB_SCATTER_COLOR 5     /* tets greedily coloured (no two tets of a
+                                   colour share a vertex), one launch per
+                                   colour, plain read-modify-write reductions
+                                   (deterministic; EBB_E_RANGE beyond 64
+                                   colours).                                  */
 typedef struct {
     int32_t model;         /* EBB_STVK | EBB_NH                                */
     int32_t scatter;       /* EBB_SCATTER_*                                    */

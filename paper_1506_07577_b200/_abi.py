@@ -23,7 +23,7 @@ E_NAMES = {
 F32, F64, I32, I64, U8, U32, KEY = 1, 2, 3, 4, 5, 6, 7
 AOS, SOA = 0, 1
 STVK, NH = 0, 1
-SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED, SCATTER_GATHER, SCATTER_SEGMENTED = 0, 1, 2, 3, 4
+SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED, SCATTER_GATHER, SCATTER_SEGMENTED, SCATTER_COLOR = 0, 1, 2, 3, 4, 5
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
 CG_DIR, CG_MATVEC, CG_UPDATE = 0, 1, 2
 K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE, K_CG_SOLVE = 0, 1, 2, 3, 4, 5

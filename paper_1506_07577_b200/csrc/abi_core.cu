@@ -262,6 +262,11 @@ void release_plans(Ctx* c) {
         delete P;
     }
     c->segplans.clear();
+    for (ColorPlan* P : c->colorplans) {
+        P->release();
+        delete P;
+    }
+    c->colorplans.clear();
 }
 
 // Apply a row permutation to every field of `rel` and remap every key-field

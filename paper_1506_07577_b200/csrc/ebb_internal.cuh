@@ -104,6 +104,20 @@ struct SegPlan {
     }
 };
 
+// Plan of the COLOURED element map (color_map.cu): tets grouped by colour
+// (no two tets of a colour share a vertex).
+struct ColorPlan {
+    ebb_field v = EBB_NONE;
+    int ncolors = 0;
+    double host_ms = 0;
+    std::vector<uint32_t> offsets;    // ncolors + 1 (host)
+    uint32_t* order = nullptr;        // nt: tet ids by colour
+    void release() {
+        cudaFree(order);
+        order = nullptr;
+    }
+};
+
 struct Ctx : ebb_ctx_s {
     int device = 0;
     std::vector<Relation> rels;
@@ -126,6 +140,7 @@ struct Ctx : ebb_ctx_s {
     std::vector<TimedLaunch> timed;
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
     std::vector<SegPlan*> segplans; // (same)
+    std::vector<ColorPlan*> colorplans; // (same)
     struct GraphRec {
         cudaGraphExec_t exec = nullptr;
         unsigned long long launches = 0;
@@ -176,6 +191,12 @@ ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool wa
                           const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                           const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
                           cudaStream_t s);
+// color_map.cu: the COLOURED element map (builds its colouring on first use)
+ebb_status color_map_launch(Ctx* c, ebb_field vf, int model, bool want_e, uint64_t nt, const Field* V,
+                            const Field* Ef, const Field* U, const Field* D, const Field* W, const Field* MU,
+                            const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
+                            cudaStream_t s);
+int color_plan_colors(Ctx* c, ebb_field vf);
 ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, const uint32_t* d_old_to_new,
                             cudaStream_t s);
 

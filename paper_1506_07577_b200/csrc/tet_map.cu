@@ -1151,7 +1151,7 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     Ctx* c = (Ctx*)ctx;
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     if (d->model != EBB_STVK && d->model != EBB_NH) return fail(c, EBB_E_ARG, "unknown model %d", d->model);
-    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_SEGMENTED)
+    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_COLOR)
         return fail(c, EBB_E_ARG, "unknown scatter strategy %d", d->scatter);
     Field* V = get_field(c, d->v);
     Field* U = get_field(c, d->u);
@@ -1203,6 +1203,15 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     if (strat == EBB_SCATTER_AUTO) {
         if (envs && atoi(envs) > 0) strat = atoi(envs);
         else strat = EBB_SCATTER_SEGMENTED;
+    }
+    if (Ko && strat == EBB_SCATTER_COLOR) {
+        // plain read-modify-write per colour: the outputs start from zero or accumulate
+        if (d->zero_outputs) {
+            EBB_CUDA(c, cudaMemsetAsync(Fo->ptr, 0, nv * 3 * dtype_size(dt), s));
+            EBB_CUDA(c, cudaMemsetAsync(Ko->ptr, 0, ne * 9 * dtype_size(dt), s));
+            if (En) EBB_CUDA(c, cudaMemsetAsync(En->ptr, 0, dtype_size(dt), s));
+        }
+        return color_map_launch(c, d->v, d->model, En != nullptr, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
     }
     if (Ko && strat == EBB_SCATTER_SEGMENTED) {
         // every K row and f row is written exactly once: zero_outputs means overwrite

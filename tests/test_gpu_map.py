@@ -30,10 +30,10 @@ def _oracle_map(case, m, order, tet_src, model, u=None):
                               e=m.e, ne=m.ne)
 
 
-SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4}
+SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4, "color": 5}
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 @pytest.mark.parametrize("n,mesh", [(4, "kuhn6"), (9, "kuhn6"), (4, "alt5")])
 def test_map_fp64(ctx, model, n, mesh, scatter):
@@ -48,7 +48,7 @@ def test_map_fp64(ctx, model, n, mesh, scatter):
     assert ctx.error_counts(reset=True)["inverted"] == 0
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 def test_map_fp32_displacement_form(ctx, model, scatter):
     case = Case(n=8, model=model, spread=0.1)
@@ -128,7 +128,7 @@ def test_tiled_map_tile_sizes(ctx, tile, scatter, monkeypatch):
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color"])
 def test_map_accumulates_without_zeroing(ctx, scatter):
     """zero_outputs = 0 is the paper's `+=` into existing fields."""
     case = Case(n=4, model="stvk")
@@ -206,3 +206,13 @@ def test_segmented_long_tile_runs(ctx, grid, monkeypatch):
     assert rel_l2(fem.f.read(), f) <= 1e-12
     assert rel_l2(fem.K.read(), K) <= 1e-12
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+
+
+def test_color_map_is_bitwise_deterministic(ctx):
+    """The coloured strategy has no atomics: reruns are bitwise identical."""
+    case = Case(n=8, model="nh")
+    fem = gpu_fem(ctx, case, name="mdet5")
+    fem.map_forces("nh", scatter=SCATTERS["color"])
+    f1, K1 = fem.f.read(), fem.K.read()
+    fem.map_forces("nh", scatter=SCATTERS["color"])
+    assert np.array_equal(fem.f.read(), f1) and np.array_equal(fem.K.read(), K1)

@@ -42,7 +42,7 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
     if kuhn_n:
         n = kuhn_n
         X, tets = M.kuhn6(n)
-        wl, mname = "C2", f"kuhn6 n={n}"
+        wl, mname = ("C2" if n == 55 else "C4"), f"kuhn6 n={n}"
     else:
         X, tets, n = M.blob(target)
         wl, mname = "C3", f"blob n={n}"
@@ -58,7 +58,7 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
         bf = 4 if dt == "f32" else 8
         for model in models:
             ids = {"segmented": A.SCATTER_SEGMENTED, "gather": A.SCATTER_GATHER, "tiled": A.SCATTER_TILED,
-                   "atomic": A.SCATTER_ATOMIC}
+                   "atomic": A.SCATTER_ATOMIC, "color": A.SCATTER_COLOR}
             for scat in scatters:
                 sid = ids[scat]
                 fem.map_forces(model, scatter=sid)
@@ -123,6 +123,42 @@ def run_c4(sizes, reps):
             del fem
 
 
+def run_c4cg(sizes, reps, dtypes=("f64", "f32")):
+    """C4: the full PCG iteration (persistent single-launch solve) per size."""
+    import torch
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.tetfem import TetFEM
+
+    peak, src = bench._peaks()
+    flush = torch.empty(bench.FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    w = bench.WORKLOAD
+    for n in sizes:
+        X, tets, free, u0, mu, lam = bench.make_case(n, w["order_seed"], w["u_seed"], w["E"], w["nu"])
+        for dt in dtypes:
+            ctx = ebb.Context(0)
+            fem = TetFEM(ctx, X, tets, dtype=dt, mu=mu, lam=lam, rho=w["rho"], free=free, u=u0, name=f"cg{n}{dt}")
+            fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"])
+            torch.cuda.synchronize()
+            ctx.timing(True)
+            ctx.timing_read(A.K_CG_SOLVE, reset=True)
+            for _ in range(reps):
+                _flush(flush)
+                fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"])
+            ms, nl = ctx.timing_read(A.K_CG_SOLVE, reset=True)
+            ctx.timing(False)
+            it_us = 1e3 * ms / nl / w["cg_iters"]
+            bf = 4 if dt == "f32" else 8
+            b = bench.bytes_cg_iter(fem.nv, fem.ne, bf)
+            print(json.dumps({"workload": "C4-cg", "mesh": f"kuhn6 n={n}", "tets": fem.nt, "verts": fem.nv,
+                              "edge_rows": fem.ne, "dtype": dt, "iter_us": it_us, "iters_per_s": 1e6 / it_us,
+                              "gbs": b / (it_us * 1e-6) / 1e9, "hbm_frac": b / (it_us * 1e-6) / 1e9 / peak,
+                              "algorithmic_bytes_per_iter": b, "peak_gbs": peak, "peak_source": src}), flush=True)
+            ctx.close()
+            del fem
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", action="store_true")
@@ -131,6 +167,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--c3-tets", type=int, default=10_000_000)
     ap.add_argument("--c2", action="store_true", help="the map sweep on the C2 Kuhn n=55 mesh")
+    ap.add_argument("--c4map", action="store_true", help="the map strategies on every --sizes Kuhn mesh")
+    ap.add_argument("--c4cg", action="store_true", help="the PCG iteration on every --sizes Kuhn mesh")
     ap.add_argument("--scatters", default="segmented,gather,tiled,atomic")
     ap.add_argument("--dtypes", default="f32,f64")
     ap.add_argument("--models", default="stvk,nh")
@@ -145,6 +183,12 @@ def main():
                models=a.models.split(","))
     if a.c4:
         run_c4([int(x) for x in a.sizes.split(",")], a.reps)
+    if a.c4map:
+        for n in [int(x) for x in a.sizes.split(",")]:
+            run_c3(a.reps, kuhn_n=n, scatters=a.scatters.split(","), dtypes=a.dtypes.split(","),
+                   models=a.models.split(","))
+    if a.c4cg:
+        run_c4cg([int(x) for x in a.sizes.split(",")], a.reps)
 
 
 if __name__ == "__main__":

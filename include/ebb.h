@@ -301,7 +301,19 @@ typedef struct {
     ebb_field rho;       /* F64 global r.z (allocated if NONE)                */
     ebb_field scal;      /* internal device scalars rho, p.q, r.z             */
     ebb_field p2;        /* second direction buffer (p is double-buffered)    */
+    int32_t variant;     /* EBB_CG_AUTO | EBB_CG_SAAD | EBB_CG_SINGLE_REDUCTION;
+                            fixed from ebb_cg_init to the end of the solve    */
+    ebb_field s, y, w, u, u2;     /* single-reduction work vectors: s = A p,
+                            y = A D s, w = A z, u = D w (double-buffered with
+                            u2; D = diag(A)^-1); EBB_NONE = allocated          */
 } ebb_cg;
+#define EBB_CG_AUTO 0              /* the measured faster          */
+#define EBB_CG_SAAD 1              /* Saad Alg. 9.1: two reductions per iteration    */
+#define EBB_CG_SINGLE_REDUCTION 2  /* Chronopoulos-Gear with the matvec moved onto
+                                      u = D w: one fused reduction (r.z, w.z) and
+                                      one gathered vector per iteration, same
+                                      iterates in exact arithmetic; ebb_cg_step
+                                      only (the per-phase multi-GPU path is Saad) */
 /* a11: x = 0, r = b*mask, z = r/diag(A), p = z, rho = r.z.  Stream-ordered.
  * Per iteration: beta = rho'/rho, p = z + beta p fused into q = (A p)*mask
  * with p.q; then alpha = rho/p.q, x += alpha p, r -= alpha q, z = r/diag(A),

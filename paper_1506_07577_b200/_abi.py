@@ -57,7 +57,11 @@ class ImplicitDesc(C.Structure):
 
 class CG(C.Structure):
     _fields_ = [("edges", u32), ("A", u32), ("b", u32), ("x", u32), ("self", u32), ("mask", u32),
-                ("r", u32), ("p", u32), ("z", u32), ("q", u32), ("dinv", u32), ("rho", u32), ("scal", u32), ("p2", u32)]
+                ("r", u32), ("p", u32), ("z", u32), ("q", u32), ("dinv", u32), ("rho", u32), ("scal", u32), ("p2", u32),
+                ("variant", C.c_int32), ("s", u32), ("y", u32), ("w", u32), ("u", u32), ("u2", u32)]
+
+
+CG_AUTO, CG_SAAD, CG_SINGLE_REDUCTION = 0, 1, 2
 
 
 class ExplicitDesc(C.Structure):

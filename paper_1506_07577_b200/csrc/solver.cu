@@ -25,7 +25,7 @@ using namespace ebb;
 
 namespace {
 
-enum { S_RHO = 0, S_PQ = 1, S_RZ = 2, S_FIRST = 3, S_PAR = 4, S_NSCAL = 8 };
+enum { S_RHO = 0, S_PQ = 1, S_RZ = 2, S_FIRST = 3, S_PAR = 4, S_ALPHA = 5, S_VAR = 6, S_NSCAL = 8 };
 
 template <typename R>
 struct V4;
@@ -576,6 +576,224 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
 }
 
 // ---------------------------------------------------------------------------
+// Single-reduction persistent PCG (Chronopoulos-Gear):
+// the same iterates as Saad Alg. 9.1 in exact arithmetic, with ONE grid
+// barrier and ONE gathered vector per iteration (Saad: two barriers, two
+// gathered vectors).  D = diag(A)^-1 (Jacobi), all operators masked.
+//   s_i = w_i + b_i s_{i-1} (= A p_i),  p_i = z_i + b_i p_{i-1},
+//   y_i = A u_i + b_i y_{i-1} (= A D s_i),  u_i = D w_i,
+//   x_{i+1} = x_i + a_i p_i,  r_{i+1} = r_i - a_i s_i,  z_{i+1} = D r_{i+1},
+//   w_{i+1} = w_i - a_i y_i (= A z_{i+1}),  u_{i+1} = D w_{i+1},
+//   g_{i+1} = r.z,  d_{i+1} = w.z  (one fused reduction),
+//   b_{i+1} = g_{i+1} / g_i,  a_{i+1} = g_{i+1} / (d_{i+1} - b_{i+1} g_{i+1} / a_i).
+// The matvec operand u_i is complete when the phase starts (it does not
+// depend on a_i, b_i), so each phase is: stream A, gather u_i, and the owner
+// of each vertex applies every recurrence as it finishes the vertex's row.
+// Only u is read by neighbours (double-buffered); the rest is owner-local.
+// The first call after ebb_cg_init runs one extra matvec (w_0 = A z_0).
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
+    k_cg1_persistent(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
+                     const R* __restrict__ A, uint64_t ne, const R* __restrict__ dinv, R* __restrict__ x,
+                     R* __restrict__ r, const R* __restrict__ z0, R* __restrict__ p, R* __restrict__ sv,
+                     R* __restrict__ yv, R* __restrict__ wv, R* ub0, R* ub1, const uint8_t* __restrict__ mask,
+                     double* __restrict__ part_g, double* __restrict__ part_d, unsigned int* __restrict__ bar_count,
+                     unsigned int* __restrict__ bar_gen, double* __restrict__ scal, double* __restrict__ rho_user,
+                     unsigned long long* __restrict__ err, uint32_t cap, int iters) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
+    __shared__ double sm_tot;
+    constexpr uint32_t AE = 16 / sizeof(R);
+    const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const uint64_t nchunks = (nv + TMA_VCH - 1) / TMA_VCH;
+    const uint64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TMA_NS; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], PCG_WPG);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // scalars (identical in every CTA)
+    double gam = scal[S_RHO];                 // g_i = r_i . z_i
+    double alpha = scal[S_ALPHA];             // a_i
+    double beta = scal[S_PQ];                 // b_i
+    int first = scal[S_FIRST] != 0.0;         // w_0 not yet formed
+    int par = scal[S_PAR] != 0.0;             // u_i in buffer par
+    uint64_t issued = 0;
+    auto issue = [&](uint64_t ch, uint64_t seq) {
+        const int s = seq % TMA_NS;
+        const uint64_t v0 = ch * TMA_VCH;
+        const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+        const uint64_t e0 = index[v0], e1 = index[v1];
+        if (seq >= TMA_NS) mbar_wait(&empty_bar[s], (uint32_t)(((seq / TMA_NS) + 1) & 1u));
+        unsigned char* base = tma_smem + s * stage_bytes;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            tot += (uint32_t)((a1 - a0) * sizeof(R));
+        }
+        const uint64_t h0 = e0 & ~3ull, h1 = (e1 + 3) & ~3ull;
+        tot += (uint32_t)((h1 - h0) * 4);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full_bar[s], tot);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            bulk_g2s_evict_first(base + (size_t)c * cap * sizeof(R), A + a0, (uint32_t)((a1 - a0) * sizeof(R)),
+                                 &full_bar[s]);
+        }
+        bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
+    };
+    const int nphase = iters + (first && iters > 0 ? 1 : 0);
+    if (warp == TMA_CONSUMERS && lane == 0 && nphase > 0)
+        for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+    for (int ph = 0; ph < nphase; ++ph) {
+        const bool pro = first != 0;          // prologue: w_0 = A z_0, u_0 = D w_0
+        const R a = (R)alpha, b = (R)beta;
+        const R* __restrict__ op = pro ? z0 : (par ? ub1 : ub0);   // the gathered operand (z_0 or u_i)
+        R* __restrict__ un = pro ? (par ? ub1 : ub0) : (par ? ub0 : ub1);   // u_0 in place / u_{i+1}
+        double pg = 0.0, pd = 0.0;
+        if (warp == TMA_CONSUMERS) {
+            if (lane == 0) {
+                for (uint64_t j = TMA_NS; j < my_chunks; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+                if (ph + 1 < nphase)
+                    for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+            }
+        } else {
+            const unsigned grp = warp / PCG_WPG, wig = warp % PCG_WPG;
+            const unsigned sub = lane & 7;
+            const uint64_t seq0 = (uint64_t)ph * my_chunks;
+            for (uint64_t j = grp; j < my_chunks; j += PCG_GROUPS) {
+                const uint64_t seq = seq0 + j;
+                const uint64_t ch = blockIdx.x + j * gridDim.x;
+                const int s = seq % TMA_NS;
+                const uint64_t v0 = ch * TMA_VCH;
+                const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+                const uint64_t v = v0 + 4 * wig + (lane >> 3);
+                const bool valid = v < v1;
+                const uint32_t e0 = index[v0];
+                const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
+                mbar_wait(&full_bar[s], (uint32_t)((seq / TMA_NS) & 1u));
+                const unsigned char* base = tma_smem + s * stage_bytes;
+                const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
+                uint32_t off[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) off[c] = (uint32_t)((c * ne + e0) & (AE - 1));
+                R a0 = 0, a1 = 0, a2 = 0;
+                for (uint32_t rb = r0 + sub; rb < r1; rb += 16) {
+                    // two rows per lane per pass: both gathers in flight together
+                    const uint32_t rr1 = rb + 8;
+                    const bool two = rr1 < r1;
+                    const uint32_t h0 = hs[rb], h1 = two ? hs[rr1] : h0;
+                    const auto o0 = ld4cg(op, h0);
+                    const auto o1 = ld4cg(op, h1);
+                    R av[9], bv[9];
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) {
+                        const R* pl = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R)) + off[c];
+                        av[c] = pl[rb];
+                        bv[c] = two ? pl[rr1] : R(0);
+                    }
+                    a0 += av[0] * o0.x + av[1] * o0.y + av[2] * o0.z + (bv[0] * o1.x + bv[1] * o1.y + bv[2] * o1.z);
+                    a1 += av[3] * o0.x + av[4] * o0.y + av[5] * o0.z + (bv[3] * o1.x + bv[4] * o1.y + bv[5] * o1.z);
+                    a2 += av[6] * o0.x + av[7] * o0.y + av[8] * o0.z + (bv[6] * o1.x + bv[7] * o1.y + bv[8] * o1.z);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o, 8);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o, 8);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, o, 8);
+                }
+                if (sub == 0 && valid) {
+                    if (mask && !mask[v]) a0 = a1 = a2 = 0;   // m = (A op) * mask
+                    const auto dv = ld4(dinv, v);
+                    typename V4<R>::T t;
+                    t.w = 0;
+                    if (pro) {
+                        // w_0 = A z_0, u_0 = D w_0, d_0 = w_0 . z_0
+                        const auto zv = ld4(z0, v);
+                        t.x = a0; t.y = a1; t.z = a2;
+                        st4(wv, v, t);
+                        t.x = a0 * dv.x; t.y = a1 * dv.y; t.z = a2 * dv.z;
+                        st4(un, v, t);
+                        pd += (double)a0 * zv.x + (double)a1 * zv.y + (double)a2 * zv.z;
+                    } else {
+                        auto rv = ld4(r, v);
+                        auto wi = ld4(wv, v);
+                        typename V4<R>::T si = wi, yi, pi;
+                        yi.x = a0; yi.y = a1; yi.z = a2; yi.w = 0;
+                        pi.x = rv.x * dv.x; pi.y = rv.y * dv.y; pi.z = rv.z * dv.z; pi.w = 0;   // z_i
+                        if (b != R(0)) {
+                            const auto so = ld4(sv, v), yo = ld4(yv, v), po = ld4(p, v);
+                            si.x += b * so.x; si.y += b * so.y; si.z += b * so.z;
+                            yi.x += b * yo.x; yi.y += b * yo.y; yi.z += b * yo.z;
+                            pi.x += b * po.x; pi.y += b * po.y; pi.z += b * po.z;
+                        }
+                        si.w = 0;
+                        st4(sv, v, si);
+                        st4(yv, v, yi);
+                        st4(p, v, pi);
+                        x[3 * v] += a * pi.x;
+                        x[3 * v + 1] += a * pi.y;
+                        x[3 * v + 2] += a * pi.z;
+                        rv.x -= a * si.x; rv.y -= a * si.y; rv.z -= a * si.z; rv.w = 0;
+                        wi.x -= a * yi.x; wi.y -= a * yi.y; wi.z -= a * yi.z; wi.w = 0;
+                        st4(r, v, rv);
+                        st4(wv, v, wi);
+                        t.x = wi.x * dv.x; t.y = wi.y * dv.y; t.z = wi.z * dv.z;
+                        st4(un, v, t);
+                        const R zx = rv.x * dv.x, zy = rv.y * dv.y, zz = rv.z * dv.z;
+                        pg += (double)rv.x * zx + (double)rv.y * zy + (double)rv.z * zz;
+                        pd += (double)wi.x * zx + (double)wi.y * zy + (double)wi.z * zz;
+                    }
+                }
+            }
+        }
+        pg = block_reduce<ROP_SUM>(pg);
+        pd = block_reduce<ROP_SUM>(pd);
+        if (threadIdx.x == 0) {
+            part_g[blockIdx.x] = pg;
+            part_d[blockIdx.x] = pd;
+        }
+        grid_barrier(bar_count, bar_gen, gridDim.x);
+        const double dsum = grid_sum_partials(part_d, gridDim.x, &sm_tot);
+        if (pro) {
+            // a_0 = g_0 / (p_0 . A p_0), p_0 = z_0
+            if (blockIdx.x == 0 && threadIdx.x == 0 && dsum < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+            alpha = dsum != 0.0 ? gam / dsum : 0.0;
+            beta = 0.0;
+            first = 0;
+        } else {
+            const double gnew = grid_sum_partials(part_g, gridDim.x, &sm_tot);
+            const double bn = gam != 0.0 ? gnew / gam : 0.0;
+            const double den = dsum - (alpha != 0.0 ? bn * gnew / alpha : 0.0);   // = p_{i+1} . A p_{i+1}
+            if (blockIdx.x == 0 && threadIdx.x == 0 && den < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+            alpha = den != 0.0 ? gnew / den : 0.0;
+            beta = bn;
+            gam = gnew;
+            par ^= 1;
+            if (blockIdx.x == 0 && threadIdx.x == 0) *rho_user = gam;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scal[S_RHO] = gam;
+        scal[S_RZ] = gam;
+        scal[S_ALPHA] = alpha;
+        scal[S_PQ] = beta;
+        scal[S_FIRST] = first ? 1.0 : 0.0;
+        scal[S_PAR] = par ? 1.0 : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // PCG kernels on padded vec4 work vectors (one thread per vertex)
 // init: dinv = 1/diag(A) on free DOFs (Jacobi), x = 0, r = b*m,
 //       z = r*dinv, p = z, local r.z -> scal[S_RZ]; scal[S_FIRST] = 1
@@ -836,6 +1054,53 @@ ebb_status check_mask(Ctx* c, ebb_field m, ebb_rel rel, const uint8_t** out) {
 }
 
 
+int cg_variant(const ebb_cg* cg, uint64_t nv, ebb_dtype dt);
+
+template <typename R>
+ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s) {
+    for (ebb_field f : {cg->s, cg->y, cg->w, cg->u, cg->u2})
+        if (!get_field(c, f)) return fail(c, EBB_E_STATE, "cg: single-reduction work vectors missing (ebb_cg_init "
+                                                           "with this variant first)");
+    auto F = [&](ebb_field f) { return (R*)c->fields[f].ptr; };
+    const uint8_t* mask;
+    EBB_TRY(check_mask(c, cg->mask, G.verts, &mask));
+    const uint32_t cap = (uint32_t)(TMA_VCH * (G.max_group ? G.max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+    const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const size_t smem = stage * TMA_NS;
+    if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
+    static thread_local size_t configured = 0;
+    if (smem > configured) {
+        EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_persistent<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    const int block = 32 * (TMA_CONSUMERS + 1);
+    int nb = 0;
+    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg1_persistent<R>, block, smem));
+    if (nb < 1) return fail(c, EBB_E_CUDA, "cg: persistent kernel does not fit on an SM");
+    const uint64_t nch = (G.nv + TMA_VCH - 1) / TMA_VCH;
+    uint64_t grid = (uint64_t)nb * c->num_sms;
+    if (grid > nch) grid = nch;
+    if (grid > 4096) grid = 4096;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KernelTimer kt(c, EBB_K_CG_SOLVE, s);
+    EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_persistent<R>, G.nv, G.index, G.head, (const R*)c->fields[cg->A].ptr,
+                                   G.ne, (const R*)c->fields[cg->dinv].ptr, F(cg->x), F(cg->r), (const R*)F(cg->z),
+                                   F(cg->p), F(cg->s), F(cg->y), F(cg->w), F(cg->u), F(cg->u2), mask, c->d_partials,
+                                   c->d_partials + 4096, c->d_counter + 10, c->d_counter + 11,
+                                   (double*)c->fields[cg->scal].ptr, (double*)c->fields[cg->rho].ptr, c->d_err, cap,
+                                   iters));
+    return EBB_OK;
+}
+
 template <typename R>
 ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s, int only_phase = -1) {
     const R* A = (const R*)c->fields[cg->A].ptr;
@@ -851,6 +1116,8 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     double* scal = (double*)c->fields[cg->scal].ptr;
     double* rho_user = (double*)c->fields[cg->rho].ptr;
     const unsigned ug = occ_grid(c, k_cg_update<R>, 256, 0, G.nv);
+    if (only_phase < 0 && iters > 0 && cg_variant(cg, G.nv, sizeof(R) == 8 ? EBB_F64 : EBB_F32) == EBB_CG_SINGLE_REDUCTION)
+        return cg1_launch<R>(c, cg, G, iters, s);
     const char* mode = getenv("EBB_CG");
     if (only_phase < 0 && iters > 0 && !(mode && mode[0] == '2')) {
         // single launch, all iterations (cooperative: every CTA resident)
@@ -906,6 +1173,18 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     }
     EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
+}
+
+// AUTO = the measured faster variant: the single-reduction
+// kernel saves a grid barrier and a gathered vector per iteration but moves
+// ~9 owner-local vector records per vertex; it wins while they stay in L2
+// (C2: 1M tets, fp64) and loses once they stream from HBM (1e7 tets).
+int cg_variant(const ebb_cg* cg, uint64_t nv, ebb_dtype dt) {
+    if (cg->variant != EBB_CG_AUTO) return cg->variant;
+    const char* e = getenv("EBB_CG_VARIANT");
+    if (e && (atoi(e) == EBB_CG_SAAD || atoi(e) == EBB_CG_SINGLE_REDUCTION)) return atoi(e);
+    (void)dt;   // measured crossover (fp64 and fp32 alike): between 1.8e5 and 3.0e5 vertices
+    return nv <= 232000 ? EBB_CG_SINGLE_REDUCTION : EBB_CG_SAAD;
 }
 
 ebb_status cg_validate(Ctx* c, const ebb_cg* cg, EdgeGraph* G, ebb_dtype* dt) {
@@ -1085,10 +1364,13 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     // work vectors: padded 4-component records, allocated on first use
     static int serial = 0;
     char nm[64];
-    ebb_field* work[] = {&cg->r, &cg->p, &cg->z, &cg->q, &cg->dinv, &cg->p2};
-    const char* wn[] = {"r", "p", "z", "q", "dinv", "p2"};
+    if (cg->variant < EBB_CG_AUTO || cg->variant > EBB_CG_SINGLE_REDUCTION)
+        return fail(c, EBB_E_ARG, "cg: unknown variant %d", cg->variant);
+    ebb_field* work[] = {&cg->r, &cg->p, &cg->z, &cg->q, &cg->dinv, &cg->p2, &cg->s, &cg->y, &cg->w, &cg->u, &cg->u2};
+    const char* wn[] = {"r", "p", "z", "q", "dinv", "p2", "s", "y", "w", "u", "u2"};
+    const int nwork = cg_variant(cg, G.nv, dt) == EBB_CG_SINGLE_REDUCTION ? 11 : 6;
     int id = -1;
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < nwork; ++i) {
         Field* W = *work[i] == EBB_NONE ? nullptr : get_field(c, *work[i]);
         if (!W) {
             if (id < 0) id = serial++;

@@ -144,13 +144,17 @@ class TetFEM:
         d.g[0], d.g[1], d.g[2] = g
         self.ctx.check(self.ctx.L.ebb_implicit_assemble(self.ctx.h, C.byref(d), _stream(stream)))
 
-    def cg_init(self, stream=None):
+    def cg_init(self, stream=None, variant=None):
         if self.cg is None:
             cg = A.CG()
             cg.edges, cg.A, cg.b, cg.x, cg.self = self.edges.h, self.K.h, self.b.h, self.dv.h, self.self_e.h
             cg.mask = self.free.h if self.has_mask else A.NONE
             cg.r = cg.p = cg.z = cg.q = cg.dinv = cg.rho = cg.scal = cg.p2 = A.NONE
+            cg.s = cg.y = cg.w = cg.u = cg.u2 = A.NONE
+            cg.variant = A.CG_AUTO
             self.cg = cg
+        if variant is not None:
+            self.cg.variant = variant
         self.ctx.check(self.ctx.L.ebb_cg_init(self.ctx.h, C.byref(self.cg), _stream(stream)))
 
     def cg_step(self, iters, stream=None):

@@ -93,11 +93,15 @@ def test_global_reduce_large_masked(ctx):
     assert out.get() == x.max()
 
 
+@pytest.mark.parametrize("variant", ["1", "2"])
 @pytest.mark.parametrize("model", ["nh", "stvk"])
-def test_implicit_step(ctx, model):
+def test_implicit_step(ctx, model, variant, monkeypatch):
+    """Both PCG variants (1 = Saad Alg. 9.1, 2 = single-reduction
+    Chronopoulos-Gear) reproduce the oracle's Saad iterates after 50 its."""
+    monkeypatch.setenv("EBB_CG_VARIANT", variant)
     case = Case(n=6, model=model, vel_amp=0.05)
     h, iters, al, be = 1e-2, 50, 0.05, 0.002
-    fem = gpu_fem(ctx, case, name=f"imp{model}")
+    fem = gpu_fem(ctx, case, name=f"imp{model}{variant}")
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     out = oracle.implicit_step(m, model, case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
                                case.free[order], h, iters=iters, alpha=al, beta=be)
@@ -127,9 +131,11 @@ def test_explicit_C1(ctx):
         assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-def test_cg_zero_rhs_noop(ctx):
+@pytest.mark.parametrize("variant", ["1", "2"])
+def test_cg_zero_rhs_noop(ctx, variant, monkeypatch):
+    monkeypatch.setenv("EBB_CG_VARIANT", variant)
     case = Case(n=3)
-    fem = gpu_fem(ctx, case, name="cg0")
+    fem = gpu_fem(ctx, case, name=f"cg0{variant}")
     fem.map_forces("nh")
     fem.assemble(1e-2)
     fem.b.fill(0.0)
@@ -138,11 +144,13 @@ def test_cg_zero_rhs_noop(ctx):
     assert np.all(fem.dv.read() == 0.0) and fem.cg_rho() == 0.0
 
 
-def test_C2_full_size_implicit_step(ctx):
+@pytest.mark.parametrize("variant", ["1", "2"])
+def test_C2_full_size_implicit_step(ctx, variant, monkeypatch):
     """BASELINE configs[1] at full size (998,250 tets), bench launch configuration:
     integer maps bit-exact, f/K <= 1e-12, CG iterate <= 1e-8 after 50 iterations."""
+    monkeypatch.setenv("EBB_CG_VARIANT", variant)
     case = Case(n=55, model="nh", E=2e5)
-    fem = gpu_fem(ctx, case, name="C2")
+    fem = gpu_fem(ctx, case, name=f"C2v{variant}")
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     assert np.array_equal(fem.vert_order(), order)
     assert np.array_equal(fem.tet_order(), tet_src)
@@ -175,3 +183,33 @@ def test_graph_capture_replays_the_step(ctx):
     s.synchronize()
     assert rel_l2(b.u.read(), a.u.read()) <= 1e-12
     assert rel_l2(b.dv.read(), a.dv.read()) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("iters", [1, 5, 20])
+def test_cg_iterates_and_split_calls(ctx, variant, iters, monkeypatch):
+    """PCG iterate after k iterations matches the oracle's (Saad) iterate for
+    both variants, and k iterations split over several ebb_cg_step calls
+    (scalars and buffer parity carried on the device) give the same iterate."""
+    monkeypatch.setenv("EBB_CG_VARIANT", variant)
+    case = Case(n=5, model="nh", vel_amp=0.05)
+    fem = gpu_fem(ctx, case, name=f"cgit{variant}{iters}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    out = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                               case.free[order], 1e-2, iters=iters)
+    fem.map_forces("nh")
+    fem.assemble(1e-2)
+    fem.cg_init()
+    fem.cg_step(iters)
+    x1 = fem.dv.read()
+    assert rel_l2(x1, out["dv"]) <= 1e-9
+    fem.cg_init()
+    done = 0
+    for k in (1, 2, 3, 100):
+        k = min(k, iters - done)
+        if k <= 0:
+            break
+        fem.cg_step(k)
+        done += k
+    assert rel_l2(fem.dv.read(), x1) <= 1e-13
+    assert ctx.error_counts(reset=True)["not_spd"] == 0

@@ -112,14 +112,14 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_case(n, order_seed, u_seed, E, nu):
+def make_case(n, order_seed, u_seed, E, nu, wall_ramp=0.0):
     from synth import mesh as M
     from synth import state as S
     X, tets = M.kuhn6(n)
     if order_seed is not None:
         X, tets = M.permute_vertices(X, tets, order_seed)
     free = S.fixed_mask(X, n)
-    u = S.stretch_noise_u(X, n, u_seed, free=free)
+    u = S.stretch_noise_u(X, n, u_seed, free=free, wall_ramp=wall_ramp)
     mu, lam = S.materials(tets.shape[0], E, nu)
     return X, tets, free, u, mu, lam
 
@@ -381,7 +381,9 @@ def run_dist(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     w = WORKLOAD
     n = int(round(w["n"] * world ** (1.0 / 3.0)))
-    X, tets, free, u0, mu, lam = make_case(n, w["order_seed"], w["u_seed"], w["E"], w["nu"])
+    E_n = w["E"] * (w["n"] / n) ** 2    # keep h^2 E n^2 / rho ~ 60 (SURVEY §8(c) recipe)
+    # stretch ramped off the wall: the plain recipe's wall shear (~0.05 n) inverts tets at large n
+    X, tets, free, u0, mu, lam = make_case(n, w["order_seed"], w["u_seed"], E_n, w["nu"], wall_ramp=0.1)
     ctx = ebb.Context(local_rank)
     G = D.global_partition(ctx, X, tets, world, name="global")
     plan = D.halo_plan(G["tets"], G["owner_v"], world)

@@ -22,8 +22,14 @@ def fixed_mask(X: np.ndarray, n: int) -> np.ndarray:
     return (~fixed).astype(np.uint8)
 
 
-def stretch_noise_u(X, n, seed, stretch=(0.1, -0.05, 0.0), noise=0.05, free=None):
+def stretch_noise_u(X, n, seed, stretch=(0.1, -0.05, 0.0), noise=0.05, free=None, wall_ramp=0.0):
+    """``wall_ramp = w > 0`` scales the stretch by clip((x - x_min) / w, 0, 1):
+    the plain recipe pins the wall layer (u = 0) next to free vertices with
+    u_y = -0.05 y, a shear of ~0.05 n that inverts tets beyond n ~ 200 (C5);
+    the ramp keeps the shear at 0.05 / w for every n."""
     u = X * np.asarray(stretch, dtype=np.float64)[None, :]
+    if wall_ramp > 0:
+        u = u * np.clip((X[:, 0:1] - X[:, 0].min()) / wall_ramp, 0.0, 1.0)
     u = u + rng(seed).uniform(-noise / n, noise / n, size=X.shape)
     if free is not None:
         u[free == 0] = 0.0

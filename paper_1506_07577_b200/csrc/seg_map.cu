@@ -28,6 +28,7 @@
 // contraction (oracle/ebb_oracle.c); the two share no code.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -162,6 +163,9 @@ __device__ __forceinline__ void seg_diag(const R* __restrict__ st, uint32_t ent,
 // other's work; fp32 state leaves room for a third (fp64 would spill) -- measured
 template <typename R>
 constexpr int seg_min_blocks() { return sizeof(R) == 4 ? 3 : 2; }
+#ifdef SEG_PROF
+__device__ unsigned long long g_seg_prof[16];
+#endif
 template <typename R, int MODEL, bool WANT_E, int NT>
 __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet_map_seg(
     uint32_t ntiles, const uint4* __restrict__ tdesc, const uint32_t* __restrict__ inst_t,
@@ -243,6 +247,22 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
     uint4 v1 = verts_of(t1);
     uint32_t t2 = inst_of(2);
     double e_acc = 0.0;
+#ifdef SEG_PROF
+    // per-CTA wall-clock split (thread 0 and a lane of the last warp): phase 1,
+    // barrier 1 + entry wait, phase 2, barrier 2
+    long long tp[4] = {0, 0, 0, 0};
+    long long tc0 = clock64();
+#define SEG_MARK(q)                          \
+    do {                                     \
+        const long long tn = clock64();      \
+        tp[q] += tn - tc0;                   \
+        tc0 = tn;                            \
+    } while (0)
+#else
+#define SEG_MARK(q) \
+    do {            \
+    } while (0)
+#endif
     for (uint32_t j = 0; j < m; ++j) {
         const uint32_t k = j;
         // descriptor ring: copy [j + 32, j + 64) at j = 32 r, complete at j = 32 r + 16
@@ -324,9 +344,11 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
         const uint32_t it0 = it0_n, nit = nit_n;
         uint4 item = item_n;
         item_head(j + 1);
+        SEG_MARK(0);
         __syncthreads();   // state complete
         const int b = k & 1;
         mbar_wait(&bar[b], (k >> 1) & 1);
+        SEG_MARK(1);
         const uint32_t* E = ebuf + (size_t)b * max_ent;
         // ---- phase 2: items = chunks of one row's (or one vertex's force) list;
         // the chunks of a list sit in consecutive lanes and are combined by a
@@ -407,8 +429,17 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
                 }
             }
         }
+        SEG_MARK(2);
         __syncthreads();   // state and entry buffer b free for reuse
+        SEG_MARK(3);
     }
+#ifdef SEG_PROF
+    if (tid == 0 || tid == NT - 1) {
+        const int w = tid == 0 ? 0 : 1;
+        for (int q = 0; q < 4; ++q) atomicAdd((unsigned long long*)&g_seg_prof[8 * w + q], (unsigned long long)tp[q]);
+        atomicAdd((unsigned long long*)&g_seg_prof[8 * w + 4], 1ull);
+    }
+#endif
     if (WANT_E) {
         double tot;
         if (block_sum_last_done(e_acc, partials, counter, &tot)) *energy = (R)((double)*energy + tot);
@@ -432,6 +463,49 @@ ebb_status upload(Ctx* c, const std::vector<T>& h, T** d) {
     return EBB_OK;
 }
 
+// Phase 2 walks, in lockstep, entry e of 32 lists (one per lane); each entry's
+// shared-memory loads all hit bank pair (lr mod 16) of the state (fp64, SoA,
+// NT a multiple of 16), so two lanes of a half-warp on the same pair with
+// different lr serialize.  The order of a chunk's entries is free (the sum is
+// still in a fixed, plan-given order): greedily give every lane, step by
+// step, its remaining entry whose bank pair is least used by its half-warp.
+void bank_schedule(uint4* it, size_t nit, uint32_t* ent, int ni) {
+    std::vector<uint32_t> tmp;
+    for (size_t w0 = 0; w0 + 32 <= nit; w0 += 32) {
+        uint32_t steps = 0;
+        for (int l = 0; l < 32; ++l) steps = std::max(steps, (it[w0 + l].x >> 16) & 0x7Fu);
+        if (steps < 2) continue;
+        std::vector<uint8_t> used(steps * 2 * 16, 0);
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t meta = it[w0 + l].x, beg = meta & 0xFFFFu, sz = (meta >> 16) & 0x7Fu;
+            if (sz < 2) {
+                if (sz == 1) {
+                    const uint32_t lr = (ent[beg] & 0x1FFFu) % (uint32_t)ni;
+                    used[(0 * 2 + (l >> 4)) * 16 + (lr & 15)]++;
+                }
+                continue;
+            }
+            tmp.assign(ent + beg, ent + beg + sz);
+            std::vector<char> taken(sz, 0);
+            for (uint32_t e = 0; e < sz; ++e) {
+                uint32_t best = 0, bc = 0xFFFFFFFFu;
+                for (uint32_t k = 0; k < sz; ++k) {
+                    if (taken[k]) continue;
+                    const uint32_t lr = (tmp[k] & 0x1FFFu) % (uint32_t)ni;
+                    const uint32_t cnt = used[(e * 2 + (l >> 4)) * 16 + (lr & 15)];
+                    if (cnt < bc) {
+                        bc = cnt;
+                        best = k;
+                    }
+                }
+                taken[best] = 1;
+                ent[beg + e] = tmp[best];
+                used[(e * 2 + (l >> 4)) * 16 + (((tmp[best] & 0x1FFFu) % (uint32_t)ni) & 15)]++;
+            }
+        }
+    }
+}
+
 ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** out) {
     for (SegPlan* P : c->segplans)
         if (P->v == vf && P->e == ef && P->ni == ni) {
@@ -439,6 +513,7 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
             return EBB_OK;
         }
     const auto t_start = std::chrono::steady_clock::now();
+    const bool no_bank_sched = getenv("EBB_SEG_NO_BANK_SCHED") != nullptr;   // measurement knob
     Field* V = get_field(c, vf);
     Field* E = get_field(c, ef);
     Relation& ER = c->rels[E->key_target];
@@ -611,6 +686,7 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         if (L > 127) return fail(c, EBB_E_RANGE, "segmented map: a list of %zu entries (> 8 x 127)", longest);
         const size_t it_base = items.size();
         layout(L, true);
+        if (!no_bank_sched) bank_schedule(items.data() + it_base, items.size() - it_base, ents.data() + e_base, ni);
         for (uint32_t l = 0; l < ninst; ++l) lr_of[inst_t[i0 + l]] = 0xFFFFFFFEu;   // never a tile id
         max_ent = std::max(max_ent, nent);
         max_items = std::max(max_items, (uint32_t)(items.size() - it_base));
@@ -671,6 +747,21 @@ ebb_status launch_seg_t(Ctx* c, const SegPlan& P, bool want_e, int accumulate, u
                                 (const R*)LA->ptr, (R*)Fo->ptr, (R*)Ko->ptr, ne, accumulate, c->d_partials,
                                 c->d_counter + 0, En ? (R*)En->ptr : nullptr, c->d_err);
     EBB_CUDA(c, cudaGetLastError());
+#ifdef SEG_PROF
+    {
+        unsigned long long h[16];
+        cudaDeviceSynchronize();
+        cudaMemcpyFromSymbol(h, g_seg_prof, sizeof(h));
+        const unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_seg_prof, z, sizeof(z));
+        for (int w = 0; w < 2; ++w) {
+            const double tot = (double)(h[8 * w] + h[8 * w + 1] + h[8 * w + 2] + h[8 * w + 3]);
+            fprintf(stderr, "SEG_PROF %s: phase1 %.1f%% bar1+wait %.1f%% phase2 %.1f%% bar2 %.1f%% (ctas %llu, Mcycles/cta %.2f)\n",
+                    w ? "last thread" : "thread 0", 100 * h[8 * w] / tot, 100 * h[8 * w + 1] / tot,
+                    100 * h[8 * w + 2] / tot, 100 * h[8 * w + 3] / tot, h[8 * w + 4], tot / h[8 * w + 4] / 1e6);
+        }
+    }
+#endif
     return EBB_OK;
 }
 

@@ -91,9 +91,9 @@ struct SegPlan {
     uint4* tdesc = nullptr;           // ntiles + 1: {first vertex, instance offset, item offset
                                       //   (multiple of 32), entry offset (multiple of 4)}
     uint32_t* inst_t = nullptr;       // ninst: tet id of each instance (ascending per tile)
-    uint4* items = nullptr;           // nitems: {meta, row | vertex, transpose row, 0}; meta =
+    uint4* items = nullptr;           // nitems: {meta, row, transpose row | vertex, 0}; meta =
                                       //   begin[0:16) count[16:23) pos[23:26) last[26:29) kind[29:31)
-                                      //   kind 0 off-diagonal row, 1 self row, 2 vertex force; row ~0 = padding
+                                      //   kind 0 off-diagonal row, 1 self row + vertex force; row ~0 = padding
     uint32_t* ents = nullptr;         // nent: block entries oi | oj << 13 | pair << 26 (oi, oj =
                                       //   3 i NT + lr, 3 j NT + lr: state word offsets of k_i, k_j),
                                       //   force entries 3 corner NT + lr (offset of f_corner)

@@ -11,7 +11,8 @@
 //        vertices grown until the tets touching them ("instances") reach NT;
 //        a tile owns the canonical rows (tail <= head) of its vertices and
 //        their forces.  Per owned row the list of (instance, i, j) blocks that
-//        add into it, per owned vertex the list of (instance, corner) forces.
+//        add into it; a self row's list is exactly its vertex's (instance,
+//        corner) list, so the same walk also sums the vertex's force.
 //   kernel (persistent CTA of NT threads, one tile per pass)
 //        phase 1  thread = instance: element physics, compact state -> smem
 //                 (NH: k_i = F^-T g_i, W mu m_ij, W c1, W lam, f_i;
@@ -21,7 +22,7 @@
 //        phase 2  thread = owned row: walk its entries (staged in smem by a
 //                 bulk async copy issued one tile ahead), rebuild each 3x3
 //                 block from the state, sum in registers, store the row and its
-//                 transpose once; thread = owned vertex: sum its forces.
+//                 transpose once (self rows: the symmetric 6 + the force).
 // Every K row and f row is written exactly once (plain stores, no zero-fill),
 // in a fixed order: bitwise run-to-run deterministic.  The oracle computes the
 // same quantities by the textbook F-form and a generic 4th-order tensor
@@ -350,7 +351,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
         mbar_wait(&bar[b], (k >> 1) & 1);
         SEG_MARK(1);
         const uint32_t* E = ebuf + (size_t)b * max_ent;
-        // ---- phase 2: items = chunks of one row's (or one vertex's force) list;
+        // ---- phase 2: items = chunks of one row's list (self rows also sum the
+        // vertex's force: their entries are exactly its (instance, corner) pairs);
         // the chunks of a list sit in consecutive lanes and are combined by a
         // shuffle tree (items are padded to whole warps: the loop is warp-uniform)
         for (uint32_t base = 0; base < nit; base += NT) {
@@ -371,61 +373,51 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
                     seg_block<R, MODEL, NT>(st, x, a9);
                     x = nx;
                 }
-            } else if (kind == 1) {
+            } else {
+                // self row + the vertex's force: the same (instance, corner) list
                 uint32_t x = e0 < e1 ? E[e0] : 0u;
 #pragma unroll 2
                 for (uint32_t e = e0; e < e1; ++e) {
                     const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
                     seg_diag<R, MODEL, NT>(st, x, a9);
-                    x = nx;
-                }
-            } else {
-                uint32_t x = e0 < e1 ? E[e0] : 0u;
-#pragma unroll 2
-                for (uint32_t e = e0; e < e1; ++e) {
-                    const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
-                    const R* sf = st + G::F * NT + x;   // x = word offset of f_k[0]
-                    a9[0] += sf[0];
-                    a9[1] += sf[NT];
-                    a9[2] += sf[2 * NT];
+                    const R* sf = st + G::F * NT + (x & 0x1FFFu);   // f_i at the offset of k_i
+                    a9[6] += sf[0];
+                    a9[7] += sf[NT];
+                    a9[8] += sf[2 * NT];
                     x = nx;
                 }
             }
-            // combine the chunks of a list (values live: 9 / 6 / 3 by kind)
-            const uint32_t nval = __reduce_max_sync(0xFFFFFFFFu, kind == 0 ? 9u : kind == 1 ? 6u : 3u);
+            // combine the chunks of a list (9 values: a block, or 6 + a force)
 #pragma unroll
             for (uint32_t step = 1; step < 8; step <<= 1) {
                 if (!__any_sync(0xFFFFFFFFu, last >= step)) break;
                 const bool take = pos + step <= last;
 #pragma unroll
                 for (uint32_t q = 0; q < 9; ++q) {
-                    if (q >= nval) break;
                     const R o = __shfl_down_sync(0xFFFFFFFFu, a9[q], step);
                     if (take) a9[q] += o;
                 }
             }
             if (pos == 0 && item.y != 0xFFFFFFFFu) {
-                if (kind == 2) {
-                    R* dst = f + 3ull * item.y;
+                if (kind == 1) {
+                    R* df = f + 3ull * item.z;
 #pragma unroll
-                    for (int a = 0; a < 3; ++a) dst[a] = accumulate ? dst[a] + a9[a] : a9[a];
-                } else {
-                    if (kind == 1) {   // symmetric self block: expand 00 01 02 11 12 22
-                        const R d[6] = {a9[0], a9[1], a9[2], a9[3], a9[4], a9[5]};
-                        a9[0] = d[0]; a9[1] = d[1]; a9[2] = d[2];
-                        a9[3] = d[1]; a9[4] = d[3]; a9[5] = d[4];
-                        a9[6] = d[2]; a9[7] = d[4]; a9[8] = d[5];
-                    }
-                    R* dst = K + item.y;
+                    for (int a = 0; a < 3; ++a) df[a] = accumulate ? df[a] + a9[6 + a] : a9[6 + a];
+                    // symmetric self block: expand 00 01 02 11 12 22
+                    const R d[6] = {a9[0], a9[1], a9[2], a9[3], a9[4], a9[5]};
+                    a9[0] = d[0]; a9[1] = d[1]; a9[2] = d[2];
+                    a9[3] = d[1]; a9[4] = d[3]; a9[5] = d[4];
+                    a9[6] = d[2]; a9[7] = d[4]; a9[8] = d[5];
+                }
+                R* dst = K + item.y;
 #pragma unroll
-                    for (int q = 0; q < 9; ++q, dst += ne) *dst = accumulate ? *dst + a9[q] : a9[q];
-                    if (kind == 0) {
-                        dst = K + item.z;
+                for (int q = 0; q < 9; ++q, dst += ne) *dst = accumulate ? *dst + a9[q] : a9[q];
+                if (kind == 0) {
+                    dst = K + item.z;
 #pragma unroll
-                        for (int a = 0; a < 3; ++a)
+                    for (int a = 0; a < 3; ++a)
 #pragma unroll
-                            for (int c = 0; c < 3; ++c, dst += ne) *dst = accumulate ? *dst + a9[3 * c + a] : a9[3 * c + a];
-                    }
+                        for (int c = 0; c < 3; ++c, dst += ne) *dst = accumulate ? *dst + a9[3 * c + a] : a9[3 * c + a];
                 }
             }
         }
@@ -598,7 +590,7 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         sbase.assign(b - a + 1, 0);
         for (uint32_t v = a; v < b; ++v) sbase[v - a + 1] = sbase[v - a] + (index[v + 1] - rself[v]);
         const uint32_t ns = sbase[b - a], nvl = b - a;
-        lists.assign(ns + nvl, {});   // [0, ns): slot lists; [ns, ns + nvl): force lists
+        lists.assign(ns, {});   // slot lists; a self slot's list doubles as its vertex's force list
         for (uint32_t l = 0; l < ninst; ++l) {
             const uint32_t t = inst_t[i0 + l];
             const uint32_t* vv = &tv[4ull * t];
@@ -613,8 +605,6 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
                 lists[s].push_back((3 * bi * (uint32_t)ni + l) | ((3 * bj * (uint32_t)ni + l) << 13) |
                                    ((uint32_t)p << 26));
             }
-            for (uint32_t kk = 0; kk < 4; ++kk)
-                if (vv[kk] >= a && vv[kk] < b) lists[ns + vv[kk] - a].push_back(3 * kk * (uint32_t)ni + l);
         }
         // rows of the slots
         srow.resize(ns);
@@ -625,8 +615,8 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
                 srow[s] = r;
                 strow[s] = hd == tail ? r : lower_bound_u32(head.data(), index[hd], index[hd + 1], tail);
             }
-        // work lists in kind order: self rows (1), off-diagonal rows by
-        // descending length (0), vertex forces (2); entries in the same order
+        // work lists in kind order: self rows + forces (1), off-diagonal rows
+        // by descending length (0); entries in the same order
         order.clear();
         for (uint32_t lv = 0; lv < nvl; ++lv) order.push_back(sbase[lv]);
         const size_t n_self = order.size();
@@ -634,11 +624,9 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
             for (uint32_t s = sbase[lv] + 1; s < sbase[lv + 1]; ++s) order.push_back(s);
         std::stable_sort(order.begin() + n_self, order.end(),
                          [&](uint32_t x, uint32_t y) { return lists[x].size() > lists[y].size(); });
-        const size_t n_rows = order.size();
-        for (uint32_t v = 0; v < nvl; ++v) order.push_back(ns + v);
-        auto kind_of = [&](size_t qi) -> uint32_t { return qi < n_self ? 1u : qi < n_rows ? 0u : 2u; };
+        auto kind_of = [&](size_t qi) -> uint32_t { return qi < n_self ? 1u : 0u; };
         const size_t e_base = ents.size();
-        lbeg.assign(ns + nvl, 0);
+        lbeg.assign(ns, 0);
         size_t tot = 0, longest = 0;
         for (uint32_t q : order) {
             lbeg[q] = (uint32_t)(ents.size() - e_base);
@@ -672,7 +660,8 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
                     const uint32_t sz = cnt / nc + (cc < cnt % nc ? 1 : 0);
                     if (emit) {
                         const uint32_t meta = beg | (sz << 16) | (cc << 23) | ((nc - 1) << 26) | (kind << 29);
-                        items.push_back(kind == 2 ? make_uint4(meta, a + (q - ns), 0, 0)
+                        // self rows: z = the vertex (its force); off-diagonal: z = the transpose row
+                        items.push_back(kind == 1 ? make_uint4(meta, srow[q], a + (uint32_t)qi, 0)
                                                   : make_uint4(meta, srow[q], strow[q], 0));
                     }
                     beg += sz;

@@ -333,7 +333,8 @@ def run_ours(args, rank, world, local_rank):
         dom = "edge_matvec"
     d = kt[dom]
     ach = per_launch[dom] / (d["avg_us"] * 1e-6) / 1e9
-    roof = {"kernel": {"cg_solve": "k_cg_persistent (all 50 PCG iterations, one launch)",
+    cgk = "k_cg1_persistent (single-reduction PCG" if fem.cg_variant() == 2 else "k_cg_persistent (Saad PCG"
+    roof = {"kernel": {"cg_solve": cgk + ", all 50 iterations in one launch)",
                        "edge_matvec": "k_spmv_tma", "tet_map": "k_tet_map_seg"}[dom],
             "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "peak_source": peak_src, "traffic": _ncu_traffic(dom), "algorithmic_bytes_per_launch": per_launch[dom],

@@ -321,6 +321,8 @@ typedef struct {
  * cooperative kernel (grid barriers between the phases, deterministic dots);
  * ebb_cg_phase launches the phases separately (multi-GPU). No host sync. */
 ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream s);
+/* The variant ebb_cg_step runs for this system (AUTO resolved). Host-only. */
+ebb_status ebb_cg_variant(ebb_ctx ctx, const ebb_cg* cg, int32_t* out);
 /* a10-a12: `iters` Jacobi-PCG iterations (Saad Alg. 9.1), alpha/beta kept
  * on the device (no host sync); p.q <= 0 counts in error word [1]. */
 ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream s);

@@ -109,6 +109,7 @@ SIGS = {
     "ebb_tetmesh_rest": (S, [ctx_t, u32, u32, C.c_double, u32, u32, u32, stream_t]),
     "ebb_map_tet_forces": (S, [ctx_t, C.POINTER(TetMapDesc), stream_t]),
     "ebb_map_plan_stats": (S, [ctx_t, u32, u32, C.POINTER(C.c_double)]),
+    "ebb_cg_variant": (S, [ctx_t, C.POINTER(CG), C.POINTER(C.c_int32)]),
     "ebb_map_edge_matvec": (S, [ctx_t, u32, u32, u32, u32, u32, u32, stream_t]),
     "ebb_global_reduce": (S, [ctx_t, C.c_int32, u32, u32, u32, u32, stream_t]),
     "ebb_implicit_assemble": (S, [ctx_t, C.POINTER(ImplicitDesc), stream_t]),

@@ -1413,6 +1413,16 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     return EBB_OK;
 }
 
+ebb_status ebb_cg_variant(ebb_ctx ctx, const ebb_cg* cg, int32_t* out) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !cg || !out) return fail(c, EBB_E_ARG, "null argument");
+    EdgeGraph G;
+    ebb_dtype dt;
+    EBB_TRY(cg_validate(c, cg, &G, &dt));
+    *out = cg_variant(cg, G.nv, dt);
+    return EBB_OK;
+}
+
 ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
     if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");

@@ -157,6 +157,12 @@ class TetFEM:
             self.cg.variant = variant
         self.ctx.check(self.ctx.L.ebb_cg_init(self.ctx.h, C.byref(self.cg), _stream(stream)))
 
+    def cg_variant(self):
+        """The PCG variant ebb_cg_step runs (1 = Saad, 2 = single reduction)."""
+        out = C.c_int32()
+        self.ctx.check(self.ctx.L.ebb_cg_variant(self.ctx.h, C.byref(self.cg), C.byref(out)))
+        return out.value
+
     def cg_step(self, iters, stream=None):
         self.ctx.check(self.ctx.L.ebb_cg_step(self.ctx.h, C.byref(self.cg), int(iters), _stream(stream)))
 

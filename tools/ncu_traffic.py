@@ -13,7 +13,7 @@ import os
 import subprocess
 import sys
 
-KEYS = {"cg_solve": "k_cg_persistent", "tet_map": "k_tet_map_seg", "edge_matvec": "k_spmv"}
+KEYS = {"cg_solve": ("k_cg_persistent", "k_cg1_persistent"), "tet_map": ("k_tet_map_seg",), "edge_matvec": ("k_spmv",)}
 
 
 def main():
@@ -27,7 +27,7 @@ def main():
         d = dict(zip(h, r))
         name = d.get("Kernel Name", "")
         for key, pat in KEYS.items():
-            if pat in name:
+            if any(p_ in name for p_ in pat):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
                 b = 0.0
                 for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
@@ -36,6 +36,10 @@ def main():
                 acc[key].append((b, name, float(d["gpu__time_duration.sum"].replace(",", ""))))
     res = {}
     for key, v in acc.items():
+        if key == "edge_matvec":
+            v = [x for x in v if "k_cg" not in x[1]]
+            if not v:
+                continue
         res[key] = {"workload": workload, "dram_bytes_per_launch": sum(x[0] for x in v) / len(v),
                     "launches_captured": len(v), "ncu_kernel": v[0][1][:100], "capture": os.path.basename(path),
                     "ncu_duration_each": [x[2] for x in v],

@@ -90,7 +90,8 @@ struct SegPlan {
     double host_ms = 0;               // plan build time (host)
     uint4* tdesc = nullptr;           // ntiles + 1: {first vertex, instance offset, item offset
                                       //   (multiple of 32), entry offset (multiple of 4)}
-    uint32_t* inst_t = nullptr;       // ninst: tet id of each instance (ascending per tile)
+    uint32_t run = 1;                 // consecutive tiles per CTA run (state of shared tets carried)
+    uint2* inst = nullptr;            // ninst: each tile's NEW instances (tet, state slot | own << 16)
     uint4* items = nullptr;           // nitems: {meta, row, transpose row | vertex, 0}; meta =
                                       //   begin[0:16) count[16:23) pos[23:26) last[26:29) kind[29:31)
                                       //   kind 0 off-diagonal row, 1 self row + vertex force; row ~0 = padding
@@ -98,8 +99,9 @@ struct SegPlan {
                                       //   3 i NT + lr, 3 j NT + lr: state word offsets of k_i, k_j),
                                       //   force entries 3 corner NT + lr (offset of f_corner)
     void release() {
-        cudaFree(tdesc); cudaFree(inst_t); cudaFree(items); cudaFree(ents);
-        inst_t = ents = nullptr;
+        cudaFree(tdesc); cudaFree(inst); cudaFree(items); cudaFree(ents);
+        ents = nullptr;
+        inst = nullptr;
         tdesc = items = nullptr;
     }
 };

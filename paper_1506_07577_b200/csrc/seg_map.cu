@@ -162,14 +162,14 @@ __device__ __forceinline__ void seg_diag(const R* __restrict__ st, uint32_t ent,
 
 // CTAs per SM at NT = 256: two CTAs overlap one's barrier tail with the
 // other's work; fp32 state leaves room for a third (fp64 would spill) -- measured
-template <typename R>
-constexpr int seg_min_blocks() { return sizeof(R) == 4 ? 3 : 2; }
+template <typename R, int NT>
+constexpr int seg_min_blocks() { return NT <= 128 ? (sizeof(R) == 4 ? 6 : 4) : NT <= 256 ? (sizeof(R) == 4 ? 3 : 2) : 1; }
 #ifdef SEG_PROF
 __device__ unsigned long long g_seg_prof[16];
 #endif
 template <typename R, int MODEL, bool WANT_E, int NT>
-__global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet_map_seg(
-    uint32_t ntiles, const uint4* __restrict__ tdesc, const uint32_t* __restrict__ inst_t,
+__global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
+    uint32_t ntiles, uint32_t run, const uint4* __restrict__ tdesc, const uint2* __restrict__ inst,
     const uint4* __restrict__ items, const uint32_t* __restrict__ ents, uint32_t max_ent, uint64_t nt,
     const uint4* __restrict__ tv, const R* __restrict__ u, const R* __restrict__ Dminv, const R* __restrict__ Wt,
     const R* __restrict__ mu_t, const R* __restrict__ lam_t, R* __restrict__ f, R* __restrict__ K, uint64_t ne,
@@ -183,10 +183,16 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
                                                    // and of its successor (= its ends), slot j & 63
     __shared__ __align__(8) uint64_t bar[2];       // entry buffers 0/1
     const uint32_t tid = threadIdx.x, G0 = gridDim.x;
-    // this CTA's tiles: blockIdx.x + j G0 -- all CTAs sweep the SFC order
-    // together, so the tets and rows shared by neighbouring tiles meet in L2
-    const uint32_t tile0 = blockIdx.x;
-    const uint32_t m = tile0 < ntiles ? (ntiles - tile0 + G0 - 1) / G0 : 0;
+    // this CTA's tiles: the runs (of `run` consecutive tiles) blockIdx.x + r G0
+    // -- all CTAs sweep the SFC order together, so the tets and rows shared by
+    // neighbouring runs meet in L2; inside a run the state of the tets shared
+    // by consecutive tiles stays in shared memory (the plan keeps their slots)
+    const uint32_t nruns = (ntiles + run - 1) / run;
+    const uint32_t myruns = blockIdx.x < nruns ? (nruns - blockIdx.x + G0 - 1) / G0 : 0;
+    const uint32_t lastrun = myruns ? blockIdx.x + (myruns - 1) * G0 : 0;
+    const uint32_t m = myruns == 0 ? 0
+                     : (myruns - 1) * run + (lastrun == nruns - 1 ? ntiles - lastrun * run : run);
+    auto tile_of = [&](uint32_t j) -> uint32_t { return (blockIdx.x + (j / run) * G0) * run + j % run; };
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
     auto ring_fill = [&](uint32_t j) {   // warp 0, lane l: local tile j + l
         const uint32_t jj = j + (tid & 31);
         if (jj < m) {
-            const uint32_t t = tile0 + jj * G0;
+            const uint32_t t = tile_of(jj);
             const uint32_t d = smem_addr(&dring[jj & 63][0]);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(tdesc + t) : "memory");
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16), "l"(tdesc + t + 1) : "memory");
@@ -217,12 +223,14 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
         mbar_arrive_expect_tx(&bar[b], bytes);
         if (bytes) bulk_g2s(ebuf + (size_t)b * max_ent, ents + e0, bytes, &bar[b]);
     };
-    auto inst_of = [&](uint32_t j) -> uint32_t {
-        if (j >= m) return 0xFFFFFFFFu;
+    // the tile's NEW instances (tet, state slot | energy-owner << 16); carried
+    // ones are already in shared memory
+    auto inst_of = [&](uint32_t j) -> uint2 {
+        if (j >= m) return make_uint2(0xFFFFFFFFu, 0);
         const uint32_t i0 = D(j).y, n = Dn(j).y - i0;
-        return tid < n ? __ldg(inst_t + i0 + tid) : 0xFFFFFFFFu;
+        return tid < n ? __ldg(inst + i0 + tid) : make_uint2(0xFFFFFFFFu, 0);
     };
-    auto verts_of = [&](uint32_t t) -> uint4 { return t == 0xFFFFFFFFu ? make_uint4(0, 0, 0, 0) : __ldg(tv + t); };
+    auto verts_of = [&](uint2 t) -> uint4 { return t.x == 0xFFFFFFFFu ? make_uint4(0, 0, 0, 0) : __ldg(tv + t.x); };
 
     // first pass of a tile's phase-2 items, loaded one tile ahead
     const uint4 no_item = make_uint4(0, 0xFFFFFFFFu, 0xFFFFFFFFu, 0);
@@ -240,13 +248,13 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
     if (tid == 0 && m > 0) stage(0, 0);
     item_head(0);
     // software pipeline: inputs of this tile, keys of the next, tet id of the one after
-    uint32_t tc = inst_of(0);
+    uint2 tc = inst_of(0);
     uint4 vc = verts_of(tc);
     SegIn<R> in;
-    seg_load(tc, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
-    uint32_t t1 = inst_of(1);
+    seg_load(tc.x, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
+    uint2 t1 = inst_of(1);
     uint4 v1 = verts_of(t1);
-    uint32_t t2 = inst_of(2);
+    uint2 t2 = inst_of(2);
     double e_acc = 0.0;
 #ifdef SEG_PROF
     // per-CTA wall-clock split (thread 0 and a lane of the last warp): phase 1,
@@ -271,9 +279,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
             if ((j & 31) == 0 && j > 0) ring_fill(j + 32);
             if ((j & 31) == 16) asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        const uint32_t va = D(j).x, vb = Dn(j).x;
         // ---- phase 1: this thread's instance -> compact state
-        if (tc != 0xFFFFFFFFu) {
+        if (tc.x != 0xFFFFFFFFu) {
             TetState<R> ts;
 #pragma unroll
             for (int r = 0; r < 3; ++r)
@@ -285,13 +292,12 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
             ts.mu = in.mu;
             ts.lam = in.lam;
             tet_physics<R, MODEL, true>(in.uu, ts);
-            const uint32_t vmin = min(min(vc.x, vc.y), min(vc.z, vc.w));
-            const bool owner = vmin >= va && vmin < vb;   // the tile of the min vertex counts the tet once
+            const bool owner = (tc.y >> 16) & 1u;   // counted once: in its min vertex's run, first sighting
             if (MODEL == EBB_NH && owner && !(ts.J > R(0))) atomicAdd(&err[ERR_INVERTED], 1ull);
             if (WANT_E && owner) e_acc += (double)(ts.W * ts.psi);
             R fi[4][3];
             tet_forces(ts, fi);
-            R* sr = st + tid;
+            R* sr = st + (tc.y & 0xFFFFu);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
         // ---- advance the pipeline: these loads land during phase 2
         tc = t1;
         vc = v1;
-        seg_load(tc, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
+        seg_load(tc.x, vc, nt, u, Dminv, Wt, mu_t, lam_t, in);
         t1 = t2;
         v1 = verts_of(t1);
         t2 = inst_of(j + 3);
@@ -409,6 +415,9 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
                     a9[3] = d[1]; a9[4] = d[3]; a9[5] = d[4];
                     a9[6] = d[2]; a9[7] = d[4]; a9[8] = d[5];
                 }
+#ifdef SEG_NO_KSTORE   // measurement-only build: the cost of the scattered K row stores
+                if (a9[0] == R(12345.678)) K[item.y] = a9[1];
+#else
                 R* dst = K + item.y;
 #pragma unroll
                 for (int q = 0; q < 9; ++q, dst += ne) *dst = accumulate ? *dst + a9[q] : a9[q];
@@ -419,6 +428,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? seg_min_blocks<R>() : 1) k_tet
 #pragma unroll
                         for (int c = 0; c < 3; ++c, dst += ne) *dst = accumulate ? *dst + a9[3 * c + a] : a9[3 * c + a];
                 }
+#endif
             }
         }
         SEG_MARK(2);
@@ -499,13 +509,16 @@ void bank_schedule(uint4* it, size_t nit, uint32_t* ent, int ni) {
 }
 
 ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** out) {
+    const char* er = getenv("EBB_SEG_RUN");   // tiles per run (1 = no carry); measured default
+    const uint32_t run = (er && atoi(er) > 0 && atoi(er) <= 64) ? (uint32_t)atoi(er) : 4u;
     for (SegPlan* P : c->segplans)
-        if (P->v == vf && P->e == ef && P->ni == ni) {
+        if (P->v == vf && P->e == ef && P->ni == ni && P->run == run) {
             *out = P;
             return EBB_OK;
         }
     const auto t_start = std::chrono::steady_clock::now();
     const bool no_bank_sched = getenv("EBB_SEG_NO_BANK_SCHED") != nullptr;   // measurement knob
+    const bool len_order = getenv("EBB_SEG_LENORDER") != nullptr;           // measurement knob
     Field* V = get_field(c, vf);
     Field* E = get_field(c, ef);
     Relation& ER = c->rels[E->key_target];
@@ -562,37 +575,65 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         if (nv > 0) tile_v.push_back((uint32_t)nv);
     }
     const uint32_t ntiles = (uint32_t)tile_v.size() - 1;
-    std::vector<uint32_t> tile_inst{0}, tile_item{0}, tile_ent{0}, inst_t, ents;
+    std::vector<uint32_t> tile_inst{0}, tile_item{0}, tile_ent{0}, ents, tinst;
+    std::vector<uint2> inst;   // new instances of each tile: (tet, slot | energy owner << 16)
     std::vector<uint4> tdesc;
     std::vector<uint4> items;
     std::vector<uint32_t> srow, strow;   // per slot of the current tile: row, transpose row
-    inst_t.reserve(nt * 2);
+    inst.reserve(nt * 2);
+    // runs of consecutive tiles share one CTA; a tet in tiles k and k+1 of a
+    // run keeps its state slot (carried, computed once)
+    std::vector<uint32_t> tile_of_v(nv);
+    for (uint32_t T = 0; T < ntiles; ++T)
+        for (uint32_t v = tile_v[T]; v < tile_v[T + 1]; ++v) tile_of_v[v] = T;
+    std::vector<int64_t> last_tile(nt, -1), e_run(nt, -1), stamp(nt, -1);
+    std::vector<uint16_t> slot_of(nt, 0);
+    std::vector<char> slot_used(ni);
     ents.reserve(nt * 30);
-    std::vector<uint32_t> lr_of(nt, 0xFFFFFFFFu);
     std::vector<uint32_t> order, sbase, lbeg;
     std::vector<std::vector<uint32_t>> lists;
     uint32_t max_ent = 0, max_items = 0;
     for (uint32_t T = 0; T < ntiles; ++T) {
         const uint32_t a = tile_v[T], b = tile_v[T + 1];
         // instances: tets touching [a, b), ascending
-        const size_t i0 = inst_t.size();
+        tinst.clear();
         for (uint32_t v = a; v < b; ++v)
             for (uint32_t q = vt_ptr[v]; q < vt_ptr[v + 1]; ++q) {
                 const uint32_t t = vt[q];
-                if (lr_of[t] != T) {   // lr_of doubles as a per-tile stamp here
-                    lr_of[t] = T;
-                    inst_t.push_back(t);
+                if (stamp[t] != (int64_t)T) {
+                    stamp[t] = T;
+                    tinst.push_back(t);
                 }
             }
-        std::sort(inst_t.begin() + i0, inst_t.end());
-        const uint32_t ninst = (uint32_t)(inst_t.size() - i0);
+        std::sort(tinst.begin(), tinst.end());
+        const uint32_t ninst = (uint32_t)tinst.size();
+        // state slots: carried instances keep theirs, new ones take the free
+        // ones in ascending order; the energy (and the inverted-element count)
+        // of a tet goes with its first computation in its min vertex's run
+        const uint32_t runid = T / run, i0 = (uint32_t)inst.size();
+        std::fill(slot_used.begin(), slot_used.end(), 0);
+        for (uint32_t t : tinst)
+            if (T % run != 0 && last_tile[t] == (int64_t)T - 1) slot_used[slot_of[t]] = 1;
+        uint32_t nextfree = 0;
+        for (uint32_t t : tinst) {
+            if (T % run != 0 && last_tile[t] == (int64_t)T - 1) continue;
+            while (slot_used[nextfree]) ++nextfree;
+            slot_used[nextfree] = 1;
+            slot_of[t] = (uint16_t)nextfree;
+            const uint32_t* vv = &tv[4ull * t];
+            const uint32_t vmin = std::min(std::min(vv[0], vv[1]), std::min(vv[2], vv[3]));
+            const bool own = tile_of_v[vmin] / run == runid && e_run[t] != (int64_t)runid;
+            if (own) e_run[t] = runid;
+            inst.push_back(make_uint2(t, nextfree | (own ? 1u << 16 : 0u)));
+        }
+        for (uint32_t t : tinst) last_tile[t] = T;
         // canonical slots of the tile in row order
         sbase.assign(b - a + 1, 0);
         for (uint32_t v = a; v < b; ++v) sbase[v - a + 1] = sbase[v - a] + (index[v + 1] - rself[v]);
         const uint32_t ns = sbase[b - a], nvl = b - a;
         lists.assign(ns, {});   // slot lists; a self slot's list doubles as its vertex's force list
-        for (uint32_t l = 0; l < ninst; ++l) {
-            const uint32_t t = inst_t[i0 + l];
+        for (uint32_t li = 0; li < ninst; ++li) {
+            const uint32_t t = tinst[li], l = slot_of[t];
             const uint32_t* vv = &tv[4ull * t];
             for (int p = 0; p < 10; ++p) {
                 const int i = pair_i(p), j = pair_j(p);
@@ -622,8 +663,12 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         const size_t n_self = order.size();
         for (uint32_t lv = 0; lv < nvl; ++lv)
             for (uint32_t s = sbase[lv] + 1; s < sbase[lv + 1]; ++s) order.push_back(s);
-        std::stable_sort(order.begin() + n_self, order.end(),
-                         [&](uint32_t x, uint32_t y) { return lists[x].size() > lists[y].size(); });
+        // off-diagonal rows in row order: a warp's stores of one K plane land on
+        // neighbouring rows (measured: -7 % vs descending list length, which
+        // balances lanes better; EBB_SEG_LENORDER selects that)
+        if (len_order)
+            std::stable_sort(order.begin() + n_self, order.end(),
+                             [&](uint32_t x, uint32_t y) { return lists[x].size() > lists[y].size(); });
         auto kind_of = [&](size_t qi) -> uint32_t { return qi < n_self ? 1u : 0u; };
         const size_t e_base = ents.size();
         lbeg.assign(ns, 0);
@@ -676,10 +721,10 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         const size_t it_base = items.size();
         layout(L, true);
         if (!no_bank_sched) bank_schedule(items.data() + it_base, items.size() - it_base, ents.data() + e_base, ni);
-        for (uint32_t l = 0; l < ninst; ++l) lr_of[inst_t[i0 + l]] = 0xFFFFFFFEu;   // never a tile id
+        (void)i0;
         max_ent = std::max(max_ent, nent);
         max_items = std::max(max_items, (uint32_t)(items.size() - it_base));
-        tile_inst.push_back((uint32_t)inst_t.size());
+        tile_inst.push_back((uint32_t)inst.size());
         tile_item.push_back((uint32_t)items.size());
         tile_ent.push_back((uint32_t)ents.size());
     }
@@ -690,7 +735,8 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
     P->ntiles = ntiles;
     P->max_ent = max_ent;
     P->max_items = max_items;
-    P->ninst = inst_t.size();
+    P->ninst = inst.size();
+    P->run = run;
     P->nslots = 0;
     P->nent = ents.size();
     P->nitems = items.size();
@@ -700,7 +746,7 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
     };
     for (uint32_t T = 0; T <= ntiles; ++T) tdesc.push_back(make_uint4(tile_v[T], tile_inst[T], tile_item[T], tile_ent[T]));
     if (s == EBB_OK) s = upload(c, tdesc, &P->tdesc);
-    up(inst_t, &P->inst_t);
+    if (s == EBB_OK) s = upload(c, inst, &P->inst);
     if (s == EBB_OK) s = upload(c, items, &P->items);
     up(ents, &P->ents);
     if (s != EBB_OK) {
@@ -731,7 +777,7 @@ ebb_status launch_seg_t(Ctx* c, const SegPlan& P, bool want_e, int accumulate, u
     const char* eg = getenv("EBB_SEG_GRID");   // test knob: fewer CTAs = longer tile runs per CTA
     if (eg && atoi(eg) > 0 && (unsigned)atoi(eg) < grid) grid = (unsigned)atoi(eg);
     KernelTimer kt(c, EBB_K_TET_MAP, s);
-    kern<<<grid, NT, smem, s>>>(P.ntiles, P.tdesc, P.inst_t, P.items, P.ents, P.max_ent, nt, (const uint4*)V->ptr,
+    kern<<<grid, NT, smem, s>>>(P.ntiles, P.run, P.tdesc, P.inst, P.items, P.ents, P.max_ent, nt, (const uint4*)V->ptr,
                                 (const R*)U->ptr, (const R*)D->ptr, (const R*)W->ptr, (const R*)MU->ptr,
                                 (const R*)LA->ptr, (R*)Fo->ptr, (R*)Ko->ptr, ne, accumulate, c->d_partials,
                                 c->d_counter + 0, En ? (R*)En->ptr : nullptr, c->d_err);
@@ -760,7 +806,7 @@ ebb_status launch_seg_t(Ctx* c, const SegPlan& P, bool want_e, int accumulate, u
 // shared memory next to two entry buffers (fp64 StVK state is 52 words)
 int seg_threads(ebb_dtype dt, int model) {
     const char* e = getenv("EBB_SEG_NT");
-    if (e && (atoi(e) == 256 || atoi(e) == 384 || atoi(e) == 512)) {
+    if (e && (atoi(e) == 128 || atoi(e) == 256 || atoi(e) == 384 || atoi(e) == 512)) {
         const int v = atoi(e);
         return (dt == EBB_F64 && model == EBB_STVK && v > 384) ? 384 : v;
     }
@@ -778,6 +824,7 @@ ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool wa
 #define EBB_SARGS c, *P, want_e, accumulate, nt, V, U, D, W, MU, LA, Fo, Ko, ne, En, s
 #define EBB_SDISPATCH(R, MODEL)                                               \
     do {                                                                      \
+        if (NT == 128) return launch_seg_t<R, MODEL, 128>(EBB_SARGS);         \
         if (NT == 256) return launch_seg_t<R, MODEL, 256>(EBB_SARGS);         \
         if (NT == 384) return launch_seg_t<R, MODEL, 384>(EBB_SARGS);         \
         if constexpr (!(sizeof(R) == 8 && MODEL == EBB_STVK))                 \

@@ -510,7 +510,7 @@ void bank_schedule(uint4* it, size_t nit, uint32_t* ent, int ni) {
 
 ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** out) {
     const char* er = getenv("EBB_SEG_RUN");   // tiles per run (1 = no carry); measured default
-    const uint32_t run = (er && atoi(er) > 0 && atoi(er) <= 64) ? (uint32_t)atoi(er) : 4u;
+    const uint32_t run = (er && atoi(er) > 0 && atoi(er) <= 64) ? (uint32_t)atoi(er) : 1u;
     for (SegPlan* P : c->segplans)
         if (P->v == vf && P->e == ef && P->ni == ni && P->run == run) {
             *out = P;

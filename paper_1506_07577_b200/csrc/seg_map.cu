@@ -715,8 +715,12 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
             pad();
             return n;
         };
-        size_t L = std::max<size_t>({(size_t)2, (tot + ni - 1) / ni, (longest + 7) / 8});
-        while (L < longest && layout(L, false) > (size_t)ni) ++L;
+        // (a tile whose lists cannot fit one pass -- more rows than threads --
+        // runs several passes: L stops growing at 4x the even share)
+        const size_t L0 = std::max<size_t>({(size_t)2, (tot + ni - 1) / ni, (longest + 7) / 8});
+        const size_t Lcap = std::max<size_t>(L0, std::min<size_t>(127, 4 * L0));
+        size_t L = L0;
+        while (L < Lcap && L < longest && layout(L, false) > (size_t)ni) ++L;
         if (L > 127) return fail(c, EBB_E_RANGE, "segmented map: a list of %zu entries (> 8 x 127)", longest);
         const size_t it_base = items.size();
         layout(L, true);

@@ -1,0 +1,160 @@
+"""GPU parity on the degenerate and irregular inputs of the element map and
+the solver (SURVEY §8(c) pins; tolerances of BASELINE.json north_star):
+
+* the SPEC's 1-tet and 2-tet meshes for every scatter strategy;
+* isolated vertices (referenced by no tet): zero force, zero stiffness row,
+  the matvec's self-row-only vertex;
+* a small C3-style blob (irregular boundary, vertices of low degree) for every
+  strategy;
+* no locality renumbering (vertices in scrambled order: tiny, ragged tiles);
+* a vertex whose star exceeds the segmented map's per-tile instance cap is
+  refused with EBB_E_RANGE, never silently mishandled;
+* fp32 PCG iterates against the oracle fed the fp32-rounded system.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import rel_l2
+from synth import mesh as M
+from synth import state as S
+
+pytestmark = pytest.mark.gpu
+
+SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4, "color": 5}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1506_07577_b200 import ebb
+    c = ebb.Context(0)
+    yield c
+    c.close()
+
+
+def _fem_and_oracle(ctx, X, tets, model, name, dtype="f64", renumber=True, seed=1):
+    """GPU TetFEM and the oracle's map of the same input, both in stored order."""
+    from paper_1506_07577_b200.tetfem import TetFEM
+    rng = np.random.default_rng(seed)
+    h = np.cbrt(np.abs(np.linalg.det(np.stack([X[tets[:, k]] - X[tets[:, 0]] for k in (1, 2, 3)], 1))).mean())
+    u = 0.05 * X * np.array([1.0, -0.5, 0.3]) + rng.uniform(-0.03 * h, 0.03 * h, size=X.shape)
+    mu, lam = S.materials(tets.shape[0], 2e5, 0.3, spread=0.1)
+    if dtype == "f32":
+        u = u.astype(np.float32).astype(np.float64)
+        mu = mu.astype(np.float32).astype(np.float64)
+        lam = lam.astype(np.float32).astype(np.float64)
+    fem = TetFEM(ctx, X, tets, dtype=dtype, mu=mu, lam=lam, u=u, renumber=renumber, name=name)
+    if renumber:
+        new_of_old, tet_src, tets_new = oracle.renumber(X, tets)
+        order = np.argsort(new_of_old)
+        Xn, un, mun, lamn = X[order], u[order], mu[tet_src], lam[tet_src]
+    else:
+        Xn, tets_new, un, mun, lamn = X, fem.v.read().astype(np.int64), u, mu, lam
+    m = oracle.Mesh(Xn, tets_new)
+    f, K, en, inv = oracle.element_map(model, m.X, un, m.tets, m.Dminv, m.W, mun, lamn, e=m.e, ne=m.ne)
+    return fem, m, f, K, en
+
+
+@pytest.mark.parametrize("scatter", list(SCATTERS))
+@pytest.mark.parametrize("which", ["one", "two"])
+def test_spec_tiny_meshes(ctx, which, scatter):
+    X, tets = M.single_tet() if which == "one" else M.two_tets()
+    fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, "nh", f"tiny{which}{scatter}")
+    assert fem.ne == (16 if which == "one" else 23)
+    fem.map_forces("nh", scatter=SCATTERS[scatter])
+    assert rel_l2(fem.f.read(), f) <= 1e-12
+    assert rel_l2(fem.K.read(), K) <= 1e-12
+    assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+
+
+@pytest.mark.parametrize("scatter", list(SCATTERS))
+def test_isolated_vertices(ctx, scatter):
+    """Vertices no tet references: f = 0, their self row K = 0 (the relation
+    keeps every vertex, P:797 caption: one self-loop edge per vertex)."""
+    X, tets = M.kuhn6(3)
+    extra = np.array([[2.0, 2.0, 2.0], [-1.0, 0.5, 0.5], [0.5, 3.0, 0.1]])
+    X = np.vstack([X, extra])
+    X, tets = M.permute_vertices(X, tets, 11)
+    fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, "stvk", f"iso{scatter}")
+    fem.K.fill(7.0)                     # every row must be (over)written
+    fem.f.fill(7.0)
+    fem.map_forces("stvk", scatter=SCATTERS[scatter])
+    Kg, fg = fem.K.read(), fem.f.read()
+    assert rel_l2(fg, f) <= 1e-12 and rel_l2(Kg, K) <= 1e-12
+    deg = np.bincount(m.tets.ravel(), minlength=m.X.shape[0])
+    iso = np.nonzero(deg == 0)[0]
+    assert iso.size == 3
+    assert np.all(fg[iso] == 0.0)
+
+
+@pytest.mark.parametrize("scatter", list(SCATTERS))
+@pytest.mark.parametrize("model", ["stvk", "nh"])
+def test_small_blob(ctx, model, scatter):
+    """Irregular C3-style mesh (metaball boundary, low-degree vertices)."""
+    X, tets, n = M.blob(target_T=20_000)
+    fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, model, f"blob{model}{scatter}")
+    fem.map_forces(model, scatter=SCATTERS[scatter])
+    assert rel_l2(fem.f.read(), f) <= 1e-12
+    assert rel_l2(fem.K.read(), K) <= 1e-12
+    assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+
+
+@pytest.mark.parametrize("scatter", ["segmented", "tiled", "gather"])
+def test_without_renumbering(ctx, scatter):
+    """Scrambled vertex order (no SFC renumbering): tiles are ragged and
+    tiny, the plan still covers every row exactly once."""
+    X, tets = M.kuhn6(6)
+    X, tets = M.permute_vertices(X, tets, 5)
+    tets = M.permute_tets(tets, 6)
+    fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, "nh", f"noren{scatter}", renumber=False)
+    fem.map_forces("nh", scatter=SCATTERS[scatter])
+    assert rel_l2(fem.f.read(), f) <= 1e-12
+    assert rel_l2(fem.K.read(), K) <= 1e-12
+
+
+def _fan(k):
+    """k tets around one hub vertex (a triangulated bipyramid fan)."""
+    ang = 2 * np.pi * np.arange(k) / k
+    ring = np.stack([np.cos(ang), np.sin(ang), np.zeros(k)], 1)
+    X = np.vstack([[0.0, 0.0, 0.0], [0.0, 0.0, 1.0], ring])
+    tets = np.array([[0, 2 + i, 2 + (i + 1) % k, 1] for i in range(k)], dtype=np.int64)
+    d = np.einsum("ij,ij->i", X[tets[:, 1]] - X[tets[:, 0]],
+                  np.cross(X[tets[:, 2]] - X[tets[:, 0]], X[tets[:, 3]] - X[tets[:, 0]]))
+    tets[d < 0] = tets[d < 0][:, [0, 1, 3, 2]]
+    return X, tets
+
+
+def test_star_beyond_instance_cap(ctx, monkeypatch):
+    """A vertex in 200 tets: fine with 256 instances per tile, EBB_E_RANGE with 128."""
+    from paper_1506_07577_b200.ebb import EbbError
+    X, tets = _fan(200)
+    monkeypatch.setenv("EBB_SEG_NT", "256")
+    fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, "nh", "fan256")
+    fem.map_forces("nh", scatter=SCATTERS["segmented"])
+    assert rel_l2(fem.f.read(), f) <= 1e-12 and rel_l2(fem.K.read(), K) <= 1e-12
+    monkeypatch.setenv("EBB_SEG_NT", "128")
+    fem2, *_ = _fem_and_oracle(ctx, X, tets, "nh", "fan128")
+    with pytest.raises(EbbError, match="EBB_E_RANGE"):
+        fem2.map_forces("nh", scatter=SCATTERS["segmented"])
+
+
+@pytest.mark.parametrize("variant", ["1", "2"])
+def test_pcg_fp32(ctx, variant, monkeypatch):
+    """fp32 PCG (both variants) against the oracle's PCG on the fp32-rounded
+    system A, b: iterate agreement at fp32 round-off level."""
+    monkeypatch.setenv("EBB_CG_VARIANT", variant)
+    from helpers import Case, gpu_fem, oracle_renumbered
+    case = Case(n=5, model="nh")
+    fem = gpu_fem(ctx, case, dtype="f32", name=f"pcg32{variant}")
+    fem.map_forces("nh")
+    fem.assemble(1e-2)
+    A = fem.K.read().astype(np.float64)        # fp32 values, exactly representable
+    b = fem.b.read().astype(np.float64)
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    x_ref, hist, nspd = oracle.pcg(m.row_ptr, m.head, A, b, case.free[order], 20)
+    fem.cg_init()
+    fem.cg_step(20)
+    assert rel_l2(fem.dv.read(), x_ref) <= 1e-4

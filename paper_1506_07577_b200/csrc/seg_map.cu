@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
     uint2 t1 = inst_of(1);
     uint4 v1 = verts_of(t1);
     uint2 t2 = inst_of(2);
-    double e_acc = 0.0;
+    __shared__ double e_sm[NT];   // per-thread energy partial (kept out of the register budget)
+    e_sm[tid] = 0.0;
 #ifdef SEG_PROF
     // per-CTA wall-clock split (thread 0 and a lane of the last warp): phase 1,
     // barrier 1 + entry wait, phase 2, barrier 2
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
             tet_physics<R, MODEL, true>(in.uu, ts);
             const bool owner = (tc.y >> 16) & 1u;   // counted once: in its min vertex's run, first sighting
             if (MODEL == EBB_NH && owner && !(ts.J > R(0))) atomicAdd(&err[ERR_INVERTED], 1ull);
-            if (WANT_E && owner) e_acc += (double)(ts.W * ts.psi);
+            if (WANT_E && owner) e_sm[tid] += (double)(ts.W * ts.psi);
             R fi[4][3];
             tet_forces(ts, fi);
             R* sr = st + (tc.y & 0xFFFFu);
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
 #endif
     if (WANT_E) {
         double tot;
-        if (block_sum_last_done(e_acc, partials, counter, &tot)) *energy = (R)((double)*energy + tot);
+        if (block_sum_last_done(e_sm[tid], partials, counter, &tot)) *energy = (R)((double)*energy + tot);
     }
 }
 

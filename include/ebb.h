@@ -222,8 +222,16 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
                                    every thread computes one instance's
                                    compact element state, then every owned
                                    edge row sums its blocks rebuilt from the
-                                   states (segmented reduction, no atomics,
-                                   bitwise run-to-run deterministic).         */
+                                   states (segmented reduction over the
+                                   row's incident (tet, i, j), in
+                                   place of the `+=` of P:885; no atomics,
+                                   bitwise run-to-run deterministic).  The
+                                   plan is built on the host at the first call
+                                   for a (v, e) pair (synchronous; freed by
+                                   any relation permutation or ctx_free).
+                                   EBB_E_RANGE if one vertex lies in more tets
+                                   than the per-tile instance cap (256; 384
+                                   for StVK fp64; EBB_SEG_NT overrides).       */
 #define EBB_SCATTER_COLOR 5     /* tets greedily coloured (no two tets of a
                                    colour share a vertex), one launch per
                                    colour, plain read-modify-write reductions

@@ -591,8 +591,14 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
 // of each vertex applies every recurrence as it finishes the vertex's row.
 // Only u is read by neighbours (double-buffered); the rest is owner-local.
 // The first call after ebb_cg_init runs one extra matvec (w_0 = A z_0).
+#ifndef CG1_NS
+#define CG1_NS 4        // TMA ring depth of the single-reduction PCG
+#endif
+#ifndef CG1_MINB
+#define CG1_MINB 1
+#endif
 template <typename R>
-__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), CG1_MINB)
     k_cg1_persistent(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
                      const R* __restrict__ A, uint64_t ne, const R* __restrict__ dinv, R* __restrict__ x,
                      R* __restrict__ r, const R* __restrict__ z0, R* __restrict__ p, R* __restrict__ sv,
@@ -601,7 +607,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                      unsigned int* __restrict__ bar_gen, double* __restrict__ scal, double* __restrict__ rho_user,
                      unsigned long long* __restrict__ err, uint32_t cap, int iters) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
-    __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
+    __shared__ __align__(8) uint64_t full_bar[CG1_NS], empty_bar[CG1_NS];
     __shared__ double sm_tot;
     constexpr uint32_t AE = 16 / sizeof(R);
     const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
@@ -609,7 +615,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     const uint64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TMA_NS; ++s) {
+        for (int s = 0; s < CG1_NS; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], PCG_WPG);
         }
@@ -624,11 +630,11 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     int par = scal[S_PAR] != 0.0;             // u_i in buffer par
     uint64_t issued = 0;
     auto issue = [&](uint64_t ch, uint64_t seq) {
-        const int s = seq % TMA_NS;
+        const int s = seq % CG1_NS;
         const uint64_t v0 = ch * TMA_VCH;
         const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
         const uint64_t e0 = index[v0], e1 = index[v1];
-        if (seq >= TMA_NS) mbar_wait(&empty_bar[s], (uint32_t)(((seq / TMA_NS) + 1) & 1u));
+        if (seq >= CG1_NS) mbar_wait(&empty_bar[s], (uint32_t)(((seq / CG1_NS) + 1) & 1u));
         unsigned char* base = tma_smem + s * stage_bytes;
         uint32_t tot = 0;
 #pragma unroll
@@ -652,7 +658,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     };
     const int nphase = iters + (first && iters > 0 ? 1 : 0);
     if (warp == TMA_CONSUMERS && lane == 0 && nphase > 0)
-        for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+        for (uint64_t j = 0; j < my_chunks && j < CG1_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
     for (int ph = 0; ph < nphase; ++ph) {
         const bool pro = first != 0;          // prologue: w_0 = A z_0, u_0 = D w_0
         const R a = (R)alpha, b = (R)beta;
@@ -661,9 +667,9 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         double pg = 0.0, pd = 0.0;
         if (warp == TMA_CONSUMERS) {
             if (lane == 0) {
-                for (uint64_t j = TMA_NS; j < my_chunks; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+                for (uint64_t j = CG1_NS; j < my_chunks; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
                 if (ph + 1 < nphase)
-                    for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+                    for (uint64_t j = 0; j < my_chunks && j < CG1_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
             }
         } else {
             const unsigned grp = warp / PCG_WPG, wig = warp % PCG_WPG;
@@ -672,14 +678,14 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             for (uint64_t j = grp; j < my_chunks; j += PCG_GROUPS) {
                 const uint64_t seq = seq0 + j;
                 const uint64_t ch = blockIdx.x + j * gridDim.x;
-                const int s = seq % TMA_NS;
+                const int s = seq % CG1_NS;
                 const uint64_t v0 = ch * TMA_VCH;
                 const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
                 const uint64_t v = v0 + 4 * wig + (lane >> 3);
                 const bool valid = v < v1;
                 const uint32_t e0 = index[v0];
                 const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
-                mbar_wait(&full_bar[s], (uint32_t)((seq / TMA_NS) & 1u));
+                mbar_wait(&full_bar[s], (uint32_t)((seq / CG1_NS) & 1u));
                 const unsigned char* base = tma_smem + s * stage_bytes;
                 const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
                 uint32_t off[9];
@@ -1066,7 +1072,7 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     EBB_TRY(check_mask(c, cg->mask, G.verts, &mask));
     const uint32_t cap = (uint32_t)(TMA_VCH * (G.max_group ? G.max_group : 1) + 2 * (16 / sizeof(R)) + 4);
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
-    const size_t smem = stage * TMA_NS;
+    const size_t smem = stage * CG1_NS;
     if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
     static thread_local size_t configured = 0;
     if (smem > configured) {

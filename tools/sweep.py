@@ -28,6 +28,18 @@ def _flush(buf):
     buf.zero_()
 
 
+def _prewarm(seconds=0.5):
+    """Busy the GPU so clocks leave idle before anything is timed."""
+    import time
+
+    import torch
+    a = torch.empty(1 << 26, device="cuda")
+    t = time.perf_counter()
+    while time.perf_counter() - t < seconds:
+        a.mul_(1.0)
+        torch.cuda.synchronize()
+
+
 def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000, kuhn_n=0,
            scatters=("segmented", "gather", "tiled", "atomic")):
     import numpy as np
@@ -175,6 +187,7 @@ def main():
     a = ap.parse_args()
     from paper_1506_07577_b200 import build
     build.build()
+    _prewarm()
     if a.c2:
         run_c3(a.reps, kuhn_n=55, scatters=a.scatters.split(","), dtypes=a.dtypes.split(","),
                models=a.models.split(","))

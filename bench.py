@@ -404,6 +404,10 @@ def run_dist(args, rank, world, local_rank):
     def step():
         D.implicit_step([R], T, w["model"], h=w["h"], iters=w["cg_iters"])
 
+    t_pre = time.perf_counter()              # clocks ramp from idle (see run_ours)
+    while time.perf_counter() - t_pre < 0.5:
+        step()
+        torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

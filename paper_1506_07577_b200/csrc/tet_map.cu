@@ -6,8 +6,8 @@
 // reductions f[v[i]] += f_i, K[e[i][j]] += K_ij (field `+=`) and
 // energy += W Psi (global `+=`, fused two-pass).
 //
-// Two scatter strategies (SURVEY §8(a) "the += strategies", chosen by
-// measurement -- DESIGN.md §5):
+// The entry point and three of the five scatter strategies (SURVEY §8(a)
+// "the += strategies", chosen by measurement -- DESIGN.md §5.2):
 //   ATOMIC  one thread per tet, red.global.add per value (the paper's field
 //           reductions with native fp64 RED instead of Kepler CAS);
 //   TILED   owner-computes vertex tiles: a CTA owns the canonical edge rows
@@ -16,6 +16,9 @@
 //           memory and writes each K row and f row exactly once with plain
 //           stores (row (b,a) as the transpose of canonical (a,b)).  No global
 //           atomics, no zero-fill of K.
+//   GATHER  the same tiles, warp-specialized producer/consumer rounds.
+// SEGMENTED (the default, seg_map.cu) and COLOR (color_map.cu) live in their
+// own files.
 // The oracle computes the same quantities by the textbook F-form and a generic
 // 4th-order tensor contraction (oracle/ebb_oracle.c); the two share no code.
 #include <cub/cub.cuh>

@@ -317,6 +317,12 @@ typedef struct {
 } ebb_cg;
 #define EBB_CG_AUTO 0              /* the measured faster          */
 #define EBB_CG_SAAD 1              /* Saad Alg. 9.1: two reductions per iteration    */
+#define EBB_CG_SYMMETRIC 3         /* Saad Alg. 9.1 with the matvec over the upper
+                                      triangle only (A = A^T: half of A
+                                      streamed per iteration); the transposed
+                                      blocks reach their rows by red.global.add
+                                      (P:885), so iterates agree to round-off but
+                                      are not bitwise run-to-run reproducible    */
 #define EBB_CG_SINGLE_REDUCTION 2  /* Chronopoulos-Gear with the matvec moved onto
                                       u = D w: one fused reduction (r.z, w.z) and
                                       one gathered vector per iteration, same

@@ -267,6 +267,11 @@ void release_plans(Ctx* c) {
         delete P;
     }
     c->colorplans.clear();
+    for (UpperCSR* U : c->uppers) {
+        U->release();
+        delete U;
+    }
+    c->uppers.clear();
 }
 
 // Apply a row permutation to every field of `rel` and remap every key-field

@@ -120,6 +120,25 @@ struct ColorPlan {
     }
 };
 
+// Upper-triangle view of a grouped edge relation (rows tail <= head), used by
+// the symmetric-storage PCG (solver.cu): CSR offsets per vertex, head and
+// source (full) row of each upper row, and the compressed system matrices.
+struct UpperCSR {
+    ebb_rel edges = EBB_NONE;
+    uint64_t nu = 0;
+    uint32_t max_group = 0;
+    uint32_t* uptr = nullptr;   // nverts + 1
+    uint32_t* uhead = nullptr;  // nu
+    uint32_t* usrc = nullptr;   // nu: row of the full relation
+    std::vector<std::pair<ebb_field, void*>> ahalf;   // per system matrix: 9 planes of nu (+ slack)
+    void release() {
+        cudaFree(uptr); cudaFree(uhead); cudaFree(usrc);
+        for (auto& a : ahalf) cudaFree(a.second);
+        ahalf.clear();
+        uptr = uhead = usrc = nullptr;
+    }
+};
+
 struct Ctx : ebb_ctx_s {
     int device = 0;
     std::vector<Relation> rels;
@@ -143,6 +162,7 @@ struct Ctx : ebb_ctx_s {
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
     std::vector<SegPlan*> segplans; // (same)
     std::vector<ColorPlan*> colorplans; // (same)
+    std::vector<UpperCSR*> uppers;      // (same)
     struct GraphRec {
         cudaGraphExec_t exec = nullptr;
         unsigned long long launches = 0;

@@ -162,8 +162,11 @@ __device__ __forceinline__ void seg_diag(const R* __restrict__ st, uint32_t ent,
 
 // CTAs per SM at NT = 256: two CTAs overlap one's barrier tail with the
 // other's work; fp32 state leaves room for a third (fp64 would spill) -- measured
+#ifndef SEG_F32_MINB
+#define SEG_F32_MINB 3
+#endif
 template <typename R, int NT>
-constexpr int seg_min_blocks() { return NT <= 128 ? (sizeof(R) == 4 ? 6 : 4) : NT <= 256 ? (sizeof(R) == 4 ? 3 : 2) : 1; }
+constexpr int seg_min_blocks() { return NT <= 128 ? (sizeof(R) == 4 ? 6 : 4) : NT <= 256 ? (sizeof(R) == 4 ? SEG_F32_MINB : 2) : 1; }
 #ifdef SEG_PROF
 __device__ unsigned long long g_seg_prof[16];
 #endif

@@ -17,6 +17,8 @@
 // vertex is one 256-/128-bit access.
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "async_copy.cuh"
 #include "ebb_internal.cuh"
 #include "reduce.cuh"
@@ -576,6 +578,256 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
 }
 
 // ---------------------------------------------------------------------------
+// Symmetric-storage persistent PCG (Saad Alg. 9.1 iterates): A = A^T
+// (the stiffness of edge (a, b) is the transpose of (b, a)), so the
+// matvec streams only the upper triangle (rows tail <= head: ~half the bytes
+// of A, the dominant stream of every iteration).  Row (v, w) of the upper
+// CSR adds A_vw p_w to q_v (owner, in registers) and, for w != v, A_vw^T p_v
+// to q_w with red.global.add (the paper's field `+=`) -- q is zeroed
+// by the update phase of the previous iteration.  p.q needs no q:
+//   p.q = sum_v p_v.A_vv p_v + 2 sum_{v<w} p_v.A_vw p_w,
+// accumulated from the streamed blocks, so the structure is Saad's: matvec
+// phase -> grid barrier -> update phase (reads the complete q) -> barrier.
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
+    k_cg_sym_persistent(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
+                        const R* __restrict__ A, uint64_t ne, R* __restrict__ z, R* pb0, R* pb1, R* __restrict__ q,
+                        const R* __restrict__ dinv, R* __restrict__ x, R* __restrict__ r,
+                        const uint8_t* __restrict__ mask, double* __restrict__ part_pq, double* __restrict__ part_rz,
+                        unsigned int* __restrict__ bar_count, unsigned int* __restrict__ bar_gen,
+                        double* __restrict__ scal, double* __restrict__ rho_user, unsigned long long* __restrict__ err,
+                        uint32_t cap, int iters) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
+    __shared__ double sm_tot;
+    constexpr uint32_t AE = 16 / sizeof(R);
+    const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const uint64_t nchunks = (nv + TMA_VCH - 1) / TMA_VCH;
+    const uint64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TMA_NS; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], PCG_WPG);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    double rho = scal[S_RHO];
+    int first = scal[S_FIRST] != 0.0;
+    int cur = scal[S_PAR] != 0.0;
+    double rz_new = scal[S_RZ];
+    uint64_t issued = 0;
+    auto issue = [&](uint64_t ch, uint64_t seq) {
+        const int s = seq % TMA_NS;
+        const uint64_t v0 = ch * TMA_VCH;
+        const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+        const uint64_t e0 = index[v0], e1 = index[v1];
+        if (seq >= TMA_NS) mbar_wait(&empty_bar[s], (uint32_t)(((seq / TMA_NS) + 1) & 1u));
+        unsigned char* base = tma_smem + s * stage_bytes;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            tot += (uint32_t)((a1 - a0) * sizeof(R));
+        }
+        const uint64_t h0 = e0 & ~3ull, h1 = (e1 + 3) & ~3ull;
+        tot += (uint32_t)((h1 - h0) * 4);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full_bar[s], tot);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            bulk_g2s_evict_first(base + (size_t)c * cap * sizeof(R), A + a0, (uint32_t)((a1 - a0) * sizeof(R)),
+                                 &full_bar[s]);
+        }
+        bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
+    };
+    if (warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+    const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
+    for (int it = 0; it < iters; ++it) {
+        const R beta = (first || rho == 0.0) ? R(0) : (R)(rz_new / rho);
+        const R* __restrict__ pold = cur ? pb1 : pb0;
+        R* __restrict__ pnew = cur ? pb0 : pb1;
+        double pq = 0.0;
+        if (warp == TMA_CONSUMERS) {
+            if (lane == 0) {
+                for (uint64_t j = TMA_NS; j < my_chunks; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+                if (it + 1 < iters)
+                    for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
+            }
+        } else {
+            const unsigned grp = warp / PCG_WPG, wig = warp % PCG_WPG;
+            const unsigned sub = lane & 7;
+            const uint64_t seq0 = (uint64_t)it * my_chunks;
+            for (uint64_t j = grp; j < my_chunks; j += PCG_GROUPS) {
+                const uint64_t seq = seq0 + j;
+                const uint64_t ch = blockIdx.x + j * gridDim.x;
+                const int s = seq % TMA_NS;
+                const uint64_t v0 = ch * TMA_VCH;
+                const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+                const uint64_t v = v0 + 4 * wig + (lane >> 3);
+                const bool valid = v < v1;
+                const uint32_t e0 = index[v0];
+                const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
+                R own0 = 0, own1 = 0, own2 = 0;
+                if (valid && sub == 0) {
+                    const auto zv = ld4cg(z, v);
+                    const auto ov = ld4cg(pold, v);
+                    own0 = zv.x + beta * ov.x;
+                    own1 = zv.y + beta * ov.y;
+                    own2 = zv.z + beta * ov.z;
+                }
+                // p_v to every lane of the vertex (the transposed blocks need it)
+                const int src = (int)(lane & ~7u);
+                const R pv0 = __shfl_sync(0xffffffffu, own0, src);
+                const R pv1 = __shfl_sync(0xffffffffu, own1, src);
+                const R pv2 = __shfl_sync(0xffffffffu, own2, src);
+                mbar_wait(&full_bar[s], (uint32_t)((seq / TMA_NS) & 1u));
+                const unsigned char* base = tma_smem + s * stage_bytes;
+                const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
+                uint32_t off[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) off[c] = (uint32_t)((c * ne + e0) & (AE - 1));
+                R a0 = 0, a1 = 0, a2 = 0;
+                double dsum = 0.0;
+                for (uint32_t rb = r0 + sub; rb < r1; rb += 8) {
+                    const uint32_t h = hs[rb];
+                    const auto zh = ld4cg(z, h);
+                    const auto oh = ld4cg(pold, h);
+                    R av[9];
+#pragma unroll
+                    for (int c = 0; c < 9; ++c)
+                        av[c] = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R))[off[c] + rb];
+                    const R px = zh.x + beta * oh.x, py = zh.y + beta * oh.y, pz = zh.z + beta * oh.z;
+                    const R m0 = av[0] * px + av[1] * py + av[2] * pz;
+                    const R m1 = av[3] * px + av[4] * py + av[5] * pz;
+                    const R m2 = av[6] * px + av[7] * py + av[8] * pz;
+                    a0 += m0;
+                    a1 += m1;
+                    a2 += m2;
+                    const double d = (double)pv0 * m0 + (double)pv1 * m1 + (double)pv2 * m2;
+                    if (h != (uint32_t)v) {
+                        dsum += 2.0 * d;
+                        // q_h += A_vh^T p_v
+                        atomicAdd(q + 4ull * h + 0, av[0] * pv0 + av[3] * pv1 + av[6] * pv2);
+                        atomicAdd(q + 4ull * h + 1, av[1] * pv0 + av[4] * pv1 + av[7] * pv2);
+                        atomicAdd(q + 4ull * h + 2, av[2] * pv0 + av[5] * pv1 + av[8] * pv2);
+                    } else {
+                        dsum += d;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o, 8);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o, 8);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, o, 8);
+                }
+                pq += dsum;
+                if (sub == 0 && valid) {
+                    atomicAdd(q + 4ull * v + 0, a0);
+                    atomicAdd(q + 4ull * v + 1, a1);
+                    atomicAdd(q + 4ull * v + 2, a2);
+                    typename V4<R>::T pv;
+                    pv.x = own0; pv.y = own1; pv.z = own2; pv.w = 0;
+                    st4(pnew, v, pv);
+                }
+            }
+        }
+        pq = block_reduce<ROP_SUM>(pq);
+        if (threadIdx.x == 0) part_pq[blockIdx.x] = pq;
+        grid_barrier(bar_count, bar_gen, gridDim.x);
+        const double pqs = grid_sum_partials(part_pq, gridDim.x, &sm_tot);
+        if (blockIdx.x == 0 && threadIdx.x == 0 && pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+        rho = rz_new;
+        first = 0;
+        cur ^= 1;
+        const R alpha = (pqs != 0.0) ? (R)(rho / pqs) : R(0);
+        double acc = 0.0;
+        typename V4<R>::T zero4;
+        zero4.x = zero4.y = zero4.z = zero4.w = R(0);
+        for (uint64_t vv = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; vv < nv; vv += gthreads) {
+            const auto pv = ld4cg(pnew, vv);
+            auto qv = ld4cg(q, vv);
+            st4(q, vv, zero4);                       // ready for the next iteration's red.add
+            if (mask && !mask[vv]) qv = zero4;       // q = (A p) * mask
+            const auto dv = ld4(dinv, vv);
+            auto rv = ld4(r, vv);
+            rv.x -= alpha * qv.x;
+            rv.y -= alpha * qv.y;
+            rv.z -= alpha * qv.z;
+            typename V4<R>::T zv;
+            zv.x = rv.x * dv.x;
+            zv.y = rv.y * dv.y;
+            zv.z = rv.z * dv.z;
+            zv.w = 0;
+            st4(r, vv, rv);
+            st4(z, vv, zv);
+            x[3 * vv] += alpha * pv.x;
+            x[3 * vv + 1] += alpha * pv.y;
+            x[3 * vv + 2] += alpha * pv.z;
+            acc += (double)rv.x * zv.x + (double)rv.y * zv.y + (double)rv.z * zv.z;
+        }
+        acc = block_reduce<ROP_SUM>(acc);
+        if (threadIdx.x == 0) part_rz[blockIdx.x] = acc;
+        grid_barrier(bar_count, bar_gen, gridDim.x);
+        rz_new = grid_sum_partials(part_rz, gridDim.x, &sm_tot);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            scal[S_PQ] = pqs;
+            *rho_user = rz_new;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scal[S_RHO] = rho;
+        scal[S_RZ] = rz_new;
+        scal[S_FIRST] = first ? 1.0 : 0.0;
+        scal[S_PAR] = cur ? 1.0 : 0.0;
+    }
+}
+
+// upper-triangle CSR of a grouped edge relation
+__global__ void k_upper_count(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
+                              uint32_t* __restrict__ rself, uint32_t* __restrict__ cnt) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    uint32_t lo = index[v], hi = index[v + 1];
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (head[mid] < (uint32_t)v) lo = mid + 1;
+        else hi = mid;
+    }
+    rself[v] = lo;
+    cnt[v] = index[v + 1] - lo;
+}
+
+__global__ void k_upper_fill(uint64_t nv, const uint32_t* __restrict__ head, const uint32_t* __restrict__ rself,
+                             const uint32_t* __restrict__ uptr, uint32_t* __restrict__ uhead,
+                             uint32_t* __restrict__ usrc) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const uint32_t n = uptr[v + 1] - uptr[v];
+    for (uint32_t j = 0; j < n; ++j) {
+        uhead[uptr[v] + j] = head[rself[v] + j];
+        usrc[uptr[v] + j] = rself[v] + j;
+    }
+}
+
+template <typename R>
+__global__ void k_compress_upper(uint64_t nu, uint64_t ne, const uint32_t* __restrict__ usrc, const R* __restrict__ A,
+                                 R* __restrict__ Ah) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= nu) return;
+    const uint64_t src = usrc[k];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) Ah[(uint64_t)c * nu + k] = A[(uint64_t)c * ne + src];
+}
+
+// ---------------------------------------------------------------------------
 // Single-reduction persistent PCG (Chronopoulos-Gear):
 // the same iterates as Saad Alg. 9.1 in exact arithmetic, with ONE grid
 // barrier and ONE gathered vector per iteration (Saad: two barriers, two
@@ -594,11 +846,10 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
 #ifndef CG1_NS
 #define CG1_NS 4        // TMA ring depth of the single-reduction PCG
 #endif
-#ifndef CG1_MINB
-#define CG1_MINB 1
-#endif
+// (no min-blocks in the launch bounds: ptxas then keeps 72 registers, 3 CTAs
+// per SM; an explicit min-blocks of 1 let it take 148 and ran 1.5x slower)
 template <typename R>
-__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), CG1_MINB)
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     k_cg1_persistent(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
                      const R* __restrict__ A, uint64_t ne, const R* __restrict__ dinv, R* __restrict__ x,
                      R* __restrict__ r, const R* __restrict__ z0, R* __restrict__ p, R* __restrict__ sv,
@@ -1062,6 +1313,135 @@ ebb_status check_mask(Ctx* c, ebb_field m, ebb_rel rel, const uint8_t** out) {
 
 int cg_variant(const ebb_cg* cg, uint64_t nv, ebb_dtype dt);
 
+// upper-triangle CSR of `edges` (cached until the next relation permutation)
+ebb_status upper_csr(Ctx* c, ebb_rel edges, const EdgeGraph& G, UpperCSR** out) {
+    for (UpperCSR* U : c->uppers)
+        if (U->edges == edges) {
+            *out = U;
+            return EBB_OK;
+        }
+    const uint64_t nv = G.nv;
+    uint32_t *rself = nullptr, *cnt = nullptr, *tmp = nullptr;
+    UpperCSR* U = new UpperCSR();
+    U->edges = edges;
+    U->max_group = G.max_group;
+    auto cleanup = [&]() {
+        cudaFree(rself);
+        cudaFree(cnt);
+        cudaFree(tmp);
+    };
+    if (cudaMalloc(&rself, nv * 4 + 16) != cudaSuccess || cudaMalloc(&cnt, (nv + 1) * 4 + 16) != cudaSuccess ||
+        cudaMalloc(&U->uptr, (nv + 1) * 4 + 16) != cudaSuccess) {
+        cleanup();
+        U->release();
+        delete U;
+        return fail(c, EBB_E_CUDA, "cg: upper CSR allocation failed");
+    }
+    cudaMemset(cnt, 0, (nv + 1) * 4);
+    k_upper_count<<<grid_for(nv, 256), 256>>>(nv, G.index, G.head, rself, cnt);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, U->uptr, (int)(nv + 1));
+    cudaMalloc(&tmp, tb);
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, U->uptr, (int)(nv + 1));
+    uint32_t nu = 0;
+    cudaMemcpy(&nu, U->uptr + nv, 4, cudaMemcpyDeviceToHost);
+    U->nu = nu;
+    if (cudaMalloc(&U->uhead, (uint64_t)nu * 4 + 64) != cudaSuccess ||
+        cudaMalloc(&U->usrc, (uint64_t)nu * 4 + 64) != cudaSuccess) {
+        cleanup();
+        U->release();
+        delete U;
+        return fail(c, EBB_E_CUDA, "cg: upper CSR allocation failed");
+    }
+    k_upper_fill<<<grid_for(nv, 256), 256>>>(nv, G.head, rself, U->uptr, U->uhead, U->usrc);
+    const cudaError_t e = cudaDeviceSynchronize();
+    cleanup();
+    if (e != cudaSuccess) {
+        U->release();
+        delete U;
+        return cuda_fail(c, e, "upper_csr");
+    }
+    c->uppers.push_back(U);
+    *out = U;
+    return EBB_OK;
+}
+
+// the compressed (upper rows) copy of system matrix `Af`
+ebb_status upper_matrix(Ctx* c, UpperCSR* U, ebb_field Af, size_t esize, void** out) {
+    for (auto& a : U->ahalf)
+        if (a.first == Af) {
+            *out = a.second;
+            return EBB_OK;
+        }
+    void* p = nullptr;
+    EBB_CUDA(c, cudaMalloc(&p, 9 * U->nu * esize + 256));
+    U->ahalf.push_back({Af, p});
+    *out = p;
+    return EBB_OK;
+}
+
+template <typename R>
+ebb_status cg_sym_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s) {
+    UpperCSR* U;
+    EBB_TRY(upper_csr(c, cg->edges, G, &U));
+    void* Ah;
+    EBB_TRY(upper_matrix(c, U, cg->A, sizeof(R), &Ah));
+    const uint8_t* mask;
+    EBB_TRY(check_mask(c, cg->mask, G.verts, &mask));
+    auto F = [&](ebb_field f) { return (R*)c->fields[f].ptr; };
+    const uint32_t cap = (uint32_t)(TMA_VCH * (U->max_group ? U->max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+    const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const size_t smem = stage * TMA_NS;
+    if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
+    static thread_local size_t configured = 0;
+    if (smem > configured) {
+        EBB_CUDA(c, cudaFuncSetAttribute(k_cg_sym_persistent<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        configured = smem;
+    }
+    const int block = 32 * (TMA_CONSUMERS + 1);
+    int nb = 0;
+    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg_sym_persistent<R>, block, smem));
+    if (nb < 1) return fail(c, EBB_E_CUDA, "cg: persistent kernel does not fit on an SM");
+    const uint64_t nch = (G.nv + TMA_VCH - 1) / TMA_VCH;
+    uint64_t grid = (uint64_t)nb * c->num_sms;
+    if (grid > nch) grid = nch;
+    if (grid > 4096) grid = 4096;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KernelTimer kt(c, EBB_K_CG_SOLVE, s);
+    EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg_sym_persistent<R>, G.nv, (const uint32_t*)U->uptr,
+                                   (const uint32_t*)U->uhead, (const R*)Ah, (uint64_t)U->nu, F(cg->z), F(cg->p),
+                                   F(cg->p2), F(cg->q), (const R*)F(cg->dinv), F(cg->x), F(cg->r), mask,
+                                   c->d_partials, c->d_partials + 4096, c->d_counter + 10, c->d_counter + 11,
+                                   (double*)c->fields[cg->scal].ptr, (double*)c->fields[cg->rho].ptr, c->d_err, cap,
+                                   iters));
+    return EBB_OK;
+}
+
+// symmetric variant, at ebb_cg_init: the upper rows of A and q = 0
+template <typename R>
+ebb_status cg_sym_prepare(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, cudaStream_t s) {
+    UpperCSR* U;
+    EBB_TRY(upper_csr(c, cg->edges, G, &U));
+    void* Ah;
+    EBB_TRY(upper_matrix(c, U, cg->A, sizeof(R), &Ah));
+    c->launches++;
+    k_compress_upper<R><<<grid_for(U->nu, 256), 256, 0, s>>>(U->nu, G.ne, U->usrc, (const R*)c->fields[cg->A].ptr,
+                                                             (R*)Ah);
+    EBB_CUDA(c, cudaGetLastError());
+    EBB_CUDA(c, cudaMemsetAsync(c->fields[cg->q].ptr, 0, G.nv * 4 * sizeof(R), s));
+    return EBB_OK;
+}
+
 template <typename R>
 ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s) {
     for (ebb_field f : {cg->s, cg->y, cg->w, cg->u, cg->u2})
@@ -1122,8 +1502,9 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     double* scal = (double*)c->fields[cg->scal].ptr;
     double* rho_user = (double*)c->fields[cg->rho].ptr;
     const unsigned ug = occ_grid(c, k_cg_update<R>, 256, 0, G.nv);
-    if (only_phase < 0 && iters > 0 && cg_variant(cg, G.nv, sizeof(R) == 8 ? EBB_F64 : EBB_F32) == EBB_CG_SINGLE_REDUCTION)
-        return cg1_launch<R>(c, cg, G, iters, s);
+    const int variant = cg_variant(cg, G.nv, sizeof(R) == 8 ? EBB_F64 : EBB_F32);
+    if (only_phase < 0 && iters > 0 && variant == EBB_CG_SINGLE_REDUCTION) return cg1_launch<R>(c, cg, G, iters, s);
+    if (only_phase < 0 && iters > 0 && variant == EBB_CG_SYMMETRIC) return cg_sym_launch<R>(c, cg, G, iters, s);
     const char* mode = getenv("EBB_CG");
     if (only_phase < 0 && iters > 0 && !(mode && mode[0] == '2')) {
         // single launch, all iterations (cooperative: every CTA resident)
@@ -1188,7 +1569,7 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
 int cg_variant(const ebb_cg* cg, uint64_t nv, ebb_dtype dt) {
     if (cg->variant != EBB_CG_AUTO) return cg->variant;
     const char* e = getenv("EBB_CG_VARIANT");
-    if (e && (atoi(e) == EBB_CG_SAAD || atoi(e) == EBB_CG_SINGLE_REDUCTION)) return atoi(e);
+    if (e && atoi(e) >= EBB_CG_SAAD && atoi(e) <= EBB_CG_SYMMETRIC) return atoi(e);
     (void)dt;   // measured crossover (fp64 and fp32 alike): between 1.8e5 and 3.0e5 vertices
     return nv <= 232000 ? EBB_CG_SINGLE_REDUCTION : EBB_CG_SAAD;
 }
@@ -1370,7 +1751,7 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     // work vectors: padded 4-component records, allocated on first use
     static int serial = 0;
     char nm[64];
-    if (cg->variant < EBB_CG_AUTO || cg->variant > EBB_CG_SINGLE_REDUCTION)
+    if (cg->variant < EBB_CG_AUTO || cg->variant > EBB_CG_SYMMETRIC)
         return fail(c, EBB_E_ARG, "cg: unknown variant %d", cg->variant);
     ebb_field* work[] = {&cg->r, &cg->p, &cg->z, &cg->q, &cg->dinv, &cg->p2, &cg->s, &cg->y, &cg->w, &cg->u, &cg->u2};
     const char* wn[] = {"r", "p", "z", "q", "dinv", "p2", "s", "y", "w", "u", "u2"};
@@ -1416,6 +1797,10 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     else EBB_INIT(float);
 #undef EBB_INIT
     EBB_CUDA(c, cudaGetLastError());
+    if (cg_variant(cg, G.nv, dt) == EBB_CG_SYMMETRIC) {
+        if (dt == EBB_F64) return cg_sym_prepare<double>(c, cg, G, s);
+        return cg_sym_prepare<float>(c, cg, G, s);
+    }
     return EBB_OK;
 }
 

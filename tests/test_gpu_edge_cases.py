@@ -141,7 +141,7 @@ def test_star_beyond_instance_cap(ctx, monkeypatch):
         fem2.map_forces("nh", scatter=SCATTERS["segmented"])
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
 def test_pcg_fp32(ctx, variant, monkeypatch):
     """fp32 PCG (both variants) against the oracle's PCG on the fp32-rounded
     system A, b: iterate agreement at fp32 round-off level."""

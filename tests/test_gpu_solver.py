@@ -93,11 +93,12 @@ def test_global_reduce_large_masked(ctx):
     assert out.get() == x.max()
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
 @pytest.mark.parametrize("model", ["nh", "stvk"])
 def test_implicit_step(ctx, model, variant, monkeypatch):
-    """Both PCG variants (1 = Saad Alg. 9.1, 2 = single-reduction
-    Chronopoulos-Gear) reproduce the oracle's Saad iterates after 50 its."""
+    """Every PCG variant (1 = Saad Alg. 9.1, 2 = single-reduction
+    Chronopoulos-Gear, 3 = Saad on the symmetric half of A with red.add
+    transposes) reproduces the oracle's Saad iterates after 50 its."""
     monkeypatch.setenv("EBB_CG_VARIANT", variant)
     case = Case(n=6, model=model, vel_amp=0.05)
     h, iters, al, be = 1e-2, 50, 0.05, 0.002
@@ -131,7 +132,7 @@ def test_explicit_C1(ctx):
         assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
 def test_cg_zero_rhs_noop(ctx, variant, monkeypatch):
     monkeypatch.setenv("EBB_CG_VARIANT", variant)
     case = Case(n=3)
@@ -144,7 +145,7 @@ def test_cg_zero_rhs_noop(ctx, variant, monkeypatch):
     assert np.all(fem.dv.read() == 0.0) and fem.cg_rho() == 0.0
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
 def test_C2_full_size_implicit_step(ctx, variant, monkeypatch):
     """BASELINE configs[1] at full size (998,250 tets), bench launch configuration:
     integer maps bit-exact, f/K <= 1e-12, CG iterate <= 1e-8 after 50 iterations."""
@@ -185,7 +186,7 @@ def test_graph_capture_replays_the_step(ctx):
     assert rel_l2(b.dv.read(), a.dv.read()) <= 1e-12
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
 @pytest.mark.parametrize("iters", [1, 5, 20])
 def test_cg_iterates_and_split_calls(ctx, variant, iters, monkeypatch):
     """PCG iterate after k iterations matches the oracle's (Saad) iterate for
@@ -211,5 +212,6 @@ def test_cg_iterates_and_split_calls(ctx, variant, iters, monkeypatch):
             break
         fem.cg_step(k)
         done += k
-    assert rel_l2(fem.dv.read(), x1) <= 1e-13
+    # variant 3 sums the transposed blocks with red.add: run-to-run round-off
+    assert rel_l2(fem.dv.read(), x1) <= (1e-13 if variant != "3" else 1e-11)
     assert ctx.error_counts(reset=True)["not_spd"] == 0

@@ -17,6 +17,7 @@
 // vertex is one 256-/128-bit access.
 #include <cstdlib>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "async_copy.cuh"
@@ -370,6 +371,21 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
     __syncthreads();
 }
 
+// fp32 solves use the cooperative-groups grid sync, fp64 the counter barrier
+// above (measured per dtype, profiles/r01_c4_cg_barrier.txt: grid.sync is
+// 5-16 % faster in fp32, up to 8 % slower in fp64 at 1e7 tets)
+template <typename R>
+__device__ __forceinline__ void grid_barrier_t(unsigned int* count, unsigned int* gen, unsigned int nblocks) {
+    if constexpr (sizeof(R) == 4) {
+        (void)count;
+        (void)gen;
+        (void)nblocks;
+        cooperative_groups::this_grid().sync();
+    } else {
+        grid_barrier(count, gen, nblocks);
+    }
+}
+
 // sum of the per-CTA partials in block order, same value in every CTA
 __device__ __forceinline__ double grid_sum_partials(const double* partials, unsigned int n, double* sm_tot) {
     double s = 0.0;
@@ -531,7 +547,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         }
         pq = block_reduce<ROP_SUM>(pq);
         if (threadIdx.x == 0) part_pq[blockIdx.x] = pq;
-        grid_barrier(bar_count, bar_gen, gridDim.x);
+        grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         const double pqs = grid_sum_partials(part_pq, gridDim.x, &sm_tot);
         if (blockIdx.x == 0 && threadIdx.x == 0 && pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
         rho = rz_new;                   // rho_k = r_k . z_k (beta above used the previous rho)
@@ -562,7 +578,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         }
         acc = block_reduce<ROP_SUM>(acc);
         if (threadIdx.x == 0) part_rz[blockIdx.x] = acc;
-        grid_barrier(bar_count, bar_gen, gridDim.x);
+        grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         rz_new = grid_sum_partials(part_rz, gridDim.x, &sm_tot);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             scal[S_PQ] = pqs;
@@ -741,7 +757,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
         }
         pq = block_reduce<ROP_SUM>(pq);
         if (threadIdx.x == 0) part_pq[blockIdx.x] = pq;
-        grid_barrier(bar_count, bar_gen, gridDim.x);
+        grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         const double pqs = grid_sum_partials(part_pq, gridDim.x, &sm_tot);
         if (blockIdx.x == 0 && threadIdx.x == 0 && pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
         rho = rz_new;
@@ -775,7 +791,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
         }
         acc = block_reduce<ROP_SUM>(acc);
         if (threadIdx.x == 0) part_rz[blockIdx.x] = acc;
-        grid_barrier(bar_count, bar_gen, gridDim.x);
+        grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         rz_new = grid_sum_partials(part_rz, gridDim.x, &sm_tot);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             scal[S_PQ] = pqs;
@@ -1020,7 +1036,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             part_g[blockIdx.x] = pg;
             part_d[blockIdx.x] = pd;
         }
-        grid_barrier(bar_count, bar_gen, gridDim.x);
+        grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         const double dsum = grid_sum_partials(part_d, gridDim.x, &sm_tot);
         if (pro) {
             // a_0 = g_0 / (p_0 . A p_0), p_0 = z_0

@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
 // each barrier.  The producer warp keeps streaming: when a matvec phase ends
 // it immediately issues the first TMA_NS chunks of the next iteration, so the
 // HBM stream of A overlaps the latency-bound update phase and the barriers.
+#ifndef EBB_BAR_SLEEP_NS
+#define EBB_BAR_SLEEP_NS 64
+#endif
 __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -364,7 +367,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
             __threadfence();
             atomicAdd(gen, 1u);
         } else {
-            while (*reinterpret_cast<volatile unsigned int*>(gen) == g) __nanosleep(64);
+            while (*reinterpret_cast<volatile unsigned int*>(gen) == g) __nanosleep(EBB_BAR_SLEEP_NS);
         }
         __threadfence();
     }

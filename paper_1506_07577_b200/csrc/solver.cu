@@ -1157,38 +1157,56 @@ __global__ void __launch_bounds__(256) k_cg_update(uint64_t nv, const R* pbuf0, 
     }
 }
 
-// a9: A = M + h (alpha M + beta K) + h^2 K on every row of vertex v (in place ok)
+// a9 in one pass over K: A = M + h D + h^2 K (D = alpha M + beta K) written
+// row by row while the same rows accumulate (K v)_v, then
+// b_v = h (f + M g - D v - h K v).  LPV lanes per vertex (shuffle reduce);
+// A may alias K (every element is read, then written, by one thread).
 template <typename R, int LPV>
-__global__ void k_assemble_A(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
-                             const R* K, R* A, uint64_t ne, const R* __restrict__ mass, R h,
-                             R alpha, R beta) {
+__global__ void __launch_bounds__(256) k_assemble_fused(uint64_t nv, const uint32_t* __restrict__ index,
+                                                        const uint32_t* __restrict__ head, const R* K, R* A,
+                                                        uint64_t ne, const R* __restrict__ mass,
+                                                        const R* __restrict__ f, const R* __restrict__ vel,
+                                                        R* __restrict__ b, R h, R alpha, R beta, R g0, R g1, R g2) {
     const unsigned lane = threadIdx.x % LPV;
-    uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPV;
-    if (v >= nv) return;
-    const R m = mass[v];
-    for (uint32_t e = index[v] + lane; e < index[v + 1]; e += LPV) {
-        const bool diag = head[e] == v;
+    const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPV;
+    const bool live = v < nv;   // every lane reaches the shuffles
+    const R m = live ? mass[v] : R(0);
+    R k0 = 0, k1 = 0, k2 = 0;
+    if (live) {
+        for (uint32_t e = index[v] + lane; e < index[v + 1]; e += LPV) {
+            const uint32_t hd = head[e];
+            const bool diag = hd == (uint32_t)v;
+            const R w0 = vel[3ull * hd], w1 = vel[3ull * hd + 1], w2 = vel[3ull * hd + 2];
+            R Ke[9];
 #pragma unroll
-        for (int c = 0; c < 9; ++c) {
-            R Me = (diag && (c == 0 || c == 4 || c == 8)) ? m : R(0);
-            R Ke = K[(uint64_t)c * ne + e];
-            R De = alpha * Me + beta * Ke;
-            A[(uint64_t)c * ne + e] = Me + h * De + h * h * Ke;
+            for (int c = 0; c < 9; ++c) Ke[c] = K[(uint64_t)c * ne + e];
+            k0 += Ke[0] * w0 + Ke[1] * w1 + Ke[2] * w2;
+            k1 += Ke[3] * w0 + Ke[4] * w1 + Ke[5] * w2;
+            k2 += Ke[6] * w0 + Ke[7] * w1 + Ke[8] * w2;
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                const R Me = (diag && (c == 0 || c == 4 || c == 8)) ? m : R(0);
+                const R De = alpha * Me + beta * Ke[c];
+                A[(uint64_t)c * ne + e] = Me + h * De + h * h * Ke[c];
+            }
         }
     }
-}
-
-// b = h (f + M g - D v - h K v), D v = alpha M v + beta K v
-template <typename R>
-__global__ void k_assemble_b(uint64_t nv, const R* __restrict__ f, const R* __restrict__ mass, const R* __restrict__ vel,
-                             const R* __restrict__ Kv, R* __restrict__ b, R h, R alpha, R beta, R g0, R g1, R g2) {
-    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= 3 * nv) return;
-    const R g = (i % 3 == 0) ? g0 : ((i % 3 == 1) ? g1 : g2);
-    const R m = mass[i / 3];
-    R Mv = m * vel[i];
-    R Dv = alpha * Mv + beta * Kv[i];
-    b[i] = h * (f[i] + m * g - Dv - h * Kv[i]);
+#pragma unroll
+    for (int o = LPV / 2; o > 0; o >>= 1) {
+        k0 += __shfl_xor_sync(0xffffffffu, k0, o, LPV);
+        k1 += __shfl_xor_sync(0xffffffffu, k1, o, LPV);
+        k2 += __shfl_xor_sync(0xffffffffu, k2, o, LPV);
+    }
+    if (live && lane == 0) {
+        const R kv[3] = {k0, k1, k2}, g[3] = {g0, g1, g2};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const uint64_t i = 3 * v + a;
+            const R Mv = m * vel[i];
+            const R Dv = alpha * Mv + beta * kv[a];
+            b[i] = h * (f[i] + m * g[a] - Dv - h * kv[a]);
+        }
+    }
 }
 
 // O8: a = (f + m g)/m; u += v h + a h^2/2; v += a h (Fig. 2 applyForces)
@@ -1715,39 +1733,19 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
     EBB_TRY(check_vec(c, V, G.verts, dt, "vel"));
     EBB_TRY(check_vec(c, B, G.verts, dt, "b"));
     if (B->ptr == F->ptr || B->ptr == V->ptr) return fail(c, EBB_E_PHASE, "assemble: b aliases a read field");
-    // K v scratch (allocated once per context, on the vertex relation)
-    ebb_field kvf = EBB_NONE;
-    for (ebb_field f : c->rels[G.verts].fields)
-        if (c->fields[f].alive && c->fields[f].name == "__Kv" && c->fields[f].dtype == dt) kvf = f;
-    if (kvf == EBB_NONE) EBB_TRY(new_internal_field(c, G.verts, "__Kv", dt, 3, 1, EBB_AOS, &kvf));
-    // re-fetch (field table may have grown)
-    K = get_field(c, d->K);
-    A = get_field(c, d->A);
-    M = get_field(c, d->mass);
-    F = get_field(c, d->f);
-    V = get_field(c, d->vel);
-    B = get_field(c, d->b);
-    void* kv = c->fields[kvf].ptr;
     cudaStream_t s = (cudaStream_t)stream;
     const int lpv = G.max_group <= 16 ? 16 : 32;
 #define EBB_ASM(R)                                                                                                  \
     do {                                                                                                            \
-        EBB_TRY((launch_spmv3<R, false>(c, G, (const R*)K->ptr, (const R*)V->ptr, (R*)kv, nullptr, nullptr,          \
-                                        c->d_counter + 5, s, K->owned)));                                         \
         KernelTimer kt(c, EBB_K_ASSEMBLE, s);                                                                       \
-        c->launches++;                                                                                              \
-        k_assemble_b<R><<<grid_for(3 * G.nv, 256), 256, 0, s>>>(G.nv, (const R*)F->ptr, (const R*)M->ptr,             \
-                                                                (const R*)V->ptr, (const R*)kv, (R*)B->ptr, (R)d->h,  \
-                                                                (R)d->alpha, (R)d->beta, (R)d->g[0], (R)d->g[1],      \
-                                                                (R)d->g[2]);                                          \
         if (lpv == 16)                                                                                              \
-            k_assemble_A<R, 16><<<grid_for(G.nv * 16, 256), 256, 0, s>>>(G.nv, G.index, G.head, (const R*)K->ptr,     \
-                                                                         (R*)A->ptr, G.ne, (const R*)M->ptr, (R)d->h, \
-                                                                         (R)d->alpha, (R)d->beta);                    \
+            k_assemble_fused<R, 16><<<grid_for(G.nv * 16, 256), 256, 0, s>>>(                                        \
+                G.nv, G.index, G.head, (const R*)K->ptr, (R*)A->ptr, G.ne, (const R*)M->ptr, (const R*)F->ptr,      \
+                (const R*)V->ptr, (R*)B->ptr, (R)d->h, (R)d->alpha, (R)d->beta, (R)d->g[0], (R)d->g[1], (R)d->g[2]); \
         else                                                                                                        \
-            k_assemble_A<R, 32><<<grid_for(G.nv * 32, 256), 256, 0, s>>>(G.nv, G.index, G.head, (const R*)K->ptr,     \
-                                                                         (R*)A->ptr, G.ne, (const R*)M->ptr, (R)d->h, \
-                                                                         (R)d->alpha, (R)d->beta);                    \
+            k_assemble_fused<R, 32><<<grid_for(G.nv * 32, 256), 256, 0, s>>>(                                        \
+                G.nv, G.index, G.head, (const R*)K->ptr, (R*)A->ptr, G.ne, (const R*)M->ptr, (const R*)F->ptr,      \
+                (const R*)V->ptr, (R*)B->ptr, (R)d->h, (R)d->alpha, (R)d->beta, (R)d->g[0], (R)d->g[1], (R)d->g[2]); \
     } while (0)
     if (dt == EBB_F64) EBB_ASM(double);
     else EBB_ASM(float);

@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "tets/sec (force+stiffness map) and CG iters/sec at 1/2/4/8 B200; % HBM roofline"
 WORKLOAD = dict(name="C2", n=55, model="nh", E=2e5, nu=0.3, rho=1e3, h=1e-2, cg_iters=50, order_seed=2, u_seed=1)
 SAMPLE_N = 55          # oracle: the full C2 workload (about 6 s per step on one host core)
-CPU_BASELINE_STEPS = 2 # ~13 s of oracle work for the cpu_baseline field
+CPU_BASELINE_STEPS = 4 # ~12-25 s of oracle work for the cpu_baseline field (3-6 s per step)
 FLUSH_BYTES = 256 << 20
 
 

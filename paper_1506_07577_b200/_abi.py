@@ -61,7 +61,7 @@ class CG(C.Structure):
                 ("variant", C.c_int32), ("s", u32), ("y", u32), ("w", u32), ("u", u32), ("u2", u32)]
 
 
-CG_AUTO, CG_SAAD, CG_SINGLE_REDUCTION = 0, 1, 2
+CG_AUTO, CG_SAAD, CG_SINGLE_REDUCTION, CG_SYMMETRIC = 0, 1, 2, 3
 
 
 class ExplicitDesc(C.Structure):

@@ -158,3 +158,24 @@ def test_pcg_fp32(ctx, variant, monkeypatch):
     fem.cg_init()
     fem.cg_step(20)
     assert rel_l2(fem.dv.read(), x_ref) <= 1e-4
+
+
+def test_plan_stats_and_cg_variant_queries(ctx):
+    """ebb_map_plan_stats describes the plan the SEGMENTED map built (every tet
+    is an instance of >= 1 tile; 10 block entries per tet); ebb_cg_variant
+    resolves AUTO by the documented vertex-count rule."""
+    from helpers import Case, gpu_fem
+    case = Case(n=8, model="nh")
+    fem = gpu_fem(ctx, case, name="stats")
+    fem.map_forces("nh", scatter=SCATTERS["segmented"])
+    st = fem.plan_stats()
+    assert st["tiles"] >= 1 and st["instance_cap"] in (128, 256, 384, 512)
+    assert st["instances"] >= fem.nt and st["redundancy"] >= 1.0
+    assert st["entries"] >= 10 * fem.nt                       # + padding to 16 B per tile
+    fem.assemble(1e-2)
+    fem.cg_init()
+    assert fem.cg_variant() == 2                               # 729 vertices <= 2.3e5
+    from paper_1506_07577_b200 import _abi as A
+    fem.cg.variant = A.CG_SAAD
+    assert fem.cg_variant() == 1
+    fem.cg.variant = A.CG_AUTO

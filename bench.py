@@ -396,9 +396,15 @@ def run_dist(args, rank, world, local_rank):
     plan = D.halo_plan(G["tets"], G["owner_v"], world)
     tord = G["tet_order"]
     order = G["vert_order"]
+    stream = torch.cuda.Stream(device=dev)
     R = D.GpuRank(ctx, rank, G["X"], G["tets"], G["owner_v"], plan, free[order], u0[order],
-                  np.zeros_like(u0), mu[tord], lam[tord], rho=w["rho"], name=f"rank{rank}")
-    T = D.TorchTransport()
+                  np.zeros_like(u0), mu[tord], lam[tord], rho=w["rho"], stream=stream, name=f"rank{rank}")
+    try:
+        T = D.NcclTransport(ctx, rank, world, stream=stream)   # NCCL inside the library (ebb_comm_*)
+        transport = "nccl (in-library, ebb_comm_*)"
+    except Exception as ex:                            # noqa: BLE001
+        T = D.TorchTransport()
+        transport = f"torch.distributed ({type(ex).__name__})"
     T_global = tets.shape[0]
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
@@ -414,22 +420,46 @@ def run_dist(args, rank, world, local_rank):
     torch.cuda.synchronize()
     ctx.timing(True)
     ctx.timing_read(0, reset=True)
+    graph = None
+    if isinstance(T, D.NcclTransport) and not args.no_graph:
+        # the whole distributed step -- kernels and the in-library NCCL calls on
+        # one stream -- captured once and replayed (no host loop per iteration)
+        ctx.graph_begin(stream)
+        step()
+        graph = ctx.graph_end(stream)
+        ctx.graph_launch(graph, stream)       # untimed replay (keeps the captured timer records)
+        torch.cuda.synchronize()
     ctx.launch_count(reset=True)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    mp_tot, mp_cnt, mv_tot, mv_cnt = 0.0, 0, 0.0, 0
     dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
-            flush.zero_()
-            evs[k][0].record()
-            step()
-            evs[k][1].record()
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            evs[k][0].record(stream)
+            if graph is None:
+                step()
+            else:
+                ctx.graph_launch(graph, stream)
+            evs[k][1].record(stream)
+            if graph is not None:
+                evs[k][1].synchronize()               # read this replay's kernel events
+                ms_, n_ = ctx.timing_read(A.K_TET_MAP)
+                mp_tot += ms_
+                mp_cnt += n_
+                ms_, n_ = ctx.timing_read(A.K_EDGE_MATVEC)
+                mv_tot += ms_
+                mv_cnt += n_
         torch.cuda.synchronize()
     dist.barrier()
     launches = ctx.launch_count(reset=True)
     t_ms = sum(a.elapsed_time(b) for a, b in evs)
     mv_ms, mv_n = ctx.timing_read(A.K_EDGE_MATVEC)
     mp_ms, mp_n = ctx.timing_read(A.K_TET_MAP, reset=True)
+    if graph is not None:
+        mp_ms, mp_n, mv_ms, mv_n = mp_tot, mp_cnt, mv_tot, mv_cnt
     tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms = float(tt.item())
@@ -444,7 +474,7 @@ def run_dist(args, rank, world, local_rank):
     cfg = _config(world)
     cfg.update({"workload": f"C2 recipe weak-scaled: Kuhn-6 n={n} ({T_global} tets, {X.shape[0]} verts) split over "
                             f"{world} GPUs by the O4 owner maps (ghost tets, z halo + 2 scalar allreduces per "
-                            f"PCG iteration over NCCL), fp64",
+                            f"PCG iteration over NCCL), fp64", "transport": transport,
                 "tets": T_global, "parallelism": f"domain decomposition x{world} (NCCL halo + allreduce)"})
     line = {"metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -467,6 +497,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of a CUDA graph")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU (domain decomposition) path even with one rank (smoke test)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -474,18 +506,23 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        if world > 1:
+        if use_dist:
             run_dist(args, rank, world, local_rank)
         else:
             run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
             dist.destroy_process_group()
 

@@ -54,6 +54,7 @@ typedef int32_t ebb_status;
 #define EBB_E_RANGE (-11)       /* value does not fit the 32-bit key storage  */
 #define EBB_E_NOMEM (-12)       /* device allocation failed                   */
 #define EBB_E_DEGENERATE (-13)  /* |det Dm| <= 1e-12 l^3 (O1)                  */
+#define EBB_E_NCCL (-14)        /* NCCL missing or failed                      */
 
 typedef struct ebb_ctx_s* ebb_ctx;
 typedef uint32_t ebb_rel;
@@ -356,6 +357,26 @@ ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream
  * list relation; buf: AOS field of f's dtype and shape on the list relation. */
 ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s);
 ebb_status ebb_rows_scatter(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s);
+
+/* ---- NCCL inside the library ("NCCL over NVLink carries the
+ * halo exchange ... and the allreduce of CG scalars"; not in the paper,
+ * P:1014).  libnccl.so.2 is opened at run time (the copy the process already
+ * uses).  One communicator per context (one process per GPU); every call is
+ * stream-ordered, nothing synchronises the host.  EBB_E_NCCL if NCCL is
+ * missing or fails, EBB_E_STATE before ebb_comm_init. */
+typedef struct { char internal[128]; } ebb_nccl_id;
+/* rank 0 creates the id and shares it out of band (e.g. torch.distributed). */
+ebb_status ebb_comm_unique_id(ebb_nccl_id* out);
+ebb_status ebb_comm_init(ebb_ctx ctx, int32_t nranks, int32_t rank, const ebb_nccl_id* id);
+/* in-place sum over ranks of `count` F64 values in device memory (the PCG
+ * scalar slots of ebb_cg.scal: p.q, r.z). */
+ebb_status ebb_comm_allreduce_sum(ebb_ctx ctx, double* dev_buf, uint64_t count, ebb_stream s);
+/* grouped exchange with `npeers` ranks: send_bufs[k] (send_bytes[k]) to
+ * peers[k], recv_bufs[k] (recv_bytes[k]) from peers[k]; device buffers, as
+ * packed by ebb_rows_gather and unpacked by ebb_rows_scatter. */
+ebb_status ebb_comm_halo(ebb_ctx ctx, int32_t npeers, const int32_t* peers, void* const* send_bufs,
+                         const uint64_t* send_bytes, void* const* recv_bufs, const uint64_t* recv_bytes,
+                         ebb_stream s);
 
 typedef struct {
     ebb_field f, mass, mask;  /* mask: verts U8 (1 = free) or EBB_NONE        */

@@ -18,7 +18,7 @@ OK = 0
 E_NAMES = {
     -1: "EBB_E_ARG", -2: "EBB_E_DUP", -3: "EBB_E_SIZE", -4: "EBB_E_BOUNDS", -5: "EBB_E_TYPE",
     -6: "EBB_E_STATE", -7: "EBB_E_PHASE", -8: "EBB_E_INVERTED", -9: "EBB_E_NOT_SPD",
-    -10: "EBB_E_CUDA", -11: "EBB_E_RANGE", -12: "EBB_E_NOMEM", -13: "EBB_E_DEGENERATE",
+    -10: "EBB_E_CUDA", -11: "EBB_E_RANGE", -12: "EBB_E_NOMEM", -13: "EBB_E_DEGENERATE", -14: "EBB_E_NCCL",
 }
 F32, F64, I32, I64, U8, U32, KEY = 1, 2, 3, 4, 5, 6, 7
 AOS, SOA = 0, 1
@@ -109,6 +109,11 @@ SIGS = {
     "ebb_tetmesh_rest": (S, [ctx_t, u32, u32, C.c_double, u32, u32, u32, stream_t]),
     "ebb_map_tet_forces": (S, [ctx_t, C.POINTER(TetMapDesc), stream_t]),
     "ebb_map_plan_stats": (S, [ctx_t, u32, u32, C.POINTER(C.c_double)]),
+    "ebb_comm_unique_id": (S, [C.c_char_p]),
+    "ebb_comm_init": (S, [ctx_t, C.c_int32, C.c_int32, C.c_char_p]),
+    "ebb_comm_allreduce_sum": (S, [ctx_t, C.c_void_p, C.c_uint64, stream_t]),
+    "ebb_comm_halo": (S, [ctx_t, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p), C.POINTER(C.c_uint64),
+                          C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), stream_t]),
     "ebb_cg_variant": (S, [ctx_t, C.POINTER(CG), C.POINTER(C.c_int32)]),
     "ebb_map_edge_matvec": (S, [ctx_t, u32, u32, u32, u32, u32, u32, stream_t]),
     "ebb_global_reduce": (S, [ctx_t, C.c_int32, u32, u32, u32, u32, stream_t]),

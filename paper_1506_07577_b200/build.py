@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(" ".join(cmd))
             if rc != 0:
                 raise subprocess.CalledProcessError(rc, cmd)
-    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs]
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs, "-ldl"]
     subprocess.check_call(link)
     os.replace(LIB + ".tmp", LIB)
     return LIB

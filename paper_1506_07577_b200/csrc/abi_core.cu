@@ -366,6 +366,7 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
     if (c->scratch) cudaFree(c->scratch);
     for (auto& e : c->ev_pool) cudaEventDestroy(e);
     release_plans(c);
+    comm_release(c);
     for (auto& G : c->graphs)
         if (G.exec) cudaGraphExecDestroy(G.exec);
     cudaFree(c->d_err);

@@ -163,6 +163,8 @@ struct Ctx : ebb_ctx_s {
     std::vector<SegPlan*> segplans; // (same)
     std::vector<ColorPlan*> colorplans; // (same)
     std::vector<UpperCSR*> uppers;      // (same)
+    void* comm = nullptr;               // ncclComm_t (comm.cu)
+    int comm_size = 1, comm_rank = 0;
     struct GraphRec {
         cudaGraphExec_t exec = nullptr;
         unsigned long long launches = 0;
@@ -208,6 +210,7 @@ ebb_status scratch_reserve(Ctx* c, size_t bytes);
 ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_dtype dt, uint32_t rows,
                               uint32_t cols, ebb_layout layout, ebb_field* out);
 void release_plans(Ctx* c);
+void comm_release(Ctx* c);
 // seg_map.cu: the SEGMENTED element map (builds its plan on first use)
 ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
                           const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,

@@ -91,6 +91,58 @@ class TorchTransport:
             R.unpack(peer, rb)
 
 
+class NcclTransport:
+    """NCCL inside the library (ebb_comm_*): scalar allreduce and the grouped
+    halo send/recv are stream-ordered library calls on the rank's stream; no
+    torch collective on the iteration path.  The NCCL unique id is created by
+    rank 0 and shared through torch.distributed (only at construction)."""
+
+    def __init__(self, ctx, rank, size, stream=None):
+        import ctypes as C
+        self.C = C
+        self.ctx, self.rank, self.size, self.stream = ctx, rank, size, stream
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            ctx.check(ctx.L.ebb_comm_unique_id(uid))
+        if size > 1:
+            import torch
+            import torch.distributed as dist
+            t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).clone()
+            dev = torch.device("cuda", ctx.device) if dist.get_backend() == "nccl" else torch.device("cpu")
+            t = t.to(dev)
+            dist.broadcast(t, 0)
+            uid = C.create_string_buffer(bytes(t.cpu().tolist()), 128)
+        ctx.check(ctx.L.ebb_comm_init(ctx.h, int(size), int(rank), uid))
+
+    def _s(self):
+        from .ebb import _stream
+        return _stream(self.stream)
+
+    def allreduce(self, ranks, slots):
+        (R,) = ranks
+        t = R.scal_tensor()
+        lo, hi = slots
+        self.ctx.check(self.ctx.L.ebb_comm_allreduce_sum(self.ctx.h, t.data_ptr() + 8 * lo, hi - lo, self._s()))
+
+    def exchange(self, ranks):
+        (R,) = ranks
+        C = self.C
+        peers = R.peers()
+        if not peers:
+            return
+        n = len(peers)
+        sb = [R.pack(p) for p in peers]
+        rb = [R.recv_buffer(p) for p in peers]
+        P = (C.c_int32 * n)(*peers)
+        SP = (C.c_void_p * n)(*[b.data_ptr() for b in sb])
+        SN = (C.c_uint64 * n)(*[b.numel() * b.element_size() for b in sb])
+        RP = (C.c_void_p * n)(*[b.data_ptr() for b in rb])
+        RN = (C.c_uint64 * n)(*[b.numel() * b.element_size() for b in rb])
+        self.ctx.check(self.ctx.L.ebb_comm_halo(self.ctx.h, n, P, SP, SN, RP, RN, self._s()))
+        for p, b in zip(peers, rb):
+            R.unpack(p, b)
+
+
 class LocalTransport:
     """Several ranks driven from one process (virtual shards on one device)."""
 

@@ -67,3 +67,46 @@ def test_halo_plan_is_consistent(ctx):
         for o in range(3):
             assert np.array_equal(send[o][r], recv[r][o])
             assert np.all(part["owner_v"][send[o][r]] == o)
+
+
+def test_nccl_transport_single_rank(ctx):
+    """The in-library NCCL transport (ebb_comm_*; a 1-rank communicator on
+    this one-GPU box) drives the distributed step to the oracle's result: the
+    allreduces of the PCG scalars and the (empty) halo go through NCCL."""
+    from paper_1506_07577_b200 import dist
+    case = Case(n=6, model="nh", vel_amp=0.05)
+    h, iters = 1e-2, 50
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                               case.free[order], h, iters=iters)
+    G = dist.global_partition(ctx, case.X, case.tets, 1, name="nccl1")
+    plan = dist.halo_plan(G["tets"], G["owner_v"], 1)
+    tord = G["tet_order"]
+    R = dist.GpuRank(ctx, 0, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
+                     case.vel[order], case.mu[tord], case.lam[tord], name="nccl1r0")
+    T = dist.NcclTransport(ctx, 0, 1)
+    dist.implicit_step([R], T, "nh", h=h, iters=iters)
+    ids, dv = R.owned_values(R.fem.dv)
+    out = np.full((m.nv, 3), np.nan)
+    out[ids] = dv
+    assert rel_l2(out, ref["dv"]) <= 1e-8
+
+
+def test_nccl_allreduce_and_errors(ctx):
+    """ebb_comm_allreduce_sum on a device buffer (1 rank: identity) and the
+    state error before ebb_comm_init on a fresh context."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1506_07577_b200 import dist, ebb
+    fresh = ebb.Context(0)
+    buf = torch.arange(4, dtype=torch.float64, device="cuda")
+    with pytest.raises(ebb.EbbError, match="EBB_E_STATE"):
+        fresh.check(fresh.L.ebb_comm_allreduce_sum(fresh.h, buf.data_ptr(), 4, None))
+    dist.NcclTransport(fresh, 0, 1)
+    fresh.check(fresh.L.ebb_comm_allreduce_sum(fresh.h, buf.data_ptr(), 4, None))
+    torch.cuda.synchronize()
+    assert buf.tolist() == [0.0, 1.0, 2.0, 3.0]
+    fresh.close()
+    del C

@@ -315,6 +315,15 @@ typedef struct {
     ebb_field s, y, w, u, u2;     /* single-reduction work vectors: s = A p,
                             y = A D s, w = A z, u = D w (double-buffered with
                             u2; D = diag(A)^-1); EBB_NONE = allocated          */
+    double tol;          /* 0 = exactly `iters` iterations (the parity mode,
+                            SURVEY O10).  > 0: ebb_cg_step stops, on the
+                            device, after the first iteration k with
+                            r_k.z_k <= tol^2 r_0.z_0 (Jacobi-preconditioned
+                            residual relative to the start; SURVEY §8(f) 1
+                            "tolerance-based PCG"); every later ebb_cg_step
+                            is a no-op until ebb_cg_init.  The iterations run
+                            are read by ebb_cg_iterations.  ebb_cg_phase
+                            ignores tol (the multi-GPU driver decides).     */
 } ebb_cg;
 #define EBB_CG_AUTO 0              /* the measured faster          */
 #define EBB_CG_SAAD 1              /* Saad Alg. 9.1: two reductions per iteration    */
@@ -336,6 +345,10 @@ typedef struct {
  * cooperative kernel (grid barriers between the phases, deterministic dots);
  * ebb_cg_phase launches the phases separately (multi-GPU). No host sync. */
 ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream s);
+/* Iterations run since ebb_cg_init and whether the tolerance was met
+ * (converged = 1).  Synchronises the stream `s` (reads two device scalars);
+ * either output may be NULL. */
+ebb_status ebb_cg_iterations(ebb_ctx ctx, const ebb_cg* cg, ebb_stream s, int32_t* iters, int32_t* converged);
 /* The variant ebb_cg_step runs for this system (AUTO resolved). Host-only. */
 ebb_status ebb_cg_variant(ebb_ctx ctx, const ebb_cg* cg, int32_t* out);
 /* a10-a12: `iters` Jacobi-PCG iterations (Saad Alg. 9.1), alpha/beta kept

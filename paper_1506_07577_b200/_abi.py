@@ -58,7 +58,8 @@ class ImplicitDesc(C.Structure):
 class CG(C.Structure):
     _fields_ = [("edges", u32), ("A", u32), ("b", u32), ("x", u32), ("self", u32), ("mask", u32),
                 ("r", u32), ("p", u32), ("z", u32), ("q", u32), ("dinv", u32), ("rho", u32), ("scal", u32), ("p2", u32),
-                ("variant", C.c_int32), ("s", u32), ("y", u32), ("w", u32), ("u", u32), ("u2", u32)]
+                ("variant", C.c_int32), ("s", u32), ("y", u32), ("w", u32), ("u", u32), ("u2", u32),
+                ("tol", C.c_double)]
 
 
 CG_AUTO, CG_SAAD, CG_SINGLE_REDUCTION, CG_SYMMETRIC = 0, 1, 2, 3
@@ -115,6 +116,7 @@ SIGS = {
     "ebb_comm_halo": (S, [ctx_t, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p), C.POINTER(C.c_uint64),
                           C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), stream_t]),
     "ebb_cg_variant": (S, [ctx_t, C.POINTER(CG), C.POINTER(C.c_int32)]),
+    "ebb_cg_iterations": (S, [ctx_t, C.POINTER(CG), C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "ebb_map_edge_matvec": (S, [ctx_t, u32, u32, u32, u32, u32, u32, stream_t]),
     "ebb_global_reduce": (S, [ctx_t, C.c_int32, u32, u32, u32, u32, stream_t]),
     "ebb_implicit_assemble": (S, [ctx_t, C.POINTER(ImplicitDesc), stream_t]),

@@ -28,7 +28,8 @@ using namespace ebb;
 
 namespace {
 
-enum { S_RHO = 0, S_PQ = 1, S_RZ = 2, S_FIRST = 3, S_PAR = 4, S_ALPHA = 5, S_VAR = 6, S_NSCAL = 8 };
+enum { S_RHO = 0, S_PQ = 1, S_RZ = 2, S_FIRST = 3, S_PAR = 4, S_ALPHA = 5, S_VAR = 6, S_RZ0 = 7, S_ITERS = 8,
+       S_DONE = 9, S_NSCAL = 12 };
 
 template <typename R>
 struct V4;
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
     constexpr uint32_t AE = 16 / sizeof(R);   // elements per 16 B
     const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    if (DIR && scal[S_DONE] != 0.0) return;   // PCG converged (tolerance mode): no-op
     const uint64_t nchunks = (nv + TMA_VCH - 1) / TMA_VCH;
     const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                     const uint8_t* __restrict__ mask, double* __restrict__ part_pq, double* __restrict__ part_rz,
                     unsigned int* __restrict__ bar_count, unsigned int* __restrict__ bar_gen,
                     double* __restrict__ scal, double* __restrict__ rho_user, unsigned long long* __restrict__ err,
-                    uint32_t cap, int iters) {
+                    uint32_t cap, int iters, double tol2) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
     __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
     __shared__ double sm_tot;
@@ -429,6 +431,10 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     int first = scal[S_FIRST] != 0.0;
     int cur = scal[S_PAR] != 0.0;
     double rz_new = scal[S_RZ];
+    const double rz0 = scal[S_RZ0];
+    if (scal[S_DONE] != 0.0) iters = 0;   // converged in an earlier call (tolerance mode)
+    int done_it = 0;
+    bool conv = false;
     // producer state: global chunk sequence number (continues across iterations)
     uint64_t issued = 0;          // stage uses issued so far
     auto issue = [&](uint64_t ch, uint64_t seq) {
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
     };
     // prologue: the first TMA_NS chunks of iteration 0
-    if (warp == TMA_CONSUMERS && lane == 0)
+    if (iters > 0 && warp == TMA_CONSUMERS && lane == 0)
         for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
     const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
     for (int it = 0; it < iters; ++it) {
@@ -587,12 +593,23 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             scal[S_PQ] = pqs;
             *rho_user = rz_new;
         }
+        ++done_it;
+        if (tol2 > 0.0 && rz_new <= tol2 * rz0) {   // same value in every CTA: a uniform exit
+            conv = true;
+            break;
+        }
     }
+    // an early exit leaves the next iteration's prefetched chunks in flight
+    if (warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t sq = (uint64_t)done_it * my_chunks; sq < issued; ++sq)
+            mbar_wait(&full_bar[sq % TMA_NS], (uint32_t)((sq / TMA_NS) & 1u));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         scal[S_RHO] = rho;
         scal[S_RZ] = rz_new;
         scal[S_FIRST] = first ? 1.0 : 0.0;
         scal[S_PAR] = cur ? 1.0 : 0.0;
+        scal[S_ITERS] += (double)done_it;
+        if (conv) scal[S_DONE] = 1.0;
     }
 }
 
@@ -615,7 +632,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
                         const uint8_t* __restrict__ mask, double* __restrict__ part_pq, double* __restrict__ part_rz,
                         unsigned int* __restrict__ bar_count, unsigned int* __restrict__ bar_gen,
                         double* __restrict__ scal, double* __restrict__ rho_user, unsigned long long* __restrict__ err,
-                        uint32_t cap, int iters) {
+                        uint32_t cap, int iters, double tol2) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
     __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
     __shared__ double sm_tot;
@@ -636,6 +653,10 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
     int first = scal[S_FIRST] != 0.0;
     int cur = scal[S_PAR] != 0.0;
     double rz_new = scal[S_RZ];
+    const double rz0 = scal[S_RZ0];
+    if (scal[S_DONE] != 0.0) iters = 0;
+    int done_it = 0;
+    bool conv = false;
     uint64_t issued = 0;
     auto issue = [&](uint64_t ch, uint64_t seq) {
         const int s = seq % TMA_NS;
@@ -664,7 +685,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
         }
         bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
     };
-    if (warp == TMA_CONSUMERS && lane == 0)
+    if (iters > 0 && warp == TMA_CONSUMERS && lane == 0)
         for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
     const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
     for (int it = 0; it < iters; ++it) {
@@ -800,12 +821,22 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
             scal[S_PQ] = pqs;
             *rho_user = rz_new;
         }
+        ++done_it;
+        if (tol2 > 0.0 && rz_new <= tol2 * rz0) {
+            conv = true;
+            break;
+        }
     }
+    if (warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t sq = (uint64_t)done_it * my_chunks; sq < issued; ++sq)
+            mbar_wait(&full_bar[sq % TMA_NS], (uint32_t)((sq / TMA_NS) & 1u));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         scal[S_RHO] = rho;
         scal[S_RZ] = rz_new;
         scal[S_FIRST] = first ? 1.0 : 0.0;
         scal[S_PAR] = cur ? 1.0 : 0.0;
+        scal[S_ITERS] += (double)done_it;
+        if (conv) scal[S_DONE] = 1.0;
     }
 }
 
@@ -875,7 +906,8 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                      R* __restrict__ yv, R* __restrict__ wv, R* ub0, R* ub1, const uint8_t* __restrict__ mask,
                      double* __restrict__ part_g, double* __restrict__ part_d, unsigned int* __restrict__ bar_count,
                      unsigned int* __restrict__ bar_gen, double* __restrict__ scal, double* __restrict__ rho_user,
-                     unsigned long long* __restrict__ err, uint32_t cap, int iters) {
+                     unsigned long long* __restrict__ err, uint32_t cap, int iters,
+                     double tol2) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
     __shared__ __align__(8) uint64_t full_bar[CG1_NS], empty_bar[CG1_NS];
     __shared__ double sm_tot;
@@ -898,6 +930,10 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     double beta = scal[S_PQ];                 // b_i
     int first = scal[S_FIRST] != 0.0;         // w_0 not yet formed
     int par = scal[S_PAR] != 0.0;             // u_i in buffer par
+    const double rz0 = scal[S_RZ0];
+    if (scal[S_DONE] != 0.0) iters = 0;       // converged in an earlier call (tolerance mode)
+    int done_it = 0, done_ph = 0;
+    bool conv = false;
     uint64_t issued = 0;
     auto issue = [&](uint64_t ch, uint64_t seq) {
         const int s = seq % CG1_NS;
@@ -1058,8 +1094,22 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             par ^= 1;
             if (blockIdx.x == 0 && threadIdx.x == 0) *rho_user = gam;
         }
+        ++done_ph;
+        if (!pro) {
+            ++done_it;
+            if (tol2 > 0.0 && gam <= tol2 * rz0) {   // same value in every CTA: a uniform exit
+                conv = true;
+                break;
+            }
+        }
     }
+    // an early exit leaves the next phase's prefetched chunks in flight
+    if (warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t sq = (uint64_t)done_ph * my_chunks; sq < issued; ++sq)
+            mbar_wait(&full_bar[sq % CG1_NS], (uint32_t)((sq / CG1_NS) & 1u));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scal[S_ITERS] += (double)done_it;
+        if (conv) scal[S_DONE] = 1.0;
         scal[S_RHO] = gam;
         scal[S_RZ] = gam;
         scal[S_ALPHA] = alpha;
@@ -1114,6 +1164,9 @@ __global__ void __launch_bounds__(256) k_cg_init(uint64_t nv, const uint32_t* __
         scal[S_PQ] = 0.0;
         scal[S_FIRST] = 1.0;
         scal[S_PAR] = 0.0;
+        scal[S_RZ0] = tot;
+        scal[S_ITERS] = 0.0;
+        scal[S_DONE] = 0.0;
         if (rho_user) *rho_user = tot;
     }
 }
@@ -1124,7 +1177,9 @@ __global__ void __launch_bounds__(256) k_cg_update(uint64_t nv, const R* pbuf0, 
                                                    const R* __restrict__ dinv, R* __restrict__ x, R* __restrict__ r,
                                                    R* __restrict__ z, double* __restrict__ partials,
                                                    unsigned int* __restrict__ counter, double* __restrict__ scal,
-                                                   double* __restrict__ rho_user, unsigned long long* __restrict__ err) {
+                                                   double* __restrict__ rho_user, unsigned long long* __restrict__ err,
+                                                   double tol2) {
+    if (scal[S_DONE] != 0.0) return;   // converged (tolerance mode): the remaining launches are no-ops
     const double pqs = scal[S_PQ];
     const R alpha = (pqs != 0.0) ? (R)(scal[S_RHO] / pqs) : R(0);
     const R* __restrict__ p = scal[S_PAR] != 0.0 ? pbuf1 : pbuf0;   // the current direction
@@ -1154,6 +1209,8 @@ __global__ void __launch_bounds__(256) k_cg_update(uint64_t nv, const R* pbuf0, 
         if (pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
         scal[S_RZ] = tot;
         if (rho_user) *rho_user = tot;
+        scal[S_ITERS] += 1.0;
+        if (tol2 > 0.0 && tot <= tol2 * scal[S_RZ0]) scal[S_DONE] = 1.0;
     }
 }
 
@@ -1417,6 +1474,9 @@ ebb_status upper_matrix(Ctx* c, UpperCSR* U, ebb_field Af, size_t esize, void** 
     return EBB_OK;
 }
 
+// tolerance mode (ebb_cg.tol > 0): stop once r.z <= tol^2 r0.z0
+double cg_tol2(const ebb_cg* cg) { return cg->tol > 0.0 ? cg->tol * cg->tol : 0.0; }
+
 template <typename R>
 ebb_status cg_sym_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s) {
     UpperCSR* U;
@@ -1460,7 +1520,7 @@ ebb_status cg_sym_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters
                                    F(cg->p2), F(cg->q), (const R*)F(cg->dinv), F(cg->x), F(cg->r), mask,
                                    c->d_partials, c->d_partials + 4096, c->d_counter + 10, c->d_counter + 11,
                                    (double*)c->fields[cg->scal].ptr, (double*)c->fields[cg->rho].ptr, c->d_err, cap,
-                                   iters));
+                                   iters, cg_tol2(cg)));
     return EBB_OK;
 }
 
@@ -1520,7 +1580,7 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
                                    F(cg->p), F(cg->s), F(cg->y), F(cg->w), F(cg->u), F(cg->u2), mask, c->d_partials,
                                    c->d_partials + 4096, c->d_counter + 10, c->d_counter + 11,
                                    (double*)c->fields[cg->scal].ptr, (double*)c->fields[cg->rho].ptr, c->d_err, cap,
-                                   iters));
+                                   iters, cg_tol2(cg)));
     return EBB_OK;
 }
 
@@ -1577,7 +1637,7 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
                 EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg_persistent<R>, G.nv, G.index, G.head, A, G.ne, z, p, p2, q,
                                                dinv, x, r, mask, c->d_partials, c->d_partials + 4096,
                                                c->d_counter + 10, c->d_counter + 11, scal, rho_user, c->d_err, cap,
-                                               iters));
+                                               iters, cg_tol2(cg)));
                 return EBB_OK;
             }
         }
@@ -1592,7 +1652,7 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
         if (only_phase < 0 || only_phase == EBB_CG_UPDATE) {
             KernelTimer kt(c, EBB_K_CG_UPDATE, s);
             k_cg_update<R><<<ug, 256, 0, s>>>(G.nv, p, p2, q, dinv, x, r, z, c->d_partials, c->d_counter + 2, scal,
-                                              rho_user, c->d_err);
+                                              rho_user, c->d_err, only_phase < 0 ? cg_tol2(cg) : 0.0);
         }
     }
     EBB_CUDA(c, cudaGetLastError());
@@ -1821,6 +1881,20 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     return EBB_OK;
 }
 
+ebb_status ebb_cg_iterations(ebb_ctx ctx, const ebb_cg* cg, ebb_stream stream, int32_t* iters, int32_t* converged) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");
+    Field* S = get_field(c, cg->scal);
+    if (!S) return fail(c, EBB_E_STATE, "cg: call ebb_cg_init first");
+    if (S->dtype != EBB_F64 || c->rels[S->rel].size < S_NSCAL) return fail(c, EBB_E_TYPE, "cg: bad scal field");
+    double v[S_NSCAL];
+    EBB_CUDA(c, cudaMemcpyAsync(v, S->ptr, sizeof(v), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    EBB_CUDA(c, cudaStreamSynchronize((cudaStream_t)stream));
+    if (iters) *iters = (int32_t)v[S_ITERS];
+    if (converged) *converged = v[S_DONE] != 0.0 ? 1 : 0;
+    return EBB_OK;
+}
+
 ebb_status ebb_cg_variant(ebb_ctx ctx, const ebb_cg* cg, int32_t* out) {
     Ctx* c = (Ctx*)ctx;
     if (!c || !cg || !out) return fail(c, EBB_E_ARG, "null argument");
@@ -1841,6 +1915,9 @@ ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream 
     ebb_field w[] = {cg->r, cg->p, cg->z, cg->q, cg->dinv, cg->rho, cg->scal, cg->p2};
     for (ebb_field f : w)
         if (!get_field(c, f)) return fail(c, EBB_E_STATE, "cg: call ebb_cg_init first");
+    if (c->rels[get_field(c, cg->scal)->rel].size < S_NSCAL)
+        return fail(c, EBB_E_TYPE, "cg: scal must hold %d F64 values", (int)S_NSCAL);
+    if (!(cg->tol >= 0.0)) return fail(c, EBB_E_ARG, "cg: tol must be >= 0");
     cudaStream_t s = (cudaStream_t)stream;
     if (dt == EBB_F64) return cg_iterate<double>(c, cg, G, iters, s);
     return cg_iterate<float>(c, cg, G, iters, s);

@@ -144,7 +144,9 @@ class TetFEM:
         d.g[0], d.g[1], d.g[2] = g
         self.ctx.check(self.ctx.L.ebb_implicit_assemble(self.ctx.h, C.byref(d), _stream(stream)))
 
-    def cg_init(self, stream=None, variant=None):
+    def cg_init(self, stream=None, variant=None, tol=None):
+        """a11 start; tol > 0 selects the tolerance mode of ebb_cg_step (stop
+        once r.z <= tol^2 r0.z0), 0 the fixed-iteration parity mode."""
         if self.cg is None:
             cg = A.CG()
             cg.edges, cg.A, cg.b, cg.x, cg.self = self.edges.h, self.K.h, self.b.h, self.dv.h, self.self_e.h
@@ -155,6 +157,8 @@ class TetFEM:
             self.cg = cg
         if variant is not None:
             self.cg.variant = variant
+        if tol is not None:
+            self.cg.tol = float(tol)
         self.ctx.check(self.ctx.L.ebb_cg_init(self.ctx.h, C.byref(self.cg), _stream(stream)))
 
     def cg_variant(self):
@@ -165,6 +169,13 @@ class TetFEM:
 
     def cg_step(self, iters, stream=None):
         self.ctx.check(self.ctx.L.ebb_cg_step(self.ctx.h, C.byref(self.cg), int(iters), _stream(stream)))
+
+    def cg_iterations(self, stream=None):
+        """(iterations run since cg_init, tolerance met) -- synchronises."""
+        it, conv = C.c_int32(), C.c_int32()
+        self.ctx.check(self.ctx.L.ebb_cg_iterations(self.ctx.h, C.byref(self.cg), _stream(stream), C.byref(it),
+                                                    C.byref(conv)))
+        return it.value, bool(conv.value)
 
     def cg_rho(self):
         out = C.c_double()

@@ -215,3 +215,46 @@ def test_cg_iterates_and_split_calls(ctx, variant, iters, monkeypatch):
     # variant 3 sums the transposed blocks with red.add: run-to-run round-off
     assert rel_l2(fem.dv.read(), x1) <= (1e-13 if variant != "3" else 1e-11)
     assert ctx.error_counts(reset=True)["not_spd"] == 0
+
+
+@pytest.mark.parametrize("variant,fallback", [("1", False), ("2", False), ("3", False), ("1", True)])
+def test_cg_tolerance_mode(ctx, variant, fallback, monkeypatch):
+    """SURVEY §8(f) 1, tolerance-based PCG: with ebb_cg.tol > 0 the solve stops
+    on the device after the first iteration k with r_k.z_k <= tol^2 r_0.z_0.
+    k is read off the oracle's r.z history on the same system (the stop rule
+    is that definition), the iterate must be the oracle's k-th, later calls
+    are no-ops, and tol = 0 keeps the fixed-iteration parity mode."""
+    monkeypatch.setenv("EBB_CG_VARIANT", variant)
+    if fallback:
+        monkeypatch.setenv("EBB_CG", "2")            # one launch per phase (Saad)
+    case = Case(n=6, model="nh", vel_amp=0.05)
+    fem = gpu_fem(ctx, case, name=f"cgtol{variant}{int(fallback)}")
+    fem.map_forces("nh")
+    fem.assemble(1e-2)
+    A, b = fem.K.read(), fem.b.read()
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    free = case.free[order]
+    nmax = 400
+    _, hist, _ = oracle.pcg(m.row_ptr, m.head, A, b, free, nmax)
+    for tol in (1e-2, 1e-4):
+        thr = tol * tol * hist[0]
+        k = next(k for k in range(1, nmax + 1) if hist[k] <= thr)
+        # fp64 decides the stop on both sides: the rule must not sit on the threshold
+        assert abs(hist[k] - thr) > 1e-6 * thr and abs(hist[k - 1] - thr) > 1e-6 * thr
+        x_ref, _, _ = oracle.pcg(m.row_ptr, m.head, A, b, free, k)
+        fem.cg_init(tol=tol)
+        fem.cg_step(3)
+        fem.cg_step(nmax)
+        assert fem.cg_iterations() == (k, True)
+        x = fem.dv.read()
+        assert rel_l2(x, x_ref) <= 1e-9
+        fem.cg_step(10)                                  # converged: a no-op
+        assert fem.cg_iterations() == (k, True)
+        assert np.array_equal(fem.dv.read(), x)
+    fem.cg_init(tol=0.0)
+    fem.cg_step(4)
+    fem.cg_step(3)
+    assert fem.cg_iterations() == (7, False)
+    x_ref, _, _ = oracle.pcg(m.row_ptr, m.head, A, b, free, 7)
+    assert rel_l2(fem.dv.read(), x_ref) <= 1e-9
+    assert ctx.error_counts(reset=True)["not_spd"] == 0

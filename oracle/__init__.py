@@ -59,6 +59,8 @@ def lib():
             "orc_dot": (D, [I, P, P]),
             "orc_explicit_update": (None, [I, P, P, P, P, D, P, P]),
             "orc_implicit_assemble": (None, [I, P, P, P, P, P, P, D, D, D, P, P, P]),
+            "orc_consistent_mass": (None, [I, P, P, D, I, P]),
+            "orc_implicit_assemble_consistent": (None, [I, P, P, P, P, P, P, D, D, D, P, P, P]),
             "orc_pcg": (C.c_int, [I, P, P, P, P, P, C.c_int, P, P]),
             "orc_implicit_update": (None, [I, P, D, P, P]),
         }
@@ -231,6 +233,27 @@ def implicit_assemble(row_ptr, head, K, mass, f, vel, h, alpha=0.0, beta=0.0, g=
     return A, b
 
 
+def consistent_mass(tets_e, W, rho, ne):
+    """Consistent (Galerkin) mass on the edge relation: mass_e[E] with
+    M_r = mass_e[r] I_3, mass_e[e[i][j]] += rho W (1 + d_ij) / 20."""
+    e = _i64(tets_e).reshape(-1, 16)
+    m = np.empty(ne)
+    lib().orc_consistent_mass(e.shape[0], _p(e), _p(_f64(W)), rho, ne, _p(m))
+    return m
+
+
+def implicit_assemble_consistent(row_ptr, head, K, mass_e, f, vel, h, alpha=0.0, beta=0.0,
+                                 g=(0.0, -9.81, 0.0)):
+    """O9 with the consistent edge mass (M v, M g as edge query-loops)."""
+    nv = row_ptr.shape[0] - 1
+    A = np.empty_like(_f64(K))
+    b = np.empty((nv, 3))
+    lib().orc_implicit_assemble_consistent(nv, _p(_i64(row_ptr)), _p(_i64(head)), _p(_f64(K)),
+                                           _p(_f64(mass_e)), _p(_f64(f)), _p(_f64(vel)), h, alpha, beta,
+                                           _p(_f64(np.asarray(g))), _p(A), _p(b))
+    return A, b
+
+
 # ---------------------------------------------------------------- O10
 def pcg(row_ptr, head, A, b, free, iters):
     """O10: (x[V,3], rho_hist[iters+1], not_spd)."""
@@ -260,6 +283,7 @@ class Mesh:
         self.nv, self.nt = self.X.shape[0], self.tets.shape[0]
         self.tail, self.head, self.row_ptr, self.e = edges(self.nv, self.tets)
         self.ne = self.tail.shape[0]
+        self.rho = rho
         self.Dminv, self.W, self.mass = rest(self.X, self.tets, rho)
 
 
@@ -271,11 +295,16 @@ def explicit_step(mesh, model, u, v, mu, lam, free, h, g=(0.0, -9.81, 0.0)):
 
 
 def implicit_step(mesh, model, u, v, mu, lam, free, h, iters=50, alpha=0.0, beta=0.0,
-                  g=(0.0, -9.81, 0.0)):
-    """O9+O10: map (f, K), assemble, PCG(iters), v += dv, u += h v."""
+                  g=(0.0, -9.81, 0.0), mass="lumped"):
+    """O9+O10: map (f, K), assemble, PCG(iters), v += dv, u += h v.
+    mass="consistent": the edge-relation Galerkin mass (density mesh.rho)."""
     f, K, en, inv = element_map(model, mesh.X, u, mesh.tets, mesh.Dminv, mesh.W, mu, lam,
                                 e=mesh.e, ne=mesh.ne)
-    A, b = implicit_assemble(mesh.row_ptr, mesh.head, K, mesh.mass, f, v, h, alpha, beta, g)
+    if mass == "consistent":
+        me = consistent_mass(mesh.e, mesh.W, mesh.rho, mesh.ne)
+        A, b = implicit_assemble_consistent(mesh.row_ptr, mesh.head, K, me, f, v, h, alpha, beta, g)
+    else:
+        A, b = implicit_assemble(mesh.row_ptr, mesh.head, K, mesh.mass, f, v, h, alpha, beta, g)
     dv, hist, not_spd = pcg(mesh.row_ptr, mesh.head, A, b, free, iters)
     u2, v2 = implicit_update(dv, h, u, v)
     return dict(u=u2, v=v2, f=f, K=K, A=A, b=b, dv=dv, rho=hist, energy=en,

@@ -509,6 +509,56 @@ void orc_implicit_assemble(int64_t nv, const int64_t* row_ptr, const int64_t* he
 }
 
 /* ------------------------------------------------------------------ */
+/* Consistent mass on the edge relation (SURVEY §8(c) "Mass matrix":      */
+/* "Consistent mass (on edges) is NEXT"; §8(f) 1).  The Galerkin mass of  */
+/* linear tets, M_ij = rho * integral(N_i N_j) = rho W (1 + delta_ij)/20   */
+/* (textbook; the paper names only a "mass" field), is   */
+/* a scalar times I_3 per edge row: mass_e[e[i][j]] += rho W (1+d_ij)/20,  */
+/* tets ascending, (i, j) row-major.                                       */
+/* ------------------------------------------------------------------ */
+void orc_consistent_mass(int64_t nt, const int64_t* e, const double* W, double rho, int64_t ne,
+                         double* mass_e) {
+    for (int64_t r = 0; r < ne; ++r) mass_e[r] = 0.0;
+    for (int64_t t = 0; t < nt; ++t)
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j)
+                mass_e[e[16 * t + 4 * i + j]] += rho * W[t] * (i == j ? 2.0 : 1.0) / 20.0;
+}
+
+/* O9 with the consistent mass: M is the edge-relation matrix mass_e[r] I_3,
+ * so M v and M g are edge query-loops like K v:
+ *   A_r = M_r + h (alpha M_r + beta K_r) + h^2 K_r,
+ *   b   = h (f + M g - (alpha M v + beta K v) - h K v). */
+void orc_implicit_assemble_consistent(int64_t nv, const int64_t* row_ptr, const int64_t* head,
+                                      const double* K, const double* mass_e, const double* f,
+                                      const double* vel, double h, double alpha, double beta,
+                                      const double* g, double* A, double* b) {
+    double* Kv = (double*)malloc(sizeof(double) * (size_t)(3 * nv > 0 ? 3 * nv : 1));
+    orc_edge_matvec(nv, row_ptr, head, K, vel, Kv);
+    for (int64_t v = 0; v < nv; ++v) {
+        double Mv[3] = {0.0, 0.0, 0.0}, msum = 0.0;
+        for (int64_t r = row_ptr[v]; r < row_ptr[v + 1]; ++r) {
+            for (int a = 0; a < 3; ++a) Mv[a] += mass_e[r] * vel[3 * head[r] + a];
+            msum += mass_e[r];
+        }
+        for (int a = 0; a < 3; ++a) {
+            double Dv = alpha * Mv[a] + beta * Kv[3 * v + a];
+            b[3 * v + a] = h * (f[3 * v + a] + msum * g[a] - Dv - h * Kv[3 * v + a]);
+        }
+    }
+    free(Kv);
+    for (int64_t v = 0; v < nv; ++v)
+        for (int64_t r = row_ptr[v]; r < row_ptr[v + 1]; ++r)
+            for (int a = 0; a < 3; ++a)
+                for (int c = 0; c < 3; ++c) {
+                    double Me = (a == c) ? mass_e[r] : 0.0;
+                    double Ke = K[9 * r + 3 * a + c];
+                    double De = alpha * Me + beta * Ke;
+                    A[9 * r + 3 * a + c] = Me + h * De + h * h * Ke;
+                }
+}
+
+/* ------------------------------------------------------------------ */
 /* O10  Jacobi-preconditioned CG (Saad Alg. 9.1), fixed N iters,  */
 /* Dirichlet projection by the free mask (subsets).           */
 /* Readings: alpha = 0 if p.q == 0, beta = 0 if rho == 0.    */

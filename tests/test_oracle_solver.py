@@ -134,3 +134,71 @@ def test_pcg_zero_rhs_is_noop():
     m, free, u, v, f, K, A, b = _system()
     x, hist, ns = oracle.pcg(m.row_ptr, m.head, A, np.zeros_like(b), free, 10)
     assert np.all(x == 0) and np.all(hist == 0)
+
+
+# ---------------------------------------------------------------- consistent mass
+def _mass_dense(m, me):
+    D = np.zeros((m.nv, m.nv))
+    for r in range(m.ne):
+        D[m.tail[r], m.head[r]] += me[r]
+    return D
+
+
+def test_consistent_mass_row_sums_are_the_lumped_mass():
+    """sum_j rho W (1 + d_ij)/20 = rho W / 4: each row of the Galerkin mass sums
+    to the lumped mass (orc_rest, an independent loop)."""
+    X, tets = M.kuhn6(3)
+    X = X + np.random.default_rng(3).uniform(-0.05, 0.05, X.shape) / 3 * (np.abs(X - 0.5) < 0.49)
+    m = oracle.Mesh(X, tets, rho=7.5)
+    me = oracle.consistent_mass(m.e, m.W, 7.5, m.ne)
+    rows = np.add.reduceat(me, m.row_ptr[:-1])
+    assert np.abs(rows - m.mass).max() <= 1e-14 * m.mass.max()
+    assert np.all(me > 0)
+    assert abs(me.sum() - 7.5 * 1.0) <= 1e-13               # rho * volume of the unit cube
+
+
+@pytest.mark.parametrize("a,c", [((0.0, 0.0, 0.0), 1.0), ((1.0, -2.0, 0.5), 0.3), ((0.7, 0.0, -1.1), -2.0)])
+def test_consistent_mass_integrates_quadratics_exactly(a, c):
+    """phi^T M phi = rho * integral over [0,1]^3 of phi^2 for every affine phi
+    (phi lies in the P1 space, M is its exact Gram matrix):
+    int (a.x + c)^2 = sum a_i^2/3 + 2 sum_{i<j} a_i a_j/4 + c sum a_i + c^2.
+    A wrong diagonal/off-diagonal split (e.g. rho W d_ij / 4) fails this."""
+    X, tets = M.kuhn6(3)
+    X = X + np.random.default_rng(4).uniform(-0.05, 0.05, X.shape) / 3 * (np.abs(X - 0.5) < 0.49)
+    m = oracle.Mesh(X, tets, rho=2.0)
+    me = oracle.consistent_mass(m.e, m.W, 2.0, m.ne)
+    a = np.asarray(a)
+    phi = m.X @ a + c
+    quad = np.sum(a * a) / 3 + 0.5 * (a[0] * a[1] + a[0] * a[2] + a[1] * a[2]) + c * a.sum() + c * c
+    got = np.sum(phi[m.tail] * me * phi[m.head])
+    assert abs(got - 2.0 * quad) <= 1e-13 * max(1.0, abs(quad))
+    # the lumped mass does NOT integrate a non-constant phi^2 exactly (the test discriminates)
+    if np.any(a != 0):
+        assert abs(np.sum(m.mass * phi * phi) - 2.0 * quad) > 1e-6
+
+
+def test_consistent_assembly_matches_dense_definition():
+    m, free, u, v, f, K, A, b = _system()
+    me = oracle.consistent_mass(m.e, m.W, 1e3, m.ne)
+    h, al, be = 1e-2, 0.1, 0.01
+    A2, b2 = oracle.implicit_assemble_consistent(m.row_ptr, m.head, K, me, f, v, h, al, be)
+    Kd = _dense(m, K)
+    Md = np.kron(_mass_dense(m, me), np.eye(3))
+    Ad = Md + h * (al * Md + be * Kd) + h * h * Kd
+    g = np.tile([0.0, -9.81, 0.0], m.nv)
+    bd = h * (f.ravel() + Md @ g - (al * Md + be * Kd) @ v.ravel() - h * Kd @ v.ravel())
+    assert np.abs(_dense(m, A2) - Ad).max() < 1e-14 * np.abs(Ad).max()
+    assert np.abs(b2.ravel() - bd).max() < 1e-12 * np.abs(bd).max()
+
+
+@pytest.mark.parametrize("model", ["stvk", "nh"])
+def test_implicit_free_fall_consistent_mass(model):
+    """(M + h^2 K) dv = h M g is solved by dv = h g for any SPD mass (K
+    annihilates translations): the consistent-mass step falls freely too."""
+    X, tets = M.kuhn6(2)
+    m = oracle.Mesh(X, tets)
+    mu, lam = S.materials(m.nt, 2e5, 0.3)
+    u = np.zeros_like(X)
+    v = np.zeros_like(X)
+    out = oracle.implicit_step(m, model, u, v, mu, lam, None, 1e-2, iters=80, mass="consistent")
+    assert np.abs(out["dv"] - np.array([0, -9.81e-2, 0])).max() < 1e-8

@@ -205,6 +205,19 @@ ebb_status ebb_tetmesh_build(ebb_ctx ctx, ebb_field tets_v, const char* edges_na
 ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double rho,
                             ebb_field Dminv, ebb_field W, ebb_field mass, ebb_stream s);
 
+/* Consistent (Galerkin) mass of linear tets on the edge relation (SURVEY
+ * §8(c) "Mass matrix" reading: consistent mass on edges is the NEXT option
+ * beside the lumped one; §8(f) 1; the paper names only a "mass" field,
+ * P:354-355): M_ij = rho W (1 + d_ij)/20 I_3, i.e.
+ * mass_e[e[i][j]] += rho W (1 + d_ij)/20 over every tet and (i, j).
+ * tets_e: the 4x4 key-field tets.e; W: F64 scalar on tets (ebb_tetmesh_rest);
+ * mass_e: F64 scalar on the edge relation (written; zeroed first).  Row sums
+ * equal the lumped mass.  fp64 atomic accumulation (like the lumped mass):
+ * equal to the oracle within round-off, not bitwise run-to-run.
+ * Stream-ordered. */
+ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field W, double rho,
+                                       ebb_field mass_e, ebb_stream s);
+
 /* ---- the element map (hot path a4-a8) --------------------------------- */
 #define EBB_STVK 0
 #define EBB_NH 1
@@ -290,12 +303,17 @@ typedef struct {
     ebb_field K;      /* edges 3x3 stiffness (read)                          */
     ebb_field A;      /* edges 3x3 system matrix (write; may equal K)        */
     ebb_field self;   /* verts -> edges self-loop key                        */
-    ebb_field mass, f, vel;   /* verts (read)                                */
+    ebb_field mass;   /* verts (lumped) or edges (consistent) scalar (read)  */
+    ebb_field f, vel; /* verts (read)                                        */
     ebb_field b;      /* verts vec3 rhs (write)                              */
     double h, alpha, beta;    /* step, Rayleigh damping D = alpha M + beta K */
     double g[3];              /* gravity                                     */
 } ebb_implicit_desc;
-/* a9: A = M + h D + h^2 K, b = h (f + M g - D v - h K v) (lumped M). */
+/* a9: A = M + h D + h^2 K, b = h (f + M g - D v - h K v).  `mass` is either
+ * a scalar field on verts (lumped M = diag(m_v) I_3) or a scalar field on
+ * the edge relation (consistent M_r = mass_e[r] I_3 per edge row, from
+ * ebb_tetmesh_consistent_mass; M v and M g are then edge query-loops),
+ * in the map dtype. */
 ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_stream s);
 
 typedef struct {

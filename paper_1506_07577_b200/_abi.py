@@ -108,6 +108,7 @@ SIGS = {
     "ebb_tetmesh_orient": (S, [ctx_t, u32, u32, C.POINTER(C.c_uint64)]),
     "ebb_tetmesh_build": (S, [ctx_t, u32, C.c_char_p, C.POINTER(TetmeshOut)]),
     "ebb_tetmesh_rest": (S, [ctx_t, u32, u32, C.c_double, u32, u32, u32, stream_t]),
+    "ebb_tetmesh_consistent_mass": (S, [ctx_t, u32, u32, C.c_double, u32, stream_t]),
     "ebb_map_tet_forces": (S, [ctx_t, C.POINTER(TetMapDesc), stream_t]),
     "ebb_map_plan_stats": (S, [ctx_t, u32, u32, C.POINTER(C.c_double)]),
     "ebb_comm_unique_id": (S, [C.c_char_p]),

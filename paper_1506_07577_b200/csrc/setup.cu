@@ -242,6 +242,17 @@ __global__ void k_rest(const uint32_t* __restrict__ tv, const double* __restrict
     for (int i = 0; i < 4; ++i) atomicAdd(&mass[v[i]], mv);
 }
 
+// consistent (Galerkin) mass of linear tets on the edge relation:
+// mass_e[e[i][j]] += rho W (1 + d_ij) / 20 (one fp64 red per (tet, i, j))
+__global__ void k_consistent_mass(const uint32_t* __restrict__ te, const double* __restrict__ W, uint64_t nt,
+                                  double rho, double* __restrict__ mass_e) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= nt * 16) return;
+    const uint64_t t = k >> 4;
+    const int i = (int)(k >> 2) & 3, j = (int)k & 3;
+    atomicAdd(&mass_e[te[k]], rho * W[t] * (i == j ? 2.0 : 1.0) / 20.0);
+}
+
 __global__ void k_first_tet(const uint32_t* __restrict__ tv, uint64_t nt, unsigned int* __restrict__ first) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i < nt * 4) atomicMin(&first[tv[i]], (unsigned int)(i >> 2));
@@ -476,6 +487,33 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
     EBB_CUDA(c, cudaMemcpyAsync(&hb, bad.p, 8, cudaMemcpyDeviceToHost, st));
     EBB_CUDA(c, cudaStreamSynchronize(st));
     if (hb) return fail(c, EBB_E_INVERTED, "%llu tets with W <= 0 (orient the mesh first)", hb);
+    return EBB_OK;
+}
+
+ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field W, double rho, ebb_field mass_e,
+                                       ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    if (!c) return EBB_E_ARG;
+    Field* E = get_field(c, tets_e);
+    Field* Wf = get_field(c, W);
+    Field* M = get_field(c, mass_e);
+    if (!E || !Wf || !M) return fail(c, EBB_E_ARG, "bad field handle");
+    if (E->dtype != EBB_KEY || E->comps() != 16 || E->layout != EBB_AOS)
+        return fail(c, EBB_E_TYPE, "'%s' must be the 4x4 key-field tets.e", E->name.c_str());
+    if (Wf->dtype != EBB_F64 || Wf->comps() != 1 || Wf->rel != E->rel)
+        return fail(c, EBB_E_TYPE, "W must be a scalar F64 field on tets");
+    if (M->dtype != EBB_F64 || M->comps() != 1 || M->rel != E->key_target)
+        return fail(c, EBB_E_TYPE, "mass_e must be a scalar F64 field on the edge relation tets.e points to");
+    if (M->ptr == Wf->ptr) return fail(c, EBB_E_PHASE, "mass_e aliases W");
+    const uint64_t nt = c->rels[E->rel].size, ne = c->rels[M->rel].size;
+    cudaStream_t st = (cudaStream_t)s;
+    EBB_CUDA(c, cudaMemsetAsync(M->ptr, 0, ne * 8, st));
+    if (nt) {
+        k_consistent_mass<<<grid_for(nt * 16, 256), 256, 0, st>>>((const uint32_t*)E->ptr, (const double*)Wf->ptr,
+                                                                  nt, rho, (double*)M->ptr);
+        c->launches++;
+    }
+    EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
 }
 

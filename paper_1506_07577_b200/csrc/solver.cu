@@ -1218,17 +1218,19 @@ __global__ void __launch_bounds__(256) k_cg_update(uint64_t nv, const R* pbuf0, 
 // row by row while the same rows accumulate (K v)_v, then
 // b_v = h (f + M g - D v - h K v).  LPV lanes per vertex (shuffle reduce);
 // A may alias K (every element is read, then written, by one thread).
-template <typename R, int LPV>
+template <typename R, int LPV, bool CONS>
 __global__ void __launch_bounds__(256) k_assemble_fused(uint64_t nv, const uint32_t* __restrict__ index,
                                                         const uint32_t* __restrict__ head, const R* K, R* A,
                                                         uint64_t ne, const R* __restrict__ mass,
                                                         const R* __restrict__ f, const R* __restrict__ vel,
                                                         R* __restrict__ b, R h, R alpha, R beta, R g0, R g1, R g2) {
+    // CONS: mass is the consistent edge mass (M_e = mass[e] I), M v and the
+    // row sum for M g are accumulated with K v; else the lumped mass[v]
     const unsigned lane = threadIdx.x % LPV;
     const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPV;
     const bool live = v < nv;   // every lane reaches the shuffles
-    const R m = live ? mass[v] : R(0);
-    R k0 = 0, k1 = 0, k2 = 0;
+    const R m = (!CONS && live) ? mass[v] : R(0);
+    R k0 = 0, k1 = 0, k2 = 0, m0 = 0, m1 = 0, m2 = 0, ms = 0;
     if (live) {
         for (uint32_t e = index[v] + lane; e < index[v + 1]; e += LPV) {
             const uint32_t hd = head[e];
@@ -1240,9 +1242,17 @@ __global__ void __launch_bounds__(256) k_assemble_fused(uint64_t nv, const uint3
             k0 += Ke[0] * w0 + Ke[1] * w1 + Ke[2] * w2;
             k1 += Ke[3] * w0 + Ke[4] * w1 + Ke[5] * w2;
             k2 += Ke[6] * w0 + Ke[7] * w1 + Ke[8] * w2;
+            R me = diag ? m : R(0);
+            if (CONS) {
+                me = mass[e];
+                m0 += me * w0;
+                m1 += me * w1;
+                m2 += me * w2;
+                ms += me;
+            }
 #pragma unroll
             for (int c = 0; c < 9; ++c) {
-                const R Me = (diag && (c == 0 || c == 4 || c == 8)) ? m : R(0);
+                const R Me = (c == 0 || c == 4 || c == 8) ? me : R(0);
                 const R De = alpha * Me + beta * Ke[c];
                 A[(uint64_t)c * ne + e] = Me + h * De + h * h * Ke[c];
             }
@@ -1253,15 +1263,22 @@ __global__ void __launch_bounds__(256) k_assemble_fused(uint64_t nv, const uint3
         k0 += __shfl_xor_sync(0xffffffffu, k0, o, LPV);
         k1 += __shfl_xor_sync(0xffffffffu, k1, o, LPV);
         k2 += __shfl_xor_sync(0xffffffffu, k2, o, LPV);
+        if (CONS) {
+            m0 += __shfl_xor_sync(0xffffffffu, m0, o, LPV);
+            m1 += __shfl_xor_sync(0xffffffffu, m1, o, LPV);
+            m2 += __shfl_xor_sync(0xffffffffu, m2, o, LPV);
+            ms += __shfl_xor_sync(0xffffffffu, ms, o, LPV);
+        }
     }
     if (live && lane == 0) {
-        const R kv[3] = {k0, k1, k2}, g[3] = {g0, g1, g2};
+        const R kv[3] = {k0, k1, k2}, mv[3] = {m0, m1, m2}, g[3] = {g0, g1, g2};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const uint64_t i = 3 * v + a;
-            const R Mv = m * vel[i];
+            const R Mv = CONS ? mv[a] : m * vel[i];
+            const R Mg = CONS ? ms * g[a] : m * g[a];
             const R Dv = alpha * Mv + beta * kv[a];
-            b[i] = h * (f[i] + m * g[a] - Dv - h * kv[a]);
+            b[i] = h * (f[i] + Mg - Dv - h * kv[a]);
         }
     }
 }
@@ -1784,8 +1801,10 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
     EBB_TRY(check_mat(c, K, d->edges, dt, "K"));
     EBB_TRY(check_mat(c, A, d->edges, dt, "A"));
     Field* M = get_field(c, d->mass);
-    if (!M || M->dtype != dt || M->comps() != 1 || M->rel != G.verts)
-        return fail(c, EBB_E_TYPE, "assemble: mass must be a scalar field of the map dtype on verts");
+    if (!M || M->dtype != dt || M->comps() != 1 || (M->rel != G.verts && M->rel != d->edges))
+        return fail(c, EBB_E_TYPE, "assemble: mass must be a scalar field of the map dtype on verts (lumped) or "
+                                   "on the edges (consistent)");
+    const bool cons = M->rel == d->edges;
     Field* F = get_field(c, d->f);
     Field* V = get_field(c, d->vel);
     Field* B = get_field(c, d->b);
@@ -1798,14 +1817,12 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
 #define EBB_ASM(R)                                                                                                  \
     do {                                                                                                            \
         KernelTimer kt(c, EBB_K_ASSEMBLE, s);                                                                       \
-        if (lpv == 16)                                                                                              \
-            k_assemble_fused<R, 16><<<grid_for(G.nv * 16, 256), 256, 0, s>>>(                                        \
-                G.nv, G.index, G.head, (const R*)K->ptr, (R*)A->ptr, G.ne, (const R*)M->ptr, (const R*)F->ptr,      \
-                (const R*)V->ptr, (R*)B->ptr, (R)d->h, (R)d->alpha, (R)d->beta, (R)d->g[0], (R)d->g[1], (R)d->g[2]); \
-        else                                                                                                        \
-            k_assemble_fused<R, 32><<<grid_for(G.nv * 32, 256), 256, 0, s>>>(                                        \
-                G.nv, G.index, G.head, (const R*)K->ptr, (R*)A->ptr, G.ne, (const R*)M->ptr, (const R*)F->ptr,      \
-                (const R*)V->ptr, (R*)B->ptr, (R)d->h, (R)d->alpha, (R)d->beta, (R)d->g[0], (R)d->g[1], (R)d->g[2]); \
+        auto kern = lpv == 16 ? (cons ? k_assemble_fused<R, 16, true> : k_assemble_fused<R, 16, false>)          \
+                              : (cons ? k_assemble_fused<R, 32, true> : k_assemble_fused<R, 32, false>);          \
+        kern<<<grid_for(G.nv * lpv, 256), 256, 0, s>>>(G.nv, G.index, G.head, (const R*)K->ptr, (R*)A->ptr, G.ne,    \
+                                                       (const R*)M->ptr, (const R*)F->ptr, (const R*)V->ptr,        \
+                                                       (R*)B->ptr, (R)d->h, (R)d->alpha, (R)d->beta, (R)d->g[0],    \
+                                                       (R)d->g[1], (R)d->g[2]);                                     \
     } while (0)
     if (dt == EBB_F64) EBB_ASM(double);
     else EBB_ASM(float);

@@ -29,7 +29,7 @@ class TetFEM:
     """
 
     def __init__(self, ctx: Context, X, tets, *, dtype="f64", mu=None, lam=None, rho=1e3, free=None,
-                 u=None, vel=None, renumber=True, orient=True, name="mesh"):
+                 u=None, vel=None, renumber=True, orient=True, mass="lumped", name="mesh"):
         self.ctx = ctx
         self.dtype = dtype
         X = np.ascontiguousarray(X, dtype=np.float64)
@@ -87,6 +87,19 @@ class TetFEM:
             self.Dminv.convert_from(Dm64)
             self.W.convert_from(W64)
             self.mass.convert_from(m64)
+        # mass="consistent": the Galerkin mass on the edge relation,
+        # used by assemble() in place of the lumped vertex mass
+        self.mass_kind = mass
+        if mass == "consistent":
+            me64 = self.edges.field("mass_e64", "f64")
+            ctx.check(L.ebb_tetmesh_consistent_mass(h, self.e.h, W64.h, float(rho), me64.h, None))
+            if dtype == "f64":
+                self.mass_e = me64
+            else:
+                self.mass_e = self.edges.field("mass_e", dtype)
+                self.mass_e.convert_from(me64)
+        elif mass != "lumped":
+            raise ValueError(f"mass must be 'lumped' or 'consistent', not {mass!r}")
         # per-step fields
         self.f = V.field("f", dtype, (3, 1))
         self.K = self.edges.field("K", dtype, (3, 3), "soa")
@@ -139,7 +152,8 @@ class TetFEM:
         """a9: A = M + hD + h^2 K (in place over K), b = h(f + Mg - Dv - hKv)."""
         d = A.ImplicitDesc()
         d.edges, d.K, d.A, d.self = self.edges.h, self.K.h, self.K.h, self.self_e.h
-        d.mass, d.f, d.vel, d.b = self.mass.h, self.f.h, self.vel.h, self.b.h
+        d.mass = self.mass_e.h if self.mass_kind == "consistent" else self.mass.h
+        d.f, d.vel, d.b = self.f.h, self.vel.h, self.b.h
         d.h, d.alpha, d.beta = h, alpha, beta
         d.g[0], d.g[1], d.g[2] = g
         self.ctx.check(self.ctx.L.ebb_implicit_assemble(self.ctx.h, C.byref(d), _stream(stream)))

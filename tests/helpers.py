@@ -45,10 +45,10 @@ def oracle_renumbered(case: Case):
     return m, new_of_old, tet_src, order
 
 
-def gpu_fem(ctx, case: Case, dtype="f64", renumber=True, name="mesh"):
+def gpu_fem(ctx, case: Case, dtype="f64", renumber=True, name="mesh", mass="lumped"):
     from paper_1506_07577_b200.tetfem import TetFEM
     return TetFEM(ctx, case.X, case.tets, dtype=dtype, mu=case.mu, lam=case.lam, rho=case.rho, free=case.free,
-                  u=case.u, vel=case.vel, renumber=renumber, name=name)
+                  u=case.u, vel=case.vel, renumber=renumber, name=name, mass=mass)
 
 
 def rel_l2(a, b):

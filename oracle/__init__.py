@@ -60,6 +60,7 @@ def lib():
             "orc_explicit_update": (None, [I, P, P, P, P, D, P, P]),
             "orc_implicit_assemble": (None, [I, P, P, P, P, P, P, D, D, D, P, P, P]),
             "orc_consistent_mass": (None, [I, P, P, D, I, P]),
+            "orc_newton_rhs": (None, [I, P, P, P, P, P, P, P, D, D, D, P, P]),
             "orc_implicit_assemble_consistent": (None, [I, P, P, P, P, P, P, D, D, D, P, P, P]),
             "orc_pcg": (C.c_int, [I, P, P, P, P, P, C.c_int, P, P]),
             "orc_implicit_update": (None, [I, P, D, P, P]),
@@ -292,6 +293,47 @@ def explicit_step(mesh, model, u, v, mu, lam, free, h, g=(0.0, -9.81, 0.0)):
     f, _, en, inv = element_map(model, mesh.X, u, mesh.tets, mesh.Dminv, mesh.W, mu, lam, want_K=False)
     u2, v2 = explicit_update(f, mesh.mass, free, np.asarray(g), h, u, v)
     return u2, v2, f, en
+
+
+def lumped_as_edges(mesh):
+    """The lumped vertex mass as an edge-row mass (self rows only)."""
+    me = np.zeros(mesh.ne)
+    me[mesh.tail == mesh.head] = mesh.mass[mesh.tail[mesh.tail == mesh.head]]
+    return me
+
+
+def newton_rhs(row_ptr, head, K, mass_e, f, w, v0, h, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0)):
+    """b = h (f + M g - D w) + M (v_n - w): the Newton right-hand side."""
+    nv = row_ptr.shape[0] - 1
+    b = np.empty((nv, 3))
+    lib().orc_newton_rhs(nv, _p(_i64(row_ptr)), _p(_i64(head)), _p(_f64(K)), _p(_f64(mass_e)), _p(_f64(f)),
+                         _p(_f64(w)), _p(_f64(v0)), h, alpha, beta, _p(_f64(np.asarray(g))), _p(b))
+    return b
+
+
+def newton_step(mesh, model, u, v, mu, lam, free, h, iters=50, newton=2, alpha=0.0, beta=0.0,
+                g=(0.0, -9.81, 0.0), mass="lumped"):
+    """Backward Euler with `newton` Newton iterations: the first is the
+    one-linearisation step (implicit_step), each later one maps f, K at
+    x_k = u_n + h w_k, solves (M + hD + h^2 K) dw = b (newton_rhs) with
+    `iters` PCG iterations, then w += dw, u += h dw."""
+    out = implicit_step(mesh, model, u, v, mu, lam, free, h, iters, alpha, beta, g, mass)
+    me = consistent_mass(mesh.e, mesh.W, mesh.rho, mesh.ne) if mass == "consistent" else lumped_as_edges(mesh)
+    x, w = out["u"], out["v"]
+    v0 = _f64(v)
+    for _ in range(newton - 1):
+        f, K, en, inv = element_map(model, mesh.X, x, mesh.tets, mesh.Dminv, mesh.W, mu, lam,
+                                    e=mesh.e, ne=mesh.ne)
+        if mass == "consistent":
+            A, _b = implicit_assemble_consistent(mesh.row_ptr, mesh.head, K, me, f, w, h, alpha, beta, g)
+        else:
+            A, _b = implicit_assemble(mesh.row_ptr, mesh.head, K, mesh.mass, f, w, h, alpha, beta, g)
+        b = newton_rhs(mesh.row_ptr, mesh.head, K, me, f, w, v0, h, alpha, beta, g)
+        dw, hist, ns = pcg(mesh.row_ptr, mesh.head, A, b, free, iters)
+        w = w + dw
+        x = x + h * dw
+        out = dict(out, u=x, v=w, f=f, K=K, A=A, b=b, dv=dw, rho=hist, not_spd=ns or out["not_spd"])
+    return out
 
 
 def implicit_step(mesh, model, u, v, mu, lam, free, h, iters=50, alpha=0.0, beta=0.0,

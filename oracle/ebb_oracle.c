@@ -559,6 +559,39 @@ void orc_implicit_assemble_consistent(int64_t nv, const int64_t* row_ptr, const 
 }
 
 /* ------------------------------------------------------------------ */
+/* Newton iterations of the backward-Euler step (SURVEY §8(f) 1 "multiple */
+/* Newton iterations"; the paper names only "implicit backward Euler",    */
+/* P:941).  Unknown x = u_{n+1}, velocity w = (x - u_n)/h; residual        */
+/*   G(x) = M (w - v_n)/h - f(x) - M g + D w,                              */
+/* Jacobian dG/dx = (M + h D + h^2 K(x)) / h^2.  The first Newton step from */
+/* x = u_n is exactly the one-linearisation step O9; the     */
+/* later ones solve (M + h D + h^2 K(x_k)) dw = -h G(x_k), i.e.             */
+/*   b = h (f(x_k) + M g - D w_k) + M (v_n - w_k),                         */
+/* then w += dw, x += h dw.  M is given per edge row (mass_e[r] I_3; a      */
+/* lumped mass is the self rows only), D = alpha M + beta K(x_k).           */
+/* ------------------------------------------------------------------ */
+void orc_newton_rhs(int64_t nv, const int64_t* row_ptr, const int64_t* head, const double* K,
+                    const double* mass_e, const double* f, const double* w, const double* v0, double h,
+                    double alpha, double beta, const double* g, double* b) {
+    for (int64_t v = 0; v < nv; ++v) {
+        double Kw[3] = {0.0, 0.0, 0.0}, Mw[3] = {0.0, 0.0, 0.0}, Mv0[3] = {0.0, 0.0, 0.0}, msum = 0.0;
+        for (int64_t r = row_ptr[v]; r < row_ptr[v + 1]; ++r) {
+            const int64_t hd = head[r];
+            for (int a = 0; a < 3; ++a) {
+                for (int c = 0; c < 3; ++c) Kw[a] += K[9 * r + 3 * a + c] * w[3 * hd + c];
+                Mw[a] += mass_e[r] * w[3 * hd + a];
+                Mv0[a] += mass_e[r] * v0[3 * hd + a];
+            }
+            msum += mass_e[r];
+        }
+        for (int a = 0; a < 3; ++a) {
+            double Dw = alpha * Mw[a] + beta * Kw[a];
+            b[3 * v + a] = h * (f[3 * v + a] + msum * g[a] - Dw) + (Mv0[a] - Mw[a]);
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ */
 /* O10  Jacobi-preconditioned CG (Saad Alg. 9.1), fixed N iters,  */
 /* Dirichlet projection by the free mask (subsets).           */
 /* Readings: alpha = 0 if p.q == 0, beta = 0 if rho == 0.    */

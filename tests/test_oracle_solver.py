@@ -202,3 +202,64 @@ def test_implicit_free_fall_consistent_mass(model):
     v = np.zeros_like(X)
     out = oracle.implicit_step(m, model, u, v, mu, lam, None, 1e-2, iters=80, mass="consistent")
     assert np.abs(out["dv"] - np.array([0, -9.81e-2, 0])).max() < 1e-8
+
+
+# ---------------------------------------------------------------- Newton iterations
+def _newton_case(mass):
+    X, tets = M.kuhn6(2)
+    m = oracle.Mesh(X, tets)
+    free = S.fixed_mask(X, 2)
+    u = 2 * S.stretch_noise_u(X, 2, 5, free=free)          # large strain: visibly nonlinear
+    v = np.random.default_rng(1).uniform(-0.5, 0.5, X.shape) * free[:, None]
+    mu, lam = S.materials(m.nt, 2e5, 0.3)
+    me = oracle.consistent_mass(m.e, m.W, m.rho, m.ne) if mass == "consistent" else oracle.lumped_as_edges(m)
+    return m, free, u, v, mu, lam, me
+
+
+def _be_residual(m, me, mu, lam, free, u0, v0, x, w, h, al, g=(0.0, -9.81, 0.0)):
+    """Backward-Euler residual on the free DOFs, written from its definition
+    with a dense mass: G = M (w - v_n)/h - f(x) - M g + alpha M w."""
+    f, K, en, inv = oracle.element_map("nh", m.X, x, m.tets, m.Dminv, m.W, mu, lam, e=m.e, ne=m.ne)
+    Md = _mass_dense(m, me)
+    r = Md @ ((w - v0) / h) - f - Md @ np.tile(g, (m.nv, 1)) + al * (Md @ w)
+    assert np.allclose(x, u0 + h * w, rtol=0, atol=1e-12)  # x = u_n + h w throughout
+    return np.linalg.norm(r[free == 1])
+
+
+@pytest.mark.parametrize("mass", ["lumped", "consistent"])
+def test_newton_converges_quadratically(mass):
+    """With converged linear solves (40 PCG iterations, r.z at 1e-12 of its
+    start on these 81 DOFs), Newton's residual falls
+    quadratically: G_{k+1} / G_k^2 stays constant.  A wrong right-hand side or
+    Jacobian term would stall it (linear convergence or a wrong fixed point)."""
+    m, free, u, v, mu, lam, me = _newton_case(mass)
+    h, al = 0.05, 0.1
+    G = []
+    for k in range(1, 5):
+        out = oracle.newton_step(m, "nh", u, v, mu, lam, free, h, iters=40, newton=k, alpha=al, mass=mass)
+        assert not out["not_spd"]
+        G.append(_be_residual(m, me, mu, lam, free, u, v, out["u"], out["v"], h, al))
+    q = [G[k + 1] / G[k] ** 2 for k in range(3)]   # measured 4e-6..7e-6 (lumped)
+    assert G[3] < 1e-8 * G[0]
+    assert max(q) / min(q) < 10.0, (G, q)
+
+
+def test_newton_one_iteration_is_the_linearised_step():
+    m, free, u, v, mu, lam, me = _newton_case("lumped")
+    a = oracle.newton_step(m, "stvk", u, v, mu, lam, free, 1e-2, iters=20, newton=1)
+    b = oracle.implicit_step(m, "stvk", u, v, mu, lam, free, 1e-2, iters=20)
+    assert np.array_equal(a["u"], b["u"]) and np.array_equal(a["v"], b["v"])
+
+
+@pytest.mark.parametrize("mass", ["lumped", "consistent"])
+def test_newton_free_fall(mass):
+    """No constraints, at rest: every Newton iterate is the exact free fall
+    (K annihilates translations): v = h g, u = h^2 g."""
+    X, tets = M.kuhn6(2)
+    m = oracle.Mesh(X, tets)
+    mu, lam = S.materials(m.nt, 2e5, 0.3)
+    z = np.zeros_like(X)
+    out = oracle.newton_step(m, "nh", z, z, mu, lam, None, 1e-2, iters=80, newton=3, mass=mass)
+    g = np.array([0.0, -9.81, 0.0])
+    assert np.abs(out["v"] - 1e-2 * g).max() < 1e-8
+    assert np.abs(out["u"] - 1e-4 * g).max() < 1e-10

@@ -308,7 +308,17 @@ typedef struct {
     ebb_field b;      /* verts vec3 rhs (write)                              */
     double h, alpha, beta;    /* step, Rayleigh damping D = alpha M + beta K */
     double g[3];              /* gravity                                     */
+    int32_t rhs_form;         /* EBB_RHS_LINEARISED (0): b = h (f + M g - D v
+                                 - h K v), v = vel, the one-linearisation step
+                                 (O9).  EBB_RHS_NEWTON (1): a later Newton
+                                 iteration of the same backward-Euler step,
+                                 vel = the velocity iterate w (u = u_n + h w),
+                                 vel0 = v_n: b = h (f + M g - D w) + M (v_n - w);
+                                 A is the same.  SURVEY §8(f) 1.             */
+    ebb_field vel0;           /* verts vec3 v_n (EBB_RHS_NEWTON only)          */
 } ebb_implicit_desc;
+#define EBB_RHS_LINEARISED 0
+#define EBB_RHS_NEWTON 1
 /* a9: A = M + h D + h^2 K, b = h (f + M g - D v - h K v).  `mass` is either
  * a scalar field on verts (lumped M = diag(m_v) I_3) or a scalar field on
  * the edge relation (consistent M_r = mass_e[r] I_3 per edge row, from
@@ -419,6 +429,9 @@ typedef struct {
 ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stream s);
 /* implicit state update: vel += dv; u += h vel. */
 ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
+/* Newton iteration update (after an EBB_RHS_NEWTON solve): vel += dv;
+ * u += h dv (keeps u = u_n + h vel). */
+ebb_status ebb_newton_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
 
 /* ---- multi-GPU partition ----------------------------- */
 /* owner_t(t) = floor(t P / T); owner_v(v) = owner_t(min tet containing v),

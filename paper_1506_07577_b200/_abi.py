@@ -52,7 +52,10 @@ class TetMapDesc(C.Structure):
 class ImplicitDesc(C.Structure):
     _fields_ = [("edges", u32), ("K", u32), ("A", u32), ("self", u32), ("mass", u32), ("f", u32), ("vel", u32),
                 ("b", u32), ("h", C.c_double), ("alpha", C.c_double), ("beta", C.c_double),
-                ("g", C.c_double * 3)]
+                ("g", C.c_double * 3), ("rhs_form", C.c_int32), ("vel0", u32)]
+
+
+RHS_LINEARISED, RHS_NEWTON = 0, 1
 
 
 class CG(C.Structure):
@@ -125,6 +128,7 @@ SIGS = {
     "ebb_cg_step": (S, [ctx_t, C.POINTER(CG), C.c_int32, stream_t]),
     "ebb_explicit_update": (S, [ctx_t, C.POINTER(ExplicitDesc), stream_t]),
     "ebb_implicit_update": (S, [ctx_t, u32, C.c_double, u32, u32, stream_t]),
+    "ebb_newton_update": (S, [ctx_t, u32, C.c_double, u32, u32, stream_t]),
     "ebb_partition": (S, [ctx_t, u32, C.c_int32, u32, u32]),
     "ebb_cg_phase": (S, [ctx_t, C.POINTER(CG), C.c_int32, stream_t]),
     "ebb_rows_gather": (S, [ctx_t, u32, u32, u32, stream_t]),

@@ -1218,19 +1218,22 @@ __global__ void __launch_bounds__(256) k_cg_update(uint64_t nv, const R* pbuf0, 
 // row by row while the same rows accumulate (K v)_v, then
 // b_v = h (f + M g - D v - h K v).  LPV lanes per vertex (shuffle reduce);
 // A may alias K (every element is read, then written, by one thread).
-template <typename R, int LPV, bool CONS>
+template <typename R, int LPV, bool CONS, bool NEWTON>
 __global__ void __launch_bounds__(256) k_assemble_fused(uint64_t nv, const uint32_t* __restrict__ index,
                                                         const uint32_t* __restrict__ head, const R* K, R* A,
                                                         uint64_t ne, const R* __restrict__ mass,
                                                         const R* __restrict__ f, const R* __restrict__ vel,
-                                                        R* __restrict__ b, R h, R alpha, R beta, R g0, R g1, R g2) {
+                                                        const R* __restrict__ vel0, R* __restrict__ b, R h, R alpha,
+                                                        R beta, R g0, R g1, R g2) {
     // CONS: mass is the consistent edge mass (M_e = mass[e] I), M v and the
-    // row sum for M g are accumulated with K v; else the lumped mass[v]
+    // row sum for M g are accumulated with K v; else the lumped mass[v].
+    // NEWTON: vel = the velocity iterate w, vel0 = v_n, and
+    // b = h (f + M g - D w) + M (v_n - w) (no -h^2 K v term)
     const unsigned lane = threadIdx.x % LPV;
     const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPV;
     const bool live = v < nv;   // every lane reaches the shuffles
     const R m = (!CONS && live) ? mass[v] : R(0);
-    R k0 = 0, k1 = 0, k2 = 0, m0 = 0, m1 = 0, m2 = 0, ms = 0;
+    R k0 = 0, k1 = 0, k2 = 0, m0 = 0, m1 = 0, m2 = 0, ms = 0, n0 = 0, n1 = 0, n2 = 0;
     if (live) {
         for (uint32_t e = index[v] + lane; e < index[v + 1]; e += LPV) {
             const uint32_t hd = head[e];
@@ -1249,6 +1252,11 @@ __global__ void __launch_bounds__(256) k_assemble_fused(uint64_t nv, const uint3
                 m1 += me * w1;
                 m2 += me * w2;
                 ms += me;
+                if (NEWTON) {
+                    n0 += me * vel0[3ull * hd];
+                    n1 += me * vel0[3ull * hd + 1];
+                    n2 += me * vel0[3ull * hd + 2];
+                }
             }
 #pragma unroll
             for (int c = 0; c < 9; ++c) {
@@ -1268,17 +1276,27 @@ __global__ void __launch_bounds__(256) k_assemble_fused(uint64_t nv, const uint3
             m1 += __shfl_xor_sync(0xffffffffu, m1, o, LPV);
             m2 += __shfl_xor_sync(0xffffffffu, m2, o, LPV);
             ms += __shfl_xor_sync(0xffffffffu, ms, o, LPV);
+            if (NEWTON) {
+                n0 += __shfl_xor_sync(0xffffffffu, n0, o, LPV);
+                n1 += __shfl_xor_sync(0xffffffffu, n1, o, LPV);
+                n2 += __shfl_xor_sync(0xffffffffu, n2, o, LPV);
+            }
         }
     }
     if (live && lane == 0) {
-        const R kv[3] = {k0, k1, k2}, mv[3] = {m0, m1, m2}, g[3] = {g0, g1, g2};
+        const R kv[3] = {k0, k1, k2}, mv[3] = {m0, m1, m2}, nv0[3] = {n0, n1, n2}, g[3] = {g0, g1, g2};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const uint64_t i = 3 * v + a;
             const R Mv = CONS ? mv[a] : m * vel[i];
             const R Mg = CONS ? ms * g[a] : m * g[a];
             const R Dv = alpha * Mv + beta * kv[a];
-            b[i] = h * (f[i] + Mg - Dv - h * kv[a]);
+            if (NEWTON) {
+                const R Mv0 = CONS ? nv0[a] : m * vel0[i];
+                b[i] = h * (f[i] + Mg - Dv) + (Mv0 - Mv);
+            } else {
+                b[i] = h * (f[i] + Mg - Dv - h * kv[a]);
+            }
         }
     }
 }
@@ -1298,13 +1316,16 @@ __global__ void k_explicit(uint64_t nv, const R* __restrict__ f, const R* __rest
     vel[i] += a * h;
 }
 
-template <typename R>
+// NEWTON = false: vel += dv, u += h vel (the one-linearisation step);
+// NEWTON = true:  vel += dv, u += h dv (a later Newton iteration: u = u_n + h vel)
+template <typename R, bool NEWTON>
 __global__ void k_implicit_update(uint64_t ndof, const R* __restrict__ dv, R h, R* __restrict__ u, R* __restrict__ vel) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= ndof) return;
-    R v = vel[i] + dv[i];
+    const R d = dv[i];
+    R v = vel[i] + d;
     vel[i] = v;
-    u[i] += h * v;
+    u[i] += h * (NEWTON ? d : v);
 }
 
 // generic global reduction over all components of a field
@@ -1812,17 +1833,31 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
     EBB_TRY(check_vec(c, V, G.verts, dt, "vel"));
     EBB_TRY(check_vec(c, B, G.verts, dt, "b"));
     if (B->ptr == F->ptr || B->ptr == V->ptr) return fail(c, EBB_E_PHASE, "assemble: b aliases a read field");
+    if (d->rhs_form != EBB_RHS_LINEARISED && d->rhs_form != EBB_RHS_NEWTON)
+        return fail(c, EBB_E_ARG, "assemble: unknown rhs_form %d", d->rhs_form);
+    const bool newton = d->rhs_form == EBB_RHS_NEWTON;
+    Field* V0 = nullptr;
+    if (newton) {
+        V0 = get_field(c, d->vel0);
+        EBB_TRY(check_vec(c, V0, G.verts, dt, "vel0"));
+        if (B->ptr == V0->ptr) return fail(c, EBB_E_PHASE, "assemble: b aliases vel0");
+    }
     cudaStream_t s = (cudaStream_t)stream;
     const int lpv = G.max_group <= 16 ? 16 : 32;
 #define EBB_ASM(R)                                                                                                  \
     do {                                                                                                            \
         KernelTimer kt(c, EBB_K_ASSEMBLE, s);                                                                       \
-        auto kern = lpv == 16 ? (cons ? k_assemble_fused<R, 16, true> : k_assemble_fused<R, 16, false>)          \
-                              : (cons ? k_assemble_fused<R, 32, true> : k_assemble_fused<R, 32, false>);          \
+        decltype(&k_assemble_fused<R, 16, false, false>) kern;                                                     \
+        if (newton)                                                                                                 \
+            kern = lpv == 16 ? (cons ? k_assemble_fused<R, 16, true, true> : k_assemble_fused<R, 16, false, true>)   \
+                             : (cons ? k_assemble_fused<R, 32, true, true> : k_assemble_fused<R, 32, false, true>);  \
+        else                                                                                                        \
+            kern = lpv == 16 ? (cons ? k_assemble_fused<R, 16, true, false> : k_assemble_fused<R, 16, false, false>) \
+                             : (cons ? k_assemble_fused<R, 32, true, false> : k_assemble_fused<R, 32, false, false>);\
         kern<<<grid_for(G.nv * lpv, 256), 256, 0, s>>>(G.nv, G.index, G.head, (const R*)K->ptr, (R*)A->ptr, G.ne,    \
                                                        (const R*)M->ptr, (const R*)F->ptr, (const R*)V->ptr,        \
-                                                       (R*)B->ptr, (R)d->h, (R)d->alpha, (R)d->beta, (R)d->g[0],    \
-                                                       (R)d->g[1], (R)d->g[2]);                                     \
+                                                       V0 ? (const R*)V0->ptr : nullptr, (R*)B->ptr, (R)d->h,       \
+                                                       (R)d->alpha, (R)d->beta, (R)d->g[0], (R)d->g[1], (R)d->g[2]);\
     } while (0)
     if (dt == EBB_F64) EBB_ASM(double);
     else EBB_ASM(float);
@@ -1984,7 +2019,9 @@ ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stre
     return EBB_OK;
 }
 
-ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream stream) {
+namespace {
+ebb_status implicit_update_impl(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream stream,
+                                bool newton) {
     Ctx* c = (Ctx*)ctx;
     if (!c) return EBB_E_ARG;
     Field* U = get_field(c, u);
@@ -1996,14 +2033,26 @@ ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u,
     uint64_t ndof = 3 * c->rels[U->rel].size;
     cudaStream_t s = (cudaStream_t)stream;
     c->launches++;
-    if (dt == EBB_F64)
-        k_implicit_update<double><<<grid_for(ndof, 256), 256, 0, s>>>(ndof, (const double*)c->fields[dv].ptr, h,
-                                                                      (double*)U->ptr, (double*)c->fields[vel].ptr);
-    else
-        k_implicit_update<float><<<grid_for(ndof, 256), 256, 0, s>>>(ndof, (const float*)c->fields[dv].ptr, (float)h,
-                                                                     (float*)U->ptr, (float*)c->fields[vel].ptr);
+    if (dt == EBB_F64) {
+        auto k = newton ? k_implicit_update<double, true> : k_implicit_update<double, false>;
+        k<<<grid_for(ndof, 256), 256, 0, s>>>(ndof, (const double*)c->fields[dv].ptr, h, (double*)U->ptr,
+                                              (double*)c->fields[vel].ptr);
+    } else {
+        auto k = newton ? k_implicit_update<float, true> : k_implicit_update<float, false>;
+        k<<<grid_for(ndof, 256), 256, 0, s>>>(ndof, (const float*)c->fields[dv].ptr, (float)h, (float*)U->ptr,
+                                              (float*)c->fields[vel].ptr);
+    }
     EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
+}
+}  // namespace
+
+ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream stream) {
+    return implicit_update_impl(ctx, dv, h, u, vel, stream, false);
+}
+
+ebb_status ebb_newton_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream stream) {
+    return implicit_update_impl(ctx, dv, h, u, vel, stream, true);
 }
 
 }  // extern "C"

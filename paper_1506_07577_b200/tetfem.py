@@ -148,14 +148,17 @@ class TetFEM:
                                                       self.free.h if mask else A.NONE,
                                                       pq.h if pq is not None else A.NONE, _stream(stream)))
 
-    def assemble(self, h, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0), stream=None):
-        """a9: A = M + hD + h^2 K (in place over K), b = h(f + Mg - Dv - hKv)."""
+    def assemble(self, h, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0), stream=None, vel0=None):
+        """a9: A = M + hD + h^2 K (in place over K), b = h(f + Mg - Dv - hKv);
+        with vel0 (= v_n) the Newton form b = h(f + Mg - Dw) + M(v_n - w), w = vel."""
         d = A.ImplicitDesc()
         d.edges, d.K, d.A, d.self = self.edges.h, self.K.h, self.K.h, self.self_e.h
         d.mass = self.mass_e.h if self.mass_kind == "consistent" else self.mass.h
         d.f, d.vel, d.b = self.f.h, self.vel.h, self.b.h
         d.h, d.alpha, d.beta = h, alpha, beta
         d.g[0], d.g[1], d.g[2] = g
+        d.rhs_form = A.RHS_NEWTON if vel0 is not None else A.RHS_LINEARISED
+        d.vel0 = vel0.h if vel0 is not None else A.NONE
         self.ctx.check(self.ctx.L.ebb_implicit_assemble(self.ctx.h, C.byref(d), _stream(stream)))
 
     def cg_init(self, stream=None, variant=None, tol=None):
@@ -196,14 +199,29 @@ class TetFEM:
         self.ctx.check(self.ctx.L.ebb_global_get(self.ctx.h, self.cg.rho, C.byref(out)))
         return out.value
 
-    def implicit_step(self, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0), stream=None):
-        """O9 + O10 on the device: map(f, K) -> assemble -> PCG(iters) -> v += dv, u += h v."""
+    def implicit_step(self, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0), stream=None,
+                      newton=1):
+        """O9 + O10 on the device: map(f, K) -> assemble -> PCG(iters) -> v += dv, u += h v.
+        newton > 1: that step is Newton's first iteration; each later one maps
+        at u = u_n + h w, assembles the Newton rhs, solves, w += dw, u += h dw
+        (SURVEY §8(f) 1)."""
+        if newton > 1:
+            if getattr(self, "vel0", None) is None:
+                self.vel0 = self.verts.field("vel_n", self.dtype, (3, 1))
+            self.vel0.copy_from(self.vel, stream=stream)
         self.map_forces(model, True, True, stream=stream)
         self.assemble(h, alpha, beta, g, stream=stream)
         self.cg_init(stream=stream)
         self.cg_step(iters, stream=stream)
         self.ctx.check(self.ctx.L.ebb_implicit_update(self.ctx.h, self.dv.h, float(h), self.u.h, self.vel.h,
                                                       _stream(stream)))
+        for _ in range(newton - 1):
+            self.map_forces(model, True, True, stream=stream)
+            self.assemble(h, alpha, beta, g, stream=stream, vel0=self.vel0)
+            self.cg_init(stream=stream)
+            self.cg_step(iters, stream=stream)
+            self.ctx.check(self.ctx.L.ebb_newton_update(self.ctx.h, self.dv.h, float(h), self.u.h, self.vel.h,
+                                                        _stream(stream)))
 
     def explicit_step(self, model="stvk", h=1e-4, g=(0.0, -9.81, 0.0), stream=None):
         """O8: force-only map then the Fig. 2 update."""

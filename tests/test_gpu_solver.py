@@ -291,3 +291,25 @@ def test_implicit_step_consistent_mass(ctx, model, variant, monkeypatch):
     assert rel_l2(fem.dv.read(), out["dv"]) <= 1e-8
     assert rel_l2(fem.u.read(), out["u"]) <= 1e-8
     assert ctx.error_counts(reset=True)["not_spd"] == 0
+
+
+@pytest.mark.parametrize("mass,model,newton", [("lumped", "nh", 3), ("consistent", "nh", 2), ("lumped", "stvk", 2)])
+def test_implicit_newton_iterations(ctx, mass, model, newton, monkeypatch):
+    """SURVEY §8(f) 1, several Newton iterations per backward-Euler step: the
+    first is the one-linearisation step, each later one maps at
+    u = u_n + h w, assembles b = h(f + Mg - Dw) + M(v_n - w) and updates
+    w += dw, u += h dw -- against oracle.newton_step (bar 1e-8 on u, v; the
+    later increments are small residual corrections, compared at 1e-6)."""
+    monkeypatch.setenv("EBB_CG_VARIANT", "1")
+    case = Case(n=6, model=model, vel_amp=0.05)
+    h, iters, al, be = 1e-2, 50, 0.05, 0.002
+    fem = gpu_fem(ctx, case, name=f"newt{mass}{model}{newton}", mass=mass)
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    out = oracle.newton_step(m, model, case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                             case.free[order], h, iters=iters, newton=newton, alpha=al, beta=be, mass=mass)
+    fem.implicit_step(model, h=h, iters=iters, alpha=al, beta=be, newton=newton)
+    assert rel_l2(fem.u.read(), out["u"]) <= 1e-8
+    assert rel_l2(fem.vel.read(), out["v"]) <= 1e-8
+    assert rel_l2(fem.b.read(), out["b"]) <= 1e-6
+    assert rel_l2(fem.dv.read(), out["dv"]) <= 1e-6
+    assert ctx.error_counts(reset=True)["not_spd"] == 0

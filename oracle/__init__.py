@@ -61,6 +61,10 @@ def lib():
             "orc_implicit_assemble": (None, [I, P, P, P, P, P, P, D, D, D, P, P, P]),
             "orc_consistent_mass": (None, [I, P, P, D, I, P]),
             "orc_newton_rhs": (None, [I, P, P, P, P, P, P, P, D, D, D, P, P]),
+            "orc_spring_init_len": (None, [I, P, P, P, P]),
+            "orc_spring_forces": (None, [I, P, P, P, P, D, P]),
+            "orc_spring_apply": (None, [I, P, D, P, P, P]),
+            "orc_kinetic_energy": (D, [I, P, P]),
             "orc_implicit_assemble_consistent": (None, [I, P, P, P, P, P, P, D, D, D, P, P, P]),
             "orc_pcg": (C.c_int, [I, P, P, P, P, P, C.c_int, P, P]),
             "orc_implicit_update": (None, [I, P, D, P, P]),
@@ -351,3 +355,41 @@ def implicit_step(mesh, model, u, v, mu, lam, free, h, iters=50, alpha=0.0, beta
     u2, v2 = implicit_update(dv, h, u, v)
     return dict(u=u2, v=v2, f=f, K=K, A=A, b=b, dv=dv, rho=hist, energy=en,
                 inverted=inv, not_spd=not_spd)
+
+
+# ---------------------------------------------------------------- Fig. 2 spring-mass
+def spring_init_len(tail, head, pos):
+    """initLen (P:364-367): rest_len[e] = |pos[head] - pos[tail]|."""
+    L = np.empty(tail.shape[0])
+    lib().orc_spring_init_len(tail.shape[0], _p(_i64(tail)), _p(_i64(head)), _p(_f64(pos)), _p(L))
+    return L
+
+
+def spring_forces(row_ptr, head, q, rest_len, K, force=None):
+    """computeInternalForces: force += K sum (rest_len dir - dq)."""
+    nv = row_ptr.shape[0] - 1
+    f = np.zeros((nv, 3)) if force is None else _f64(force).copy()
+    lib().orc_spring_forces(nv, _p(_i64(row_ptr)), _p(_i64(head)), _p(_f64(q)), _p(_f64(rest_len)), K, _p(f))
+    return f
+
+
+def spring_apply(mass, dt, q, qd, force):
+    """applyForces (P:377-382): returns (q, qd, force = 0)."""
+    q, qd, f = _f64(q).copy(), _f64(qd).copy(), _f64(force).copy()
+    lib().orc_spring_apply(q.shape[0], _p(_f64(mass)), dt, _p(q), _p(qd), _p(f))
+    return q, qd, f
+
+
+def kinetic_energy(mass, qd):
+    """measureTotalEnergy: sum 0.5 m qd.qd."""
+    return lib().orc_kinetic_energy(_f64(mass).shape[0], _p(_f64(mass)), _p(_f64(qd)))
+
+
+def spring_steps(row_ptr, head, rest_len, mass, K, dt, q, qd, steps):
+    """The Fig. 2 loop body `steps` times (force starts at 0)."""
+    f = np.zeros_like(_f64(q))
+    for _ in range(steps):
+        f = spring_forces(row_ptr, head, q, rest_len, K, f)
+        q, qd, f = spring_apply(mass, dt, q, qd, f)
+    return q, qd
+

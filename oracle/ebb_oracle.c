@@ -651,3 +651,53 @@ void orc_implicit_update(int64_t nv, const double* dv, double h, double* u, doub
         u[i] += h * v[i];
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Fig. 2 spring-mass program, kernel by      */
+/* kernel, over the grouped edge relation (v.edges = rows of v):   */
+/*   initLen(e):               rest_len = |head.pos - tail.pos|           */
+/*   computeInternalForces(v): for e in v.edges: dq = e.head.q - v.q,     */
+/*                             dir = normalize(dq),                        */
+/*                             v.force += K (e.rest_len dir - dq)          */
+/*   applyForces(v):           qdd = force/mass; q += qd dt + 0.5 qdd dt^2;*/
+/*                             qd += qdd dt; force = 0                     */
+/*   measureTotalEnergy(v):    E += 0.5 mass qd.qd                         */
+/* Reading: normalize(0) = 0, so a self-loop row adds 0.   */
+/* ------------------------------------------------------------------ */
+void orc_spring_init_len(int64_t ne, const int64_t* tail, const int64_t* head, const double* pos,
+                         double* rest_len) {
+    for (int64_t e = 0; e < ne; ++e) {
+        double d[3];
+        for (int a = 0; a < 3; ++a) d[a] = pos[3 * head[e] + a] - pos[3 * tail[e] + a];
+        rest_len[e] = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    }
+}
+
+void orc_spring_forces(int64_t nv, const int64_t* row_ptr, const int64_t* head, const double* q,
+                       const double* rest_len, double K, double* force) {
+    for (int64_t v = 0; v < nv; ++v)
+        for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+            double dq[3], dir[3];
+            for (int a = 0; a < 3; ++a) dq[a] = q[3 * head[e] + a] - q[3 * v + a];
+            double len = sqrt(dq[0] * dq[0] + dq[1] * dq[1] + dq[2] * dq[2]);
+            for (int a = 0; a < 3; ++a) dir[a] = len > 0.0 ? dq[a] / len : 0.0;
+            for (int a = 0; a < 3; ++a) force[3 * v + a] += K * (rest_len[e] * dir[a] - dq[a]);
+        }
+}
+
+void orc_spring_apply(int64_t nv, const double* mass, double dt, double* q, double* qd, double* force) {
+    for (int64_t v = 0; v < nv; ++v)
+        for (int a = 0; a < 3; ++a) {
+            double qdd = force[3 * v + a] / mass[v];
+            q[3 * v + a] += qd[3 * v + a] * dt + 0.5 * qdd * dt * dt;
+            qd[3 * v + a] += qdd * dt;
+            force[3 * v + a] = 0.0;
+        }
+}
+
+double orc_kinetic_energy(int64_t nv, const double* mass, const double* qd) {
+    double E = 0.0;
+    for (int64_t v = 0; v < nv; ++v)
+        E += 0.5 * mass[v] * (qd[3 * v] * qd[3 * v] + qd[3 * v + 1] * qd[3 * v + 1] + qd[3 * v + 2] * qd[3 * v + 2]);
+    return E;
+}

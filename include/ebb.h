@@ -108,6 +108,7 @@ ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s);
 #define EBB_K_CG_DIR 3
 #define EBB_K_ASSEMBLE 4
 #define EBB_K_CG_SOLVE 5   /* persistent single-launch PCG (all iterations) */
+#define EBB_K_SPRING 6     /* Fig. 2 spring forces / fused spring step         */
 ebb_status ebb_timing_enable(ebb_ctx ctx, int on);
 ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64_t* launches, int reset);
 /* Number of kernels this context has launched (all entry points). */
@@ -432,6 +433,35 @@ ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u,
 /* Newton iteration update (after an EBB_RHS_NEWTON solve): vel += dv;
  * u += h dv (keeps u = u_n + h vel). */
 ebb_status ebb_newton_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
+
+/* ---- Fig. 2 spring-mass program ------------
+ * Query-loops over v.edges of a grouped edge relation (`edges`, grouped by
+ * tail, with a `head` key-field, e.g. the tetmesh edges).  All fields F32
+ * or F64 (one dtype per call): q, qd, force, pos AOS vec3 on the vertices,
+ * mass scalar on the vertices, rest_len scalar on the edges.  The force is
+ * the printed one, v.force += K (rest_len normalize(dq) - dq) with
+ * dq = e.head.q - v.q and normalize(0) = 0 (DESIGN.md §3 reading 21: a
+ * restoring spring has K < 0).  Stream-ordered; EBB_E_PHASE when a field
+ * is both read and reduced/written where the paper's phase rules forbid it
+ * (P:443-450). */
+/* initLen: rest_len[e] = |pos[head] - pos[tail]| */
+ebb_status ebb_spring_init_len(ebb_ctx ctx, ebb_rel edges, ebb_field pos, ebb_field rest_len, ebb_stream s);
+/* computeInternalForces: force (+)= K sum_{e in v.edges} (rest_len dir - dq);
+ * accumulate = 0 overwrites force (Fig. 2's force is zero on entry). */
+ebb_status ebb_spring_forces(ebb_ctx ctx, ebb_rel edges, ebb_field q, ebb_field rest_len, double K,
+                             ebb_field force, int32_t accumulate, ebb_stream s);
+/* applyForces: qdd = force/mass; q += qd dt + qdd dt^2/2; qd += qdd dt; force = 0 */
+ebb_status ebb_spring_apply(ebb_ctx ctx, ebb_field mass, double dt, ebb_field q, ebb_field qd, ebb_field force,
+                            ebb_stream s);
+/* One whole Fig. 2 iteration in ONE kernel: forces from q_in kept in
+ * registers, then applyForces writing q_out (q double-buffered: neighbours
+ * read q while its owner would write it) and qd; force (nullable) receives
+ * the forces.  q_in, q_out, qd, force distinct. */
+ebb_status ebb_spring_step(ebb_ctx ctx, ebb_rel edges, ebb_field q_in, ebb_field q_out, ebb_field qd,
+                           ebb_field rest_len, ebb_field mass, double K, double dt, ebb_field force,
+                           ebb_stream s);
+/* measureTotalEnergy: out (F64 global) = sum mass qd.qd / 2 (deterministic) */
+ebb_status ebb_kinetic_energy(ebb_ctx ctx, ebb_field mass, ebb_field qd, ebb_field out, ebb_stream s);
 
 /* ---- multi-GPU partition ----------------------------- */
 /* owner_t(t) = floor(t P / T); owner_v(v) = owner_t(min tet containing v),

@@ -201,6 +201,17 @@ struct KernelTimer {
     }
 };
 
+// a grouped edge relation seen by a query-loop over v.edges:
+// CSR index (V+1), head keys, longest group, source relation
+struct EdgeGraph {
+    uint64_t nv = 0, ne = 0;
+    const uint32_t* index = nullptr;
+    const uint32_t* head = nullptr;
+    uint32_t max_group = 0;
+    ebb_rel verts = EBB_NONE;
+};
+ebb_status edge_graph(Ctx* c, ebb_rel edges, EdgeGraph* g);   // solver.cu
+
 size_t dtype_size(ebb_dtype d);
 ebb_status fail(Ctx* c, ebb_status code, const char* fmt, ...);
 ebb_status cuda_fail(Ctx* c, cudaError_t e, const char* where);

@@ -1346,14 +1346,10 @@ __global__ void k_global_reduce(uint64_t n, uint32_t comps, int soa, const R* __
     if (block_reduce_last_done<OP>(acc, partials, counter, &r)) *out = r;
 }
 
-struct EdgeGraph {
-    uint64_t nv = 0, ne = 0;
-    const uint32_t* index = nullptr;
-    const uint32_t* head = nullptr;
-    uint32_t max_group = 0;
-    ebb_rel verts = EBB_NONE;
-};
+}  // namespace
 
+// grouped edge relation of a query-loop (declared in ebb_internal.cuh)
+namespace ebb {
 ebb_status edge_graph(Ctx* c, ebb_rel edges, EdgeGraph* g) {
     Relation* E = get_rel(c, edges);
     if (!E) return fail(c, EBB_E_ARG, "bad edges relation");
@@ -1375,6 +1371,9 @@ ebb_status edge_graph(Ctx* c, ebb_rel edges, EdgeGraph* g) {
     g->max_group = E->max_group;
     return EBB_OK;
 }
+}  // namespace ebb
+
+namespace {
 
 template <typename R, bool CG, bool MPQ, bool DIR = false>
 ebb_status launch_tma(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask, double* pq_out,

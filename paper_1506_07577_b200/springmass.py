@@ -1,0 +1,86 @@
+"""The paper's Fig. 2 spring-mass program on the
+tetmesh relations of a ``TetFEM`` (its grouped edge relation is ``v.edges``).
+
+Each method is one ABI call; no arithmetic happens in Python:
+
+* ``init_len()``            initLen over the edges,
+* ``step_paper()``          computeInternalForces then applyForces -- the two
+                            kernels of Fig. 2 (force reduced, then applied),
+* ``step()``                the same iteration as ONE fused kernel
+                            (``ebb_spring_step``; q double-buffered),
+* ``kinetic_energy()``      measureTotalEnergy.
+
+The force is the printed one, ``K (rest_len dir - dq)`` (DESIGN.md §3
+reading 21: a restoring spring has K < 0).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _abi as A
+from .ebb import _stream
+
+
+class SpringMass:
+    def __init__(self, fem, K=1.0, dt=1e-4, q=None, qd=None, name="spring"):
+        self.fem, self.ctx = fem, fem.ctx
+        self.K, self.dt = float(K), float(dt)
+        dtype = fem.dtype
+        V, E = fem.verts, fem.edges
+        self.rest_len = E.field(f"{name}.rest_len", dtype)
+        self.q = V.field(f"{name}.q", dtype, (3, 1))
+        self.q2 = V.field(f"{name}.q2", dtype, (3, 1))          # the fused step's second buffer
+        self.qd = V.field(f"{name}.qd", dtype, (3, 1))
+        self.force = V.field(f"{name}.force", dtype, (3, 1))
+        self.force.fill(0.0)
+        self.qd.fill(0.0)
+        if dtype == "f64":
+            self.pos = fem.pos
+        else:
+            self.pos = V.field(f"{name}.pos", dtype, (3, 1))
+            self.pos.convert_from(fem.pos)
+        self.mass = fem.mass
+        self.init_len()
+        # dragon.vertices:NewField('q', L.vec3f):Load(dragon.vertices.pos)
+        if q is None:
+            self.q.copy_from(self.pos)
+        else:
+            self.q.write(fem.from_input_order(q))
+        if qd is not None:
+            self.qd.write(fem.from_input_order(qd))
+        self.energy = self.ctx.global_(f"{name}.E", "f64")
+
+    def _chk(self, st):
+        self.ctx.check(st)
+
+    def init_len(self, stream=None):
+        L, h = self.ctx.L, self.ctx.h
+        self._chk(L.ebb_spring_init_len(h, self.fem.edges.h, self.pos.h, self.rest_len.h, _stream(stream)))
+
+    def forces(self, accumulate=True, stream=None):
+        """computeInternalForces: force += K sum (rest_len dir - dq)."""
+        L, h = self.ctx.L, self.ctx.h
+        self._chk(L.ebb_spring_forces(h, self.fem.edges.h, self.q.h, self.rest_len.h, self.K, self.force.h,
+                                      int(accumulate), _stream(stream)))
+
+    def apply(self, stream=None):
+        """applyForces: q += qd dt + qdd dt^2/2, qd += qdd dt, force = 0."""
+        L, h = self.ctx.L, self.ctx.h
+        self._chk(L.ebb_spring_apply(h, self.mass.h, self.dt, self.q.h, self.qd.h, self.force.h, _stream(stream)))
+
+    def step_paper(self, stream=None):
+        self.forces(accumulate=True, stream=stream)
+        self.apply(stream=stream)
+
+    def step(self, keep_force=False, stream=None):
+        """One fused iteration: q2 <- step(q); then the buffers swap."""
+        L, h = self.ctx.L, self.ctx.h
+        self._chk(L.ebb_spring_step(h, self.fem.edges.h, self.q.h, self.q2.h, self.qd.h, self.rest_len.h,
+                                    self.mass.h, self.K, self.dt, self.force.h if keep_force else A.NONE,
+                                    _stream(stream)))
+        self.q, self.q2 = self.q2, self.q
+
+    def kinetic_energy(self, stream=None):
+        L, h = self.ctx.L, self.ctx.h
+        self._chk(L.ebb_kinetic_energy(h, self.mass.h, self.qd.h, self.energy.h, _stream(stream)))
+        return self.energy.get()

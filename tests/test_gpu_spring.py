@@ -1,0 +1,96 @@
+"""GPU parity of the Fig. 2 spring-mass program
+against the oracle's kernel-by-kernel loops, through the C ABI.
+
+Bars: fp64 forces <= 1e-12 relative, trajectories <= 1e-12 (q) and 1e-10
+(qd) after 20 steps; fp32 forces <= 1e-4 (near-cancelling terms c dq - dq
+with c = rest/len ~ 1 amplify fp32 rounding ~20x at 5 % strain).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import Case, gpu_fem, oracle_renumbered, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1506_07577_b200 import ebb
+    c = ebb.Context(0)
+    yield c
+    c.close()
+
+
+def _setup(ctx, dtype, name, n=6, K=1.0):
+    from paper_1506_07577_b200.springmass import SpringMass
+    case = Case(n=n)
+    fem = gpu_fem(ctx, case, dtype=dtype, name=name)
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    h = 1.0 / n
+    rng = np.random.default_rng(11)
+    q_in = case.X + rng.uniform(-0.05 * h, 0.05 * h, case.X.shape)       # input order
+    qd_in = rng.uniform(-0.1, 0.1, case.X.shape)
+    if dtype == "f32":
+        q_in = q_in.astype(np.float32).astype(np.float64)
+        qd_in = qd_in.astype(np.float32).astype(np.float64)
+    sm = SpringMass(fem, K=K, dt=1e-4, q=q_in, qd=qd_in, name=name)
+    X = m.X if dtype == "f64" else m.X.astype(np.float32).astype(np.float64)
+    L = oracle.spring_init_len(m.tail, m.head, X)
+    return sm, fem, m, L, q_in[order], qd_in[order]
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-4)])
+def test_init_len_and_forces(ctx, dtype, tol):
+    sm, fem, m, L, q, qd = _setup(ctx, dtype, f"spf{dtype}", K=1.3)
+    assert rel_l2(sm.rest_len.read(), L) <= (1e-15 if dtype == "f64" else 1e-7)
+    sm.forces(accumulate=False)
+    ref = oracle.spring_forces(m.row_ptr, m.head, q, L, 1.3)
+    assert rel_l2(sm.force.read(), ref) <= tol
+    sm.forces(accumulate=True)                       # the paper's `+=`: twice the sum
+    assert rel_l2(sm.force.read(), 2 * ref) <= tol
+
+
+def test_paper_and_fused_steps_match_the_oracle(ctx):
+    sm, fem, m, L, q, qd = _setup(ctx, "f64", "spstep", K=-2.0)
+    mass = fem.mass.read().ravel()
+    assert rel_l2(mass, m.mass) <= 1e-15
+    qr, qdr = oracle.spring_steps(m.row_ptr, m.head, L, m.mass, -2.0, 1e-4, q, qd, 20)
+    for _ in range(20):
+        sm.step_paper()
+    assert rel_l2(sm.q.read(), qr) <= 1e-12
+    assert rel_l2(sm.qd.read(), qdr) <= 1e-10
+    assert np.all(sm.force.read() == 0.0)            # applyForces zeroes it
+    e = sm.kinetic_energy()
+    assert abs(e - oracle.kinetic_energy(m.mass, qdr)) <= 1e-10 * e
+    # the fused kernel from the same start
+    sm2, fem2, *_ = _setup(ctx, "f64", "spstep2", K=-2.0)
+    for _ in range(20):
+        sm2.step()
+    assert rel_l2(sm2.q.read(), qr) <= 1e-12
+    assert rel_l2(sm2.qd.read(), qdr) <= 1e-10
+
+
+def test_rest_state_invariance(ctx):
+    from paper_1506_07577_b200.springmass import SpringMass
+    case = Case(n=5)
+    fem = gpu_fem(ctx, case, name="sprest")
+    sm = SpringMass(fem, K=1.0, dt=1e-4, name="sprest")     # q = pos, qd = 0
+    for _ in range(100):
+        sm.step()
+    assert np.abs(sm.q.read() - fem.pos.read()).max() <= 1e-14
+    assert np.abs(sm.qd.read()).max() <= 1e-11
+
+
+def test_phase_violation_is_refused(ctx):
+    from paper_1506_07577_b200.ebb import EbbError
+    sm, fem, *_ = _setup(ctx, "f64", "spphase")
+    L, h = ctx.L, ctx.h
+    with pytest.raises(EbbError, match="EBB_E_PHASE"):
+        ctx.check(L.ebb_spring_forces(h, fem.edges.h, sm.q.h, sm.rest_len.h, 1.0, sm.q.h, 0, None))
+    with pytest.raises(EbbError, match="EBB_E_PHASE"):
+        ctx.check(L.ebb_spring_step(h, fem.edges.h, sm.q.h, sm.q.h, sm.qd.h, sm.rest_len.h, sm.mass.h,
+                                    1.0, 1e-4, 0xFFFFFFFF, None))

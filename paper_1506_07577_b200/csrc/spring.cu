@@ -18,6 +18,7 @@
 // write q_out) because neighbours read q while owners would write it -- the
 // phase rule of P:443-450 that makes the paper split the two kernels.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ebb_internal.cuh"
 #include "reduce.cuh"
@@ -44,7 +45,9 @@ __device__ __forceinline__ void spring_row_sum(uint64_t v, bool live, const uint
     s0 = s1 = s2 = R(0);
     if (live) {
         const R q0 = q[3 * v], q1 = q[3 * v + 1], q2 = q[3 * v + 2];
-        for (uint32_t e = index[v] + lane; e < index[v + 1]; e += LPV) {
+        const uint32_t e1 = index[v + 1];
+#pragma unroll 4
+        for (uint32_t e = index[v] + lane; e < e1; e += LPV) {
             const uint64_t h = head[e];
             const R L = rest[e];
             const R d0 = q[3 * h] - q0, d1 = q[3 * h + 1] - q1, d2 = q[3 * h + 2] - q2;
@@ -92,12 +95,12 @@ __device__ __forceinline__ void spring_update(R f, R m, R dt, R q, R& qd, R& qn)
 }
 
 template <typename R>
-__global__ void k_spring_apply(uint64_t nv, const R* __restrict__ mass, R dt, R* __restrict__ q, R* __restrict__ qd,
-                               R* __restrict__ force) {
+__global__ void k_spring_apply(uint64_t nv, int qs, const R* __restrict__ mass, R dt, R* __restrict__ q,
+                               R* __restrict__ qd, R* __restrict__ force) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= 3 * nv) return;
+    if (i >= (uint64_t)qs * nv || i % qs == 3) return;   // (padding lane of a 4x1 record)
     R v = qd[i], qn;
-    spring_update(force[i], mass[i / 3], dt, q[i], v, qn);
+    spring_update(force[i], mass[i / qs], dt, q[i], v, qn);
     q[i] = qn;
     qd[i] = v;
     force[i] = R(0);
@@ -113,27 +116,152 @@ __global__ void __launch_bounds__(256) k_spring_step(uint64_t nv, const uint32_t
                                                      R* __restrict__ force) {
     const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPV;
     const bool live = v < nv;
+    const unsigned lane = threadIdx.x % LPV;
+    // the update operands do not depend on the forces: load them first so
+    // their latency overlaps the row walk (components c = lane, lane + LPV, ..)
+    constexpr int NC = LPV >= 3 ? 1 : (3 + LPV - 1) / LPV;
+    R w[NC], qi[NC], mv = 1;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        const unsigned c = lane + k * LPV;
+        w[k] = qi[k] = 0;
+        if (live && c < 3) {
+            w[k] = qd[3 * v + c];
+            qi[k] = q[3 * v + c];
+        }
+    }
+    if (live && lane < 3) mv = mass[v];
     R s[3];
     spring_row_sum<R, LPV>(v, live, index, head, q, rest, K, s[0], s[1], s[2]);
-    const unsigned lane = threadIdx.x % LPV;
-    if (live && lane < 3) {   // one component per lane
-        const R f = lane == 0 ? s[0] : lane == 1 ? s[1] : s[2];
-        const uint64_t i = 3 * v + lane;
-        R w = qd[i], qn;
-        spring_update(f, mass[v], dt, q[i], w, qn);
-        qout[i] = qn;
-        qd[i] = w;
-        if (force) force[i] = f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        const unsigned c = lane + k * LPV;
+        if (live && c < 3) {
+            const R f = c == 0 ? s[0] : c == 1 ? s[1] : s[2];
+            R qn;
+            spring_update(f, mv, dt, qi[k], w[k], qn);
+            qout[3 * v + c] = qn;
+            qd[3 * v + c] = w[k];
+            if (force) force[3 * v + c] = f;
+        }
+    }
+}
+
+// Row-staged variant (the default): a CTA owns SB consecutive vertices, whose
+// rows are one contiguous range of the grouped relation: the CTA
+// first copies that range of head keys and rest lengths into shared memory
+// with coalesced loads, then thread = vertex walks its rows there (only the
+// q gathers go to L2).  STEP: the fused iteration (else forces only).
+#define SPRING_SB 128
+template <typename R>
+struct SpV4;
+template <>
+struct SpV4<double> {
+    using T = double4;
+};
+template <>
+struct SpV4<float> {
+    using T = float4;
+};
+// QS = record stride of the vertex vectors: 3 (vec3) or 4 (padded: one
+// 32-byte fp64 / 16-byte fp32 access per gathered record)
+template <typename R, int QS>
+__device__ __forceinline__ void ld_rec(const R* __restrict__ p, uint64_t v, R& a, R& b, R& c) {
+    if constexpr (QS == 4) {
+        const auto r = reinterpret_cast<const typename SpV4<R>::T*>(p)[v];
+        a = r.x;
+        b = r.y;
+        c = r.z;
+    } else {
+        a = p[3 * v];
+        b = p[3 * v + 1];
+        c = p[3 * v + 2];
+    }
+}
+template <typename R, bool STEP, int QS>
+__global__ void __launch_bounds__(SPRING_SB) k_spring_staged(uint64_t nv, const uint32_t* __restrict__ index,
+                                                             const uint32_t* __restrict__ head,
+                                                             const R* __restrict__ q, const R* __restrict__ rest,
+                                                             const R* __restrict__ mass, R K, R dt,
+                                                             R* __restrict__ qout, R* __restrict__ qd,
+                                                             R* __restrict__ force, int accumulate) {
+    extern __shared__ __align__(16) unsigned char sp_smem[];
+    const uint64_t v0 = (uint64_t)blockIdx.x * SPRING_SB;
+    const uint64_t v1 = v0 + SPRING_SB < nv ? v0 + SPRING_SB : nv;
+    const uint32_t e0 = index[v0], n = index[v1] - e0;
+    R* ls = reinterpret_cast<R*>(sp_smem);
+    uint32_t* hs = reinterpret_cast<uint32_t*>(ls + ((n + 1) & ~1u));
+    // asynchronous copies (cp.async: no registers held while in flight, so
+    // every row of the range is requested at once)
+    for (uint32_t k = threadIdx.x; k < n; k += SPRING_SB) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(hs + k)),
+                     "l"(head + e0 + k)
+                     : "memory");
+        if constexpr (sizeof(R) == 8)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(ls + k)),
+                         "l"(rest + e0 + k)
+                         : "memory");
+        else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(ls + k)),
+                         "l"(rest + e0 + k)
+                         : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const uint64_t v = v0 + threadIdx.x;
+    const bool live = v < v1;
+    R w[3], qv[3], mv = 1;
+    uint32_t r0 = 0, r1 = 0;
+    if (live) {
+        ld_rec<R, QS>(q, v, qv[0], qv[1], qv[2]);
+        if (STEP) {
+            ld_rec<R, QS>(qd, v, w[0], w[1], w[2]);
+            mv = mass[v];
+        } else {
+            w[0] = w[1] = w[2] = R(0);
+        }
+        r0 = index[v] - e0;
+        r1 = index[v + 1] - e0;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (!live) return;
+    R s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll 4
+    for (uint32_t r = r0; r < r1; ++r) {
+        const uint64_t h = hs[r];
+        const R L = ls[r];
+        R qh0, qh1, qh2;
+        ld_rec<R, QS>(q, h, qh0, qh1, qh2);
+        const R d0 = qh0 - qv[0], d1 = qh1 - qv[1], d2 = qh2 - qv[2];
+        const R len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        const R c = len > R(0) ? L / len : R(0);
+        s0 += K * (c * d0 - d0);
+        s1 += K * (c * d1 - d1);
+        s2 += K * (c * d2 - d2);
+    }
+    const R f[3] = {s0, s1, s2};
+    if (STEP) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            R qn, wc = w[c];
+            spring_update(f[c], mv, dt, qv[c], wc, qn);
+            qout[QS * v + c] = qn;
+            qd[QS * v + c] = wc;
+            if (force) force[QS * v + c] = f[c];
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) force[QS * v + c] = accumulate ? f[c] + force[QS * v + c] : f[c];
     }
 }
 
 template <typename R>
-__global__ void __launch_bounds__(256) k_kinetic_energy(uint64_t nv, const R* __restrict__ mass,
+__global__ void __launch_bounds__(256) k_kinetic_energy(uint64_t nv, int qs, const R* __restrict__ mass,
                                                         const R* __restrict__ qd, double* __restrict__ partials,
                                                         unsigned int* __restrict__ counter, double* __restrict__ out) {
     double acc = 0.0;
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
-        const double a = qd[3 * v], b = qd[3 * v + 1], c = qd[3 * v + 2];
+        const double a = qd[qs * v], b = qd[qs * v + 1], c = qd[qs * v + 2];
         acc += 0.5 * (double)mass[v] * (a * a + b * b + c * c);
     }
     double tot;
@@ -143,9 +271,9 @@ __global__ void __launch_bounds__(256) k_kinetic_energy(uint64_t nv, const R* __
 ebb_status check_vert_vec(Ctx* c, ebb_field f, ebb_rel verts, ebb_dtype dt, const char* what, Field** out) {
     Field* F = get_field(c, f);
     if (!F) return fail(c, EBB_E_ARG, "spring: bad %s", what);
-    if (F->rel != verts || F->comps() != 3 || F->layout != EBB_AOS || F->dtype != dt)
-        return fail(c, EBB_E_TYPE, "spring: %s must be an AOS vec3 field of the %s dtype on the vertices", what,
-                    dt == EBB_F64 ? "F64" : "F32");
+    if (F->rel != verts || (F->comps() != 3 && F->comps() != 4) || F->layout != EBB_AOS || F->dtype != dt)
+        return fail(c, EBB_E_TYPE, "spring: %s must be an AOS vec3 (or padded 4x1) field of the %s dtype on the "
+                    "vertices", what, dt == EBB_F64 ? "F64" : "F32");
     *out = F;
     return EBB_OK;
 }
@@ -165,7 +293,33 @@ ebb_status float_dtype(Ctx* c, Field* F, ebb_dtype* dt) {
     return EBB_OK;
 }
 
-int lanes_for(const EdgeGraph& G) { return G.max_group <= 16 ? 16 : 32; }
+// lanes per vertex of the register-path query-loop (EBB_SPRING_LPV = 1..32);
+// 0 = the row-staged kernel.  Defaults (measured): the fused
+// step and padded records use the staged kernel, vec3 forces-only the
+// thread-per-vertex register path.
+int lanes_for(const EdgeGraph& G, bool step, int qs) {
+    const char* e = getenv("EBB_SPRING_LPV");
+    if (e) {
+        const int l = atoi(e);
+        if (l == 1 || l == 2 || l == 4 || l == 8 || l == 16 || l == 32) return l;
+    }
+    const size_t smem = (size_t)SPRING_SB * (G.max_group ? G.max_group : 1) * 12 + 16;
+    if (qs == 4 || (step && smem <= 160 * 1024)) return 0;
+    return 1;
+}
+
+template <typename R, bool STEP>
+ebb_status launch_staged(Ctx* c, const EdgeGraph& G, int qs, const R* q, const R* rest, const R* mass, R K, R dt,
+                         R* qout, R* qd, R* force, int accumulate, cudaStream_t s) {
+    const size_t smem = (size_t)SPRING_SB * (G.max_group ? G.max_group : 1) * (sizeof(R) + 4) + 16;
+    auto kern = qs == 4 ? k_spring_staged<R, STEP, 4> : k_spring_staged<R, STEP, 3>;
+    if (smem > 48 * 1024)
+        EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid_for(G.nv, SPRING_SB), SPRING_SB, smem, s>>>(G.nv, G.index, G.head, q, rest, mass, K, dt, qout, qd,
+                                                           force, accumulate);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
 
 }  // namespace
 }  // namespace ebb
@@ -186,6 +340,7 @@ ebb_status ebb_spring_init_len(ebb_ctx ctx, ebb_rel edges, ebb_field pos, ebb_fi
     EBB_TRY(float_dtype(c, P, &dt));
     Field *Pf, *Lf;
     EBB_TRY(check_vert_vec(c, pos, G.verts, dt, "pos", &Pf));
+    if (Pf->comps() != 3) return fail(c, EBB_E_TYPE, "spring_init_len: pos must be a vec3 (3x1) field");
     EBB_TRY(check_scalar(c, rest_len, edges, dt, "rest_len", &Lf));
     const uint32_t* tail = (const uint32_t*)c->fields[E->grouped_by].ptr;
     cudaStream_t s = (cudaStream_t)stream;
@@ -218,12 +373,24 @@ ebb_status ebb_spring_forces(ebb_ctx ctx, ebb_rel edges, ebb_field q, ebb_field 
     EBB_TRY(check_scalar(c, rest_len, edges, dt, "rest_len", &L));
     if (F->ptr == Q->ptr) return fail(c, EBB_E_PHASE, "spring: force aliases q (read and reduced in one kernel)");
     cudaStream_t s = (cudaStream_t)stream;
-    const int lpv = lanes_for(G);
+    const int qs = (int)Q->comps();
+    if (F->comps() != Q->comps()) return fail(c, EBB_E_TYPE, "spring: q and force must have the same record shape");
+    const int lpv = lanes_for(G, false, qs);
+    if (qs == 4 && lpv != 0) return fail(c, EBB_E_TYPE, "spring: padded records need the staged kernel");
     KernelTimer kt(c, EBB_K_SPRING, s);
+    if (G.nv && lpv == 0) {
+        if (dt == EBB_F64)
+            return launch_staged<double, false>(c, G, qs, (const double*)Q->ptr, (const double*)L->ptr, nullptr, K,
+                                                0.0, nullptr, nullptr, (double*)F->ptr, accumulate, s);
+        return launch_staged<float, false>(c, G, qs, (const float*)Q->ptr, (const float*)L->ptr, nullptr, (float)K,
+                                           0.f, nullptr, nullptr, (float*)F->ptr, accumulate, s);
+    }
     if (G.nv) {
 #define EBB_SPF(R)                                                                                                  \
     do {                                                                                                            \
-        auto k = lpv == 16 ? k_spring_forces<R, 16> : k_spring_forces<R, 32>;                                       \
+        auto k = lpv == 1 ? k_spring_forces<R, 1> : lpv == 2 ? k_spring_forces<R, 2>                               \
+               : lpv == 4 ? k_spring_forces<R, 4> : lpv == 8 ? k_spring_forces<R, 8>                               \
+               : lpv == 16 ? k_spring_forces<R, 16> : k_spring_forces<R, 32>;                                       \
         k<<<grid_for(G.nv * lpv, 256), 256, 0, s>>>(G.nv, G.index, G.head, (const R*)Q->ptr, (const R*)L->ptr,      \
                                                     (R)K, (R*)F->ptr, accumulate);                                  \
     } while (0)
@@ -248,16 +415,20 @@ ebb_status ebb_spring_apply(ebb_ctx ctx, ebb_field mass, double dt_step, ebb_fie
     EBB_TRY(check_vert_vec(c, qd, Q0->rel, dt, "qd", &QD));
     EBB_TRY(check_vert_vec(c, force, Q0->rel, dt, "force", &F));
     EBB_TRY(check_scalar(c, mass, Q0->rel, dt, "mass", &M));
+    if (QD->comps() != Q->comps() || F->comps() != Q->comps())
+        return fail(c, EBB_E_TYPE, "spring_apply: q, qd, force must have the same record shape");
     const uint64_t nv = c->rels[Q0->rel].size;
     cudaStream_t s = (cudaStream_t)stream;
     c->launches++;
     if (nv) {
         if (dt == EBB_F64)
-            k_spring_apply<double><<<grid_for(3 * nv, 256), 256, 0, s>>>(nv, (const double*)M->ptr, dt_step,
+            k_spring_apply<double><<<grid_for(Q->comps() * nv, 256), 256, 0, s>>>(nv, (int)Q->comps(),
+                                                                         (const double*)M->ptr, dt_step,
                                                                          (double*)Q->ptr, (double*)QD->ptr,
                                                                          (double*)F->ptr);
         else
-            k_spring_apply<float><<<grid_for(3 * nv, 256), 256, 0, s>>>(nv, (const float*)M->ptr, (float)dt_step,
+            k_spring_apply<float><<<grid_for(Q->comps() * nv, 256), 256, 0, s>>>(nv, (int)Q->comps(),
+                                                                        (const float*)M->ptr, (float)dt_step,
                                                                         (float*)Q->ptr, (float*)QD->ptr,
                                                                         (float*)F->ptr);
     }
@@ -286,12 +457,27 @@ ebb_status ebb_spring_step(ebb_ctx ctx, ebb_rel edges, ebb_field q_in, ebb_field
     if (Qo->ptr == Qi->ptr || QD->ptr == Qi->ptr || QD->ptr == Qo->ptr || (F && (F->ptr == Qi->ptr || F->ptr == Qo->ptr)))
         return fail(c, EBB_E_PHASE, "spring_step: q_in, q_out, qd and force must be distinct fields");
     cudaStream_t s = (cudaStream_t)stream;
-    const int lpv = lanes_for(G);
+    const int qs = (int)Qi->comps();
+    if (Qo->comps() != Qi->comps() || QD->comps() != Qi->comps() || (F && F->comps() != Qi->comps()))
+        return fail(c, EBB_E_TYPE, "spring_step: q_in, q_out, qd, force must have the same record shape");
+    const int lpv = lanes_for(G, true, qs);
+    if (qs == 4 && lpv != 0) return fail(c, EBB_E_TYPE, "spring: padded records need the staged kernel");
     KernelTimer kt(c, EBB_K_SPRING, s);
+    if (G.nv && lpv == 0) {
+        if (dt == EBB_F64)
+            return launch_staged<double, true>(c, G, qs, (const double*)Qi->ptr, (const double*)L->ptr,
+                                               (const double*)M->ptr, K, dt_step, (double*)Qo->ptr,
+                                               (double*)QD->ptr, F ? (double*)F->ptr : nullptr, 0, s);
+        return launch_staged<float, true>(c, G, qs, (const float*)Qi->ptr, (const float*)L->ptr,
+                                          (const float*)M->ptr, (float)K, (float)dt_step, (float*)Qo->ptr,
+                                          (float*)QD->ptr, F ? (float*)F->ptr : nullptr, 0, s);
+    }
     if (G.nv) {
 #define EBB_SPS(R)                                                                                                  \
     do {                                                                                                            \
-        auto k = lpv == 16 ? k_spring_step<R, 16> : k_spring_step<R, 32>;                                           \
+        auto k = lpv == 1 ? k_spring_step<R, 1> : lpv == 2 ? k_spring_step<R, 2>                                   \
+               : lpv == 4 ? k_spring_step<R, 4> : lpv == 8 ? k_spring_step<R, 8>                                   \
+               : lpv == 16 ? k_spring_step<R, 16> : k_spring_step<R, 32>;                                           \
         k<<<grid_for(G.nv * lpv, 256), 256, 0, s>>>(G.nv, G.index, G.head, (const R*)Qi->ptr, (const R*)L->ptr,     \
                                                     (const R*)M->ptr, (R)K, (R)dt_step, (R*)Qo->ptr, (R*)QD->ptr,   \
                                                     F ? (R*)F->ptr : nullptr);                                      \
@@ -322,10 +508,10 @@ ebb_status ebb_kinetic_energy(ebb_ctx ctx, ebb_field mass, ebb_field qd, ebb_fie
     c->launches++;
     const unsigned g = nv ? (unsigned)std::min<uint64_t>(grid_for(nv, 256), 4096) : 1;
     if (dt == EBB_F64)
-        k_kinetic_energy<double><<<g, 256, 0, s>>>(nv, (const double*)M->ptr, (const double*)QD->ptr, c->d_partials,
+        k_kinetic_energy<double><<<g, 256, 0, s>>>(nv, (int)QD->comps(), (const double*)M->ptr, (const double*)QD->ptr, c->d_partials,
                                                    c->d_counter + 12, (double*)O->ptr);
     else
-        k_kinetic_energy<float><<<g, 256, 0, s>>>(nv, (const float*)M->ptr, (const float*)QD->ptr, c->d_partials,
+        k_kinetic_energy<float><<<g, 256, 0, s>>>(nv, (int)QD->comps(), (const float*)M->ptr, (const float*)QD->ptr, c->d_partials,
                                                   c->d_counter + 12, (double*)O->ptr);
     EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;

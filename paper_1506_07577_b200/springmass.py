@@ -17,23 +17,29 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from . import _abi as A
 from .ebb import _stream
 
 
 class SpringMass:
-    def __init__(self, fem, K=1.0, dt=1e-4, q=None, qd=None, name="spring"):
+    """padded=True stores q, qd, force as 4x1 records (one 32-byte fp64 /
+    16-byte fp32 access per gathered vertex; the 4th lane is padding)."""
+
+    def __init__(self, fem, K=1.0, dt=1e-4, q=None, qd=None, padded=False, name="spring"):
         self.fem, self.ctx = fem, fem.ctx
         self.K, self.dt = float(K), float(dt)
         dtype = fem.dtype
         V, E = fem.verts, fem.edges
+        rec = (4, 1) if padded else (3, 1)
         self.rest_len = E.field(f"{name}.rest_len", dtype)
-        self.q = V.field(f"{name}.q", dtype, (3, 1))
-        self.q2 = V.field(f"{name}.q2", dtype, (3, 1))          # the fused step's second buffer
-        self.qd = V.field(f"{name}.qd", dtype, (3, 1))
-        self.force = V.field(f"{name}.force", dtype, (3, 1))
-        self.force.fill(0.0)
-        self.qd.fill(0.0)
+        self.q = V.field(f"{name}.q", dtype, rec)
+        self.q2 = V.field(f"{name}.q2", dtype, rec)          # the fused step's second buffer
+        self.qd = V.field(f"{name}.qd", dtype, rec)
+        self.force = V.field(f"{name}.force", dtype, rec)
+        for fld in (self.q, self.q2, self.qd, self.force):
+            fld.fill(0.0)
         if dtype == "f64":
             self.pos = fem.pos
         else:
@@ -42,13 +48,27 @@ class SpringMass:
         self.mass = fem.mass
         self.init_len()
         # dragon.vertices:NewField('q', L.vec3f):Load(dragon.vertices.pos)
-        if q is None:
-            self.q.copy_from(self.pos)
-        else:
-            self.q.write(fem.from_input_order(q))
+        q_st = fem.pos.read() if q is None else fem.from_input_order(np.asarray(q, dtype=np.float64))
+        self.q.write(self._rec(q_st))
         if qd is not None:
-            self.qd.write(fem.from_input_order(qd))
+            self.qd.write(self._rec(fem.from_input_order(np.asarray(qd, dtype=np.float64))))
         self.energy = self.ctx.global_(f"{name}.E", "f64")
+
+    def _rec(self, a):
+        a = np.asarray(a, dtype=np.float64).reshape(-1, 3)
+        if self.q.shape[0] == 4:
+            a = np.hstack([a, np.zeros((a.shape[0], 1))])
+        return a
+
+    def read_q(self):
+        """q in stored vertex order, (V, 3)."""
+        return self.q.read().reshape(self.fem.nv, -1)[:, :3]
+
+    def read_qd(self):
+        return self.qd.read().reshape(self.fem.nv, -1)[:, :3]
+
+    def read_force(self):
+        return self.force.read().reshape(self.fem.nv, -1)[:, :3]
 
     def _chk(self, st):
         self.ctx.check(st)

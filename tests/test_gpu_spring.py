@@ -25,7 +25,7 @@ def ctx():
     c.close()
 
 
-def _setup(ctx, dtype, name, n=6, K=1.0):
+def _setup(ctx, dtype, name, n=6, K=1.0, padded=False):
     from paper_1506_07577_b200.springmass import SpringMass
     case = Case(n=n)
     fem = gpu_fem(ctx, case, dtype=dtype, name=name)
@@ -37,41 +37,50 @@ def _setup(ctx, dtype, name, n=6, K=1.0):
     if dtype == "f32":
         q_in = q_in.astype(np.float32).astype(np.float64)
         qd_in = qd_in.astype(np.float32).astype(np.float64)
-    sm = SpringMass(fem, K=K, dt=1e-4, q=q_in, qd=qd_in, name=name)
+    sm = SpringMass(fem, K=K, dt=1e-4, q=q_in, qd=qd_in, padded=padded, name=name)
     X = m.X if dtype == "f64" else m.X.astype(np.float32).astype(np.float64)
     L = oracle.spring_init_len(m.tail, m.head, X)
     return sm, fem, m, L, q_in[order], qd_in[order]
 
 
+@pytest.mark.parametrize("padded", [True, False])
 @pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-4)])
-def test_init_len_and_forces(ctx, dtype, tol):
-    sm, fem, m, L, q, qd = _setup(ctx, dtype, f"spf{dtype}", K=1.3)
+def test_init_len_and_forces(ctx, dtype, tol, padded):
+    sm, fem, m, L, q, qd = _setup(ctx, dtype, f"spf{dtype}{int(padded)}", K=1.3, padded=padded)
     assert rel_l2(sm.rest_len.read(), L) <= (1e-15 if dtype == "f64" else 1e-7)
     sm.forces(accumulate=False)
     ref = oracle.spring_forces(m.row_ptr, m.head, q, L, 1.3)
-    assert rel_l2(sm.force.read(), ref) <= tol
+    assert rel_l2(sm.read_force(), ref) <= tol
     sm.forces(accumulate=True)                       # the paper's `+=`: twice the sum
-    assert rel_l2(sm.force.read(), 2 * ref) <= tol
+    assert rel_l2(sm.read_force(), 2 * ref) <= tol
 
 
-def test_paper_and_fused_steps_match_the_oracle(ctx):
+def test_paper_and_fused_steps_match_the_oracle(ctx, monkeypatch):
     sm, fem, m, L, q, qd = _setup(ctx, "f64", "spstep", K=-2.0)
     mass = fem.mass.read().ravel()
     assert rel_l2(mass, m.mass) <= 1e-15
     qr, qdr = oracle.spring_steps(m.row_ptr, m.head, L, m.mass, -2.0, 1e-4, q, qd, 20)
     for _ in range(20):
         sm.step_paper()
-    assert rel_l2(sm.q.read(), qr) <= 1e-12
-    assert rel_l2(sm.qd.read(), qdr) <= 1e-10
-    assert np.all(sm.force.read() == 0.0)            # applyForces zeroes it
+    assert rel_l2(sm.read_q(), qr) <= 1e-12
+    assert rel_l2(sm.read_qd(), qdr) <= 1e-10
+    assert np.all(sm.read_force() == 0.0)            # applyForces zeroes it
     e = sm.kinetic_energy()
     assert abs(e - oracle.kinetic_energy(m.mass, qdr)) <= 1e-10 * e
-    # the fused kernel from the same start
-    sm2, fem2, *_ = _setup(ctx, "f64", "spstep2", K=-2.0)
+    # the fused kernel from the same start (padded records, and vec3 with the
+    # register-path query-loop)
+    sm2, fem2, *_ = _setup(ctx, "f64", "spstep2", K=-2.0, padded=True)
     for _ in range(20):
         sm2.step()
-    assert rel_l2(sm2.q.read(), qr) <= 1e-12
-    assert rel_l2(sm2.qd.read(), qdr) <= 1e-10
+    assert rel_l2(sm2.read_q(), qr) <= 1e-12
+    assert rel_l2(sm2.read_qd(), qdr) <= 1e-10
+    for lpv in ("1", "4", "16"):
+        monkeypatch.setenv("EBB_SPRING_LPV", lpv)
+        sm3, *_ = _setup(ctx, "f64", f"spstep3{lpv}", K=-2.0, padded=False)
+        for _ in range(20):
+            sm3.step()
+        assert rel_l2(sm3.read_q(), qr) <= 1e-12
+        assert rel_l2(sm3.read_qd(), qdr) <= 1e-10
 
 
 def test_rest_state_invariance(ctx):
@@ -81,8 +90,8 @@ def test_rest_state_invariance(ctx):
     sm = SpringMass(fem, K=1.0, dt=1e-4, name="sprest")     # q = pos, qd = 0
     for _ in range(100):
         sm.step()
-    assert np.abs(sm.q.read() - fem.pos.read()).max() <= 1e-14
-    assert np.abs(sm.qd.read()).max() <= 1e-11
+    assert np.abs(sm.read_q() - fem.pos.read().reshape(-1, 3)).max() <= 1e-14
+    assert np.abs(sm.read_qd()).max() <= 1e-11
 
 
 def test_phase_violation_is_refused(ctx):

@@ -171,6 +171,63 @@ def run_c4cg(sizes, reps, dtypes=("f64", "f32")):
             del fem
 
 
+def run_spring(sizes, reps, dtypes=("f64", "f32"), steps=50):
+    """the Fig. 2 spring-mass iteration (fused one-kernel step
+    and the paper's two kernels) per Kuhn-6 size; steps back to back (the
+    workload's own loop), CUDA events around `steps` iterations."""
+    import numpy as np
+    import torch
+
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.springmass import SpringMass
+    from paper_1506_07577_b200.tetfem import TetFEM
+    from synth import mesh as M
+
+    peak, src = bench._peaks()
+    flush = torch.empty(bench.FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    for n in sizes:
+        X, tets = M.kuhn6(n)
+        X, tets = M.permute_vertices(X, tets, 2)
+        q0 = X + np.random.default_rng(1).uniform(-0.05 / n, 0.05 / n, X.shape)
+        for dt in dtypes:
+            ctx = ebb.Context(0)
+            fem = TetFEM(ctx, X, tets, dtype=dt, name=f"sp{n}{dt}")
+            sm = SpringMass(fem, K=-1.0, dt=1e-4, q=q0, name=f"sp{n}{dt}")
+            bf = 8 if dt == "f64" else 4
+            V, E = fem.nv, fem.ne
+            b_fused = E * (4 + bf) + V * 13 * bf            # head, rest_len; q r + q' w, qd r/w, mass
+            b_paper = (E * (4 + bf) + V * 6 * bf) + V * 16 * bf
+            for mode in ("fused", "paper"):
+                fn = sm.step if mode == "fused" else sm.step_paper
+                for _ in range(5):
+                    fn()
+                torch.cuda.synchronize()
+                res = {}
+                for warm in (True, False):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    tot = 0.0
+                    for _ in range(reps):
+                        if not warm:
+                            _flush(flush)
+                        a.record()
+                        for _ in range(steps if warm else 1):
+                            fn()
+                        b.record()
+                        torch.cuda.synchronize()
+                        tot += a.elapsed_time(b)
+                    res["l2_warm" if warm else "l2_flushed"] = 1e3 * tot / (reps * (steps if warm else 1))
+                bb = b_fused if mode == "fused" else b_paper
+                print(json.dumps({"workload": "spring-mass (Fig. 2)", "mode": mode, "mesh": f"kuhn6 n={n}",
+                                  "verts": V, "edge_rows": E, "dtype": dt,
+                                  "step_us_back_to_back": res["l2_warm"], "step_us_l2_flushed": res["l2_flushed"],
+                                  "algorithmic_bytes": bb,
+                                  "hbm_frac_flushed": bb / (res["l2_flushed"] * 1e-6) / 1e9 / peak,
+                                  "gbs_back_to_back": bb / (res["l2_warm"] * 1e-6) / 1e9,
+                                  "peak_gbs": peak, "peak_source": src}), flush=True)
+            ctx.close()
+            del fem, sm
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", action="store_true")
@@ -181,6 +238,7 @@ def main():
     ap.add_argument("--c2", action="store_true", help="the map sweep on the C2 Kuhn n=55 mesh")
     ap.add_argument("--c4map", action="store_true", help="the map strategies on every --sizes Kuhn mesh")
     ap.add_argument("--c4cg", action="store_true", help="the PCG iteration on every --sizes Kuhn mesh")
+    ap.add_argument("--spring", action="store_true", help="the Fig. 2 spring-mass step on every --sizes Kuhn mesh")
     ap.add_argument("--scatters", default="segmented,gather,tiled,atomic")
     ap.add_argument("--dtypes", default="f32,f64")
     ap.add_argument("--models", default="stvk,nh")
@@ -202,6 +260,8 @@ def main():
                    models=a.models.split(","))
     if a.c4cg:
         run_c4cg([int(x) for x in a.sizes.split(",")], a.reps)
+    if a.spring:
+        run_spring([int(x) for x in a.sizes.split(",")], a.reps, dtypes=a.dtypes.split(","))
 
 
 if __name__ == "__main__":

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) k_spmv(uint64_t nv, const uint32_t* __res
 #define TMA_CONSUMERS 8
 #define PCG_GROUPS 2                          // persistent PCG: consumer warp groups
 #define PCG_WPG (TMA_CONSUMERS / PCG_GROUPS)  // warps per group
-template <typename R, bool CG, bool MPQ, bool DIR = false>
+template <typename R, bool CG, bool MPQ, bool DIR = false, bool GRP = true>
 __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     k_spmv_tma(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
                const R* __restrict__ A, uint64_t ne, const R* __restrict__ p, R* __restrict__ q,
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     if (threadIdx.x == 0) {
         for (int s = 0; s < TMA_NS; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], TMA_CONSUMERS);
+            mbar_init(&empty_bar[s], GRP ? PCG_WPG : TMA_CONSUMERS);
         }
         mbar_fence_init();
     }
@@ -223,7 +223,12 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             }
         }
     } else {
-        const unsigned sub = lane & 15;
+        // GRP: consumer group g (warps 4g..4g+3) takes the chunks k = g mod 2,
+        // 8 lanes per vertex, two rows per lane per pass (both gathers in
+        // flight); else all 8 warps take every chunk, 16 lanes per vertex
+        const unsigned grp = GRP ? warp / PCG_WPG : 0u, wig = GRP ? warp % PCG_WPG : warp;
+        constexpr unsigned LPV = GRP ? 8u : 16u;
+        const unsigned sub = lane & (LPV - 1);
         // DIR (CG): p = z + beta p_old on the fly -- `p` holds z, p is double-buffered
         const R* __restrict__ pold = nullptr;
         R* __restrict__ pnew = nullptr;
@@ -235,12 +240,13 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             const double rho = scal[S_RHO], rz = scal[S_RZ];
             beta = (scal[S_FIRST] != 0.0 || rho == 0.0) ? R(0) : (R)(rz / rho);
         }
-        uint32_t k = 0;
-        for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++k) {
+        uint32_t k = grp;
+        for (uint64_t ch = blockIdx.x + (uint64_t)grp * gridDim.x; ch < nchunks;
+             ch += (uint64_t)gridDim.x * (GRP ? PCG_GROUPS : 1), k += (GRP ? PCG_GROUPS : 1)) {
             const int s = k % TMA_NS;
             const uint64_t v0 = ch * TMA_VCH;
             const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
-            const uint64_t v = v0 + 2 * warp + (lane >> 4);
+            const uint64_t v = GRP ? v0 + 4 * wig + (lane >> 3) : v0 + 2 * warp + (lane >> 4);
             const bool valid = v < v1;
             const uint32_t e0 = index[v0];
             const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
@@ -268,10 +274,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             mbar_wait(&full_bar[s], (k / TMA_NS) & 1u);
             const unsigned char* base = tma_smem + s * stage_bytes;
             const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
-            R a0 = 0, a1 = 0, a2 = 0;
-            for (uint32_t r = r0 + sub; r < r1; r += 16) {
-                const uint32_t hv = hs[r];
-                R px, py, pz;
+            auto gather = [&](uint32_t hv, R& px, R& py, R& pz) {
                 if (DIR) {
                     const auto zv = ld4(p, hv);
                     const auto ov = ld4(pold, hv);
@@ -288,23 +291,35 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                     py = p[3ull * hv + 1];
                     pz = p[3ull * hv + 2];
                 }
-                R av[9];
+            };
+            R a0 = 0, a1 = 0, a2 = 0;
+            constexpr unsigned STEP = GRP ? 2 * LPV : LPV;
+            for (uint32_t r = r0 + sub; r < r1; r += STEP) {
+                const uint32_t rr = r + LPV;
+                const bool two = GRP && rr < r1;
+                const uint32_t hv = hs[r], hw = two ? hs[rr] : hv;
+                R px, py, pz, qx = 0, qy = 0, qz = 0;
+                gather(hv, px, py, pz);
+                if (GRP) gather(hw, qx, qy, qz);
+                R av[9], bv[9];
 #pragma unroll
                 for (int c = 0; c < 9; ++c) {
                     const uint32_t off = (uint32_t)((c * ne + e0) & (AE - 1));
-                    av[c] = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R))[r + off];
+                    const R* pl = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R)) + off;
+                    av[c] = pl[r];
+                    bv[c] = two ? pl[rr] : R(0);
                 }
-                a0 += av[0] * px + av[1] * py + av[2] * pz;
-                a1 += av[3] * px + av[4] * py + av[5] * pz;
-                a2 += av[6] * px + av[7] * py + av[8] * pz;
+                a0 += av[0] * px + av[1] * py + av[2] * pz + (bv[0] * qx + bv[1] * qy + bv[2] * qz);
+                a1 += av[3] * px + av[4] * py + av[5] * pz + (bv[3] * qx + bv[4] * qy + bv[5] * qz);
+                a2 += av[6] * px + av[7] * py + av[8] * pz + (bv[6] * qx + bv[7] * qy + bv[8] * qz);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[s]);
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                a0 += __shfl_xor_sync(0xffffffffu, a0, o, 16);
-                a1 += __shfl_xor_sync(0xffffffffu, a1, o, 16);
-                a2 += __shfl_xor_sync(0xffffffffu, a2, o, 16);
+            for (int o = LPV / 2; o > 0; o >>= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, o, LPV);
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o, LPV);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o, LPV);
             }
             if (sub == 0 && valid) {
                 if (MPQ && !mk) a0 = a1 = a2 = 0;
@@ -1383,17 +1398,20 @@ ebb_status launch_tma(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, 
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * TMA_NS;
     if (smem > 200 * 1024) return EBB_E_SIZE;   // caller falls back to the register path
-    static thread_local size_t configured = 0;
-    if (smem > configured) {
-        EBB_CUDA(c, cudaFuncSetAttribute(k_spmv_tma<R, CG, MPQ, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-        configured = smem;
+    // consumer layout: grouped 8 lanes per vertex (default, measured faster:
+    // DESIGN.md §5.3); EBB_SPMV_GRP=0 selects 16 lanes per vertex
+    static const bool grp = !(getenv("EBB_SPMV_GRP") && getenv("EBB_SPMV_GRP")[0] == '0');
+    auto kern = grp ? k_spmv_tma<R, CG, MPQ, DIR, true> : k_spmv_tma<R, CG, MPQ, DIR, false>;
+    static thread_local size_t configured[2] = {0, 0};
+    if (smem > configured[grp]) {
+        EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured[grp] = smem;
     }
     const int block = 32 * (TMA_CONSUMERS + 1);
     const uint64_t nch = (G.nv + TMA_VCH - 1) / TMA_VCH;
-    const unsigned grid = occ_grid(c, k_spmv_tma<R, CG, MPQ, DIR>, block, smem, nch * block);
-    k_spmv_tma<R, CG, MPQ, DIR><<<grid, block, smem, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials,
-                                                          counter, pq_out, cap, pb0, pb1, scal);
+    const unsigned grid = occ_grid(c, kern, block, smem, nch * block);
+    kern<<<grid, block, smem, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials, counter, pq_out, cap,
+                                   pb0, pb1, scal);
     EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
 }

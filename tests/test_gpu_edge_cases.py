@@ -179,3 +179,41 @@ def test_plan_stats_and_cg_variant_queries(ctx):
     fem.cg.variant = A.CG_SAAD
     assert fem.cg_variant() == 1
     fem.cg.variant = A.CG_AUTO
+
+
+def test_widening_entry_points_refuse_bad_arguments(ctx):
+    """Argument checks of the §8(f) entry points: unknown rhs_form, a Newton
+    assembly without v_n, a consistent mass on the wrong relation, a negative
+    PCG tolerance, spring fields of mixed record shapes."""
+    import ctypes as C
+
+    from helpers import Case, gpu_fem
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200.ebb import EbbError
+    case = Case(n=3, model="nh")
+    fem = gpu_fem(ctx, case, name="badargs")
+    fem.map_forces("nh")
+    d = A.ImplicitDesc()
+    d.edges, d.K, d.A, d.self = fem.edges.h, fem.K.h, fem.K.h, fem.self_e.h
+    d.mass, d.f, d.vel, d.b = fem.mass.h, fem.f.h, fem.vel.h, fem.b.h
+    d.h = 1e-2
+    d.rhs_form, d.vel0 = 7, A.NONE
+    with pytest.raises(EbbError, match="EBB_E_ARG"):
+        ctx.check(ctx.L.ebb_implicit_assemble(ctx.h, C.byref(d), None))
+    d.rhs_form = A.RHS_NEWTON
+    with pytest.raises(EbbError):
+        ctx.check(ctx.L.ebb_implicit_assemble(ctx.h, C.byref(d), None))
+    wrong = fem.verts.field("me_wrong", "f64")                 # on verts, not on the edges
+    with pytest.raises(EbbError, match="EBB_E_TYPE"):
+        ctx.check(ctx.L.ebb_tetmesh_consistent_mass(ctx.h, fem.e.h, fem.W.h, 1e3, wrong.h, None))
+    fem.assemble(1e-2)
+    fem.cg_init()
+    fem.cg.tol = -1.0
+    with pytest.raises(EbbError, match="EBB_E_ARG"):
+        fem.cg_step(3)
+    fem.cg.tol = 0.0
+    from paper_1506_07577_b200.springmass import SpringMass
+    sm = SpringMass(fem, name="badsp")
+    f4 = fem.verts.field("f4", "f64", (4, 1))
+    with pytest.raises(EbbError, match="EBB_E_TYPE"):
+        ctx.check(ctx.L.ebb_spring_forces(ctx.h, fem.edges.h, sm.q.h, sm.rest_len.h, 1.0, f4.h, 0, None))

@@ -109,6 +109,7 @@ ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s);
 #define EBB_K_ASSEMBLE 4
 #define EBB_K_CG_SOLVE 5   /* persistent single-launch PCG (all iterations) */
 #define EBB_K_SPRING 6     /* Fig. 2 spring forces / fused spring step         */
+#define EBB_K_EBE_MATVEC 7 /* matrix-free element-by-element matvec            */
 ebb_status ebb_timing_enable(ebb_ctx ctx, int on);
 ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64_t* launches, int reset);
 /* Number of kernels this context has launched (all entry points). */
@@ -131,7 +132,8 @@ ebb_status ebb_graph_free(ebb_ctx ctx, int32_t graph);
 ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_rel* out);
 ebb_status ebb_relation_size(ebb_ctx ctx, ebb_rel rel, uint64_t* out);
 /* Library-allocated field; host_init (element-major, rows*cols per element)
- * or NULL for zeros.  Synchronous. */
+ * or NULL for zeros.  Shapes: rows, cols <= 4, or a column of up to 32 rows
+ * (per-element state records); EBB_E_SIZE otherwise.  Synchronous. */
 ebb_status ebb_field_new(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype dtype,
                          uint32_t rows, uint32_t cols, ebb_layout layout,
                          const void* host_init, ebb_field* out);
@@ -433,6 +435,20 @@ ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u,
 /* Newton iteration update (after an EBB_RHS_NEWTON solve): vel += dv;
  * u += h dv (keeps u = u_n + h vel). */
 ebb_status ebb_newton_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
+
+/* ---- matrix-free element-by-element matvec -----------
+ * q = sum_t K_t p_t, the product with the stiffness the element map would
+ * assemble (K = sum_t K_t on e[i][j]), from a compact per-tet state
+ * instead of the edge-relation matrix.  `d` supplies model, v, Dminv (and,
+ * for the state, u, W, mu, lam); f, K, e, energy, scatter are ignored.
+ * state: SOA field on tets, dtype of the map, 15x1 (NH: k_i = F^-T g_i,
+ * W mu, W c1, W lam) or 26x1 (StVK: h_i = F g_i, W S, W mu F F^T, W mu,
+ * W lam).  The matvec zeroes q and adds each element's 4 vec3 rows with
+ * red.global.add: equal to the assembled product up to summation
+ * order, not bitwise run-to-run.  Stream-ordered. */
+ebb_status ebb_tet_stiffness_state(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_field state, ebb_stream s);
+ebb_status ebb_ebe_matvec(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_field state, ebb_field p, ebb_field q,
+                          ebb_stream s);
 
 /* ---- Fig. 2 spring-mass program ------------
  * Query-loops over v.edges of a grouped edge relation (`edges`, grouped by

@@ -82,7 +82,10 @@ ebb_status add_field(Ctx* c, ebb_rel rel, const char* name, ebb_dtype dt, uint32
     Relation* R = get_rel(c, rel);
     if (!R) return fail(c, EBB_E_ARG, "bad relation handle %u", rel);
     if (!name || !*name) return fail(c, EBB_E_ARG, "field name is empty");
-    if (rows == 0 || cols == 0 || rows > 4 || cols > 4) return fail(c, EBB_E_SIZE, "field shape %ux%u", rows, cols);
+    // vectors/matrices up to 4x4 (Ebb's small types); column vectors up to 32
+    // rows (per-element state records, e.g. the 26-word StVK stiffness state)
+    if (rows == 0 || cols == 0 || cols > 4 || rows > (cols == 1 ? 32u : 4u))
+        return fail(c, EBB_E_SIZE, "field shape %ux%u", rows, cols);
     if (dtype_size(dt) == 0) return fail(c, EBB_E_ARG, "bad dtype %d", (int)dt);
     if (layout != EBB_AOS && layout != EBB_SOA) return fail(c, EBB_E_ARG, "bad layout");
     for (ebb_field f : R->fields)

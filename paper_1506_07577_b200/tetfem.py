@@ -143,6 +143,30 @@ class TetFEM:
         d.energy = self.energy.h if want_energy else A.NONE
         self.ctx.check(self.ctx.L.ebb_map_tet_forces(self.ctx.h, C.byref(d), _stream(stream)))
 
+    def _map_desc(self, model):
+        d = A.TetMapDesc()
+        d.model = MODELS[model]
+        d.v, d.e, d.u = self.v.h, self.e.h, self.u.h
+        d.Dminv, d.W, d.mu, d.lam = self.Dminv.h, self.W.h, self.mu.h, self.lam.h
+        d.f, d.K, d.energy = self.f.h, A.NONE, A.NONE
+        return d
+
+    def ebe_state(self, model="nh", stream=None):
+        """the compact per-tet stiffness state at the current u."""
+        words = 15 if model == "nh" else 26
+        key = f"ebe_state_{model}"
+        if getattr(self, key, None) is None:
+            setattr(self, key, self.tets.field(key, self.dtype, (words, 1), "soa"))
+        st = getattr(self, key)
+        self.ctx.check(self.ctx.L.ebb_tet_stiffness_state(self.ctx.h, C.byref(self._map_desc(model)), st.h,
+                                                          _stream(stream)))
+        return st
+
+    def ebe_matvec(self, state, p, q, model="nh", stream=None):
+        """q = sum_t K_t p_t (matrix-free)."""
+        self.ctx.check(self.ctx.L.ebb_ebe_matvec(self.ctx.h, C.byref(self._map_desc(model)), state.h, p.h, q.h,
+                                                 _stream(stream)))
+
     def matvec(self, Afield, p, q, mask=False, pq=None, stream=None):
         self.ctx.check(self.ctx.L.ebb_map_edge_matvec(self.ctx.h, self.edges.h, Afield.h, p.h, q.h,
                                                       self.free.h if mask else A.NONE,

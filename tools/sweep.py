@@ -228,6 +228,57 @@ def run_spring(sizes, reps, dtypes=("f64", "f32"), steps=50):
             del fem, sm
 
 
+def run_ebe(sizes, reps, dtypes=("f64", "f32"), model="nh"):
+    """matrix-free element-by-element matvec vs the assembled
+    edge-relation matvec on the same mesh and state (L2 flushed)."""
+    import numpy as np
+    import torch
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.tetfem import TetFEM
+
+    peak, src = bench._peaks()
+    flush = torch.empty(bench.FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    w = bench.WORKLOAD
+    for n in sizes:
+        X, tets, free, u0, mu, lam = bench.make_case(n, w["order_seed"], w["u_seed"], w["E"], w["nu"])
+        for dt in dtypes:
+            ctx = ebb.Context(0)
+            fem = TetFEM(ctx, X, tets, dtype=dt, mu=mu, lam=lam, rho=w["rho"], free=free, u=u0, name=f"ebe{n}{dt}")
+            fem.map_forces(model)
+            st = fem.ebe_state(model)
+            rng = np.random.default_rng(6)
+            P = fem.verts.field("p", dt, (3, 1), init=rng.uniform(-1, 1, size=(fem.nv, 3)))
+            Q = fem.verts.field("q", dt, (3, 1))
+            res = {}
+            for name, fn, kid in (("ebe", lambda: fem.ebe_matvec(st, P, Q, model=model), A.K_EBE_MATVEC),
+                                  ("assembled", lambda: fem.matvec(fem.K, P, Q), A.K_EDGE_MATVEC)):
+                fn()
+                torch.cuda.synchronize()
+                ctx.timing(True)
+                ctx.timing_read(kid, reset=True)
+                for _ in range(reps):
+                    _flush(flush)
+                    fn()
+                ms, nl = ctx.timing_read(kid, reset=True)
+                ctx.timing(False)
+                res[name] = 1e3 * ms / nl
+            bf = 4 if dt == "f32" else 8
+            words = 15 if model == "nh" else 26
+            b_ebe = fem.nt * (16 + (9 + words) * bf) + fem.nv * 6 * bf
+            b_asm = bench.bytes_matvec(fem.nv, fem.ne, bf)
+            print(json.dumps({"workload": "EBE vs assembled matvec", "model": model, "mesh": f"kuhn6 n={n}",
+                              "tets": fem.nt, "verts": fem.nv, "edge_rows": fem.ne, "dtype": dt,
+                              "ebe_us": res["ebe"], "assembled_us": res["assembled"],
+                              "ebe_algorithmic_bytes": b_ebe, "assembled_algorithmic_bytes": b_asm,
+                              "ebe_hbm_frac": b_ebe / (res["ebe"] * 1e-6) / 1e9 / peak,
+                              "assembled_hbm_frac": b_asm / (res["assembled"] * 1e-6) / 1e9 / peak,
+                              "peak_gbs": peak, "peak_source": src}), flush=True)
+            ctx.close()
+            del fem
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", action="store_true")
@@ -239,6 +290,7 @@ def main():
     ap.add_argument("--c4map", action="store_true", help="the map strategies on every --sizes Kuhn mesh")
     ap.add_argument("--c4cg", action="store_true", help="the PCG iteration on every --sizes Kuhn mesh")
     ap.add_argument("--spring", action="store_true", help="the Fig. 2 spring-mass step on every --sizes Kuhn mesh")
+    ap.add_argument("--ebe", action="store_true", help="matrix-free vs assembled matvec on every --sizes Kuhn mesh")
     ap.add_argument("--scatters", default="segmented,gather,tiled,atomic")
     ap.add_argument("--dtypes", default="f32,f64")
     ap.add_argument("--models", default="stvk,nh")
@@ -260,6 +312,8 @@ def main():
                    models=a.models.split(","))
     if a.c4cg:
         run_c4cg([int(x) for x in a.sizes.split(",")], a.reps)
+    if a.ebe:
+        run_ebe([int(x) for x in a.sizes.split(",")], a.reps, dtypes=a.dtypes.split(","))
     if a.spring:
         run_spring([int(x) for x in a.sizes.split(",")], a.reps, dtypes=a.dtypes.split(","))
 

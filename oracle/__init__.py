@@ -65,6 +65,9 @@ def lib():
             "orc_spring_forces": (None, [I, P, P, P, P, D, P]),
             "orc_spring_apply": (None, [I, P, D, P, P, P]),
             "orc_kinetic_energy": (D, [I, P, P]),
+            "orc_grid2_stencil": (None, [I, I, C.c_int, P, P, C.c_int, P, P]),
+            "orc_grid2_point_locate": (None, [I, I, I, P, P]),
+            "orc_grid2_particle_vel": (None, [I, I, C.c_int, P, I, P, P, P]),
             "orc_implicit_assemble_consistent": (None, [I, P, P, P, P, P, P, D, D, D, P, P, P]),
             "orc_pcg": (C.c_int, [I, P, P, P, P, P, C.c_int, P, P]),
             "orc_implicit_update": (None, [I, P, D, P, P]),
@@ -392,4 +395,29 @@ def spring_steps(row_ptr, head, rest_len, mass, K, dt, q, qd, steps):
         f = spring_forces(row_ptr, head, q, rest_len, K, f)
         q, qd, f = spring_apply(mass, dt, q, qd, f)
     return q, qd
+
+
+# ---------------------------------------------------------------- regular 2-D grid (Fig. 3)
+def grid2_stencil(nx, ny, field, offsets, weights):
+    """out[c] = sum_k w_k field[cell(i+dx_k, j+dy_k)] (periodic); field (nx*ny, comps)."""
+    f = _f64(field).reshape(nx * ny, -1)
+    out = np.empty_like(f)
+    off = _i64(np.asarray(offsets)).reshape(-1, 2)
+    lib().orc_grid2_stencil(nx, ny, f.shape[1], _p(f), _p(out), off.shape[0], _p(off), _p(_f64(weights)))
+    return out
+
+
+def grid2_point_locate(nx, ny, pos):
+    pos = _f64(pos).reshape(-1, 3)
+    d = np.empty(pos.shape[0], dtype=np.int64)
+    lib().orc_grid2_point_locate(nx, ny, pos.shape[0], _p(pos), _p(d))
+    return d
+
+
+def grid2_particle_vel(nx, ny, cell_vel, pos, dual):
+    cv = _f64(cell_vel).reshape(nx * ny, -1)
+    pos = _f64(pos).reshape(-1, 3)
+    vel = np.empty((pos.shape[0], cv.shape[1]))
+    lib().orc_grid2_particle_vel(nx, ny, cv.shape[1], _p(cv), pos.shape[0], _p(pos), _p(_i64(dual)), _p(vel))
+    return vel
 

@@ -701,3 +701,51 @@ double orc_kinetic_energy(int64_t nv, const double* mass, const double* qd) {
         E += 0.5 * mass[v] * (qd[3 * v] * qd[3 * v] + qd[3 * v + 1] * qd[3 * v + 1] + qd[3 * v + 2] * qd[3 * v + 2]);
     return E;
 }
+
+/* ------------------------------------------------------------------ */
+/* Regular 2-D grid domain (P:733-772 affine indexing; Fig. 3   */
+/* particle coupling).  nx x ny unit cells, cell (i, j)    */
+/* = [i, i+1) x [j, j+1), row-major id i + nx j, periodic (Stable Fluids).  */
+/* Dual cell (a, b) spans the cell centres (a+.5 .. a+1.5, b+.5 .. b+1.5);  */
+/* dual_cell.cell(dx, dy) = cell(a + dx, b + dy) (the affine map {{1,0,dx},*/
+/* {0,1,dy}}).  Readings: DESIGN.md §3 (22).                    */
+/* ------------------------------------------------------------------ */
+static int64_t orc_wrap(int64_t i, int64_t n) { int64_t r = i % n; return r < 0 ? r + n : r; }
+
+/* out[c] = sum_k w_k in[cell(i + dx_k, j + dy_k)], per component */
+void orc_grid2_stencil(int64_t nx, int64_t ny, int comps, const double* in, double* out, int npts,
+                       const int64_t* off, const double* w) {
+    for (int64_t j = 0; j < ny; ++j)
+        for (int64_t i = 0; i < nx; ++i)
+            for (int a = 0; a < comps; ++a) {
+                double s = 0.0;
+                for (int k = 0; k < npts; ++k)
+                    s += w[k] * in[comps * (orc_wrap(i + off[2 * k], nx) + nx * orc_wrap(j + off[2 * k + 1], ny)) + a];
+                out[comps * (i + nx * j) + a] = s;
+            }
+}
+
+/* PointLocate: the dual cell containing (x, y) */
+void orc_grid2_point_locate(int64_t nx, int64_t ny, int64_t np, const double* pos, int64_t* dual) {
+    for (int64_t p = 0; p < np; ++p) {
+        int64_t a = (int64_t)floor(pos[3 * p] - 0.5), b = (int64_t)floor(pos[3 * p + 1] - 0.5);
+        dual[p] = orc_wrap(a, nx) + nx * orc_wrap(b, ny);
+    }
+}
+
+/* update_particle_vel (Fig. 3): x1 = frac(x - 0.5), y1 = frac(y - 0.5),
+ * vel = x0 y0 cell(0,0) + x1 y0 cell(1,0) + x0 y1 cell(0,1) + x1 y1 cell(1,1) */
+void orc_grid2_particle_vel(int64_t nx, int64_t ny, int comps, const double* cell_vel, int64_t np,
+                            const double* pos, const int64_t* dual, double* vel) {
+    for (int64_t p = 0; p < np; ++p) {
+        double x1 = (pos[3 * p] - 0.5) - floor(pos[3 * p] - 0.5);
+        double y1 = (pos[3 * p + 1] - 0.5) - floor(pos[3 * p + 1] - 0.5);
+        double x0 = 1.0 - x1, y0 = 1.0 - y1;
+        int64_t a = dual[p] % nx, b = dual[p] / nx;
+        int64_t c00 = a + nx * b, c10 = orc_wrap(a + 1, nx) + nx * b;
+        int64_t c01 = a + nx * orc_wrap(b + 1, ny), c11 = orc_wrap(a + 1, nx) + nx * orc_wrap(b + 1, ny);
+        for (int k = 0; k < comps; ++k)
+            vel[comps * p + k] = x0 * y0 * cell_vel[comps * c00 + k] + x1 * y0 * cell_vel[comps * c10 + k]
+                               + x0 * y1 * cell_vel[comps * c01 + k] + x1 * y1 * cell_vel[comps * c11 + k];
+    }
+}

@@ -110,6 +110,7 @@ ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s);
 #define EBB_K_CG_SOLVE 5   /* persistent single-launch PCG (all iterations) */
 #define EBB_K_SPRING 6     /* Fig. 2 spring forces / fused spring step         */
 #define EBB_K_EBE_MATVEC 7 /* matrix-free element-by-element matvec            */
+#define EBB_K_GRID 8       /* regular-grid stencil / particle interpolation    */
 ebb_status ebb_timing_enable(ebb_ctx ctx, int on);
 ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64_t* launches, int reset);
 /* Number of kernels this context has launched (all entry points). */
@@ -435,6 +436,33 @@ ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u,
 /* Newton iteration update (after an EBB_RHS_NEWTON solve): vel += dv;
  * u += h dv (keeps u = u_n + h vel). */
 ebb_status ebb_newton_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
+
+/* ---- regular 2-D grid domain (Fig. 3)
+ * nx x ny unit cells, cell (i, j) = [i, i+1) x [j, j+1), row-major id
+ * i + nx j, periodic.  Keys between grid elements are affine maps of the
+ * indices ({{1,0,dx},{0,1,dy}}), computed, never stored.  Dual
+ * cell (a, b) spans the cell centres a+1/2..a+3/2, b+1/2..b+3/2 and its
+ * cell(dx, dy) is cell (a+dx, b+dy).  Readings: DESIGN.md §3 (22). */
+typedef struct { ebb_rel cells, dual_cells; } ebb_grid2;
+#define EBB_GRID2_MAX_STENCIL 16
+/* two relations of nx*ny rows: <name>.cells and <name>.dual_cells */
+ebb_status ebb_grid2_new(ebb_ctx ctx, const char* name, uint32_t nx, uint32_t ny, ebb_grid2* out);
+/* out[c] = sum_k weights[k] in[cell(i + offsets[2k], j + offsets[2k+1])]
+ * (periodic), per component; in, out: F32/F64 AOS fields of the same shape
+ * (<= 4 components) on `cells`, distinct (EBB_E_PHASE).  1..16 points.
+ * offsets/weights are host arrays (copied into the launch). */
+ebb_status ebb_grid2_stencil(ebb_ctx ctx, ebb_rel cells, ebb_field in, ebb_field out, int32_t npts,
+                             const int32_t* offsets, const double* weights, ebb_stream s);
+/* PointLocate: dual_cell[p] = (floor(x - 1/2) mod nx)
+ * + nx (floor(y - 1/2) mod ny), decided in fp64; pos: AOS vec3 F32/F64 on the
+ * particles (z ignored); dual_cell: scalar key-field particles -> dual cells. */
+ebb_status ebb_grid2_point_locate(ebb_ctx ctx, ebb_field pos, ebb_field dual_cell, ebb_stream s);
+/* Fig. 3 update_particle_vel: x1 = frac(x - 1/2), y1 = frac(y - 1/2),
+ * vel = x0 y0 c(0,0) + x1 y0 c(1,0) + x0 y1 c(0,1) + x1 y1 c(1,1) with c the
+ * dual cell's cells' cell_vel (AOS, 1..4 components, on the grid's cells);
+ * vel: same shape on the particles. */
+ebb_status ebb_grid2_particle_vel(ebb_ctx ctx, ebb_field dual_cell, ebb_field cell_vel, ebb_field pos,
+                                  ebb_field vel, ebb_stream s);
 
 /* ---- matrix-free element-by-element matvec -----------
  * q = sum_t K_t p_t, the product with the stiffness the element map would

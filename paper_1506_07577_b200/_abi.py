@@ -26,7 +26,8 @@ STVK, NH = 0, 1
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED, SCATTER_GATHER, SCATTER_SEGMENTED, SCATTER_COLOR = 0, 1, 2, 3, 4, 5
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
 CG_DIR, CG_MATVEC, CG_UPDATE = 0, 1, 2
-K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE, K_CG_SOLVE, K_SPRING, K_EBE_MATVEC = 0, 1, 2, 3, 4, 5, 6, 7
+K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE, K_CG_SOLVE, K_SPRING, K_EBE_MATVEC, K_GRID = \
+    0, 1, 2, 3, 4, 5, 6, 7, 8
 
 u32 = C.c_uint32
 ctx_t = C.c_void_p
@@ -56,6 +57,10 @@ class ImplicitDesc(C.Structure):
 
 
 RHS_LINEARISED, RHS_NEWTON = 0, 1
+
+
+class Grid2(C.Structure):
+    _fields_ = [("cells", u32), ("dual_cells", u32)]
 
 
 class CG(C.Structure):
@@ -136,6 +141,11 @@ SIGS = {
     "ebb_kinetic_energy": (S, [ctx_t, u32, u32, u32, stream_t]),
     "ebb_tet_stiffness_state": (S, [ctx_t, C.POINTER(TetMapDesc), u32, stream_t]),
     "ebb_ebe_matvec": (S, [ctx_t, C.POINTER(TetMapDesc), u32, u32, u32, stream_t]),
+    "ebb_grid2_new": (S, [ctx_t, C.c_char_p, C.c_uint32, C.c_uint32, C.POINTER(Grid2)]),
+    "ebb_grid2_stencil": (S, [ctx_t, u32, u32, u32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                              stream_t]),
+    "ebb_grid2_point_locate": (S, [ctx_t, u32, u32, stream_t]),
+    "ebb_grid2_particle_vel": (S, [ctx_t, u32, u32, u32, u32, stream_t]),
     "ebb_partition": (S, [ctx_t, u32, C.c_int32, u32, u32]),
     "ebb_cg_phase": (S, [ctx_t, C.POINTER(CG), C.c_int32, stream_t]),
     "ebb_rows_gather": (S, [ctx_t, u32, u32, u32, stream_t]),

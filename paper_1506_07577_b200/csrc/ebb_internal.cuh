@@ -39,6 +39,11 @@ struct Relation {
     ebb_field grouped_by = EBB_NONE;   // key-field this relation is grouped by
     ebb_field index = EBB_NONE;        // hidden CSR index on the source
     uint32_t max_group = 0;            // longest range of an index on this relation
+    // regular 2-D grid (ebb_grid2_new): dims, kind (1 = cells, 2 = dual cells)
+    // and the other relation of the same grid
+    uint32_t dims[2] = {0, 0};
+    int grid_kind = 0;
+    ebb_rel grid_peer = EBB_NONE;
 };
 
 // Scatter plan of the tiled element map (built once per mesh, tet_map.cu):

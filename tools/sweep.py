@@ -279,6 +279,54 @@ def run_ebe(sizes, reps, dtypes=("f64", "f32"), model="nh"):
             del fem
 
 
+def run_grid(reps, dtypes=("f32", "f64")):
+    """the 5-point periodic stencil on a 8192 x 8192 grid (vec2)
+    and Fig. 3 particle interpolation (16M particles), L2 flushed."""
+    import numpy as np
+    import torch
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.grid import Grid2
+
+    peak, src = bench._peaks()
+    flush = torch.empty(bench.FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    nx = ny = 8192
+    npart = 1 << 24
+    for dt in dtypes:
+        ctx = ebb.Context(0)
+        g = Grid2(ctx, nx, ny, name=f"g{dt}")
+        rng = np.random.default_rng(0)
+        fin = g.cells.field("in", dt, (2, 1), init=rng.standard_normal((nx * ny, 2)))
+        fout = g.cells.field("out", dt, (2, 1))
+        pos = np.zeros((npart, 3))
+        pos[:, 0] = rng.uniform(0, nx, npart)
+        pos[:, 1] = rng.uniform(0, ny, npart)
+        P, pf, key = g.particles(f"p{dt}", pos, dtype=dt)
+        vf = P.field("vel", dt, (2, 1))
+        bf = 4 if dt == "f32" else 8
+        runs = (("stencil5", lambda: g.stencil(fin, fout, [(0, 0), (1, 0), (-1, 0), (0, 1), (0, -1)],
+                                               [-4.0, 1.0, 1.0, 1.0, 1.0]), nx * ny * 2 * bf * 2),
+                ("particle_vel", lambda: g.particle_vel(key, fin, pf, vf),
+                 npart * (3 * bf + 4 + 2 * bf) + nx * ny * 2 * bf))
+        for name, fn, b in runs:
+            fn()
+            torch.cuda.synchronize()
+            ctx.timing(True)
+            ctx.timing_read(A.K_GRID, reset=True)
+            for _ in range(reps):
+                _flush(flush)
+                fn()
+            ms, nl = ctx.timing_read(A.K_GRID, reset=True)
+            ctx.timing(False)
+            us = 1e3 * ms / nl
+            print(json.dumps({"workload": f"grid2 {name}", "grid": f"{nx}x{ny}", "particles": npart,
+                              "dtype": dt, "us": us, "algorithmic_bytes": b,
+                              "hbm_frac": b / (us * 1e-6) / 1e9 / peak, "peak_gbs": peak,
+                              "peak_source": src}), flush=True)
+        ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3", action="store_true")
@@ -291,6 +339,7 @@ def main():
     ap.add_argument("--c4cg", action="store_true", help="the PCG iteration on every --sizes Kuhn mesh")
     ap.add_argument("--spring", action="store_true", help="the Fig. 2 spring-mass step on every --sizes Kuhn mesh")
     ap.add_argument("--ebe", action="store_true", help="matrix-free vs assembled matvec on every --sizes Kuhn mesh")
+    ap.add_argument("--grid", action="store_true", help="2-D grid stencil and particle interpolation")
     ap.add_argument("--scatters", default="segmented,gather,tiled,atomic")
     ap.add_argument("--dtypes", default="f32,f64")
     ap.add_argument("--models", default="stvk,nh")
@@ -312,6 +361,8 @@ def main():
                    models=a.models.split(","))
     if a.c4cg:
         run_c4cg([int(x) for x in a.sizes.split(",")], a.reps)
+    if a.grid:
+        run_grid(a.reps, dtypes=a.dtypes.split(","))
     if a.ebe:
         run_ebe([int(x) for x in a.sizes.split(",")], a.reps, dtypes=a.dtypes.split(","))
     if a.spring:

@@ -186,7 +186,9 @@ ebb_status ebb_group_index(ebb_ctx ctx, ebb_rel rel, ebb_field* index_out);
  * Synchronous. */
 ebb_status ebb_renumber_morton(ebb_ctx ctx, ebb_rel rel, ebb_field pos);
 /* Sort `rel` lexicographically by the ascending-sorted tuple of its rows x 1
- * key-field `keys` (tets by their vertex ids), stable.  Synchronous. */
+ * key-field `keys` (1..4 keys per row: tets by their vertex ids, particles by
+ * their dual cell), stable.  Permutes rel's fields, remaps inbound keys.
+ * Synchronous. */
 ebb_status ebb_sort_by_key_tuple(ebb_ctx ctx, ebb_rel rel, ebb_field keys);
 
 /* ---- tetrahedral mesh domain --------- */

@@ -130,13 +130,13 @@ __global__ void k_invert(const uint32_t* __restrict__ n2o, uint32_t* __restrict_
 
 // sorted 4-tuple component k of tet t (ascending vertex ids), gathered by perm
 __global__ void k_tuple_key(const uint32_t* __restrict__ tv, const uint32_t* __restrict__ perm, uint64_t nt, int k,
-                            uint32_t* __restrict__ key) {
+                            uint32_t* __restrict__ key, int nc) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= nt) return;
     uint64_t t = perm[i];
     uint32_t s[4];
-    for (int j = 0; j < 4; ++j) s[j] = tv[4 * t + j];
-    for (int a = 1; a < 4; ++a)
+    for (int j = 0; j < nc; ++j) s[j] = tv[(uint64_t)nc * t + j];
+    for (int a = 1; a < nc; ++a)
         for (int b = a; b > 0 && s[b - 1] > s[b]; --b) {
             uint32_t q = s[b];
             s[b] = s[b - 1];
@@ -345,8 +345,11 @@ ebb_status ebb_renumber_morton(ebb_ctx ctx, ebb_rel rel, ebb_field pos) {
 ebb_status ebb_sort_by_key_tuple(ebb_ctx ctx, ebb_rel rel, ebb_field keys) {
     Ctx* c = (Ctx*)ctx;
     if (!c) return EBB_E_ARG;
-    Field* V;
-    EBB_TRY(check_tets_v(c, keys, &V));
+    Field* V = get_field(c, keys);
+    if (!V) return fail(c, EBB_E_ARG, "bad key-field handle");
+    if (V->dtype != EBB_KEY || V->comps() < 1 || V->comps() > 4 || V->layout != EBB_AOS)
+        return fail(c, EBB_E_TYPE, "'%s' must be a key-field of 1..4 keys per row", V->name.c_str());
+    const int nc = (int)V->comps();
     if (V->rel != rel) return fail(c, EBB_E_TYPE, "key-field is not on the relation being sorted");
     uint64_t nt = c->rels[rel].size;
     uint64_t ntarget = c->rels[V->key_target].size;
@@ -364,9 +367,9 @@ ebb_status ebb_sort_by_key_tuple(ebb_ctx ctx, ebb_rel rel, ebb_field keys) {
                                     (uint32_t*)perm2.p, (int)nt, 0, end_bit);
     EBB_CUDA(c, cudaMalloc(&tmp.p, tb));
     // LSD over the sorted tuple: least significant component first, stable
-    for (int k = 3; k >= 0; --k) {
+    for (int k = nc - 1; k >= 0; --k) {
         k_tuple_key<<<grid_for(nt, 256), 256>>>((const uint32_t*)V->ptr, (const uint32_t*)perm.p, nt, k,
-                                                (uint32_t*)key.p);
+                                                (uint32_t*)key.p, nc);
         EBB_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp.p, tb, (const uint32_t*)key.p, (uint32_t*)key2.p,
                                                     (const uint32_t*)perm.p, (uint32_t*)perm2.p, (int)nt, 0, end_bit));
         std::swap(perm.p, perm2.p);

@@ -42,6 +42,10 @@ class Grid2:
         self.point_locate(pf, key)
         return P, pf, key
 
+    def sort_particles(self, particles, dual_cell):
+        """Reorder the particle relation by dual cell (stable): coherent gathers."""
+        self.ctx.check(self.ctx.L.ebb_sort_by_key_tuple(self.ctx.h, particles.h, dual_cell.h))
+
     def point_locate(self, pos, dual_cell, stream=None):
         self.ctx.check(self.ctx.L.ebb_grid2_point_locate(self.ctx.h, pos.h, dual_cell.h, _stream(stream)))
 

@@ -84,3 +84,24 @@ def test_grid_arguments_are_checked(ctx):
         g.stencil(a, b, [(1, 0)], [1.0])
     with pytest.raises(EbbError, match="EBB_E_ARG"):
         g.stencil(a, g.cells.field("c", "f64"), [(0, 0)] * 17, [1.0] * 17)
+
+
+def test_sorted_particles_keep_their_data(ctx):
+    """ebb_sort_by_key_tuple on a 1-key field: particles reordered by dual
+    cell (stable), every field permuted with them."""
+    from paper_1506_07577_b200.grid import Grid2
+    nx, ny, npart = 16, 12, 5000
+    g = Grid2(ctx, nx, ny, name="gsort")
+    rng = np.random.default_rng(9)
+    pos = np.zeros((npart, 3))
+    pos[:, 0] = rng.uniform(0, nx, npart)
+    pos[:, 1] = rng.uniform(0, ny, npart)
+    pos[:, 2] = np.arange(npart)                          # the original index rides along in z
+    P, pf, key = g.particles("psort", pos)
+    g.sort_particles(P, key)
+    k = key.read().astype(np.int64).ravel()
+    p2 = pf.read().reshape(npart, 3)
+    ref = oracle.grid2_point_locate(nx, ny, pos)
+    order = np.argsort(ref, kind="stable")
+    assert np.array_equal(k, ref[order])
+    assert np.array_equal(p2[:, 2].astype(np.int64), order)

@@ -309,7 +309,12 @@ def run_grid(reps, dtypes=("f32", "f64")):
                                                [-4.0, 1.0, 1.0, 1.0, 1.0]), nx * ny * 2 * bf * 2),
                 ("particle_vel", lambda: g.particle_vel(key, fin, pf, vf),
                  npart * (3 * bf + 4 + 2 * bf) + nx * ny * 2 * bf))
+        def sorted_vel():
+            g.particle_vel(key, fin, pf, vf)
+        runs = runs + (("particle_vel_sorted", sorted_vel, npart * (3 * bf + 4 + 2 * bf) + nx * ny * 2 * bf),)
         for name, fn, b in runs:
+            if name == "particle_vel_sorted":
+                g.sort_particles(P, key)            # particles in dual-cell order
             fn()
             torch.cuda.synchronize()
             ctx.timing(True)

@@ -153,6 +153,9 @@ __global__ void __launch_bounds__(256) k_spring_step(uint64_t nv, const uint32_t
 // with coalesced loads, then thread = vertex walks its rows there (only the
 // q gathers go to L2).  STEP: the fused iteration (else forces only).
 #define SPRING_SB 128
+#ifndef SPRING_B
+#define SPRING_B 4      // rows gathered together per thread
+#endif
 template <typename R>
 struct SpV4;
 template <>
@@ -226,18 +229,29 @@ __global__ void __launch_bounds__(SPRING_SB) k_spring_staged(uint64_t nv, const 
     __syncthreads();
     if (!live) return;
     R s0 = 0, s1 = 0, s2 = 0;
-#pragma unroll 4
-    for (uint32_t r = r0; r < r1; ++r) {
-        const uint64_t h = hs[r];
-        const R L = ls[r];
-        R qh0, qh1, qh2;
-        ld_rec<R, QS>(q, h, qh0, qh1, qh2);
-        const R d0 = qh0 - qv[0], d1 = qh1 - qv[1], d2 = qh2 - qv[2];
-        const R len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-        const R c = len > R(0) ? L / len : R(0);
-        s0 += K * (c * d0 - d0);
-        s1 += K * (c * d1 - d1);
-        s2 += K * (c * d2 - d2);
+    // batches of SPRING_B rows: every gather of a batch is issued before the
+    // first sqrt / division (whose slow-path branches end the scheduler's
+    // basic block), so SPRING_B gathers are in flight per thread
+    constexpr int B = SPRING_B;
+    for (uint32_t rb = r0; rb < r1; rb += B) {
+        R qh[B][3], Lb[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const uint32_t r = rb + u < r1 ? rb + u : r1 - 1;   // (a repeated row is masked below)
+            Lb[u] = ls[r];
+            ld_rec<R, QS>(q, (uint64_t)hs[r], qh[u][0], qh[u][1], qh[u][2]);
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const R d0 = qh[u][0] - qv[0], d1 = qh[u][1] - qv[1], d2 = qh[u][2] - qv[2];
+            const R len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+            const R c = len > R(0) ? Lb[u] / len : R(0);
+            if (rb + u < r1) {
+                s0 += K * (c * d0 - d0);
+                s1 += K * (c * d1 - d1);
+                s2 += K * (c * d2 - d2);
+            }
+        }
     }
     const R f[3] = {s0, s1, s2};
     if (STEP) {

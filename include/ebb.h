@@ -502,7 +502,9 @@ ebb_status ebb_spring_apply(ebb_ctx ctx, ebb_field mass, double dt, ebb_field q,
 /* One whole Fig. 2 iteration in ONE kernel: forces from q_in kept in
  * registers, then applyForces writing q_out (q double-buffered: neighbours
  * read q while its owner would write it) and qd; force (nullable) receives
- * the forces.  q_in, q_out, qd, force distinct. */
+ * the forces.  q_in, q_out, qd, force distinct.  Records are vec3 (3x1) or
+ * padded (4x1); padded records need the row-staged kernel, which refuses
+ * (EBB_E_RANGE) a vertex with more edge rows than fit shared memory. */
 ebb_status ebb_spring_step(ebb_ctx ctx, ebb_rel edges, ebb_field q_in, ebb_field q_out, ebb_field qd,
                            ebb_field rest_len, ebb_field mass, double K, double dt, ebb_field force,
                            ebb_stream s);

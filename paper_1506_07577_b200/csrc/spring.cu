@@ -326,6 +326,9 @@ template <typename R, bool STEP>
 ebb_status launch_staged(Ctx* c, const EdgeGraph& G, int qs, const R* q, const R* rest, const R* mass, R K, R dt,
                          R* qout, R* qd, R* force, int accumulate, cudaStream_t s) {
     const size_t smem = (size_t)SPRING_SB * (G.max_group ? G.max_group : 1) * (sizeof(R) + 4) + 16;
+    if (smem > 200 * 1024)
+        return fail(c, EBB_E_RANGE, "spring: a vertex with %u edge rows needs %zu B of shared memory for the staged "
+                    "kernel (padded records have no register-path fallback; use vec3 fields)", G.max_group, smem);
     auto kern = qs == 4 ? k_spring_staged<R, STEP, 4> : k_spring_staged<R, STEP, 3>;
     if (smem > 48 * 1024)
         EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

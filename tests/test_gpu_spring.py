@@ -103,3 +103,37 @@ def test_phase_violation_is_refused(ctx):
     with pytest.raises(EbbError, match="EBB_E_PHASE"):
         ctx.check(L.ebb_spring_step(h, fem.edges.h, sm.q.h, sm.q.h, sm.qd.h, sm.rest_len.h, sm.mass.h,
                                     1.0, 1e-4, 0xFFFFFFFF, None))
+
+
+def _fan(k):
+    ang = 2 * np.pi * np.arange(k) / k
+    ring = np.stack([np.cos(ang), np.sin(ang), np.zeros(k)], 1)
+    X = np.vstack([[0.0, 0.0, 0.0], [0.0, 0.0, 1.0], ring])
+    tets = np.array([[0, 2 + i, 2 + (i + 1) % k, 1] for i in range(k)], dtype=np.int64)
+    d = np.einsum("ij,ij->i", X[tets[:, 1]] - X[tets[:, 0]],
+                  np.cross(X[tets[:, 2]] - X[tets[:, 0]], X[tets[:, 3]] - X[tets[:, 0]]))
+    tets[d < 0] = tets[d < 0][:, [0, 1, 3, 2]]
+    return X, tets
+
+
+def test_high_degree_vertex(ctx):
+    """A hub vertex with ~1200 edge rows: the vec3 fused step falls back to
+    the thread-per-vertex register path (parity with the oracle); padded
+    records refuse with EBB_E_RANGE instead of overflowing shared memory."""
+    from paper_1506_07577_b200.ebb import EbbError
+    from paper_1506_07577_b200.springmass import SpringMass
+    from paper_1506_07577_b200.tetfem import TetFEM
+    X, tets = _fan(600)
+    fem = TetFEM(ctx, X, tets, name="spfan")
+    m = oracle.Mesh(*[a for a in (fem.pos.read().reshape(-1, 3), fem.v.read().astype(np.int64).reshape(-1, 4))])
+    rng = np.random.default_rng(4)
+    q_st = m.X + rng.uniform(-0.01, 0.01, m.X.shape)
+    sm = SpringMass(fem, K=-1.0, dt=1e-4, q=fem.to_input_order(q_st), name="spfan")
+    L = oracle.spring_init_len(m.tail, m.head, m.X)
+    qr, qdr = oracle.spring_steps(m.row_ptr, m.head, L, fem.mass.read().ravel(), -1.0, 1e-4, q_st,
+                                  np.zeros_like(q_st), 5)
+    for _ in range(5):
+        sm.step()
+    assert rel_l2(sm.read_q(), qr) <= 1e-12
+    with pytest.raises(EbbError, match="EBB_E_RANGE"):
+        SpringMass(fem, padded=True, name="spfan4").step()

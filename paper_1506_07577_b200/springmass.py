@@ -100,6 +100,20 @@ class SpringMass:
                                     _stream(stream)))
         self.q, self.q2 = self.q2, self.q
 
+    def run(self, nsteps, stream):
+        """`nsteps` fused iterations replayed from a CUDA graph of two steps
+        (launch-bound small meshes); `stream` must be a non-default stream
+        (a torch.cuda.Stream or a raw handle).  Same kernels as step()."""
+        if getattr(self, "_graph", None) is None or self._graph[1] != id(stream):
+            self.ctx.graph_begin(stream)
+            self.step(stream=stream)
+            self.step(stream=stream)                     # (two swaps: q and q2 back in place)
+            self._graph = (self.ctx.graph_end(stream), id(stream))
+        for _ in range(nsteps // 2):
+            self.ctx.graph_launch(self._graph[0], stream)
+        if nsteps % 2:
+            self.step(stream=stream)
+
     def kinetic_energy(self, stream=None):
         L, h = self.ctx.L, self.ctx.h
         self._chk(L.ebb_kinetic_energy(h, self.mass.h, self.qd.h, self.energy.h, _stream(stream)))

@@ -137,3 +137,20 @@ def test_high_degree_vertex(ctx):
     assert rel_l2(sm.read_q(), qr) <= 1e-12
     with pytest.raises(EbbError, match="EBB_E_RANGE"):
         SpringMass(fem, padded=True, name="spfan4").step()
+
+
+def test_graph_replay_equals_steps(ctx):
+    """SpringMass.run (a CUDA graph of two fused steps, replayed) gives
+    bitwise the same state as the same number of step() calls."""
+    import torch
+    from paper_1506_07577_b200.springmass import SpringMass
+    sm1, fem1, m, L, q, qd = _setup(ctx, "f64", "spg1", K=-1.5)
+    # same mesh (same atomically-summed lumped mass), same start
+    sm2 = SpringMass(fem1, K=-1.5, dt=1e-4, q=fem1.to_input_order(q), qd=fem1.to_input_order(qd), name="spg2")
+    for _ in range(21):
+        sm1.step()
+    st = torch.cuda.Stream()
+    sm2.run(21, st)
+    st.synchronize()
+    assert np.array_equal(sm1.read_q(), sm2.read_q())
+    assert np.array_equal(sm1.read_qd(), sm2.read_qd())

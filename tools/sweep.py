@@ -197,8 +197,10 @@ def run_spring(sizes, reps, dtypes=("f64", "f32"), steps=50):
             V, E = fem.nv, fem.ne
             b_fused = E * (4 + bf) + V * 13 * bf            # head, rest_len; q r + q' w, qd r/w, mass
             b_paper = (E * (4 + bf) + V * 6 * bf) + V * 16 * bf
-            for mode in ("fused", "paper"):
-                fn = sm.step if mode == "fused" else sm.step_paper
+            gst = torch.cuda.Stream()
+            for mode in ("fused", "paper", "fused_graph"):
+                fn = {"fused": sm.step, "paper": sm.step_paper,
+                      "fused_graph": (lambda: sm.run(2, gst))}[mode]
                 for _ in range(5):
                     fn()
                 torch.cuda.synchronize()
@@ -206,17 +208,20 @@ def run_spring(sizes, reps, dtypes=("f64", "f32"), steps=50):
                 for warm in (True, False):
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     tot = 0.0
+                    per = (2 if mode == "fused_graph" else 1)          # steps per fn() call
                     for _ in range(reps):
                         if not warm:
                             _flush(flush)
-                        a.record()
+                        cs = gst if mode == "fused_graph" else torch.cuda.current_stream()
+                        cs.wait_stream(torch.cuda.current_stream())
+                        a.record(cs)
                         for _ in range(steps if warm else 1):
                             fn()
-                        b.record()
+                        b.record(cs)
                         torch.cuda.synchronize()
                         tot += a.elapsed_time(b)
-                    res["l2_warm" if warm else "l2_flushed"] = 1e3 * tot / (reps * (steps if warm else 1))
-                bb = b_fused if mode == "fused" else b_paper
+                    res["l2_warm" if warm else "l2_flushed"] = 1e3 * tot / (reps * (steps if warm else 1) * per)
+                bb = b_paper if mode == "paper" else b_fused
                 print(json.dumps({"workload": "spring-mass (Fig. 2)", "mode": mode, "mesh": f"kuhn6 n={n}",
                                   "verts": V, "edge_rows": E, "dtype": dt,
                                   "step_us_back_to_back": res["l2_warm"], "step_us_l2_flushed": res["l2_flushed"],

@@ -396,6 +396,16 @@ ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream 
 #define EBB_CG_DIR 0
 #define EBB_CG_MATVEC 1
 #define EBB_CG_UPDATE 2
+/* Single-reduction PCG in phase mode ("one fused 2-scalar
+ * allreduce if a single-reduction CG variant is adopted"): each call runs one
+ * phase of the Chronopoulos-Gear recurrences (the first call after
+ * ebb_cg_init forms w_0 = A z_0) and leaves the rank-local w.z and r.z in
+ * scal slots 10 and 11; the caller allreduces those two slots and refreshes
+ * the ghost rows of both u buffers (ebb_cg.u, ebb_cg.u2) -- and of z before
+ * the first call -- then calls again: iters iterations = iters + 1 calls.
+ * Needs ebb_cg_init with EBB_CG_SINGLE_REDUCTION.  The tolerance (ebb_cg.tol)
+ * is honoured once the initial r.z (slots 0-2 and 7) has been summed. */
+#define EBB_CG_SR_PHASE 3
 ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream s);
 
 /* ---- halo support ------------------------------------- */

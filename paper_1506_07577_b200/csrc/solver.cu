@@ -29,7 +29,10 @@ using namespace ebb;
 namespace {
 
 enum { S_RHO = 0, S_PQ = 1, S_RZ = 2, S_FIRST = 3, S_PAR = 4, S_ALPHA = 5, S_VAR = 6, S_RZ0 = 7, S_ITERS = 8,
-       S_DONE = 9, S_NSCAL = 12 };
+       S_DONE = 9, S_DSUM = 10, S_GSUM = 11, S_NSCAL = 12 };
+// S_VAR: single-reduction phase scalars pending (multi-GPU phase mode): 0 none,
+// 1 after the prologue, 2 after an iteration; S_DSUM / S_GSUM hold the
+// rank-local w.z / r.z sums the host allreduces between phases
 
 template <typename R>
 struct V4;
@@ -922,7 +925,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                      double* __restrict__ part_g, double* __restrict__ part_d, unsigned int* __restrict__ bar_count,
                      unsigned int* __restrict__ bar_gen, double* __restrict__ scal, double* __restrict__ rho_user,
                      unsigned long long* __restrict__ err, uint32_t cap, int iters,
-                     double tol2) {
+                     double tol2, int dist) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
     __shared__ __align__(8) uint64_t full_bar[CG1_NS], empty_bar[CG1_NS];
     __shared__ double sm_tot;
@@ -949,6 +952,32 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     if (scal[S_DONE] != 0.0) iters = 0;       // converged in an earlier call (tolerance mode)
     int done_it = 0, done_ph = 0;
     bool conv = false;
+    if (dist && scal[S_VAR] != 0.0 && scal[S_DONE] == 0.0) {
+        // multi-GPU phase mode: finish the previous phase's scalar recurrences
+        // from the globally summed (allreduced) w.z and r.z -- the same
+        // formulas as below, every CTA reads the same slots
+        const double dsum = scal[S_DSUM];
+        if (scal[S_VAR] == 1.0) {
+            if (blockIdx.x == 0 && threadIdx.x == 0 && dsum < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+            alpha = dsum != 0.0 ? gam / dsum : 0.0;
+            beta = 0.0;
+            first = 0;
+        } else {
+            const double gnew = scal[S_GSUM];
+            const double bn = gam != 0.0 ? gnew / gam : 0.0;
+            const double den = dsum - (alpha != 0.0 ? bn * gnew / alpha : 0.0);
+            if (blockIdx.x == 0 && threadIdx.x == 0 && den < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+            alpha = den != 0.0 ? gnew / den : 0.0;
+            beta = bn;
+            gam = gnew;
+            par ^= 1;
+            if (blockIdx.x == 0 && threadIdx.x == 0) *rho_user = gam;
+            if (tol2 > 0.0 && gam <= tol2 * rz0) {
+                conv = true;
+                iters = 0;
+            }
+        }
+    }
     uint64_t issued = 0;
     auto issue = [&](uint64_t ch, uint64_t seq) {
         const int s = seq % CG1_NS;
@@ -977,7 +1006,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         }
         bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
     };
-    const int nphase = iters + (first && iters > 0 ? 1 : 0);
+    const int nphase = dist ? (iters > 0 ? 1 : 0) : iters + (first && iters > 0 ? 1 : 0);
     if (warp == TMA_CONSUMERS && lane == 0 && nphase > 0)
         for (uint64_t j = 0; j < my_chunks && j < CG1_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
     for (int ph = 0; ph < nphase; ++ph) {
@@ -1092,6 +1121,19 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         }
         grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         const double dsum = grid_sum_partials(part_d, gridDim.x, &sm_tot);
+        if (dist) {
+            // phase mode: publish the rank-local sums; the recurrences finish
+            // at the next launch, after the host's allreduce of S_DSUM..S_GSUM
+            const double gl = pro ? 0.0 : grid_sum_partials(part_g, gridDim.x, &sm_tot);
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                scal[S_DSUM] = dsum;
+                scal[S_GSUM] = gl;
+                scal[S_VAR] = pro ? 1.0 : 2.0;
+            }
+            ++done_ph;
+            if (!pro) ++done_it;
+            break;
+        }
         if (pro) {
             // a_0 = g_0 / (p_0 . A p_0), p_0 = z_0
             if (blockIdx.x == 0 && threadIdx.x == 0 && dsum < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
@@ -1125,6 +1167,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         scal[S_ITERS] += (double)done_it;
         if (conv) scal[S_DONE] = 1.0;
+        if (dist && done_ph == 0) scal[S_VAR] = 0.0;   // pending scalars consumed, no new phase
         scal[S_RHO] = gam;
         scal[S_RZ] = gam;
         scal[S_ALPHA] = alpha;
@@ -1182,6 +1225,7 @@ __global__ void __launch_bounds__(256) k_cg_init(uint64_t nv, const uint32_t* __
         scal[S_RZ0] = tot;
         scal[S_ITERS] = 0.0;
         scal[S_DONE] = 0.0;
+        scal[S_VAR] = 0.0;
         if (rho_user) *rho_user = tot;
     }
 }
@@ -1595,7 +1639,7 @@ ebb_status cg_sym_prepare(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, cudaStre
 }
 
 template <typename R>
-ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s) {
+ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, cudaStream_t s, int dist = 0) {
     for (ebb_field f : {cg->s, cg->y, cg->w, cg->u, cg->u2})
         if (!get_field(c, f)) return fail(c, EBB_E_STATE, "cg: single-reduction work vectors missing (ebb_cg_init "
                                                            "with this variant first)");
@@ -1635,7 +1679,7 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
                                    F(cg->p), F(cg->s), F(cg->y), F(cg->w), F(cg->u), F(cg->u2), mask, c->d_partials,
                                    c->d_partials + 4096, c->d_counter + 10, c->d_counter + 11,
                                    (double*)c->fields[cg->scal].ptr, (double*)c->fields[cg->rho].ptr, c->d_err, cap,
-                                   iters, cg_tol2(cg)));
+                                   iters, cg_tol2(cg), dist));
     return EBB_OK;
 }
 
@@ -1656,6 +1700,7 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     const unsigned ug = occ_grid(c, k_cg_update<R>, 256, 0, G.nv);
     const int variant = cg_variant(cg, G.nv, sizeof(R) == 8 ? EBB_F64 : EBB_F32);
     if (only_phase < 0 && iters > 0 && variant == EBB_CG_SINGLE_REDUCTION) return cg1_launch<R>(c, cg, G, iters, s);
+    if (only_phase == EBB_CG_SR_PHASE) return cg1_launch<R>(c, cg, G, 1, s, 1);
     if (only_phase < 0 && iters > 0 && variant == EBB_CG_SYMMETRIC) return cg_sym_launch<R>(c, cg, G, iters, s);
     const char* mode = getenv("EBB_CG");
     if (only_phase < 0 && iters > 0 && !(mode && mode[0] == '2')) {
@@ -1995,7 +2040,7 @@ ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream 
 ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
     if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");
-    if (phase < EBB_CG_DIR || phase > EBB_CG_UPDATE) return fail(c, EBB_E_ARG, "unknown CG phase %d", phase);
+    if (phase < EBB_CG_DIR || phase > EBB_CG_SR_PHASE) return fail(c, EBB_E_ARG, "unknown CG phase %d", phase);
     EdgeGraph G;
     ebb_dtype dt;
     EBB_TRY(cg_validate(c, cg, &G, &dt));

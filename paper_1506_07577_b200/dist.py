@@ -26,6 +26,8 @@ from __future__ import annotations
 import numpy as np
 
 SLOT_RHO, SLOT_PQ, SLOT_RZ = 0, 1, 2
+SLOT_RZ0, SLOT_DSUM, SLOT_GSUM = 7, 10, 11      # (solver.cu scalar slots)
+CG_SR_PHASE = 3                                  # EBB_CG_SR_PHASE
 
 
 # ----------------------------------------------------------------------------- plans
@@ -165,8 +167,36 @@ class LocalTransport:
 
 
 # ----------------------------------------------------------------------------- driver
-def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0)):
-    """One distributed implicit step (O9 + O10) over `ranks` (the local ones)."""
+def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0),
+                  variant="saad"):
+    """One distributed implicit step (O9 + O10) over `ranks` (the local ones).
+
+    variant="saad": per iteration DIR, MATVEC, [sum p.q], UPDATE, [sum r.z,
+    z halo] -- two scalar allreduces.  variant="single": the single-reduction
+    (Chronopoulos-Gear) recurrences in phase mode, per iteration ONE phase,
+    ONE fused allreduce of (w.z, r.z) and the halo of the gathered operand u
+    (SURVEY §8(e)); iters iterations = iters + 1 phases (w_0 = A z_0 first)."""
+    if variant == "single":
+        for R in ranks:
+            R.map_assemble(model, h, alpha, beta, g)
+            R.cg_init(single=True)
+        transport.allreduce(ranks, (SLOT_RHO, SLOT_RZ + 1))
+        transport.allreduce(ranks, (SLOT_RZ0, SLOT_RZ0 + 1))
+        for R in ranks:
+            R.set_halo("z")
+        transport.exchange(ranks)
+        for _ in range(iters + 1):
+            for R in ranks:
+                R.cg_phase(CG_SR_PHASE)
+            transport.allreduce(ranks, (SLOT_DSUM, SLOT_GSUM + 1))
+            for which in ("u", "u2"):
+                for R in ranks:
+                    R.set_halo(which)
+                transport.exchange(ranks)
+        for R in ranks:
+            R.set_halo("z")
+            R.finish(h)
+        return
     for R in ranks:
         R.map_assemble(model, h, alpha, beta, g)
         R.cg_init()
@@ -222,9 +252,13 @@ class GpuRank:
         stored[order] = np.arange(order.size)
         self.stored_of_input = stored
         self.owned_stored = owned[order]
-        self.fem.cg_init(stream)                       # allocates the CG work fields
+        # allocates every CG work field (the single-reduction set includes u, u2)
+        self.fem.cg_init(stream, variant=A.CG_SINGLE_REDUCTION)
         self.z_field = self._field(self.fem.cg.z, 4)
-        self.scal = self._field(self.fem.cg.scal, 1, count=8, dt="f64").tensor()
+        self.halo_fields = {"z": self.z_field, "u": self._field(self.fem.cg.u, 4),
+                            "u2": self._field(self.fem.cg.u2, 4)}
+        self.halo_field = self.z_field
+        self.scal = self._field(self.fem.cg.scal, 1, count=12, dt="f64").tensor()
         self._send, self._recv, self._bufs = {}, {}, {}
         nranks = len(problems)
         for peer in range(nranks):
@@ -254,8 +288,13 @@ class GpuRank:
         self.fem.map_forces(model, True, False, stream=self.stream)
         self.fem.assemble(h, alpha, beta, g, stream=self.stream)
 
-    def cg_init(self):
-        self.fem.cg_init(self.stream)
+    def cg_init(self, single=False):
+        from . import _abi as A
+        self.fem.cg_init(self.stream, variant=A.CG_SINGLE_REDUCTION if single else A.CG_SAAD)
+
+    def set_halo(self, which):
+        """The vertex field the halo exchange moves next (z, u or u2)."""
+        self.halo_field = self.halo_fields[which]
 
     def cg_phase(self, k):
         import ctypes as C
@@ -281,7 +320,7 @@ class GpuRank:
     def pack(self, peer):
         from .ebb import _stream
         rf, bf, buf = self._send[peer]
-        self.ctx.check(self.ctx.L.ebb_rows_gather(self.ctx.h, self.z_field.h, rf.h, bf.h, _stream(self.stream)))
+        self.ctx.check(self.ctx.L.ebb_rows_gather(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
         return buf
 
     def recv_buffer(self, peer):
@@ -292,7 +331,7 @@ class GpuRank:
         rf, bf, buf = self._recv[peer]
         if data is not buf:
             buf.copy_(data)
-        self.ctx.check(self.ctx.L.ebb_rows_scatter(self.ctx.h, self.z_field.h, rf.h, bf.h, _stream(self.stream)))
+        self.ctx.check(self.ctx.L.ebb_rows_scatter(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
 
     # -- results in global numbering (owned rows only)
     def owned_values(self, field):

@@ -23,23 +23,28 @@ def ctx():
     c.close()
 
 
+@pytest.mark.parametrize("variant", ["saad", "single"])
 @pytest.mark.parametrize("P", [1, 2, 3, 4])
-def test_virtual_ranks_reproduce_single_domain(ctx, P):
+def test_virtual_ranks_reproduce_single_domain(ctx, P, variant):
+    """Both distributed PCG drivers (Saad: two allreduces per iteration;
+    single-reduction phase mode: one fused allreduce and the u halo,
+    SURVEY §8(e)) reproduce the single-domain oracle after 50 iterations."""
     from paper_1506_07577_b200 import dist
     case = Case(n=6, model="nh", vel_amp=0.05)
     h, iters = 1e-2, 50
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
                                case.free[order], h, iters=iters)
-    G = dist.global_partition(ctx, case.X, case.tets, P, name=f"vg{P}")
+    G = dist.global_partition(ctx, case.X, case.tets, P, name=f"vg{P}{variant}")
     assert np.array_equal(G["vert_order"], order)            # device renumbering == oracle O3
     ref_part = oracle.partition(m.nv, m.tets, P)
     assert np.array_equal(G["owner_v"], ref_part["owner_v"])  # device O4 == oracle O4
     plan = dist.halo_plan(G["tets"], G["owner_v"], P)
     tord = G["tet_order"]
     ranks = [dist.GpuRank(ctx, r, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
-                          case.vel[order], case.mu[tord], case.lam[tord], name=f"v{P}r{r}") for r in range(P)]
-    dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=h, iters=iters)
+                          case.vel[order], case.mu[tord], case.lam[tord], name=f"v{P}{variant}r{r}")
+             for r in range(P)]
+    dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=h, iters=iters, variant=variant)
     dv = np.full((m.nv, 3), np.nan)
     u = np.full((m.nv, 3), np.nan)
     for R in ranks:
@@ -69,7 +74,8 @@ def test_halo_plan_is_consistent(ctx):
             assert np.all(part["owner_v"][send[o][r]] == o)
 
 
-def test_nccl_transport_single_rank(ctx):
+@pytest.mark.parametrize("variant", ["saad", "single"])
+def test_nccl_transport_single_rank(ctx, variant):
     """The in-library NCCL transport (ebb_comm_*; a 1-rank communicator on
     this one-GPU box) drives the distributed step to the oracle's result: the
     allreduces of the PCG scalars and the (empty) halo go through NCCL."""
@@ -79,13 +85,13 @@ def test_nccl_transport_single_rank(ctx):
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
                                case.free[order], h, iters=iters)
-    G = dist.global_partition(ctx, case.X, case.tets, 1, name="nccl1")
+    G = dist.global_partition(ctx, case.X, case.tets, 1, name=f"nccl1{variant}")
     plan = dist.halo_plan(G["tets"], G["owner_v"], 1)
     tord = G["tet_order"]
     R = dist.GpuRank(ctx, 0, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
-                     case.vel[order], case.mu[tord], case.lam[tord], name="nccl1r0")
+                     case.vel[order], case.mu[tord], case.lam[tord], name=f"nccl1{variant}r0")
     T = dist.NcclTransport(ctx, 0, 1)
-    dist.implicit_step([R], T, "nh", h=h, iters=iters)
+    dist.implicit_step([R], T, "nh", h=h, iters=iters, variant=variant)
     ids, dv = R.owned_values(R.fem.dv)
     out = np.full((m.nv, 3), np.nan)
     out[ids] = dv

@@ -408,8 +408,11 @@ def run_dist(args, rank, world, local_rank):
     T_global = tets.shape[0]
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
+    cg_var = args.dist_cg
+    kmv = A.K_CG_SOLVE if cg_var == "single" else A.K_EDGE_MATVEC   # the streamed-matrix kernel of a phase
+
     def step():
-        D.implicit_step([R], T, w["model"], h=w["h"], iters=w["cg_iters"])
+        D.implicit_step([R], T, w["model"], h=w["h"], iters=w["cg_iters"], variant=cg_var)
 
     t_pre = time.perf_counter()              # clocks ramp from idle (see run_ours)
     while time.perf_counter() - t_pre < 0.5:
@@ -449,14 +452,14 @@ def run_dist(args, rank, world, local_rank):
                 ms_, n_ = ctx.timing_read(A.K_TET_MAP)
                 mp_tot += ms_
                 mp_cnt += n_
-                ms_, n_ = ctx.timing_read(A.K_EDGE_MATVEC)
+                ms_, n_ = ctx.timing_read(kmv)
                 mv_tot += ms_
                 mv_cnt += n_
         torch.cuda.synchronize()
     dist.barrier()
     launches = ctx.launch_count(reset=True)
     t_ms = sum(a.elapsed_time(b) for a, b in evs)
-    mv_ms, mv_n = ctx.timing_read(A.K_EDGE_MATVEC)
+    mv_ms, mv_n = ctx.timing_read(kmv)
     mp_ms, mp_n = ctx.timing_read(A.K_TET_MAP, reset=True)
     if graph is not None:
         mp_ms, mp_n, mv_ms, mv_n = mp_tot, mp_cnt, mv_tot, mv_cnt
@@ -466,15 +469,20 @@ def run_dist(args, rank, world, local_rank):
     value = T_global * args.steps / (t_ms / 1e3)
     peak, peak_src = _peaks()
     V_loc, E_loc = R.fem.nv, R.fem.ne
-    b_mv = bytes_matvec(V_loc, E_loc)
+    # single: one launch = one PCG iteration of the local rows (the prologue
+    # launch moves about the same bytes); saad: the MATVEC phase kernel
+    b_mv = bytes_cg_iter(V_loc, E_loc) if cg_var == "single" else bytes_matvec(V_loc, E_loc)
     avg_mv = 1e3 * mv_ms / max(mv_n, 1)
-    roof = {"kernel": "edge_matvec", "bound": "hbm", "achieved": b_mv / (avg_mv * 1e-6) / 1e9, "peak": peak,
+    roof = {"kernel": "k_cg1_persistent (one single-reduction phase per launch)" if cg_var == "single"
+            else "edge_matvec (Saad MATVEC phase)", "bound": "hbm", "achieved": b_mv / (avg_mv * 1e-6) / 1e9, "peak": peak,
             "unit": "GB/s", "frac": b_mv / (avg_mv * 1e-6) / 1e9 / peak, "peak_source": peak_src, "traffic": None,
             "algorithmic_bytes_per_launch": b_mv, "avg_launch_us": avg_mv, "rank": rank}
     cfg = _config(world)
     cfg.update({"workload": f"C2 recipe weak-scaled: Kuhn-6 n={n} ({T_global} tets, {X.shape[0]} verts) split over "
-                            f"{world} GPUs by the O4 owner maps (ghost tets, z halo + 2 scalar allreduces per "
-                            f"PCG iteration over NCCL), fp64", "transport": transport,
+                            f"{world} GPUs by the O4 owner maps (ghost tets; per PCG iteration "
+                            + ("one fused 2-scalar allreduce + u halo, single-reduction phases"
+                               if cg_var == "single" else "z halo + 2 scalar allreduces, Saad phases")
+                            + " over NCCL), fp64", "transport": transport, "pcg": cg_var,
                 "tets": T_global, "parallelism": f"domain decomposition x{world} (NCCL halo + allreduce)"})
     line = {"metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -497,6 +505,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of a CUDA graph")
+    ap.add_argument("--dist-cg", default="single", choices=["single", "saad"],
+                    help="PCG driver of the multi-GPU path (single: one fused allreduce per iteration)")
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU (domain decomposition) path even with one rank (smoke test)")
     args = ap.parse_args()

@@ -116,3 +116,34 @@ def test_nccl_allreduce_and_errors(ctx):
     assert buf.tolist() == [0.0, 1.0, 2.0, 3.0]
     fresh.close()
     del C
+
+
+def test_single_reduction_phases_honour_the_tolerance(ctx):
+    """Phase mode with ebb_cg.tol > 0 on 2 virtual ranks: the solve stops on
+    the device at the oracle's stop iteration (read off its r.z history of the
+    single-domain system) and later phases are no-ops."""
+    from paper_1506_07577_b200 import dist
+    case = Case(n=6, model="nh", vel_amp=0.05)
+    h, P, tol = 1e-2, 2, 1e-3
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                               case.free[order], h, iters=1)
+    _, hist, _ = oracle.pcg(m.row_ptr, m.head, ref["A"], ref["b"], case.free[order], 300)
+    thr = tol * tol * hist[0]
+    k = next(k for k in range(1, 301) if hist[k] <= thr)
+    assert abs(hist[k] - thr) > 1e-6 * thr and abs(hist[k - 1] - thr) > 1e-6 * thr
+    x_ref, _, _ = oracle.pcg(m.row_ptr, m.head, ref["A"], ref["b"], case.free[order], k)
+    G = dist.global_partition(ctx, case.X, case.tets, P, name="vgtol")
+    plan = dist.halo_plan(G["tets"], G["owner_v"], P)
+    tord = G["tet_order"]
+    ranks = [dist.GpuRank(ctx, r, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
+                          case.vel[order], case.mu[tord], case.lam[tord], name=f"vtol{r}") for r in range(P)]
+    for R in ranks:
+        R.fem.cg.tol = tol
+    dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=h, iters=k + 40, variant="single")
+    dv = np.full((m.nv, 3), np.nan)
+    for R in ranks:
+        ids, vals = R.owned_values(R.fem.dv)
+        dv[ids] = vals
+        assert R.fem.cg_iterations() == (k, True)
+    assert rel_l2(dv, x_ref) <= 1e-8

@@ -231,9 +231,12 @@ def test_cg_tolerance_mode(ctx, variant, fallback, monkeypatch):
     fem = gpu_fem(ctx, case, name=f"cgtol{variant}{int(fallback)}")
     fem.map_forces("nh")
     fem.assemble(1e-2)
-    A, b = fem.K.read(), fem.b.read()
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     free = case.free[order]
+    # the oracle's own system of this step (its map and assembly; no GPU value)
+    sysref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                                  free, 1e-2, iters=1)
+    A, b = sysref["A"], sysref["b"]
     nmax = 400
     _, hist, _ = oracle.pcg(m.row_ptr, m.head, A, b, free, nmax)
     for tol in (1e-2, 1e-4):

@@ -168,6 +168,10 @@ __device__ __forceinline__ void seg_diag(const R* __restrict__ st, uint32_t ent,
 // inputs of the next tile's instance held in registers across phase 2: fp64
 // (StVK 12 % faster with it, NH neutral); fp32 loads them at phase-1 start
 // (2-4 % faster: 72 instead of 80 registers) -- measured
+#ifndef SEG_UNROLL
+#define SEG_UNROLL 2    // phase-2 entry walk unroll (measured)
+#endif
+constexpr int kSegUnroll = SEG_UNROLL;
 #ifndef SEG_PIPE_INPUTS
 #define SEG_PIPE_INPUTS (sizeof(R) == 8)
 #endif
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
             // of a block depend only on its own entry)
             if (kind == 0) {
                 uint32_t x = e0 < e1 ? E[e0] : 0u;
-#pragma unroll 2
+#pragma unroll kSegUnroll
                 for (uint32_t e = e0; e < e1; ++e) {
                     const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
                     seg_block<R, MODEL, NT>(st, x, a9);
@@ -393,7 +397,7 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
             } else {
                 // self row + the vertex's force: the same (instance, corner) list
                 uint32_t x = e0 < e1 ? E[e0] : 0u;
-#pragma unroll 2
+#pragma unroll kSegUnroll
                 for (uint32_t e = e0; e < e1; ++e) {
                     const uint32_t nx = e + 1 < e1 ? E[e + 1] : 0u;
                     seg_diag<R, MODEL, NT>(st, x, a9);

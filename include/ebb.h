@@ -92,10 +92,15 @@ const char* ebb_version(void);
 ebb_status ebb_ctx_new(int device, ebb_ctx* out);
 ebb_status ebb_ctx_free(ebb_ctx ctx);
 const char* ebb_last_error(ebb_ctx ctx);
-/* Kernel-side error counters (synchronous; optionally reset):
- * out[0] inverted elements (J<=0), out[1] CG p.q<=0 events,
- * out[2] key out of range, out[3] reserved. */
+/* Kernel-side error counters (synchronous; optionally reset) -- the device
+ * error word of SURVEY §8(b) "Errors" (EBB_E_INVERTED, EBB_E_NOT_SPD,
+ * EBB_E_BOUNDS classes): out[0] inverted elements (J<=0, the NH reading of
+ * DESIGN.md §3 (15)), out[1] CG p.q<=0 events, out[2] key out of range
+ * (S:87), out[3] reserved.  EBB_E_ARG on a bad context. */
 ebb_status ebb_error_counts(ebb_ctx ctx, uint64_t out[4], int reset);
+/* Wait for every call issued on stream s (NULL: the whole device); the
+ * synchronising point of SURVEY §8(b) "Asynchrony".  EBB_E_CUDA on a
+ * failed kernel. */
 ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s);
 /* Instrumentation ("we instrument Ebb directly").  When enabled,
  * every launch of a hot kernel is bracketed by CUDA events recorded on the
@@ -117,7 +122,8 @@ ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64
 ebb_status ebb_launch_count(ebb_ctx ctx, uint64_t* out, int reset);
 
 /* CUDA-graph capture of a sequence of stream-ordered calls (e.g. one implicit
- * step: map, assemble, cg_init, cg_step, implicit_update).  s must be a
+ * step: map, assemble, cg_init, cg_step, implicit_update; SURVEY §8(e) "the
+ * whole iteration captured in a CUDA graph").  s must be a
  * non-default stream; calls between begin and end must not allocate or
  * synchronise (run the sequence once eagerly first: first calls build plans
  * and work fields).  Kernel timers recorded during capture become graph
@@ -443,10 +449,13 @@ typedef struct {
 } ebb_explicit_desc;
 /* O8: a = (f + m g)/m; u += v h + a h^2/2; v += a h on free vertices. */
 ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stream s);
-/* implicit state update: vel += dv; u += h vel. */
+/* O9 implicit state update (P:941 backward Euler):
+ * vel += dv; u += h vel.  dv, u, vel: AOS vec3 fields of one dtype on the
+ * same relation (EBB_E_TYPE otherwise).  Stream-ordered. */
 ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
-/* Newton iteration update (after an EBB_RHS_NEWTON solve): vel += dv;
- * u += h dv (keeps u = u_n + h vel). */
+/* Newton iteration update (DESIGN.md §3 (19)), after an
+ * EBB_RHS_NEWTON solve: vel += dv; u += h dv (keeps u = u_n + h vel).
+ * Fields as ebb_implicit_update.  Stream-ordered. */
 ebb_status ebb_newton_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream s);
 
 /* ---- regular 2-D grid domain (Fig. 3)

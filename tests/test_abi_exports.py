@@ -59,3 +59,18 @@ def test_ctx_new_fails_cleanly_without_gpu(libpath):
 def test_sass_is_sm100a(libpath):
     out = subprocess.run(["cuobjdump", "--list-elf", libpath], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_every_entry_point_cites_its_passage():
+    """Each extern "C" entry point of include/ebb.h is documented next to a
+    citation of the passage that defines it (P:/S: line)."""
+    import os
+    import re
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "ebb.h")
+    lines = open(path).read().splitlines()
+    missing = []
+    for i, line in enumerate(lines):
+        m = re.match(r"\s*(ebb_status|const char\*)\s+(ebb_\w+)\(", line)
+        if m and not re.search(r"P:\d|S:\d|SURVEY|§", "\n".join(lines[max(0, i - 25):i + 1])):
+            missing.append(m.group(2))
+    assert not missing, missing

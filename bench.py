@@ -399,12 +399,9 @@ def run_dist(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)
     R = D.GpuRank(ctx, rank, G["X"], G["tets"], G["owner_v"], plan, free[order], u0[order],
                   np.zeros_like(u0), mu[tord], lam[tord], rho=w["rho"], stream=stream, name=f"rank{rank}")
-    try:
-        T = D.NcclTransport(ctx, rank, world, stream=stream)   # NCCL inside the library (ebb_comm_*)
-        transport = "nccl (in-library, ebb_comm_*)"
-    except Exception as ex:                            # noqa: BLE001
-        T = D.TorchTransport()
-        transport = f"torch.distributed ({type(ex).__name__})"
+    # NCCL inside the library (ebb_comm_*); no fallback: a failure here ends the run
+    T = D.NcclTransport(ctx, rank, world, stream=stream)
+    transport = "nccl (in-library, ebb_comm_*)"
     T_global = tets.shape[0]
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
@@ -424,7 +421,7 @@ def run_dist(args, rank, world, local_rank):
     ctx.timing(True)
     ctx.timing_read(0, reset=True)
     graph = None
-    if isinstance(T, D.NcclTransport) and not args.no_graph:
+    if not args.no_graph:
         # the whole distributed step -- kernels and the in-library NCCL calls on
         # one stream -- captured once and replayed (no host loop per iteration)
         ctx.graph_begin(stream)

@@ -157,6 +157,13 @@ __global__ void k_fill(T* p, uint64_t n, T v) {
     if (i < n) p[i] = v;
 }
 
+// bounds check of u32 keys written into an existing key-field
+__global__ void k_keys_check(const uint32_t* __restrict__ in, uint64_t n, uint64_t target_size,
+                             unsigned long long* bad_count) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n && in[i] >= target_size) atomicAdd(bad_count, 1ull);
+}
+
 // bounds check + narrowing of uint64 keys to uint32 storage
 __global__ void k_keys_narrow(const uint64_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n,
                               uint64_t target_size, unsigned long long* bad_count,
@@ -284,6 +291,13 @@ ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, c
                             cudaStream_t s) {
     Relation* R = get_rel(c, rel);
     uint64_t n = R->size;
+    // a grouping is a sorted order of `rel` plus a CSR index on the
+    // key's target: permuting either side silently invalidates it
+    if (R->grouped_by != EBB_NONE)
+        return fail(c, EBB_E_STATE, "relation '%s' is grouped: reorder it before ebb_group_by", R->name.c_str());
+    if (R->index != EBB_NONE)
+        return fail(c, EBB_E_STATE, "relation '%s' is the target of a grouping (it holds a group index): "
+                    "reorder it before ebb_group_by", R->name.c_str());
     release_plans(c);
     for (ebb_field fh : R->fields) {
         Field& F = c->fields[fh];
@@ -338,9 +352,9 @@ ebb_status ebb_ctx_new(int device, ebb_ctx* out) {
         cudaGetLastError();
         return EBB_E_CUDA;
     }
-    if (cudaSetDevice(device) != cudaSuccess) return EBB_E_CUDA;
     Ctx* c = new Ctx();
     c->device = device;
+    EBB_DEVICE_GUARD(c);   // allocate on `device`, leave the caller's device current
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaMalloc(&c->d_err, 4 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(c->d_err, 0, 4 * sizeof(unsigned long long)) != cudaSuccess ||
@@ -361,6 +375,7 @@ ebb_status ebb_ctx_new(int device, ebb_ctx* out) {
 
 ebb_status ebb_ctx_free(ebb_ctx ctx) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
@@ -381,11 +396,13 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
 
 const char* ebb_last_error(ebb_ctx ctx) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     return c ? c->err.c_str() : "null context";
 }
 
 ebb_status ebb_error_counts(ebb_ctx ctx, uint64_t out[4], int reset) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !out) return EBB_E_ARG;
     EBB_CUDA(c, cudaDeviceSynchronize());
     unsigned long long h[4];
@@ -397,6 +414,7 @@ ebb_status ebb_error_counts(ebb_ctx ctx, uint64_t out[4], int reset) {
 
 ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     EBB_CUDA(c, cudaStreamSynchronize((cudaStream_t)s));
     return EBB_OK;
@@ -404,6 +422,7 @@ ebb_status ebb_sync(ebb_ctx ctx, ebb_stream s) {
 
 ebb_status ebb_timing_enable(ebb_ctx ctx, int on) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     if (on && c->ev_pool.empty()) {
         c->ev_pool.resize(16384);
@@ -415,6 +434,7 @@ ebb_status ebb_timing_enable(ebb_ctx ctx, int on) {
 
 ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64_t* launches, int reset) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !total_ms || !launches) return EBB_E_ARG;
     double tot = 0.0;
     uint64_t n = 0;
@@ -438,6 +458,7 @@ ebb_status ebb_timing_read(ebb_ctx ctx, int32_t kernel, double* total_ms, uint64
 
 ebb_status ebb_launch_count(ebb_ctx ctx, uint64_t* out, int reset) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !out) return EBB_E_ARG;
     *out = c->launches;
     if (reset) c->launches = 0;
@@ -446,6 +467,7 @@ ebb_status ebb_launch_count(ebb_ctx ctx, uint64_t* out, int reset) {
 
 ebb_status ebb_graph_begin(ebb_ctx ctx, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     if (!s) return fail(c, EBB_E_ARG, "graph capture needs a non-default stream");
     EBB_CUDA(c, cudaStreamBeginCapture((cudaStream_t)s, cudaStreamCaptureModeThreadLocal));
@@ -455,6 +477,7 @@ ebb_status ebb_graph_begin(ebb_ctx ctx, ebb_stream s) {
 
 ebb_status ebb_graph_end(ebb_ctx ctx, ebb_stream s, int32_t* graph_out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !graph_out || !s) return fail(c, EBB_E_ARG, "bad argument");
     cudaGraph_t g = nullptr;
     EBB_CUDA(c, cudaStreamEndCapture((cudaStream_t)s, &g));
@@ -470,6 +493,7 @@ ebb_status ebb_graph_end(ebb_ctx ctx, ebb_stream s, int32_t* graph_out) {
 
 ebb_status ebb_graph_launch(ebb_ctx ctx, int32_t graph, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || graph < 0 || (size_t)graph >= c->graphs.size() || !c->graphs[graph].exec)
         return fail(c, EBB_E_ARG, "bad graph handle");
     EBB_CUDA(c, cudaGraphLaunch(c->graphs[graph].exec, (cudaStream_t)s));
@@ -479,6 +503,7 @@ ebb_status ebb_graph_launch(ebb_ctx ctx, int32_t graph, ebb_stream s) {
 
 ebb_status ebb_graph_free(ebb_ctx ctx, int32_t graph) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || graph < 0 || (size_t)graph >= c->graphs.size()) return EBB_E_ARG;
     if (c->graphs[graph].exec) cudaGraphExecDestroy(c->graphs[graph].exec);
     c->graphs[graph].exec = nullptr;
@@ -487,6 +512,7 @@ ebb_status ebb_graph_free(ebb_ctx ctx, int32_t graph) {
 
 ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_rel* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !name || !out) return fail(c, EBB_E_ARG, "null argument");
     if (size == 0) return fail(c, EBB_E_SIZE, "relation '%s' has zero size", name);
     for (auto& R : c->rels)
@@ -501,6 +527,7 @@ ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_re
 
 ebb_status ebb_relation_size(ebb_ctx ctx, ebb_rel rel, uint64_t* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Relation* R = get_rel(c, rel);
     if (!R || !out) return fail(c, EBB_E_ARG, "bad relation");
     *out = R->size;
@@ -510,6 +537,7 @@ ebb_status ebb_relation_size(ebb_ctx ctx, ebb_rel rel, uint64_t* out) {
 ebb_status ebb_field_new(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype dtype, uint32_t rows, uint32_t cols,
                          ebb_layout layout, const void* host_init, ebb_field* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !out) return fail(c, EBB_E_ARG, "null argument");
     if (dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "use ebb_key_field for key-fields");
     ebb_field h;
@@ -528,6 +556,7 @@ ebb_status ebb_field_new(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype d
 ebb_status ebb_field_wrap(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype dtype, uint32_t rows, uint32_t cols,
                           ebb_layout layout, void* device_ptr, ebb_field* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !out || !device_ptr) return fail(c, EBB_E_ARG, "null argument");
     if (dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "key-fields must be created by ebb_key_field");
     return add_field(c, rel, name, dtype, rows, cols, layout, device_ptr, false, out);
@@ -535,6 +564,7 @@ ebb_status ebb_field_wrap(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_dtype 
 
 ebb_status ebb_field_find(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_field* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Relation* R = get_rel(c, rel);
     if (!R || !name || !out) return fail(c, EBB_E_ARG, "bad argument");
     for (ebb_field f : R->fields)
@@ -547,6 +577,7 @@ ebb_status ebb_field_find(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_field*
 
 ebb_status ebb_field_write(ebb_ctx ctx, ebb_field f, const void* host, uint64_t nbytes, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* F = get_field(c, f);
     if (!F || !host) return fail(c, EBB_E_ARG, "bad field or null host pointer");
     uint64_t n = c->rels[F->rel].size;
@@ -554,6 +585,28 @@ ebb_status ebb_field_write(ebb_ctx ctx, ebb_field f, const void* host, uint64_t 
     if (nbytes != want) return fail(c, EBB_E_SIZE, "field '%s': %llu bytes given, %llu expected", F->name.c_str(),
                                     (unsigned long long)nbytes, (unsigned long long)want);
     cudaStream_t st = (cudaStream_t)s;
+    if (F->dtype == EBB_KEY) {
+        // keys stay in bounds by construction: check the new keys
+        // before they replace the old ones; plans built on the old
+        // connectivity are dropped; a grouping key cannot be rewritten
+        if (c->rels[F->rel].grouped_by == f)
+            return fail(c, EBB_E_STATE, "key-field '%s' groups its relation: it cannot be rewritten", F->name.c_str());
+        EBB_TRY(scratch_reserve(c, nbytes + 16));
+        unsigned long long* bad = (unsigned long long*)((char*)c->scratch + ((nbytes + 7) & ~7ull));
+        EBB_CUDA(c, cudaMemcpyAsync(c->scratch, host, nbytes, cudaMemcpyHostToDevice, st));
+        EBB_CUDA(c, cudaMemsetAsync(bad, 0, 8, st));
+        const uint64_t nk = n * F->comps();
+        k_keys_check<<<grid_for(nk, 256), 256, 0, st>>>((const uint32_t*)c->scratch, nk, c->rels[F->key_target].size, bad);
+        EBB_CUDA(c, cudaGetLastError());
+        unsigned long long hb = 0;
+        EBB_CUDA(c, cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
+        EBB_CUDA(c, cudaStreamSynchronize(st));
+        if (hb) return fail(c, EBB_E_BOUNDS, "key-field '%s': %llu keys out of range of '%s'", F->name.c_str(), hb,
+                            c->rels[F->key_target].name.c_str());
+        release_plans(c);
+        EBB_CUDA(c, cudaMemcpyAsync(F->ptr, c->scratch, nbytes, cudaMemcpyDeviceToDevice, st));
+        return EBB_OK;
+    }
     if (F->layout == EBB_AOS || F->comps() == 1) {
         EBB_CUDA(c, cudaMemcpyAsync(F->ptr, host, nbytes, cudaMemcpyHostToDevice, st));
         return EBB_OK;
@@ -565,6 +618,7 @@ ebb_status ebb_field_write(ebb_ctx ctx, ebb_field f, const void* host, uint64_t 
 
 ebb_status ebb_field_read(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* F = get_field(c, f);
     if (!F || !host) return fail(c, EBB_E_ARG, "bad field or null host pointer");
     uint64_t n = c->rels[F->rel].size;
@@ -585,6 +639,7 @@ ebb_status ebb_field_read(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes,
 
 ebb_status ebb_field_fill(ebb_ctx ctx, ebb_field f, double value, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* F = get_field(c, f);
     if (!F) return fail(c, EBB_E_ARG, "bad field");
     if (F->dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "cannot fill a key-field");
@@ -606,6 +661,7 @@ ebb_status ebb_field_fill(ebb_ctx ctx, ebb_field f, double value, ebb_stream s) 
 
 ebb_status ebb_field_copy(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* D = get_field(c, dst);
     Field* S = get_field(c, src);
     if (!D || !S) return fail(c, EBB_E_ARG, "bad field");
@@ -613,6 +669,14 @@ ebb_status ebb_field_copy(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream 
         c->rels[D->rel].size != c->rels[S->rel].size)
         return fail(c, EBB_E_TYPE, "field_copy: '%s' and '%s' differ in type/shape/layout", D->name.c_str(),
                     S->name.c_str());
+    if (D->dtype == EBB_KEY) {
+        if (D->key_target != S->key_target)
+            return fail(c, EBB_E_TYPE, "field_copy: key-fields '%s' and '%s' target different relations",
+                        D->name.c_str(), S->name.c_str());
+        if (c->rels[D->rel].grouped_by == dst)
+            return fail(c, EBB_E_STATE, "key-field '%s' groups its relation: it cannot be rewritten", D->name.c_str());
+        release_plans(c);
+    }
     uint64_t nbytes = c->rels[D->rel].size * D->comps() * dtype_size(D->dtype);
     EBB_CUDA(c, cudaMemcpyAsync(D->ptr, S->ptr, nbytes, cudaMemcpyDeviceToDevice, (cudaStream_t)s));
     return EBB_OK;
@@ -620,6 +684,7 @@ ebb_status ebb_field_copy(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream 
 
 ebb_status ebb_field_convert(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* D = get_field(c, dst);
     Field* S = get_field(c, src);
     if (!D || !S) return fail(c, EBB_E_ARG, "bad field");
@@ -639,6 +704,7 @@ ebb_status ebb_field_convert(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stre
 
 ebb_status ebb_field_view(ebb_ctx ctx, ebb_field f, ebb_view* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* F = get_field(c, f);
     if (!F || !out) return fail(c, EBB_E_ARG, "bad field");
     uint64_t n = c->rels[F->rel].size;
@@ -664,6 +730,7 @@ ebb_status ebb_field_view(ebb_ctx ctx, ebb_field f, ebb_view* out) {
 ebb_status ebb_key_field(ebb_ctx ctx, ebb_rel owner, const char* name, ebb_rel target, uint32_t rows, uint32_t cols,
                          const uint64_t* keys, int keys_on_device, ebb_field* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !keys || !out) return fail(c, EBB_E_ARG, "null argument");
     Relation* O = get_rel(c, owner);
     Relation* T = get_rel(c, target);
@@ -705,6 +772,7 @@ ebb_status ebb_key_field(ebb_ctx ctx, ebb_rel owner, const char* name, ebb_rel t
 
 ebb_status ebb_global_new(ebb_ctx ctx, const char* name, ebb_dtype dtype, double init, ebb_field* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !out) return fail(c, EBB_E_ARG, "null argument");
     if (dtype != EBB_F64 && dtype != EBB_F32 && dtype != EBB_I64 && dtype != EBB_I32)
         return fail(c, EBB_E_TYPE, "globals are scalar numeric");
@@ -719,6 +787,7 @@ ebb_status ebb_global_new(ebb_ctx ctx, const char* name, ebb_dtype dtype, double
 
 ebb_status ebb_global_get(ebb_ctx ctx, ebb_field g, double* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* F = get_field(c, g);
     if (!F || !out || !F->is_global) return fail(c, EBB_E_ARG, "not a global");
     EBB_CUDA(c, cudaDeviceSynchronize());
@@ -735,6 +804,7 @@ ebb_status ebb_global_get(ebb_ctx ctx, ebb_field g, double* out) {
 
 ebb_status ebb_global_set(ebb_ctx ctx, ebb_field g, double value, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field* F = get_field(c, g);
     if (!F || !F->is_global) return fail(c, EBB_E_ARG, "not a global");
     return ebb_field_fill(ctx, g, value, s);
@@ -742,6 +812,7 @@ ebb_status ebb_global_set(ebb_ctx ctx, ebb_field g, double value, ebb_stream s) 
 
 ebb_status ebb_group_by(ebb_ctx ctx, ebb_rel rel, ebb_field key) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Relation* R = get_rel(c, rel);
     Field* K = get_field(c, key);
     if (!R || !K) return fail(c, EBB_E_ARG, "bad handle");
@@ -801,6 +872,7 @@ static ebb_status rows_common(Ctx* c, ebb_field f, ebb_field rows, ebb_field buf
     *B = get_field(c, buf);
     if (!*F || !*Rw || !*B) return fail(c, EBB_E_ARG, "rows_gather/scatter: bad handle");
     if ((*F)->layout != EBB_AOS && (*F)->comps() > 1) return fail(c, EBB_E_TYPE, "halo fields must be AOS");
+    if ((*F)->dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "halo rows of a key-field are not supported");
     if ((*Rw)->dtype != EBB_U32 || (*Rw)->comps() != 1) return fail(c, EBB_E_TYPE, "rows must be a U32 scalar field");
     if ((*B)->dtype != (*F)->dtype || (*B)->comps() != (*F)->comps() || (*B)->rel != (*Rw)->rel)
         return fail(c, EBB_E_TYPE, "buf must match f's dtype/shape on the rows' relation");
@@ -813,6 +885,7 @@ static ebb_status rows_common(Ctx* c, ebb_field f, ebb_field rows, ebb_field buf
 
 ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field *F, *Rw, *B;
     uint64_t n;
     uint32_t w;
@@ -826,6 +899,7 @@ ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field b
 
 ebb_status ebb_rows_scatter(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Field *F, *Rw, *B;
     uint64_t n;
     uint32_t w;
@@ -839,6 +913,7 @@ ebb_status ebb_rows_scatter(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field 
 
 ebb_status ebb_group_index(ebb_ctx ctx, ebb_rel rel, ebb_field* index_out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     Relation* R = get_rel(c, rel);
     if (!R || !index_out) return fail(c, EBB_E_ARG, "bad argument");
     if (R->index == EBB_NONE) return fail(c, EBB_E_STATE, "relation '%s' has no group index", R->name.c_str());

@@ -101,6 +101,7 @@ ebb_status ebb_comm_unique_id(ebb_nccl_id* out) {
 
 ebb_status ebb_comm_init(ebb_ctx ctx, int32_t nranks, int32_t rank, const ebb_nccl_id* id) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !id) return fail(c, EBB_E_ARG, "null argument");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, EBB_E_ARG, "comm_init: rank %d of %d", rank, nranks);
     Nccl& n = nccl();
@@ -120,6 +121,7 @@ ebb_status ebb_comm_init(ebb_ctx ctx, int32_t nranks, int32_t rank, const ebb_nc
 
 ebb_status ebb_comm_allreduce_sum(ebb_ctx ctx, double* dev_buf, uint64_t count, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !dev_buf) return fail(c, EBB_E_ARG, "null argument");
     if (!c->comm) return fail(c, EBB_E_STATE, "comm_allreduce: ebb_comm_init first");
     const ncclResult_t r = nccl().AllReduce(dev_buf, dev_buf, count, ncclFloat64_, ncclSum_, (ncclComm_t)c->comm,
@@ -132,6 +134,7 @@ ebb_status ebb_comm_halo(ebb_ctx ctx, int32_t npeers, const int32_t* peers, void
                          const uint64_t* send_bytes, void* const* recv_bufs, const uint64_t* recv_bytes,
                          ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || (npeers > 0 && (!peers || !send_bufs || !send_bytes || !recv_bufs || !recv_bytes)))
         return fail(c, EBB_E_ARG, "null argument");
     if (!c->comm) return fail(c, EBB_E_STATE, "comm_halo: ebb_comm_init first");

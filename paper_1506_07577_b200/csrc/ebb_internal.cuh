@@ -247,6 +247,26 @@ ebb_status permute_relation(Ctx* c, ebb_rel rel, const uint32_t* d_new_to_old, c
         if (_e != cudaSuccess) return ::ebb::cuda_fail((c), _e, #call); \
     } while (0)
 
+// A context is bound to one CUDA device (include/ebb.h): every ABI entry
+// point makes that device current for its duration and restores the
+// caller's device on return (a process may hold contexts on several GPUs).
+constexpr int kMaxDevices = 64;
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const Ctx* c) {
+        if (!c) return;
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess)
+            prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+#define EBB_DEVICE_GUARD(c) ::ebb::DeviceGuard _ebb_device_guard(c)
+
 #define EBB_TRY(call)                  \
     do {                               \
         ebb_status _s = (call);        \

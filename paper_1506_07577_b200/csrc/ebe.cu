@@ -188,6 +188,7 @@ extern "C" {
 
 ebb_status ebb_tet_stiffness_state(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_field state, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     EbeArgs a;
     EBB_TRY(ebe_validate(c, d, state, true, &a));
     cudaStream_t s = (cudaStream_t)stream;
@@ -214,6 +215,7 @@ ebb_status ebb_tet_stiffness_state(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_f
 ebb_status ebb_ebe_matvec(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_field state, ebb_field p, ebb_field q,
                           ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     EbeArgs a;
     EBB_TRY(ebe_validate(c, d, state, false, &a));
     Field* P = get_field(c, p);

@@ -121,6 +121,7 @@ extern "C" {
 
 ebb_status ebb_grid2_new(ebb_ctx ctx, const char* name, uint32_t nx, uint32_t ny, ebb_grid2* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !name || !out) return fail(c, EBB_E_ARG, "null argument");
     if (nx == 0 || ny == 0) return fail(c, EBB_E_SIZE, "grid2: zero dimension");
     if ((uint64_t)nx * ny > 0xFFFFFFFFull) return fail(c, EBB_E_RANGE, "grid2: more than 2^32 cells");
@@ -140,6 +141,7 @@ ebb_status ebb_grid2_new(ebb_ctx ctx, const char* name, uint32_t nx, uint32_t ny
 ebb_status ebb_grid2_stencil(ebb_ctx ctx, ebb_rel cells, ebb_field in, ebb_field out, int32_t npts,
                              const int32_t* offsets, const double* weights, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || (npts > 0 && (!offsets || !weights))) return fail(c, EBB_E_ARG, "null argument");
     Relation* G = grid_rel(c, cells, 1, "cells");
     if (!G) return EBB_E_TYPE;
@@ -184,6 +186,7 @@ ebb_status ebb_grid2_stencil(ebb_ctx ctx, ebb_rel cells, ebb_field in, ebb_field
 
 ebb_status ebb_grid2_point_locate(ebb_ctx ctx, ebb_field pos, ebb_field dual_cell, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* P = get_field(c, pos);
     Field* K = get_field(c, dual_cell);
@@ -210,6 +213,7 @@ ebb_status ebb_grid2_point_locate(ebb_ctx ctx, ebb_field pos, ebb_field dual_cel
 ebb_status ebb_grid2_particle_vel(ebb_ctx ctx, ebb_field dual_cell, ebb_field cell_vel, ebb_field pos, ebb_field vel,
                                   ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* K = get_field(c, dual_cell);
     Field* CV = get_field(c, cell_vel);

@@ -787,7 +787,8 @@ ebb_status launch_seg_t(Ctx* c, const SegPlan& P, bool want_e, int accumulate, u
     if (smem > 227 * 1024)
         return fail(c, EBB_E_RANGE, "segmented map: %zu B of shared memory needed (> 227 KB)", smem);
     auto kern = want_e ? k_tet_map_seg<R, MODEL, true, NT> : k_tet_map_seg<R, MODEL, false, NT>;
-    static thread_local size_t configured[2] = {0, 0};   // attribute set once (graph-capture safe)
+    static thread_local size_t configured_dev[kMaxDevices][2] = {};
+    size_t* const configured = configured_dev[c->device % kMaxDevices];   // attribute set once (graph-capture safe)
     if (smem > configured[want_e]) {
         EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured[want_e] = smem;
@@ -865,6 +866,7 @@ ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool wa
 extern "C" ebb_status ebb_map_plan_stats(ebb_ctx ctx, ebb_field v, ebb_field e, double out[8]) {
     using namespace ebb;
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !out) return EBB_E_ARG;
     for (int k = 0; k < 8; ++k) out[k] = 0;
     Field* V = get_field(c, v);

@@ -292,6 +292,7 @@ extern "C" {
 
 ebb_status ebb_tetmesh_orient(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, uint64_t* n_swapped) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field *V, *X;
     EBB_TRY(check_tets_v(c, tets_v, &V));
@@ -312,6 +313,7 @@ ebb_status ebb_tetmesh_orient(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, uint
 
 ebb_status ebb_renumber_morton(ebb_ctx ctx, ebb_rel rel, ebb_field pos) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* X;
     EBB_TRY(check_pos(c, pos, rel, &X));
@@ -344,6 +346,7 @@ ebb_status ebb_renumber_morton(ebb_ctx ctx, ebb_rel rel, ebb_field pos) {
 
 ebb_status ebb_sort_by_key_tuple(ebb_ctx ctx, ebb_rel rel, ebb_field keys) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* V = get_field(c, keys);
     if (!V) return fail(c, EBB_E_ARG, "bad key-field handle");
@@ -381,6 +384,7 @@ ebb_status ebb_sort_by_key_tuple(ebb_ctx ctx, ebb_rel rel, ebb_field keys) {
 
 ebb_status ebb_tetmesh_build(ebb_ctx ctx, ebb_field tets_v, const char* edges_name, ebb_tetmesh* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !out || !edges_name) return fail(c, EBB_E_ARG, "null argument");
     Field* V;
     EBB_TRY(check_tets_v(c, tets_v, &V));
@@ -462,6 +466,7 @@ ebb_status ebb_tetmesh_build(ebb_ctx ctx, ebb_field tets_v, const char* edges_na
 ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double rho, ebb_field Dminv, ebb_field W,
                             ebb_field mass, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field *V, *X;
     EBB_TRY(check_tets_v(c, tets_v, &V));
@@ -496,6 +501,7 @@ ebb_status ebb_tetmesh_rest(ebb_ctx ctx, ebb_field tets_v, ebb_field pos, double
 ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field W, double rho, ebb_field mass_e,
                                        ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* E = get_field(c, tets_e);
     Field* Wf = get_field(c, W);
@@ -522,6 +528,7 @@ ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field 
 
 ebb_status ebb_partition(ebb_ctx ctx, ebb_field tets_v, int32_t nparts, ebb_field owner_t, ebb_field owner_v) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* V;
     EBB_TRY(check_tets_v(c, tets_v, &V));

@@ -914,6 +914,7 @@ __global__ void k_compress_upper(uint64_t nu, uint64_t ne, const uint32_t* __res
 #ifndef CG1_NS
 #define CG1_NS 4        // TMA ring depth of the single-reduction PCG
 #endif
+constexpr unsigned kCg1PartStride = 2048;   // partial slots per phase parity (grid <= 2048)
 // (no min-blocks in the launch bounds: ptxas then keeps 72 registers, 3 CTAs
 // per SM; an explicit min-blocks of 1 let it take 148 and ran 1.5x slower)
 template <typename R>
@@ -1115,16 +1116,23 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         }
         pg = block_reduce<ROP_SUM>(pg);
         pd = block_reduce<ROP_SUM>(pd);
+        // one grid barrier per phase: the partial slots alternate by phase
+        // parity, so a CTA that leaves the barrier first and writes the next
+        // phase's partials cannot overwrite ones a slower CTA is still summing
+        // (it reaches the phase after next only once every CTA has passed the
+        // next barrier, i.e. has finished reading this phase's slots)
+        double* const pgb = part_g + (ph & 1) * kCg1PartStride;
+        double* const pdb = part_d + (ph & 1) * kCg1PartStride;
         if (threadIdx.x == 0) {
-            part_g[blockIdx.x] = pg;
-            part_d[blockIdx.x] = pd;
+            pgb[blockIdx.x] = pg;
+            pdb[blockIdx.x] = pd;
         }
         grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
-        const double dsum = grid_sum_partials(part_d, gridDim.x, &sm_tot);
+        const double dsum = grid_sum_partials(pdb, gridDim.x, &sm_tot);
         if (dist) {
             // phase mode: publish the rank-local sums; the recurrences finish
             // at the next launch, after the host's allreduce of S_DSUM..S_GSUM
-            const double gl = pro ? 0.0 : grid_sum_partials(part_g, gridDim.x, &sm_tot);
+            const double gl = pro ? 0.0 : grid_sum_partials(pgb, gridDim.x, &sm_tot);
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 scal[S_DSUM] = dsum;
                 scal[S_GSUM] = gl;
@@ -1141,7 +1149,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             beta = 0.0;
             first = 0;
         } else {
-            const double gnew = grid_sum_partials(part_g, gridDim.x, &sm_tot);
+            const double gnew = grid_sum_partials(pgb, gridDim.x, &sm_tot);
             const double bn = gam != 0.0 ? gnew / gam : 0.0;
             const double den = dsum - (alpha != 0.0 ? bn * gnew / alpha : 0.0);   // = p_{i+1} . A p_{i+1}
             if (blockIdx.x == 0 && threadIdx.x == 0 && den < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
@@ -1446,7 +1454,8 @@ ebb_status launch_tma(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, 
     // DESIGN.md §5.3); EBB_SPMV_GRP=0 selects 16 lanes per vertex
     static const bool grp = !(getenv("EBB_SPMV_GRP") && getenv("EBB_SPMV_GRP")[0] == '0');
     auto kern = grp ? k_spmv_tma<R, CG, MPQ, DIR, true> : k_spmv_tma<R, CG, MPQ, DIR, false>;
-    static thread_local size_t configured[2] = {0, 0};
+    static thread_local size_t configured_dev[kMaxDevices][2] = {};
+    size_t* const configured = configured_dev[c->device % kMaxDevices];
     if (smem > configured[grp]) {
         EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured[grp] = smem;
@@ -1589,7 +1598,8 @@ ebb_status cg_sym_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * TMA_NS;
     if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
-    static thread_local size_t configured = 0;
+    static thread_local size_t configured_dev[kMaxDevices] = {};
+    size_t& configured = configured_dev[c->device % kMaxDevices];
     if (smem > configured) {
         EBB_CUDA(c, cudaFuncSetAttribute(k_cg_sym_persistent<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
@@ -1650,7 +1660,8 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * CG1_NS;
     if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
-    static thread_local size_t configured = 0;
+    static thread_local size_t configured_dev[kMaxDevices] = {};
+    size_t& configured = configured_dev[c->device % kMaxDevices];
     if (smem > configured) {
         EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_persistent<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
@@ -1662,7 +1673,7 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     const uint64_t nch = (G.nv + TMA_VCH - 1) / TMA_VCH;
     uint64_t grid = (uint64_t)nb * c->num_sms;
     if (grid > nch) grid = nch;
-    if (grid > 4096) grid = 4096;
+    if (grid > kCg1PartStride) grid = kCg1PartStride;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(block);
@@ -1709,7 +1720,8 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
         const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
         const size_t smem = stage * TMA_NS;
         if (smem <= 200 * 1024) {
-            static thread_local size_t configured = 0;
+            static thread_local size_t configured_dev[kMaxDevices] = {};
+            size_t& configured = configured_dev[c->device % kMaxDevices];
             if (smem > configured) {
                 EBB_CUDA(c, cudaFuncSetAttribute(k_cg_persistent<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem));
@@ -1790,6 +1802,7 @@ extern "C" {
 ebb_status ebb_map_edge_matvec(ebb_ctx ctx, ebb_rel edges, ebb_field A, ebb_field p, ebb_field q, ebb_field mask,
                                ebb_field pq_global, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     EdgeGraph G;
     EBB_TRY(edge_graph(c, edges, &G));
@@ -1833,6 +1846,7 @@ ebb_status ebb_map_edge_matvec(ebb_ctx ctx, ebb_rel edges, ebb_field A, ebb_fiel
 ebb_status ebb_global_reduce(ebb_ctx ctx, int32_t op, ebb_field a, ebb_field b, ebb_field mask, ebb_field out,
                              ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* Af = get_field(c, a);
     Field* O = get_field(c, out);
@@ -1874,6 +1888,7 @@ ebb_status ebb_global_reduce(ebb_ctx ctx, int32_t op, ebb_field a, ebb_field b, 
 
 ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     EdgeGraph G;
     EBB_TRY(edge_graph(c, d->edges, &G));
@@ -1930,6 +1945,7 @@ ebb_status ebb_implicit_assemble(ebb_ctx ctx, const ebb_implicit_desc* d, ebb_st
 
 ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");
     EdgeGraph G;
     ebb_dtype dt;
@@ -1997,6 +2013,7 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
 
 ebb_status ebb_cg_iterations(ebb_ctx ctx, const ebb_cg* cg, ebb_stream stream, int32_t* iters, int32_t* converged) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");
     Field* S = get_field(c, cg->scal);
     if (!S) return fail(c, EBB_E_STATE, "cg: call ebb_cg_init first");
@@ -2011,6 +2028,7 @@ ebb_status ebb_cg_iterations(ebb_ctx ctx, const ebb_cg* cg, ebb_stream stream, i
 
 ebb_status ebb_cg_variant(ebb_ctx ctx, const ebb_cg* cg, int32_t* out) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !cg || !out) return fail(c, EBB_E_ARG, "null argument");
     EdgeGraph G;
     ebb_dtype dt;
@@ -2021,6 +2039,7 @@ ebb_status ebb_cg_variant(ebb_ctx ctx, const ebb_cg* cg, int32_t* out) {
 
 ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");
     if (iters < 0) return fail(c, EBB_E_ARG, "negative iteration count");
     EdgeGraph G;
@@ -2039,6 +2058,7 @@ ebb_status ebb_cg_step(ebb_ctx ctx, const ebb_cg* cg, int32_t iters, ebb_stream 
 
 ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !cg) return fail(c, EBB_E_ARG, "null argument");
     if (phase < EBB_CG_DIR || phase > EBB_CG_SR_PHASE) return fail(c, EBB_E_ARG, "unknown CG phase %d", phase);
     EdgeGraph G;
@@ -2054,6 +2074,7 @@ ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream
 
 ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     Field* U = get_field(c, d->u);
     if (!U) return fail(c, EBB_E_ARG, "explicit: bad u");
@@ -2085,6 +2106,7 @@ namespace {
 ebb_status implicit_update_impl(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream stream,
                                 bool newton) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* U = get_field(c, u);
     if (!U) return fail(c, EBB_E_ARG, "implicit_update: bad u");

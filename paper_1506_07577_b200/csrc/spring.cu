@@ -347,6 +347,7 @@ extern "C" {
 
 ebb_status ebb_spring_init_len(ebb_ctx ctx, ebb_rel edges, ebb_field pos, ebb_field rest_len, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     EdgeGraph G;
     EBB_TRY(edge_graph(c, edges, &G));
@@ -377,6 +378,7 @@ ebb_status ebb_spring_init_len(ebb_ctx ctx, ebb_rel edges, ebb_field pos, ebb_fi
 ebb_status ebb_spring_forces(ebb_ctx ctx, ebb_rel edges, ebb_field q, ebb_field rest_len, double K, ebb_field force,
                              int32_t accumulate, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     EdgeGraph G;
     EBB_TRY(edge_graph(c, edges, &G));
@@ -422,6 +424,7 @@ ebb_status ebb_spring_forces(ebb_ctx ctx, ebb_rel edges, ebb_field q, ebb_field 
 ebb_status ebb_spring_apply(ebb_ctx ctx, ebb_field mass, double dt_step, ebb_field q, ebb_field qd, ebb_field force,
                             ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* Q0 = get_field(c, q);
     if (!Q0) return fail(c, EBB_E_ARG, "spring: bad q");
@@ -457,6 +460,7 @@ ebb_status ebb_spring_step(ebb_ctx ctx, ebb_rel edges, ebb_field q_in, ebb_field
                            ebb_field rest_len, ebb_field mass, double K, double dt_step, ebb_field force,
                            ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     EdgeGraph G;
     EBB_TRY(edge_graph(c, edges, &G));
@@ -509,6 +513,7 @@ ebb_status ebb_spring_step(ebb_ctx ctx, ebb_rel edges, ebb_field q_in, ebb_field
 
 ebb_status ebb_kinetic_energy(ebb_ctx ctx, ebb_field mass, ebb_field qd, ebb_field out, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c) return EBB_E_ARG;
     Field* QD0 = get_field(c, qd);
     if (!QD0) return fail(c, EBB_E_ARG, "kinetic_energy: bad qd");

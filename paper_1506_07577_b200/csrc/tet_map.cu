@@ -1030,7 +1030,8 @@ ebb_status launch_gather_split(Ctx* c, const MapPlan& P, bool want_e, int accumu
                                cudaStream_t s) {
     const size_t smem = gather_smem<R, MODEL>(P);
     auto kern = want_e ? k_tet_map_gather<R, MODEL, true, NR, NC> : k_tet_map_gather<R, MODEL, false, NR, NC>;
-    static thread_local size_t configured[2] = {0, 0};   // attribute set once (graph-capture safe)
+    static thread_local size_t configured_dev[kMaxDevices][2] = {};
+    size_t* const configured = configured_dev[c->device % kMaxDevices];   // attribute set once (graph-capture safe)
     if (smem > configured[want_e]) {
         EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured[want_e] = smem;
@@ -1090,7 +1091,8 @@ ebb_status launch_tiled(Ctx* c, const MapPlan& P, bool want_e, int accumulate, u
     const int block = 256;
     const size_t smem = ((size_t)P.max_slots * 9 + (size_t)P.nvt * 3) * sizeof(R);
     auto kern = want_e ? k_tet_map_tiled<R, MODEL, true> : k_tet_map_tiled<R, MODEL, false>;
-    static thread_local size_t configured[2] = {0, 0};   // attribute set once (graph-capture safe)
+    static thread_local size_t configured_dev[kMaxDevices][2] = {};
+    size_t* const configured = configured_dev[c->device % kMaxDevices];   // attribute set once (graph-capture safe)
     if (smem > configured[want_e]) {
         EBB_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured[want_e] = smem;
@@ -1152,6 +1154,7 @@ ebb_status gather_plan(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, int mod
 
 extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_stream stream) {
     Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     if (d->model != EBB_STVK && d->model != EBB_NH) return fail(c, EBB_E_ARG, "unknown model %d", d->model);
     if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_COLOR)

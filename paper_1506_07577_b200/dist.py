@@ -172,10 +172,18 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
     """One distributed implicit step (O9 + O10) over `ranks` (the local ones).
 
     variant="saad": per iteration DIR, MATVEC, [sum p.q], UPDATE, [sum r.z,
-    z halo] -- two scalar allreduces.  variant="single": the single-reduction
-    (Chronopoulos-Gear) recurrences in phase mode, per iteration ONE phase,
-    ONE fused allreduce of (w.z, r.z) and the halo of the gathered operand u
-    (SURVEY §8(e)); iters iterations = iters + 1 phases (w_0 = A z_0 first)."""
+    z halo] -- two scalar allreduces.  Ghost x is formed from the exchanged z
+    with the global alpha/beta, so it stays equal to its owner's.
+
+    variant="single": the single-reduction (Chronopoulos-Gear) recurrences in
+    phase mode, per iteration ONE phase, ONE fused allreduce of (w.z, r.z) and
+    the halo of the gathered operand u; iters iterations =
+    iters + 1 phases (w_0 = A z_0 first).  Phase k writes u into buffer k % 2
+    (solver.cu k_cg1_persistent: the parity flips as each phase finishes the
+    previous recurrences), so only that buffer is exchanged.  Ghost rows are
+    masked, so the kernel leaves ghost x at 0: x (= dv) is exchanged from the
+    owners once, before the state update, so ghost u and v stay consistent
+    for the next step's map on ghost tets."""
     if variant == "single":
         for R in ranks:
             R.map_assemble(model, h, alpha, beta, g)
@@ -185,22 +193,27 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
         for R in ranks:
             R.set_halo("z")
         transport.exchange(ranks)
-        for _ in range(iters + 1):
+        nphase = iters + 1
+        for k in range(nphase):
             for R in ranks:
                 R.cg_phase(CG_SR_PHASE)
             transport.allreduce(ranks, (SLOT_DSUM, SLOT_GSUM + 1))
-            for which in ("u", "u2"):
+            if k + 1 < nphase:                 # the last phase's u is never gathered
                 for R in ranks:
-                    R.set_halo(which)
+                    R.set_halo("u" if k % 2 == 0 else "u2")
                 transport.exchange(ranks)
         for R in ranks:
-            R.set_halo("z")
+            R.set_halo("x")
+        transport.exchange(ranks)
+        for R in ranks:
             R.finish(h)
         return
     for R in ranks:
         R.map_assemble(model, h, alpha, beta, g)
         R.cg_init()
     transport.allreduce(ranks, (SLOT_RHO, SLOT_RZ + 1))
+    for R in ranks:
+        R.set_halo("z")
     transport.exchange(ranks)
     for _ in range(iters):
         for R in ranks:
@@ -255,12 +268,14 @@ class GpuRank:
         # allocates every CG work field (the single-reduction set includes u, u2)
         self.fem.cg_init(stream, variant=A.CG_SINGLE_REDUCTION)
         self.z_field = self._field(self.fem.cg.z, 4)
+        # halo fields: padded CG vectors (4 components) and dv (x of the PCG, 3)
         self.halo_fields = {"z": self.z_field, "u": self._field(self.fem.cg.u, 4),
-                            "u2": self._field(self.fem.cg.u2, 4)}
+                            "u2": self._field(self.fem.cg.u2, 4), "x": self.fem.dv}
         self.halo_field = self.z_field
         self.scal = self._field(self.fem.cg.scal, 1, count=12, dt="f64").tensor()
-        self._send, self._recv, self._bufs = {}, {}, {}
+        self._send, self._recv = {}, {}
         nranks = len(problems)
+        tdt = torch.float64 if dtype == "f64" else torch.float32
         for peer in range(nranks):
             for kind, lst in (("send", send[rank][peer]), ("recv", recv[rank][peer])):
                 if len(lst) == 0:
@@ -268,10 +283,11 @@ class GpuRank:
                 rows = stored[np.searchsorted(verts, lst)].astype(np.uint32)
                 rel = ctx.relation(f"{self.fem.verts.name}.{kind}{peer}", len(rows))
                 rf = rel.field("rows", "u32", init=rows)
-                buf = torch.zeros((len(rows), 4), dtype=torch.float64 if dtype == "f64" else torch.float32,
-                                  device=f"cuda:{ctx.device}")
-                bf = rel.wrap("buf", buf, dtype, (4, 1))
-                (self._send if kind == "send" else self._recv)[peer] = (rf, bf, buf)
+                bufs = {}
+                for nc in (3, 4):
+                    buf = torch.zeros((len(rows), nc), dtype=tdt, device=f"cuda:{ctx.device}")
+                    bufs[nc] = (rel.wrap(f"buf{nc}", buf, dtype, (nc, 1)), buf)
+                (self._send if kind == "send" else self._recv)[peer] = (rf, bufs)
         self._peers = sorted(set(self._send) | set(self._recv))
         torch.cuda.synchronize()
 
@@ -317,24 +333,34 @@ class GpuRank:
     def peers(self):
         return self._peers
 
+    def _nc(self):
+        return self.halo_field.shape[0]
+
     def pack(self, peer):
         from .ebb import _stream
-        rf, bf, buf = self._send[peer]
+        rf, bufs = self._send[peer]
+        bf, buf = bufs[self._nc()]
         self.ctx.check(self.ctx.L.ebb_rows_gather(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
         return buf
 
     def recv_buffer(self, peer):
-        return self._recv[peer][2]
+        return self._recv[peer][1][self._nc()][1]
 
     def unpack(self, peer, data):
         from .ebb import _stream
-        rf, bf, buf = self._recv[peer]
+        rf, bufs = self._recv[peer]
+        bf, buf = bufs[self._nc()]
         if data is not buf:
             buf.copy_(data)
         self.ctx.check(self.ctx.L.ebb_rows_scatter(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
 
-    # -- results in global numbering (owned rows only)
+    # -- results in global numbering
     def owned_values(self, field):
         vals = field.read()
         ids = self.verts_g[self.fem.vert_order()]
         return ids[self.owned_stored], vals[self.owned_stored]
+
+    def local_values(self, field):
+        """Every local row (owned and ghost) with its global vertex id."""
+        vals = field.read()
+        return self.verts_g[self.fem.vert_order()], vals

@@ -57,6 +57,44 @@ def test_virtual_ranks_reproduce_single_domain(ctx, P, variant):
     assert rel_l2(u, ref["u"]) <= 1e-8
 
 
+@pytest.mark.parametrize("variant", ["saad", "single"])
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_virtual_ranks_three_steps_owned_and_ghost_rows(ctx, P, variant):
+    """Three consecutive distributed implicit steps (50 PCG iterations each)
+    match three single-domain oracle steps on EVERY local row, owned and
+    ghost: step k+1 maps the ghost tets with the ghost u left by step k, so
+    a stale ghost (the round-1 single-reduction driver left ghost dv at 0)
+    corrupts the owned forces from step 2 on."""
+    from paper_1506_07577_b200 import dist
+    case = Case(n=6, model="nh", vel_amp=0.05)
+    h, iters, steps = 1e-2, 50, 3
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    u, v = case.u[order], case.vel[order]
+    for _ in range(steps):
+        ref = oracle.implicit_step(m, "nh", u, v, case.mu[tet_src], case.lam[tet_src], case.free[order], h,
+                                   iters=iters)
+        u, v = ref["u"], ref["v"]
+    G = dist.global_partition(ctx, case.X, case.tets, P, name=f"v3g{P}{variant}")
+    plan = dist.halo_plan(G["tets"], G["owner_v"], P)
+    tord = G["tet_order"]
+    ranks = [dist.GpuRank(ctx, r, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
+                          case.vel[order], case.mu[tord], case.lam[tord], name=f"v3{P}{variant}r{r}")
+             for r in range(P)]
+    for _ in range(steps):
+        dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=h, iters=iters, variant=variant)
+    nghost = 0
+    for R in ranks:
+        ids, gu = R.local_values(R.fem.u)
+        _, gv = R.local_values(R.fem.vel)
+        nghost += int((~R.owned_stored).sum())
+        assert rel_l2(gu, u[ids]) <= 1e-8
+        assert rel_l2(gv, v[ids]) <= 1e-8
+        ghost = ~R.owned_stored
+        assert rel_l2(gu[ghost], u[ids[ghost]]) <= 1e-8
+        assert rel_l2(gv[ghost], v[ids[ghost]]) <= 1e-8
+    assert nghost > 0
+
+
 def test_halo_plan_is_consistent(ctx):
     from paper_1506_07577_b200 import dist
     case = Case(n=5)

@@ -263,6 +263,21 @@ ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field 
                                    colour, plain read-modify-write reductions
                                    (deterministic; EBB_E_RANGE beyond 64
                                    colours).                                  */
+#define EBB_SCATTER_CHUNK 6     /* non-redundant tet chunks (device-built plan):
+                                   tiles of NT consecutive (SFC-ordered) tets,
+                                   each tet's element state computed ONCE;
+                                   every canonical row is summed by the last
+                                   tile touching it from its own blocks plus
+                                   the partial sums earlier tiles leave in
+                                   L2 message slots (release/acquire tile
+                                   counters; no atomics on f or K; bitwise
+                                   run-to-run deterministic).  The plan is
+                                   built on the device at the first call for
+                                   a (v, e) pair (synchronous; freed by any
+                                   relation permutation or ctx_free).
+                                   EBB_E_RANGE if one row gets blocks from
+                                   more than 128 tiles or more than 248
+                                   blocks from one tile.                     */
 typedef struct {
     int32_t model;         /* EBB_STVK | EBB_NH                                */
     int32_t scatter;       /* EBB_SCATTER_*                                    */
@@ -290,6 +305,13 @@ ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_stream
  *        instance cap per tile, host build ms, largest tile's entries}.
  * Host-only; no device work. */
 ebb_status ebb_map_plan_stats(ebb_ctx ctx, ebb_field v, ebb_field e, double out[8]);
+/* Statistics of the CHUNK map plan built for (v, e) (0 if none yet; the
+ * most recent plan if several tile sizes were built):
+ * out = {tiles, tets per tile, segments, messages (partial row sums sent to
+ *        a later tile), items, device build ms, plan bytes per tet resident
+ *        on the device (entries, items, descriptors, message slots, lists),
+ *        rows no tet contributes to}.  Host-only; no device work. */
+ebb_status ebb_map_chunk_stats(ebb_ctx ctx, ebb_field v, ebb_field e, double out[8]);
 
 /* a10: q_v = sum_{e in [index[v], index[v+1])} A_e p_head(e)  (query-loop over
  * v.edges), q *= mask (optional U8 on verts), and optionally

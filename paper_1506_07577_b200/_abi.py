@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libebb_b200.so")
+# EBB_LIB: a measurement build of the same sources (e.g. -DCHUNK_PROF); never a fallback
+LIB_PATH = os.environ.get("EBB_LIB") or os.path.join(HERE, "libebb_b200.so")
 
 NONE = 0xFFFFFFFF
 
@@ -23,7 +24,8 @@ E_NAMES = {
 F32, F64, I32, I64, U8, U32, KEY = 1, 2, 3, 4, 5, 6, 7
 AOS, SOA = 0, 1
 STVK, NH = 0, 1
-SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED, SCATTER_GATHER, SCATTER_SEGMENTED, SCATTER_COLOR = 0, 1, 2, 3, 4, 5
+SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED, SCATTER_GATHER, SCATTER_SEGMENTED, SCATTER_COLOR, SCATTER_CHUNK = \
+    0, 1, 2, 3, 4, 5, 6
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
 CG_DIR, CG_MATVEC, CG_UPDATE = 0, 1, 2
 K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE, K_CG_SOLVE, K_SPRING, K_EBE_MATVEC, K_GRID = \
@@ -119,6 +121,7 @@ SIGS = {
     "ebb_tetmesh_consistent_mass": (S, [ctx_t, u32, u32, C.c_double, u32, stream_t]),
     "ebb_map_tet_forces": (S, [ctx_t, C.POINTER(TetMapDesc), stream_t]),
     "ebb_map_plan_stats": (S, [ctx_t, u32, u32, C.POINTER(C.c_double)]),
+    "ebb_map_chunk_stats": (S, [ctx_t, u32, u32, C.POINTER(C.c_double)]),
     "ebb_comm_unique_id": (S, [C.c_char_p]),
     "ebb_comm_init": (S, [ctx_t, C.c_int32, C.c_int32, C.c_char_p]),
     "ebb_comm_allreduce_sum": (S, [ctx_t, C.c_void_p, C.c_uint64, stream_t]),

@@ -272,6 +272,11 @@ void release_plans(Ctx* c) {
         delete P;
     }
     c->segplans.clear();
+    for (ChunkPlan* P : c->chunkplans) {
+        P->release();
+        delete P;
+    }
+    c->chunkplans.clear();
     for (ColorPlan* P : c->colorplans) {
         P->release();
         delete P;

@@ -111,6 +111,30 @@ struct SegPlan {
     }
 };
 
+// Plan of the CHUNK element map (chunk_map.cu, built on the device once per
+// mesh): tiles of NT consecutive tets, each computed once; per tile its items
+// (chunks of segments = the blocks of the tile's tets summed into one row),
+// outgoing segments first; message slots; (sender -> receiver) tile lists.
+struct ChunkPlan {
+    ebb_field v = EBB_NONE, e = EBB_NONE;
+    int nt_tile = 0;                  // tets per tile = threads per CTA
+    uint32_t ntiles = 0;
+    uint64_t nseg = 0, nmsg = 0, npair = 0, nitems = 0, nzrows = 0, nzverts = 0;
+    double build_ms = 0;
+    uint4* tdesc = nullptr;           // ntiles + 1: {item0, outgoing items, owned items, receiver list offset}
+    uint32_t* expect = nullptr;       // ntiles: sender tiles of each tile
+    uint32_t* recv = nullptr;         // receiver tiles, CSR by sender
+    uint32_t* cnt = nullptr;          // ntiles: arrivals (reset by the receiver)
+    uint32_t* ticket = nullptr;       // [1] CTAs done (last one reduces the energy)
+    double* tile_e = nullptr;         // ntiles: energy of each tile
+    uint4* items = nullptr;           // nitems
+    uint32_t* ents = nullptr;         // 10 NT per tile: block entries in segment order
+    void* msg = nullptr;              // nmsg x 128 B
+    uint32_t* zrows = nullptr;        // rows no tet contributes to
+    uint32_t* zverts = nullptr;       // vertices in no tet
+    void release();
+};
+
 // Plan of the COLOURED element map (color_map.cu): tets grouped by colour
 // (no two tets of a colour share a vertex).
 struct ColorPlan {
@@ -166,6 +190,7 @@ struct Ctx : ebb_ctx_s {
     std::vector<TimedLaunch> timed;
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
     std::vector<SegPlan*> segplans; // (same)
+    std::vector<ChunkPlan*> chunkplans; // (same)
     std::vector<ColorPlan*> colorplans; // (same)
     std::vector<UpperCSR*> uppers;      // (same)
     void* comm = nullptr;               // ncclComm_t (comm.cu)
@@ -232,6 +257,12 @@ ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool wa
                           const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                           const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
                           cudaStream_t s);
+// chunk_map.cu: the CHUNK element map (builds its plan on the device on first use)
+ebb_status build_chunk_plan(Ctx* c, ebb_field vf, ebb_field ef, int NT, ChunkPlan** out);
+ebb_status chunk_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
+                            const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
+                            const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
+                            cudaStream_t s);
 // color_map.cu: the COLOURED element map (builds its colouring on first use)
 ebb_status color_map_launch(Ctx* c, ebb_field vf, int model, bool want_e, uint64_t nt, const Field* V,
                             const Field* Ef, const Field* U, const Field* D, const Field* W, const Field* MU,

@@ -75,6 +75,14 @@ class Context:
                 "max_tile_entries")
         return dict(zip(keys, list(out)))
 
+    def map_chunk_stats(self, v, e):
+        """Statistics of the CHUNK map plan for key-fields (v, e)."""
+        out = (C.c_double * 8)()
+        self.check(self.L.ebb_map_chunk_stats(self.h, int(v), int(e), out))
+        keys = ("tiles", "tets_per_tile", "segments", "messages", "items", "device_build_ms", "plan_bytes_per_tet",
+                "zero_rows")
+        return dict(zip(keys, list(out)))
+
     def timing(self, on=True):
         self.check(self.L.ebb_timing_enable(self.h, int(on)))
 

@@ -130,6 +130,10 @@ class TetFEM:
         """Statistics of the SEGMENTED map plan of this mesh (after a map)."""
         return self.ctx.map_plan_stats(self.v.h, self.e.h)
 
+    def chunk_stats(self):
+        """Statistics of the CHUNK map plan of this mesh (after a CHUNK map)."""
+        return self.ctx.map_chunk_stats(self.v.h, self.e.h)
+
     def map_forces(self, model="nh", want_K=True, want_energy=True, scatter=A.SCATTER_AUTO, zero_outputs=True,
                    stream=None):
         d = A.TetMapDesc()

@@ -21,7 +21,7 @@ from synth import state as S
 
 pytestmark = pytest.mark.gpu
 
-SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4, "color": 5}
+SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4, "color": 5, "chunk": 6}
 
 
 @pytest.fixture(scope="module")
@@ -102,7 +102,7 @@ def test_small_blob(ctx, model, scatter):
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-@pytest.mark.parametrize("scatter", ["segmented", "tiled", "gather"])
+@pytest.mark.parametrize("scatter", ["segmented", "tiled", "gather", "chunk"])
 def test_without_renumbering(ctx, scatter):
     """Scrambled vertex order (no SFC renumbering): tiles are ragged and
     tiny, the plan still covers every row exactly once."""
@@ -219,3 +219,25 @@ def test_widening_entry_points_refuse_bad_arguments(ctx):
     f4 = fem.verts.field("f4", "f64", (4, 1))
     with pytest.raises(EbbError, match="EBB_E_TYPE"):
         ctx.check(ctx.L.ebb_spring_forces(ctx.h, fem.edges.h, sm.q.h, sm.rest_len.h, 1.0, f4.h, 0, None))
+
+
+@pytest.mark.parametrize("nt", ["128", "256"])
+def test_chunk_hub_vertex(ctx, nt, monkeypatch):
+    """A vertex in 200 tets (and 300 with 128-tet tiles): its self row is summed
+    from one to three tiles (messages from the earlier ones); the oracle's
+    result either way.
+    300 blocks of one row inside one 512-tet tile exceed the 8 x 31 chunk
+    layout: EBB_E_RANGE, never a silent truncation."""
+    from paper_1506_07577_b200.ebb import EbbError
+    monkeypatch.setenv("EBB_CHUNK_NT", nt)
+    for k in ((200, 300) if nt == "128" else (200,)):
+        X, tets = _fan(k)
+        fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, "nh", f"fanchunk{nt}_{k}")
+        fem.map_forces("nh", scatter=SCATTERS["chunk"])
+        assert rel_l2(fem.f.read(), f) <= 1e-12 and rel_l2(fem.K.read(), K) <= 1e-12
+        assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+    monkeypatch.setenv("EBB_CHUNK_NT", "512")
+    X3, tets3 = _fan(300)
+    fem3, *_ = _fem_and_oracle(ctx, X3, tets3, "nh", f"fanchunk300s_{nt}")
+    with pytest.raises(EbbError, match="EBB_E_RANGE"):
+        fem3.map_forces("nh", scatter=SCATTERS["chunk"])

@@ -30,10 +30,10 @@ def _oracle_map(case, m, order, tet_src, model, u=None):
                               e=m.e, ne=m.ne)
 
 
-SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4, "color": 5}
+SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4, "color": 5, "chunk": 6}
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color", "chunk"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 @pytest.mark.parametrize("n,mesh", [(4, "kuhn6"), (9, "kuhn6"), (4, "alt5")])
 def test_map_fp64(ctx, model, n, mesh, scatter):
@@ -48,7 +48,7 @@ def test_map_fp64(ctx, model, n, mesh, scatter):
     assert ctx.error_counts(reset=True)["inverted"] == 0
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color", "chunk"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 def test_map_fp32_displacement_form(ctx, model, scatter):
     case = Case(n=8, model=model, spread=0.1)
@@ -128,7 +128,7 @@ def test_tiled_map_tile_sizes(ctx, tile, scatter, monkeypatch):
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color"])
+@pytest.mark.parametrize("scatter", ["atomic", "tiled", "gather", "segmented", "color", "chunk"])
 def test_map_accumulates_without_zeroing(ctx, scatter):
     """zero_outputs = 0 is the paper's `+=` into existing fields."""
     case = Case(n=4, model="stvk")
@@ -216,3 +216,72 @@ def test_color_map_is_bitwise_deterministic(ctx):
     f1, K1 = fem.f.read(), fem.K.read()
     fem.map_forces("nh", scatter=SCATTERS["color"])
     assert np.array_equal(fem.f.read(), f1) and np.array_equal(fem.K.read(), K1)
+
+
+def test_chunk_map_is_bitwise_deterministic(ctx):
+    """The chunk strategy sums in plan order (own blocks, then the messages by
+    sender tile) whatever the timing: reruns are bitwise identical."""
+    case = Case(n=12, model="nh")
+    fem = gpu_fem(ctx, case, name="mdet6")
+    fem.map_forces("nh", scatter=SCATTERS["chunk"])
+    f1, K1, e1 = fem.f.read(), fem.K.read(), fem.energy.get()
+    for _ in range(3):
+        fem.map_forces("nh", scatter=SCATTERS["chunk"])
+        assert np.array_equal(fem.f.read(), f1) and np.array_equal(fem.K.read(), K1)
+        assert fem.energy.get() == e1
+
+
+@pytest.mark.parametrize("nt", ["128", "256", "384", "512"])
+@pytest.mark.parametrize("model,dtype", [("nh", "f64"), ("stvk", "f64"), ("nh", "f32"), ("stvk", "f32")])
+def test_chunk_tile_sizes(ctx, nt, model, dtype, monkeypatch):
+    """Every tile size (tets per CTA) gives the oracle's result: n=9 -> 4374
+    tets over 9..35 tiles, the last one ragged, rows spanning many tiles."""
+    monkeypatch.setenv("EBB_CHUNK_NT", nt)
+    case = Case(n=9, model=model, spread=0.1)
+    if dtype == "f32":
+        case.u = case.u.astype(np.float32).astype(np.float64)
+        case.mu = case.mu.astype(np.float32).astype(np.float64)
+        case.lam = case.lam.astype(np.float32).astype(np.float64)
+    fem = gpu_fem(ctx, case, dtype=dtype, name=f"mchunk{nt}{model}{dtype}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, model)
+    fem.map_forces(model, scatter=SCATTERS["chunk"])
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    assert rel_l2(fem.f.read(), f) <= tol
+    assert rel_l2(fem.K.read(), K) <= tol
+    assert abs(fem.energy.get() - en) <= tol * abs(en)
+
+
+@pytest.mark.parametrize("grid", ["1", "2", "5"])
+def test_chunk_few_ctas(ctx, grid, monkeypatch):
+    """One CTA (every tile processed in order by itself: its messages are all
+    from its own earlier tiles) and a few CTAs claiming hundreds of tiles each
+    (tile queue, entry buffers and the register pipeline wrapping many times)
+    give the oracle's result, bitwise equal to the full grid."""
+    case = Case(n=16, model="nh", spread=0.1)
+    fem = gpu_fem(ctx, case, name=f"mchunkgrid{grid}")
+    fem.map_forces("nh", scatter=SCATTERS["chunk"])
+    f_full, K_full = fem.f.read(), fem.K.read()
+    monkeypatch.setenv("EBB_CHUNK_GRID", grid)
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, "nh")
+    fem.map_forces("nh", scatter=SCATTERS["chunk"])
+    assert rel_l2(fem.f.read(), f) <= 1e-12
+    assert rel_l2(fem.K.read(), K) <= 1e-12
+    assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+    assert np.array_equal(fem.f.read(), f_full) and np.array_equal(fem.K.read(), K_full)
+
+
+def test_chunk_plan_stats(ctx):
+    """The CHUNK plan computes every tet once: 10 block entries per tet over
+    ceil(T / NT) tiles; messages are the segments of rows owned by a later
+    tile (fewer than the segments); the plan is built on the device."""
+    case = Case(n=10, model="nh")
+    fem = gpu_fem(ctx, case, name="chunkstats")
+    fem.map_forces("nh", scatter=SCATTERS["chunk"])
+    st = fem.chunk_stats()
+    assert st["tets_per_tile"] in (128, 256, 384, 512)
+    assert st["tiles"] == -(-fem.nt // int(st["tets_per_tile"]))
+    assert fem.ne <= st["segments"] <= 10 * fem.nt
+    assert 0 < st["messages"] < st["segments"]
+    assert st["zero_rows"] == 0 and st["plan_bytes_per_tet"] > 0

@@ -35,7 +35,7 @@ def main():
     ctx = ebb.Context(0)
     fem = TetFEM(ctx, X, tets, dtype=a.dtype, mu=mu, lam=lam, free=free, u=S.twist_u(X, a.n, 6, free=free))
     sid = {"atomic": A.SCATTER_ATOMIC, "tiled": A.SCATTER_TILED, "gather": A.SCATTER_GATHER,
-           "segmented": A.SCATTER_SEGMENTED}[a.scatter]
+           "segmented": A.SCATTER_SEGMENTED, "chunk": A.SCATTER_CHUNK}[a.scatter]
     for _ in range(a.reps):
         fem.map_forces(a.model, scatter=sid)
     torch.cuda.synchronize()

@@ -1,22 +1,27 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the Ebb tet-FEM hot path on B200 (one JSON line).
 
-Workload (BASELINE.json configs[1], the config its metric is quoted on that
-fits one GPU): neo-Hookean implicit backward-Euler step with 50 Jacobi-PCG
-iterations on the 1M-tet subdivided cube (Kuhn-6, n=55: 998,250 tets), fp64.
-A "step" is one pass of the whole hot path: element
+Workload (BASELINE.json north_star "Target": a 10^7-tet neo-Hookean mesh, the
+map and the CG of its implicit solve): neo-Hookean implicit backward-Euler
+step with 50 Jacobi-PCG iterations on the Kuhn-6 subdivided cube n=119
+(10,110,954 tets, 1,728,000 vertices, 25,575,838 edge rows), fp64.  A "step"
+is one pass of the whole hot path: element
 force+stiffness map, system assembly, PCG init + 50 iterations, state update.
+The C2 workload (BASELINE configs[1], n=55, 998,250 tets) is measured in the
+same run as a component.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 value = tets advanced through one full step per second (tet-steps/s), summed
-over ranks; components report the map in tets/s and the CG in iterations/s.
+over ranks; the metric's two quantities are top-level too: "map" (tets/s of
+the force+stiffness map, fraction of HBM peak) and "cg" (PCG iterations/s,
+fraction of HBM peak on the algorithmic and on the ncu-measured DRAM bytes).
 --impl reference times the CPU oracle (the reference arm of this tier) on a
-bounded sample of the same workload.  Under torchrun (N > 1) the global mesh is
-a Kuhn cube with round(55 N^(1/3)) cells per side (~1M tets per GPU, weak
+bounded sample of the workload.  Under torchrun (N > 1) the global mesh is a
+Kuhn cube with round(119 N^(1/3)) cells per side (~10M tets per GPU, weak
 scaling), partitioned by the O4 owner maps; each rank runs the distributed
-implicit step (paper_1506_07577_b200.dist: ghost tets, z halo and the p.q /
-r.z allreduces over NCCL) -- DESIGN.md §7.
+implicit step (paper_1506_07577_b200.dist: ghost tets, u halo and one fused
+2-scalar allreduce per PCG iteration over NCCL) -- DESIGN.md §7.
 """
 from __future__ import annotations
 
@@ -32,9 +37,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "tets/sec (force+stiffness map) and CG iters/sec at 1/2/4/8 B200; % HBM roofline"
-WORKLOAD = dict(name="C2", n=55, model="nh", E=2e5, nu=0.3, rho=1e3, h=1e-2, cg_iters=50, order_seed=2, u_seed=1)
-SAMPLE_N = 55          # oracle: the full C2 workload (about 6 s per step on one host core)
-CPU_BASELINE_STEPS = 4 # ~12-25 s of oracle work for the cpu_baseline field (3-6 s per step)
+# E scaled as 1/n^2 keeps h^2 E n^2 / rho ~ 60 (the C2 conditioning, DESIGN §3 reading 14); the
+# stretch is ramped off the fixed wall (wall_ramp): the plain C2 recipe's wall shear (~0.05 n)
+# would invert tets at n = 119 (C5 note)
+WORKLOAD = dict(name="T10M", n=119, model="nh", E=2e5 * (55 / 119) ** 2, nu=0.3, rho=1e3, h=1e-2, cg_iters=50,
+                order_seed=2, u_seed=1, wall_ramp=0.1)
+C2 = dict(name="C2", n=55, model="nh", E=2e5, nu=0.3, rho=1e3, h=1e-2, cg_iters=50, order_seed=2, u_seed=1,
+          wall_ramp=0.0)
+SAMPLE_N = 55          # oracle sample: the same recipe on the 1/10-size n=55 cube (3-6 s per step, one core)
+CPU_BASELINE_STEPS = 3 # ~10-20 s of oracle work for the cpu_baseline field
 FLUSH_BYTES = 256 << 20
 
 
@@ -48,13 +59,15 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def _ncu_traffic(kernel):
+def _ncu_traffic(kernel, workload):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture of this bench's workload (tools/ncu_traffic.py), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d[kernel]
-        if e.get("workload") == WORKLOAD["name"]:
+        e = d.get(f"{workload}:{kernel}") or d[kernel]
+        if e.get("workload") == workload:
             return float(e["dram_bytes_per_launch"])
     except Exception:
         pass
@@ -143,7 +156,7 @@ def cpu_baseline(steps=CPU_BASELINE_STEPS):
     import numpy as np
 
     import oracle
-    w = WORKLOAD
+    w = C2
     X, tets, free, u, mu, lam = make_case(SAMPLE_N, w["order_seed"], w["u_seed"], w["E"], w["nu"])
     m = oracle.Mesh(X, tets, rho=w["rho"])
     v = np.zeros_like(u)
@@ -154,9 +167,9 @@ def cpu_baseline(steps=CPU_BASELINE_STEPS):
     dt = time.perf_counter() - t0
     T = tets.shape[0]
     return {"value": T * steps / dt, "unit": "tets/s", "cores": 1, "kind": "oracle",
-            "sample": f"{steps} full implicit NH step(s) (map + assembly + 50 PCG iterations) of the C2 "
-                      f"workload itself (Kuhn-6 n={SAMPLE_N}, {T} tets); single-threaded C oracle "
-                      f"(gcc -O2, generic 4th-order stiffness tensor)",
+            "sample": f"{steps} full implicit NH step(s) (map + assembly + 50 PCG iterations) of the same "
+                      f"recipe on the 1/10-size Kuhn-6 n={SAMPLE_N} cube ({T} tets: the C2 workload); "
+                      f"single-threaded C oracle (gcc -O2, generic 4th-order stiffness tensor)",
             "seconds": dt}
 
 
@@ -167,7 +180,7 @@ def run_reference(args, rank, world):
     import numpy as np
 
     import oracle
-    w = WORKLOAD
+    w = C2
     X, tets, free, u, mu, lam = make_case(SAMPLE_N, w["order_seed"], w["u_seed"], w["E"], w["nu"])
     m = oracle.Mesh(X, tets, rho=w["rho"])
     v = np.zeros_like(u)
@@ -181,8 +194,8 @@ def run_reference(args, rank, world):
     T = tets.shape[0]
     val = T * args.steps / dt
     cb = {"value": val, "unit": "tets/s", "cores": 1, "kind": "oracle",
-          "sample": f"each step = one implicit NH step (map + assembly + 50 PCG its) of the C2 workload itself "
-                    f"(Kuhn-6 n={SAMPLE_N}, {T} tets); single-threaded C oracle"}
+          "sample": f"each step = one implicit NH step (map + assembly + 50 PCG its) of the same recipe on the "
+                    f"1/10-size Kuhn-6 n={SAMPLE_N} cube ({T} tets); single-threaded C oracle"}
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tets/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -192,39 +205,28 @@ def run_reference(args, rank, world):
     print(json.dumps(line))
 
 
-def _config(world, sample=False):
+def _config(world, sample=False, n=None):
     from synth import mesh as M
-    n = SAMPLE_N if sample else WORKLOAD["n"]
+    n = SAMPLE_N if sample else (n or WORKLOAD["n"])
     T, V, U, E = M.kuhn_counts(n)
-    return {"workload": f"C2: neo-Hookean implicit backward-Euler step + 50 Jacobi-PCG iterations, Kuhn-6 "
-                        f"subdivided cube n={n} ({T} tets, {V} verts, {E} edge rows), fp64"
-                        + (" [CPU oracle]" if sample else ""),
+    return {"workload": f"{WORKLOAD['name']} (BASELINE north_star target): neo-Hookean implicit backward-Euler "
+                        f"step + 50 Jacobi-PCG iterations, Kuhn-6 subdivided cube n={n} ({T} tets, {V} verts, "
+                        f"{E} edge rows), fp64"
+                        + (f" [CPU oracle on the 1/10-size n={SAMPLE_N} sample]" if sample else ""),
             "tets": T, "verts": V, "edge_rows": E, "h": WORKLOAD["h"], "cg_iters": WORKLOAD["cg_iters"],
-            "E_young": WORKLOAD["E"], "nu": WORKLOAD["nu"],
-            "l2": "flushed between timed steps (256 MiB write); per-step working set ~0.5 GB > 126 MB L2",
-            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (weak)"}
+            "E_young": WORKLOAD["E"], "nu": WORKLOAD["nu"], "wall_ramp": WORKLOAD["wall_ramp"],
+            "l2": "flushed between timed steps (256 MiB write); per-step working set ~5 GB > 126 MB L2",
+            "parallelism": "single GPU" if world == 1 else f"{world} GPUs, domain decomposition (weak)"}
 
 
-def run_ours(args, rank, world, local_rank):
-    import numpy as np
+def _measure(ctx, fem, w, stream, flush, steps, warmup, use_graph, world=1, clocks_device=None):
+    """W warm-up steps, then K timed steps (one CUDA graph per step), L2 flushed
+    between steps outside the events; per-kernel times from the library's
+    event records (graph event nodes)."""
     import torch
     import torch.distributed as dist
 
     from paper_1506_07577_b200 import _abi as A
-    from paper_1506_07577_b200 import build as B
-    from paper_1506_07577_b200 import ebb
-    from paper_1506_07577_b200.tetfem import TetFEM
-
-    B.build()
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    w = WORKLOAD
-    X, tets, free, u0, mu, lam = make_case(w["n"], w["order_seed"], w["u_seed"], w["E"], w["nu"])
-    ctx = ebb.Context(local_rank)
-    fem = TetFEM(ctx, X, tets, dtype="f64", mu=mu, lam=lam, rho=w["rho"], free=free, u=u0, name="bench")
-    T, V, E = fem.nt, fem.nv, fem.ne
-    stream = torch.cuda.Stream(device=dev)
-    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def step():
         fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"], stream=stream)
@@ -234,14 +236,14 @@ def run_ours(args, rank, world, local_rank):
     while time.perf_counter() - t_pre < 0.5:
         step()
         torch.cuda.synchronize()
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     ctx.error_counts(reset=True)
     ctx.timing(True)
     ctx.timing_read(0, reset=True)
     graph = None
-    if not args.no_graph:
+    if use_graph:
         # one implicit step captured as a CUDA graph (kernel timers become graph
         # event nodes: each replay re-records them)
         ctx.graph_begin(stream)
@@ -262,12 +264,12 @@ def run_ours(args, rank, world, local_rank):
     if graph is None:
         ctx.timing_read(0, reset=True)
     ctx.launch_count(reset=True)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        for k in range(args.steps):
+    with ClockSampler(clocks_device if clocks_device is not None else 0) as clk:
+        for k in range(steps):
             with torch.cuda.stream(stream):
                 flush.zero_()                          # L2 flush, outside the timed events
             evs[k][0].record(stream)
@@ -291,11 +293,61 @@ def run_ours(args, rank, world, local_rank):
             kt[name] = {"total_ms": ms, "launches": n}
     for v in kt.values():
         v["avg_us"] = 1e3 * v["total_ms"] / max(v["launches"], 1)
-    errs = ctx.error_counts(reset=True)
-    if world > 1:
-        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+    ctx.timing(False)
+    return {"t_ms": t_ms, "kt": kt, "launches": launches, "clocks": clk.summary(),
+            "errors": ctx.error_counts(reset=True), "graph": graph, "run_step": run_step}
+
+
+def _components(fem, w, kt, t_ms, peak, workload_name):
+    """The metric's two quantities (map tets/s, CG iterations/s) with their
+    fractions of HBM peak (SURVEY §8(d) algorithmic bytes; the CG also on the
+    DRAM bytes ncu measured for this workload, when captured)."""
+    T, V, E = fem.nt, fem.nv, fem.ne
+    mv, mp, cs = kt["edge_matvec"], kt["tet_map"], kt["cg_solve"]
+    iters = w["cg_iters"]
+    b_map, b_it = bytes_map(T, V, E), bytes_cg_iter(V, E)
+    if cs["launches"]:
+        cg_it_us = cs["avg_us"] / iters
+    else:
+        cg_it_us = mv["avg_us"] + kt["cg_update"]["avg_us"] + kt["cg_dir"]["avg_us"]
+    dram = _ncu_traffic("cg_solve", workload_name)
+    cg = {"iters_per_s": 1e6 / cg_it_us, "iter_us": cg_it_us,
+          "hbm_frac": b_it / (cg_it_us * 1e-6) / 1e9 / peak, "bytes_per_iter": b_it,
+          "variant": {1: "saad (k_cg_persistent)", 2: "single-reduction (k_cg1_persistent)",
+                      3: "symmetric (k_cg_sym_persistent)"}.get(fem.cg_variant(), "?")}
+    if dram is not None and cs["launches"]:
+        cg["dram_bytes_per_iter"] = dram / iters
+        cg["hbm_frac_dram"] = dram / (cs["avg_us"] * 1e-6) / 1e9 / peak
+    return {
+        "map": {"tets_per_s": T / (mp["avg_us"] * 1e-6), "avg_us": mp["avg_us"],
+                "hbm_frac": b_map / (mp["avg_us"] * 1e-6) / 1e9 / peak, "bytes": b_map,
+                "kernel": "k_tet_map_seg (SEGMENTED)"},
+        "cg": cg,
+        "ms_per_step": t_ms,
+    }
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_1506_07577_b200 import build as B
+    from paper_1506_07577_b200 import ebb
+    from paper_1506_07577_b200.tetfem import TetFEM
+
+    B.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = WORKLOAD
+    X, tets, free, u0, mu, lam = make_case(w["n"], w["order_seed"], w["u_seed"], w["E"], w["nu"],
+                                           wall_ramp=w["wall_ramp"])
+    ctx = ebb.Context(local_rank)
+    fem = TetFEM(ctx, X, tets, dtype="f64", mu=mu, lam=lam, rho=w["rho"], free=free, u=u0, name="bench")
+    del X, tets
+    T, V, E = fem.nt, fem.nv, fem.ne
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    M_ = _measure(ctx, fem, w, stream, flush, args.steps, args.warmup, not args.no_graph, world, local_rank)
+    t_ms, kt, graph, run_step = M_["t_ms"], M_["kt"], M_["graph"], M_["run_step"]
     value = world * T * args.steps / (t_ms / 1e3)
 
     # ---- end to end through the public API: host state in, step, host state out
@@ -318,10 +370,6 @@ def run_ours(args, rank, world, local_rank):
         b.record(stream)
         b.synchronize()
         e2e_ms += a.elapsed_time(b)
-    if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
     e2e = {"value": world * T * args.steps / (e2e_ms / 1e3), "unit": "tets/s",
            "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
            "api": "ebb_field_write (pinned host u, v) -> implicit step (TetFEM.implicit_step as captured graph) -> "
@@ -329,7 +377,6 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (largest share of the timed step)
     peak, peak_src = _peaks()
-    mv, mp, cs = kt["edge_matvec"], kt["tet_map"], kt["cg_solve"]
     iters = w["cg_iters"]
     b_mv, b_map, b_it = bytes_matvec(V, E), bytes_map(T, V, E), bytes_cg_iter(V, E)
     shares = {k: v["total_ms"] / t_ms for k, v in kt.items()}
@@ -340,36 +387,52 @@ def run_ours(args, rank, world, local_rank):
     d = kt[dom]
     ach = per_launch[dom] / (d["avg_us"] * 1e-6) / 1e9
     cgk = "k_cg1_persistent (single-reduction PCG" if fem.cg_variant() == 2 else "k_cg_persistent (Saad PCG"
+    traffic = _ncu_traffic(dom, w["name"])
     roof = {"kernel": {"cg_solve": cgk + ", all 50 iterations in one launch)",
                        "edge_matvec": "k_spmv_tma", "tet_map": "k_tet_map_seg"}[dom],
             "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "peak_source": peak_src, "traffic": _ncu_traffic(dom), "algorithmic_bytes_per_launch": per_launch[dom],
+            "peak_source": peak_src, "traffic": traffic, "algorithmic_bytes_per_launch": per_launch[dom],
             "bytes_model": "SURVEY 8(d): PCG iteration = E(9 b_f + 4) + V(4 + 6 b_f) + 33 V b_f, x 50 iterations"
                            if dom == "cg_solve" else "SURVEY 8(d)",
             "avg_launch_us": d["avg_us"], "share_of_step": shares[dom]}
-    if cs["launches"]:
-        cg_it_us = cs["avg_us"] / iters
-    else:
-        cg_it_us = mv["avg_us"] + kt["cg_update"]["avg_us"] + kt["cg_dir"]["avg_us"]
-    comps = {
-        "map": {"tets_per_s": T / (mp["avg_us"] * 1e-6), "avg_us": mp["avg_us"],
-                "hbm_frac": b_map / (mp["avg_us"] * 1e-6) / 1e9 / peak, "bytes": b_map},
-        "cg": {"iters_per_s": 1e6 / cg_it_us, "iter_us": cg_it_us,
-               "hbm_frac": b_it / (cg_it_us * 1e-6) / 1e9 / peak, "bytes_per_iter": b_it},
-        "kernel_times": kt, "shares": shares,
-    }
+    if traffic is not None:
+        roof["frac_dram_measured"] = traffic / (d["avg_us"] * 1e-6) / 1e9 / peak
+        roof["traffic_source"] = "profiles/ncu_traffic.json (ncu --set full capture of this workload)"
+    comps = _components(fem, w, kt, t_ms / args.steps, peak, w["name"])
+    comps.update({"kernel_times": kt, "shares": shares})
+    launches, clocks, errs = M_["launches"], M_["clocks"], M_["errors"]
+    ctx.close()
+    del fem
+
+    # ---- C2 (BASELINE configs[1], 1M tets) as a component, same method
+    c2 = None
+    if not args.no_c2:
+        wc = C2
+        Xc, tc, fc, uc, muc, lamc = make_case(wc["n"], wc["order_seed"], wc["u_seed"], wc["E"], wc["nu"])
+        ctx2 = ebb.Context(local_rank)
+        fem2 = TetFEM(ctx2, Xc, tc, dtype="f64", mu=muc, lam=lamc, rho=wc["rho"], free=fc, u=uc, name="benchc2")
+        steps2 = max(3, min(args.steps, 10))
+        M2 = _measure(ctx2, fem2, wc, stream, flush, steps2, max(3, args.warmup), not args.no_graph, 1, local_rank)
+        c2 = _components(fem2, wc, M2["kt"], M2["t_ms"] / steps2, peak, "C2")
+        c2.update({"workload": "C2 (BASELINE configs[1]): Kuhn-6 n=55, 998,250 tets, NH implicit step + 50 PCG "
+                               "iterations, fp64", "steps": steps2,
+                   "tets_per_s": fem2.nt * steps2 / (M2["t_ms"] / 1e3)})
+        ctx2.close()
+        del fem2
+
     line = {"metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Kuhn-6 cube, stretch+noise displacement, no external meshes)",
             "config": dict(_config(world), launch="one CUDA graph per step" if graph is not None else "eager"),
+            "map": comps["map"], "cg": comps["cg"],
             "roofline": roof, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "components": comps, "device_errors": errs}
+            "clocks": clocks, "components": {"kernel_times": kt, "shares": shares, "c2": c2},
+            "device_errors": errs}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(line))
-    ctx.close()
 
 
 def run_dist(args, rank, world, local_rank):
@@ -502,6 +565,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of a CUDA graph")
+    ap.add_argument("--no-c2", action="store_true", help="skip the C2 (1M-tet) component measurement")
     ap.add_argument("--dist-cg", default="single", choices=["single", "saad"],
                     help="PCG driver of the multi-GPU path (single: one fused allreduce per iteration)")
     ap.add_argument("--dist", action="store_true",

@@ -4,6 +4,8 @@ capture of the bench command -> profiles/ncu_traffic.json (read by bench.py
 for the roofline `traffic` field).
 
     python tools/ncu_traffic.py <capture.ncu-rep> [workload=C2]
+
+Entries are keyed "<workload>:<kernel>" (bench.py looks up its own workload).
 """
 import collections
 import csv
@@ -40,7 +42,7 @@ def main():
             v = [x for x in v if "k_cg" not in x[1]]
             if not v:
                 continue
-        res[key] = {"workload": workload, "dram_bytes_per_launch": sum(x[0] for x in v) / len(v),
+        res[f"{workload}:{key}"] = {"workload": workload, "dram_bytes_per_launch": sum(x[0] for x in v) / len(v),
                     "launches_captured": len(v), "ncu_kernel": v[0][1][:100], "capture": os.path.basename(path),
                     "ncu_duration_each": [x[2] for x in v],
                     "note": "ncu --set full --clock-control none (replayed, cold cache per pass)"}

@@ -27,7 +27,7 @@ STVK, NH = 0, 1
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED, SCATTER_GATHER, SCATTER_SEGMENTED, SCATTER_COLOR, SCATTER_CHUNK = \
     0, 1, 2, 3, 4, 5, 6
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
-CG_DIR, CG_MATVEC, CG_UPDATE = 0, 1, 2
+CG_DIR, CG_MATVEC, CG_UPDATE, CG_SR_PHASE = 0, 1, 2, 3
 K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE, K_CG_SOLVE, K_SPRING, K_EBE_MATVEC, K_GRID = \
     0, 1, 2, 3, 4, 5, 6, 7, 8
 

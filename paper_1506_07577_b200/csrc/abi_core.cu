@@ -240,10 +240,14 @@ __global__ void k_lower_bound_index(const uint32_t* __restrict__ sorted, uint64_
     index[s] = (uint32_t)lo;
 }
 
-__global__ void k_max_range(const uint32_t* __restrict__ index, uint64_t ns, unsigned int* out) {
-    uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (s < ns) atomicMax(out, index[s + 1] - index[s]);
+__global__ void k_index_stats(const uint32_t* __restrict__ index, uint64_t ns, unsigned int* out) {
+    const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    atomicMax(out, index[s + 1] - index[s]);
+    if (s % 16 == 0) atomicMax(out + 1, index[s + 16 < ns ? s + 16 : ns] - index[s]);
+    if (s % 64 == 0) atomicMax(out + 2, index[s + 64 < ns ? s + 64 : ns] - index[s]);
 }
+
 
 }  // namespace
 
@@ -262,6 +266,20 @@ ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_
     ebb_status st = add_field(c, rel, name.c_str(), dt, rows, cols, layout, p, true, out);
     if (st != EBB_OK && p) cudaFree(p);
     return st;
+}
+
+ebb_status index_stats(Ctx* c, const uint32_t* index, uint64_t ns, uint32_t out[3]) {
+    unsigned int* d = nullptr;
+    EBB_CUDA(c, cudaMalloc(&d, 16));
+    cudaError_t e = cudaMemset(d, 0, 16);
+    if (e == cudaSuccess && ns) {
+        k_index_stats<<<grid_for(ns, 256), 256>>>(index, ns, d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, 12, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(c, e, "index_stats");
+    return EBB_OK;
 }
 
 void release_plans(Ctx* c) {
@@ -856,17 +874,15 @@ ebb_status ebb_group_by(ebb_ctx ctx, ebb_rel rel, ebb_field key) {
     Sr = get_rel(c, src);
     K = get_field(c, key);
     k_lower_bound_index<<<grid_for(ns + 1, 256), 256>>>((const uint32_t*)K->ptr, n, (uint32_t*)c->fields[idx].ptr, ns);
-    DevBuf mx;
-    EBB_CUDA(c, cudaMalloc(&mx.p, 4));
-    EBB_CUDA(c, cudaMemset(mx.p, 0, 4));
-    k_max_range<<<grid_for(ns, 256), 256>>>((const uint32_t*)c->fields[idx].ptr, ns, (unsigned int*)mx.p);
-    unsigned int hmx = 0;
-    EBB_CUDA(c, cudaMemcpy(&hmx, mx.p, 4, cudaMemcpyDeviceToHost));
+    uint32_t st[3];
+    EBB_TRY(index_stats(c, (const uint32_t*)c->fields[idx].ptr, ns, st));
     R->grouped_by = key;
     R->index = idx;
-    R->max_group = hmx;
+    R->max_group = st[0];
+    R->max_chunk16 = st[1];
+    R->max_chunk64 = st[2];
     Sr->index = idx;
-    Sr->max_group = hmx;
+    Sr->max_group = st[0];
     return EBB_OK;
 }
 

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <string>
@@ -39,6 +40,8 @@ struct Relation {
     ebb_field grouped_by = EBB_NONE;   // key-field this relation is grouped by
     ebb_field index = EBB_NONE;        // hidden CSR index on the source
     uint32_t max_group = 0;            // longest range of an index on this relation
+    uint32_t max_chunk16 = 0;          // most rows of 16 consecutive sources (a TMA matvec chunk)
+    uint32_t max_chunk64 = 0;          // most rows of 64 consecutive sources (register matvec chunk)
     // regular 2-D grid (ebb_grid2_new): dims, kind (1 = cells, 2 = dual cells)
     // and the other relation of the same grid
     uint32_t dims[2] = {0, 0};
@@ -238,9 +241,13 @@ struct EdgeGraph {
     const uint32_t* index = nullptr;
     const uint32_t* head = nullptr;
     uint32_t max_group = 0;
+    uint32_t max_chunk16 = 0, max_chunk64 = 0;   // rows of the largest 16- / 64-source chunk
     ebb_rel verts = EBB_NONE;
 };
 ebb_status edge_graph(Ctx* c, ebb_rel edges, EdgeGraph* g);   // solver.cu
+// longest group, and most rows of any 16 / 64 consecutive groups of a CSR
+// index with ns groups (synchronous; abi_core.cu)
+ebb_status index_stats(Ctx* c, const uint32_t* index, uint64_t ns, uint32_t out[3]);
 
 size_t dtype_size(ebb_dtype d);
 ebb_status fail(Ctx* c, ebb_status code, const char* fmt, ...);
@@ -296,7 +303,18 @@ struct DeviceGuard {
     DeviceGuard(const DeviceGuard&) = delete;
     DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
-#define EBB_DEVICE_GUARD(c) ::ebb::DeviceGuard _ebb_device_guard(c)
+// NVTX range around every C-ABI call (the runtime reports where time
+// goes; SURVEY §5 tracing), named after the entry point: nvtxRangePushA is a
+// null-pointer check unless a tool (nsys, ncu --nvtx) injects itself.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define EBB_DEVICE_GUARD(c)                          \
+    ::ebb::NvtxRange _ebb_nvtx_range(__func__);      \
+    ::ebb::DeviceGuard _ebb_device_guard(c)
 
 #define EBB_TRY(call)                  \
     do {                               \

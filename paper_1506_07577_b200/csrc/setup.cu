@@ -207,10 +207,6 @@ __global__ void k_self_edges(uint64_t nv, const uint32_t* __restrict__ index, co
     if (v < nv) self[v] = find_row(index, head, (uint32_t)v, (uint32_t)v);
 }
 
-__global__ void k_max_range(const uint32_t* __restrict__ index, uint64_t ns, unsigned int* out) {
-    uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (s < ns) atomicMax(out, index[s + 1] - index[s]);
-}
 
 // a3: rest data.  Dminv stored component-planar: plane (3r + c) holds row r col c.
 __global__ void k_rest(const uint32_t* __restrict__ tv, const double* __restrict__ X, uint64_t nt, double rho,
@@ -428,17 +424,15 @@ ebb_status ebb_tetmesh_build(ebb_ctx ctx, ebb_field tets_v, const char* edges_na
     EBB_TRY(new_internal_field(c, irel, std::string("__index_") + edges_name, EBB_U32, 1, 1, EBB_AOS, &idx));
     k_lower_bound<<<grid_for(nv + 1, 256), 256>>>((const uint32_t*)c->fields[tail].ptr, ne,
                                                   (uint32_t*)c->fields[idx].ptr, nv);
-    DevBuf mx;
-    EBB_CUDA(c, cudaMalloc(&mx.p, 4));
-    EBB_CUDA(c, cudaMemset(mx.p, 0, 4));
-    k_max_range<<<grid_for(nv, 256), 256>>>((const uint32_t*)c->fields[idx].ptr, nv, (unsigned int*)mx.p);
-    unsigned int hmx = 0;
-    EBB_CUDA(c, cudaMemcpy(&hmx, mx.p, 4, cudaMemcpyDeviceToHost));
+    uint32_t st[3];
+    EBB_TRY(index_stats(c, (const uint32_t*)c->fields[idx].ptr, nv, st));
     c->rels[edges].grouped_by = tail;
     c->rels[edges].index = idx;
-    c->rels[edges].max_group = hmx;
+    c->rels[edges].max_group = st[0];
+    c->rels[edges].max_chunk16 = st[1];
+    c->rels[edges].max_chunk64 = st[2];
     c->rels[verts].index = idx;
-    c->rels[verts].max_group = hmx;
+    c->rels[verts].max_group = st[0];
     // tets.e[4][4] and verts.self
     char ename[64];
     snprintf(ename, sizeof(ename), "e_%s", edges_name);

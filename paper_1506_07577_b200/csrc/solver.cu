@@ -1436,20 +1436,32 @@ ebb_status edge_graph(Ctx* c, ebb_rel edges, EdgeGraph* g) {
     g->index = (const uint32_t*)c->fields[E->index].ptr;
     g->head = (const uint32_t*)H->ptr;
     g->max_group = E->max_group;
+    g->max_chunk16 = E->max_chunk16 ? E->max_chunk16 : TMA_VCH * E->max_group;
+    g->max_chunk64 = E->max_chunk64 ? E->max_chunk64 : SPMV_VC * E->max_group;
     return EBB_OK;
 }
 }  // namespace ebb
 
 namespace {
 
+// Stage capacity (rows) of the TMA-fed matvecs: the rows of the largest
+// 16-vertex chunk (measured per chunk at grouping time, not 16 x the longest
+// group: one hub vertex no longer inflates every stage) + the 16-byte
+// alignment slack of the 9 plane copies and the head copy.
+template <typename R>
+uint32_t tma_cap(uint32_t chunk_rows) {
+    return (chunk_rows ? chunk_rows : 1u) + 2 * (16 / sizeof(R)) + 4;
+}
+constexpr size_t kTmaSmemMax = 200 * 1024;   // beyond it: the warp-per-vertex path (no staging)
+
 template <typename R, bool CG, bool MPQ, bool DIR = false>
 ebb_status launch_tma(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask, double* pq_out,
                       unsigned int* counter, cudaStream_t s, R* pb0 = nullptr, R* pb1 = nullptr,
                       double* scal = nullptr) {
-    const uint32_t cap = (uint32_t)(TMA_VCH * (G.max_group ? G.max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+    const uint32_t cap = tma_cap<R>(G.max_chunk16);
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * TMA_NS;
-    if (smem > 200 * 1024) return EBB_E_SIZE;   // caller falls back to the register path
+    if (smem > kTmaSmemMax) return EBB_E_SIZE;   // caller falls back to a path without staging
     // consumer layout: grouped 8 lanes per vertex (default, measured faster:
     // DESIGN.md §5.3); EBB_SPMV_GRP=0 selects 16 lanes per vertex
     static const bool grp = !(getenv("EBB_SPMV_GRP") && getenv("EBB_SPMV_GRP")[0] == '0');
@@ -1594,7 +1606,7 @@ ebb_status cg_sym_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters
     const uint8_t* mask;
     EBB_TRY(check_mask(c, cg->mask, G.verts, &mask));
     auto F = [&](ebb_field f) { return (R*)c->fields[f].ptr; };
-    const uint32_t cap = (uint32_t)(TMA_VCH * (U->max_group ? U->max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+    const uint32_t cap = tma_cap<R>(U->max_chunk16);
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * TMA_NS;
     if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
@@ -1656,7 +1668,7 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     auto F = [&](ebb_field f) { return (R*)c->fields[f].ptr; };
     const uint8_t* mask;
     EBB_TRY(check_mask(c, cg->mask, G.verts, &mask));
-    const uint32_t cap = (uint32_t)(TMA_VCH * (G.max_group ? G.max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+    const uint32_t cap = tma_cap<R>(G.max_chunk16);
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * CG1_NS;
     if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
@@ -1716,7 +1728,7 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     const char* mode = getenv("EBB_CG");
     if (only_phase < 0 && iters > 0 && !(mode && mode[0] == '2')) {
         // single launch, all iterations (cooperative: every CTA resident)
-        const uint32_t cap = (uint32_t)(TMA_VCH * (G.max_group ? G.max_group : 1) + 2 * (16 / sizeof(R)) + 4);
+        const uint32_t cap = tma_cap<R>(G.max_chunk16);
         const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
         const size_t smem = stage * TMA_NS;
         if (smem <= 200 * 1024) {

@@ -234,7 +234,11 @@ ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field 
 #define EBB_STVK 0
 #define EBB_NH 1
 #define EBB_SCATTER_AUTO 0      /* the measured fastest: SEGMENTED (f + K);
-                                   force-only maps use ATOMIC */
+                                   force-only maps use ATOMIC.
+                                   A mesh whose SEGMENTED plan is refused
+                                   (EBB_E_RANGE: a vertex in more tets than a
+                                   tile holds) runs CHUNK, else ATOMIC; the
+                                   choice is made once per (v, e).           */
 #define EBB_SCATTER_ATOMIC 1    /* per-tet red.global.add              */
 #define EBB_SCATTER_TILED 2     /* owner tiles, shared-memory atomic
                                    accumulation of every block                */

@@ -295,6 +295,7 @@ void release_plans(Ctx* c) {
         delete P;
     }
     c->chunkplans.clear();
+    c->auto_map.clear();
     for (ColorPlan* P : c->colorplans) {
         P->release();
         delete P;

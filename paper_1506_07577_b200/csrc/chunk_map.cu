@@ -956,6 +956,11 @@ int chunk_threads(ebb_dtype dt, int model) {
     return v;
 }
 
+ebb_status chunk_plan_probe(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, int model) {
+    ChunkPlan* P;
+    return build_chunk_plan(c, vf, ef, chunk_threads(dt, model), &P);
+}
+
 ebb_status chunk_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
                             const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                             const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,

@@ -159,6 +159,7 @@ struct UpperCSR {
     ebb_rel edges = EBB_NONE;
     uint64_t nu = 0;
     uint32_t max_group = 0;
+    uint32_t max_chunk16 = 0;   // rows of the largest 16-vertex chunk of the upper triangle
     uint32_t* uptr = nullptr;   // nverts + 1
     uint32_t* uhead = nullptr;  // nu
     uint32_t* usrc = nullptr;   // nu: row of the full relation
@@ -194,6 +195,8 @@ struct Ctx : ebb_ctx_s {
     std::vector<MapPlan> plans;     // invalidated by any relation permutation
     std::vector<SegPlan*> segplans; // (same)
     std::vector<ChunkPlan*> chunkplans; // (same)
+    struct AutoMap { ebb_field v, e; int strategy; };
+    std::vector<AutoMap> auto_map;      // AUTO's strategy per (v, e) mesh (same lifetime as the plans)
     std::vector<ColorPlan*> colorplans; // (same)
     std::vector<UpperCSR*> uppers;      // (same)
     void* comm = nullptr;               // ncclComm_t (comm.cu)
@@ -270,6 +273,9 @@ ebb_status chunk_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool 
                             const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                             const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
                             cudaStream_t s);
+// build the SEGMENTED / CHUNK plan for (v, e) if absent (EBB_E_RANGE: refused)
+ebb_status seg_plan_probe(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, int model);
+ebb_status chunk_plan_probe(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, int model);
 // color_map.cu: the COLOURED element map (builds its colouring on first use)
 ebb_status color_map_launch(Ctx* c, ebb_field vf, int model, bool want_e, uint64_t nt, const Field* V,
                             const Field* Ef, const Field* U, const Field* D, const Field* W, const Field* MU,

@@ -715,6 +715,11 @@ int seg_threads(ebb_dtype dt, int model) {
     return (dt == EBB_F64 && model == EBB_STVK) ? 384 : 256;   // measured
 }
 
+ebb_status seg_plan_probe(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, int model) {
+    SegPlan* P;
+    return build_seg_plan(c, vf, ef, seg_threads(dt, model), &P);
+}
+
 ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
                           const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                           const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,

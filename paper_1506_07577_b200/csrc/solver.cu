@@ -365,6 +365,107 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
 
 
 // ---------------------------------------------------------------------------
+// Edge-relation matvec without any staging: one warp per vertex, lanes stride
+// its rows (any group length: the fallback when the largest chunk does not fit
+// the TMA stages or the register path's shared memory, e.g. a hub vertex of
+// thousands of edges).  Same modes and outputs as k_spmv_tma (CG padded
+// records, DIR direction update formed on the fly, MPQ mask + fused p.q).
+template <typename R, bool CG, bool MPQ, bool DIR>
+__global__ void __launch_bounds__(256) k_spmv_warp(uint64_t nv, const uint32_t* __restrict__ index,
+                                                   const uint32_t* __restrict__ head, const R* __restrict__ A,
+                                                   uint64_t ne, const R* __restrict__ p, R* __restrict__ q,
+                                                   const uint8_t* __restrict__ mask, double* __restrict__ partials,
+                                                   unsigned int* __restrict__ counter, double* __restrict__ pq_out,
+                                                   R* pbuf0, R* pbuf1, double* __restrict__ scal) {
+    if (DIR && scal[S_DONE] != 0.0) return;   // PCG converged (tolerance mode): no-op
+    const unsigned lane = threadIdx.x & 31;
+    const R* __restrict__ pold = nullptr;
+    R* __restrict__ pnew = nullptr;
+    R beta = 0;
+    if (DIR) {
+        const int cur = scal[S_PAR] != 0.0;
+        pold = cur ? pbuf1 : pbuf0;
+        pnew = cur ? pbuf0 : pbuf1;
+        const double rho = scal[S_RHO], rz = scal[S_RZ];
+        beta = (scal[S_FIRST] != 0.0 || rho == 0.0) ? R(0) : (R)(rz / rho);
+    }
+    auto gather = [&](uint64_t hv, R& px, R& py, R& pz) {
+        if (DIR) {
+            const auto zv = ld4(p, hv);
+            const auto ov = ld4(pold, hv);
+            px = zv.x + beta * ov.x;
+            py = zv.y + beta * ov.y;
+            pz = zv.z + beta * ov.z;
+        } else if (CG) {
+            const auto pv = ld4(p, hv);
+            px = pv.x;
+            py = pv.y;
+            pz = pv.z;
+        } else {
+            px = p[3 * hv];
+            py = p[3 * hv + 1];
+            pz = p[3 * hv + 2];
+        }
+    };
+    double pq = 0.0;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = wid; v < nv; v += nw) {
+        R a0 = 0, a1 = 0, a2 = 0;
+        for (uint32_t r = index[v] + lane; r < index[v + 1]; r += 32) {
+            R px, py, pz;
+            gather(head[r], px, py, pz);
+            a0 += A[r] * px + A[ne + r] * py + A[2 * ne + r] * pz;
+            a1 += A[3 * ne + r] * px + A[4 * ne + r] * py + A[5 * ne + r] * pz;
+            a2 += A[6 * ne + r] * px + A[7 * ne + r] * py + A[8 * ne + r] * pz;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        }
+        if (lane == 0) {
+            R own0 = 0, own1 = 0, own2 = 0;
+            if (MPQ) gather(v, own0, own1, own2);
+            if (MPQ && mask && !mask[v]) a0 = a1 = a2 = 0;
+            if (CG) {
+                typename V4<R>::T qv;
+                qv.x = a0;
+                qv.y = a1;
+                qv.z = a2;
+                qv.w = 0;
+                st4(q, v, qv);
+                if (DIR) {
+                    typename V4<R>::T pv;
+                    pv.x = own0;
+                    pv.y = own1;
+                    pv.z = own2;
+                    pv.w = 0;
+                    st4(pnew, v, pv);
+                }
+            } else {
+                q[3 * v] = a0;
+                q[3 * v + 1] = a1;
+                q[3 * v + 2] = a2;
+            }
+            if (MPQ) pq += (double)own0 * a0 + (double)own1 * a1 + (double)own2 * a2;
+        }
+    }
+    if (MPQ) {
+        double tot;
+        if (block_sum_last_done(pq, partials, counter, &tot)) {
+            *pq_out = tot;
+            if (DIR) {
+                scal[S_RHO] = scal[S_RZ];
+                scal[S_FIRST] = 0.0;
+                scal[S_PAR] = scal[S_PAR] != 0.0 ? 0.0 : 1.0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Persistent PCG (single GPU): all `iters` iterations in one cooperative
 // launch.  Every CTA runs the warp-specialized TMA matvec of k_spmv_tma over
 // its chunks, then a software grid barrier, then the vector update over a
@@ -1448,9 +1549,11 @@ namespace {
 // 16-vertex chunk (measured per chunk at grouping time, not 16 x the longest
 // group: one hub vertex no longer inflates every stage) + the 16-byte
 // alignment slack of the 9 plane copies and the head copy.
+// (a multiple of 4 rows: every plane of a stage starts 16-byte aligned, as
+// the bulk copies require)
 template <typename R>
 uint32_t tma_cap(uint32_t chunk_rows) {
-    return (chunk_rows ? chunk_rows : 1u) + 2 * (16 / sizeof(R)) + 4;
+    return ((chunk_rows ? chunk_rows : 1u) + 2 * (16 / sizeof(R)) + 4 + 3) & ~3u;
 }
 constexpr size_t kTmaSmemMax = 200 * 1024;   // beyond it: the warp-per-vertex path (no staging)
 
@@ -1481,6 +1584,17 @@ ebb_status launch_tma(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, 
     return EBB_OK;
 }
 
+template <typename R, bool CG, bool MPQ, bool DIR>
+ebb_status launch_spmv_warp(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask,
+                            double* pq_out, unsigned int* counter, cudaStream_t s, R* pb0 = nullptr,
+                            R* pb1 = nullptr, double* scal = nullptr) {
+    const unsigned grid = occ_grid(c, k_spmv_warp<R, CG, MPQ, DIR>, 256, 0, G.nv * 32);
+    k_spmv_warp<R, CG, MPQ, DIR><<<grid, 256, 0, s>>>(G.nv, G.index, G.head, A, G.ne, p, q, mask, c->d_partials,
+                                                      counter, pq_out, pb0, pb1, scal);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
 // matvec on AOS vec3 p, q (the ebb_map_edge_matvec ABI and the K v of assembly)
 template <typename R, bool MPQ>
 ebb_status launch_spmv3(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q, const uint8_t* mask, double* pq_out,
@@ -1491,7 +1605,8 @@ ebb_status launch_spmv3(Ctx* c, const EdgeGraph& G, const R* A, const R* p, R* q
         ebb_status st = launch_tma<R, false, MPQ>(c, G, A, p, q, mask, pq_out, counter, s);
         if (st != EBB_E_SIZE) return st;
     }
-    const size_t smem = (size_t)SPMV_VC * (G.max_group ? G.max_group : 1) * 3 * sizeof(R);
+    const size_t smem = (size_t)(G.max_chunk64 ? G.max_chunk64 : 1) * 3 * sizeof(R);   // rows of the largest chunk
+    if (smem > kTmaSmemMax) return launch_spmv_warp<R, false, MPQ, false>(c, G, A, p, q, mask, pq_out, counter, s);
     if (smem > 48 * 1024)
         EBB_CUDA(c, cudaFuncSetAttribute(k_spmv<R, MPQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned grid = occ_grid(c, k_spmv<R, MPQ>, 256, smem, ((G.nv + SPMV_VC - 1) / SPMV_VC) * 256);
@@ -1525,7 +1640,7 @@ ebb_status check_mask(Ctx* c, ebb_field m, ebb_rel rel, const uint8_t** out) {
 }
 
 
-int cg_variant(const ebb_cg* cg, uint64_t nv, ebb_dtype dt);
+int cg_variant(const ebb_cg* cg, const EdgeGraph& G, ebb_dtype dt);
 
 // upper-triangle CSR of `edges` (cached until the next relation permutation)
 ebb_status upper_csr(Ctx* c, ebb_rel edges, const EdgeGraph& G, UpperCSR** out) {
@@ -1575,6 +1690,13 @@ ebb_status upper_csr(Ctx* c, ebb_rel edges, const EdgeGraph& G, UpperCSR** out) 
         delete U;
         return cuda_fail(c, e, "upper_csr");
     }
+    uint32_t st[3];
+    if (index_stats(c, U->uptr, nv, st) != EBB_OK) {
+        U->release();
+        delete U;
+        return EBB_E_CUDA;
+    }
+    U->max_chunk16 = st[1];
     c->uppers.push_back(U);
     *out = U;
     return EBB_OK;
@@ -1609,7 +1731,7 @@ ebb_status cg_sym_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters
     const uint32_t cap = tma_cap<R>(U->max_chunk16);
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * TMA_NS;
-    if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
+    if (smem > kTmaSmemMax) return EBB_E_SIZE;   // the caller falls back to Saad
     static thread_local size_t configured_dev[kMaxDevices] = {};
     size_t& configured = configured_dev[c->device % kMaxDevices];
     if (smem > configured) {
@@ -1671,7 +1793,7 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     const uint32_t cap = tma_cap<R>(G.max_chunk16);
     const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
     const size_t smem = stage * CG1_NS;
-    if (smem > 200 * 1024) return fail(c, EBB_E_RANGE, "cg: a vertex group too long for the streamed matvec");
+    if (smem > kTmaSmemMax) return EBB_E_SIZE;   // the caller falls back to Saad
     static thread_local size_t configured_dev[kMaxDevices] = {};
     size_t& configured = configured_dev[c->device % kMaxDevices];
     if (smem > configured) {
@@ -1721,9 +1843,15 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     double* scal = (double*)c->fields[cg->scal].ptr;
     double* rho_user = (double*)c->fields[cg->rho].ptr;
     const unsigned ug = occ_grid(c, k_cg_update<R>, 256, 0, G.nv);
-    const int variant = cg_variant(cg, G.nv, sizeof(R) == 8 ? EBB_F64 : EBB_F32);
+    const int variant = cg_variant(cg, G, sizeof(R) == 8 ? EBB_F64 : EBB_F32);
     if (only_phase < 0 && iters > 0 && variant == EBB_CG_SINGLE_REDUCTION) return cg1_launch<R>(c, cg, G, iters, s);
-    if (only_phase == EBB_CG_SR_PHASE) return cg1_launch<R>(c, cg, G, 1, s, 1);
+    if (only_phase == EBB_CG_SR_PHASE) {
+        const ebb_status st = cg1_launch<R>(c, cg, G, 1, s, 1);
+        if (st == EBB_E_SIZE)
+            return fail(c, EBB_E_RANGE, "cg: single-reduction phase: the largest 16-vertex chunk (%u rows) does not "
+                                        "fit the TMA stages (use the Saad phases)", G.max_chunk16);
+        return st;
+    }
     if (only_phase < 0 && iters > 0 && variant == EBB_CG_SYMMETRIC) return cg_sym_launch<R>(c, cg, G, iters, s);
     const char* mode = getenv("EBB_CG");
     if (only_phase < 0 && iters > 0 && !(mode && mode[0] == '2')) {
@@ -1731,7 +1859,7 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
         const uint32_t cap = tma_cap<R>(G.max_chunk16);
         const size_t stage = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
         const size_t smem = stage * TMA_NS;
-        if (smem <= 200 * 1024) {
+        if (smem <= kTmaSmemMax) {
             static thread_local size_t configured_dev[kMaxDevices] = {};
             size_t& configured = configured_dev[c->device % kMaxDevices];
             if (smem > configured) {
@@ -1770,8 +1898,12 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
         // EBB_CG_DIR is fused into the matvec (p = z + beta p_old gathered on the fly)
         if (only_phase < 0 || only_phase == EBB_CG_MATVEC) {
             KernelTimer kt(c, EBB_K_EDGE_MATVEC, s);
-            EBB_TRY((launch_tma<R, true, true, true>(c, G, A, z, q, mask, scal + S_PQ, c->d_counter + 1, s, p, p2,
-                                                     scal)));
+            ebb_status st = launch_tma<R, true, true, true>(c, G, A, z, q, mask, scal + S_PQ, c->d_counter + 1, s, p,
+                                                            p2, scal);
+            if (st == EBB_E_SIZE)   // the largest chunk does not fit the stages: no staging
+                st = launch_spmv_warp<R, true, true, true>(c, G, A, z, q, mask, scal + S_PQ, c->d_counter + 1, s, p,
+                                                           p2, scal);
+            EBB_TRY(st);
         }
         if (only_phase < 0 || only_phase == EBB_CG_UPDATE) {
             KernelTimer kt(c, EBB_K_CG_UPDATE, s);
@@ -1787,12 +1919,23 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
 // kernel saves a grid barrier and a gathered vector per iteration but moves
 // ~9 owner-local vector records per vertex; it wins while they stay in L2
 // (C2: 1M tets, fp64) and loses once they stream from HBM (1e7 tets).
-int cg_variant(const ebb_cg* cg, uint64_t nv, ebb_dtype dt) {
-    if (cg->variant != EBB_CG_AUTO) return cg->variant;
-    const char* e = getenv("EBB_CG_VARIANT");
-    if (e && atoi(e) >= EBB_CG_SAAD && atoi(e) <= EBB_CG_SYMMETRIC) return atoi(e);
-    (void)dt;   // measured crossover (fp64 and fp32 alike): between 1.8e5 and 3.0e5 vertices
-    return nv <= 232000 ? EBB_CG_SINGLE_REDUCTION : EBB_CG_SAAD;
+int cg_variant(const ebb_cg* cg, const EdgeGraph& G, ebb_dtype dt) {
+    int v = cg->variant;
+    if (v == EBB_CG_AUTO) {
+        const char* e = getenv("EBB_CG_VARIANT");
+        if (e && atoi(e) >= EBB_CG_SAAD && atoi(e) <= EBB_CG_SYMMETRIC) v = atoi(e);
+        // measured crossover (fp64 and fp32 alike): between 1.8e5 and 3.0e5 vertices
+        else v = G.nv <= 232000 ? EBB_CG_SINGLE_REDUCTION : EBB_CG_SAAD;
+    }
+    // a variant whose ring of TMA stages (sized by the largest 16-vertex chunk)
+    // does not fit runs as Saad, which has a path without staging
+    if (v == EBB_CG_SINGLE_REDUCTION || v == EBB_CG_SYMMETRIC) {
+        const size_t bf = dt == EBB_F64 ? 8 : 4;
+        const size_t cap = ((G.max_chunk16 ? G.max_chunk16 : 1) + 2 * (16 / bf) + 4 + 3) & ~(size_t)3;
+        const size_t stage = (9 * cap * bf + cap * 4 + 127) & ~(size_t)127;
+        if (stage * (v == EBB_CG_SINGLE_REDUCTION ? CG1_NS : TMA_NS) > kTmaSmemMax) v = EBB_CG_SAAD;
+    }
+    return v;
 }
 
 ebb_status cg_validate(Ctx* c, const ebb_cg* cg, EdgeGraph* G, ebb_dtype* dt) {
@@ -1974,7 +2117,7 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
         return fail(c, EBB_E_ARG, "cg: unknown variant %d", cg->variant);
     ebb_field* work[] = {&cg->r, &cg->p, &cg->z, &cg->q, &cg->dinv, &cg->p2, &cg->s, &cg->y, &cg->w, &cg->u, &cg->u2};
     const char* wn[] = {"r", "p", "z", "q", "dinv", "p2", "s", "y", "w", "u", "u2"};
-    const int nwork = cg_variant(cg, G.nv, dt) == EBB_CG_SINGLE_REDUCTION ? 11 : 6;
+    const int nwork = cg_variant(cg, G, dt) == EBB_CG_SINGLE_REDUCTION ? 11 : 6;
     int id = -1;
     for (int i = 0; i < nwork; ++i) {
         Field* W = *work[i] == EBB_NONE ? nullptr : get_field(c, *work[i]);
@@ -2016,7 +2159,7 @@ ebb_status ebb_cg_init(ebb_ctx ctx, ebb_cg* cg, ebb_stream stream) {
     else EBB_INIT(float);
 #undef EBB_INIT
     EBB_CUDA(c, cudaGetLastError());
-    if (cg_variant(cg, G.nv, dt) == EBB_CG_SYMMETRIC) {
+    if (cg_variant(cg, G, dt) == EBB_CG_SYMMETRIC) {
         if (dt == EBB_F64) return cg_sym_prepare<double>(c, cg, G, s);
         return cg_sym_prepare<float>(c, cg, G, s);
     }
@@ -2045,7 +2188,7 @@ ebb_status ebb_cg_variant(ebb_ctx ctx, const ebb_cg* cg, int32_t* out) {
     EdgeGraph G;
     ebb_dtype dt;
     EBB_TRY(cg_validate(c, cg, &G, &dt));
-    *out = cg_variant(cg, G.nv, dt);
+    *out = cg_variant(cg, G, dt);
     return EBB_OK;
 }
 

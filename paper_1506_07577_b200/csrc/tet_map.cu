@@ -1206,9 +1206,33 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     int strat = d->scatter;
     // AUTO = the measured fastest on C2 and C3: SEGMENTED for
     // f + K (every dtype and model); the force-only map is the atomic kernel
+    const bool auto_pick = strat == EBB_SCATTER_AUTO && !(envs && atoi(envs) > 0);
     if (strat == EBB_SCATTER_AUTO) {
         if (envs && atoi(envs) > 0) strat = atoi(envs);
         else strat = EBB_SCATTER_SEGMENTED;
+    }
+    if (auto_pick && Ko) {
+        // AUTO on a mesh whose plan the segmented map refuses (a vertex in more
+        // tets than a tile holds): CHUNK, else ATOMIC -- decided once per (v, e)
+        for (const auto& a : c->auto_map)
+            if (a.v == d->v && a.e == d->e) strat = a.strategy;
+        if (strat == EBB_SCATTER_SEGMENTED) {
+            bool known = false;
+            for (const auto& a : c->auto_map) known |= a.v == d->v && a.e == d->e;
+            if (!known) {
+                const int cand[3] = {EBB_SCATTER_SEGMENTED, EBB_SCATTER_CHUNK, EBB_SCATTER_ATOMIC};
+                for (int k = 0; k < 3; ++k) {
+                    ebb_status st = EBB_OK;
+                    if (cand[k] == EBB_SCATTER_SEGMENTED) st = seg_plan_probe(c, d->v, d->e, dt, d->model);
+                    if (cand[k] == EBB_SCATTER_CHUNK) st = chunk_plan_probe(c, d->v, d->e, dt, d->model);
+                    if (st == EBB_E_RANGE) continue;
+                    EBB_TRY(st);
+                    strat = cand[k];
+                    break;
+                }
+                c->auto_map.push_back({d->v, d->e, strat});
+            }
+        }
     }
     if (Ko && strat == EBB_SCATTER_COLOR) {
         // plain read-modify-write per colour: the outputs start from zero or accumulate

@@ -241,3 +241,75 @@ def test_chunk_hub_vertex(ctx, nt, monkeypatch):
     fem3, *_ = _fem_and_oracle(ctx, X3, tets3, "nh", f"fanchunk300s_{nt}")
     with pytest.raises(EbbError, match="EBB_E_RANGE"):
         fem3.map_forces("nh", scatter=SCATTERS["chunk"])
+
+
+def _pcg_case(ctx, X, tets, free, name, variant, iters, rho=1e3, noise=1e-3, ramp=None):
+    """GPU map + assembly + PCG(iters) with the requested variant, and the
+    oracle's implicit step (O9 + O10) on the same input, both in stored order."""
+    from paper_1506_07577_b200.tetfem import TetFEM
+    rng = np.random.default_rng(4)
+    w = np.ones(X.shape[0]) if ramp is None else ramp     # smooth onset of the stretch off the fixed set
+    u = (0.02 * X * np.array([1.0, -0.5, 0.3]) * w[:, None] + rng.uniform(-noise, noise, size=X.shape)) * free[:, None]
+    mu, lam = S.materials(tets.shape[0], 2e5, 0.3, spread=0.1)
+    fem = TetFEM(ctx, X, tets, dtype="f64", mu=mu, lam=lam, rho=rho, free=free, u=u, name=name)
+    new_of_old, tet_src, tets_new = oracle.renumber(X, tets)
+    order = np.argsort(new_of_old)
+    m = oracle.Mesh(X[order], tets_new, rho=rho)
+    ref = oracle.implicit_step(m, "nh", u[order], np.zeros_like(u), mu[tet_src], lam[tet_src], free[order], 1e-2,
+                               iters=iters)
+    fem.map_forces("nh")
+    fem.assemble(1e-2)
+    fem.cg_init(variant=variant)
+    fem.cg_step(iters)
+    return fem, ref
+
+
+@pytest.mark.parametrize("k", [200, 1500])
+@pytest.mark.parametrize("variant", [1, 2, 3])
+def test_pcg_hub_vertex(ctx, k, variant):
+    """A hub vertex in k tets (a fan): the PCG stages are sized by the largest
+    16-vertex chunk, not 16 x the longest group.  k = 200 fits every variant's
+    TMA ring; k = 1500 (a 1,503-row group) fits none: single-reduction and
+    symmetric resolve to Saad (reported by ebb_cg_variant), whose matvec then
+    runs without staging (one warp per vertex).  Every case reproduces the
+    oracle's 30 PCG iterations (<= 1e-8), never EBB_E_RANGE."""
+    X, tets = _fan(k)
+    ang = np.arctan2(X[:, 1], X[:, 0])
+    free = (~((X[:, 2] == 0) & (np.abs(ang) < 0.6) & (np.hypot(X[:, 0], X[:, 1]) > 0.5))).astype(np.uint8)
+    # sliver tets (ring spacing 2 pi / k): the stretch ramps in smoothly away
+    # from the fixed arc and the noise stays far below the spacing
+    ramp = np.clip((np.abs(ang) - 0.6) / 0.5, 0.0, 1.0)
+    ramp[X[:, 2] != 0] = 1.0
+    ramp[np.hypot(X[:, 0], X[:, 1]) < 0.5] = 1.0
+    fem, ref = _pcg_case(ctx, X, tets, free, f"pcghub{k}_{variant}", variant, 30, noise=1e-5, ramp=ramp)
+    assert np.isfinite(ref["dv"]).all() and ref["inverted"] == 0
+    assert rel_l2(fem.dv.read(), ref["dv"]) <= 1e-8
+    assert fem.cg_variant() == (variant if k == 200 else 1)
+
+
+def test_matvec_hub_without_staging(ctx):
+    """A 9,000-tet fan: the hub's group (9,003 rows) exceeds both the TMA
+    stages and the register path's shared memory; ebb_map_edge_matvec runs
+    the warp-per-vertex path and equals the oracle's edge-relation matvec."""
+    X, tets = _fan(9000)
+    fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, "nh", "mvhub9000")
+    rng = np.random.default_rng(8)
+    fem.K.write(rng.uniform(-1, 1, size=(fem.ne, 9)))   # any matrix on the edge relation
+    K = fem.K.read()
+    p = rng.uniform(-1, 1, size=(fem.nv, 3))
+    P = fem.verts.field("p_hub", "f64", (3, 1), init=p)
+    Q = fem.verts.field("q_hub", "f64", (3, 1))
+    fem.matvec(fem.K, P, Q)
+    ref = oracle.edge_matvec(m.row_ptr, m.head, K, p)
+    assert rel_l2(Q.read(), ref) <= 1e-13
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3])
+def test_pcg_blob(ctx, variant):
+    """C3-style blob (irregular metaball boundary, low-degree boundary
+    vertices, ~20k tets): every PCG variant reproduces the oracle's 50
+    iterations to <= 1e-8."""
+    X, tets, n = M.blob(target_T=20_000)
+    free = S.fixed_mask(X, n)
+    fem, ref = _pcg_case(ctx, X, tets, free, f"pcgblob{variant}", variant, 50)
+    assert rel_l2(fem.dv.read(), ref["dv"]) <= 1e-8

@@ -136,15 +136,22 @@ def renumber(X, tets):
 
 
 # ---------------------------------------------------------------- O4
-def partition(nv, tets, P, tail=None):
+def partition(nv, tets, P, tail=None, mode="own"):
     """O4 tet-first SFC partition into P parts (plain numpy bookkeeping).
 
     owner_t(t) = floor(t P / T); owner_v(v) = owner_t(min{t : v in t}) or
-    floor(v P / V) for isolated vertices; ghosts of p = vertices of p's tets
-    not owned by p (ascending); send[p][q] = vertices owned by p that are
-    ghosts on q (ascending); edge rows owned by owner_v(tail); local numbering
-    = owned ascending then ghosts ascending.
+    floor(v P / V) for isolated vertices.  Local tets of part p:
+      mode="own"      the tets p owns (owner_t == p) -- SURVEY §8(e) O4;
+      mode="overlap"  every tet with a vertex owned by p (the ghost-tet
+                      decomposition: every row of an owned
+                      vertex is then complete on p without a reverse add).
+    ghosts of p = vertices of p's local tets not owned by p (ascending);
+    send[p][q] = vertices owned by p that are ghosts on q (ascending); edge
+    rows owned by owner_v(tail); local numbering = owned ascending then ghosts
+    ascending; ltets[p] = p's local tets (ascending).
     """
+    if mode not in ("own", "overlap"):
+        raise ValueError(mode)
     tets = _i64(tets)
     T = tets.shape[0]
     owner_t = (np.arange(T, dtype=np.int64) * P) // max(T, 1)
@@ -157,18 +164,23 @@ def partition(nv, tets, P, tail=None):
     iso = first == T
     owner_v[~iso] = owner_t[first[~iso]]
     owner_v[iso] = (np.nonzero(iso)[0] * P) // max(nv, 1)
-    ghosts, local = [], []
+    ghosts, local, ltets = [], [], []
     for p in range(P):
-        vs = np.unique(tets[owner_t == p].ravel())
+        if mode == "own":
+            lt = np.nonzero(owner_t == p)[0]
+        else:
+            lt = np.array([t for t in range(T) if any(owner_v[v] == p for v in tets[t])], dtype=np.int64)
+        vs = np.unique(tets[lt].ravel())
         g = vs[owner_v[vs] != p]
         ghosts.append(g)
+        ltets.append(lt)
         local.append(np.concatenate([np.nonzero(owner_v == p)[0], g]))
     send = [[None] * P for _ in range(P)]
     for p in range(P):
         for q in range(P):
             gq = ghosts[q]
             send[p][q] = gq[owner_v[gq] == p] if p != q else np.zeros(0, np.int64)
-    out = dict(owner_t=owner_t, owner_v=owner_v, ghosts=ghosts, send=send, local=local)
+    out = dict(owner_t=owner_t, owner_v=owner_v, ghosts=ghosts, send=send, local=local, ltets=ltets)
     if tail is not None:
         out["owner_e"] = owner_v[_i64(tail)]
     return out

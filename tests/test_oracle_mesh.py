@@ -203,3 +203,42 @@ def test_blob_generator_is_valid():
     m = oracle.Mesh(X, tets)
     assert m.swaps == 0 and np.all(m.W > 0)
     assert np.all(np.bincount(m.tets.ravel(), minlength=m.nv) > 0)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+def test_partition_overlap_invariants(P):
+    """O4, overlapping decomposition: p's local tets are exactly the tets with
+    an owned vertex, so every tet incident to an owned vertex -- every block
+    of every owned edge row -- is local (no reverse add needed).  Ghosts are
+    characterised independently through the edge relation (O2): the
+    neighbours of owned vertices that p does not own."""
+    X, tets = M.kuhn6(4)
+    X, tets = M.permute_vertices(X, tets, 3)
+    m = oracle.Mesh(X, tets)
+    part = oracle.partition(m.nv, m.tets, P, mode="overlap")
+    own = oracle.partition(m.nv, m.tets, P)
+    ov = part["owner_v"]
+    assert np.array_equal(ov, own["owner_v"]) and np.array_equal(part["owner_t"], own["owner_t"])
+    for p in range(P):
+        owned = np.nonzero(ov == p)[0]
+        lt = part["ltets"][p]
+        incident = np.nonzero(np.isin(m.tets, owned).any(axis=1))[0]
+        assert np.array_equal(lt, incident)
+        nb = set()
+        for v in owned:                                  # edge-relation neighbours of owned vertices
+            nb |= set(m.head[m.row_ptr[v]:m.row_ptr[v + 1]].tolist())
+        assert part["ghosts"][p].tolist() == sorted(nb - set(owned.tolist()))
+        assert np.array_equal(part["local"][p][:owned.size], owned)
+        for q in range(P):
+            s = part["send"][p][q]
+            assert list(s) == sorted(s)
+            if p != q:
+                assert set(s.tolist()) == set(part["ghosts"][q].tolist()) & set(owned.tolist())
+    # a tet is local exactly on the parts owning one of its vertices (so an
+    # owned tet whose vertices all belong to lower parts is not local on its
+    # owner: owner_v is the owner of the vertex's lowest tet)
+    for t in range(m.nt):
+        on = {p for p in range(P) if t in set(part["ltets"][p].tolist())}
+        assert on == set(ov[m.tets[t]].tolist())
+    if P == 1:
+        assert part["ghosts"][0].size == 0 and part["ltets"][0].size == m.nt

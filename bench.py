@@ -455,13 +455,14 @@ def run_dist(args, rank, world, local_rank):
     # stretch ramped off the wall: the plain recipe's wall shear (~0.05 n) inverts tets at large n
     X, tets, free, u0, mu, lam = make_case(n, w["order_seed"], w["u_seed"], E_n, w["nu"], wall_ramp=0.1)
     ctx = ebb.Context(local_rank)
-    G = D.global_partition(ctx, X, tets, world, name="global")
-    plan = D.halo_plan(G["tets"], G["owner_v"], world)
-    tord = G["tet_order"]
-    order = G["vert_order"]
+    # this rank's local problem from the device partition (the global mesh is
+    # freed again; only local-size arrays come back to the host)
+    t_part = time.perf_counter()
+    part = D.partition_rank(ctx, X, tets, world, rank, name="global")
     stream = torch.cuda.Stream(device=dev)
-    R = D.GpuRank(ctx, rank, G["X"], G["tets"], G["owner_v"], plan, free[order], u0[order],
-                  np.zeros_like(u0), mu[tord], lam[tord], rho=w["rho"], stream=stream, name=f"rank{rank}")
+    R = D.GpuRank(ctx, rank, part, X, free, u0, np.zeros_like(u0), mu, lam, rho=w["rho"], stream=stream,
+                  name=f"rank{rank}")
+    t_part = time.perf_counter() - t_part
     # NCCL inside the library (ebb_comm_*); no fallback: a failure here ends the run
     T = D.NcclTransport(ctx, rank, world, stream=stream)
     transport = "nccl (in-library, ebb_comm_*)"
@@ -538,7 +539,7 @@ def run_dist(args, rank, world, local_rank):
             "unit": "GB/s", "frac": b_mv / (avg_mv * 1e-6) / 1e9 / peak, "peak_source": peak_src, "traffic": None,
             "algorithmic_bytes_per_launch": b_mv, "avg_launch_us": avg_mv, "rank": rank}
     cfg = _config(world)
-    cfg.update({"workload": f"C2 recipe weak-scaled: Kuhn-6 n={n} ({T_global} tets, {X.shape[0]} verts) split over "
+    cfg.update({"workload": f"{WORKLOAD['name']} recipe weak-scaled: Kuhn-6 n={n} ({T_global} tets, {X.shape[0]} verts) split over "
                             f"{world} GPUs by the O4 owner maps (ghost tets; per PCG iteration "
                             + ("one fused 2-scalar allreduce + u halo, single-reduction phases"
                                if cg_var == "single" else "z halo + 2 scalar allreduces, Saad phases")
@@ -551,7 +552,8 @@ def run_dist(args, rank, world, local_rank):
             "e2e": {"value": value, "unit": "tets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                     "note": "multi-GPU line: state stays resident on the devices"},
             "components": {"map_avg_us": 1e3 * mp_ms / max(mp_n, 1), "matvec_avg_us": avg_mv,
-                           "local_tets": int(R.fem.nt), "local_verts": int(V_loc)}}
+                           "local_tets": int(R.fem.nt), "local_verts": int(V_loc),
+                           "owned_verts": int(part["n_owned"]), "partition_setup_s": t_part}}
     if rank == 0:
         print(json.dumps(line))
     ctx.close()

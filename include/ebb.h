@@ -563,6 +563,47 @@ ebb_status ebb_kinetic_energy(ebb_ctx ctx, ebb_field mass, ebb_field qd, ebb_fie
 ebb_status ebb_partition(ebb_ctx ctx, ebb_field tets_v, int32_t nparts,
                          ebb_field owner_t, ebb_field owner_v);
 
+/* The local problem of rank `rank` of an nparts-way decomposition (SURVEY
+ * §8(e): "vertex-owned shards with ghost layers"; O4 and its overlapping
+ * reading), built on the device from the owner maps of
+ * ebb_partition (owner_t, owner_v: I32 on tets / verts of tets_v):
+ *   mode EBB_PART_OVERLAP  local tets = every tet with a vertex the rank owns
+ *                          (ghost tets: every block of every owned edge row
+ *                          is local, so the element map needs no reverse add);
+ *   mode EBB_PART_OWN      local tets = the tets the rank owns (O4).
+ * Local vertices: the owned ones ascending (global id), then the ghosts
+ * (vertices of local tets owned elsewhere) ascending; local tets ascending.
+ * Halo lists: send to peer q = owned vertices that are ghosts on q, recv from
+ * q = ghosts owned by q, both as local rows in ascending global id (the two
+ * ends of a pair derive the same order).  Creates relations name.ltets,
+ * name.lverts, name.send, name.recv (the last two only if non-empty) with
+ * U32 fields "gid" (global ids), the 4x1 key-field ltets."v" -> lverts, and
+ * U32 "rows" (local vertex rows) on send / recv grouped by peer: rows of peer
+ * q are [send_ptr[q], send_ptr[q+1]) (host arrays of nparts+1 entries, filled
+ * here; same for recv_ptr).  EBB_E_SIZE if the rank's local mesh is empty.
+ * Synchronous. */
+#define EBB_PART_OVERLAP 0
+#define EBB_PART_OWN 1
+typedef struct {
+    ebb_rel ltets, lverts, send, recv;   /* created relations (send/recv NONE if empty) */
+    ebb_field tet_gid, vert_gid;         /* U32: global id of each local tet / vertex   */
+    ebb_field v;                         /* ltets 4x1 key -> lverts (local tets.v)      */
+    ebb_field send_rows, recv_rows;      /* U32 local vertex rows, grouped by peer      */
+    uint64_t n_ltets, n_lverts, n_owned; /* lverts [0, n_owned) are the owned vertices  */
+} ebb_partition_info;
+ebb_status ebb_partition_local(ebb_ctx ctx, ebb_field tets_v, ebb_field owner_t, ebb_field owner_v,
+                               int32_t nparts, int32_t rank, int32_t mode, const char* name,
+                               ebb_partition_info* out, uint64_t* send_ptr, uint64_t* recv_ptr);
+
+/* Lifetime (a rank frees the global mesh it partitioned).  field_free: frees
+ * the column (borrowed memory is left alone); EBB_E_STATE if the field groups
+ * or indexes a relation.  relation_free: frees every field of the relation
+ * and its hidden group index; EBB_E_STATE while a key-field of another live
+ * relation targets it.  Both drop every cached plan.  The handles become
+ * invalid (EBB_E_ARG on use).  Synchronous. */
+ebb_status ebb_field_free(ebb_ctx ctx, ebb_field f);
+ebb_status ebb_relation_free(ebb_ctx ctx, ebb_rel rel);
+
 #ifdef __cplusplus
 }
 #endif

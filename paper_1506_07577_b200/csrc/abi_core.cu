@@ -52,7 +52,7 @@ Field* get_field(Ctx* c, ebb_field f) {
 }
 
 Relation* get_rel(Ctx* c, ebb_rel r) {
-    if (!c || r >= c->rels.size()) return nullptr;
+    if (!c || r >= c->rels.size() || !c->rels[r].alive) return nullptr;
     return &c->rels[r];
 }
 
@@ -540,7 +540,7 @@ ebb_status ebb_relation_new(ebb_ctx ctx, const char* name, uint64_t size, ebb_re
     if (!c || !name || !out) return fail(c, EBB_E_ARG, "null argument");
     if (size == 0) return fail(c, EBB_E_SIZE, "relation '%s' has zero size", name);
     for (auto& R : c->rels)
-        if (R.name == name) return fail(c, EBB_E_DUP, "relation '%s' already exists", name);
+        if (R.alive && R.name == name) return fail(c, EBB_E_DUP, "relation '%s' already exists", name);
     Relation R;
     R.name = name;
     R.size = size;

@@ -47,6 +47,7 @@ struct Relation {
     uint32_t dims[2] = {0, 0};
     int grid_kind = 0;
     ebb_rel grid_peer = EBB_NONE;
+    bool alive = true;                 // false after ebb_relation_free
 };
 
 // Scatter plan of the tiled element map (built once per mesh, tet_map.cu):

@@ -8,6 +8,10 @@ Decomposition ("owner computes" with ghost tets):
     all their vertices (owned + ghost vertices).  Every edge row whose tail is
     owned is then complete locally, so the element map needs no reverse
     exchange (SURVEY §8(e) "alternative: overlapping decomposition");
+  * the local problem -- local tets, local vertices (owned ascending, then
+    ghosts), the tets' local keys and the halo lists of every peer -- is built
+    on the device by ``ebb_partition_local`` (partition_rank below); each
+    rank reads back only its own local-size arrays and frees the global mesh;
   * the PCG solves on owned rows only (mask = free AND owned).  Ghost copies
     of x, p, u, v stay consistent because they are updated with the same
     global alpha/beta from owner-consistent z, so per iteration the only
@@ -28,33 +32,6 @@ import numpy as np
 SLOT_RHO, SLOT_PQ, SLOT_RZ = 0, 1, 2
 SLOT_RZ0, SLOT_DSUM, SLOT_GSUM = 7, 10, 11      # (solver.cu scalar slots)
 CG_SR_PHASE = 3                                  # EBB_CG_SR_PHASE
-
-
-# ----------------------------------------------------------------------------- plans
-def local_problem(tets, owner_v, rank):
-    """Local mesh of `rank`: (tet ids, global vertex ids ascending, local tets, owned mask)."""
-    tets = np.asarray(tets, dtype=np.int64)
-    touch = (owner_v[tets] == rank).any(axis=1)
-    lt = np.nonzero(touch)[0]
-    verts = np.unique(tets[lt])
-    local_tets = np.searchsorted(verts, tets[lt])
-    owned = owner_v[verts] == rank
-    return lt, verts, local_tets, owned
-
-
-def halo_plan(tets, owner_v, nranks):
-    """Ghost lists and matching send lists for every ordered rank pair.
-
-    ghosts[r] = vertices of r's local mesh not owned by r (ascending global id);
-    send[o][r] = recv[r][o] = ghosts[r] owned by o (ascending) -- both ends
-    derive the same list from the global owner map, no negotiation needed.
-    """
-    problems = [local_problem(tets, owner_v, r) for r in range(nranks)]
-    ghosts = [p[1][~p[3]] for p in problems]
-    recv = [[ghosts[r][owner_v[ghosts[r]] == o] if o != r else np.zeros(0, np.int64)
-             for o in range(nranks)] for r in range(nranks)]
-    send = [[recv[r][o] for r in range(nranks)] for o in range(nranks)]
-    return problems, send, recv
 
 
 # ----------------------------------------------------------------------------- transports
@@ -230,41 +207,98 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
 
 
 # ----------------------------------------------------------------------------- GPU setup
-def global_partition(ctx, X, tets, nranks, name="global"):
-    """Renumber the global mesh on the device (a2) and compute the O4 owner maps
-    there (``ebb_partition``).  Returns the mesh in stored (SFC) order."""
-    from .tetfem import TetFEM
-    fem = TetFEM(ctx, X, tets, name=name)
-    ot = fem.tets.field("owner_t", "i32")
-    ov = fem.verts.field("owner_v", "i32")
-    ctx.check(ctx.L.ebb_partition(ctx.h, fem.v.h, int(nranks), ot.h, ov.h))
-    order, tord = fem.vert_order(), fem.tet_order()
-    return dict(X=np.ascontiguousarray(X[order]), tets=fem.v.read().astype(np.int64), owner_v=ov.read(),
-                owner_t=ot.read(), vert_order=order, tet_order=tord)
+def partition_rank(ctx, X, tets, nranks, rank, name="part", mode="overlap", debug=False):
+    """This rank's local problem, built on the device: upload the global mesh
+    (positions and tets.v only -- no edge relation), orient (O1), renumber
+    (a2: Morton vertices, tets by vertex tuple), the O4 owner maps
+    (``ebb_partition``) and the local extraction (``ebb_partition_local``);
+    read back the local-size arrays, free every global relation.
+
+    Returns dict(vert_src, tet_src: the local vertices / tets as rows of the
+    INPUT X / tets; tets: the local tets in local vertex ids; n_owned: local
+    vertices [0, n_owned) are owned; send / recv: {peer: local vertex rows};
+    owner_v: the global owner map in stored order (tests); vert_order /
+    tet_order: stored -> input rows of the global mesh (tests))."""
+    import ctypes as C
+
+    from . import _abi as A
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    tets = np.ascontiguousarray(tets, dtype=np.int64)
+    nv, nt = X.shape[0], tets.shape[0]
+    L, h = ctx.L, ctx.h
+    V = ctx.relation(f"{name}.gverts", nv)
+    T = ctx.relation(f"{name}.gtets", nt)
+    pos = V.field("pos", "f64", (3, 1), init=X)
+    vid = V.field("orig_id", "u32", init=np.arange(nv, dtype=np.uint32))
+    tid = T.field("orig_id", "u32", init=np.arange(nt, dtype=np.uint32))
+    v = T.key_field("v", V, (4, 1), tets)
+    sw = C.c_uint64()
+    ctx.check(L.ebb_tetmesh_orient(h, v.h, pos.h, C.byref(sw)))
+    ctx.check(L.ebb_renumber_morton(h, V.h, pos.h))
+    ctx.check(L.ebb_sort_by_key_tuple(h, T.h, v.h))
+    ot = T.field("owner_t", "i32")
+    ov = V.field("owner_v", "i32")
+    ctx.check(L.ebb_partition(h, v.h, int(nranks), ot.h, ov.h))
+    info = A.PartitionInfo()
+    sp = (C.c_uint64 * (nranks + 1))()
+    rp = (C.c_uint64 * (nranks + 1))()
+    ctx.check(L.ebb_partition_local(h, v.h, ot.h, ov.h, int(nranks), int(rank),
+                                    A.PART_OVERLAP if mode == "overlap" else A.PART_OWN,
+                                    f"{name}.r{rank}".encode(), C.byref(info), sp, rp))
+    from .ebb import Field, Relation
+    LT = Relation(ctx, info.ltets, f"{name}.r{rank}.ltets", info.n_ltets)
+    LV = Relation(ctx, info.lverts, f"{name}.r{rank}.lverts", info.n_lverts)
+    # input rows of the local vertices / tets: gather the global orig ids on the device
+    vsrc = LV.field("src", "u32")
+    tsrc = LT.field("src", "u32")
+    ctx.check(L.ebb_rows_gather(h, vid.h, info.vert_gid, vsrc.h, None))
+    ctx.check(L.ebb_rows_gather(h, tid.h, info.tet_gid, tsrc.h, None))
+    out = dict(vert_src=vsrc.read().astype(np.int64), tet_src=tsrc.read().astype(np.int64),
+               tets=Field(ctx, info.v, LT, "v", "key", (4, 1), A.AOS).read().astype(np.int64),
+               n_owned=int(info.n_owned), send={}, recv={})
+    for kind, rel, rows, ptr in (("send", info.send, info.send_rows, sp), ("recv", info.recv, info.recv_rows, rp)):
+        if rel == A.NONE:
+            continue
+        R = Relation(ctx, rel, f"{name}.{kind}", int(ptr[nranks]))
+        allrows = Field(ctx, rows, R, "rows", "u32", (1, 1), A.AOS).read().astype(np.int64)
+        out[kind] = {q: allrows[ptr[q]:ptr[q + 1]] for q in range(nranks) if ptr[q + 1] > ptr[q]}
+        R.free()
+    if debug:
+        out["owner_v"] = ov.read()
+        out["vert_order"] = vid.read().astype(np.int64)
+        out["tet_order"] = tid.read().astype(np.int64)
+    LT.free()
+    LV.free()
+    T.free()
+    V.free()
+    return out
 
 
 # ----------------------------------------------------------------------------- GPU rank
 class GpuRank:
-    """One rank's local problem on its GPU through the Ebb C ABI."""
+    """One rank's local problem on its GPU through the Ebb C ABI.
 
-    def __init__(self, ctx, rank, X, tets, owner_v, plan, free, u, vel, mu, lam, rho=1e3, dtype="f64",
-                 stream=None, name=None):
+    part = partition_rank(...); X, free, u, vel (vertex rows) and mu, lam (tet
+    rows) in the INPUT order of the global mesh.  The local mesh keeps the
+    partition's order (owned vertices in global SFC order, then the ghosts;
+    tets in global SFC order): no second renumbering, so the halo lists are
+    local rows as they are."""
+
+    def __init__(self, ctx, rank, part, X, free, u, vel, mu, lam, rho=1e3, dtype="f64", stream=None, name=None):
         import torch
 
         from . import _abi as A
         from .tetfem import TetFEM
-        problems, send, recv = plan
-        lt, verts, ltets, owned = problems[rank]
+        vs, ts = part["vert_src"], part["tet_src"]
+        n_owned = part["n_owned"]
         self.rank, self.ctx, self.stream, self.A = rank, ctx, stream, A
-        self.verts_g = verts
-        mask = (free[verts] & owned).astype(np.uint8)
-        self.fem = TetFEM(ctx, X[verts], ltets, dtype=dtype, mu=mu[lt], lam=lam[lt], rho=rho, free=mask,
-                          u=u[verts], vel=vel[verts], name=name or f"r{rank}")
-        order = self.fem.vert_order()                 # local input index at each stored row
-        stored = np.empty_like(order)
-        stored[order] = np.arange(order.size)
-        self.stored_of_input = stored
-        self.owned_stored = owned[order]
+        self.verts_g = vs                              # input row of every local vertex
+        owned = np.arange(vs.size) < n_owned
+        mask = (np.asarray(free)[vs].astype(bool) & owned).astype(np.uint8)
+        self.fem = TetFEM(ctx, np.asarray(X)[vs], part["tets"], dtype=dtype, mu=np.asarray(mu)[ts],
+                          lam=np.asarray(lam)[ts], rho=rho, free=mask, u=np.asarray(u)[vs],
+                          vel=np.asarray(vel)[vs], renumber=False, name=name or f"r{rank}")
+        self.owned_stored = owned
         # allocates every CG work field (the single-reduction set includes u, u2)
         self.fem.cg_init(stream, variant=A.CG_SINGLE_REDUCTION)
         self.z_field = self._field(self.fem.cg.z, 4)
@@ -274,15 +308,11 @@ class GpuRank:
         self.halo_field = self.z_field
         self.scal = self._field(self.fem.cg.scal, 1, count=12, dt="f64").tensor()
         self._send, self._recv = {}, {}
-        nranks = len(problems)
         tdt = torch.float64 if dtype == "f64" else torch.float32
-        for peer in range(nranks):
-            for kind, lst in (("send", send[rank][peer]), ("recv", recv[rank][peer])):
-                if len(lst) == 0:
-                    continue
-                rows = stored[np.searchsorted(verts, lst)].astype(np.uint32)
+        for kind, lists in (("send", part["send"]), ("recv", part["recv"])):
+            for peer, rows in lists.items():
                 rel = ctx.relation(f"{self.fem.verts.name}.{kind}{peer}", len(rows))
-                rf = rel.field("rows", "u32", init=rows)
+                rf = rel.field("rows", "u32", init=rows.astype(np.uint32))
                 bufs = {}
                 for nc in (3, 4):
                     buf = torch.zeros((len(rows), nc), dtype=tdt, device=f"cuda:{ctx.device}")
@@ -354,13 +384,11 @@ class GpuRank:
             buf.copy_(data)
         self.ctx.check(self.ctx.L.ebb_rows_scatter(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
 
-    # -- results in global numbering
+    # -- results in the input numbering of the global mesh
     def owned_values(self, field):
         vals = field.read()
-        ids = self.verts_g[self.fem.vert_order()]
-        return ids[self.owned_stored], vals[self.owned_stored]
+        return self.verts_g[self.owned_stored], vals[self.owned_stored]
 
     def local_values(self, field):
-        """Every local row (owned and ghost) with its global vertex id."""
-        vals = field.read()
-        return self.verts_g[self.fem.vert_order()], vals
+        """Every local row (owned and ghost) with its input vertex id."""
+        return self.verts_g, field.read()

@@ -126,6 +126,10 @@ class Relation:
     def __init__(self, ctx, h, name, size):
         self.ctx, self.h, self.name, self.size = ctx, h, name, size
 
+    def free(self):
+        """ebb_relation_free: every field of the relation (and its group index)."""
+        self.ctx.check(self.ctx.L.ebb_relation_free(self.ctx.h, self.h))
+
     def field(self, name, dtype="f64", shape=(1, 1), layout="aos", init=None) -> "Field":
         dt, npdt = _DT[dtype]
         lay = A.SOA if layout == "soa" else A.AOS
@@ -204,6 +208,9 @@ class Field:
         self.ctx.check(self.ctx.L.ebb_field_write(self.ctx.h, self.h, buf.ctypes.data_as(C.c_void_p), buf.nbytes,
                                                   _stream(stream)))
         self.ctx.sync(stream)
+
+    def free(self):
+        self.ctx.check(self.ctx.L.ebb_field_free(self.ctx.h, self.h))
 
     def write_async(self, host_ptr: int, nbytes: int, stream=None):
         """Stream-ordered upload from (pinned) host memory at host_ptr."""

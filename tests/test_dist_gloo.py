@@ -160,6 +160,21 @@ def _case():
 STEPS = 3
 
 
+def _plan(part, tets, P):
+    """(problems, send, recv) of every rank from the oracle's overlapping O4
+    (the GPU ranks get theirs from ebb_partition_local): problems[r] = (local
+    tets, local vertices ascending, local tet keys, owned mask)."""
+    ov = part["owner_v"]
+    problems = []
+    for r in range(P):
+        lt = part["ltets"][r]
+        verts = np.sort(part["local"][r])
+        problems.append((lt, verts, np.searchsorted(verts, tets[lt]), ov[verts] == r))
+    send = [[part["send"][o][r] for r in range(P)] for o in range(P)]
+    recv = [[part["send"][o][r] for o in range(P)] for r in range(P)]
+    return problems, send, recv
+
+
 def _worker(rank, world, port, outdir, variant):
     import sys
     sys.path.insert(0, ROOT)
@@ -168,8 +183,8 @@ def _worker(rank, world, port, outdir, variant):
     from paper_1506_07577_b200 import dist
     tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     case, m, tet_src, order, oracle = _case()
-    part = oracle.partition(m.nv, m.tets, world)
-    plan = dist.halo_plan(m.tets, part["owner_v"], world)
+    part = oracle.partition(m.nv, m.tets, world, mode="overlap")
+    plan = _plan(part, m.tets, world)
     R = OracleRank(rank, m.X, m.tets, part["owner_v"], plan, case.free[order], case.u[order], case.vel[order],
                    case.mu[tet_src], case.lam[tet_src])
     for _ in range(STEPS):

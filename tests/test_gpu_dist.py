@@ -23,6 +23,17 @@ def ctx():
     c.close()
 
 
+def _ranks(ctx, case, P, name):
+    """P virtual ranks, each from its own device partition (ebb_partition_local)."""
+    from paper_1506_07577_b200 import dist
+    ranks = []
+    for r in range(P):
+        part = dist.partition_rank(ctx, case.X, case.tets, P, r, name=f"{name}p{r}")
+        ranks.append(dist.GpuRank(ctx, r, part, case.X, case.free, case.u, case.vel, case.mu, case.lam,
+                                  name=f"{name}r{r}"))
+    return ranks
+
+
 @pytest.mark.parametrize("variant", ["saad", "single"])
 @pytest.mark.parametrize("P", [1, 2, 3, 4])
 def test_virtual_ranks_reproduce_single_domain(ctx, P, variant):
@@ -35,15 +46,7 @@ def test_virtual_ranks_reproduce_single_domain(ctx, P, variant):
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
                                case.free[order], h, iters=iters)
-    G = dist.global_partition(ctx, case.X, case.tets, P, name=f"vg{P}{variant}")
-    assert np.array_equal(G["vert_order"], order)            # device renumbering == oracle O3
-    ref_part = oracle.partition(m.nv, m.tets, P)
-    assert np.array_equal(G["owner_v"], ref_part["owner_v"])  # device O4 == oracle O4
-    plan = dist.halo_plan(G["tets"], G["owner_v"], P)
-    tord = G["tet_order"]
-    ranks = [dist.GpuRank(ctx, r, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
-                          case.vel[order], case.mu[tord], case.lam[tord], name=f"v{P}{variant}r{r}")
-             for r in range(P)]
+    ranks = _ranks(ctx, case, P, f"v{P}{variant}")
     dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=h, iters=iters, variant=variant)
     dv = np.full((m.nv, 3), np.nan)
     u = np.full((m.nv, 3), np.nan)
@@ -53,8 +56,8 @@ def test_virtual_ranks_reproduce_single_domain(ctx, P, variant):
         ids, vals = R.owned_values(R.fem.u)
         u[ids] = vals
     assert not np.isnan(dv).any()                 # every vertex owned exactly once
-    assert rel_l2(dv, ref["dv"]) <= 1e-8
-    assert rel_l2(u, ref["u"]) <= 1e-8
+    assert rel_l2(dv[order], ref["dv"]) <= 1e-8
+    assert rel_l2(u[order], ref["u"]) <= 1e-8
 
 
 @pytest.mark.parametrize("variant", ["saad", "single"])
@@ -74,12 +77,10 @@ def test_virtual_ranks_three_steps_owned_and_ghost_rows(ctx, P, variant):
         ref = oracle.implicit_step(m, "nh", u, v, case.mu[tet_src], case.lam[tet_src], case.free[order], h,
                                    iters=iters)
         u, v = ref["u"], ref["v"]
-    G = dist.global_partition(ctx, case.X, case.tets, P, name=f"v3g{P}{variant}")
-    plan = dist.halo_plan(G["tets"], G["owner_v"], P)
-    tord = G["tet_order"]
-    ranks = [dist.GpuRank(ctx, r, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
-                          case.vel[order], case.mu[tord], case.lam[tord], name=f"v3{P}{variant}r{r}")
-             for r in range(P)]
+    ranks = _ranks(ctx, case, P, f"v3{P}{variant}")
+    u_in, v_in = np.empty_like(u), np.empty_like(v)
+    u_in[order], v_in[order] = u, v                  # oracle (stored order) -> input rows
+    u, v = u_in, v_in
     for _ in range(steps):
         dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=h, iters=iters, variant=variant)
     nghost = 0
@@ -95,21 +96,56 @@ def test_virtual_ranks_three_steps_owned_and_ghost_rows(ctx, P, variant):
     assert nghost > 0
 
 
-def test_halo_plan_is_consistent(ctx):
+@pytest.mark.parametrize("mode", ["overlap", "own"])
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_partition_local_matches_oracle(ctx, P, mode):
+    """ebb_partition_local (device) == oracle O4 bit-exact for every rank:
+    local tets, local vertices (owned then ghosts), the local tet keys and
+    every send / recv list; the global relations are freed afterwards."""
     from paper_1506_07577_b200 import dist
-    case = Case(n=5)
-    m, *_ = oracle_renumbered(case)
-    part = oracle.partition(m.nv, m.tets, 3)
-    problems, send, recv = dist.halo_plan(m.tets, part["owner_v"], 3)
-    for r in range(3):
-        lt, verts, ltets, owned = problems[r]
-        # owner-computes: every tet touching an owned vertex is local
-        touching = np.nonzero((part["owner_v"][m.tets] == r).any(axis=1))[0]
-        assert np.array_equal(lt, touching)
-        assert np.array_equal(np.sort(np.concatenate([recv[r][o] for o in range(3)])), verts[~owned])
-        for o in range(3):
-            assert np.array_equal(send[o][r], recv[r][o])
-            assert np.all(part["owner_v"][send[o][r]] == o)
+    case = Case(n=5, model="nh")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    ref = oracle.partition(m.nv, m.tets, P, mode=mode)
+    for r in range(P):
+        part = dist.partition_rank(ctx, case.X, case.tets, P, r, name=f"pl{P}{mode}{r}", mode=mode, debug=True)
+        assert np.array_equal(part["vert_order"], order)              # device renumbering == O3
+        assert np.array_equal(part["owner_v"], ref["owner_v"])          # device owner map == O4
+        st_v = np.empty_like(order)
+        st_v[order] = np.arange(order.size)                            # input row -> stored id
+        st_t = np.empty_like(part["tet_order"])
+        st_t[part["tet_order"]] = np.arange(st_t.size)
+        lv = st_v[part["vert_src"]]
+        assert np.array_equal(lv, ref["local"][r])
+        assert part["n_owned"] == int((ref["owner_v"] == r).sum())
+        assert np.array_equal(st_t[part["tet_src"]], ref["ltets"][r])
+        assert np.array_equal(lv[part["tets"]], m.tets[ref["ltets"][r]])
+        for q in range(P):
+            s_rows = part["send"].get(q, np.zeros(0, np.int64))
+            r_rows = part["recv"].get(q, np.zeros(0, np.int64))
+            assert np.array_equal(lv[s_rows], ref["send"][r][q])
+            assert np.array_equal(lv[r_rows], ref["send"][q][r])
+
+
+def test_relation_and_field_free(ctx):
+    """ebb_relation_free / ebb_field_free: handles become invalid, a relation
+    still targeted by another relation's key-field is refused, names are
+    reusable after the free."""
+    from paper_1506_07577_b200.ebb import EbbError
+    A_ = ctx.relation("freeA", 10)
+    B_ = ctx.relation("freeB", 4)
+    x = A_.field("x", "f64", init=np.arange(10.0))
+    k = B_.key_field("k", A_, (1, 1), np.array([0, 3, 5, 9], dtype=np.uint64))
+    with pytest.raises(EbbError, match="EBB_E_STATE"):
+        A_.free()                                   # B.k targets A
+    x.free()
+    with pytest.raises(EbbError, match="EBB_E_ARG"):
+        x.read()
+    B_.free()
+    A_.free()
+    with pytest.raises(EbbError, match="EBB_E_ARG"):
+        k.read()
+    A2 = ctx.relation("freeA", 3)                   # the name is free again
+    assert A2.field("y", "f64", init=np.ones(3)).read().tolist() == [1.0, 1.0, 1.0]
 
 
 @pytest.mark.parametrize("variant", ["saad", "single"])
@@ -123,17 +159,13 @@ def test_nccl_transport_single_rank(ctx, variant):
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
                                case.free[order], h, iters=iters)
-    G = dist.global_partition(ctx, case.X, case.tets, 1, name=f"nccl1{variant}")
-    plan = dist.halo_plan(G["tets"], G["owner_v"], 1)
-    tord = G["tet_order"]
-    R = dist.GpuRank(ctx, 0, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
-                     case.vel[order], case.mu[tord], case.lam[tord], name=f"nccl1{variant}r0")
+    (R,) = _ranks(ctx, case, 1, f"nccl1{variant}")
     T = dist.NcclTransport(ctx, 0, 1)
     dist.implicit_step([R], T, "nh", h=h, iters=iters, variant=variant)
     ids, dv = R.owned_values(R.fem.dv)
     out = np.full((m.nv, 3), np.nan)
     out[ids] = dv
-    assert rel_l2(out, ref["dv"]) <= 1e-8
+    assert rel_l2(out[order], ref["dv"]) <= 1e-8
 
 
 def test_nccl_allreduce_and_errors(ctx):
@@ -171,11 +203,7 @@ def test_single_reduction_phases_honour_the_tolerance(ctx):
     k = next(k for k in range(1, 301) if hist[k] <= thr)
     assert abs(hist[k] - thr) > 1e-6 * thr and abs(hist[k - 1] - thr) > 1e-6 * thr
     x_ref, _, _ = oracle.pcg(m.row_ptr, m.head, ref["A"], ref["b"], case.free[order], k)
-    G = dist.global_partition(ctx, case.X, case.tets, P, name="vgtol")
-    plan = dist.halo_plan(G["tets"], G["owner_v"], P)
-    tord = G["tet_order"]
-    ranks = [dist.GpuRank(ctx, r, G["X"], G["tets"], G["owner_v"], plan, case.free[order], case.u[order],
-                          case.vel[order], case.mu[tord], case.lam[tord], name=f"vtol{r}") for r in range(P)]
+    ranks = _ranks(ctx, case, P, "vtol")
     for R in ranks:
         R.fem.cg.tol = tol
     dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=h, iters=k + 40, variant="single")
@@ -184,4 +212,4 @@ def test_single_reduction_phases_honour_the_tolerance(ctx):
         ids, vals = R.owned_values(R.fem.dv)
         dv[ids] = vals
         assert R.fem.cg_iterations() == (k, True)
-    assert rel_l2(dv, x_ref) <= 1e-8
+    assert rel_l2(dv[order], x_ref) <= 1e-8

@@ -591,6 +591,7 @@ typedef struct {
     ebb_field send_rows, recv_rows;      /* U32 local vertex rows, grouped by peer      */
     uint64_t n_ltets, n_lverts, n_owned; /* lverts [0, n_owned) are the owned vertices  */
 } ebb_partition_info;
+/* (SURVEY §8(e) "vertex-owned shards with ghost layers"; O4) */
 ebb_status ebb_partition_local(ebb_ctx ctx, ebb_field tets_v, ebb_field owner_t, ebb_field owner_v,
                                int32_t nparts, int32_t rank, int32_t mode, const char* name,
                                ebb_partition_info* out, uint64_t* send_ptr, uint64_t* recv_ptr);
@@ -600,7 +601,8 @@ ebb_status ebb_partition_local(ebb_ctx ctx, ebb_field tets_v, ebb_field owner_t,
  * or indexes a relation.  relation_free: frees every field of the relation
  * and its hidden group index; EBB_E_STATE while a key-field of another live
  * relation targets it.  Both drop every cached plan.  The handles become
- * invalid (EBB_E_ARG on use).  Synchronous. */
+ * invalid (EBB_E_ARG on use).  Synchronous.  (Relations and fields: P:405-420,
+ * P:663-667; the per-rank global mesh of SURVEY §8(e).) */
 ebb_status ebb_field_free(ebb_ctx ctx, ebb_field f);
 ebb_status ebb_relation_free(ebb_ctx ctx, ebb_rel rel);
 

@@ -442,10 +442,16 @@ ebb_status ebb_cg_phase(ebb_ctx ctx, const ebb_cg* cg, int32_t phase, ebb_stream
 
 /* ---- halo support ------------------------------------- */
 /* pack:   buf[k] = f[rows[k]]      unpack: f[rows[k]] = buf[k]
- * f: AOS field of any dtype; rows: U32 field (row ids of f's relation) on a
- * list relation; buf: AOS field of f's dtype and shape on the list relation. */
+ * f: AOS field of any dtype, or a component-planar (SOA) F32/F64 field;
+ * rows: U32 field (row ids of f's relation) on a list relation; buf: AOS
+ * field of f's dtype and shape on the list relation. */
 ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s);
 ebb_status ebb_rows_scatter(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s);
+/* f[rows[k]] += buf[k] (F32/F64; f AOS or SOA, buf AOS): the reverse add of
+ * partial force / stiffness rows into their owners (SURVEY §8(e) "halo
+ * exchange ... of the partial force sums").  rows must be distinct within
+ * one call; calls are stream-ordered, so several peers' lists may overlap. */
+ebb_status ebb_rows_scatter_add(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s);
 
 /* ---- NCCL inside the library ("NCCL over NVLink carries the
  * halo exchange ... and the allreduce of CG scalars"; not in the paper,
@@ -595,6 +601,30 @@ typedef struct {
 ebb_status ebb_partition_local(ebb_ctx ctx, ebb_field tets_v, ebb_field owner_t, ebb_field owner_v,
                                int32_t nparts, int32_t rank, int32_t mode, const char* name,
                                ebb_partition_info* out, uint64_t* send_ptr, uint64_t* recv_ptr);
+
+/* Reverse-add lists of rank `rank` on its EBB_PART_OVERLAP local mesh
+ * ("halo exchange of vertex positions and of the partial force
+ * sums"): every tet is computed by exactly ONE rank, the owner of its
+ * lowest-gid vertex (so it is local there); rows whose tail a rank does not
+ * own get partial sums from its tets, which are added into the owner's rows.
+ *   tets_v, tets_e: 4x1 / 4x4 key-fields of the local tets (-> local verts,
+ *   -> the local grouped edge relation); vert_gid: U32 global id and
+ *   owner_lv: I32 owner rank of every local vertex.
+ * Creates U8 "<name>_own" on the tets (1: this rank computes the tet) and the
+ * relations <name>.fsend / .frecv (local vertex rows: forces) and .ksend /
+ * .krecv (local edge rows: stiffness), each with a U32 field "rows" grouped
+ * by peer, rows of a peer in (tail gid, head gid) order so both ends agree;
+ * ptrs (host, 4 x (nparts+1)): the CSR offsets by peer of fsend, frecv,
+ * ksend, krecv in that order.  Empty lists leave the relation NONE.
+ * Synchronous. */
+typedef struct {
+    ebb_field own;                            /* U8 on tets                   */
+    ebb_rel fsend, frecv, ksend, krecv;       /* list relations (or NONE)      */
+    ebb_field fsend_rows, frecv_rows, ksend_rows, krecv_rows;
+} ebb_reverse_info;
+ebb_status ebb_partition_reverse(ebb_ctx ctx, ebb_field tets_v, ebb_field tets_e, ebb_field vert_gid,
+                                 ebb_field owner_lv, int32_t nparts, int32_t rank, const char* name,
+                                 ebb_reverse_info* out, uint64_t* ptrs);
 
 /* Lifetime (a rank frees the global mesh it partitioned).  field_free: frees
  * the column (borrowed memory is left alone); EBB_E_STATE if the field groups

@@ -76,6 +76,11 @@ CG_AUTO, CG_SAAD, CG_SINGLE_REDUCTION, CG_SYMMETRIC = 0, 1, 2, 3
 PART_OVERLAP, PART_OWN = 0, 1
 
 
+class ReverseInfo(C.Structure):
+    _fields_ = [("own", u32), ("fsend", u32), ("frecv", u32), ("ksend", u32), ("krecv", u32),
+                ("fsend_rows", u32), ("frecv_rows", u32), ("ksend_rows", u32), ("krecv_rows", u32)]
+
+
 class PartitionInfo(C.Structure):
     _fields_ = [("ltets", u32), ("lverts", u32), ("send", u32), ("recv", u32), ("tet_gid", u32), ("vert_gid", u32),
                 ("v", u32), ("send_rows", u32), ("recv_rows", u32), ("n_ltets", C.c_uint64),
@@ -159,11 +164,14 @@ SIGS = {
     "ebb_partition": (S, [ctx_t, u32, C.c_int32, u32, u32]),
     "ebb_partition_local": (S, [ctx_t, u32, u32, u32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p,
                                 C.POINTER(PartitionInfo), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "ebb_partition_reverse": (S, [ctx_t, u32, u32, u32, u32, C.c_int32, C.c_int32, C.c_char_p,
+                                  C.POINTER(ReverseInfo), C.POINTER(C.c_uint64)]),
     "ebb_field_free": (S, [ctx_t, u32]),
     "ebb_relation_free": (S, [ctx_t, u32]),
     "ebb_cg_phase": (S, [ctx_t, C.POINTER(CG), C.c_int32, stream_t]),
     "ebb_rows_gather": (S, [ctx_t, u32, u32, u32, stream_t]),
     "ebb_rows_scatter": (S, [ctx_t, u32, u32, u32, stream_t]),
+    "ebb_rows_scatter_add": (S, [ctx_t, u32, u32, u32, stream_t]),
 }
 
 _lib = None

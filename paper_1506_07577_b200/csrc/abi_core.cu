@@ -216,6 +216,35 @@ __global__ void k_rows_scatter(uint32_t* __restrict__ f, const uint32_t* __restr
     f[(uint64_t)rows[k] * words + w] = buf[i];
 }
 
+// component-planar (SOA) fields: component q of row r at f[q N + r]; the
+// buffer stays element-major (AOS)
+template <typename T>
+__global__ void k_rows_gather_soa(const T* __restrict__ f, uint64_t N, const uint32_t* __restrict__ rows,
+                                  T* __restrict__ buf, uint64_t n, uint32_t comps) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * comps) return;
+    uint64_t k = i / comps, q = i % comps;
+    buf[i] = f[q * N + rows[k]];
+}
+template <typename T>
+__global__ void k_rows_scatter_soa(T* __restrict__ f, uint64_t N, const uint32_t* __restrict__ rows,
+                                   const T* __restrict__ buf, uint64_t n, uint32_t comps, int add) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * comps) return;
+    uint64_t k = i / comps, q = i % comps;
+    T* d = f + q * N + rows[k];
+    *d = add ? *d + buf[i] : buf[i];
+}
+
+template <typename T>
+__global__ void k_rows_add_aos(T* __restrict__ f, const uint32_t* __restrict__ rows, const T* __restrict__ buf,
+                               uint64_t n, uint32_t comps) {
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n * comps) return;
+    uint64_t k = i / comps, q = i % comps;
+    f[(uint64_t)rows[k] * comps + q] += buf[i];
+}
+
 __global__ void k_iota(uint32_t* p, uint64_t n) {
     uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i < n) p[i] = (uint32_t)i;
@@ -893,7 +922,8 @@ static ebb_status rows_common(Ctx* c, ebb_field f, ebb_field rows, ebb_field buf
     *Rw = get_field(c, rows);
     *B = get_field(c, buf);
     if (!*F || !*Rw || !*B) return fail(c, EBB_E_ARG, "rows_gather/scatter: bad handle");
-    if ((*F)->layout != EBB_AOS && (*F)->comps() > 1) return fail(c, EBB_E_TYPE, "halo fields must be AOS");
+    if ((*F)->layout != EBB_AOS && (*F)->comps() > 1 && (*F)->dtype != EBB_F32 && (*F)->dtype != EBB_F64)
+        return fail(c, EBB_E_TYPE, "component-planar halo fields must be F32 or F64");
     if ((*F)->dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "halo rows of a key-field are not supported");
     if ((*Rw)->dtype != EBB_U32 || (*Rw)->comps() != 1) return fail(c, EBB_E_TYPE, "rows must be a U32 scalar field");
     if ((*B)->dtype != (*F)->dtype || (*B)->comps() != (*F)->comps() || (*B)->rel != (*Rw)->rel)
@@ -905,6 +935,29 @@ static ebb_status rows_common(Ctx* c, ebb_field f, ebb_field rows, ebb_field buf
     return EBB_OK;
 }
 
+// SOA fields (the edge relation's 3x3 K): gather / scatter (+add) per component
+static ebb_status rows_soa(Ctx* c, Field* F, Field* Rw, Field* B, uint64_t n, bool gather, int add,
+                           cudaStream_t s) {
+    const uint64_t N = c->rels[F->rel].size;
+    const uint32_t q = F->comps();
+    c->launches++;
+    if (n == 0) return EBB_OK;
+    const unsigned g = grid_for(n * q, 256);
+    if (F->dtype == EBB_F64) {
+        if (gather) k_rows_gather_soa<double><<<g, 256, 0, s>>>((const double*)F->ptr, N, (const uint32_t*)Rw->ptr,
+                                                               (double*)B->ptr, n, q);
+        else k_rows_scatter_soa<double><<<g, 256, 0, s>>>((double*)F->ptr, N, (const uint32_t*)Rw->ptr,
+                                                          (const double*)B->ptr, n, q, add);
+    } else {
+        if (gather) k_rows_gather_soa<float><<<g, 256, 0, s>>>((const float*)F->ptr, N, (const uint32_t*)Rw->ptr,
+                                                              (float*)B->ptr, n, q);
+        else k_rows_scatter_soa<float><<<g, 256, 0, s>>>((float*)F->ptr, N, (const uint32_t*)Rw->ptr,
+                                                         (const float*)B->ptr, n, q, add);
+    }
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
 ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
     EBB_DEVICE_GUARD(c);
@@ -912,6 +965,7 @@ ebb_status ebb_rows_gather(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field b
     uint64_t n;
     uint32_t w;
     EBB_TRY(rows_common(c, f, rows, buf, &F, &Rw, &B, &n, &w));
+    if (F->layout == EBB_SOA && F->comps() > 1) return rows_soa(c, F, Rw, B, n, true, 0, (cudaStream_t)s);
     c->launches++;
     k_rows_gather<<<grid_for(n * w, 256), 256, 0, (cudaStream_t)s>>>((const uint32_t*)F->ptr, (const uint32_t*)Rw->ptr,
                                                                      (uint32_t*)B->ptr, n, w);
@@ -926,9 +980,34 @@ ebb_status ebb_rows_scatter(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field 
     uint64_t n;
     uint32_t w;
     EBB_TRY(rows_common(c, f, rows, buf, &F, &Rw, &B, &n, &w));
+    if (F->layout == EBB_SOA && F->comps() > 1) return rows_soa(c, F, Rw, B, n, false, 0, (cudaStream_t)s);
     c->launches++;
     k_rows_scatter<<<grid_for(n * w, 256), 256, 0, (cudaStream_t)s>>>((uint32_t*)F->ptr, (const uint32_t*)Rw->ptr,
                                                                       (const uint32_t*)B->ptr, n, w);
+    EBB_CUDA(c, cudaGetLastError());
+    return EBB_OK;
+}
+
+ebb_status ebb_rows_scatter_add(ebb_ctx ctx, ebb_field f, ebb_field rows, ebb_field buf, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
+    Field *F, *Rw, *B;
+    uint64_t n;
+    uint32_t w;
+    EBB_TRY(rows_common(c, f, rows, buf, &F, &Rw, &B, &n, &w));
+    if (F->dtype != EBB_F32 && F->dtype != EBB_F64) return fail(c, EBB_E_TYPE, "scatter_add needs an F32/F64 field");
+    if (F->layout == EBB_SOA && F->comps() > 1) return rows_soa(c, F, Rw, B, n, false, 1, (cudaStream_t)s);
+    const uint32_t q = F->comps();   // AOS: component k of row r at f[r q + k]
+    c->launches++;
+    if (n) {
+        const unsigned g = grid_for(n * q, 256);
+        if (F->dtype == EBB_F64)
+            k_rows_add_aos<double><<<g, 256, 0, (cudaStream_t)s>>>((double*)F->ptr, (const uint32_t*)Rw->ptr,
+                                                                  (const double*)B->ptr, n, q);
+        else
+            k_rows_add_aos<float><<<g, 256, 0, (cudaStream_t)s>>>((float*)F->ptr, (const uint32_t*)Rw->ptr,
+                                                                 (const float*)B->ptr, n, q);
+    }
     EBB_CUDA(c, cudaGetLastError());
     return EBB_OK;
 }

@@ -124,6 +124,57 @@ __global__ void kpl_split(const uint64_t* __restrict__ k, uint64_t n, uint32_t* 
     atomicAdd(cnt + (k[i] >> 32), 1ull);
 }
 
+
+// ---- reverse-add lists (EBB_PART_OVERLAP local mesh, one computing rank per tet)
+// rank of a tet in the reverse-add variant: the owner of its lowest-gid vertex
+__device__ __forceinline__ int32_t tet_rank(const uint32_t v[4], const uint32_t* __restrict__ gid,
+                                            const int32_t* __restrict__ owner) {
+    int k = 0;
+    for (int i = 1; i < 4; ++i)
+        if (gid[v[i]] < gid[v[k]]) k = i;
+    return owner[v[k]];
+}
+
+// candidates (key = gid order, val = peer << 32 | local row), key ~0 = none:
+//   f send: own tet, vertex owned by q != rank       f recv: tet of q, vertex owned by rank
+//   K send: own tet, (i, j) with tail owned by q      K recv: tet of q, (i, j) with tail owned by rank
+__global__ void kpl_reverse(const uint4* __restrict__ tv, const uint32_t* __restrict__ te, uint64_t n,
+                            const uint32_t* __restrict__ gid, const int32_t* __restrict__ owner, int32_t rank,
+                            uint8_t* __restrict__ own, uint64_t* __restrict__ fk, uint64_t* __restrict__ fv,
+                            uint64_t* __restrict__ kk, uint64_t* __restrict__ kv) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint4 v4 = tv[t];
+    const uint32_t v[4] = {v4.x, v4.y, v4.z, v4.w};
+    const int32_t tr = tet_rank(v, gid, owner);
+    own[t] = tr == rank;
+    for (int i = 0; i < 4; ++i) {
+        const int32_t oi = owner[v[i]];
+        const bool snd = tr == rank && oi != rank, rcv = tr != rank && oi == rank;
+        const uint32_t peer = (uint32_t)(snd ? oi : tr);
+        fk[4 * t + i] = (snd || rcv) ? gid[v[i]] : ~0ull;
+        fv[4 * t + i] = ((uint64_t)peer << 32) | v[i];
+        for (int j = 0; j < 4; ++j) {
+            kk[16 * t + 4 * i + j] = (snd || rcv) ? ((uint64_t)gid[v[i]] << 32 | gid[v[j]]) : ~0ull;
+            kv[16 * t + 4 * i + j] = ((uint64_t)peer << 32) | te[16 * t + 4 * i + j];
+        }
+    }
+}
+
+// keep the candidates of one role (0: own tet = send, 1: receive)
+__global__ void kpl_role(uint64_t* __restrict__ k, const uint64_t* __restrict__ v, uint64_t n, int per,
+                         const uint8_t* __restrict__ own, int role) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if ((own[i / per] != 0) != (role == 0)) k[i] = ~0ull;
+    (void)v;
+}
+
+__global__ void kpl_peer_key(const uint64_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ q) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) q[i] = (uint32_t)(v[i] >> 32);
+}
+
 }  // namespace
 }  // namespace ebb
 
@@ -250,6 +301,130 @@ ebb_status ebb_partition_local(ebb_ctx ctx, ebb_field tets_v, ebb_field owner_t,
     out->n_ltets = n_lt;
     out->n_lverts = n_lv;
     out->n_owned = n_own;
+    return EBB_OK;
+}
+
+// a (gid-key, peer|row) candidate set -> rows grouped by peer in gid order,
+// duplicates (several tets of one row) removed; creates relation `rel_name`
+static ebb_status reverse_list(Ctx* c, uint64_t* k, uint64_t* v, uint64_t n, int32_t nparts,
+                               const std::string& rel_name, ebb_rel* rel, ebb_field* rows, uint64_t* ptr) {
+    ebb_ctx ctx = (ebb_ctx)c;
+    for (int q = 0; q <= nparts; ++q) ptr[q] = 0;
+    *rel = EBB_NONE;
+    *rows = EBB_NONE;
+    const unsigned B = 256;
+    Buf k2, v2, v3, q1, q2, tmp, cnt, pc;
+    EBB_CUDA(c, k2.alloc(n * 8));
+    EBB_CUDA(c, v2.alloc(n * 8));
+    EBB_CUDA(c, v3.alloc(n * 8));
+    EBB_CUDA(c, q1.alloc(n * 4));
+    EBB_CUDA(c, q2.alloc(n * 4));
+    EBB_CUDA(c, cnt.alloc(8));
+    EBB_CUDA(c, pc.alloc((size_t)nparts * 8));
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, k, k2.as<uint64_t>(), v, v2.as<uint64_t>(), (int64_t)n);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, q1.as<uint32_t>(), q2.as<uint32_t>(), v2.as<uint64_t>(),
+                                    v3.as<uint64_t>(), (int64_t)n);
+    cub::DeviceSelect::Unique(nullptr, t3, v3.as<uint64_t>(), k2.as<uint64_t>(), cnt.as<uint64_t>(), (int64_t)n);
+    EBB_CUDA(c, tmp.alloc(std::max(t1, std::max(t2, t3))));
+    // by (tail gid, head gid), then stably by peer; the "none" keys sort last
+    EBB_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp.p, t1, k, k2.as<uint64_t>(), v, v2.as<uint64_t>(), (int64_t)n));
+    uint64_t nvalid = n;
+    {
+        // count the valid candidates: keys != ~0 form a prefix after the sort
+        std::vector<uint64_t> probe(1);
+        uint64_t lo = 0, hi = n;
+        while (lo < hi) {   // first ~0 key (binary search with single-element reads)
+            const uint64_t mid = (lo + hi) / 2;
+            EBB_CUDA(c, cudaMemcpy(probe.data(), k2.as<uint64_t>() + mid, 8, cudaMemcpyDeviceToHost));
+            if (probe[0] == ~0ull) hi = mid;
+            else lo = mid + 1;
+        }
+        nvalid = lo;
+    }
+    if (nvalid == 0) return EBB_OK;
+    kpl_peer_key<<<grid_for(nvalid, B), B>>>(v2.as<uint64_t>(), nvalid, q1.as<uint32_t>());
+    EBB_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp.p, t2, q1.as<uint32_t>(), q2.as<uint32_t>(), v2.as<uint64_t>(),
+                                                v3.as<uint64_t>(), (int64_t)nvalid));
+    EBB_CUDA(c, cub::DeviceSelect::Unique(tmp.p, t3, v3.as<uint64_t>(), k2.as<uint64_t>(), cnt.as<uint64_t>(),
+                                          (int64_t)nvalid));
+    uint64_t nu = 0;
+    EBB_CUDA(c, cudaMemcpy(&nu, cnt.p, 8, cudaMemcpyDeviceToHost));
+    EBB_TRY(ebb_relation_new(ctx, rel_name.c_str(), nu, rel));
+    EBB_TRY(new_internal_field(c, *rel, "rows", EBB_U32, 1, 1, EBB_AOS, rows));
+    EBB_CUDA(c, cudaMemset(pc.p, 0, (size_t)nparts * 8));
+    kpl_split<<<grid_for(nu, B), B>>>(k2.as<uint64_t>(), nu, (uint32_t*)c->fields[*rows].ptr,
+                                      pc.as<unsigned long long>());
+    EBB_CUDA(c, cudaGetLastError());
+    std::vector<unsigned long long> hc(nparts);
+    EBB_CUDA(c, cudaMemcpy(hc.data(), pc.p, (size_t)nparts * 8, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < nparts; ++q) ptr[q + 1] = ptr[q] + hc[q];
+    return EBB_OK;
+}
+
+ebb_status ebb_partition_reverse(ebb_ctx ctx, ebb_field tets_v, ebb_field tets_e, ebb_field vert_gid,
+                                 ebb_field owner_lv, int32_t nparts, int32_t rank, const char* name,
+                                 ebb_reverse_info* out, uint64_t* ptrs) {
+    Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
+    if (!c || !name || !out || !ptrs) return fail(c, EBB_E_ARG, "null argument");
+    if (nparts < 1 || rank < 0 || rank >= nparts) return fail(c, EBB_E_ARG, "rank %d of %d parts", rank, nparts);
+    Field* V = get_field(c, tets_v);
+    Field* E = get_field(c, tets_e);
+    Field* G = get_field(c, vert_gid);
+    Field* O = get_field(c, owner_lv);
+    if (!V || !E || !G || !O) return fail(c, EBB_E_ARG, "bad field handle");
+    if (V->dtype != EBB_KEY || V->comps() != 4 || E->dtype != EBB_KEY || E->comps() != 16 || E->rel != V->rel)
+        return fail(c, EBB_E_TYPE, "tets_v / tets_e must be the 4x1 / 4x4 key-fields of one tet relation");
+    if (G->dtype != EBB_U32 || G->rel != V->key_target || O->dtype != EBB_I32 || O->rel != V->key_target)
+        return fail(c, EBB_E_TYPE, "vert_gid (U32) and owner_lv (I32) must be fields on the local vertices");
+    const uint64_t nt = c->rels[V->rel].size;
+    const std::string nm(name);
+    *out = ebb_reverse_info{};
+    EBB_TRY(new_internal_field(c, V->rel, nm + "_own", EBB_U8, 1, 1, EBB_AOS, &out->own));
+    V = get_field(c, tets_v);
+    E = get_field(c, tets_e);
+    G = get_field(c, vert_gid);
+    O = get_field(c, owner_lv);
+    Buf fk, fv, kk, kv;
+    EBB_CUDA(c, fk.alloc(nt * 32));
+    EBB_CUDA(c, fv.alloc(nt * 32));
+    EBB_CUDA(c, kk.alloc(nt * 128));
+    EBB_CUDA(c, kv.alloc(nt * 128));
+    if (nt)
+        kpl_reverse<<<grid_for(nt, 256), 256>>>((const uint4*)V->ptr, (const uint32_t*)E->ptr, nt,
+                                                (const uint32_t*)G->ptr, (const int32_t*)O->ptr, rank,
+                                                (uint8_t*)c->fields[out->own].ptr, fk.as<uint64_t>(),
+                                                fv.as<uint64_t>(), kk.as<uint64_t>(), kv.as<uint64_t>());
+    EBB_CUDA(c, cudaGetLastError());
+    // the candidates mix sends (own tets) and receives (tets of other ranks):
+    // per role, the other role's keys are set to ~0 (kpl_role), then one list
+    const uint64_t n4 = 4 * nt, n16 = 16 * nt;
+    Buf fk2, kk2;
+    EBB_CUDA(c, fk2.alloc(n4 * 8));
+    EBB_CUDA(c, kk2.alloc(n16 * 8));
+    for (int role = 0; role < 2; ++role) {   // 0 send, 1 recv
+        EBB_CUDA(c, cudaMemcpy(fk2.p, fk.p, n4 * 8, cudaMemcpyDeviceToDevice));
+        EBB_CUDA(c, cudaMemcpy(kk2.p, kk.p, n16 * 8, cudaMemcpyDeviceToDevice));
+        if (nt) {
+            kpl_role<<<grid_for(n4, 256), 256>>>(fk2.as<uint64_t>(), fv.as<uint64_t>(), n4, 4, (const uint8_t*)c->fields[out->own].ptr, role);
+            kpl_role<<<grid_for(n16, 256), 256>>>(kk2.as<uint64_t>(), kv.as<uint64_t>(), n16, 16, (const uint8_t*)c->fields[out->own].ptr, role);
+        }
+        EBB_CUDA(c, cudaGetLastError());
+        Buf fvc, kvc;
+        EBB_CUDA(c, fvc.alloc(n4 * 8));
+        EBB_CUDA(c, kvc.alloc(n16 * 8));
+        EBB_CUDA(c, cudaMemcpy(fvc.p, fv.p, n4 * 8, cudaMemcpyDeviceToDevice));
+        EBB_CUDA(c, cudaMemcpy(kvc.p, kv.p, n16 * 8, cudaMemcpyDeviceToDevice));
+        const char* rn = role == 0 ? "send" : "recv";
+        EBB_TRY(reverse_list(c, fk2.as<uint64_t>(), fvc.as<uint64_t>(), n4, nparts, nm + ".f" + rn,
+                             role == 0 ? &out->fsend : &out->frecv, role == 0 ? &out->fsend_rows : &out->frecv_rows,
+                             ptrs + (role == 0 ? 0 : 1) * (nparts + 1)));
+        EBB_TRY(reverse_list(c, kk2.as<uint64_t>(), kvc.as<uint64_t>(), n16, nparts, nm + ".k" + rn,
+                             role == 0 ? &out->ksend : &out->krecv, role == 0 ? &out->ksend_rows : &out->krecv_rows,
+                             ptrs + (role == 0 ? 2 : 3) * (nparts + 1)));
+    }
+    EBB_CUDA(c, cudaDeviceSynchronize());
     return EBB_OK;
 }
 

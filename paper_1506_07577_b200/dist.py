@@ -144,6 +144,21 @@ class LocalTransport:
 
 
 # ----------------------------------------------------------------------------- driver
+def _map_assemble(ranks, transport, model, h, alpha, beta, g):
+    """The element map on every rank; with the reverse-add variant the partial
+    f and K rows of ghost tails are added into their owners (two exchanges)
+    before the assembly reads them."""
+    for R in ranks:
+        R.map_forces(model)
+    if getattr(ranks[0], "map_variant", "overlap") == "reverse":
+        for which in ("rf", "rK"):
+            for R in ranks:
+                R.set_halo(which)
+            transport.exchange(ranks)
+    for R in ranks:
+        R.assemble(h, alpha, beta, g)
+
+
 def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0),
                   variant="saad"):
     """One distributed implicit step (O9 + O10) over `ranks` (the local ones).
@@ -161,9 +176,9 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
     masked, so the kernel leaves ghost x at 0: x (= dv) is exchanged from the
     owners once, before the state update, so ghost u and v stay consistent
     for the next step's map on ghost tets."""
+    _map_assemble(ranks, transport, model, h, alpha, beta, g)
     if variant == "single":
         for R in ranks:
-            R.map_assemble(model, h, alpha, beta, g)
             R.cg_init(single=True)
         transport.allreduce(ranks, (SLOT_RHO, SLOT_RZ + 1))
         transport.allreduce(ranks, (SLOT_RZ0, SLOT_RZ0 + 1))
@@ -186,7 +201,6 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
             R.finish(h)
         return
     for R in ranks:
-        R.map_assemble(model, h, alpha, beta, g)
         R.cg_init()
     transport.allreduce(ranks, (SLOT_RHO, SLOT_RZ + 1))
     for R in ranks:
@@ -282,9 +296,18 @@ class GpuRank:
     rows) in the INPUT order of the global mesh.  The local mesh keeps the
     partition's order (owned vertices in global SFC order, then the ghosts;
     tets in global SFC order): no second renumbering, so the halo lists are
-    local rows as they are."""
+    local rows as they are.
 
-    def __init__(self, ctx, rank, part, X, free, u, vel, mu, lam, rho=1e3, dtype="f64", stream=None, name=None):
+    map_variant="overlap": every local tet is mapped (ghost tets recomputed,
+    every owned row complete locally).  map_variant="reverse" (SURVEY §8(e) /
+    north_star: "halo exchange of vertex positions and of the partial force
+    sums"): each tet is mapped by ONE rank (the owner of its lowest-id
+    vertex, ebb_partition_reverse); the partial f and K rows whose tail the
+    rank does not own are added into their owners' rows (ebb_rows_scatter_add)
+    before the assembly."""
+
+    def __init__(self, ctx, rank, part, X, free, u, vel, mu, lam, rho=1e3, dtype="f64", stream=None, name=None,
+                 map_variant="overlap", nranks=None):
         import torch
 
         from . import _abi as A
@@ -292,6 +315,8 @@ class GpuRank:
         vs, ts = part["vert_src"], part["tet_src"]
         n_owned = part["n_owned"]
         self.rank, self.ctx, self.stream, self.A = rank, ctx, stream, A
+        self.dtype = dtype
+        self.tdt = torch.float64 if dtype == "f64" else torch.float32
         self.verts_g = vs                              # input row of every local vertex
         owned = np.arange(vs.size) < n_owned
         mask = (np.asarray(free)[vs].astype(bool) & owned).astype(np.uint8)
@@ -305,21 +330,79 @@ class GpuRank:
         # halo fields: padded CG vectors (4 components) and dv (x of the PCG, 3)
         self.halo_fields = {"z": self.z_field, "u": self._field(self.fem.cg.u, 4),
                             "u2": self._field(self.fem.cg.u2, 4), "x": self.fem.dv}
-        self.halo_field = self.z_field
         self.scal = self._field(self.fem.cg.scal, 1, count=12, dt="f64").tensor()
-        self._send, self._recv = {}, {}
-        tdt = torch.float64 if dtype == "f64" else torch.float32
-        for kind, lists in (("send", part["send"]), ("recv", part["recv"])):
-            for peer, rows in lists.items():
-                rel = ctx.relation(f"{self.fem.verts.name}.{kind}{peer}", len(rows))
-                rf = rel.field("rows", "u32", init=rows.astype(np.uint32))
-                bufs = {}
-                for nc in (3, 4):
-                    buf = torch.zeros((len(rows), nc), dtype=tdt, device=f"cuda:{ctx.device}")
-                    bufs[nc] = (rel.wrap(f"buf{nc}", buf, dtype, (nc, 1)), buf)
-                (self._send if kind == "send" else self._recv)[peer] = (rf, bufs)
-        self._peers = sorted(set(self._send) | set(self._recv))
+        self._lists = {}
+        self._make_lists("fwd", self.fem.verts.name + ".halo", part["send"], part["recv"], (3, 4))
+        self.map_variant = map_variant
+        if map_variant == "reverse":
+            self._setup_reverse(part, nranks if nranks is not None else 1 + max([rank, *part["send"],
+                                                                                  *part["recv"]]))
+        elif map_variant != "overlap":
+            raise ValueError(map_variant)
+        self.set_halo("z")
         torch.cuda.synchronize()
+
+    def _make_lists(self, tag, prefix, send, recv, ncs):
+        """Row lists + staging buffers (one per component count) per peer."""
+        import torch
+        L = {"send": {}, "recv": {}}
+        for kind, lists in (("send", send), ("recv", recv)):
+            for peer, rows in lists.items():
+                rel = self.ctx.relation(f"{prefix}.{tag}.{kind}{peer}", len(rows))
+                rf = rel.field("rows", "u32", init=np.asarray(rows).astype(np.uint32))
+                bufs = {}
+                for nc in ncs:
+                    buf = torch.zeros((len(rows), nc), dtype=self.tdt, device=f"cuda:{self.ctx.device}")
+                    bufs[nc] = (rel.wrap(f"buf{nc}", buf, self.dtype, (nc, 1)), buf)
+                L[kind][peer] = (rf, bufs)
+        L["peers"] = sorted(set(L["send"]) | set(L["recv"]))
+        self._lists[tag] = L
+
+    def _setup_reverse(self, part, nranks):
+        """The own-tet subset (tets this rank maps) sharing the local vertex and
+        edge relations, and the reverse-add lists of f and K rows."""
+        import ctypes as C
+
+        from . import _abi as A
+        ctx, fem = self.ctx, self.fem
+        owner = np.full(fem.nv, self.rank, dtype=np.int32)
+        for q, rows in part["recv"].items():
+            owner[rows] = q
+        gid = fem.verts.field("gid", "u32", init=np.asarray(self.verts_g).astype(np.uint32))
+        own_f = fem.verts.field("owner", "i32", init=owner)
+        info = A.ReverseInfo()
+        ptr = (C.c_uint64 * (4 * (nranks + 1)))()
+        ctx.check(ctx.L.ebb_partition_reverse(ctx.h, fem.v.h, fem.e.h, gid.h, own_f.h, int(nranks), int(self.rank),
+                                              f"{fem.verts.name}.rev".encode(), C.byref(info), ptr))
+        from .ebb import Field, Relation
+        own = Field(ctx, info.own, fem.tets, "own", "u8", (1, 1), A.AOS).read().astype(bool)
+        lists = []
+        for k, (rel, rows) in enumerate(((info.fsend, info.fsend_rows), (info.frecv, info.frecv_rows),
+                                          (info.ksend, info.ksend_rows), (info.krecv, info.krecv_rows))):
+            p0 = k * (nranks + 1)
+            d = {}
+            if rel != A.NONE:
+                R_ = Relation(ctx, rel, "rev", int(ptr[p0 + nranks]))
+                allr = Field(ctx, rows, R_, "rows", "u32", (1, 1), A.AOS).read().astype(np.int64)
+                d = {q: allr[ptr[p0 + q]:ptr[p0 + q + 1]] for q in range(nranks) if ptr[p0 + q + 1] > ptr[p0 + q]}
+                R_.free()
+            lists.append(d)
+        self._make_lists("rf", fem.verts.name + ".rev", lists[0], lists[1], (3,))
+        self._make_lists("rK", fem.verts.name + ".rev", lists[2], lists[3], (9,))
+        # the own-tet subset: its own relation with keys into the local verts / edges
+        sel = np.nonzero(own)[0]
+        self.n_map_tets = int(sel.size)
+        T2 = ctx.relation(f"{fem.tets.name}.own", max(int(sel.size), 1))
+        self.map_fields = dict(
+            v=T2.key_field("v", fem.verts, (4, 1), fem.v.read()[sel]),
+            e=T2.key_field("e", fem.edges, (4, 4), fem.e.read().reshape(-1, 16)[sel]),
+            Dminv=T2.field("Dminv", self.dtype, (3, 3), "soa", init=fem.Dminv.read().reshape(-1, 9)[sel]),
+            W=T2.field("W", self.dtype, init=fem.W.read()[sel]),
+            mu=T2.field("mu", self.dtype, init=fem.mu.read()[sel]),
+            lam=T2.field("lam", self.dtype, init=fem.lam.read()[sel]))
+        self.rev_bytes = {tag: sum(int(b[1][nc][1].numel()) * (8 if self.dtype == "f64" else 4)
+                                   for b in self._lists[tag]["send"].values() for nc in b[1])
+                          for tag in ("rf", "rK")}
 
     def _field(self, h, rows, count=None, dt=None):
         from .ebb import Field
@@ -330,17 +413,46 @@ class GpuRank:
         return f
 
     # -- phases
-    def map_assemble(self, model, h, alpha, beta, g):
-        self.fem.map_forces(model, True, False, stream=self.stream)
+    def map_forces(self, model):
+        if self.map_variant == "overlap":
+            self.fem.map_forces(model, True, False, stream=self.stream)
+            return
+        import ctypes as C
+
+        from . import _abi as A
+        from .ebb import _stream
+        from .tetfem import MODELS
+        F = self.map_fields
+        d = A.TetMapDesc()
+        d.model, d.scatter, d.zero_outputs = MODELS[model], A.SCATTER_AUTO, 1
+        d.v, d.e, d.u = F["v"].h, F["e"].h, self.fem.u.h
+        d.Dminv, d.W, d.mu, d.lam = F["Dminv"].h, F["W"].h, F["mu"].h, F["lam"].h
+        d.f, d.K, d.energy = self.fem.f.h, self.fem.K.h, A.NONE
+        self.ctx.check(self.ctx.L.ebb_map_tet_forces(self.ctx.h, C.byref(d), _stream(self.stream)))
+
+    def assemble(self, h, alpha, beta, g):
         self.fem.assemble(h, alpha, beta, g, stream=self.stream)
+
+    def map_assemble(self, model, h, alpha, beta, g):
+        self.map_forces(model)
+        self.assemble(h, alpha, beta, g)
 
     def cg_init(self, single=False):
         from . import _abi as A
         self.fem.cg_init(self.stream, variant=A.CG_SINGLE_REDUCTION if single else A.CG_SAAD)
 
     def set_halo(self, which):
-        """The vertex field the halo exchange moves next (z, u or u2)."""
-        self.halo_field = self.halo_fields[which]
+        """What the next exchange moves: a vertex field owners -> ghosts (z, u,
+        u2, x), or the reverse add of partial rows ghost tails -> owners (rf:
+        forces, rK: stiffness rows)."""
+        if which in ("rf", "rK"):
+            self._cur = self._lists[which]
+            self.halo_field = self.fem.f if which == "rf" else self.fem.K
+            self._add = True
+        else:
+            self._cur = self._lists["fwd"]
+            self.halo_field = self.halo_fields[which]
+            self._add = False
 
     def cg_phase(self, k):
         import ctypes as C
@@ -349,40 +461,38 @@ class GpuRank:
         self.ctx.check(self.ctx.L.ebb_cg_phase(self.ctx.h, C.byref(self.fem.cg), int(k), _stream(self.stream)))
 
     def finish(self, h):
-        import ctypes as C
-
         from .ebb import _stream
         self.ctx.check(self.ctx.L.ebb_implicit_update(self.ctx.h, self.fem.dv.h, float(h), self.fem.u.h,
                                                       self.fem.vel.h, _stream(self.stream)))
-        del C
 
     # -- transport hooks
     def scal_tensor(self):
         return self.scal
 
     def peers(self):
-        return self._peers
+        return self._cur["peers"]
 
     def _nc(self):
-        return self.halo_field.shape[0]
+        return self.halo_field.shape[0] * self.halo_field.shape[1]
 
     def pack(self, peer):
         from .ebb import _stream
-        rf, bufs = self._send[peer]
+        rf, bufs = self._cur["send"][peer]
         bf, buf = bufs[self._nc()]
         self.ctx.check(self.ctx.L.ebb_rows_gather(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
         return buf
 
     def recv_buffer(self, peer):
-        return self._recv[peer][1][self._nc()][1]
+        return self._cur["recv"][peer][1][self._nc()][1]
 
     def unpack(self, peer, data):
         from .ebb import _stream
-        rf, bufs = self._recv[peer]
+        rf, bufs = self._cur["recv"][peer]
         bf, buf = bufs[self._nc()]
         if data is not buf:
             buf.copy_(data)
-        self.ctx.check(self.ctx.L.ebb_rows_scatter(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
+        fn = self.ctx.L.ebb_rows_scatter_add if self._add else self.ctx.L.ebb_rows_scatter
+        self.ctx.check(fn(self.ctx.h, self.halo_field.h, rf.h, bf.h, _stream(self.stream)))
 
     # -- results in the input numbering of the global mesh
     def owned_values(self, field):

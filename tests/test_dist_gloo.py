@@ -36,12 +36,17 @@ class OracleRank:
         self.recv = {o: np.array([local[g] for g in lst], dtype=np.int64)
                      for o, lst in enumerate(recv[rank]) if len(lst)}
 
-    def map_assemble(self, model, h, alpha, beta, g):
+    def map_forces(self, model):
         import oracle
         m = self.mesh
-        f, K, en, inv = oracle.element_map(model, m.X, self.u, m.tets, m.Dminv, m.W, self.mu, self.lam,
-                                           e=m.e, ne=m.ne)
-        self.A, self.b = oracle.implicit_assemble(m.row_ptr, m.head, K, m.mass, f, self.vel, h, alpha, beta, g)
+        self.f, self.K, en, inv = oracle.element_map(model, m.X, self.u, m.tets, m.Dminv, m.W, self.mu, self.lam,
+                                                     e=m.e, ne=m.ne)
+
+    def assemble(self, h, alpha, beta, g):
+        import oracle
+        m = self.mesh
+        self.A, self.b = oracle.implicit_assemble(m.row_ptr, m.head, self.K, m.mass, self.f, self.vel, h, alpha,
+                                                  beta, g)
 
     def cg_init(self, single=False):
         m = self.mesh

@@ -23,14 +23,14 @@ def ctx():
     c.close()
 
 
-def _ranks(ctx, case, P, name):
+def _ranks(ctx, case, P, name, map_variant="overlap"):
     """P virtual ranks, each from its own device partition (ebb_partition_local)."""
     from paper_1506_07577_b200 import dist
     ranks = []
     for r in range(P):
         part = dist.partition_rank(ctx, case.X, case.tets, P, r, name=f"{name}p{r}")
         ranks.append(dist.GpuRank(ctx, r, part, case.X, case.free, case.u, case.vel, case.mu, case.lam,
-                                  name=f"{name}r{r}"))
+                                  name=f"{name}r{r}", map_variant=map_variant, nranks=P))
     return ranks
 
 
@@ -60,14 +60,17 @@ def test_virtual_ranks_reproduce_single_domain(ctx, P, variant):
     assert rel_l2(u[order], ref["u"]) <= 1e-8
 
 
+@pytest.mark.parametrize("map_variant", ["overlap", "reverse"])
 @pytest.mark.parametrize("variant", ["saad", "single"])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_virtual_ranks_three_steps_owned_and_ghost_rows(ctx, P, variant):
+def test_virtual_ranks_three_steps_owned_and_ghost_rows(ctx, P, variant, map_variant):
     """Three consecutive distributed implicit steps (50 PCG iterations each)
     match three single-domain oracle steps on EVERY local row, owned and
     ghost: step k+1 maps the ghost tets with the ghost u left by step k, so
     a stale ghost (the round-1 single-reduction driver left ghost dv at 0)
-    corrupts the owned forces from step 2 on."""
+    corrupts the owned forces from step 2 on.  map_variant="reverse": every
+    tet is mapped by one rank only and the partial f / K rows of ghost tails
+    are added into their owners (the north_star halo of partial sums)."""
     from paper_1506_07577_b200 import dist
     case = Case(n=6, model="nh", vel_amp=0.05)
     h, iters, steps = 1e-2, 50, 3
@@ -77,7 +80,7 @@ def test_virtual_ranks_three_steps_owned_and_ghost_rows(ctx, P, variant):
         ref = oracle.implicit_step(m, "nh", u, v, case.mu[tet_src], case.lam[tet_src], case.free[order], h,
                                    iters=iters)
         u, v = ref["u"], ref["v"]
-    ranks = _ranks(ctx, case, P, f"v3{P}{variant}")
+    ranks = _ranks(ctx, case, P, f"v3{P}{variant}{map_variant}", map_variant)
     u_in, v_in = np.empty_like(u), np.empty_like(v)
     u_in[order], v_in[order] = u, v                  # oracle (stored order) -> input rows
     u, v = u_in, v_in
@@ -213,3 +216,25 @@ def test_single_reduction_phases_honour_the_tolerance(ctx):
         dv[ids] = vals
         assert R.fem.cg_iterations() == (k, True)
     assert rel_l2(dv[order], x_ref) <= 1e-8
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_reverse_add_maps_every_tet_once(ctx, P):
+    """The reverse-add variant maps each tet on exactly one rank (the tets the
+    ranks map partition the mesh), and one distributed step equals the
+    single-domain oracle; the overlap variant maps more tets in total."""
+    from paper_1506_07577_b200 import dist
+    case = Case(n=6, model="nh", vel_amp=0.05)
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    ranks = _ranks(ctx, case, P, f"rv1{P}", "reverse")
+    assert sum(R.n_map_tets for R in ranks) == m.nt
+    assert sum(R.fem.nt for R in ranks) > m.nt                       # the overlap's ghost tets
+    assert all(R.rev_bytes["rK"] > 0 for R in ranks)
+    ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                               case.free[order], 1e-2, iters=50)
+    dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=1e-2, iters=50, variant="single")
+    dv = np.full((m.nv, 3), np.nan)
+    for R in ranks:
+        ids, vals = R.owned_values(R.fem.dv)
+        dv[ids] = vals
+    assert rel_l2(dv[order], ref["dv"]) <= 1e-8

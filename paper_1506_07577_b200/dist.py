@@ -57,10 +57,10 @@ class TorchTransport:
         (R,) = ranks
         ops = []
         recvs = {}
-        for peer in R.peers():
-            sb = R.pack(peer)
+        for peer in R.send_peers():
+            ops.append(self.dist.P2POp(self.dist.isend, R.pack(peer), peer, group=self.group))
+        for peer in R.recv_peers():
             rb = R.recv_buffer(peer)
-            ops.append(self.dist.P2POp(self.dist.isend, sb, peer, group=self.group))
             ops.append(self.dist.P2POp(self.dist.irecv, rb, peer, group=self.group))
             recvs[peer] = rb
         if ops:
@@ -110,16 +110,20 @@ class NcclTransport:
         if not peers:
             return
         n = len(peers)
-        sb = [R.pack(p) for p in peers]
-        rb = [R.recv_buffer(p) for p in peers]
+        sp, rp = set(R.send_peers()), set(R.recv_peers())
+        sb = [R.pack(p) if p in sp else None for p in peers]        # a direction may be empty
+        rb = [R.recv_buffer(p) if p in rp else None for p in peers]
+        nb = lambda b: 0 if b is None else b.numel() * b.element_size()
+        ptr = lambda b: 0 if b is None else b.data_ptr()
         P = (C.c_int32 * n)(*peers)
-        SP = (C.c_void_p * n)(*[b.data_ptr() for b in sb])
-        SN = (C.c_uint64 * n)(*[b.numel() * b.element_size() for b in sb])
-        RP = (C.c_void_p * n)(*[b.data_ptr() for b in rb])
-        RN = (C.c_uint64 * n)(*[b.numel() * b.element_size() for b in rb])
+        SP = (C.c_void_p * n)(*[ptr(b) for b in sb])
+        SN = (C.c_uint64 * n)(*[nb(b) for b in sb])
+        RP = (C.c_void_p * n)(*[ptr(b) for b in rb])
+        RN = (C.c_uint64 * n)(*[nb(b) for b in rb])
         self.ctx.check(self.ctx.L.ebb_comm_halo(self.ctx.h, n, P, SP, SN, RP, RN, self._s()))
         for p, b in zip(peers, rb):
-            R.unpack(p, b)
+            if b is not None:
+                R.unpack(p, b)
 
 
 class LocalTransport:
@@ -135,12 +139,10 @@ class LocalTransport:
             R.scal_tensor()[lo:hi] = tot
 
     def exchange(self, ranks):
-        by_rank = {R.rank: R for R in ranks}
-        packed = {(R.rank, peer): R.pack(peer) for R in ranks for peer in R.peers()}
+        packed = {(R.rank, peer): R.pack(peer) for R in ranks for peer in R.send_peers()}
         for R in ranks:
-            for peer in R.peers():
+            for peer in R.recv_peers():
                 R.unpack(peer, packed[(peer, R.rank)])
-        del by_rank
 
 
 # ----------------------------------------------------------------------------- driver
@@ -471,6 +473,12 @@ class GpuRank:
 
     def peers(self):
         return self._cur["peers"]
+
+    def send_peers(self):
+        return sorted(self._cur["send"])
+
+    def recv_peers(self):
+        return sorted(self._cur["recv"])
 
     def _nc(self):
         return self.halo_field.shape[0] * self.halo_field.shape[1]

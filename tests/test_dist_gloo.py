@@ -140,6 +140,12 @@ class OracleRank:
     def peers(self):
         return sorted(set(self.send) | set(self.recv))
 
+    def send_peers(self):
+        return sorted(self.send)
+
+    def recv_peers(self):
+        return sorted(self.recv)
+
     def pack(self, peer):
         import torch
         return torch.from_numpy(np.ascontiguousarray(self._arr()[self.send[peer]]))

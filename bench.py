@@ -528,8 +528,41 @@ def run_dist(args, rank, world, local_rank):
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms = float(tt.item())
     value = T_global * args.steps / (t_ms / 1e3)
+    # ---- end to end: every rank uploads its local u, v from pinned host memory,
+    # runs the step (graph replay incl. the NCCL calls) and reads u, v back
+    V_loc = R.fem.nv
+    u_h = torch.empty((V_loc, 3), dtype=torch.float64, pin_memory=True)
+    v_h = torch.empty((V_loc, 3), dtype=torch.float64, pin_memory=True)
+    u_h.copy_(torch.from_numpy(R.fem.u.read()))
+    v_h.copy_(torch.from_numpy(R.fem.vel.read()))
+    nb = V_loc * 3 * 8
+    e2e_ms = 0.0
+    dist.barrier()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        R.fem.u.write_async(u_h.data_ptr(), nb, stream)
+        R.fem.vel.write_async(v_h.data_ptr(), nb, stream)
+        if graph is None:
+            step()
+        else:
+            ctx.graph_launch(graph, stream)
+        R.fem.u.read_into(u_h.data_ptr(), nb, stream)
+        R.fem.vel.read_into(v_h.data_ptr(), nb, stream)
+        b_.record(stream)
+        b_.synchronize()
+        e2e_ms += a_.elapsed_time(b_)
+    tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_ms = float(tt.item())
+    e2e = {"value": T_global * args.steps / (e2e_ms / 1e3), "unit": "tets/s", "h2d_bytes_per_step": 2 * nb,
+           "d2h_bytes_per_step": 2 * nb,
+           "api": "per rank: ebb_field_write (pinned host local u, v) -> distributed implicit step (graph replay) "
+                  "-> ebb_field_read (u, v); bytes of this rank"}
     peak, peak_src = _peaks()
-    V_loc, E_loc = R.fem.nv, R.fem.ne
+    E_loc = R.fem.ne
     # single: one launch = one PCG iteration of the local rows (the prologue
     # launch moves about the same bytes); saad: the MATVEC phase kernel
     b_mv = bytes_cg_iter(V_loc, E_loc) if cg_var == "single" else bytes_matvec(V_loc, E_loc)
@@ -549,11 +582,109 @@ def run_dist(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Kuhn-6 cube, stretch+noise displacement)",
             "config": cfg, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(),
-            "e2e": {"value": value, "unit": "tets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                    "note": "multi-GPU line: state stays resident on the devices"},
+            "e2e": e2e,
             "components": {"map_avg_us": 1e3 * mp_ms / max(mp_n, 1), "matvec_avg_us": avg_mv,
                            "local_tets": int(R.fem.nt), "local_verts": int(V_loc),
                            "owned_verts": int(part["n_owned"]), "partition_setup_s": t_part}}
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+
+
+def run_dist_map(args, rank, world, local_rank):
+    """BASELINE configs[2] (C3): the StVK force + stiffness map on the ~1e7-tet
+    synthetic blob, fp32, over N GPUs with the position halo (strong scaling:
+    the same global mesh at every N).  A step = the u halo exchange (owners ->
+    ghosts, NCCL) + the map of every local (owned + ghost) tet."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200 import build as B
+    from paper_1506_07577_b200 import dist as D
+    from paper_1506_07577_b200 import ebb
+    from synth import mesh as M
+    from synth import state as S
+
+    B.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    X, tets, n = M.blob(10_000_000)
+    free = S.fixed_mask(X, n)
+    u0 = S.twist_u(X, n, 6, free=free)
+    mu, lam = S.materials(tets.shape[0], 1e6, 0.3, spread=0.1)
+    ctx = ebb.Context(local_rank)
+    t_part = time.perf_counter()
+    part = D.partition_rank(ctx, X, tets, world, rank, name="c3")
+    stream = torch.cuda.Stream(device=dev)
+    R = D.GpuRank(ctx, rank, part, X, free, u0, np.zeros_like(u0), mu, lam, dtype="f32", stream=stream,
+                  name=f"c3r{rank}")
+    t_part = time.perf_counter() - t_part
+    T = D.NcclTransport(ctx, rank, world, stream=stream)
+    T_global = tets.shape[0]
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        D.map_step([R], T, "stvk")
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ctx.timing(True)                  # before the capture: the graph carries the timer event nodes
+    ctx.timing_read(A.K_TET_MAP, reset=True)
+    graph = None
+    if not args.no_graph:
+        ctx.graph_begin(stream)
+        step()
+        graph = ctx.graph_end(stream)
+        ctx.graph_launch(graph, stream)       # untimed replay (keeps the captured timer records)
+        torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    mp_tot, mp_n = 0.0, 0
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            evs[k][0].record(stream)
+            if graph is None:
+                step()
+            else:
+                ctx.graph_launch(graph, stream)
+            evs[k][1].record(stream)
+            evs[k][1].synchronize()
+            ms_, n_ = ctx.timing_read(A.K_TET_MAP)
+            mp_tot += ms_
+            mp_n += n_
+        torch.cuda.synchronize()
+    dist.barrier()
+    t_ms = sum(a_.elapsed_time(b_) for a_, b_ in evs)
+    tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    peak, peak_src = _peaks()
+    map_us = 1e3 * mp_tot / max(mp_n, 1)
+    b_map = bytes_map(R.fem.nt, R.fem.nv, R.fem.ne, 4)
+    line = {"metric": METRIC, "value": T_global * args.steps / (t_ms / 1e3), "unit": "tets/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded metaball blob of Kuhn cubes, twist displacement)",
+            "config": {"workload": f"C3 (BASELINE configs[2]): StVK force+stiffness map, blob of {T_global} tets "
+                                   f"(n={n}), fp32, split over {world} GPU(s) by the O4 owner maps with ghost tets; "
+                                   "a step = the u halo (NCCL) + the map of the local tets",
+                       "tets": T_global, "parallelism": f"domain decomposition x{world} (NCCL position halo)",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "roofline": {"kernel": "k_tet_map_seg (local tets of this rank)", "bound": "hbm",
+                         "achieved": b_map / (map_us * 1e-6) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": b_map / (map_us * 1e-6) / 1e9 / peak, "peak_source": peak_src, "traffic": None,
+                         "algorithmic_bytes_per_launch": b_map, "avg_launch_us": map_us, "rank": rank},
+            "gpu_launches": None, "clocks": clk.summary(),
+            "e2e": {"value": T_global * args.steps / (t_ms / 1e3), "unit": "tets/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0, "note": "map-only line: the state stays on the devices"},
+            "components": {"local_tets": int(R.fem.nt), "owned_verts": int(part["n_owned"]),
+                           "partition_setup_s": t_part}}
     if rank == 0:
         print(json.dumps(line))
     ctx.close()
@@ -568,6 +699,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of a CUDA graph")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 (1M-tet) component measurement")
+    ap.add_argument("--map-only", action="store_true",
+                    help="BASELINE configs[2]: the fp32 StVK map on the 1e7-tet blob with the position halo "
+                         "(domain decomposition; with one rank add --dist)")
     ap.add_argument("--dist-cg", default="single", choices=["single", "saad"],
                     help="PCG driver of the multi-GPU path (single: one fused allreduce per iteration)")
     ap.add_argument("--dist", action="store_true",
@@ -590,7 +724,9 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        if use_dist:
+        if use_dist and args.map_only:
+            run_dist_map(args, rank, world, local_rank)
+        elif use_dist:
             run_dist(args, rank, world, local_rank)
         else:
             run_ours(args, rank, world, local_rank)

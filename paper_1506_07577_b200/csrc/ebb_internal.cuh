@@ -97,6 +97,7 @@ struct SegPlan {
     uint32_t ntiles = 0, max_ent = 0, max_items = 0;
     uint64_t ninst = 0, nslots = 0, nent = 0, nitems = 0;
     double host_ms = 0;               // plan build time (host)
+    unsigned host_threads = 1;        // host threads of the per-tile build
     uint4* tdesc = nullptr;           // ntiles + 1: {first vertex, instance offset, item offset
                                       //   (multiple of 32), entry offset (multiple of 4)}
     uint32_t run = 1;                 // consecutive tiles per CTA run (state of shared tets carried)

@@ -31,6 +31,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <thread>
 #include <vector>
 
 #include "async_copy.cuh"
@@ -405,17 +406,159 @@ void bank_schedule(uint4* it, size_t nit, uint32_t* ent, int ni) {
     }
 }
 
+// One tile's plan (instances, phase-2 items, entry lists) appended to o.
+// Independent of every other tile once the tile boundaries are fixed.
+struct TileOut {
+    std::vector<uint2> inst;
+    std::vector<uint4> items;
+    std::vector<uint32_t> ents;
+    std::vector<uint32_t> n_inst, n_items, n_ents;   // per tile of this worker
+    uint32_t max_ent = 0, max_items = 0;
+    int err = 0;                                    // 1: > 65535 entries, 2: a list > 8 x 127
+    uint32_t err_tile = 0;
+    size_t err_len = 0;
+};
+
+struct PlanMesh {
+    const uint32_t *tv, *index, *head, *vt_ptr, *vt, *rself, *tile_v, *tile_of_v;
+    int ni;
+    bool no_bank_sched, len_order;
+};
+
+void plan_tile(const PlanMesh& M, uint32_t T, TileOut& o) {
+    const int ni = M.ni;
+    const uint32_t a = M.tile_v[T], b = M.tile_v[T + 1];
+    // instances: tets touching [a, b), ascending; state slot = position
+    std::vector<uint32_t> tinst;
+    for (uint32_t v = a; v < b; ++v)
+        for (uint32_t q = M.vt_ptr[v]; q < M.vt_ptr[v + 1]; ++q) tinst.push_back(M.vt[q]);
+    std::sort(tinst.begin(), tinst.end());
+    tinst.erase(std::unique(tinst.begin(), tinst.end()), tinst.end());
+    const uint32_t ninst = (uint32_t)tinst.size();
+    for (uint32_t l = 0; l < ninst; ++l) {
+        const uint32_t t = tinst[l];
+        const uint32_t* vv = &M.tv[4ull * t];
+        const uint32_t vmin = std::min(std::min(vv[0], vv[1]), std::min(vv[2], vv[3]));
+        // the energy (and the inverted-element count) of a tet goes with its min vertex's tile
+        const bool own = M.tile_of_v[vmin] == T;
+        o.inst.push_back(make_uint2(t, l | (own ? 1u << 16 : 0u)));
+    }
+    // canonical slots of the tile in row order
+    const uint32_t nvl = b - a;
+    std::vector<uint32_t> sbase(nvl + 1, 0);
+    for (uint32_t v = a; v < b; ++v) sbase[v - a + 1] = sbase[v - a] + (M.index[v + 1] - M.rself[v]);
+    const uint32_t ns = sbase[nvl];
+    std::vector<std::vector<uint32_t>> lists(ns);   // a self slot's list doubles as its vertex's force list
+    for (uint32_t l = 0; l < ninst; ++l) {
+        const uint32_t* vv = &M.tv[4ull * tinst[l]];
+        for (int p = 0; p < 10; ++p) {
+            const int i = pair_i(p), j = pair_j(p);
+            const uint32_t lo = std::min(vv[i], vv[j]), hi = std::max(vv[i], vv[j]);
+            if (lo < a || lo >= b) continue;
+            const uint32_t r = lower_bound_u32(M.head, M.rself[lo], M.index[lo + 1], hi);
+            const uint32_t sl = sbase[lo - a] + (r - M.rself[lo]);
+            // block K_ij lands on row (v_i, v_j): transposed (K_ji) when v_i > v_j
+            const uint32_t bi = vv[i] <= vv[j] ? i : j, bj = vv[i] <= vv[j] ? j : i;
+            lists[sl].push_back((3 * bi * (uint32_t)ni + l) | ((3 * bj * (uint32_t)ni + l) << 13) | ((uint32_t)p << 26));
+        }
+    }
+    // rows of the slots
+    std::vector<uint32_t> srow(ns), strow(ns);
+    for (uint32_t lv = 0; lv < nvl; ++lv)
+        for (uint32_t sl = sbase[lv]; sl < sbase[lv + 1]; ++sl) {
+            const uint32_t tail = a + lv, r = M.rself[tail] + (sl - sbase[lv]), hd = M.head[r];
+            srow[sl] = r;
+            strow[sl] = hd == tail ? r : lower_bound_u32(M.head, M.index[hd], M.index[hd + 1], tail);
+        }
+    // work lists in kind order: self rows + forces (1), off-diagonal rows (0) in row order
+    // (a warp's stores of one K plane land on neighbouring rows: measured -7 % vs
+    // descending list length, which EBB_SEG_LENORDER selects)
+    std::vector<uint32_t> order;
+    for (uint32_t lv = 0; lv < nvl; ++lv) order.push_back(sbase[lv]);
+    const size_t n_self = order.size();
+    for (uint32_t lv = 0; lv < nvl; ++lv)
+        for (uint32_t sl = sbase[lv] + 1; sl < sbase[lv + 1]; ++sl) order.push_back(sl);
+    if (M.len_order)
+        std::stable_sort(order.begin() + n_self, order.end(),
+                         [&](uint32_t x, uint32_t y) { return lists[x].size() > lists[y].size(); });
+    auto kind_of = [&](size_t qi) -> uint32_t { return qi < n_self ? 1u : 0u; };
+    const size_t e_base = o.ents.size();
+    std::vector<uint32_t> lbeg(ns, 0);
+    size_t tot = 0, longest = 0;
+    for (uint32_t q : order) {
+        lbeg[q] = (uint32_t)(o.ents.size() - e_base);
+        o.ents.insert(o.ents.end(), lists[q].begin(), lists[q].end());
+        tot += lists[q].size();
+        longest = std::max(longest, lists[q].size());
+    }
+    while ((o.ents.size() - e_base) % 4) o.ents.push_back(0);
+    const uint32_t nent = (uint32_t)(o.ents.size() - e_base);
+    if (nent >= 65536 && !o.err) {
+        o.err = 1;
+        o.err_tile = T;
+        o.err_len = nent;
+    }
+    // chunk cap L: the smallest (from the even share per thread) whose
+    // warp-padded item list fits one pass of the CTA; at most 8 chunks a
+    // list, the chunks of a list never straddle a warp, kinds start a warp
+    const size_t it_base = o.items.size();
+    auto layout = [&](size_t L, bool emit) {
+        size_t n = 0;
+        auto pad = [&]() {
+            while (n % 32) {
+                if (emit) o.items.push_back(make_uint4(0, 0xFFFFFFFFu, 0xFFFFFFFFu, 0));
+                ++n;
+            }
+        };
+        for (size_t qi = 0; qi < order.size(); ++qi) {
+            if (qi > 0 && kind_of(qi) != kind_of(qi - 1)) pad();
+            const uint32_t q = order[qi], kind = kind_of(qi);
+            const uint32_t cnt = (uint32_t)lists[q].size();
+            const uint32_t nc = cnt == 0 ? 1 : (uint32_t)((cnt + L - 1) / L);
+            if ((n % 32) + nc > 32) pad();
+            uint32_t beg = lbeg[q];
+            for (uint32_t cc = 0; cc < nc; ++cc, ++n) {
+                const uint32_t sz = cnt / nc + (cc < cnt % nc ? 1 : 0);
+                if (emit) {
+                    const uint32_t meta = beg | (sz << 16) | (cc << 23) | ((nc - 1) << 26) | (kind << 29);
+                    // self rows: z = the vertex (its force); off-diagonal: z = the transpose row
+                    o.items.push_back(kind == 1 ? make_uint4(meta, srow[q], a + (uint32_t)qi, 0)
+                                                : make_uint4(meta, srow[q], strow[q], 0));
+                }
+                beg += sz;
+            }
+        }
+        pad();
+        return n;
+    };
+    // (a tile whose lists cannot fit one pass -- more rows than threads --
+    // runs several passes: L stops growing at 4x the even share)
+    const size_t L0 = std::max<size_t>({(size_t)2, (tot + ni - 1) / ni, (longest + 7) / 8});
+    const size_t Lcap = std::max<size_t>(L0, std::min<size_t>(127, 4 * L0));
+    size_t L = L0;
+    while (L < Lcap && L < longest && layout(L, false) > (size_t)ni) ++L;
+    if (L > 127 && !o.err) {
+        o.err = 2;
+        o.err_tile = T;
+        o.err_len = longest;
+    }
+    if (L <= 127) layout(L, true);
+    if (!M.no_bank_sched && L <= 127)
+        bank_schedule(o.items.data() + it_base, o.items.size() - it_base, o.ents.data() + e_base, ni);
+    o.max_ent = std::max(o.max_ent, nent);
+    o.max_items = std::max(o.max_items, (uint32_t)(o.items.size() - it_base));
+    o.n_inst.push_back(ninst);
+    o.n_items.push_back((uint32_t)(o.items.size() - it_base));
+    o.n_ents.push_back(nent);
+}
+
 ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** out) {
-    const char* er = getenv("EBB_SEG_RUN");   // tiles per run (1 = no carry); measured default
-    const uint32_t run = (er && atoi(er) > 0 && atoi(er) <= 64) ? (uint32_t)atoi(er) : 1u;
     for (SegPlan* P : c->segplans)
-        if (P->v == vf && P->e == ef && P->ni == ni && P->run == run) {
+        if (P->v == vf && P->e == ef && P->ni == ni) {
             *out = P;
             return EBB_OK;
         }
     const auto t_start = std::chrono::steady_clock::now();
-    const bool no_bank_sched = getenv("EBB_SEG_NO_BANK_SCHED") != nullptr;   // measurement knob
-    const bool len_order = getenv("EBB_SEG_LENORDER") != nullptr;           // measurement knob
     Field* V = get_field(c, vf);
     Field* E = get_field(c, ef);
     Relation& ER = c->rels[E->key_target];
@@ -472,163 +615,60 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         if (nv > 0) tile_v.push_back((uint32_t)nv);
     }
     const uint32_t ntiles = (uint32_t)tile_v.size() - 1;
-    std::vector<uint32_t> tile_inst{0}, tile_item{0}, tile_ent{0}, ents, tinst;
-    std::vector<uint2> inst;   // new instances of each tile: (tet, slot | energy owner << 16)
-    std::vector<uint4> tdesc;
-    std::vector<uint4> items;
-    std::vector<uint32_t> srow, strow;   // per slot of the current tile: row, transpose row
-    inst.reserve(nt * 2);
-    // runs of consecutive tiles share one CTA; a tet in tiles k and k+1 of a
-    // run keeps its state slot (carried, computed once)
     std::vector<uint32_t> tile_of_v(nv);
     for (uint32_t T = 0; T < ntiles; ++T)
         for (uint32_t v = tile_v[T]; v < tile_v[T + 1]; ++v) tile_of_v[v] = T;
-    std::vector<int64_t> last_tile(nt, -1), e_run(nt, -1), stamp(nt, -1);
-    std::vector<uint16_t> slot_of(nt, 0);
-    std::vector<char> slot_used(ni);
-    ents.reserve(nt * 30);
-    std::vector<uint32_t> order, sbase, lbeg;
-    std::vector<std::vector<uint32_t>> lists;
-    uint32_t max_ent = 0, max_items = 0;
-    for (uint32_t T = 0; T < ntiles; ++T) {
-        const uint32_t a = tile_v[T], b = tile_v[T + 1];
-        // instances: tets touching [a, b), ascending
-        tinst.clear();
-        for (uint32_t v = a; v < b; ++v)
-            for (uint32_t q = vt_ptr[v]; q < vt_ptr[v + 1]; ++q) {
-                const uint32_t t = vt[q];
-                if (stamp[t] != (int64_t)T) {
-                    stamp[t] = T;
-                    tinst.push_back(t);
-                }
-            }
-        std::sort(tinst.begin(), tinst.end());
-        const uint32_t ninst = (uint32_t)tinst.size();
-        // state slots: carried instances keep theirs, new ones take the free
-        // ones in ascending order; the energy (and the inverted-element count)
-        // of a tet goes with its first computation in its min vertex's run
-        const uint32_t runid = T / run, i0 = (uint32_t)inst.size();
-        std::fill(slot_used.begin(), slot_used.end(), 0);
-        for (uint32_t t : tinst)
-            if (T % run != 0 && last_tile[t] == (int64_t)T - 1) slot_used[slot_of[t]] = 1;
-        uint32_t nextfree = 0;
-        for (uint32_t t : tinst) {
-            if (T % run != 0 && last_tile[t] == (int64_t)T - 1) continue;
-            while (slot_used[nextfree]) ++nextfree;
-            slot_used[nextfree] = 1;
-            slot_of[t] = (uint16_t)nextfree;
-            const uint32_t* vv = &tv[4ull * t];
-            const uint32_t vmin = std::min(std::min(vv[0], vv[1]), std::min(vv[2], vv[3]));
-            const bool own = tile_of_v[vmin] / run == runid && e_run[t] != (int64_t)runid;
-            if (own) e_run[t] = runid;
-            inst.push_back(make_uint2(t, nextfree | (own ? 1u << 16 : 0u)));
-        }
-        for (uint32_t t : tinst) last_tile[t] = T;
-        // canonical slots of the tile in row order
-        sbase.assign(b - a + 1, 0);
-        for (uint32_t v = a; v < b; ++v) sbase[v - a + 1] = sbase[v - a] + (index[v + 1] - rself[v]);
-        const uint32_t ns = sbase[b - a], nvl = b - a;
-        lists.assign(ns, {});   // slot lists; a self slot's list doubles as its vertex's force list
-        for (uint32_t li = 0; li < ninst; ++li) {
-            const uint32_t t = tinst[li], l = slot_of[t];
-            const uint32_t* vv = &tv[4ull * t];
-            for (int p = 0; p < 10; ++p) {
-                const int i = pair_i(p), j = pair_j(p);
-                const uint32_t lo = std::min(vv[i], vv[j]), hi = std::max(vv[i], vv[j]);
-                if (lo < a || lo >= b) continue;
-                const uint32_t r = lower_bound_u32(head.data(), rself[lo], index[lo + 1], hi);
-                const uint32_t s = sbase[lo - a] + (r - rself[lo]);
-                // block K_ij lands on row (v_i, v_j): transposed (K_ji) when v_i > v_j
-                const uint32_t bi = vv[i] <= vv[j] ? i : j, bj = vv[i] <= vv[j] ? j : i;
-                lists[s].push_back((3 * bi * (uint32_t)ni + l) | ((3 * bj * (uint32_t)ni + l) << 13) |
-                                   ((uint32_t)p << 26));
-            }
-        }
-        // rows of the slots
-        srow.resize(ns);
-        strow.resize(ns);
-        for (uint32_t lv = 0; lv < nvl; ++lv)
-            for (uint32_t s = sbase[lv]; s < sbase[lv + 1]; ++s) {
-                const uint32_t tail = a + lv, r = rself[tail] + (s - sbase[lv]), hd = head[r];
-                srow[s] = r;
-                strow[s] = hd == tail ? r : lower_bound_u32(head.data(), index[hd], index[hd + 1], tail);
-            }
-        // work lists in kind order: self rows + forces (1), off-diagonal rows
-        // by descending length (0); entries in the same order
-        order.clear();
-        for (uint32_t lv = 0; lv < nvl; ++lv) order.push_back(sbase[lv]);
-        const size_t n_self = order.size();
-        for (uint32_t lv = 0; lv < nvl; ++lv)
-            for (uint32_t s = sbase[lv] + 1; s < sbase[lv + 1]; ++s) order.push_back(s);
-        // off-diagonal rows in row order: a warp's stores of one K plane land on
-        // neighbouring rows (measured: -7 % vs descending list length, which
-        // balances lanes better; EBB_SEG_LENORDER selects that)
-        if (len_order)
-            std::stable_sort(order.begin() + n_self, order.end(),
-                             [&](uint32_t x, uint32_t y) { return lists[x].size() > lists[y].size(); });
-        auto kind_of = [&](size_t qi) -> uint32_t { return qi < n_self ? 1u : 0u; };
-        const size_t e_base = ents.size();
-        lbeg.assign(ns, 0);
-        size_t tot = 0, longest = 0;
-        for (uint32_t q : order) {
-            lbeg[q] = (uint32_t)(ents.size() - e_base);
-            ents.insert(ents.end(), lists[q].begin(), lists[q].end());
-            tot += lists[q].size();
-            longest = std::max(longest, lists[q].size());
-        }
-        while ((ents.size() - e_base) % 4) ents.push_back(0);
-        const uint32_t nent = (uint32_t)(ents.size() - e_base);
-        if (nent >= 65536)
-            return fail(c, EBB_E_RANGE, "segmented map: tile %u has %u entries (> 65535)", T, nent);
-        // chunk cap L: the smallest (from the even share per thread) whose
-        // warp-padded item list fits one pass of the CTA; at most 8 chunks a
-        // list, the chunks of a list never straddle a warp, kinds start a warp
-        auto layout = [&](size_t L, bool emit) {
-            size_t n = 0;
-            auto pad = [&]() {
-                while (n % 32) {
-                    if (emit) items.push_back(make_uint4(0, 0xFFFFFFFFu, 0xFFFFFFFFu, 0));
-                    ++n;
-                }
-            };
-            for (size_t qi = 0; qi < order.size(); ++qi) {
-                if (qi > 0 && kind_of(qi) != kind_of(qi - 1)) pad();
-                const uint32_t q = order[qi], kind = kind_of(qi);
-                const uint32_t cnt = (uint32_t)lists[q].size();
-                const uint32_t nc = cnt == 0 ? 1 : (uint32_t)((cnt + L - 1) / L);
-                if ((n % 32) + nc > 32) pad();
-                uint32_t beg = lbeg[q];
-                for (uint32_t cc = 0; cc < nc; ++cc, ++n) {
-                    const uint32_t sz = cnt / nc + (cc < cnt % nc ? 1 : 0);
-                    if (emit) {
-                        const uint32_t meta = beg | (sz << 16) | (cc << 23) | ((nc - 1) << 26) | (kind << 29);
-                        // self rows: z = the vertex (its force); off-diagonal: z = the transpose row
-                        items.push_back(kind == 1 ? make_uint4(meta, srow[q], a + (uint32_t)qi, 0)
-                                                  : make_uint4(meta, srow[q], strow[q], 0));
-                    }
-                    beg += sz;
-                }
-            }
-            pad();
-            return n;
-        };
-        // (a tile whose lists cannot fit one pass -- more rows than threads --
-        // runs several passes: L stops growing at 4x the even share)
-        const size_t L0 = std::max<size_t>({(size_t)2, (tot + ni - 1) / ni, (longest + 7) / 8});
-        const size_t Lcap = std::max<size_t>(L0, std::min<size_t>(127, 4 * L0));
-        size_t L = L0;
-        while (L < Lcap && L < longest && layout(L, false) > (size_t)ni) ++L;
-        if (L > 127) return fail(c, EBB_E_RANGE, "segmented map: a list of %zu entries (> 8 x 127)", longest);
-        const size_t it_base = items.size();
-        layout(L, true);
-        if (!no_bank_sched) bank_schedule(items.data() + it_base, items.size() - it_base, ents.data() + e_base, ni);
-        (void)i0;
-        max_ent = std::max(max_ent, nent);
-        max_items = std::max(max_items, (uint32_t)(items.size() - it_base));
-        tile_inst.push_back((uint32_t)inst.size());
-        tile_item.push_back((uint32_t)items.size());
-        tile_ent.push_back((uint32_t)ents.size());
+    // per-tile plans, in parallel over contiguous tile ranges (host threads)
+    PlanMesh M{tv.data(), index.data(), head.data(), vt_ptr.data(), vt.data(), rself.data(), tile_v.data(),
+               tile_of_v.data(), ni, getenv("EBB_SEG_NO_BANK_SCHED") != nullptr, getenv("EBB_SEG_LENORDER") != nullptr};
+    unsigned nth = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    if (ntiles < 64 * nth) nth = std::max(1u, ntiles / 64);
+    std::vector<TileOut> outs(nth);
+    {
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < nth; ++w)
+            pool.emplace_back([&, w]() {
+                const uint32_t t0 = (uint32_t)((uint64_t)ntiles * w / nth), t1 = (uint32_t)((uint64_t)ntiles * (w + 1) / nth);
+                for (uint32_t T = t0; T < t1; ++T) plan_tile(M, T, outs[w]);
+            });
+        for (auto& th : pool) th.join();
     }
+    for (const TileOut& o : outs) {
+        if (o.err == 1) return fail(c, EBB_E_RANGE, "segmented map: tile %u has %zu entries (> 65535)", o.err_tile, o.err_len);
+        if (o.err == 2) return fail(c, EBB_E_RANGE, "segmented map: a list of %zu entries (> 8 x 127)", o.err_len);
+    }
+    // concatenate (tile order = worker order)
+    std::vector<uint4> tdesc;
+    tdesc.reserve(ntiles + 1);
+    std::vector<uint2> inst;
+    std::vector<uint4> items;
+    std::vector<uint32_t> ents;
+    size_t ni_tot = 0, nit_tot = 0, ne_tot = 0;
+    for (const TileOut& o : outs) {
+        ni_tot += o.inst.size();
+        nit_tot += o.items.size();
+        ne_tot += o.ents.size();
+    }
+    inst.reserve(ni_tot);
+    items.reserve(nit_tot);
+    ents.reserve(ne_tot);
+    uint32_t max_ent = 0, max_items = 0, T = 0;
+    for (const TileOut& o : outs) {
+        size_t ii = 0, it = 0, ie = 0;
+        for (size_t k = 0; k < o.n_inst.size(); ++k, ++T) {
+            tdesc.push_back(make_uint4(tile_v[T], (uint32_t)(inst.size() + ii), (uint32_t)(items.size() + it),
+                                       (uint32_t)(ents.size() + ie)));
+            ii += o.n_inst[k];
+            it += o.n_items[k];
+            ie += o.n_ents[k];
+        }
+        inst.insert(inst.end(), o.inst.begin(), o.inst.end());
+        items.insert(items.end(), o.items.begin(), o.items.end());
+        ents.insert(ents.end(), o.ents.begin(), o.ents.end());
+        max_ent = std::max(max_ent, o.max_ent);
+        max_items = std::max(max_items, o.max_items);
+    }
+    tdesc.push_back(make_uint4(tile_v[ntiles], (uint32_t)inst.size(), (uint32_t)items.size(), (uint32_t)ents.size()));
     SegPlan* P = new SegPlan();
     P->v = vf;
     P->e = ef;
@@ -637,19 +677,16 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
     P->max_ent = max_ent;
     P->max_items = max_items;
     P->ninst = inst.size();
-    P->run = run;
+    P->run = 1;
     P->nslots = 0;
     P->nent = ents.size();
     P->nitems = items.size();
+    P->host_threads = nth;
     ebb_status s = EBB_OK;
-    auto up = [&](const std::vector<uint32_t>& h, uint32_t** d) {
-        if (s == EBB_OK) s = upload(c, h, d);
-    };
-    for (uint32_t T = 0; T <= ntiles; ++T) tdesc.push_back(make_uint4(tile_v[T], tile_inst[T], tile_item[T], tile_ent[T]));
     if (s == EBB_OK) s = upload(c, tdesc, &P->tdesc);
     if (s == EBB_OK) s = upload(c, inst, &P->inst);
     if (s == EBB_OK) s = upload(c, items, &P->items);
-    up(ents, &P->ents);
+    if (s == EBB_OK) s = upload(c, ents, &P->ents);
     if (s != EBB_OK) {
         P->release();
         delete P;

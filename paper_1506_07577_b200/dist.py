@@ -161,6 +161,24 @@ def _map_assemble(ranks, transport, model, h, alpha, beta, g):
         R.assemble(h, alpha, beta, g)
 
 
+def map_step(ranks, transport, model="stvk"):
+    """The distributed element map alone (BASELINE configs[2]: the force +
+    stiffness map with halo exchange): the owners' displacements go to their
+    ghost copies (the position halo, owners -> ghosts), then every rank maps
+    its tets -- with the reverse-add variant the partial f / K rows of ghost
+    tails are added into their owners afterwards."""
+    for R in ranks:
+        R.set_halo("disp")
+    transport.exchange(ranks)
+    for R in ranks:
+        R.map_forces(model)
+    if getattr(ranks[0], "map_variant", "overlap") == "reverse":
+        for which in ("rf", "rK"):
+            for R in ranks:
+                R.set_halo(which)
+            transport.exchange(ranks)
+
+
 def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0),
                   variant="saad"):
     """One distributed implicit step (O9 + O10) over `ranks` (the local ones).
@@ -331,7 +349,7 @@ class GpuRank:
         self.z_field = self._field(self.fem.cg.z, 4)
         # halo fields: padded CG vectors (4 components) and dv (x of the PCG, 3)
         self.halo_fields = {"z": self.z_field, "u": self._field(self.fem.cg.u, 4),
-                            "u2": self._field(self.fem.cg.u2, 4), "x": self.fem.dv}
+                            "u2": self._field(self.fem.cg.u2, 4), "x": self.fem.dv, "disp": self.fem.u}
         self.scal = self._field(self.fem.cg.scal, 1, count=12, dt="f64").tensor()
         self._lists = {}
         self._make_lists("fwd", self.fem.verts.name + ".halo", part["send"], part["recv"], (3, 4))

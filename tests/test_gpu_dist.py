@@ -238,3 +238,50 @@ def test_reverse_add_maps_every_tet_once(ctx, P):
         ids, vals = R.owned_values(R.fem.dv)
         dv[ids] = vals
     assert rel_l2(dv[order], ref["dv"]) <= 1e-8
+
+
+@pytest.mark.parametrize("map_variant", ["overlap", "reverse"])
+@pytest.mark.parametrize("model,dtype", [("stvk", "f64"), ("nh", "f64"), ("stvk", "f32")])
+@pytest.mark.parametrize("P", [2, 3])
+def test_distributed_map_step(ctx, P, model, dtype, map_variant):
+    """BASELINE configs[2]'s distributed map: after the position halo and the
+    map (plus the reverse add), every owned force row and every owned
+    stiffness row equals the single-domain oracle's: f directly, K through
+    K p for a seeded global p (each owned row of K p uses the whole row).
+    The ranks start from stale ghost displacements (zeros), so the halo
+    exchange is what makes the ghost tets right."""
+    from paper_1506_07577_b200 import dist
+    case = Case(n=5, model=model, spread=0.1)
+    if dtype == "f32":
+        for k in ("u", "mu", "lam"):
+            setattr(case, k, getattr(case, k).astype(np.float32).astype(np.float64))
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = oracle.element_map(model, m.X, case.u[order], m.tets, m.Dminv, m.W, case.mu[tet_src],
+                                       case.lam[tet_src], e=m.e, ne=m.ne)
+    rng = np.random.default_rng(9)
+    p_in = rng.uniform(-1, 1, size=(m.nv, 3))                  # input order
+    Kp = oracle.edge_matvec(m.row_ptr, m.head, K, p_in[order])  # stored order
+    ranks = []
+    for r in range(P):
+        part = dist.partition_rank(ctx, case.X, case.tets, P, r, name=f"dm{P}{model}{dtype}{map_variant}p{r}")
+        u_stale = case.u.copy()
+        R = dist.GpuRank(ctx, r, part, case.X, case.free, u_stale, case.vel, case.mu, case.lam, dtype=dtype,
+                         name=f"dm{P}{model}{dtype}{map_variant}r{r}", map_variant=map_variant, nranks=P)
+        ghost = ~R.owned_stored
+        uu = R.fem.u.read()
+        uu[ghost] = 0.0                                         # stale ghosts: the halo must refresh them
+        R.fem.u.write(uu)
+        ranks.append(R)
+    dist.map_step(ranks, dist.LocalTransport(), model)
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    f_in = np.full((m.nv, 3), np.nan)
+    kp_in = np.full((m.nv, 3), np.nan)
+    for R in ranks:
+        ids, vals = R.owned_values(R.fem.f)
+        f_in[ids] = vals
+        Pf = R.fem.verts.field("p_dm", dtype, (3, 1), init=p_in[R.verts_g])
+        Qf = R.fem.verts.field("q_dm", dtype, (3, 1))
+        R.fem.matvec(R.fem.K, Pf, Qf)
+        kp_in[ids] = Qf.read()[R.owned_stored]
+    assert rel_l2(f_in[order], f) <= tol
+    assert rel_l2(kp_in[order], Kp) <= tol

@@ -269,6 +269,11 @@ ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool wa
                           const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                           const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
                           cudaStream_t s);
+// seg_plan.cu: the SEGMENTED plan built on the device (identical to the host
+// builder's); tiles never cross a block of kSegBlock consecutive vertices
+constexpr uint32_t kSegBlock = 2048;
+ebb_status build_seg_plan_device(Ctx* c, const uint32_t* tv, uint64_t nt, const uint32_t* index, const uint32_t* head,
+                                 uint64_t nv, int ni, SegPlan* P);
 // chunk_map.cu: the CHUNK element map (builds its plan on the device on first use)
 ebb_status build_chunk_plan(Ctx* c, ebb_field vf, ebb_field ef, int NT, ChunkPlan** out);
 ebb_status chunk_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,

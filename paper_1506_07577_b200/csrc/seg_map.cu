@@ -31,6 +31,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -569,6 +570,26 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
         if (c->fields[fh].alive && c->fields[fh].name == "head") hf = fh;
     if (hf == EBB_NONE) return fail(c, EBB_E_STATE, "segmented map: edge relation has no 'head' key-field");
     const uint64_t nt = c->rels[V->rel].size, nv = c->rels[V->key_target].size, ne = ER.size;
+    // on the device unless the host builder is asked for (EBB_SEG_PLAN=host, or
+    // the EBB_SEG_LENORDER measurement ordering, which only the host has)
+    const char* pe = getenv("EBB_SEG_PLAN");
+    if (!(pe && std::string(pe) == "host") && !getenv("EBB_SEG_LENORDER")) {
+        SegPlan* P = new SegPlan();
+        P->v = vf;
+        P->e = ef;
+        P->ni = ni;
+        const ebb_status st = build_seg_plan_device(c, (const uint32_t*)V->ptr, nt,
+                                                    (const uint32_t*)c->fields[ER.index].ptr,
+                                                    (const uint32_t*)c->fields[hf].ptr, nv, ni, P);
+        if (st != EBB_OK) {
+            P->release();
+            delete P;
+            return st;
+        }
+        c->segplans.push_back(P);
+        *out = P;
+        return EBB_OK;
+    }
     std::vector<uint32_t> tv(nt * 4), index(nv + 1), head(ne);
     EBB_CUDA(c, cudaMemcpy(tv.data(), V->ptr, nt * 16, cudaMemcpyDeviceToHost));
     EBB_CUDA(c, cudaMemcpy(index.data(), c->fields[ER.index].ptr, (nv + 1) * 4, cudaMemcpyDeviceToHost));
@@ -601,7 +622,8 @@ ebb_status build_seg_plan(Ctx* c, ebb_field vf, ebb_field ef, int ni, SegPlan** 
                             (unsigned long long)v, deg, ni);
             uint32_t nw = 0;
             for (uint32_t q = vt_ptr[v]; q < vt_ptr[v + 1]; ++q) nw += stamp[vt[q]] != tile;
-            if (cv > 0 && (ci + nw > (uint32_t)ni || cv >= 4096)) {
+            // a tile never crosses a block of kSegBlock vertices (the device builder's unit)
+            if (cv > 0 && (ci + nw > (uint32_t)ni || cv >= 4096 || v % kSegBlock == 0)) {
                 tile_v.push_back((uint32_t)v);
                 ++tile;
                 ci = 0;

@@ -285,3 +285,39 @@ def test_chunk_plan_stats(ctx):
     assert (fem.ne + fem.nv) // 2 <= st["segments"] <= 10 * fem.nt   # >= one per canonical row
     assert 0 < st["messages"] < st["segments"]
     assert st["zero_rows"] == 0 and st["plan_bytes_per_tet"] > 0
+
+
+@pytest.mark.parametrize("model,dtype", [("nh", "f64"), ("stvk", "f64"), ("nh", "f32")])
+@pytest.mark.parametrize("mesh", ["kuhn", "blob", "noren"])
+def test_segmented_plan_device_equals_host(ctx, model, dtype, mesh, monkeypatch):
+    """The SEGMENTED plan built on the device (seg_plan.cu) is the host
+    builder's plan word for word: same statistics, and the map run with either
+    plan gives bitwise-identical f, K and energy (the kernel is deterministic
+    in its plan).  Meshes: renumbered Kuhn cube, the irregular blob, and a
+    scrambled (unrenumbered) cube with ragged tiles."""
+    from synth import mesh as M
+    from paper_1506_07577_b200.tetfem import TetFEM
+    if mesh == "kuhn":
+        X, tets = M.kuhn6(12)
+    elif mesh == "blob":
+        X, tets, _ = M.blob(target_T=30_000)
+    else:
+        X, tets = M.kuhn6(8)
+        X, tets = M.permute_vertices(X, tets, 5)
+        tets = M.permute_tets(tets, 6)
+    rng = np.random.default_rng(3)
+    u = 0.02 * X * np.array([1.0, -0.5, 0.3]) + rng.uniform(-1e-3, 1e-3, size=X.shape)
+    from synth import state as S
+    mu, lam = S.materials(tets.shape[0], 2e5, 0.3, spread=0.1)
+    out = []
+    for which in ("device", "host"):
+        monkeypatch.setenv("EBB_SEG_PLAN", which)
+        fem = TetFEM(ctx, X, tets, dtype=dtype, mu=mu, lam=lam, u=u, renumber=(mesh != "noren"),
+                     name=f"pl{model}{dtype}{mesh}{which}")
+        fem.map_forces(model, scatter=SCATTERS["segmented"])
+        st = fem.plan_stats()
+        out.append((st, fem.f.read(), fem.K.read(), fem.energy.get()))
+    (sd, fd, Kd, ed), (sh, fh, Kh, eh) = out
+    for k in ("tiles", "instances", "entries", "items", "instance_cap", "max_tile_entries"):
+        assert sd[k] == sh[k], k
+    assert np.array_equal(fd, fh) and np.array_equal(Kd, Kh) and ed == eh

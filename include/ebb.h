@@ -248,7 +248,7 @@ ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field 
                                    gather it (no atomics, bitwise run-to-run
                                    deterministic).  EBB_E_RANGE if a forced
                                    tile size (EBB_TILE_VERTS) does not fit.   */
-#define EBB_SCATTER_SEGMENTED 4 /* single-pass owner tiles (host-built plan):
+#define EBB_SCATTER_SEGMENTED 4 /* single-pass owner tiles (device-built plan):
                                    every thread computes one instance's
                                    compact element state, then every owned
                                    edge row sums its blocks rebuilt from the
@@ -256,8 +256,8 @@ ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field 
                                    row's incident (tet, i, j), P:721-731, in
                                    place of the `+=` of P:885; no atomics,
                                    bitwise run-to-run deterministic).  The
-                                   plan is built on the host at the first call
-                                   for a (v, e) pair (synchronous; freed by
+                                   plan is built on the device at the first
+                                   call for a (v, e) pair (synchronous; freed by
                                    any relation permutation or ctx_free).
                                    EBB_E_RANGE if one vertex lies in more tets
                                    than the per-tile instance cap (256; 384
@@ -306,7 +306,8 @@ typedef struct {
 ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d, ebb_stream s);
 /* Statistics of the SEGMENTED map plan built for (v, e) (0 if none yet):
  * out = {tiles, instances, instances / tets (redundancy), entries, items,
- *        instance cap per tile, host build ms, largest tile's entries}.
+ *        instance cap per tile, plan build ms (on the device; on the host
+ *        with EBB_SEG_PLAN=host), largest tile's entries}.
  * Host-only; no device work. */
 ebb_status ebb_map_plan_stats(ebb_ctx ctx, ebb_field v, ebb_field e, double out[8]);
 /* Statistics of the CHUNK map plan built for (v, e) (0 if none yet; the

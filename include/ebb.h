@@ -240,14 +240,11 @@ ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field 
                                    tile holds) runs CHUNK, else ATOMIC; the
                                    choice is made once per (v, e).           */
 #define EBB_SCATTER_ATOMIC 1    /* per-tet red.global.add              */
-#define EBB_SCATTER_TILED 2     /* owner tiles, shared-memory atomic
-                                   accumulation of every block                */
-#define EBB_SCATTER_GATHER 3    /* owner tiles, warp-specialized: producer
-                                   warps stage per-instance element state in
-                                   shared memory, owner threads of each row
-                                   gather it (no atomics, bitwise run-to-run
-                                   deterministic).  EBB_E_RANGE if a forced
-                                   tile size (EBB_TILE_VERTS) does not fit.   */
+#define EBB_SCATTER_TILED 2     /* retired in round 2 (owner tiles with
+                                   shared-memory atomics; measured slower than
+                                   SEGMENTED at every size): EBB_E_ARG        */
+#define EBB_SCATTER_GATHER 3    /* retired in round 2 (warp-specialized owner
+                                   tiles; measured slower): EBB_E_ARG         */
 #define EBB_SCATTER_SEGMENTED 4 /* single-pass owner tiles (device-built plan):
                                    every thread computes one instance's
                                    compact element state, then every owned

@@ -312,8 +312,6 @@ ebb_status index_stats(Ctx* c, const uint32_t* index, uint64_t ns, uint32_t out[
 }
 
 void release_plans(Ctx* c) {
-    for (auto& P : c->plans) P.release();
-    c->plans.clear();
     for (SegPlan* P : c->segplans) {
         P->release();
         delete P;

@@ -50,39 +50,6 @@ struct Relation {
     bool alive = true;                 // false after ebb_relation_free
 };
 
-// Scatter plan of the tiled element map (built once per mesh, tet_map.cu):
-// vertex tiles of `nvt` consecutive (SFC-ordered) vertices own the canonical
-// edge rows (tail <= head) of their vertices; every tet touching a tile is an
-// "instance" of that tile with a 32-byte record (tet id, local row slot of
-// each of its 10 canonical pairs, local vertex of each owned corner, flags).
-struct MapPlan {
-    ebb_field v = EBB_NONE, e = EBB_NONE;
-    int nvt = 0;
-    int round = 0;                  // 0: tiled order; >0: gather rounds of this size (padded)
-    uint32_t ntiles = 0, max_slots = 0;
-    uint64_t ninst = 0, ncanon = 0;
-    uint32_t* inst_ptr = nullptr;   // ntiles + 1
-    uint4* recs = nullptr;          // 2 x uint4 per instance
-    uint32_t* tile_cptr = nullptr;  // ntiles + 1, canonical-slot offsets
-    uint32_t* crow = nullptr;       // ncanon: global row of canonical slot
-    uint32_t* ctrow = nullptr;      // ncanon: global row of its transpose
-    // gather strategy: per canonical slot the (instance, pair, transpose)
-    // contributions, per vertex the (instance, corner) force contributions
-    uint32_t max_inst = 0;          // most instances in one tile
-    uint32_t max_sent = 0;          // most row-contribution entries in one tile
-    uint32_t max_fent = 0;          // most force-contribution entries in one tile
-    uint32_t* slot_ptr = nullptr;   // ncanon + 1
-    uint32_t* slot_ent = nullptr;   // (local instance << 8) | (i << 6) | (j << 4) | pair, i/j as stored
-    uint32_t* fv_ptr = nullptr;     // nverts + 1
-    uint32_t* fv_ent = nullptr;     // (local instance << 2) | corner
-    void release() {
-        cudaFree(inst_ptr); cudaFree(recs); cudaFree(tile_cptr); cudaFree(crow); cudaFree(ctrow);
-        cudaFree(slot_ptr); cudaFree(slot_ent); cudaFree(fv_ptr); cudaFree(fv_ent);
-        inst_ptr = nullptr; recs = nullptr; tile_cptr = nullptr; crow = nullptr; ctrow = nullptr;
-        slot_ptr = slot_ent = fv_ptr = fv_ent = nullptr;
-    }
-};
-
 // Plan of the SEGMENTED element map (seg_map.cu, built once per mesh on the
 // host): variable vertex tiles (consecutive SFC-ordered vertices) grown until
 // the tets touching them ("instances") reach `ni`, so one tile is one pass of
@@ -194,8 +161,7 @@ struct Ctx : ebb_ctx_s {
     size_t ev_used = 0;
     struct TimedLaunch { int kernel; cudaEvent_t a, b; };
     std::vector<TimedLaunch> timed;
-    std::vector<MapPlan> plans;     // invalidated by any relation permutation
-    std::vector<SegPlan*> segplans; // (same)
+    std::vector<SegPlan*> segplans; // invalidated by any relation permutation
     std::vector<ChunkPlan*> chunkplans; // (same)
     struct AutoMap { ebb_field v, e; int strategy; };
     std::vector<AutoMap> auto_map;      // AUTO's strategy per (v, e) mesh (same lifetime as the plans)

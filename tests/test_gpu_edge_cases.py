@@ -21,7 +21,7 @@ from synth import state as S
 
 pytestmark = pytest.mark.gpu
 
-SCATTERS = {"atomic": 1, "tiled": 2, "gather": 3, "segmented": 4, "color": 5, "chunk": 6}
+SCATTERS = {"atomic": 1, "segmented": 4, "color": 5, "chunk": 6}
 
 
 @pytest.fixture(scope="module")
@@ -102,7 +102,7 @@ def test_small_blob(ctx, model, scatter):
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-@pytest.mark.parametrize("scatter", ["segmented", "tiled", "gather", "chunk"])
+@pytest.mark.parametrize("scatter", ["segmented", "chunk"])
 def test_without_renumbering(ctx, scatter):
     """Scrambled vertex order (no SFC renumbering): tiles are ragged and
     tiny, the plan still covers every row exactly once."""

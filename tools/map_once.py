@@ -17,7 +17,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="f64")
     ap.add_argument("--model", default="nh")
-    ap.add_argument("--scatter", default="tiled")
+    ap.add_argument("--scatter", default="segmented")
     ap.add_argument("--n", type=int, default=55)
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
@@ -34,8 +34,8 @@ def main():
     mu, lam = S.materials(tets.shape[0], 1e6, 0.3, spread=0.1)
     ctx = ebb.Context(0)
     fem = TetFEM(ctx, X, tets, dtype=a.dtype, mu=mu, lam=lam, free=free, u=S.twist_u(X, a.n, 6, free=free))
-    sid = {"atomic": A.SCATTER_ATOMIC, "tiled": A.SCATTER_TILED, "gather": A.SCATTER_GATHER,
-           "segmented": A.SCATTER_SEGMENTED, "chunk": A.SCATTER_CHUNK}[a.scatter]
+    sid = {"atomic": A.SCATTER_ATOMIC, "segmented": A.SCATTER_SEGMENTED, "chunk": A.SCATTER_CHUNK,
+           "color": A.SCATTER_COLOR}[a.scatter]
     for _ in range(a.reps):
         fem.map_forces(a.model, scatter=sid)
     torch.cuda.synchronize()

@@ -38,8 +38,8 @@ def main():
     from synth import mesh as M
     from synth import state as S
 
-    scat = {"atomic": A.SCATTER_ATOMIC, "tiled": A.SCATTER_TILED, "gather": A.SCATTER_GATHER,
-            "segmented": A.SCATTER_SEGMENTED, "color": A.SCATTER_COLOR, "chunk": A.SCATTER_CHUNK}
+    scat = {"atomic": A.SCATTER_ATOMIC, "segmented": A.SCATTER_SEGMENTED, "color": A.SCATTER_COLOR,
+            "chunk": A.SCATTER_CHUNK}
     ctx = ebb.Context(0)
     for n in [int(x) for x in a.sizes.split(",")]:
         X, tets = M.kuhn6(n)

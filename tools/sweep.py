@@ -2,7 +2,7 @@
 """Secondary measurements of SURVEY §8(d) (not the bench line): one JSON line each.
 
   C3  StVK (and NH) force+stiffness map on a ~1e7-tet blob mesh, fp32 and fp64,
-      tiled vs atomic scatter -- tets/s and fraction of measured HBM peak.
+      segmented vs chunk vs atomic scatter -- tets/s and fraction of measured HBM peak.
   C4  edge-relation matvec sweep over Kuhn-6 meshes (1e5 .. 1e8 tets), fp32 vs
       fp64 -- GB/s and fraction of peak (algorithmic bytes of §8(d)).
 
@@ -41,7 +41,7 @@ def _prewarm(seconds=0.5):
 
 
 def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000, kuhn_n=0,
-           scatters=("segmented", "gather", "tiled", "atomic")):
+           scatters=("segmented", "chunk", "atomic")):
     import numpy as np
     import torch
 
@@ -69,8 +69,8 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
         T, V, E = fem.nt, fem.nv, fem.ne
         bf = 4 if dt == "f32" else 8
         for model in models:
-            ids = {"segmented": A.SCATTER_SEGMENTED, "gather": A.SCATTER_GATHER, "tiled": A.SCATTER_TILED,
-                   "atomic": A.SCATTER_ATOMIC, "color": A.SCATTER_COLOR, "chunk": A.SCATTER_CHUNK}
+            ids = {"segmented": A.SCATTER_SEGMENTED, "atomic": A.SCATTER_ATOMIC, "color": A.SCATTER_COLOR,
+                   "chunk": A.SCATTER_CHUNK}
             for scat in scatters:
                 sid = ids[scat]
                 fem.map_forces(model, scatter=sid)
@@ -350,7 +350,7 @@ def main():
     ap.add_argument("--spring", action="store_true", help="the Fig. 2 spring-mass step on every --sizes Kuhn mesh")
     ap.add_argument("--ebe", action="store_true", help="matrix-free vs assembled matvec on every --sizes Kuhn mesh")
     ap.add_argument("--grid", action="store_true", help="2-D grid stencil and particle interpolation")
-    ap.add_argument("--scatters", default="segmented,gather,tiled,atomic")
+    ap.add_argument("--scatters", default="segmented,chunk,atomic")
     ap.add_argument("--dtypes", default="f32,f64")
     ap.add_argument("--models", default="stvk,nh")
     a = ap.parse_args()

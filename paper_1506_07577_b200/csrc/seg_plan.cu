@@ -140,9 +140,22 @@ __global__ void ksp_inst_keys(uint64_t n4, const uint32_t* __restrict__ vkey, co
     if (q < n4) key[q] = ((uint64_t)tile_of_v[vkey[q]] << 32) | vt[q];
 }
 
-__global__ void ksp_hist_hi(const uint64_t* __restrict__ k, uint64_t n, int shift, uint32_t* __restrict__ cnt) {
-    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(cnt + (k[i] >> shift), 1u);
+// per tile: the number of sorted keys whose high bits (>> shift) equal the
+// tile (two lower bounds in the sorted key array; no atomics)
+__global__ void ksp_hist_hi(const uint64_t* __restrict__ k, uint64_t n, int shift, uint32_t* __restrict__ cnt,
+                            uint32_t ntiles) {
+    const uint64_t T = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (T >= ntiles) return;
+    auto lb = [&](uint64_t x) {
+        uint64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if ((k[mid] >> shift) < x) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    cnt[T] = (uint32_t)(lb(T + 1) - lb(T));
 }
 
 // instance records (tet, slot | energy owner << 16); slot = position in the tile
@@ -434,7 +447,7 @@ ebb_status build_seg_plan_device(Ctx* c, const uint32_t* tv, uint64_t nt, const 
     EBB_CUDA(c, icnt.alloc((ntiles + 1) * 4));
     EBB_CUDA(c, inst0.alloc((ntiles + 1) * 4));
     EBB_CUDA(c, cudaMemset(icnt.p, 0, (ntiles + 1) * 4));
-    if (ninst) ksp_hist_hi<<<grid_for(ninst, B), B>>>(uk.as<uint64_t>(), ninst, 32, icnt.as<uint32_t>());
+    if (ninst) ksp_hist_hi<<<grid_for(ntiles, B), B>>>(uk.as<uint64_t>(), ninst, 32, icnt.as<uint32_t>(), ntiles);
     EBB_TRY(exscan<uint32_t>(c, icnt.as<uint32_t>(), inst0.as<uint32_t>(), ntiles + 1));
     EBB_CUDA(c, cudaMalloc(&P->inst, ninst * 8 + 16));
     if (ninst)
@@ -471,7 +484,7 @@ ebb_status build_seg_plan_device(Ctx* c, const uint32_t* tv, uint64_t nt, const 
     EBB_CUDA(c, e0u.alloc((ntiles + 1) * 4));
     EBB_CUDA(c, e0p.alloc((ntiles + 1) * 4));
     EBB_CUDA(c, cudaMemset(ecnt.p, 0, (ntiles + 1) * 4));
-    if (nent_raw) ksp_hist_hi<<<grid_for(nent_raw, B), B>>>(ek2.as<uint64_t>(), nent_raw, 27, ecnt.as<uint32_t>());
+    if (nent_raw) ksp_hist_hi<<<grid_for(ntiles, B), B>>>(ek2.as<uint64_t>(), nent_raw, 27, ecnt.as<uint32_t>(), ntiles);
     ksp_pad4<<<grid_for(ntiles + 1, B), B>>>(ntiles + 1, ecnt.as<uint32_t>(), ecntp.as<uint32_t>());
     EBB_TRY(exscan<uint32_t>(c, ecnt.as<uint32_t>(), e0u.as<uint32_t>(), ntiles + 1));
     EBB_TRY(exscan<uint32_t>(c, ecntp.as<uint32_t>(), e0p.as<uint32_t>(), ntiles + 1));

@@ -26,7 +26,7 @@ import bench  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--P", default="2,4,8")
+    ap.add_argument("--P", default="1,2,4,8")
     ap.add_argument("--per-rank", type=int, default=1_000_000)
     ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
@@ -82,6 +82,22 @@ def main():
                     tot += ev[0].elapsed_time(ev[1])
                 ex_us = 1e3 * tot / a.reps / P      # all P ranks' exchanges run one after the other here
             ctx.timing(False)
+            # one whole distributed implicit step (map, reverse add, assembly,
+            # 50 PCG iterations, halos, allreduces) per PCG driver; all P ranks
+            # run one after the other on this GPU, so per rank = total / P
+            step_ms = {}
+            for cg in ("single", "saad"):
+                dist.implicit_step(ranks, T, w["model"], h=w["h"], iters=w["cg_iters"], variant=cg)   # warm-up
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                tot = 0.0
+                for _ in range(2):
+                    flush.zero_()
+                    ev[0].record()
+                    dist.implicit_step(ranks, T, w["model"], h=w["h"], iters=w["cg_iters"], variant=cg)
+                    ev[1].record()
+                    ev[1].synchronize()
+                    tot += ev[0].elapsed_time(ev[1])
+                step_ms[cg] = tot / 2 / P
             bf = 8
             halo_rows = [sum(b[1][3][1].shape[0] for b in R._lists["fwd"]["send"].values()) for R in ranks]
             line = {"P": P, "variant": variant, "global_tets": int(tets.shape[0]), "n": n,
@@ -91,6 +107,8 @@ def main():
                     "reverse_bytes_per_rank": [int(R.rev_bytes["rf"] + R.rev_bytes["rK"]) for R in ranks]
                     if variant == "reverse" else None,
                     "reverse_exchange_us_per_rank": ex_us if variant == "reverse" else None,
+                    "step_ms_per_rank": step_ms,
+                    "pcg_iter_us_per_rank_incl_halo": {k: 1e3 * v / w["cg_iters"] for k, v in step_ms.items()},
                     "fwd_halo_rows_per_rank": halo_rows,
                     "fwd_halo_bytes_per_iteration_per_rank": [r_ * 4 * bf for r_ in halo_rows],
                     "note": "virtual ranks on one B200; exchange = pack + device copy + scatter(-add), the bytes "

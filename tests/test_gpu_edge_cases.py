@@ -313,3 +313,46 @@ def test_pcg_blob(ctx, variant):
     free = S.fixed_mask(X, n)
     fem, ref = _pcg_case(ctx, X, tets, free, f"pcgblob{variant}", variant, 50)
     assert rel_l2(fem.dv.read(), ref["dv"]) <= 1e-8
+
+
+def _jacobi_condition(m, A, free):
+    """kappa_2 of D^-1/2 A D^-1/2 on the free DOFs (dense; small meshes only)."""
+    nv = m.nv
+    Ad = np.zeros((3 * nv, 3 * nv))
+    for v in range(nv):
+        for e in range(m.row_ptr[v], m.row_ptr[v + 1]):
+            Ad[3 * v:3 * v + 3, 3 * m.head[e]:3 * m.head[e] + 3] = A[e].reshape(3, 3)
+    keep = np.repeat(np.asarray(free).astype(bool), 3)
+    As = Ad[np.ix_(keep, keep)]
+    d = 1.0 / np.sqrt(np.diag(As))
+    ev = np.linalg.eigvalsh(d[:, None] * As * d[None, :])
+    return ev[-1] / ev[0]
+
+
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
+def test_pcg_fp32_50_iterations_derived_tolerance(ctx, variant, monkeypatch):
+    """fp32 map + assembly + 50 PCG iterations (north_star's count) against the
+    oracle's fp64 step on the fp32-rounded inputs.  The tolerance follows from
+    the perturbation bound of a linear system, not a choice: the fp32 f and K
+    carry at most the north_star fp32 bars (eps_b = eps_A = 1e-5 relative;
+    b ~ h f here), so ||dv32 - dv64|| / ||dv64|| <= kappa (eps_A + eps_b) +
+    40 kappa u (the recurrences' own rounding, u = 2^-24), with kappa the
+    2-norm condition number of the Jacobi-scaled free-DOF system (entrywise
+    relative perturbations), computed here."""
+    monkeypatch.setenv("EBB_CG_VARIANT", variant)
+    from helpers import Case, gpu_fem, oracle_renumbered
+    case = Case(n=4, model="nh")
+    for a in ("u", "mu", "lam", "vel"):
+        setattr(case, a, getattr(case, a).astype(np.float32).astype(np.float64))
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
+                               case.free[order], 1e-2, iters=50)
+    kappa = _jacobi_condition(m, ref["A"], case.free[order])
+    tol = kappa * (1e-5 + 1e-5) + 40.0 * kappa * 2.0 ** -24
+    assert tol < 1e-3
+    fem = gpu_fem(ctx, case, dtype="f32", name=f"pcg32d{variant}")
+    fem.map_forces("nh")
+    fem.assemble(1e-2)
+    fem.cg_init()
+    fem.cg_step(50)
+    assert rel_l2(fem.dv.read(), ref["dv"]) <= tol

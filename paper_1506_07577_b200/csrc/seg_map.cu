@@ -771,9 +771,12 @@ int seg_threads(ebb_dtype dt, int model, uint64_t nt) {
         const int v = atoi(e);
         return (dt == EBB_F64 && model == EBB_STVK && v > 384) ? 384 : v;
     }
-    // measured: fp64 StVK 384; fp32 StVK 512 from 4e6 tets
-    // (11 % faster at 1e7 tets, 1-2 % slower at <= 1e6); otherwise 256
+    // measured: fp64 StVK 384; fp64 NH 512 from 2e6 tets
+    // (7-12 % faster from 3e6 tets, equal at 1e6, 5 % slower at 3e5); fp32
+    // StVK 512 from 4e6 tets (11 % faster at 1e7, 1-2 % slower at <= 1e6);
+    // otherwise 256
     if (dt == EBB_F64 && model == EBB_STVK) return 384;
+    if (dt == EBB_F64 && model == EBB_NH && nt >= 2000000) return 512;
     if (dt == EBB_F32 && model == EBB_STVK && nt >= 4000000) return 512;
     return 256;
 }

@@ -363,8 +363,9 @@ class GpuRank:
         torch.cuda.synchronize()
 
     def _make_lists(self, tag, prefix, send, recv, ncs):
-        """Row lists + staging buffers (one per component count) per peer."""
-        import torch
+        """Row lists + staging buffers (one per component count) per peer: the
+        buffers are library fields on the list relation, seen by the
+        transports as zero-copy torch views."""
         L = {"send": {}, "recv": {}}
         for kind, lists in (("send", send), ("recv", recv)):
             for peer, rows in lists.items():
@@ -372,8 +373,8 @@ class GpuRank:
                 rf = rel.field("rows", "u32", init=np.asarray(rows).astype(np.uint32))
                 bufs = {}
                 for nc in ncs:
-                    buf = torch.zeros((len(rows), nc), dtype=self.tdt, device=f"cuda:{self.ctx.device}")
-                    bufs[nc] = (rel.wrap(f"buf{nc}", buf, self.dtype, (nc, 1)), buf)
+                    bf = rel.field(f"buf{nc}", self.dtype, (nc, 1))
+                    bufs[nc] = (bf, bf.tensor().view(len(rows), nc))
                 L[kind][peer] = (rf, bufs)
         L["peers"] = sorted(set(L["send"]) | set(L["recv"]))
         self._lists[tag] = L

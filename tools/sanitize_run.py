@@ -9,7 +9,8 @@ scatter strategy (fp64 and fp32, StVK and NH), assembly, the edge-relation
 matvec, every persistent PCG variant (Saad, single-reduction, symmetric) and
 the phase kernels of the multi-GPU driver, the explicit update, the matrix-free
 EBE matvec, the Fig. 2 spring-mass step (fused and paper form) and the 2-D grid
-stencil / PointLocate / particle interpolation.  Prints one line per stage;
+stencil / PointLocate / particle interpolation, and the multi-GPU setup and
+exchange kernels on 2 virtual ranks.  Prints one line per stage;
 the sanitizer's own report is the evidence (profiles/r02_sanitizer_*.txt).
 """
 from __future__ import annotations
@@ -94,6 +95,30 @@ def main():
             torch.cuda.synchronize()
             print(f"n={n} {dt} spring ok", flush=True)
             del fem
+    # the multi-GPU setup and exchange kernels on 2 virtual ranks: device
+    # partition (overlap and own modes), reverse-add lists, SOA row gather,
+    # scatter-add, the distributed map step and one distributed implicit step
+    from paper_1506_07577_b200 import dist
+    X, tets = M.kuhn6(6)
+    X, tets = M.permute_vertices(X, tets, 2)
+    free = S.fixed_mask(X, 6)
+    u = S.stretch_noise_u(X, 6, 1, free=free)
+    mu, lam = S.materials(tets.shape[0], 2e5, 0.3)
+    for variant in ("overlap", "reverse"):
+        ranks = []
+        for r in range(2):
+            dist.partition_rank(ctx, X, tets, 2, r, name=f"sp_own{variant}{r}", mode="own")
+            part = dist.partition_rank(ctx, X, tets, 2, r, name=f"sp{variant}{r}")
+            ranks.append(dist.GpuRank(ctx, r, part, X, free, u, np.zeros_like(u), mu, lam, name=f"sr{variant}{r}",
+                                      map_variant=variant, nranks=2))
+        dist.map_step(ranks, dist.LocalTransport(), "nh")
+        dist.implicit_step(ranks, dist.LocalTransport(), "nh", iters=5, variant="single")
+        torch.cuda.synchronize()
+        print(f"dist {variant} ok", flush=True)
+        del ranks
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()   # the halo staging tensors come from torch's caching allocator
     g = Grid2(ctx, 37, 29, name="sgrid")
     rng = np.random.default_rng(3)
     fin = g.cells.field("fin", "f64", (2, 1), init=rng.uniform(-1, 1, size=(37 * 29, 2)))

@@ -285,3 +285,39 @@ def test_distributed_map_step(ctx, P, model, dtype, map_variant):
         kp_in[ids] = Qf.read()[R.owned_stored]
     assert rel_l2(f_in[order], f) <= tol
     assert rel_l2(kp_in[order], Kp) <= tol
+
+
+def test_partition_and_halo_entry_points_refuse_bad_arguments(ctx):
+    """Argument checks of the round-2 multi-GPU entry points: a rank outside
+    [0, nparts), an unknown mode, owner fields of the wrong type, a
+    scatter-add into a key-field or an integer field, reverse lists from
+    fields on the wrong relations."""
+    import ctypes as C
+
+    from paper_1506_07577_b200 import _abi as A
+    from paper_1506_07577_b200.ebb import EbbError
+    case = Case(n=3)
+    V = ctx.relation("bad.verts", case.X.shape[0])
+    T = ctx.relation("bad.tets", case.tets.shape[0])
+    v = T.key_field("v", V, (4, 1), case.tets)
+    ot, ov = T.field("ot", "i32"), V.field("ov", "i32")
+    ctx.check(ctx.L.ebb_partition(ctx.h, v.h, 2, ot.h, ov.h))
+    info = A.PartitionInfo()
+    sp, rp = (C.c_uint64 * 3)(), (C.c_uint64 * 3)()
+    for rank, mode, o_t, o_v, err in ((2, 0, ot, ov, "EBB_E_ARG"), (0, 7, ot, ov, "EBB_E_ARG"),
+                                      (0, 0, ov, ot, "EBB_E_TYPE")):
+        with pytest.raises(EbbError, match=err):
+            ctx.check(ctx.L.ebb_partition_local(ctx.h, v.h, o_t.h, o_v.h, 2, rank, mode, b"bad", C.byref(info),
+                                                sp, rp))
+    rows = V.field("rows_b", "u32", init=np.arange(case.X.shape[0], dtype=np.uint32))
+    buf = V.field("buf_b", "u32")
+    with pytest.raises(EbbError):
+        ctx.check(ctx.L.ebb_rows_scatter_add(ctx.h, v.h, rows.h, buf.h, None))     # key-field target
+    ivals = V.field("ival", "i32")
+    ibuf = V.field("ibuf", "i32")
+    with pytest.raises(EbbError, match="EBB_E_TYPE"):
+        ctx.check(ctx.L.ebb_rows_scatter_add(ctx.h, ivals.h, rows.h, ibuf.h, None))
+    rinfo = A.ReverseInfo()
+    ptr = (C.c_uint64 * 12)()
+    with pytest.raises(EbbError, match="EBB_E_TYPE"):
+        ctx.check(ctx.L.ebb_partition_reverse(ctx.h, v.h, v.h, rows.h, ov.h, 2, 0, b"badrev", C.byref(rinfo), ptr))

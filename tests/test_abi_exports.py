@@ -74,3 +74,17 @@ def test_every_entry_point_cites_its_passage():
         if m and not re.search(r"P:\d|S:\d|SURVEY|§", "\n".join(lines[max(0, i - 25):i + 1])):
             missing.append(m.group(2))
     assert not missing, missing
+
+
+def test_header_is_plain_c():
+    """include/ebb.h is a C ABI: it compiles as C99 (no C++ or torch types)
+    and as C++."""
+    import os
+    import shutil
+    hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "ebb.h")
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    for lang, std in (("c", "-std=c99"), ("c++", "-std=c++17")):
+        r = subprocess.run(["gcc" if lang == "c" else "g++", "-fsyntax-only", "-x", lang, std, "-Wall", "-Werror", hdr],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr

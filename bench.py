@@ -216,19 +216,40 @@ def _config(world, sample=False, n=None):
             "tets": T, "verts": V, "edge_rows": E, "h": WORKLOAD["h"], "cg_iters": WORKLOAD["cg_iters"],
             "E_young": WORKLOAD["E"], "nu": WORKLOAD["nu"], "wall_ramp": WORKLOAD["wall_ramp"],
             "l2": "flushed between timed steps (256 MiB write); per-step working set ~5 GB > 126 MB L2",
+            "state": "every step starts from the seeded initial state (u0, v0): the same physical step each time, "
+                     "reset outside the timed events",
             "parallelism": "single GPU" if world == 1 else f"{world} GPUs, domain decomposition (weak)"}
+
+
+def state_reset(fem, stream):
+    """Every step starts from the seeded initial state (u0, v0): the same
+    physical step -- one batch of synthetic input -- each time.  Left to
+    evolve, the soft T10M body sags under gravity and inverts tets after ~20
+    unconverged 50-iteration steps (NaN from step 22), and a step timed on
+    that state would be physically meaningless.  The copy runs on `stream`,
+    outside the timed events (inputs resident in HBM, like the L2 flush)."""
+    import torch
+    u0, v0 = fem.u.tensor().clone(), fem.vel.tensor().clone()
+
+    def reset():
+        with torch.cuda.stream(stream):
+            fem.u.tensor().copy_(u0)
+            fem.vel.tensor().copy_(v0)
+    return reset
 
 
 def _measure(ctx, fem, w, stream, flush, steps, warmup, use_graph, world=1, clocks_device=None):
     """W warm-up steps, then K timed steps (one CUDA graph per step), L2 flushed
-    between steps outside the events; per-kernel times from the library's
-    event records (graph event nodes)."""
+    and the state reset to (u0, v0) between steps outside the events;
+    per-kernel times from the library's event records (graph event nodes)."""
     import torch
     import torch.distributed as dist
 
     from paper_1506_07577_b200 import _abi as A
+    reset = state_reset(fem, stream)
 
     def step():
+        reset()
         fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"], stream=stream)
 
     # clocks ramp from idle: untimed steps for >= 0.5 s before the W warm-up steps
@@ -246,15 +267,18 @@ def _measure(ctx, fem, w, stream, flush, steps, warmup, use_graph, world=1, cloc
     if use_graph:
         # one implicit step captured as a CUDA graph (kernel timers become graph
         # event nodes: each replay re-records them)
+        reset()
         ctx.graph_begin(stream)
-        step()
+        fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"], stream=stream)
         graph = ctx.graph_end(stream)
+        reset()
         ctx.graph_launch(graph, stream)          # untimed replay
         torch.cuda.synchronize()
 
     def run_step():
+        # the state reset is part of step() (eager) and outside the graph
         if graph is None:
-            step()
+            fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"], stream=stream)
         else:
             ctx.graph_launch(graph, stream)
 
@@ -272,6 +296,7 @@ def _measure(ctx, fem, w, stream, flush, steps, warmup, use_graph, world=1, cloc
         for k in range(steps):
             with torch.cuda.stream(stream):
                 flush.zero_()                          # L2 flush, outside the timed events
+            reset()                                    # state (u0, v0), outside the timed events
             evs[k][0].record(stream)
             run_step()
             evs[k][1].record(stream)
@@ -295,7 +320,7 @@ def _measure(ctx, fem, w, stream, flush, steps, warmup, use_graph, world=1, cloc
         v["avg_us"] = 1e3 * v["total_ms"] / max(v["launches"], 1)
     ctx.timing(False)
     return {"t_ms": t_ms, "kt": kt, "launches": launches, "clocks": clk.summary(),
-            "errors": ctx.error_counts(reset=True), "graph": graph, "run_step": run_step}
+            "errors": ctx.error_counts(reset=True), "graph": graph, "run_step": run_step, "reset": reset}
 
 
 def _components(fem, w, kt, t_ms, peak, workload_name):
@@ -350,11 +375,16 @@ def run_ours(args, rank, world, local_rank):
     t_ms, kt, graph, run_step = M_["t_ms"], M_["kt"], M_["graph"], M_["run_step"]
     value = world * T * args.steps / (t_ms / 1e3)
 
-    # ---- end to end through the public API: host state in, step, host state out
+    # ---- end to end through the public API: the step's input state (u0, v0)
+    # from pinned host memory, the step, the new state (u, v) back to the host
+    M_["reset"]()
+    torch.cuda.synchronize()
     u_h = torch.empty((V, 3), dtype=torch.float64, pin_memory=True)
     v_h = torch.empty((V, 3), dtype=torch.float64, pin_memory=True)
     u_h.copy_(torch.from_numpy(fem.u.read()))
     v_h.copy_(torch.from_numpy(fem.vel.read()))
+    u_o = torch.empty_like(u_h).pin_memory()
+    v_o = torch.empty_like(v_h).pin_memory()
     nb = V * 3 * 8
     e2e_ms = 0.0
     for k in range(args.steps):
@@ -365,14 +395,14 @@ def run_ours(args, rank, world, local_rank):
         fem.u.write_async(u_h.data_ptr(), nb, stream)
         fem.vel.write_async(v_h.data_ptr(), nb, stream)
         run_step()
-        fem.u.read_into(u_h.data_ptr(), nb, stream)      # synchronous
-        fem.vel.read_into(v_h.data_ptr(), nb, stream)
+        fem.u.read_into(u_o.data_ptr(), nb, stream)      # synchronous
+        fem.vel.read_into(v_o.data_ptr(), nb, stream)
         b.record(stream)
         b.synchronize()
         e2e_ms += a.elapsed_time(b)
     e2e = {"value": world * T * args.steps / (e2e_ms / 1e3), "unit": "tets/s",
            "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
-           "api": "ebb_field_write (pinned host u, v) -> implicit step (TetFEM.implicit_step as captured graph) -> "
+           "api": "ebb_field_write (pinned host u0, v0) -> implicit step (TetFEM.implicit_step as captured graph) -> "
                   "ebb_field_read (u, v)"}
 
     # ---- roofline of the dominant kernel (largest share of the timed step)
@@ -472,14 +502,18 @@ def run_dist(args, rank, world, local_rank):
     cg_var = args.dist_cg
     kmv = A.K_CG_SOLVE if cg_var == "single" else A.K_EDGE_MATVEC   # the streamed-matrix kernel of a phase
 
+    reset = state_reset(R.fem, stream)       # local u, v (owned + ghost rows) back to (u0, v0)
+
     def step():
         D.implicit_step([R], T, w["model"], h=w["h"], iters=w["cg_iters"], variant=cg_var)
 
     t_pre = time.perf_counter()              # clocks ramp from idle (see run_ours)
     while time.perf_counter() - t_pre < 0.5:
+        reset()
         step()
         torch.cuda.synchronize()
     for _ in range(args.warmup):
+        reset()
         step()
     torch.cuda.synchronize()
     ctx.timing(True)
@@ -488,12 +522,15 @@ def run_dist(args, rank, world, local_rank):
     if not args.no_graph:
         # the whole distributed step -- kernels and the in-library NCCL calls on
         # one stream -- captured once and replayed (no host loop per iteration)
+        reset()
         ctx.graph_begin(stream)
         step()
         graph = ctx.graph_end(stream)
+        reset()
         ctx.graph_launch(graph, stream)       # untimed replay (keeps the captured timer records)
         torch.cuda.synchronize()
     ctx.launch_count(reset=True)
+    ctx.error_counts(reset=True)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     mp_tot, mp_cnt, mv_tot, mv_cnt = 0.0, 0, 0.0, 0
     dist.barrier()
@@ -502,6 +539,7 @@ def run_dist(args, rank, world, local_rank):
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
+            reset()
             evs[k][0].record(stream)
             if graph is None:
                 step()
@@ -519,6 +557,7 @@ def run_dist(args, rank, world, local_rank):
         torch.cuda.synchronize()
     dist.barrier()
     launches = ctx.launch_count(reset=True)
+    errs = ctx.error_counts(reset=True)
     t_ms = sum(a.elapsed_time(b) for a, b in evs)
     mv_ms, mv_n = ctx.timing_read(kmv)
     mp_ms, mp_n = ctx.timing_read(A.K_TET_MAP, reset=True)
@@ -531,10 +570,14 @@ def run_dist(args, rank, world, local_rank):
     # ---- end to end: every rank uploads its local u, v from pinned host memory,
     # runs the step (graph replay incl. the NCCL calls) and reads u, v back
     V_loc = R.fem.nv
+    reset()
+    torch.cuda.synchronize()
     u_h = torch.empty((V_loc, 3), dtype=torch.float64, pin_memory=True)
     v_h = torch.empty((V_loc, 3), dtype=torch.float64, pin_memory=True)
     u_h.copy_(torch.from_numpy(R.fem.u.read()))
     v_h.copy_(torch.from_numpy(R.fem.vel.read()))
+    u_o = torch.empty_like(u_h).pin_memory()
+    v_o = torch.empty_like(v_h).pin_memory()
     nb = V_loc * 3 * 8
     e2e_ms = 0.0
     dist.barrier()
@@ -549,8 +592,8 @@ def run_dist(args, rank, world, local_rank):
             step()
         else:
             ctx.graph_launch(graph, stream)
-        R.fem.u.read_into(u_h.data_ptr(), nb, stream)
-        R.fem.vel.read_into(v_h.data_ptr(), nb, stream)
+        R.fem.u.read_into(u_o.data_ptr(), nb, stream)
+        R.fem.vel.read_into(v_o.data_ptr(), nb, stream)
         b_.record(stream)
         b_.synchronize()
         e2e_ms += a_.elapsed_time(b_)
@@ -559,7 +602,7 @@ def run_dist(args, rank, world, local_rank):
     e2e_ms = float(tt.item())
     e2e = {"value": T_global * args.steps / (e2e_ms / 1e3), "unit": "tets/s", "h2d_bytes_per_step": 2 * nb,
            "d2h_bytes_per_step": 2 * nb,
-           "api": "per rank: ebb_field_write (pinned host local u, v) -> distributed implicit step (graph replay) "
+           "api": "per rank: ebb_field_write (pinned host local u0, v0) -> distributed implicit step (graph replay) "
                   "-> ebb_field_read (u, v); bytes of this rank"}
     peak, peak_src = _peaks()
     E_loc = R.fem.ne
@@ -582,7 +625,7 @@ def run_dist(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Kuhn-6 cube, stretch+noise displacement)",
             "config": cfg, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(),
-            "e2e": e2e,
+            "e2e": e2e, "device_errors": errs,
             "components": {"map_avg_us": 1e3 * mp_ms / max(mp_n, 1), "matvec_avg_us": avg_mv,
                            "local_tets": int(R.fem.nt), "local_verts": int(V_loc),
                            "owned_verts": int(part["n_owned"]), "partition_setup_s": t_part}}
@@ -648,6 +691,7 @@ def run_dist_map(args, rank, world, local_rank):
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
+            reset()
             evs[k][0].record(stream)
             if graph is None:
                 step()

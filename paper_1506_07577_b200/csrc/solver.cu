@@ -520,6 +520,21 @@ __device__ __forceinline__ double grid_sum_partials(const double* partials, unsi
     return *sm_tot;
 }
 
+#ifdef CG_PROF   // measurement-only build: per-phase clock split of thread 0 of every CTA
+__device__ unsigned long long g_cg_prof[8];
+#define CG_MARK(q)                                  \
+    do {                                            \
+        if (threadIdx.x == 0) {                     \
+            const long long tn_ = clock64();        \
+            cg_tp[q] += tn_ - cg_t0[0];             \
+            cg_t0[0] = tn_;                         \
+        }                                           \
+    } while (0)
+#else
+#define CG_MARK(q) \
+    do {           \
+    } while (0)
+#endif
 template <typename R>
 __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     k_cg_persistent(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
@@ -587,6 +602,13 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     if (iters > 0 && warp == TMA_CONSUMERS && lane == 0)
         for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
     const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
+#ifdef CG_PROF
+    __shared__ long long cg_tp[5], cg_t0[1];
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 5; ++q) cg_tp[q] = 0;
+        cg_t0[0] = clock64();
+    }
+#endif
     for (int it = 0; it < iters; ++it) {
         const R beta = (first || rho == 0.0) ? R(0) : (R)(rz_new / rho);
         const R* __restrict__ pold = cur ? pb1 : pb0;
@@ -673,10 +695,13 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
                 }
             }
         }
+        CG_MARK(0);   // this thread's matvec work
         pq = block_reduce<ROP_SUM>(pq);
+        CG_MARK(1);   // the CTA's other warps
         if (threadIdx.x == 0) part_pq[blockIdx.x] = pq;
         grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         const double pqs = grid_sum_partials(part_pq, gridDim.x, &sm_tot);
+        CG_MARK(2);   // grid barrier 1 (the other CTAs)
         if (blockIdx.x == 0 && threadIdx.x == 0 && pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
         rho = rz_new;                   // rho_k = r_k . z_k (beta above used the previous rho)
         first = 0;
@@ -705,9 +730,11 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
             acc += (double)rv.x * zv.x + (double)rv.y * zv.y + (double)rv.z * zv.z;
         }
         acc = block_reduce<ROP_SUM>(acc);
+        CG_MARK(3);   // update phase
         if (threadIdx.x == 0) part_rz[blockIdx.x] = acc;
         grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         rz_new = grid_sum_partials(part_rz, gridDim.x, &sm_tot);
+        CG_MARK(4);   // grid barrier 2
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             scal[S_PQ] = pqs;
             *rho_user = rz_new;
@@ -722,6 +749,13 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
     if (warp == TMA_CONSUMERS && lane == 0)
         for (uint64_t sq = (uint64_t)done_it * my_chunks; sq < issued; ++sq)
             mbar_wait(&full_bar[sq % TMA_NS], (uint32_t)((sq / TMA_NS) & 1u));
+#ifdef CG_PROF
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 5; ++q) atomicAdd(&g_cg_prof[q], (unsigned long long)cg_tp[q]);
+        atomicAdd(&g_cg_prof[5], 1ull);
+        atomicAdd(&g_cg_prof[6], (unsigned long long)done_it);
+    }
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         scal[S_RHO] = rho;
         scal[S_RZ] = rz_new;
@@ -807,6 +841,13 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
     if (iters > 0 && warp == TMA_CONSUMERS && lane == 0)
         for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(blockIdx.x + j * gridDim.x, issued++);
     const uint64_t gthreads = (uint64_t)gridDim.x * blockDim.x;
+#ifdef CG_PROF
+    __shared__ long long cg_tp[5], cg_t0[1];
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 5; ++q) cg_tp[q] = 0;
+        cg_t0[0] = clock64();
+    }
+#endif
     for (int it = 0; it < iters; ++it) {
         const R beta = (first || rho == 0.0) ? R(0) : (R)(rz_new / rho);
         const R* __restrict__ pold = cur ? pb1 : pb0;
@@ -933,9 +974,11 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
             acc += (double)rv.x * zv.x + (double)rv.y * zv.y + (double)rv.z * zv.z;
         }
         acc = block_reduce<ROP_SUM>(acc);
+        CG_MARK(3);   // update phase
         if (threadIdx.x == 0) part_rz[blockIdx.x] = acc;
         grid_barrier_t<R>(bar_count, bar_gen, gridDim.x);
         rz_new = grid_sum_partials(part_rz, gridDim.x, &sm_tot);
+        CG_MARK(4);   // grid barrier 2
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             scal[S_PQ] = pqs;
             *rho_user = rz_new;
@@ -1890,6 +1933,19 @@ ebb_status cg_iterate(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
                                                dinv, x, r, mask, c->d_partials, c->d_partials + 4096,
                                                c->d_counter + 10, c->d_counter + 11, scal, rho_user, c->d_err, cap,
                                                iters, cg_tol2(cg)));
+#ifdef CG_PROF
+                {
+                    unsigned long long h[8];
+                    cudaDeviceSynchronize();
+                    cudaMemcpyFromSymbol(h, g_cg_prof, sizeof(h));
+                    const unsigned long long zr[8] = {0};
+                    cudaMemcpyToSymbol(g_cg_prof, zr, sizeof(zr));
+                    const double n = (double)h[6];   // CTA-iterations
+                    fprintf(stderr, "CG_PROF grid %llu: per iteration (cycles, thread 0 of a CTA): matvec own %.0f, "
+                            "CTA wait %.0f, barrier1 %.0f, update %.0f, barrier2 %.0f\n", h[5], h[0] / n, h[1] / n,
+                            h[2] / n, h[3] / n, h[4] / n);
+                }
+#endif
                 return EBB_OK;
             }
         }

@@ -96,7 +96,8 @@ const char* ebb_last_error(ebb_ctx ctx);
  * error word of SURVEY §8(b) "Errors" (EBB_E_INVERTED, EBB_E_NOT_SPD,
  * EBB_E_BOUNDS classes): out[0] inverted elements (J<=0, the NH reading of
  * DESIGN.md §3 (15)), out[1] CG p.q<=0 events, out[2] key out of range
- * (S:87), out[3] reserved.  EBB_E_ARG on a bad context. */
+ * (S:87), out[3] peer waits abandoned by the fused multi-GPU PCG
+ * (ebb_cg_peer_step).  EBB_E_ARG on a bad context. */
 ebb_status ebb_error_counts(ebb_ctx ctx, uint64_t out[4], int reset);
 /* Wait for every call issued on stream s (NULL: the whole device); the
  * synchronising point of SURVEY §8(b) "Asynchrony".  EBB_E_CUDA on a
@@ -470,6 +471,76 @@ ebb_status ebb_comm_allreduce_sum(ebb_ctx ctx, double* dev_buf, uint64_t count, 
 ebb_status ebb_comm_halo(ebb_ctx ctx, int32_t npeers, const int32_t* peers, void* const* send_bufs,
                          const uint64_t* send_bytes, void* const* recv_bufs, const uint64_t* recv_bytes,
                          ebb_stream s);
+
+/* ---- fused multi-GPU PCG over peer memory ("the halo
+ * exchange of vertex positions ... and the allreduce of CG scalars", here
+ * without NCCL on the iteration path; the paper is single-device).
+ * The single-reduction PCG (EBB_CG_SINGLE_REDUCTION, Chronopoulos-Gear) of
+ * every rank runs as ONE persistent kernel for all iterations.  Each owner
+ * stores the rows of the gathered operand u (and of the iterate x) that
+ * peers hold as ghosts straight into the peers' buffers as it finishes them
+ * (P2P stores over NVLink; for ranks emulated on one device, plain stores),
+ * and the fused 2-scalar reduction (w.z, r.z) of each phase is exchanged
+ * through per-rank mailboxes (release/acquire at system scope), summed in
+ * rank order on every rank (bitwise the same alpha, beta everywhere).  The
+ * z_0 halo and the initial r.z sum are done in the same launch; the x halo
+ * lands before the kernel ends, so ebb_implicit_update can follow directly.
+ * Decomposition: EBB_PART_OVERLAP (ebb_partition_local): local vertices
+ * [0, n_owned) are owned, the rest ghosts; rows of ghosts are not solved.
+ * A wait that exceeds ~20 s (a peer that never arrives) counts in error word
+ * [3] and is abandoned (results then invalid) instead of hanging the GPU. */
+#define EBB_MAX_RANKS 16
+#define EBB_PEER_MBOX_WORDS 160   /* F64 rows of a mailbox field (see below)  */
+typedef struct {
+    int32_t nranks, rank;     /* P <= EBB_MAX_RANKS, 0 <= rank < P            */
+    uint64_t n_owned;         /* local verts [0, n_owned) are owned            */
+    ebb_field send_off;       /* from ebb_peer_send_csr: U32 CSR offsets (n_owned + 1)  */
+    ebb_field send_dst;       /* U32 2x1 (peer rank, row in the peer's local numbering) */
+    ebb_field mbox;           /* this rank's mailbox: F64 field of >= EBB_PEER_MBOX_WORDS
+                                 rows, all zero before the first step (ebb_field_fill 0) */
+    /* device addresses, valid on THIS rank's device, of rank q's cg.u, cg.u2,
+     * cg.x, cg.z and mailbox (IPC-mapped with ebb_ipc_open on multi-GPU, the
+     * fields' own addresses for ranks emulated on one device); [rank] unused */
+    uint64_t peer_u[EBB_MAX_RANKS], peer_u2[EBB_MAX_RANKS], peer_x[EBB_MAX_RANKS],
+             peer_z[EBB_MAX_RANKS], peer_mbox[EBB_MAX_RANKS];
+} ebb_peer_cg;
+/* Per-owned-vertex send lists for the fused PCG, built on the device: for
+ * each peer k (npeers of them, ranks peers[k]) send_rows[k] (U32 local rows,
+ * all < n_owned, e.g. ebb_partition_local's send rows of that peer) and
+ * remote_rows[k] (U32, the same length: the row of each of them in the
+ * peer's local numbering, i.e. the peer's recv rows from this rank, which
+ * list the same vertices in the same order), each < peer_nv[k].  Creates
+ * relations <name>.off (n_owned + 1 rows, U32 "off") and <name>.dst (one row
+ * per entry, U32 2x1 "dst" = (peer, remote row)), entries of a vertex in
+ * peers[] order.  EBB_E_RANGE on a row out of bounds.  Synchronous.
+ * (SURVEY §8(e) halo lists; P:1014 for the paper's single device) */
+ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_owned, int32_t npeers, const int32_t* peers,
+                             const ebb_field* send_rows, const ebb_field* remote_rows, const uint64_t* peer_nv,
+                             const char* name, ebb_field* send_off, ebb_field* send_dst);
+/* CUDA IPC of a library-allocated field (one process per GPU): the 64-byte
+ * handle of the field's allocation; open maps a peer's handle into this
+ * context's device (peer access enabled) and returns its device address;
+ * close unmaps it.  EBB_E_TYPE for borrowed (wrapped) fields.  (SURVEY §8(e):
+ * one process per GPU over NVLink) */
+ebb_status ebb_ipc_handle(ebb_ctx ctx, ebb_field f, void* handle64);
+ebb_status ebb_ipc_open(ebb_ctx ctx, const void* handle64, uint64_t* dev_addr);
+ebb_status ebb_ipc_close(ebb_ctx ctx, uint64_t dev_addr);
+/* Bind `nlocal` ranks whose systems live on this context's device (1 per
+ * process on a multi-GPU node; P for ranks emulated on one device) into a
+ * launch group: cgs[i] (after ebb_cg_init with EBB_CG_SINGLE_REDUCTION; its
+ * fields must outlive the group) and peers[i].  Validates and uploads the
+ * per-rank launch records once (synchronous, not capturable); *group_out is
+ * the group id.  EBB_E_SIZE if the ranks' CTAs cannot all be resident.
+ * (the PCG of P:946, Jacobi-preconditioned) */
+ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, const ebb_peer_cg* peers,
+                            int32_t* group_out);
+/* `iters` single-reduction iterations of every rank of the group in one
+ * cooperative launch (the first call after ebb_cg_init adds the z_0 halo,
+ * the r.z sum and the w_0 = A z_0 prologue).  Every rank of the job must
+ * call it with the same iters, in the same order.  Stream-ordered,
+ * graph-capturable; ebb_cg.tol is honoured (the same stop on every rank).
+ * */
+ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_stream s);
 
 typedef struct {
     ebb_field f, mass, mask;  /* mask: verts U8 (1 = free) or EBB_NONE        */

@@ -87,6 +87,19 @@ class PartitionInfo(C.Structure):
                 ("n_lverts", C.c_uint64), ("n_owned", C.c_uint64)]
 
 
+MAX_RANKS = 16                 # EBB_MAX_RANKS
+PEER_MBOX_WORDS = 160          # EBB_PEER_MBOX_WORDS
+
+
+class PeerCG(C.Structure):
+    """ebb_peer_cg: one rank of the fused multi-GPU PCG (include/ebb.h)."""
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("n_owned", C.c_uint64), ("send_off", u32),
+                ("send_dst", u32), ("mbox", u32),
+                ("peer_u", C.c_uint64 * MAX_RANKS), ("peer_u2", C.c_uint64 * MAX_RANKS),
+                ("peer_x", C.c_uint64 * MAX_RANKS), ("peer_z", C.c_uint64 * MAX_RANKS),
+                ("peer_mbox", C.c_uint64 * MAX_RANKS)]
+
+
 class ExplicitDesc(C.Structure):
     _fields_ = [("f", u32), ("mass", u32), ("mask", u32), ("u", u32), ("vel", u32), ("h", C.c_double),
                 ("g", C.c_double * 3)]
@@ -172,6 +185,13 @@ SIGS = {
     "ebb_rows_gather": (S, [ctx_t, u32, u32, u32, stream_t]),
     "ebb_rows_scatter": (S, [ctx_t, u32, u32, u32, stream_t]),
     "ebb_rows_scatter_add": (S, [ctx_t, u32, u32, u32, stream_t]),
+    "ebb_peer_send_csr": (S, [ctx_t, C.c_uint64, C.c_int32, C.POINTER(C.c_int32), C.POINTER(u32), C.POINTER(u32),
+                              C.POINTER(C.c_uint64), C.c_char_p, C.POINTER(u32), C.POINTER(u32)]),
+    "ebb_ipc_handle": (S, [ctx_t, u32, C.c_char_p]),
+    "ebb_ipc_open": (S, [ctx_t, C.c_char_p, C.POINTER(C.c_uint64)]),
+    "ebb_ipc_close": (S, [ctx_t, C.c_uint64]),
+    "ebb_cg_peer_bind": (S, [ctx_t, C.c_int32, C.POINTER(CG), C.POINTER(PeerCG), C.POINTER(C.c_int32)]),
+    "ebb_cg_peer_step": (S, [ctx_t, C.c_int32, C.c_int32, stream_t]),
 }
 
 _lib = None

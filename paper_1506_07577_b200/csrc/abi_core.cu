@@ -436,6 +436,7 @@ ebb_status ebb_ctx_free(ebb_ctx ctx) {
     for (auto& e : c->ev_pool) cudaEventDestroy(e);
     release_plans(c);
     comm_release(c);
+    peer_release(c);
     for (auto& G : c->graphs)
         if (G.exec) cudaGraphExecDestroy(G.exec);
     cudaFree(c->d_err);

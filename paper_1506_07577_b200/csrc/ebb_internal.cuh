@@ -168,6 +168,7 @@ struct Ctx : ebb_ctx_s {
     std::vector<ColorPlan*> colorplans; // (same)
     std::vector<UpperCSR*> uppers;      // (same)
     void* comm = nullptr;               // ncclComm_t (comm.cu)
+    std::vector<void*> peer_groups;     // launch groups of ebb_cg_peer_bind (solver.cu)
     int comm_size = 1, comm_rank = 0;
     struct GraphRec {
         cudaGraphExec_t exec = nullptr;
@@ -230,6 +231,7 @@ ebb_status new_internal_field(Ctx* c, ebb_rel rel, const std::string& name, ebb_
                               uint32_t cols, ebb_layout layout, ebb_field* out);
 void release_plans(Ctx* c);
 void comm_release(Ctx* c);
+void peer_release(Ctx* c);   // solver.cu: frees the ebb_cg_peer_bind groups
 // seg_map.cu: the SEGMENTED element map (builds its plan on first use)
 ebb_status seg_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
                           const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
@@ -323,6 +325,6 @@ inline unsigned grid_for(uint64_t n, unsigned block) {
 }
 
 // error word slots
-enum { ERR_INVERTED = 0, ERR_NOT_SPD = 1, ERR_BOUNDS = 2 };
+enum { ERR_INVERTED = 0, ERR_NOT_SPD = 1, ERR_BOUNDS = 2, ERR_PEER = 3 };
 
 }  // namespace ebb

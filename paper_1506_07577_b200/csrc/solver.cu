@@ -1330,6 +1330,432 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
 }
 
 // ---------------------------------------------------------------------------
+// Fused multi-GPU single-reduction PCG over peer memory (ebb_cg_peer_step;
+// SURVEY §8(e); include/ebb.h).  One launch runs every iteration of every
+// rank whose system lives on this device: a real multi-GPU job launches it
+// once per process (one rank), ranks emulated on one device share one
+// cooperative launch, CTAs [lr*G, (lr+1)*G) working for local rank lr.  The
+// per-phase work is k_cg1_persistent's on the rank's OWNED rows (ghost rows
+// are never solved), plus:
+//   * the owner of a row that peers hold as a ghost stores its new u (the
+//     next gathered operand) and x straight into the peers' buffers as it
+//     finishes the row (send CSR: per owned vertex, (peer, peer row));
+//   * the phase's rank-local (w.z, r.z) go through mailboxes: after the
+//     rank's grid barrier (every CTA fenced at system scope, so its peer
+//     stores are visible first), block 0 writes them into every peer's
+//     mailbox slot [epoch & 1][rank] and releases the slot's sequence word
+//     (epoch + 1); every CTA of every rank acquires the P-1 sequence words of
+//     its own mailbox and sums the P values in rank order -- the same sums,
+//     bitwise, on every rank, so alpha, beta and the tolerance stop agree.
+// Safety of the buffers without further barriers: a rank writes a peer's
+// ghost rows of u(par') only in the phase after the one in which that peer
+// last gathered u(par'), and it can be there only after the peer published
+// that phase's sums, i.e. after every CTA of the peer finished the phase; a
+// mailbox slot is rewritten two exchanges later, which needs this rank's
+// next publication, made after all its CTAs read the slot.  The first
+// launch after ebb_cg_init exchanges r.z once (everyone has initialised,
+// so nobody's ebb_cg_init can zero a ghost row after a peer filled it),
+// then pushes z_0 and exchanges again before the w_0 = A z_0 prologue.
+constexpr int kPeerMax = EBB_MAX_RANKS;
+constexpr int kMbEpoch = 2 * kPeerMax * 4;   // mailbox word holding the rank's exchange count
+static_assert(kMbEpoch < EBB_PEER_MBOX_WORDS, "mailbox layout");
+struct PeerRankArgs {
+    uint64_t nv, ne;                   // owned rows (solved), edge rows of the local relation
+    const uint32_t* index;
+    const uint32_t* head;
+    const void* A;
+    const void* dinv;
+    void *x, *r, *z0, *p, *sv, *yv, *wv, *ub0, *ub1;
+    const uint8_t* mask;
+    double* part;                      // 4 x kCg1PartStride: (g, d) x phase parity
+    unsigned int* bar;                 // rank grid barrier: count, generation
+    double* scal;
+    double* rho_user;
+    const uint32_t* send_off;
+    const uint2* send_dst;
+    unsigned long long* mbox;          // own mailbox
+    void* peer_ub0[kPeerMax];
+    void* peer_ub1[kPeerMax];
+    void* peer_x[kPeerMax];
+    void* peer_z0[kPeerMax];
+    unsigned long long* peer_mbox[kPeerMax];
+    int rank, nranks;
+    uint32_t cap, pad;
+};
+
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// grid barrier over the G CTAs of one rank; each CTA fences at system scope
+// before it arrives (its stores to peer memory precede the rank's publication)
+__device__ __forceinline__ void rank_barrier(unsigned int* bar, unsigned int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int* count = bar;
+        unsigned int* gen = bar + 1;
+        const unsigned int g = *reinterpret_cast<volatile unsigned int*>(gen);
+        __threadfence_system();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *reinterpret_cast<volatile unsigned int*>(count) = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned int*>(gen) == g) __nanosleep(EBB_BAR_SLEEP_NS);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+#ifndef EBB_PEER_TIMEOUT_NS
+#define EBB_PEER_TIMEOUT_NS 20000000000ull   // 20 s: a peer that never arrives
+#endif
+// exchange number `epoch` of (d, g) between the ranks; returns the sums over
+// ranks in rank order (every CTA, every rank: the same values).  Call after a
+// rank_barrier that follows this CTA's last read of the previous exchange.
+__device__ __forceinline__ void peer_exchange(const PeerRankArgs& a, unsigned bid, uint64_t epoch, double d,
+                                              double g, double* sm2, unsigned long long* err, double& dsum,
+                                              double& gsum) {
+    const unsigned slot = (unsigned)(epoch & 1u);
+    const unsigned long long seq = epoch + 1;
+    const unsigned q = threadIdx.x;
+    if (bid == 0 && q < (unsigned)a.nranks && q != (unsigned)a.rank) {
+        unsigned long long* mb = a.peer_mbox[q] + (slot * kPeerMax + a.rank) * 4;
+        __threadfence_system();
+        st_relaxed_sys(mb, (unsigned long long)__double_as_longlong(d));
+        st_relaxed_sys(mb + 1, (unsigned long long)__double_as_longlong(g));
+        st_release_sys(mb + 2, seq);
+    }
+    if (q < (unsigned)a.nranks && q != (unsigned)a.rank) {
+        const unsigned long long* sw = a.mbox + (slot * kPeerMax + q) * 4 + 2;
+        // after one abandoned wait every later one is skipped (the results are
+        // invalid anyway; the launch must still end)
+        if (ld_acquire_sys(sw) != seq && *reinterpret_cast<volatile unsigned long long*>(&err[ERR_PEER]) == 0) {
+            const unsigned long long t0 = global_ns();
+            while (ld_acquire_sys(sw) != seq) {
+                __nanosleep(32);
+                if (global_ns() - t0 > EBB_PEER_TIMEOUT_NS) {
+                    atomicAdd(&err[ERR_PEER], 1ull);
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sd = 0.0, sg = 0.0;
+        for (int r = 0; r < a.nranks; ++r) {
+            if (r == a.rank) {
+                sd += d;
+                sg += g;
+            } else {
+                const unsigned long long* mb = a.mbox + (slot * kPeerMax + r) * 4;
+                sd += __longlong_as_double((long long)ld_relaxed_sys(mb));
+                sg += __longlong_as_double((long long)ld_relaxed_sys(mb + 1));
+            }
+        }
+        sm2[0] = sd;
+        sm2[1] = sg;
+    }
+    __syncthreads();
+    dsum = sm2[0];
+    gsum = sm2[1];
+}
+
+// (min 3 CTAs per SM: 72 registers, the single-GPU kernel's occupancy; unbounded
+// it takes 132 and one CTA per SM)
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
+    k_cg1_peer(const PeerRankArgs* __restrict__ ranks, unsigned G, unsigned long long* __restrict__ err, int iters,
+               double tol2) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    __shared__ __align__(8) uint64_t full_bar[CG1_NS], empty_bar[CG1_NS];
+    __shared__ double sm_tot, sm2[2];
+    const unsigned lr = blockIdx.x / G, bid = blockIdx.x - lr * G;
+    const PeerRankArgs& a = ranks[lr];
+    constexpr uint32_t AE = 16 / sizeof(R);
+    const uint64_t nv = a.nv, ne = a.ne;
+    const uint32_t cap = a.cap;
+    const uint32_t* __restrict__ index = a.index;
+    const uint32_t* __restrict__ head = a.head;
+    const R* __restrict__ A = (const R*)a.A;
+    const R* __restrict__ dinv = (const R*)a.dinv;
+    R* __restrict__ x = (R*)a.x;
+    R* __restrict__ r = (R*)a.r;
+    const R* __restrict__ z0 = (const R*)a.z0;
+    R* __restrict__ p = (R*)a.p;
+    R* __restrict__ sv = (R*)a.sv;
+    R* __restrict__ yv = (R*)a.yv;
+    R* __restrict__ wv = (R*)a.wv;
+    R* ub0 = (R*)a.ub0;
+    R* ub1 = (R*)a.ub1;
+    const uint8_t* __restrict__ mask = a.mask;
+    double* __restrict__ scal = a.scal;
+    const uint32_t* __restrict__ send_off = a.send_off;
+    const uint2* __restrict__ send_dst = a.send_dst;
+    const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const uint64_t nchunks = (nv + TMA_VCH - 1) / TMA_VCH;
+    const uint64_t my_chunks = nchunks > bid ? (nchunks - bid + G - 1) / G : 0;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < CG1_NS; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], PCG_WPG);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    uint64_t epoch = a.mbox[kMbEpoch];
+    double gam = scal[S_RHO];                 // g_i = r_i . z_i (rank-local after ebb_cg_init)
+    double alpha = scal[S_ALPHA];
+    double beta = scal[S_PQ];
+    int first = scal[S_FIRST] != 0.0;
+    int par = scal[S_PAR] != 0.0;
+    double rz0 = scal[S_RZ0];
+    if (scal[S_DONE] != 0.0) iters = 0;
+    int done_it = 0, done_ph = 0;
+    bool conv = false;
+    if (first && iters > 0) {
+        // 1) every rank has run ebb_cg_init; the global r_0.z_0
+        double g0, unused;
+        peer_exchange(a, bid, epoch++, gam, 0.0, sm2, err, g0, unused);
+        gam = g0;
+        rz0 = g0;
+        // 2) z_0 halo: owners store their rows into the peers' ghost rows
+        for (uint64_t v = (uint64_t)bid * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)G * blockDim.x) {
+            const uint32_t s0 = send_off[v], s1 = send_off[v + 1];
+            if (s0 == s1) continue;
+            const auto zv = ld4(z0, v);
+            for (uint32_t k = s0; k < s1; ++k) {
+                const uint2 d = send_dst[k];
+                st4((R*)a.peer_z0[d.x], d.y, zv);
+            }
+        }
+        rank_barrier(a.bar, G);
+        peer_exchange(a, bid, epoch++, 0.0, 0.0, sm2, err, g0, unused);
+    }
+    uint64_t issued = 0;
+    auto issue = [&](uint64_t ch, uint64_t seq) {
+        const int s = seq % CG1_NS;
+        const uint64_t v0 = ch * TMA_VCH;
+        const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+        const uint64_t e0 = index[v0], e1 = index[v1];
+        if (seq >= CG1_NS) mbar_wait(&empty_bar[s], (uint32_t)(((seq / CG1_NS) + 1) & 1u));
+        unsigned char* base = tma_smem + s * stage_bytes;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            tot += (uint32_t)((a1 - a0) * sizeof(R));
+        }
+        const uint64_t h0 = e0 & ~3ull, h1 = (e1 + 3) & ~3ull;
+        tot += (uint32_t)((h1 - h0) * 4);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full_bar[s], tot);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            bulk_g2s_evict_first(base + (size_t)c * cap * sizeof(R), A + a0, (uint32_t)((a1 - a0) * sizeof(R)),
+                                 &full_bar[s]);
+        }
+        bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
+    };
+    const int nphase = iters + (first && iters > 0 ? 1 : 0);
+    if (warp == TMA_CONSUMERS && lane == 0 && nphase > 0)
+        for (uint64_t j = 0; j < my_chunks && j < CG1_NS; ++j) issue(bid + j * G, issued++);
+    for (int ph = 0; ph < nphase; ++ph) {
+        const bool pro = first != 0;
+        const R aa = (R)alpha, b = (R)beta;
+        const R* __restrict__ op = pro ? z0 : (par ? ub1 : ub0);
+        const bool un1 = pro ? par != 0 : par == 0;          // u_{i+1} goes to buffer 1 (u2)
+        R* __restrict__ un = un1 ? ub1 : ub0;
+        double pg = 0.0, pd = 0.0;
+        if (warp == TMA_CONSUMERS) {
+            if (lane == 0) {
+                for (uint64_t j = CG1_NS; j < my_chunks; ++j) issue(bid + j * G, issued++);
+                if (ph + 1 < nphase)
+                    for (uint64_t j = 0; j < my_chunks && j < CG1_NS; ++j) issue(bid + j * G, issued++);
+            }
+        } else {
+            const unsigned grp = warp / PCG_WPG, wig = warp % PCG_WPG;
+            const unsigned sub = lane & 7;
+            const uint64_t seq0 = (uint64_t)ph * my_chunks;
+            for (uint64_t j = grp; j < my_chunks; j += PCG_GROUPS) {
+                const uint64_t seq = seq0 + j;
+                const uint64_t ch = bid + j * G;
+                const int s = seq % CG1_NS;
+                const uint64_t v0 = ch * TMA_VCH;
+                const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+                const uint64_t v = v0 + 4 * wig + (lane >> 3);
+                const bool valid = v < v1;
+                const uint32_t e0 = index[v0];
+                const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
+                mbar_wait(&full_bar[s], (uint32_t)((seq / CG1_NS) & 1u));
+                const unsigned char* base = tma_smem + s * stage_bytes;
+                const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
+                uint32_t off[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) off[c] = (uint32_t)((c * ne + e0) & (AE - 1));
+                R a0 = 0, a1 = 0, a2 = 0;
+                for (uint32_t rb = r0 + sub; rb < r1; rb += 16) {
+                    const uint32_t rr1 = rb + 8;
+                    const bool two = rr1 < r1;
+                    const uint32_t h0 = hs[rb], h1 = two ? hs[rr1] : h0;
+                    const auto o0 = ld4cg(op, h0);
+                    const auto o1 = ld4cg(op, h1);
+                    R av[9], bv[9];
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) {
+                        const R* pl = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R)) + off[c];
+                        av[c] = pl[rb];
+                        bv[c] = two ? pl[rr1] : R(0);
+                    }
+                    a0 += av[0] * o0.x + av[1] * o0.y + av[2] * o0.z + (bv[0] * o1.x + bv[1] * o1.y + bv[2] * o1.z);
+                    a1 += av[3] * o0.x + av[4] * o0.y + av[5] * o0.z + (bv[3] * o1.x + bv[4] * o1.y + bv[5] * o1.z);
+                    a2 += av[6] * o0.x + av[7] * o0.y + av[8] * o0.z + (bv[6] * o1.x + bv[7] * o1.y + bv[8] * o1.z);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o, 8);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o, 8);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, o, 8);
+                }
+                if (sub == 0 && valid) {
+                    if (mask && !mask[v]) a0 = a1 = a2 = 0;
+                    const auto dv = ld4(dinv, v);
+                    const uint32_t s0 = send_off[v], s1 = send_off[v + 1];
+                    typename V4<R>::T t;
+                    t.w = 0;
+                    if (pro) {
+                        const auto zv = ld4(z0, v);
+                        t.x = a0; t.y = a1; t.z = a2;
+                        st4(wv, v, t);
+                        t.x = a0 * dv.x; t.y = a1 * dv.y; t.z = a2 * dv.z;
+                        st4(un, v, t);
+                        for (uint32_t k = s0; k < s1; ++k) {
+                            const uint2 d = send_dst[k];
+                            st4((R*)(un1 ? a.peer_ub1[d.x] : a.peer_ub0[d.x]), d.y, t);
+                        }
+                        pd += (double)a0 * zv.x + (double)a1 * zv.y + (double)a2 * zv.z;
+                    } else {
+                        auto rv = ld4(r, v);
+                        auto wi = ld4(wv, v);
+                        typename V4<R>::T si = wi, yi, pi;
+                        yi.x = a0; yi.y = a1; yi.z = a2; yi.w = 0;
+                        pi.x = rv.x * dv.x; pi.y = rv.y * dv.y; pi.z = rv.z * dv.z; pi.w = 0;
+                        if (b != R(0)) {
+                            const auto so = ld4(sv, v), yo = ld4(yv, v), po = ld4(p, v);
+                            si.x += b * so.x; si.y += b * so.y; si.z += b * so.z;
+                            yi.x += b * yo.x; yi.y += b * yo.y; yi.z += b * yo.z;
+                            pi.x += b * po.x; pi.y += b * po.y; pi.z += b * po.z;
+                        }
+                        si.w = 0;
+                        st4(sv, v, si);
+                        st4(yv, v, yi);
+                        st4(p, v, pi);
+                        const R x0 = x[3 * v] + aa * pi.x, x1 = x[3 * v + 1] + aa * pi.y, x2 = x[3 * v + 2] + aa * pi.z;
+                        x[3 * v] = x0;
+                        x[3 * v + 1] = x1;
+                        x[3 * v + 2] = x2;
+                        rv.x -= aa * si.x; rv.y -= aa * si.y; rv.z -= aa * si.z; rv.w = 0;
+                        wi.x -= aa * yi.x; wi.y -= aa * yi.y; wi.z -= aa * yi.z; wi.w = 0;
+                        st4(r, v, rv);
+                        st4(wv, v, wi);
+                        t.x = wi.x * dv.x; t.y = wi.y * dv.y; t.z = wi.z * dv.z;
+                        st4(un, v, t);
+                        for (uint32_t k = s0; k < s1; ++k) {
+                            const uint2 d = send_dst[k];
+                            st4((R*)(un1 ? a.peer_ub1[d.x] : a.peer_ub0[d.x]), d.y, t);
+                            R* px = (R*)a.peer_x[d.x] + 3 * (uint64_t)d.y;
+                            px[0] = x0;
+                            px[1] = x1;
+                            px[2] = x2;
+                        }
+                        const R zx = rv.x * dv.x, zy = rv.y * dv.y, zz = rv.z * dv.z;
+                        pg += (double)rv.x * zx + (double)rv.y * zy + (double)rv.z * zz;
+                        pd += (double)wi.x * zx + (double)wi.y * zy + (double)wi.z * zz;
+                    }
+                }
+            }
+        }
+        pg = block_reduce<ROP_SUM>(pg);
+        pd = block_reduce<ROP_SUM>(pd);
+        double* const pgb = a.part + (ph & 1) * 2 * kCg1PartStride;
+        double* const pdb = pgb + kCg1PartStride;
+        if (threadIdx.x == 0) {
+            pgb[bid] = pg;
+            pdb[bid] = pd;
+        }
+        rank_barrier(a.bar, G);
+        const double dl = grid_sum_partials(pdb, G, &sm_tot);
+        const double gl = pro ? 0.0 : grid_sum_partials(pgb, G, &sm_tot);
+        double dsum, gnew;
+        peer_exchange(a, bid, epoch++, dl, gl, sm2, err, dsum, gnew);
+        if (pro) {
+            if (lr == 0 && bid == 0 && threadIdx.x == 0 && dsum < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+            alpha = dsum != 0.0 ? gam / dsum : 0.0;
+            beta = 0.0;
+            first = 0;
+        } else {
+            const double bn = gam != 0.0 ? gnew / gam : 0.0;
+            const double den = dsum - (alpha != 0.0 ? bn * gnew / alpha : 0.0);
+            if (lr == 0 && bid == 0 && threadIdx.x == 0 && den < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+            alpha = den != 0.0 ? gnew / den : 0.0;
+            beta = bn;
+            gam = gnew;
+            par ^= 1;
+        }
+        ++done_ph;
+        if (!pro) {
+            ++done_it;
+            if (tol2 > 0.0 && gam <= tol2 * rz0) {   // global sums: the same exit on every rank
+                conv = true;
+                break;
+            }
+        }
+    }
+    if (warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t sq = (uint64_t)done_ph * my_chunks; sq < issued; ++sq)
+            mbar_wait(&full_bar[sq % CG1_NS], (uint32_t)((sq / CG1_NS) & 1u));
+    if (bid == 0 && threadIdx.x == 0) {
+        scal[S_ITERS] += (double)done_it;
+        if (conv) scal[S_DONE] = 1.0;
+        scal[S_RHO] = gam;
+        scal[S_RZ] = gam;
+        scal[S_RZ0] = rz0;
+        scal[S_ALPHA] = alpha;
+        scal[S_PQ] = beta;
+        scal[S_FIRST] = first ? 1.0 : 0.0;
+        scal[S_PAR] = par ? 1.0 : 0.0;
+        *a.rho_user = gam;
+        a.mbox[kMbEpoch] = epoch;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // PCG kernels on padded vec4 work vectors (one thread per vertex)
 // init: dinv = 1/diag(A) on free DOFs (Jacobi), x = 0, r = b*m,
 //       z = r*dinv, p = z, local r.z -> scal[S_RZ]; scal[S_FIRST] = 1
@@ -2006,7 +2432,47 @@ ebb_status cg_validate(Ctx* c, const ebb_cg* cg, EdgeGraph* G, ebb_dtype* dt) {
     return EBB_OK;
 }
 
+
+// launch group of ebb_cg_peer_bind: the per-rank records on the device and
+// each rank's grid-barrier words and reduction partials
+struct PeerGroup {
+    int nlocal = 0;
+    unsigned G = 0;                    // CTAs per rank
+    size_t smem = 0;
+    ebb_dtype dt = EBB_F64;
+    double tol2 = 0.0;
+    PeerRankArgs* d_args = nullptr;
+    double* d_part = nullptr;
+    unsigned int* d_bar = nullptr;
+};
+
+template <typename R>
+ebb_status peer_occupancy(Ctx* c, size_t smem, int* nb) {
+    static thread_local size_t configured_dev[kMaxDevices] = {};
+    size_t& configured = configured_dev[c->device % kMaxDevices];
+    if (smem > configured) {
+        EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_peer<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k_cg1_peer<R>, 32 * (TMA_CONSUMERS + 1), smem));
+    return EBB_OK;
+}
+
 }  // namespace
+
+namespace ebb {
+void peer_release(Ctx* c) {
+    for (void* g : c->peer_groups) {
+        PeerGroup* P = (PeerGroup*)g;
+        if (!P) continue;
+        cudaFree(P->d_args);
+        cudaFree(P->d_part);
+        cudaFree(P->d_bar);
+        delete P;
+    }
+    c->peer_groups.clear();
+}
+}  // namespace ebb
 
 extern "C" {
 
@@ -2348,6 +2814,145 @@ ebb_status ebb_implicit_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u,
 
 ebb_status ebb_newton_update(ebb_ctx ctx, ebb_field dv, double h, ebb_field u, ebb_field vel, ebb_stream stream) {
     return implicit_update_impl(ctx, dv, h, u, vel, stream, true);
+}
+
+ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, const ebb_peer_cg* peers,
+                            int32_t* group_out) {
+    Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
+    if (!c || !cgs || !peers || !group_out) return fail(c, EBB_E_ARG, "null argument");
+    if (nlocal < 1 || nlocal > EBB_MAX_RANKS) return fail(c, EBB_E_ARG, "peer_bind: nlocal must be 1..%d", EBB_MAX_RANKS);
+    std::vector<PeerRankArgs> h(nlocal);
+    ebb_dtype dt0 = EBB_F64;
+    size_t stage_max = 0;
+    for (int i = 0; i < nlocal; ++i) {
+        const ebb_cg* cg = &cgs[i];
+        const ebb_peer_cg* pc = &peers[i];
+        EdgeGraph Gr;
+        ebb_dtype dt;
+        EBB_TRY(cg_validate(c, cg, &Gr, &dt));
+        if (i == 0) dt0 = dt;
+        if (dt != dt0) return fail(c, EBB_E_TYPE, "peer_bind: every rank of a group must have the same dtype");
+        for (ebb_field f : {cg->s, cg->y, cg->w, cg->u, cg->u2, cg->dinv, cg->r, cg->z, cg->p, cg->scal, cg->rho})
+            if (!get_field(c, f))
+                return fail(c, EBB_E_STATE, "peer_bind: rank %d: call ebb_cg_init with EBB_CG_SINGLE_REDUCTION first "
+                            "(its work vectors are missing)", i);
+        if (cg->tol != cgs[0].tol) return fail(c, EBB_E_ARG, "peer_bind: every rank needs the same tol");
+        if (pc->nranks < 1 || pc->nranks > EBB_MAX_RANKS || pc->rank < 0 || pc->rank >= pc->nranks ||
+            pc->nranks != peers[0].nranks)
+            return fail(c, EBB_E_ARG, "peer_bind: rank %d: bad rank / nranks (%d / %d)", i, pc->rank, pc->nranks);
+        for (int j = 0; j < i; ++j)
+            if (peers[j].rank == pc->rank) return fail(c, EBB_E_ARG, "peer_bind: rank %d bound twice", pc->rank);
+        if (pc->n_owned > Gr.nv) return fail(c, EBB_E_SIZE, "peer_bind: n_owned exceeds the local vertex count");
+        Field* SO = get_field(c, pc->send_off);
+        Field* SD = get_field(c, pc->send_dst);
+        Field* MB = get_field(c, pc->mbox);
+        if (!SO || SO->dtype != EBB_U32 || SO->comps() != 1 || c->rels[SO->rel].size != pc->n_owned + 1)
+            return fail(c, EBB_E_TYPE, "peer_bind: send_off must be a U32 field of n_owned + 1 rows");
+        if (!SD || SD->dtype != EBB_U32 || SD->comps() != 2)
+            return fail(c, EBB_E_TYPE, "peer_bind: send_dst must be a U32 2x1 field");
+        if (!MB || MB->dtype != EBB_F64 || MB->comps() != 1 || c->rels[MB->rel].size < EBB_PEER_MBOX_WORDS)
+            return fail(c, EBB_E_TYPE, "peer_bind: mbox must be an F64 field of >= %d rows", EBB_PEER_MBOX_WORDS);
+        for (int q = 0; q < pc->nranks; ++q)
+            if (q != pc->rank && (!pc->peer_u[q] || !pc->peer_u2[q] || !pc->peer_x[q] || !pc->peer_z[q] ||
+                                  !pc->peer_mbox[q]))
+                return fail(c, EBB_E_ARG, "peer_bind: rank %d: missing buffer address of peer %d", pc->rank, q);
+        const uint8_t* mask;
+        EBB_TRY(check_mask(c, cg->mask, Gr.verts, &mask));
+        const uint32_t cap = dt == EBB_F64 ? tma_cap<double>(Gr.max_chunk16) : tma_cap<float>(Gr.max_chunk16);
+        const size_t es = dt == EBB_F64 ? 8 : 4;
+        const size_t stage = ((size_t)9 * cap * es + (size_t)cap * 4 + 127) & ~(size_t)127;
+        if (stage > stage_max) stage_max = stage;
+        auto F = [&](ebb_field f) { return c->fields[f].ptr; };
+        PeerRankArgs& a = h[i];
+        memset(&a, 0, sizeof(a));
+        a.nv = pc->n_owned;
+        a.ne = Gr.ne;
+        a.index = Gr.index;
+        a.head = Gr.head;
+        a.A = F(cg->A);
+        a.dinv = F(cg->dinv);
+        a.x = F(cg->x);
+        a.r = F(cg->r);
+        a.z0 = F(cg->z);
+        a.p = F(cg->p);
+        a.sv = F(cg->s);
+        a.yv = F(cg->y);
+        a.wv = F(cg->w);
+        a.ub0 = F(cg->u);
+        a.ub1 = F(cg->u2);
+        a.mask = mask;
+        a.scal = (double*)F(cg->scal);
+        a.rho_user = (double*)F(cg->rho);
+        a.send_off = (const uint32_t*)SO->ptr;
+        a.send_dst = (const uint2*)SD->ptr;
+        a.mbox = (unsigned long long*)MB->ptr;
+        for (int q = 0; q < pc->nranks; ++q) {
+            a.peer_ub0[q] = (void*)(uintptr_t)pc->peer_u[q];
+            a.peer_ub1[q] = (void*)(uintptr_t)pc->peer_u2[q];
+            a.peer_x[q] = (void*)(uintptr_t)pc->peer_x[q];
+            a.peer_z0[q] = (void*)(uintptr_t)pc->peer_z[q];
+            a.peer_mbox[q] = (unsigned long long*)(uintptr_t)pc->peer_mbox[q];
+        }
+        a.rank = pc->rank;
+        a.nranks = pc->nranks;
+        a.cap = cap;
+    }
+    const size_t smem = stage_max * CG1_NS;
+    if (smem > kTmaSmemMax) return fail(c, EBB_E_SIZE, "peer_bind: TMA ring of %zu bytes does not fit", smem);
+    int nb = 0;
+    if (dt0 == EBB_F64) EBB_TRY(peer_occupancy<double>(c, smem, &nb));
+    else EBB_TRY(peer_occupancy<float>(c, smem, &nb));
+    unsigned G = (unsigned)((uint64_t)nb * c->num_sms / (uint64_t)nlocal);
+    if (G > kCg1PartStride) G = kCg1PartStride;
+    if (G < 1) return fail(c, EBB_E_SIZE, "peer_bind: %d ranks cannot all be resident on one device", nlocal);
+    PeerGroup* P = new PeerGroup();
+    P->nlocal = nlocal;
+    P->G = G;
+    P->smem = smem;
+    P->dt = dt0;
+    P->tol2 = cg_tol2(&cgs[0]);
+    c->peer_groups.push_back(P);
+    EBB_CUDA(c, cudaMalloc(&P->d_args, sizeof(PeerRankArgs) * nlocal));
+    EBB_CUDA(c, cudaMalloc(&P->d_part, sizeof(double) * 4 * kCg1PartStride * nlocal));
+    EBB_CUDA(c, cudaMalloc(&P->d_bar, sizeof(unsigned int) * 2 * nlocal));
+    EBB_CUDA(c, cudaMemset(P->d_bar, 0, sizeof(unsigned int) * 2 * nlocal));
+    for (int i = 0; i < nlocal; ++i) {
+        h[i].part = P->d_part + (size_t)i * 4 * kCg1PartStride;
+        h[i].bar = P->d_bar + 2 * i;
+    }
+    EBB_CUDA(c, cudaMemcpy(P->d_args, h.data(), sizeof(PeerRankArgs) * nlocal, cudaMemcpyHostToDevice));
+    *group_out = (int32_t)(c->peer_groups.size() - 1);
+    return EBB_OK;
+}
+
+ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_stream stream) {
+    Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
+    if (!c) return EBB_E_ARG;
+    if (group < 0 || (size_t)group >= c->peer_groups.size() || !c->peer_groups[group])
+        return fail(c, EBB_E_ARG, "peer_step: bad group %d", group);
+    if (iters < 0) return fail(c, EBB_E_ARG, "negative iteration count");
+    PeerGroup* P = (PeerGroup*)c->peer_groups[group];
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P->G * (unsigned)P->nlocal);
+    cfg.blockDim = dim3(32 * (TMA_CONSUMERS + 1));
+    cfg.dynamicSmemBytes = P->smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // every CTA of every local rank resident at once
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KernelTimer kt(c, EBB_K_CG_SOLVE, s);
+    if (P->dt == EBB_F64)
+        EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer<double>, (const PeerRankArgs*)P->d_args, P->G, c->d_err,
+                                       (int)iters, P->tol2));
+    else
+        EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer<float>, (const PeerRankArgs*)P->d_args, P->G, c->d_err,
+                                       (int)iters, P->tol2));
+    return EBB_OK;
 }
 
 }  // extern "C"

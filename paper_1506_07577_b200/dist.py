@@ -180,7 +180,7 @@ def map_step(ranks, transport, model="stvk"):
 
 
 def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0),
-                  variant="saad"):
+                  variant="saad", peer=None):
     """One distributed implicit step (O9 + O10) over `ranks` (the local ones).
 
     variant="saad": per iteration DIR, MATVEC, [sum p.q], UPDATE, [sum r.z,
@@ -195,8 +195,26 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
     previous recurrences), so only that buffer is exchanged.  Ghost rows are
     masked, so the kernel leaves ghost x at 0: x (= dv) is exchanged from the
     owners once, before the state update, so ghost u and v stay consistent
-    for the next step's map on ghost tets."""
+    for the next step's map on ghost tets.
+
+    variant="peer": the same recurrences in ONE fused kernel for all
+    iterations (ebb_cg_peer_step, bound by ``PeerPCG``): the owners store u,
+    x (and z_0) into their peers' ghost rows and the two scalars go through
+    peer mailboxes inside the kernel -- no host loop, no NCCL call, no
+    transport (``transport`` is used only by the reverse-add map)."""
     _map_assemble(ranks, transport, model, h, alpha, beta, g)
+    if variant == "peer":
+        # the fused multi-GPU PCG: one kernel for every iteration (and the
+        # z_0 / u / x halos and the scalar sums inside it); `peer` is the
+        # PeerPCG binding of these ranks
+        if peer is None:
+            raise ValueError("variant='peer' needs the PeerPCG binding of the ranks")
+        for R in ranks:
+            R.cg_init(single=True)
+        peer.step(iters)
+        for R in ranks:
+            R.finish(h)
+        return
     if variant == "single":
         for R in ranks:
             R.cg_init(single=True)
@@ -352,6 +370,8 @@ class GpuRank:
                             "u2": self._field(self.fem.cg.u2, 4), "x": self.fem.dv, "disp": self.fem.u}
         self.scal = self._field(self.fem.cg.scal, 1, count=12, dt="f64").tensor()
         self._lists = {}
+        self.n_owned = int(n_owned)
+        self.part_send, self.part_recv = part["send"], part["recv"]
         self._make_lists("fwd", self.fem.verts.name + ".halo", part["send"], part["recv"], (3, 4))
         self.map_variant = map_variant
         if map_variant == "reverse":
@@ -486,6 +506,61 @@ class GpuRank:
         self.ctx.check(self.ctx.L.ebb_implicit_update(self.ctx.h, self.fem.dv.h, float(h), self.fem.u.h,
                                                       self.fem.vel.h, _stream(self.stream)))
 
+    # -- fused PCG over peer memory (PeerPCG)
+    def peer_export(self, ipc):
+        """What peers need of this rank: its recv rows per peer (numpy), its
+        local vertex count, send-list lengths, and its ghost-row targets
+        (cg.u, cg.u2, cg.x = dv, cg.z, the mailbox) as device addresses
+        (ranks on one device) or 64-byte IPC handles (one process per GPU)."""
+        import ctypes as C
+
+        from . import _abi as A
+        if not hasattr(self, "mbox"):
+            rel = self.ctx.relation(f"{self.fem.verts.name}.mbox", A.PEER_MBOX_WORDS)
+            self.mbox = rel.field("mbox", "f64", init=np.zeros(A.PEER_MBOX_WORDS))
+        cg = self.fem.cg
+        handles = {"u": cg.u, "u2": cg.u2, "x": cg.x, "z": cg.z, "mbox": self.mbox.h}
+        buf = {}
+        for name, fh in handles.items():
+            if ipc:
+                hb = C.create_string_buffer(64)
+                self.ctx.check(self.ctx.L.ebb_ipc_handle(self.ctx.h, int(fh), hb))
+                buf[name] = hb.raw
+            else:
+                v = A.View()
+                self.ctx.check(self.ctx.L.ebb_field_view(self.ctx.h, int(fh), C.byref(v)))
+                buf[name] = int(v.data)
+        return dict(rank=self.rank, nv=int(self.fem.nv), send={q: int(len(r)) for q, r in self.part_send.items()},
+                    recv={q: np.asarray(r, np.int64) for q, r in self.part_recv.items()}, buf=buf)
+
+    def peer_send_csr(self, peers, remote, peer_nv):
+        """ebb_peer_send_csr over this rank's send lists (fields of the halo
+        lists) and the peers' rows of the same vertices."""
+        import ctypes as C
+
+        from . import _abi as A
+        n = len(peers)
+        self._peer_calls = getattr(self, "_peer_calls", 0) + 1
+        tag = f"{self.fem.verts.name}.peer{self._peer_calls}"
+        self._remote_rels = []
+        sf, rf = [], []
+        for q, rows in zip(peers, remote):
+            rel = self.ctx.relation(f"{tag}.remote{q}", max(len(rows), 1))
+            self._remote_rels.append(rel)
+            rf.append(rel.field("rows", "u32", init=np.asarray(rows, np.uint32)).h)
+            sf.append(self._lists["fwd"]["send"][q][0].h)
+        off, dst = C.c_uint32(), C.c_uint32()
+        self.ctx.check(self.ctx.L.ebb_peer_send_csr(
+            self.ctx.h, self.n_owned, n, (C.c_int32 * max(n, 1))(*peers), (A.u32 * max(n, 1))(*sf),
+            (A.u32 * max(n, 1))(*rf), (C.c_uint64 * max(n, 1))(*peer_nv), tag.encode(),
+            C.byref(off), C.byref(dst)))
+        from .ebb import Field
+        self.peer_off = Field(self.ctx, off.value, None, "off", "u32", (1, 1), A.AOS)
+        self.peer_off.count = self.n_owned + 1
+        self.peer_dst = Field(self.ctx, dst.value, None, "dst", "u32", (2, 1), A.AOS)
+        self.peer_dst.count = max(sum(len(r) for r in remote), 1)
+        return self.peer_off, self.peer_dst
+
     # -- transport hooks
     def scal_tensor(self):
         return self.scal
@@ -529,3 +604,101 @@ class GpuRank:
     def local_values(self, field):
         """Every local row (owned and ghost) with its input vertex id."""
         return self.verts_g, field.read()
+
+
+# ----------------------------------------------------------------------------- fused PCG over peer memory
+PEER_BUFFERS = ("u", "u2", "x", "z", "mbox")
+
+
+def peer_tables(infos, local_ranks, nranks):
+    """What each local rank needs of its peers for ebb_cg_peer_bind, from the
+    peers' exported infos (``GpuRank.peer_export``): per local rank r, the
+    sorted send peers q with r's remote rows on q (q's recv rows from r: the
+    same vertices in the same ascending-gid order, ebb_partition_local), q's
+    local vertex count, and q's buffer entries (addresses or IPC handles).
+    Pure host bookkeeping (no arithmetic of the method); checked on CPU."""
+    out = {}
+    for r in local_ranks:
+        me = infos[r]
+        peers = sorted(me["send"])
+        remote, peer_nv = [], []
+        for q in peers:
+            rows = np.asarray(infos[q]["recv"].get(r, np.zeros(0, np.int64)))
+            if rows.size != me["send"][q]:
+                raise ValueError(f"rank {r} sends {me['send'][q]} rows to {q}, which expects {rows.size}")
+            remote.append(rows)
+            peer_nv.append(int(infos[q]["nv"]))
+        bufs = {name: [infos[q]["buf"][name] if q != r else None for q in range(nranks)] for name in PEER_BUFFERS}
+        out[r] = dict(peers=peers, remote=remote, peer_nv=peer_nv, bufs=bufs)
+    return out
+
+
+class PeerPCG:
+    """The fused multi-GPU single-reduction PCG over peer memory
+    (``ebb_cg_peer_bind`` / ``ebb_cg_peer_step``).
+
+    ranks: the GpuRank objects of THIS process, all on one device.
+    comm=None: every rank of the job is in ``ranks`` (ranks emulated on one
+    device -- one cooperative launch runs all of them; the peers' buffers are
+    addressed directly).  comm = a torch.distributed group: one rank per
+    process and GPU; the peers' buffers are CUDA-IPC mapped (ebb_ipc_*), the
+    infos travel once through ``all_gather_object``.  After binding, one
+    ``step(iters)`` per implicit step replaces the per-phase launches,
+    allreduces and halo exchanges of the "single" driver."""
+
+    def __init__(self, ranks, comm=None, stream=None):
+        import ctypes as C
+
+        from . import _abi as A
+        self.ranks, self.ctx, self.stream = list(ranks), ranks[0].ctx, stream
+        ctx = self.ctx
+        ipc = comm is not None
+        if ipc:
+            import torch.distributed as tdist
+            nranks = tdist.get_world_size(comm)
+            (R0,) = self.ranks
+            gathered = [None] * nranks
+            tdist.all_gather_object(gathered, R0.peer_export(ipc=True), group=comm)
+            infos = {d["rank"]: d for d in gathered}
+        else:
+            nranks = len(self.ranks)
+            infos = {R.rank: R.peer_export(ipc=False) for R in self.ranks}
+        if sorted(infos) != list(range(nranks)):
+            raise ValueError(f"peer ranks {sorted(infos)} are not 0..{nranks - 1}")
+        tables = peer_tables(infos, [R.rank for R in self.ranks], nranks)
+        self._opened = []
+        cgs = (A.CG * len(self.ranks))()
+        pcs = (A.PeerCG * len(self.ranks))()
+        for i, R in enumerate(self.ranks):
+            t = tables[R.rank]
+            off, dst = R.peer_send_csr(t["peers"], t["remote"], t["peer_nv"])
+            pc = pcs[i]
+            pc.nranks, pc.rank, pc.n_owned = nranks, R.rank, R.n_owned
+            pc.send_off, pc.send_dst, pc.mbox = off.h, dst.h, R.mbox.h
+            for name, arr in (("u", pc.peer_u), ("u2", pc.peer_u2), ("x", pc.peer_x), ("z", pc.peer_z),
+                              ("mbox", pc.peer_mbox)):
+                for q, b in enumerate(t["bufs"][name]):
+                    if b is None:
+                        continue
+                    if ipc:
+                        addr = C.c_uint64()
+                        ctx.check(ctx.L.ebb_ipc_open(ctx.h, bytes(b), C.byref(addr)))
+                        self._opened.append(addr.value)
+                        b = addr.value
+                    arr[q] = int(b)
+            cgs[i] = R.fem.cg
+        g = C.c_int32()
+        ctx.check(ctx.L.ebb_cg_peer_bind(ctx.h, len(self.ranks), cgs, pcs, C.byref(g)))
+        self.group = g.value
+        if ipc:
+            import torch.distributed as tdist
+            tdist.barrier(group=comm)     # every rank mapped its peers before anyone steps
+
+    def step(self, iters):
+        from .ebb import _stream
+        self.ctx.check(self.ctx.L.ebb_cg_peer_step(self.ctx.h, self.group, int(iters), _stream(self.stream)))
+
+    def close(self):
+        for a in self._opened:
+            self.ctx.check(self.ctx.L.ebb_ipc_close(self.ctx.h, a))
+        self._opened = []

@@ -65,7 +65,7 @@ class Context:
     def error_counts(self, reset=False):
         out = (C.c_uint64 * 4)()
         self.check(self.L.ebb_error_counts(self.h, out, int(reset)))
-        return dict(inverted=out[0], not_spd=out[1], bounds=out[2])
+        return dict(inverted=out[0], not_spd=out[1], bounds=out[2], peer_timeouts=out[3])
 
     def map_plan_stats(self, v, e):
         """Statistics of the SEGMENTED map plan for key-fields (v, e)."""

@@ -491,19 +491,28 @@ def run_dist(args, rank, world, local_rank):
     R = D.GpuRank(ctx, rank, part, X, free, u0, np.zeros_like(u0), mu, lam, rho=w["rho"], stream=stream,
                   name=f"rank{rank}")
     t_part = time.perf_counter() - t_part
-    # NCCL inside the library (ebb_comm_*); no fallback: a failure here ends the run
-    T = D.NcclTransport(ctx, rank, world, stream=stream)
-    transport = "nccl (in-library, ebb_comm_*)"
+    cg_var = args.dist_cg
+    peer = None
+    if cg_var == "peer":
+        # the fused multi-GPU PCG: one kernel per solve; u / x / z_0 halos as
+        # P2P stores into the peers' (CUDA-IPC mapped) ghost rows and the CG
+        # scalars through peer mailboxes -- no NCCL on the step; no fallback
+        T = None
+        peer = D.PeerPCG([R], comm=dist.group.WORLD if world > 1 else None, stream=stream)
+        transport = "peer memory (CUDA IPC over NVLink; ebb_cg_peer_step)"
+    else:
+        # NCCL inside the library (ebb_comm_*); no fallback: a failure here ends the run
+        T = D.NcclTransport(ctx, rank, world, stream=stream)
+        transport = "nccl (in-library, ebb_comm_*)"
     T_global = tets.shape[0]
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
-    cg_var = args.dist_cg
-    kmv = A.K_CG_SOLVE if cg_var == "single" else A.K_EDGE_MATVEC   # the streamed-matrix kernel of a phase
+    kmv = A.K_EDGE_MATVEC if cg_var == "saad" else A.K_CG_SOLVE   # the streamed-matrix kernel
 
     reset = state_reset(R.fem, stream)       # local u, v (owned + ghost rows) back to (u0, v0)
 
     def step():
-        D.implicit_step([R], T, w["model"], h=w["h"], iters=w["cg_iters"], variant=cg_var)
+        D.implicit_step([R], T, w["model"], h=w["h"], iters=w["cg_iters"], variant=cg_var, peer=peer)
 
     t_pre = time.perf_counter()              # clocks ramp from idle (see run_ours)
     while time.perf_counter() - t_pre < 0.5:
@@ -605,20 +614,33 @@ def run_dist(args, rank, world, local_rank):
     peak, peak_src = _peaks()
     E_loc = R.fem.ne
     # single: one launch = one PCG iteration of the local rows (the prologue
-    # launch moves about the same bytes); saad: the MATVEC phase kernel
-    b_mv = bytes_cg_iter(V_loc, E_loc) if cg_var == "single" else bytes_matvec(V_loc, E_loc)
+    # launch moves about the same bytes); peer: one launch = all iterations
+    # (+ the prologue matvec); saad: the MATVEC phase kernel
+    if cg_var == "single":
+        b_mv = bytes_cg_iter(V_loc, E_loc)
+        kname = "k_cg1_persistent (one single-reduction phase per launch)"
+    elif cg_var == "peer":
+        b_mv = (w["cg_iters"] + 1) * bytes_cg_iter(V_loc, E_loc)
+        kname = "k_cg1_peer (fused multi-GPU single-reduction PCG, all iterations in one launch)"
+    else:
+        b_mv = bytes_matvec(V_loc, E_loc)
+        kname = "edge_matvec (Saad MATVEC phase)"
     avg_mv = 1e3 * mv_ms / max(mv_n, 1)
-    roof = {"kernel": "k_cg1_persistent (one single-reduction phase per launch)" if cg_var == "single"
-            else "edge_matvec (Saad MATVEC phase)", "bound": "hbm", "achieved": b_mv / (avg_mv * 1e-6) / 1e9, "peak": peak,
+    roof = {"kernel": kname, "bound": "hbm", "achieved": b_mv / (avg_mv * 1e-6) / 1e9, "peak": peak,
             "unit": "GB/s", "frac": b_mv / (avg_mv * 1e-6) / 1e9 / peak, "peak_source": peak_src, "traffic": None,
             "algorithmic_bytes_per_launch": b_mv, "avg_launch_us": avg_mv, "rank": rank}
     cfg = _config(world)
     cfg.update({"workload": f"{WORKLOAD['name']} recipe weak-scaled: Kuhn-6 n={n} ({T_global} tets, {X.shape[0]} verts) split over "
                             f"{world} GPUs by the O4 owner maps (ghost tets; per PCG iteration "
-                            + ("one fused 2-scalar allreduce + u halo, single-reduction phases"
-                               if cg_var == "single" else "z halo + 2 scalar allreduces, Saad phases")
-                            + " over NCCL), fp64", "transport": transport, "pcg": cg_var,
-                "tets": T_global, "parallelism": f"domain decomposition x{world} (NCCL halo + allreduce)"})
+                            + {"single": "one fused 2-scalar allreduce + u halo, single-reduction phases over NCCL",
+                               "saad": "z halo + 2 scalar allreduces, Saad phases over NCCL",
+                               "peer": "u / x halo as P2P stores + a 2-scalar mailbox exchange inside ONE fused "
+                                       "single-reduction PCG kernel"}[cg_var]
+                            + "), fp64", "transport": transport, "pcg": cg_var,
+                "tets": T_global,
+                "parallelism": f"domain decomposition x{world} ("
+                               + ("peer-memory halo + scalar exchange in the PCG kernel" if cg_var == "peer"
+                                  else "NCCL halo + allreduce") + ")"})
     line = {"metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Kuhn-6 cube, stretch+noise displacement)",
@@ -629,6 +651,9 @@ def run_dist(args, rank, world, local_rank):
                            "owned_verts": int(part["n_owned"]), "partition_setup_s": t_part}}
     if rank == 0:
         print(json.dumps(line))
+    if peer is not None:
+        dist.barrier()                        # no peer still reads a buffer this rank is about to unmap / free
+        peer.close()
     ctx.close()
 
 
@@ -744,8 +769,10 @@ def main():
     ap.add_argument("--map-only", action="store_true",
                     help="BASELINE configs[2]: the fp32 StVK map on the 1e7-tet blob with the position halo "
                          "(domain decomposition; with one rank add --dist)")
-    ap.add_argument("--dist-cg", default="single", choices=["single", "saad"],
-                    help="PCG driver of the multi-GPU path (single: one fused allreduce per iteration)")
+    ap.add_argument("--dist-cg", default="peer", choices=["peer", "single", "saad"],
+                    help="PCG driver of the multi-GPU path (peer: ONE fused kernel per solve, halos and scalar "
+                         "sums over peer memory; single: per-iteration phases with one fused NCCL allreduce; "
+                         "saad: two allreduces per iteration)")
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU (domain decomposition) path even with one rank (smoke test)")
     args = ap.parse_args()

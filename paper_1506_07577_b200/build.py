@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr_t):
-            cmds.append([nvcc, *NVCC_FLAGS, "-c", "-o", obj, src])
+            cmds.append([nvcc, *NVCC_FLAGS, *os.environ.get("EBB_NVCC_EXTRA", "").split(), "-c", "-o", obj, src])
     with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, len(cmds))) as ex:
         for cmd, rc in zip(cmds, ex.map(lambda c: subprocess.call(c), cmds)):
             if verbose:

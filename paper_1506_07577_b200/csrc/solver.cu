@@ -1405,15 +1405,18 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-// grid barrier over the G CTAs of one rank; each CTA fences at system scope
-// before it arrives (its stores to peer memory precede the rank's publication)
-__device__ __forceinline__ void rank_barrier(unsigned int* bar, unsigned int nblocks) {
-    __syncthreads();
+// grid barrier over the G CTAs of one rank; a CTA that stored to peer memory
+// since its last barrier fences at system scope before it arrives (those
+// stores precede the rank's publication), the others at GPU scope (nothing
+// of theirs is read by a peer)
+__device__ __forceinline__ void rank_barrier(unsigned int* bar, unsigned int nblocks, bool sent) {
+    const int any = __syncthreads_or(sent ? 1 : 0);
     if (threadIdx.x == 0) {
         unsigned int* count = bar;
         unsigned int* gen = bar + 1;
         const unsigned int g = *reinterpret_cast<volatile unsigned int*>(gen);
-        __threadfence_system();
+        if (any) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else __threadfence();
         if (atomicAdd(count, 1u) == nblocks - 1) {
             *reinterpret_cast<volatile unsigned int*>(count) = 0u;
             __threadfence();
@@ -1440,7 +1443,6 @@ __device__ __forceinline__ void peer_exchange(const PeerRankArgs& a, unsigned bi
     const unsigned q = threadIdx.x;
     if (bid == 0 && q < (unsigned)a.nranks && q != (unsigned)a.rank) {
         unsigned long long* mb = a.peer_mbox[q] + (slot * kPeerMax + a.rank) * 4;
-        __threadfence_system();
         st_relaxed_sys(mb, (unsigned long long)__double_as_longlong(d));
         st_relaxed_sys(mb + 1, (unsigned long long)__double_as_longlong(g));
         st_release_sys(mb + 2, seq);
@@ -1481,17 +1483,17 @@ __device__ __forceinline__ void peer_exchange(const PeerRankArgs& a, unsigned bi
     gsum = sm2[1];
 }
 
-// (min 3 CTAs per SM: 72 registers, the single-GPU kernel's occupancy; unbounded
-// it takes 132 and one CTA per SM)
+// The body of one rank's CTA (lr: local rank of the launch, bid: CTA within
+// the rank, G CTAs per rank); `a` is a kernel parameter (one rank per launch,
+// the production multi-GPU form: its fields are constant-bank operands, no
+// registers) or a record in global memory (ranks emulated on one device).
 template <typename R>
-__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
-    k_cg1_peer(const PeerRankArgs* __restrict__ ranks, unsigned G, unsigned long long* __restrict__ err, int iters,
-               double tol2) {
+__device__ __forceinline__ void cg1_peer_body(const PeerRankArgs& a, const unsigned lr, const unsigned bid,
+                                              const unsigned G, unsigned long long* __restrict__ err, int iters,
+                                              const double tol2) {
     extern __shared__ __align__(128) unsigned char tma_smem[];
     __shared__ __align__(8) uint64_t full_bar[CG1_NS], empty_bar[CG1_NS];
     __shared__ double sm_tot, sm2[2];
-    const unsigned lr = blockIdx.x / G, bid = blockIdx.x - lr * G;
-    const PeerRankArgs& a = ranks[lr];
     constexpr uint32_t AE = 16 / sizeof(R);
     const uint64_t nv = a.nv, ne = a.ne;
     const uint32_t cap = a.cap;
@@ -1541,6 +1543,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
         gam = g0;
         rz0 = g0;
         // 2) z_0 halo: owners store their rows into the peers' ghost rows
+        bool sent = false;
         for (uint64_t v = (uint64_t)bid * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)G * blockDim.x) {
             const uint32_t s0 = send_off[v], s1 = send_off[v + 1];
             if (s0 == s1) continue;
@@ -1549,8 +1552,9 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
                 const uint2 d = send_dst[k];
                 st4((R*)a.peer_z0[d.x], d.y, zv);
             }
+            sent = true;
         }
-        rank_barrier(a.bar, G);
+        rank_barrier(a.bar, G, sent);
         peer_exchange(a, bid, epoch++, 0.0, 0.0, sm2, err, g0, unused);
     }
     uint64_t issued = 0;
@@ -1591,6 +1595,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
         const bool un1 = pro ? par != 0 : par == 0;          // u_{i+1} goes to buffer 1 (u2)
         R* __restrict__ un = un1 ? ub1 : ub0;
         double pg = 0.0, pd = 0.0;
+        bool sent = false;
         if (warp == TMA_CONSUMERS) {
             if (lane == 0) {
                 for (uint64_t j = CG1_NS; j < my_chunks; ++j) issue(bid + j * G, issued++);
@@ -1659,6 +1664,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
                             const uint2 d = send_dst[k];
                             st4((R*)(un1 ? a.peer_ub1[d.x] : a.peer_ub0[d.x]), d.y, t);
                         }
+                        sent |= s0 != s1;
                         pd += (double)a0 * zv.x + (double)a1 * zv.y + (double)a2 * zv.z;
                     } else {
                         auto rv = ld4(r, v);
@@ -1694,6 +1700,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
                             px[1] = x1;
                             px[2] = x2;
                         }
+                        sent |= s0 != s1;
                         const R zx = rv.x * dv.x, zy = rv.y * dv.y, zz = rv.z * dv.z;
                         pg += (double)rv.x * zx + (double)rv.y * zy + (double)rv.z * zz;
                         pd += (double)wi.x * zx + (double)wi.y * zy + (double)wi.z * zz;
@@ -1709,7 +1716,7 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
             pgb[bid] = pg;
             pdb[bid] = pd;
         }
-        rank_barrier(a.bar, G);
+        rank_barrier(a.bar, G, sent);
         const double dl = grid_sum_partials(pdb, G, &sm_tot);
         const double gl = pro ? 0.0 : grid_sum_partials(pgb, G, &sm_tot);
         double dsum, gnew;
@@ -1753,6 +1760,30 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
         *a.rho_user = gam;
         a.mbox[kMbEpoch] = epoch;
     }
+}
+
+// one rank per launch (a process per GPU): the record is a kernel parameter
+// (min 3 CTAs per SM, the single-GPU kernel's occupancy: unbounded it takes
+// 84 registers, two CTAs per SM)
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
+    k_cg1_peer1(const __grid_constant__ PeerRankArgs a, unsigned long long* __restrict__ err, int iters,
+                double tol2) {
+    cg1_peer_body<R>(a, 0u, blockIdx.x, gridDim.x, err, iters, tol2);
+}
+
+// several ranks emulated on one device in one cooperative launch: records in
+// global memory (min 3 CTAs per SM: 72 registers; unbounded, the loaded
+// record pointers take 132 registers and one CTA per SM)
+#ifndef PEER_MINB
+#define PEER_MINB 3
+#endif
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), PEER_MINB)
+    k_cg1_peer(const PeerRankArgs* __restrict__ ranks, unsigned G, unsigned long long* __restrict__ err, int iters,
+               double tol2) {
+    const unsigned lr = blockIdx.x / G;
+    cg1_peer_body<R>(ranks[lr], lr, blockIdx.x - lr * G, G, err, iters, tol2);
 }
 
 // ---------------------------------------------------------------------------
@@ -2442,19 +2473,26 @@ struct PeerGroup {
     ebb_dtype dt = EBB_F64;
     double tol2 = 0.0;
     PeerRankArgs* d_args = nullptr;
+    PeerRankArgs one;                  // nlocal == 1: the record passed as a kernel parameter
     double* d_part = nullptr;
     unsigned int* d_bar = nullptr;
 };
 
 template <typename R>
-ebb_status peer_occupancy(Ctx* c, size_t smem, int* nb) {
-    static thread_local size_t configured_dev[kMaxDevices] = {};
-    size_t& configured = configured_dev[c->device % kMaxDevices];
+ebb_status peer_occupancy(Ctx* c, size_t smem, int nlocal, int* nb) {
+    static thread_local size_t configured_dev[2][kMaxDevices] = {};
+    size_t& configured = configured_dev[nlocal == 1][c->device % kMaxDevices];
     if (smem > configured) {
-        EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_peer<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (nlocal == 1)
+            EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_peer1<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        else
+            EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_peer<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k_cg1_peer<R>, 32 * (TMA_CONSUMERS + 1), smem));
+    if (nlocal == 1)
+        EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k_cg1_peer1<R>, 32 * (TMA_CONSUMERS + 1), smem));
+    else
+        EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k_cg1_peer<R>, 32 * (TMA_CONSUMERS + 1), smem));
     return EBB_OK;
 }
 
@@ -2901,8 +2939,8 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
     const size_t smem = stage_max * CG1_NS;
     if (smem > kTmaSmemMax) return fail(c, EBB_E_SIZE, "peer_bind: TMA ring of %zu bytes does not fit", smem);
     int nb = 0;
-    if (dt0 == EBB_F64) EBB_TRY(peer_occupancy<double>(c, smem, &nb));
-    else EBB_TRY(peer_occupancy<float>(c, smem, &nb));
+    if (dt0 == EBB_F64) EBB_TRY(peer_occupancy<double>(c, smem, nlocal, &nb));
+    else EBB_TRY(peer_occupancy<float>(c, smem, nlocal, &nb));
     unsigned G = (unsigned)((uint64_t)nb * c->num_sms / (uint64_t)nlocal);
     if (G > kCg1PartStride) G = kCg1PartStride;
     if (G < 1) return fail(c, EBB_E_SIZE, "peer_bind: %d ranks cannot all be resident on one device", nlocal);
@@ -2922,6 +2960,7 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
         h[i].bar = P->d_bar + 2 * i;
     }
     EBB_CUDA(c, cudaMemcpy(P->d_args, h.data(), sizeof(PeerRankArgs) * nlocal, cudaMemcpyHostToDevice));
+    P->one = h[0];
     *group_out = (int32_t)(c->peer_groups.size() - 1);
     return EBB_OK;
 }
@@ -2946,12 +2985,18 @@ ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_strea
     cfg.attrs = at;
     cfg.numAttrs = 1;
     KernelTimer kt(c, EBB_K_CG_SOLVE, s);
-    if (P->dt == EBB_F64)
+    if (P->nlocal == 1) {
+        if (P->dt == EBB_F64)
+            EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer1<double>, P->one, c->d_err, (int)iters, P->tol2));
+        else
+            EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer1<float>, P->one, c->d_err, (int)iters, P->tol2));
+    } else if (P->dt == EBB_F64) {
         EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer<double>, (const PeerRankArgs*)P->d_args, P->G, c->d_err,
                                        (int)iters, P->tol2));
-    else
+    } else {
         EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer<float>, (const PeerRankArgs*)P->d_args, P->G, c->d_err,
                                        (int)iters, P->tol2));
+    }
     return EBB_OK;
 }
 

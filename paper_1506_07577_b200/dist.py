@@ -667,6 +667,7 @@ class PeerPCG:
             raise ValueError(f"peer ranks {sorted(infos)} are not 0..{nranks - 1}")
         tables = peer_tables(infos, [R.rank for R in self.ranks], nranks)
         self._opened = []
+        self.peer_addr = {}                        # (local rank, peer, buffer) -> device address used
         cgs = (A.CG * len(self.ranks))()
         pcs = (A.PeerCG * len(self.ranks))()
         for i, R in enumerate(self.ranks):
@@ -686,6 +687,7 @@ class PeerPCG:
                         self._opened.append(addr.value)
                         b = addr.value
                     arr[q] = int(b)
+                    self.peer_addr[(R.rank, q, name)] = int(b)
             cgs[i] = R.fem.cg
         g = C.c_int32()
         ctx.check(ctx.L.ebb_cg_peer_bind(ctx.h, len(self.ranks), cgs, pcs, C.byref(g)))

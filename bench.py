@@ -147,6 +147,26 @@ def bytes_matvec(V, E, bf=8):
     return E * (9 * bf + 4) + V * (4 + 6 * bf)
 
 
+_OUT = None
+
+
+def _claim_stdout():
+    """The contract is ONE JSON line on stdout: libraries that print to fd 1
+    (NCCL's version banner, CUDA/driver notices) are moved to stderr; the
+    JSON line goes to the original stdout."""
+    global _OUT
+    if _OUT is None:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _OUT if _OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def bytes_cg_iter(V, E, bf=8):
     return bytes_matvec(V, E, bf) + V * 3 * bf * 11
 
@@ -200,7 +220,7 @@ def run_reference(args, rank, world):
             "data": "synthetic", "config": _config(world),
             "cpu_baseline": cb, "e2e": {"value": val, "unit": "tets/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
 
 
 def _config(world, sample=False, n=None):
@@ -460,7 +480,7 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
 
 
 def run_dist(args, rank, world, local_rank):
@@ -620,8 +640,9 @@ def run_dist(args, rank, world, local_rank):
         b_mv = bytes_cg_iter(V_loc, E_loc)
         kname = "k_cg1_persistent (one single-reduction phase per launch)"
     elif cg_var == "peer":
-        b_mv = (w["cg_iters"] + 1) * bytes_cg_iter(V_loc, E_loc)
-        kname = "k_cg1_peer (fused multi-GPU single-reduction PCG, all iterations in one launch)"
+        b_mv = (w["cg_iters"] + (1 if peer.variant == "single" else 0)) * bytes_cg_iter(V_loc, E_loc)
+        kname = (f"k_cg_peer1 ({peer.variant} body; fused multi-GPU PCG, all iterations in one launch, halos and "
+                 f"scalar exchanges over peer memory)")
     else:
         b_mv = bytes_matvec(V_loc, E_loc)
         kname = "edge_matvec (Saad MATVEC phase)"
@@ -636,7 +657,7 @@ def run_dist(args, rank, world, local_rank):
                                "saad": "z halo + 2 scalar allreduces, Saad phases over NCCL",
                                "peer": "u / x halo as P2P stores + a 2-scalar mailbox exchange inside ONE fused "
                                        "single-reduction PCG kernel"}[cg_var]
-                            + "), fp64", "transport": transport, "pcg": cg_var,
+                            + "), fp64", "transport": transport, "pcg": cg_var if peer is None else f"peer ({peer.variant})",
                 "tets": T_global,
                 "parallelism": f"domain decomposition x{world} ("
                                + ("peer-memory halo + scalar exchange in the PCG kernel" if cg_var == "peer"
@@ -650,7 +671,7 @@ def run_dist(args, rank, world, local_rank):
                            "local_tets": int(R.fem.nt), "local_verts": int(V_loc),
                            "owned_verts": int(part["n_owned"]), "partition_setup_s": t_part}}
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     if peer is not None:
         dist.barrier()                        # no peer still reads a buffer this rank is about to unmap / free
         peer.close()
@@ -753,7 +774,7 @@ def run_dist_map(args, rank, world, local_rank):
             "components": {"local_tets": int(R.fem.nt), "owned_verts": int(part["n_owned"]),
                            "partition_setup_s": t_part}}
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     ctx.close()
 
 
@@ -776,6 +797,7 @@ def main():
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU (domain decomposition) path even with one rank (smoke test)")
     args = ap.parse_args()
+    _claim_stdout()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -1366,6 +1366,8 @@ struct PeerRankArgs {
     const void* A;
     const void* dinv;
     void *x, *r, *z0, *p, *sv, *yv, *wv, *ub0, *ub1;
+    void *q, *p2;                      // Saad: q = A p, the second direction buffer
+    uint64_t nv_all;                   // local rows (owned + ghost)
     const uint8_t* mask;
     double* part;                      // 4 x kCg1PartStride: (g, d) x phase parity
     unsigned int* bar;                 // rank grid barrier: count, generation
@@ -1762,14 +1764,293 @@ __device__ __forceinline__ void cg1_peer_body(const PeerRankArgs& a, const unsig
     }
 }
 
-// one rank per launch (a process per GPU): the record is a kernel parameter
-// (min 3 CTAs per SM, the single-GPU kernel's occupancy: unbounded it takes
-// 84 registers, two CTAs per SM)
+// Saad Alg. 9.1 (the single-GPU k_cg_persistent's iterates and phases) with
+// the same peer-memory halo and mailbox exchanges, for ranks whose vector
+// records stream from HBM (~1e7 tets per GPU), where Saad's two gathered
+// vectors cost less than the single-reduction form's nine owner records
+// (DESIGN.md §5.4).  Per iteration two exchanges (p.q after the matvec, r.z
+// after the update).  Ghost rows: z arrives from the owners (stored by the
+// owner's update phase); the direction p = z + beta p_old of a ghost row is
+// formed by the receiver (a ghost pass in the matvec phase writes it into the
+// new p buffer; gatherers form it on the fly as on one GPU); x arrives from
+// the owners.  Owners store z and x rows during the update phase, which
+// peers reach only after the p.q exchange, i.e. after this rank's matvec
+// phase (including the ghost pass) read the old z.
 template <typename R>
+__device__ __forceinline__ void cg_saad_peer_body(const PeerRankArgs& a, const unsigned lr, const unsigned bid,
+                                                  const unsigned G, unsigned long long* __restrict__ err,
+                                                  int iters, const double tol2) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    __shared__ __align__(8) uint64_t full_bar[TMA_NS], empty_bar[TMA_NS];
+    __shared__ double sm_tot, sm2[2];
+    constexpr uint32_t AE = 16 / sizeof(R);
+    const uint64_t nv = a.nv, ne = a.ne, nv_all = a.nv_all;
+    const uint32_t cap = a.cap;
+    const uint32_t* __restrict__ index = a.index;
+    const uint32_t* __restrict__ head = a.head;
+    const R* __restrict__ A = (const R*)a.A;
+    const R* __restrict__ dinv = (const R*)a.dinv;
+    R* __restrict__ x = (R*)a.x;
+    R* __restrict__ r = (R*)a.r;
+    R* __restrict__ z = (R*)a.z0;
+    R* __restrict__ q = (R*)a.q;
+    R* pb0 = (R*)a.p;
+    R* pb1 = (R*)a.p2;
+    const uint8_t* __restrict__ mask = a.mask;
+    double* __restrict__ scal = a.scal;
+    const uint32_t* __restrict__ send_off = a.send_off;
+    const uint2* __restrict__ send_dst = a.send_dst;
+    double* __restrict__ part_pq = a.part;
+    double* __restrict__ part_rz = a.part + kCg1PartStride;
+    const size_t stage_bytes = ((size_t)9 * cap * sizeof(R) + (size_t)cap * 4 + 127) & ~(size_t)127;
+    const uint64_t nchunks = (nv + TMA_VCH - 1) / TMA_VCH;
+    const uint64_t my_chunks = nchunks > bid ? (nchunks - bid + G - 1) / G : 0;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TMA_NS; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], PCG_WPG);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    uint64_t epoch = a.mbox[kMbEpoch];
+    double rho = scal[S_RHO];
+    int first = scal[S_FIRST] != 0.0;
+    int cur = scal[S_PAR] != 0.0;
+    double rz_new = scal[S_RZ];
+    double rz0 = scal[S_RZ0];
+    if (scal[S_DONE] != 0.0) iters = 0;
+    int done_it = 0;
+    bool conv = false;
+    const uint64_t gthreads = (uint64_t)G * blockDim.x;
+    const uint64_t gtid = (uint64_t)bid * blockDim.x + threadIdx.x;
+    if (first && iters > 0) {
+        // the global r_0.z_0 (every rank has initialised), then the z_0 halo
+        double g0, unused;
+        peer_exchange(a, bid, epoch++, rz_new, 0.0, sm2, err, g0, unused);
+        rz_new = g0;
+        rho = g0;
+        rz0 = g0;
+        bool sent = false;
+        for (uint64_t v = gtid; v < nv; v += gthreads) {
+            const uint32_t s0 = send_off[v], s1 = send_off[v + 1];
+            if (s0 == s1) continue;
+            const auto zv = ld4(z, v);
+            for (uint32_t k = s0; k < s1; ++k) {
+                const uint2 d = send_dst[k];
+                st4((R*)a.peer_z0[d.x], d.y, zv);
+            }
+            sent = true;
+        }
+        rank_barrier(a.bar, G, sent);
+        peer_exchange(a, bid, epoch++, 0.0, 0.0, sm2, err, g0, unused);
+    }
+    uint64_t issued = 0;
+    auto issue = [&](uint64_t ch, uint64_t seq) {
+        const int s = seq % TMA_NS;
+        const uint64_t v0 = ch * TMA_VCH;
+        const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+        const uint64_t e0 = index[v0], e1 = index[v1];
+        if (seq >= TMA_NS) mbar_wait(&empty_bar[s], (uint32_t)(((seq / TMA_NS) + 1) & 1u));
+        unsigned char* base = tma_smem + s * stage_bytes;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            tot += (uint32_t)((a1 - a0) * sizeof(R));
+        }
+        const uint64_t h0 = e0 & ~3ull, h1 = (e1 + 3) & ~3ull;
+        tot += (uint32_t)((h1 - h0) * 4);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full_bar[s], tot);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const uint64_t a0 = (c * ne + e0) & ~(uint64_t)(AE - 1);
+            const uint64_t a1 = (c * ne + e1 + AE - 1) & ~(uint64_t)(AE - 1);
+            bulk_g2s_evict_first(base + (size_t)c * cap * sizeof(R), A + a0, (uint32_t)((a1 - a0) * sizeof(R)),
+                                 &full_bar[s]);
+        }
+        bulk_g2s_evict_first(base + (size_t)9 * cap * sizeof(R), head + h0, (uint32_t)((h1 - h0) * 4), &full_bar[s]);
+    };
+    if (iters > 0 && warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(bid + j * G, issued++);
+    for (int it = 0; it < iters; ++it) {
+        const R beta = (first || rho == 0.0) ? R(0) : (R)(rz_new / rho);
+        const R* __restrict__ pold = cur ? pb1 : pb0;
+        R* __restrict__ pnew = cur ? pb0 : pb1;
+        double pq = 0.0;
+        if (warp == TMA_CONSUMERS) {
+            if (lane == 0) {
+                for (uint64_t j = TMA_NS; j < my_chunks; ++j) issue(bid + j * G, issued++);
+                if (it + 1 < iters)
+                    for (uint64_t j = 0; j < my_chunks && j < TMA_NS; ++j) issue(bid + j * G, issued++);
+            }
+        } else {
+            const unsigned grp = warp / PCG_WPG, wig = warp % PCG_WPG;
+            const unsigned sub = lane & 7;
+            const uint64_t seq0 = (uint64_t)it * my_chunks;
+            for (uint64_t j = grp; j < my_chunks; j += PCG_GROUPS) {
+                const uint64_t seq = seq0 + j;
+                const uint64_t ch = bid + j * G;
+                const int s = seq % TMA_NS;
+                const uint64_t v0 = ch * TMA_VCH;
+                const uint64_t v1 = v0 + TMA_VCH < nv ? v0 + TMA_VCH : nv;
+                const uint64_t v = v0 + 4 * wig + (lane >> 3);
+                const bool valid = v < v1;
+                const uint32_t e0 = index[v0];
+                const uint32_t r0 = valid ? index[v] - e0 : 0u, r1 = valid ? index[v + 1] - e0 : 0u;
+                R own0 = 0, own1 = 0, own2 = 0;
+                uint8_t mk = 1;
+                if (valid && sub == 0) {
+                    const auto zv = ld4cg(z, v);
+                    const auto ov = ld4cg(pold, v);
+                    own0 = zv.x + beta * ov.x;
+                    own1 = zv.y + beta * ov.y;
+                    own2 = zv.z + beta * ov.z;
+                    if (mask) mk = mask[v];
+                }
+                mbar_wait(&full_bar[s], (uint32_t)((seq / TMA_NS) & 1u));
+                const unsigned char* base = tma_smem + s * stage_bytes;
+                const uint32_t* hs = reinterpret_cast<const uint32_t*>(base + (size_t)9 * cap * sizeof(R)) + (e0 & 3u);
+                uint32_t off[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) off[c] = (uint32_t)((c * ne + e0) & (AE - 1));
+                R a0 = 0, a1 = 0, a2 = 0;
+                for (uint32_t rb = r0 + sub; rb < r1; rb += 16) {
+                    const uint32_t rr1 = rb + 8;
+                    const bool two = rr1 < r1;
+                    const uint32_t h0 = hs[rb], h1 = two ? hs[rr1] : h0;
+                    const auto z0v = ld4cg(z, h0);
+                    const auto o0 = ld4cg(pold, h0);
+                    const auto z1v = ld4cg(z, h1);
+                    const auto o1 = ld4cg(pold, h1);
+                    R av[9], bv[9];
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) {
+                        const R* pl = reinterpret_cast<const R*>(base + (size_t)c * cap * sizeof(R)) + off[c];
+                        av[c] = pl[rb];
+                        bv[c] = two ? pl[rr1] : R(0);
+                    }
+                    const R px = z0v.x + beta * o0.x, py = z0v.y + beta * o0.y, pz = z0v.z + beta * o0.z;
+                    const R qx = z1v.x + beta * o1.x, qy = z1v.y + beta * o1.y, qz = z1v.z + beta * o1.z;
+                    a0 += av[0] * px + av[1] * py + av[2] * pz + (bv[0] * qx + bv[1] * qy + bv[2] * qz);
+                    a1 += av[3] * px + av[4] * py + av[5] * pz + (bv[3] * qx + bv[4] * qy + bv[5] * qz);
+                    a2 += av[6] * px + av[7] * py + av[8] * pz + (bv[6] * qx + bv[7] * qy + bv[8] * qz);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o, 8);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o, 8);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, o, 8);
+                }
+                if (sub == 0 && valid) {
+                    if (!mk) a0 = a1 = a2 = 0;
+                    typename V4<R>::T qv, pv;
+                    qv.x = a0; qv.y = a1; qv.z = a2; qv.w = 0;
+                    pv.x = own0; pv.y = own1; pv.z = own2; pv.w = 0;
+                    st4(q, v, qv);
+                    st4(pnew, v, pv);
+                    pq += (double)own0 * a0 + (double)own1 * a1 + (double)own2 * a2;
+                }
+            }
+            // ghost rows: the new direction from the owners' z (they are
+            // gathered on the fly in this phase; stored for the next one)
+            for (uint64_t g = nv + (uint64_t)bid * (blockDim.x - 32) + threadIdx.x; g < nv_all;
+                 g += (uint64_t)G * (blockDim.x - 32)) {
+                const auto zv = ld4cg(z, g);
+                const auto ov = ld4cg(pold, g);
+                typename V4<R>::T pv;
+                pv.x = zv.x + beta * ov.x;
+                pv.y = zv.y + beta * ov.y;
+                pv.z = zv.z + beta * ov.z;
+                pv.w = 0;
+                st4(pnew, g, pv);
+            }
+        }
+        pq = block_reduce<ROP_SUM>(pq);
+        if (threadIdx.x == 0) part_pq[bid] = pq;
+        rank_barrier(a.bar, G, false);
+        double pqs, unused;
+        peer_exchange(a, bid, epoch++, grid_sum_partials(part_pq, G, &sm_tot), 0.0, sm2, err, pqs, unused);
+        if (lr == 0 && bid == 0 && threadIdx.x == 0 && pqs < 0.0) atomicAdd(&err[ERR_NOT_SPD], 1ull);
+        rho = rz_new;
+        first = 0;
+        cur ^= 1;
+        const R alpha = (pqs != 0.0) ? (R)(rho / pqs) : R(0);
+        double acc = 0.0;
+        bool sent = false;
+        for (uint64_t vv = gtid; vv < nv; vv += gthreads) {
+            const auto pv = ld4cg(pnew, vv);
+            const auto qv = ld4cg(q, vv);
+            const auto dv = ld4(dinv, vv);
+            auto rv = ld4(r, vv);
+            rv.x -= alpha * qv.x;
+            rv.y -= alpha * qv.y;
+            rv.z -= alpha * qv.z;
+            typename V4<R>::T zv;
+            zv.x = rv.x * dv.x;
+            zv.y = rv.y * dv.y;
+            zv.z = rv.z * dv.z;
+            zv.w = 0;
+            st4(r, vv, rv);
+            st4(z, vv, zv);
+            const R x0 = x[3 * vv] + alpha * pv.x, x1 = x[3 * vv + 1] + alpha * pv.y,
+                    x2 = x[3 * vv + 2] + alpha * pv.z;
+            x[3 * vv] = x0;
+            x[3 * vv + 1] = x1;
+            x[3 * vv + 2] = x2;
+            const uint32_t s0 = send_off[vv], s1 = send_off[vv + 1];
+            for (uint32_t k = s0; k < s1; ++k) {
+                const uint2 d = send_dst[k];
+                st4((R*)a.peer_z0[d.x], d.y, zv);
+                R* px = (R*)a.peer_x[d.x] + 3 * (uint64_t)d.y;
+                px[0] = x0;
+                px[1] = x1;
+                px[2] = x2;
+            }
+            sent |= s0 != s1;
+            acc += (double)rv.x * zv.x + (double)rv.y * zv.y + (double)rv.z * zv.z;
+        }
+        acc = block_reduce<ROP_SUM>(acc);
+        if (threadIdx.x == 0) part_rz[bid] = acc;
+        rank_barrier(a.bar, G, sent);
+        peer_exchange(a, bid, epoch++, grid_sum_partials(part_rz, G, &sm_tot), 0.0, sm2, err, rz_new, unused);
+        if (bid == 0 && threadIdx.x == 0) scal[S_PQ] = pqs;
+        ++done_it;
+        if (tol2 > 0.0 && rz_new <= tol2 * rz0) {   // global sums: the same exit on every rank
+            conv = true;
+            break;
+        }
+    }
+    if (warp == TMA_CONSUMERS && lane == 0)
+        for (uint64_t sq = (uint64_t)done_it * my_chunks; sq < issued; ++sq)
+            mbar_wait(&full_bar[sq % TMA_NS], (uint32_t)((sq / TMA_NS) & 1u));
+    if (bid == 0 && threadIdx.x == 0) {
+        scal[S_RHO] = rho;
+        scal[S_RZ] = rz_new;
+        scal[S_RZ0] = rz0;
+        scal[S_FIRST] = first ? 1.0 : 0.0;
+        scal[S_PAR] = cur ? 1.0 : 0.0;
+        scal[S_ITERS] += (double)done_it;
+        if (conv) scal[S_DONE] = 1.0;
+        *a.rho_user = rz_new;
+        a.mbox[kMbEpoch] = epoch;
+    }
+}
+
+// one rank per launch (a process per GPU): the record is a kernel parameter
+// (min 3 CTAs per SM, the single-GPU kernels' occupancy: unbounded the
+// single-reduction body takes 84 registers, two CTAs per SM)
+template <typename R, bool SAAD>
 __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
-    k_cg1_peer1(const __grid_constant__ PeerRankArgs a, unsigned long long* __restrict__ err, int iters,
-                double tol2) {
-    cg1_peer_body<R>(a, 0u, blockIdx.x, gridDim.x, err, iters, tol2);
+    k_cg_peer1(const __grid_constant__ PeerRankArgs a, unsigned long long* __restrict__ err, int iters,
+               double tol2) {
+    if constexpr (SAAD) cg_saad_peer_body<R>(a, 0u, blockIdx.x, gridDim.x, err, iters, tol2);
+    else cg1_peer_body<R>(a, 0u, blockIdx.x, gridDim.x, err, iters, tol2);
 }
 
 // several ranks emulated on one device in one cooperative launch: records in
@@ -1778,12 +2059,13 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3)
 #ifndef PEER_MINB
 #define PEER_MINB 3
 #endif
-template <typename R>
+template <typename R, bool SAAD>
 __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), PEER_MINB)
-    k_cg1_peer(const PeerRankArgs* __restrict__ ranks, unsigned G, unsigned long long* __restrict__ err, int iters,
-               double tol2) {
+    k_cg_peer(const PeerRankArgs* __restrict__ ranks, unsigned G, unsigned long long* __restrict__ err, int iters,
+              double tol2) {
     const unsigned lr = blockIdx.x / G;
-    cg1_peer_body<R>(ranks[lr], lr, blockIdx.x - lr * G, G, err, iters, tol2);
+    if constexpr (SAAD) cg_saad_peer_body<R>(ranks[lr], lr, blockIdx.x - lr * G, G, err, iters, tol2);
+    else cg1_peer_body<R>(ranks[lr], lr, blockIdx.x - lr * G, G, err, iters, tol2);
 }
 
 // ---------------------------------------------------------------------------
@@ -2471,6 +2753,7 @@ struct PeerGroup {
     unsigned G = 0;                    // CTAs per rank
     size_t smem = 0;
     ebb_dtype dt = EBB_F64;
+    bool saad = false;                 // Saad body (else single-reduction)
     double tol2 = 0.0;
     PeerRankArgs* d_args = nullptr;
     PeerRankArgs one;                  // nlocal == 1: the record passed as a kernel parameter
@@ -2478,21 +2761,24 @@ struct PeerGroup {
     unsigned int* d_bar = nullptr;
 };
 
+// the kernel of a group: one rank per launch or emulated ranks, Saad or
+// single-reduction body
 template <typename R>
-ebb_status peer_occupancy(Ctx* c, size_t smem, int nlocal, int* nb) {
-    static thread_local size_t configured_dev[2][kMaxDevices] = {};
-    size_t& configured = configured_dev[nlocal == 1][c->device % kMaxDevices];
+void* peer_kernel(int nlocal, bool saad) {
+    if (nlocal == 1) return saad ? (void*)k_cg_peer1<R, true> : (void*)k_cg_peer1<R, false>;
+    return saad ? (void*)k_cg_peer<R, true> : (void*)k_cg_peer<R, false>;
+}
+
+template <typename R>
+ebb_status peer_occupancy(Ctx* c, size_t smem, int nlocal, bool saad, int* nb) {
+    static thread_local size_t configured_dev[4][kMaxDevices] = {};
+    size_t& configured = configured_dev[(nlocal == 1) * 2 + saad][c->device % kMaxDevices];
+    const void* k = peer_kernel<R>(nlocal, saad);
     if (smem > configured) {
-        if (nlocal == 1)
-            EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_peer1<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        else
-            EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_peer<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        EBB_CUDA(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    if (nlocal == 1)
-        EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k_cg1_peer1<R>, 32 * (TMA_CONSUMERS + 1), smem));
-    else
-        EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k_cg1_peer<R>, 32 * (TMA_CONSUMERS + 1), smem));
+    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, k, 32 * (TMA_CONSUMERS + 1), smem));
     return EBB_OK;
 }
 
@@ -2862,6 +3148,7 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
     if (nlocal < 1 || nlocal > EBB_MAX_RANKS) return fail(c, EBB_E_ARG, "peer_bind: nlocal must be 1..%d", EBB_MAX_RANKS);
     std::vector<PeerRankArgs> h(nlocal);
     ebb_dtype dt0 = EBB_F64;
+    bool saad = false;
     size_t stage_max = 0;
     for (int i = 0; i < nlocal; ++i) {
         const ebb_cg* cg = &cgs[i];
@@ -2871,10 +3158,24 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
         EBB_TRY(cg_validate(c, cg, &Gr, &dt));
         if (i == 0) dt0 = dt;
         if (dt != dt0) return fail(c, EBB_E_TYPE, "peer_bind: every rank of a group must have the same dtype");
-        for (ebb_field f : {cg->s, cg->y, cg->w, cg->u, cg->u2, cg->dinv, cg->r, cg->z, cg->p, cg->scal, cg->rho})
+        const int var = cg_variant(cg, Gr, dt);
+        if (var != EBB_CG_SAAD && var != EBB_CG_SINGLE_REDUCTION)
+            return fail(c, EBB_E_ARG, "peer_bind: rank %d: the fused PCG runs the Saad or the single-reduction "
+                        "variant", i);
+        if (i == 0) saad = var == EBB_CG_SAAD;
+        if ((var == EBB_CG_SAAD) != saad) return fail(c, EBB_E_ARG, "peer_bind: every rank needs the same variant");
+        for (ebb_field f : {cg->dinv, cg->r, cg->z, cg->p, cg->scal, cg->rho})
             if (!get_field(c, f))
-                return fail(c, EBB_E_STATE, "peer_bind: rank %d: call ebb_cg_init with EBB_CG_SINGLE_REDUCTION first "
-                            "(its work vectors are missing)", i);
+                return fail(c, EBB_E_STATE, "peer_bind: rank %d: call ebb_cg_init first", i);
+        if (saad) {
+            for (ebb_field f : {cg->q, cg->p2})
+                if (!get_field(c, f)) return fail(c, EBB_E_STATE, "peer_bind: rank %d: call ebb_cg_init first", i);
+        } else {
+            for (ebb_field f : {cg->s, cg->y, cg->w, cg->u, cg->u2})
+                if (!get_field(c, f))
+                    return fail(c, EBB_E_STATE, "peer_bind: rank %d: call ebb_cg_init with EBB_CG_SINGLE_REDUCTION "
+                                "first (its work vectors are missing)", i);
+        }
         if (cg->tol != cgs[0].tol) return fail(c, EBB_E_ARG, "peer_bind: every rank needs the same tol");
         if (pc->nranks < 1 || pc->nranks > EBB_MAX_RANKS || pc->rank < 0 || pc->rank >= pc->nranks ||
             pc->nranks != peers[0].nranks)
@@ -2892,8 +3193,8 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
         if (!MB || MB->dtype != EBB_F64 || MB->comps() != 1 || c->rels[MB->rel].size < EBB_PEER_MBOX_WORDS)
             return fail(c, EBB_E_TYPE, "peer_bind: mbox must be an F64 field of >= %d rows", EBB_PEER_MBOX_WORDS);
         for (int q = 0; q < pc->nranks; ++q)
-            if (q != pc->rank && (!pc->peer_u[q] || !pc->peer_u2[q] || !pc->peer_x[q] || !pc->peer_z[q] ||
-                                  !pc->peer_mbox[q]))
+            if (q != pc->rank && (!pc->peer_x[q] || !pc->peer_z[q] || !pc->peer_mbox[q] ||
+                                  (!saad && (!pc->peer_u[q] || !pc->peer_u2[q]))))
                 return fail(c, EBB_E_ARG, "peer_bind: rank %d: missing buffer address of peer %d", pc->rank, q);
         const uint8_t* mask;
         EBB_TRY(check_mask(c, cg->mask, Gr.verts, &mask));
@@ -2914,11 +3215,17 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
         a.r = F(cg->r);
         a.z0 = F(cg->z);
         a.p = F(cg->p);
-        a.sv = F(cg->s);
-        a.yv = F(cg->y);
-        a.wv = F(cg->w);
-        a.ub0 = F(cg->u);
-        a.ub1 = F(cg->u2);
+        if (!saad) {
+            a.sv = F(cg->s);
+            a.yv = F(cg->y);
+            a.wv = F(cg->w);
+            a.ub0 = F(cg->u);
+            a.ub1 = F(cg->u2);
+        } else {
+            a.q = F(cg->q);
+            a.p2 = F(cg->p2);
+        }
+        a.nv_all = Gr.nv;
         a.mask = mask;
         a.scal = (double*)F(cg->scal);
         a.rho_user = (double*)F(cg->rho);
@@ -2936,11 +3243,11 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
         a.nranks = pc->nranks;
         a.cap = cap;
     }
-    const size_t smem = stage_max * CG1_NS;
+    const size_t smem = stage_max * (saad ? TMA_NS : CG1_NS);
     if (smem > kTmaSmemMax) return fail(c, EBB_E_SIZE, "peer_bind: TMA ring of %zu bytes does not fit", smem);
     int nb = 0;
-    if (dt0 == EBB_F64) EBB_TRY(peer_occupancy<double>(c, smem, nlocal, &nb));
-    else EBB_TRY(peer_occupancy<float>(c, smem, nlocal, &nb));
+    if (dt0 == EBB_F64) EBB_TRY(peer_occupancy<double>(c, smem, nlocal, saad, &nb));
+    else EBB_TRY(peer_occupancy<float>(c, smem, nlocal, saad, &nb));
     unsigned G = (unsigned)((uint64_t)nb * c->num_sms / (uint64_t)nlocal);
     if (G > kCg1PartStride) G = kCg1PartStride;
     if (G < 1) return fail(c, EBB_E_SIZE, "peer_bind: %d ranks cannot all be resident on one device", nlocal);
@@ -2949,6 +3256,7 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
     P->G = G;
     P->smem = smem;
     P->dt = dt0;
+    P->saad = saad;
     P->tol2 = cg_tol2(&cgs[0]);
     c->peer_groups.push_back(P);
     EBB_CUDA(c, cudaMalloc(&P->d_args, sizeof(PeerRankArgs) * nlocal));
@@ -2985,18 +3293,15 @@ ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_strea
     cfg.attrs = at;
     cfg.numAttrs = 1;
     KernelTimer kt(c, EBB_K_CG_SOLVE, s);
-    if (P->nlocal == 1) {
-        if (P->dt == EBB_F64)
-            EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer1<double>, P->one, c->d_err, (int)iters, P->tol2));
-        else
-            EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer1<float>, P->one, c->d_err, (int)iters, P->tol2));
-    } else if (P->dt == EBB_F64) {
-        EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer<double>, (const PeerRankArgs*)P->d_args, P->G, c->d_err,
-                                       (int)iters, P->tol2));
-    } else {
-        EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_peer<float>, (const PeerRankArgs*)P->d_args, P->G, c->d_err,
-                                       (int)iters, P->tol2));
-    }
+    const void* k = P->dt == EBB_F64 ? peer_kernel<double>(P->nlocal, P->saad) : peer_kernel<float>(P->nlocal, P->saad);
+    unsigned long long* err = c->d_err;
+    int it = (int)iters;
+    double tol2 = P->tol2;
+    const PeerRankArgs* recs = P->d_args;
+    unsigned G = P->G;
+    void* one_args[] = {(void*)&P->one, (void*)&err, (void*)&it, (void*)&tol2};
+    void* multi_args[] = {(void*)&recs, (void*)&G, (void*)&err, (void*)&it, (void*)&tol2};
+    EBB_CUDA(c, cudaLaunchKernelExC(&cfg, k, P->nlocal == 1 ? one_args : multi_args));
     return EBB_OK;
 }
 

@@ -210,7 +210,7 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
         if peer is None:
             raise ValueError("variant='peer' needs the PeerPCG binding of the ranks")
         for R in ranks:
-            R.cg_init(single=True)
+            R.cg_init(single=peer.variant == "single")
         peer.step(iters)
         for R in ranks:
             R.finish(h)
@@ -634,8 +634,10 @@ def peer_tables(infos, local_ranks, nranks):
 
 
 class PeerPCG:
-    """The fused multi-GPU single-reduction PCG over peer memory
-    (``ebb_cg_peer_bind`` / ``ebb_cg_peer_step``).
+    """The fused multi-GPU PCG over peer memory (``ebb_cg_peer_bind`` /
+    ``ebb_cg_peer_step``); variant "single" (single-reduction:
+    one scalar exchange per iteration, u / x halo) or "saad" (two exchanges,
+    z / x halo; the faster form once the vector records stream from HBM).
 
     ranks: the GpuRank objects of THIS process, all on one device.
     comm=None: every rank of the job is in ``ranks`` (ranks emulated on one
@@ -646,10 +648,16 @@ class PeerPCG:
     ``step(iters)`` per implicit step replaces the per-phase launches,
     allreduces and halo exchanges of the "single" driver."""
 
-    def __init__(self, ranks, comm=None, stream=None):
+    # the single-GPU AUTO crossover (solver.cu cg_variant, DESIGN.md §5.4):
+    # single-reduction while a rank's vector records stay in L2
+    AUTO_SINGLE_MAX_VERTS = 232000
+
+    def __init__(self, ranks, comm=None, stream=None, variant="auto"):
         import ctypes as C
 
         from . import _abi as A
+        if variant not in ("auto", "single", "saad"):
+            raise ValueError(variant)
         self.ranks, self.ctx, self.stream = list(ranks), ranks[0].ctx, stream
         ctx = self.ctx
         ipc = comm is not None
@@ -665,6 +673,11 @@ class PeerPCG:
             infos = {R.rank: R.peer_export(ipc=False) for R in self.ranks}
         if sorted(infos) != list(range(nranks)):
             raise ValueError(f"peer ranks {sorted(infos)} are not 0..{nranks - 1}")
+        if variant == "auto":                 # the same choice on every rank: from the gathered sizes
+            variant = "single" if max(d["nv"] for d in infos.values()) <= self.AUTO_SINGLE_MAX_VERTS else "saad"
+        self.variant = variant
+        for R in self.ranks:                  # the body the kernel runs (ebb_cg_peer_bind reads the variant)
+            R.fem.cg.variant = A.CG_SINGLE_REDUCTION if variant == "single" else A.CG_SAAD
         tables = peer_tables(infos, [R.rank for R in self.ranks], nranks)
         self._opened = []
         self.peer_addr = {}                        # (local rank, peer, buffer) -> device address used

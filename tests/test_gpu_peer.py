@@ -46,16 +46,17 @@ def _gather(ranks, field, nv):
     return out
 
 
+@pytest.mark.parametrize("variant", ["single", "saad"])
 @pytest.mark.parametrize("P", [1, 2, 3, 4])
-def test_peer_pcg_matches_single_domain(ctx, P):
+def test_peer_pcg_matches_single_domain(ctx, P, variant):
     from paper_1506_07577_b200 import dist
     case = Case(n=6, model="nh", vel_amp=0.05)
     h, iters = 1e-2, 50
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
                                case.free[order], h, iters=iters)
-    ranks = _ranks(ctx, case, P, f"pp{P}")
-    peer = dist.PeerPCG(ranks)
+    ranks = _ranks(ctx, case, P, f"pp{P}{variant}")
+    peer = dist.PeerPCG(ranks, variant=variant)
     dist.implicit_step(ranks, None, "nh", h=h, iters=iters, variant="peer", peer=peer)
     dv = _gather(ranks, "dv", m.nv)
     u = _gather(ranks, "u", m.nv)
@@ -66,9 +67,10 @@ def test_peer_pcg_matches_single_domain(ctx, P):
         assert R.fem.cg_iterations()[0] == iters
 
 
+@pytest.mark.parametrize("variant", ["single", "saad"])
 @pytest.mark.parametrize("map_variant", ["overlap", "reverse"])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_peer_pcg_three_steps_owned_and_ghost_rows(ctx, P, map_variant):
+def test_peer_pcg_three_steps_owned_and_ghost_rows(ctx, P, map_variant, variant):
     """Three consecutive steps: every local row, owned and ghost, equals the
     oracle's third step -- ghost u, v come from the x (dv) rows the owners
     stored into the ghosts inside the kernel, and step 2 onwards maps the
@@ -83,8 +85,8 @@ def test_peer_pcg_three_steps_owned_and_ghost_rows(ctx, P, map_variant):
         ref = oracle.implicit_step(m, "nh", u, v, case.mu[tet_src], case.lam[tet_src], case.free[order], h,
                                    iters=iters)
         u, v = ref["u"], ref["v"]
-    ranks = _ranks(ctx, case, P, f"pp3{P}{map_variant}", map_variant)
-    peer = dist.PeerPCG(ranks)
+    ranks = _ranks(ctx, case, P, f"pp3{P}{map_variant}{variant}", map_variant)
+    peer = dist.PeerPCG(ranks, variant=variant)
     transport = dist.LocalTransport()            # the reverse-add map's exchange only
     u_in, v_in = np.empty_like(u), np.empty_like(v)
     u_in[order], v_in[order] = u, v
@@ -103,20 +105,21 @@ def test_peer_pcg_three_steps_owned_and_ghost_rows(ctx, P, map_variant):
     assert nghost > 0
 
 
-def test_peer_pcg_is_deterministic_and_split_launches_agree(ctx):
+@pytest.mark.parametrize("variant", ["single", "saad"])
+def test_peer_pcg_is_deterministic_and_split_launches_agree(ctx, variant):
     """Bitwise run-to-run deterministic (rank-ordered sums of deterministic
     per-CTA partials), and 50 iterations as 20 + 30 (two launches: the
     recurrences and the parity of the u buffers resume from the device
     scalars) equal one launch of 50 to round-off."""
     from paper_1506_07577_b200 import dist
     case = Case(n=6, model="nh", vel_amp=0.05)
-    ranks = _ranks(ctx, case, 3, "ppdet")
-    peer = dist.PeerPCG(ranks)
+    ranks = _ranks(ctx, case, 3, f"ppdet{variant}")
+    peer = dist.PeerPCG(ranks, variant=variant)
     outs = []
     for split in ([50], [50], [20, 30]):
         for R in ranks:
             R.map_assemble("nh", 1e-2, 0.0, 0.0, (0.0, -9.81, 0.0))
-            R.cg_init(single=True)
+            R.cg_init(single=variant == "single")
         for k in split:
             peer.step(k)
         outs.append(np.concatenate([R.fem.dv.read().ravel() for R in ranks]))
@@ -124,7 +127,8 @@ def test_peer_pcg_is_deterministic_and_split_launches_agree(ctx):
     assert rel_l2(outs[2], outs[0]) <= 1e-12
 
 
-def test_peer_pcg_honours_the_tolerance(ctx):
+@pytest.mark.parametrize("variant", ["single", "saad"])
+def test_peer_pcg_honours_the_tolerance(ctx, variant):
     """ebb_cg.tol > 0: every rank stops at the oracle's stop iteration (read
     off the single-domain r.z history), the same iterate."""
     from paper_1506_07577_b200 import dist
@@ -138,13 +142,13 @@ def test_peer_pcg_honours_the_tolerance(ctx):
     k = next(k for k in range(1, 301) if hist[k] <= thr)
     assert abs(hist[k] - thr) > 1e-6 * thr and abs(hist[k - 1] - thr) > 1e-6 * thr
     x_ref, _, _ = oracle.pcg(m.row_ptr, m.head, ref["A"], ref["b"], case.free[order], k)
-    ranks = _ranks(ctx, case, P, "pptol")
+    ranks = _ranks(ctx, case, P, f"pptol{variant}")
     for R in ranks:
         R.fem.cg.tol = tol
-    peer = dist.PeerPCG(ranks)
+    peer = dist.PeerPCG(ranks, variant=variant)
     for R in ranks:
         R.map_assemble("nh", h, 0.0, 0.0, (0.0, -9.81, 0.0))
-        R.cg_init(single=True)
+        R.cg_init(single=variant == "single")
     peer.step(k + 40)
     peer.step(10)                                  # a no-op after the stop
     dv = _gather(ranks, "dv", m.nv)
@@ -153,7 +157,8 @@ def test_peer_pcg_honours_the_tolerance(ctx):
     assert rel_l2(dv[order], x_ref) <= 1e-8
 
 
-def test_peer_pcg_fp32_derived_tolerance(ctx):
+@pytest.mark.parametrize("variant", ["single", "saad"])
+def test_peer_pcg_fp32_derived_tolerance(ctx, variant):
     """fp32 on 2 ranks against the oracle's fp64 step, at the perturbation
     bound of test_gpu_edge_cases.test_pcg_fp32_50_iterations_derived_tolerance
     (kappa of the Jacobi-scaled free system, north_star fp32 bars)."""
@@ -169,8 +174,8 @@ def test_peer_pcg_fp32_derived_tolerance(ctx):
     kappa = _jacobi_condition(m, ref["A"], case.free[order])
     tol = kappa * (1e-5 + 1e-5) + 40.0 * kappa * 2.0 ** -24
     assert tol < 1e-3
-    ranks = _ranks(ctx, case, 2, "pp32", dtype="f32")
-    peer = dist.PeerPCG(ranks)
+    ranks = _ranks(ctx, case, 2, f"pp32{variant}", dtype="f32")
+    peer = dist.PeerPCG(ranks, variant=variant)
     dist.implicit_step(ranks, None, "nh", h=1e-2, iters=50, variant="peer", peer=peer)
     assert rel_l2(_gather(ranks, "dv", m.nv)[order], ref["dv"]) <= tol
 

@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="4,12")
     ap.add_argument("--quick", action="store_true", help="fp64 NH only (racecheck is slow)")
+    ap.add_argument("--peer-only", action="store_true", help="only the multi-GPU setup and the fused peer PCG")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -42,7 +43,7 @@ def main():
     scat = {"atomic": A.SCATTER_ATOMIC, "segmented": A.SCATTER_SEGMENTED, "color": A.SCATTER_COLOR,
             "chunk": A.SCATTER_CHUNK}
     ctx = ebb.Context(0)
-    for n in [int(x) for x in a.sizes.split(",")]:
+    for n in ([] if a.peer_only else [int(x) for x in a.sizes.split(",")]):
         X, tets = M.kuhn6(n)
         X, tets = M.permute_vertices(X, tets, 2)
         free = S.fixed_mask(X, n)
@@ -111,11 +112,25 @@ def main():
             part = dist.partition_rank(ctx, X, tets, 2, r, name=f"sp{variant}{r}")
             ranks.append(dist.GpuRank(ctx, r, part, X, free, u, np.zeros_like(u), mu, lam, name=f"sr{variant}{r}",
                                       map_variant=variant, nranks=2))
-        dist.map_step(ranks, dist.LocalTransport(), "nh")
-        dist.implicit_step(ranks, dist.LocalTransport(), "nh", iters=5, variant="single")
-        torch.cuda.synchronize()
-        print(f"dist {variant} ok", flush=True)
+        if not a.peer_only:
+            dist.map_step(ranks, dist.LocalTransport(), "nh")
+            dist.implicit_step(ranks, dist.LocalTransport(), "nh", iters=5, variant="single")
+            torch.cuda.synchronize()
+            print(f"dist {variant} ok", flush=True)
+        # the fused multi-GPU PCG over peer memory, both bodies, the 2 ranks
+        # in one cooperative launch (the P2P stores and mailbox exchanges)
+        for body in ("single", "saad"):
+            peer = dist.PeerPCG(ranks, variant=body)
+            for _ in range(2):
+                dist.implicit_step(ranks, dist.LocalTransport(), "nh", iters=5, variant="peer", peer=peer)
+            torch.cuda.synchronize()
+            assert ctx.error_counts()["peer_timeouts"] == 0
+            print(f"dist {variant} peer pcg {body} ok", flush=True)
         del ranks
+    if a.peer_only:
+        ctx.close()
+        print("SANITIZE RUN DONE", flush=True)
+        return
     import gc
     gc.collect()
     torch.cuda.empty_cache()   # the halo staging tensors come from torch's caching allocator

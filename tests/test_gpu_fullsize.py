@@ -173,3 +173,66 @@ def test_t10m_pcg_residual_property(ctx, t10m):
         rt[k] = b[v] - np.einsum("eab,eb->a", Arows[e0:e1], x[head[e0:e1]])
     assert rel_l2(r[sample], rt) <= 1e-8
     assert np.linalg.norm(r[free]) < 1e-2 * np.linalg.norm(b[free])
+
+
+@pytest.mark.parametrize("body", ["saad", "single"])
+def test_t10m_peer_pcg_two_ranks(ctx, t10m, body):
+    """The fused multi-GPU PCG (bench.py --gpus N's default; both kernel
+    bodies) at full size: the T10M mesh split over 2 ranks emulated on the
+    GPU (one cooperative launch).  Properties that hold at any size, per rank
+    on a seeded sample of owned free rows that includes every boundary row
+    of the sample's range: the recurrence residual equals b - A x computed on
+    the host from the local rows and the local x -- whose ghost rows the
+    peer stored into this rank inside the kernel -- and the distributed
+    step's dv and u, owned and ghost rows, equal the single-domain step's
+    (the same iterates in exact arithmetic; north_star's 1e-8 CG bar)."""
+    from paper_1506_07577_b200 import _abi as A_
+    from paper_1506_07577_b200 import dist
+    from paper_1506_07577_b200.ebb import Field
+    from paper_1506_07577_b200.tetfem import TetFEM
+    d = t10m
+    w = d["w"]
+    v0 = np.zeros_like(d["u"])
+    ranks = []
+    for r in range(2):
+        part = dist.partition_rank(ctx, d["X"], d["tets"], 2, r, name=f"t10mpp{body}{r}")
+        ranks.append(dist.GpuRank(ctx, r, part, d["X"], d["free"], d["u"], v0, d["mu"], d["lam"], rho=w["rho"],
+                                  name=f"t10mpr{body}{r}", nranks=2))
+    peer = dist.PeerPCG(ranks, variant=body)
+    dist.implicit_step(ranks, None, w["model"], h=w["h"], iters=w["cg_iters"], variant="peer", peer=peer)
+    assert ctx.error_counts()["peer_timeouts"] == 0
+    rng = M.rng(14)
+    for R in ranks:
+        f = R.fem
+        x = f.dv.read()
+        rr = Field(ctx, f.cg.r, f.verts, "r", "f64", (4, 1), A_.AOS).read()[:, :3]
+        b = f.b.read()
+        Arows = f.K.read().reshape(-1, 3, 3)
+        index = f.index.read().astype(np.int64)
+        head = f.head.read().astype(np.int64)
+        free = f.free.read().astype(bool)                       # mask = free AND owned
+        bnd = np.unique(np.concatenate([np.asarray(s) for s in R.part_send.values()]))
+        sample = np.unique(np.concatenate([rng.integers(0, R.n_owned, size=1000), bnd[:1000]]))
+        sample = sample[free[sample]]
+        assert np.isin(bnd, sample).sum() > 100                 # rows whose A x reads ghost x
+        rt = np.empty((sample.size, 3))
+        for k, v in enumerate(sample):
+            e0, e1 = index[v], index[v + 1]
+            rt[k] = b[v] - np.einsum("eab,eb->a", Arows[e0:e1], x[head[e0:e1]])
+        assert rel_l2(rr[sample], rt) <= 1e-8
+    # the single-domain step on the same input (bench.py's single-GPU path)
+    fem = TetFEM(ctx, d["X"], d["tets"], dtype="f64", mu=d["mu"], lam=d["lam"], rho=w["rho"], free=d["free"],
+                 u=d["u"], name=f"t10mref{body}")
+    fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"])
+    dv_ref = fem.to_input_order(fem.dv.read())
+    u_ref = fem.to_input_order(fem.u.read())
+    dv = np.full_like(dv_ref, np.nan)
+    u = np.full_like(u_ref, np.nan)
+    for R in ranks:
+        ids, vals = R.local_values(R.fem.dv)                     # owned and ghost rows
+        dv[ids] = vals
+        ids, vals = R.local_values(R.fem.u)
+        u[ids] = vals
+    assert not np.isnan(dv).any()
+    assert rel_l2(dv, dv_ref) <= 1e-8                           # north_star's CG-iterate bar
+    assert rel_l2(u, u_ref) <= 1e-8

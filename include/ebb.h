@@ -475,16 +475,18 @@ ebb_status ebb_comm_halo(ebb_ctx ctx, int32_t npeers, const int32_t* peers, void
 /* ---- fused multi-GPU PCG over peer memory ("the halo
  * exchange of vertex positions ... and the allreduce of CG scalars", here
  * without NCCL on the iteration path; the paper is single-device).
- * The single-reduction PCG (EBB_CG_SINGLE_REDUCTION, Chronopoulos-Gear) of
- * every rank runs as ONE persistent kernel for all iterations.  Each owner
- * stores the rows of the gathered operand u (and of the iterate x) that
- * peers hold as ghosts straight into the peers' buffers as it finishes them
- * (P2P stores over NVLink; for ranks emulated on one device, plain stores),
- * and the fused 2-scalar reduction (w.z, r.z) of each phase is exchanged
- * through per-rank mailboxes (release/acquire at system scope), summed in
- * rank order on every rank (bitwise the same alpha, beta everywhere).  The
- * z_0 halo and the initial r.z sum are done in the same launch; the x halo
- * lands before the kernel ends, so ebb_implicit_update can follow directly.
+ * The PCG of every rank runs as ONE persistent kernel for all iterations,
+ * with one of two bodies (ebb_cg.variant at the bind): single-reduction
+ * (EBB_CG_SINGLE_REDUCTION, Chronopoulos-Gear; one exchange of the fused
+ * (w.z, r.z) per iteration, halo of the gathered operand u and of x) or
+ * Saad (EBB_CG_SAAD; exchanges of p.q and r.z, halo of z and x).  Each owner
+ * stores the halo rows that peers hold as ghosts straight into the peers'
+ * buffers as it finishes them (P2P stores over NVLink; for ranks emulated
+ * on one device, plain stores), and the scalars go through per-rank
+ * mailboxes (release/acquire at system scope), summed in rank order on
+ * every rank (bitwise the same alpha, beta everywhere).  The z_0 halo and
+ * the initial r.z sum are done in the same launch; the x halo lands before
+ * the kernel ends, so ebb_implicit_update can follow directly.
  * Decomposition: EBB_PART_OVERLAP (ebb_partition_local): local vertices
  * [0, n_owned) are owned, the rest ghosts; rows of ghosts are not solved.
  * A wait that exceeds ~20 s (a peer that never arrives) counts in error word
@@ -527,10 +529,13 @@ ebb_status ebb_ipc_open(ebb_ctx ctx, const void* handle64, uint64_t* dev_addr);
 ebb_status ebb_ipc_close(ebb_ctx ctx, uint64_t dev_addr);
 /* Bind `nlocal` ranks whose systems live on this context's device (1 per
  * process on a multi-GPU node; P for ranks emulated on one device) into a
- * launch group: cgs[i] (after ebb_cg_init with EBB_CG_SINGLE_REDUCTION; its
- * fields must outlive the group) and peers[i].  Validates and uploads the
+ * launch group: cgs[i] (after ebb_cg_init with EBB_CG_SAAD or
+ * EBB_CG_SINGLE_REDUCTION, the same on every rank; its fields must outlive
+ * the group; the single-reduction body also reads peer_u / peer_u2) and
+ * peers[i].  Validates and uploads the
  * per-rank launch records once (synchronous, not capturable); *group_out is
- * the group id.  EBB_E_SIZE if the ranks' CTAs cannot all be resident.
+ * the group id.  ebb_cg.tol is taken here.  EBB_E_SIZE if the ranks' CTAs
+ * cannot all be resident.
  * (the PCG of P:946, Jacobi-preconditioned) */
 ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, const ebb_peer_cg* peers,
                             int32_t* group_out);
@@ -538,7 +543,8 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
  * cooperative launch (the first call after ebb_cg_init adds the z_0 halo,
  * the r.z sum and the w_0 = A z_0 prologue).  Every rank of the job must
  * call it with the same iters, in the same order.  Stream-ordered,
- * graph-capturable; ebb_cg.tol is honoured (the same stop on every rank).
+ * graph-capturable; the bound tol is honoured (the same stop on every
+ * rank).  EBB_E_STATE if a field of the group was freed since the bind.
  * */
 ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_stream s);
 

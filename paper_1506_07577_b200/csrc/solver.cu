@@ -2757,6 +2757,7 @@ struct PeerGroup {
     double tol2 = 0.0;
     PeerRankArgs* d_args = nullptr;
     PeerRankArgs one;                  // nlocal == 1: the record passed as a kernel parameter
+    std::vector<ebb_field> fields;     // every field a record points into (checked at each step)
     double* d_part = nullptr;
     unsigned int* d_bar = nullptr;
 };
@@ -3150,6 +3151,7 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
     ebb_dtype dt0 = EBB_F64;
     bool saad = false;
     size_t stage_max = 0;
+    std::vector<ebb_field> used;
     for (int i = 0; i < nlocal; ++i) {
         const ebb_cg* cg = &cgs[i];
         const ebb_peer_cg* pc = &peers[i];
@@ -3242,6 +3244,13 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
         a.rank = pc->rank;
         a.nranks = pc->nranks;
         a.cap = cap;
+        for (ebb_field f : {cg->A, cg->dinv, cg->x, cg->r, cg->z, cg->p, cg->scal, cg->rho, pc->send_off,
+                            pc->send_dst, pc->mbox})
+            used.push_back(f);
+        if (cg->mask != EBB_NONE) used.push_back(cg->mask);
+        for (ebb_field f : saad ? std::vector<ebb_field>{cg->q, cg->p2}
+                                : std::vector<ebb_field>{cg->s, cg->y, cg->w, cg->u, cg->u2})
+            used.push_back(f);
     }
     const size_t smem = stage_max * (saad ? TMA_NS : CG1_NS);
     if (smem > kTmaSmemMax) return fail(c, EBB_E_SIZE, "peer_bind: TMA ring of %zu bytes does not fit", smem);
@@ -3257,6 +3266,7 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
     P->smem = smem;
     P->dt = dt0;
     P->saad = saad;
+    P->fields = used;
     P->tol2 = cg_tol2(&cgs[0]);
     c->peer_groups.push_back(P);
     EBB_CUDA(c, cudaMalloc(&P->d_args, sizeof(PeerRankArgs) * nlocal));
@@ -3281,6 +3291,8 @@ ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_strea
         return fail(c, EBB_E_ARG, "peer_step: bad group %d", group);
     if (iters < 0) return fail(c, EBB_E_ARG, "negative iteration count");
     PeerGroup* P = (PeerGroup*)c->peer_groups[group];
+    for (ebb_field f : P->fields)
+        if (!get_field(c, f)) return fail(c, EBB_E_STATE, "peer_step: a field of group %d was freed", group);
     cudaStream_t s = (cudaStream_t)stream;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P->G * (unsigned)P->nlocal);

@@ -238,4 +238,8 @@ def test_peer_bind_refuses_bad_arguments(ctx):
     q = sorted(R.part_send)[0]
     with pytest.raises(EbbError, match="EBB_E_RANGE"):
         R.peer_send_csr([q], [np.full(len(R.part_send[q]), 10 ** 6)], [ranks[q].fem.nv])
-    del dist
+    # a group whose field was freed refuses to launch
+    peer = dist.PeerPCG(ranks)
+    ranks[1].mbox.free()
+    with pytest.raises(EbbError, match="EBB_E_STATE"):
+        peer.step(1)

@@ -171,6 +171,68 @@ def bytes_cg_iter(V, E, bf=8):
     return bytes_matvec(V, E, bf) + V * 3 * bf * 11
 
 
+def _e2e_pipelined(ctx, fem, stream, flush, run_step, u_h, v_h, steps, dev):
+    """Device time (ms, CUDA events on the compute stream) of `steps`
+    end-to-end steps with the host copies overlapped (see run_ours)."""
+    import numpy as np
+    import torch
+    V = fem.nv
+    nb = V * 3 * 8
+    S = ctx.relation("e2e.stage", V)
+    sin = [(S.field(f"u_in{i}", "f64", (3, 1)), S.field(f"v_in{i}", "f64", (3, 1))) for i in range(2)]
+    sout = [(S.field(f"u_out{i}", "f64", (3, 1)), S.field(f"v_out{i}", "f64", (3, 1))) for i in range(2)]
+    host_out = [(torch.empty((V, 3), dtype=torch.float64, pin_memory=True),
+                 torch.empty((V, 3), dtype=torch.float64, pin_memory=True)) for _ in range(2)]
+    copy = torch.cuda.Stream(device=dev)
+    ev = lambda: torch.cuda.Event()                          # noqa: E731
+    staged, used, ready, drained = [ev(), ev()], [ev(), ev()], [ev(), ev()], [ev(), ev()]
+    used_rec, drained_rec = [False, False], [False, False]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def h2d(slot):
+        su, sv = sin[slot]
+        if used_rec[slot]:
+            copy.wait_event(used[slot])                      # the step that read this slot has copied it out
+        su.write_async(u_h.data_ptr(), nb, copy)
+        sv.write_async(v_h.data_ptr(), nb, copy)
+        staged[slot].record(copy)
+
+    torch.cuda.synchronize()
+    t0.record(stream)
+    copy.wait_event(t0)
+    h2d(0)
+    for k in range(steps):
+        s_ = k % 2
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        stream.wait_event(staged[s_])
+        fem.u.copy_from(sin[s_][0], stream)
+        fem.vel.copy_from(sin[s_][1], stream)
+        used[s_].record(stream)
+        used_rec[s_] = True
+        if k + 1 < steps:
+            h2d((k + 1) % 2)
+        run_step()
+        if drained_rec[s_]:
+            stream.wait_event(drained[s_])                   # step k-2's result left this slot
+        sout[s_][0].copy_from(fem.u, stream)
+        sout[s_][1].copy_from(fem.vel, stream)
+        ready[s_].record(stream)
+        copy.wait_event(ready[s_])
+        sout[s_][0].read_async(host_out[s_][0].data_ptr(), nb, copy)
+        sout[s_][1].read_async(host_out[s_][1].data_ptr(), nb, copy)
+        drained[s_].record(copy)
+        drained_rec[s_] = True
+    stream.wait_stream(copy)                                 # the last result is on the host
+    t1.record(stream)
+    t1.synchronize()
+    # every step starts from (u0, v0): the last result on the host is the state
+    last = host_out[(steps - 1) % 2]
+    assert np.array_equal(last[0].numpy(), fem.u.read()) and np.array_equal(last[1].numpy(), fem.vel.read())
+    S.free()
+    return t0.elapsed_time(t1)
+
+
 def cpu_baseline(steps=CPU_BASELINE_STEPS):
     """The oracle, as it stands, on a bounded sample of the workload (1 thread)."""
     import numpy as np
@@ -418,10 +480,22 @@ def run_ours(args, rank, world, local_rank):
         b.record(stream)
         b.synchronize()
         e2e_ms += a.elapsed_time(b)
-    e2e = {"value": world * T * args.steps / (e2e_ms / 1e3), "unit": "tets/s",
-           "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
-           "api": "ebb_field_write (pinned host u0, v0) -> implicit step (TetFEM.implicit_step as captured graph) -> "
-                  "ebb_field_read (u, v)"}
+    serial = world * T * args.steps / (e2e_ms / 1e3)
+    # pipelined (how a serving loop runs it): every step's inputs still come
+    # from pinned host memory and every step's result goes back to it inside
+    # the timed region, but the copies of step k+1's inputs and of step k-1's
+    # result run on a copy stream while step k computes.  Device staging
+    # fields (two slots each way) decouple the copies from the step's own
+    # u, v, which the step reads and writes; the stage <-> state moves are
+    # device copies (ebb_field_copy) on the compute stream.
+    pe_ms = _e2e_pipelined(ctx, fem, stream, flush, run_step, u_h, v_h, args.steps, dev)
+    e2e = {"value": world * T * args.steps / (pe_ms / 1e3), "unit": "tets/s",
+           "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb, "pipelined": True,
+           "serial_value": serial,
+           "api": "per step: ebb_field_write (pinned host u0, v0 -> device stage, copy stream) -> ebb_field_copy "
+                  "(stage -> u, v) -> implicit step (TetFEM.implicit_step as captured graph) -> ebb_field_copy "
+                  "(u, v -> stage) -> ebb_field_read_async (stage -> pinned host, copy stream); the copies of "
+                  "steps k+1 / k-1 overlap step k; serial_value: the same with nothing overlapped"}
 
     # ---- roofline of the dominant kernel (largest share of the timed step)
     peak, peak_src = _peaks()
@@ -624,13 +698,18 @@ def run_dist(args, rank, world, local_rank):
         b_.record(stream)
         b_.synchronize()
         e2e_ms += a_.elapsed_time(b_)
-    tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    dist.barrier()
+    pe_ms = _e2e_pipelined(ctx, R.fem, stream, flush, lambda: step() if graph is None else
+                           ctx.graph_launch(graph, stream), u_h, v_h, args.steps, dev)
+    tt = torch.tensor([e2e_ms, pe_ms], device=dev, dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    e2e_ms = float(tt.item())
-    e2e = {"value": T_global * args.steps / (e2e_ms / 1e3), "unit": "tets/s", "h2d_bytes_per_step": 2 * nb,
-           "d2h_bytes_per_step": 2 * nb,
-           "api": "per rank: ebb_field_write (pinned host local u0, v0) -> distributed implicit step (graph replay) "
-                  "-> ebb_field_read (u, v); bytes of this rank"}
+    e2e_ms, pe_ms = float(tt[0].item()), float(tt[1].item())
+    e2e = {"value": T_global * args.steps / (pe_ms / 1e3), "unit": "tets/s", "h2d_bytes_per_step": 2 * nb,
+           "d2h_bytes_per_step": 2 * nb, "pipelined": True,
+           "serial_value": T_global * args.steps / (e2e_ms / 1e3),
+           "api": "per rank: ebb_field_write (pinned host local u0, v0 -> stage, copy stream) -> ebb_field_copy -> "
+                  "distributed implicit step (graph replay) -> ebb_field_copy -> ebb_field_read_async (copy "
+                  "stream), the copies of steps k+1 / k-1 overlapping step k; bytes of this rank; max over ranks"}
     peak, peak_src = _peaks()
     E_loc = R.fem.ne
     # single: one launch = one PCG iteration of the local rows (the prologue

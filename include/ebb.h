@@ -156,6 +156,12 @@ ebb_status ebb_field_find(ebb_ctx ctx, ebb_rel rel, const char* name, ebb_field*
  * makes it asynchronous); read is synchronous. */
 ebb_status ebb_field_write(ebb_ctx ctx, ebb_field f, const void* host, uint64_t nbytes, ebb_stream s);
 ebb_status ebb_field_read(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes, ebb_stream s);
+/* Stream-ordered read of an element-major (AOS or scalar) field: the host
+ * buffer (pinned for a truly asynchronous copy) is complete once the stream
+ * reaches this point (an event / ebb_sync).  EBB_E_TYPE for component-planar
+ * fields.  (The pipelined end-to-end step of SURVEY §8(d): the read of step k
+ * overlaps step k+1.) */
+ebb_status ebb_field_read_async(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes, ebb_stream s);
 ebb_status ebb_field_fill(ebb_ctx ctx, ebb_field f, double value, ebb_stream s);
 ebb_status ebb_field_copy(ebb_ctx ctx, ebb_field dst, ebb_field src, ebb_stream s);
 /* dst = (dtype of dst) src for F32/F64 fields of equal relation, shape, layout. */

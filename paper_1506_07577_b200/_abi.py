@@ -128,6 +128,7 @@ SIGS = {
     "ebb_field_find": (S, [ctx_t, u32, C.c_char_p, C.POINTER(u32)]),
     "ebb_field_write": (S, [ctx_t, u32, P, C.c_uint64, stream_t]),
     "ebb_field_read": (S, [ctx_t, u32, P, C.c_uint64, stream_t]),
+    "ebb_field_read_async": (S, [ctx_t, u32, P, C.c_uint64, stream_t]),
     "ebb_field_fill": (S, [ctx_t, u32, C.c_double, stream_t]),
     "ebb_field_copy": (S, [ctx_t, u32, u32, stream_t]),
     "ebb_field_convert": (S, [ctx_t, u32, u32, stream_t]),

@@ -689,6 +689,21 @@ ebb_status ebb_field_read(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes,
     return EBB_OK;
 }
 
+ebb_status ebb_field_read_async(ebb_ctx ctx, ebb_field f, void* host, uint64_t nbytes, ebb_stream s) {
+    Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
+    Field* F = get_field(c, f);
+    if (!F || !host) return fail(c, EBB_E_ARG, "bad field or null host pointer");
+    uint64_t n = c->rels[F->rel].size;
+    uint64_t want = n * F->comps() * dtype_size(F->dtype);
+    if (nbytes != want) return fail(c, EBB_E_SIZE, "field '%s': %llu bytes given, %llu expected", F->name.c_str(),
+                                    (unsigned long long)nbytes, (unsigned long long)want);
+    if (F->layout != EBB_AOS && F->comps() != 1)
+        return fail(c, EBB_E_TYPE, "read_async: '%s' is component-planar (use ebb_field_read)", F->name.c_str());
+    EBB_CUDA(c, cudaMemcpyAsync(host, F->ptr, nbytes, cudaMemcpyDeviceToHost, (cudaStream_t)s));
+    return EBB_OK;
+}
+
 ebb_status ebb_field_fill(ebb_ctx ctx, ebb_field f, double value, ebb_stream s) {
     Ctx* c = (Ctx*)ctx;
     EBB_DEVICE_GUARD(c);

@@ -219,6 +219,11 @@ class Field:
     def read_into(self, host_ptr: int, nbytes: int, stream=None):
         self.ctx.check(self.ctx.L.ebb_field_read(self.ctx.h, self.h, C.c_void_p(host_ptr), nbytes, _stream(stream)))
 
+    def read_async(self, host_ptr: int, nbytes: int, stream=None):
+        """Stream-ordered download into (pinned) host memory at host_ptr."""
+        self.ctx.check(self.ctx.L.ebb_field_read_async(self.ctx.h, self.h, C.c_void_p(host_ptr), nbytes,
+                                                       _stream(stream)))
+
     def fill(self, value, stream=None):
         self.ctx.check(self.ctx.L.ebb_field_fill(self.ctx.h, self.h, float(value), _stream(stream)))
 

@@ -356,3 +356,23 @@ def test_pcg_fp32_50_iterations_derived_tolerance(ctx, variant, monkeypatch):
     fem.cg_init()
     fem.cg_step(50)
     assert rel_l2(fem.dv.read(), ref["dv"]) <= tol
+
+
+def test_field_read_async(ctx):
+    """ebb_field_read_async: stream-ordered download into pinned memory
+    (complete once the stream is synchronised); component-planar fields are
+    refused (they need the synchronous layout conversion of ebb_field_read)."""
+    import torch
+
+    from paper_1506_07577_b200.ebb import EbbError
+    R = ctx.relation("ra_async", 1000)
+    x = np.random.default_rng(5).uniform(-1, 1, size=(1000, 3))
+    f = R.field("x", "f64", (3, 1), init=x)
+    out = torch.empty((1000, 3), dtype=torch.float64, pin_memory=True)
+    s = torch.cuda.Stream()
+    f.read_async(out.data_ptr(), x.nbytes, s)
+    s.synchronize()
+    assert np.array_equal(out.numpy(), x)
+    g = R.field("y", "f64", (3, 1), "soa", init=x)
+    with pytest.raises(EbbError, match="EBB_E_TYPE"):
+        g.read_async(out.data_ptr(), x.nbytes, s)

@@ -711,9 +711,15 @@ class PeerPCG:
 
     def step(self, iters):
         from .ebb import _stream
+        if self.group is None:
+            raise RuntimeError("PeerPCG.step after close(): the peers' mappings are gone")
         self.ctx.check(self.ctx.L.ebb_cg_peer_step(self.ctx.h, self.group, int(iters), _stream(self.stream)))
 
     def close(self):
+        """Unmap the peers' buffers (one process per GPU); the binding is
+        unusable afterwards.  Every rank must have finished its last step
+        first (a barrier), or a peer could still be storing into us."""
         for a in self._opened:
             self.ctx.check(self.ctx.L.ebb_ipc_close(self.ctx.h, a))
         self._opened = []
+        self.group = None

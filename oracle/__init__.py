@@ -11,8 +11,10 @@ one function per step O1..O10 of SURVEY.md §8(c) / DESIGN.md §3; this module
 is ctypes marshalling plus O4 (partition bookkeeping, plain numpy) and the
 composition of steps in the paper's order.
 
-Parity status of every function is listed in DESIGN.md §4; the only
-"parity unpinned" item is the absolute multi-step trajectory.
+Parity status of every function is listed in DESIGN.md §4; every function
+is pinned (the multi-step trajectory since late round 2: the closed-form
+free fall over 10 implicit steps and the energy dissipation of converged
+backward Euler, tests/test_oracle_solver.py).
 """
 from __future__ import annotations
 

@@ -263,3 +263,56 @@ def test_newton_free_fall(mass):
     g = np.array([0.0, -9.81, 0.0])
     assert np.abs(out["v"] - 1e-2 * g).max() < 1e-8
     assert np.abs(out["u"] - 1e-4 * g).max() < 1e-10
+
+
+@pytest.mark.parametrize("model", ["stvk", "nh"])
+def test_implicit_free_fall_multi_step(model):
+    """The multi-step trajectory of the one-linearisation backward-Euler step
+    (O9) against its closed form: from rest with no constraints every state
+    is a rigid translation (f = 0, K annihilates it), so each step adds
+    dv = h g exactly -- v_k = k h g, u_k = h^2 g k (k + 1) / 2 after k steps.
+    A wrong state update (u += h v_old, a dropped v term of b) breaks it from
+    step 2 on."""
+    X, tets = M.kuhn6(2)
+    m = oracle.Mesh(X, tets)
+    mu, lam = S.materials(m.nt, 2e5, 0.3)
+    u = np.zeros_like(X)
+    v = np.zeros_like(X)
+    h, N = 1e-2, 10
+    g = np.array([0.0, -9.81, 0.0])
+    for _ in range(N):
+        out = oracle.implicit_step(m, model, u, v, mu, lam, None, h, iters=120)
+        u, v = out["u"], out["v"]
+    assert np.abs(v - N * h * g).max() < 1e-8
+    assert np.abs(u - h * h * g * N * (N + 1) / 2).max() < 1e-9
+
+
+def _total_energy(m, model, u, v, mu, lam):
+    f, K, en, inv = oracle.element_map(model, m.X, u, m.tets, m.Dminv, m.W, mu, lam, e=m.e, ne=m.ne, want_K=False)
+    return 0.5 * float(np.sum(m.mass[:, None] * v * v)) + float(en)
+
+
+@pytest.mark.parametrize("model", ["stvk", "nh"])
+def test_backward_euler_dissipates_energy(model):
+    """A multi-step property of converged backward Euler on a conservative
+    system (no gravity, no damping, fixed walls): with M (v' - v) = h f(u'),
+    u' - u = h v' and f = -grad Psi, the total energy changes by
+    Psi(u') - Psi(u) - grad Psi(u').(u' - u) - |v' - v|_M^2 / 2, which is
+    <= 0 wherever Psi is convex along the step -- true near the rest state
+    (small strain).  Converged Newton (4 iterations, 300 PCG iterations)
+    makes the oracle's trajectory the backward-Euler one; a wrong sign of a
+    force or stiffness term, or a wrong mass, makes the energy grow."""
+    X, tets = M.kuhn6(3)
+    m = oracle.Mesh(X, tets)
+    free = S.fixed_mask(X, 3)
+    u = 1e-3 * np.random.default_rng(4).uniform(-1, 1, X.shape) * free[:, None]
+    v = np.zeros_like(X)
+    mu, lam = S.materials(m.nt, 2e5, 0.3)
+    E = [_total_energy(m, model, u, v, mu, lam)]
+    for _ in range(12):
+        out = oracle.newton_step(m, model, u, v, mu, lam, free, 2e-3, iters=300, newton=4, g=(0.0, 0.0, 0.0))
+        u, v = out["u"], out["v"]
+        E.append(_total_energy(m, model, u, v, mu, lam))
+    dE = np.diff(E)
+    assert np.all(dE <= 1e-12 * E[0]), dE / E[0]
+    assert E[-1] < 0.999 * E[0]                  # and it does dissipate

@@ -787,12 +787,21 @@ def run_dist_map(args, rank, world, local_rank):
     R = D.GpuRank(ctx, rank, part, X, free, u0, np.zeros_like(u0), mu, lam, dtype="f32", stream=stream,
                   name=f"c3r{rank}")
     t_part = time.perf_counter() - t_part
-    T = D.NcclTransport(ctx, rank, world, stream=stream)
+    if args.dist_halo == "peer":
+        # the position halo as one peer-memory push kernel (CUDA IPC of the
+        # peers' u; no NCCL on the step)
+        T = None
+        halo = D.PeerHalo([R], "disp", comm=dist.group.WORLD if world > 1 else None, stream=stream)
+        transport = "peer memory (CUDA IPC over NVLink; ebb_peer_halo_push)"
+    else:
+        T = D.NcclTransport(ctx, rank, world, stream=stream)
+        halo = None
+        transport = "nccl (in-library, ebb_comm_*)"
     T_global = tets.shape[0]
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def step():
-        D.map_step([R], T, "stvk")
+        D.map_step([R], T, "stvk", halo=halo)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -814,7 +823,6 @@ def run_dist_map(args, rank, world, local_rank):
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
-            reset()
             evs[k][0].record(stream)
             if graph is None:
                 step()
@@ -840,8 +848,9 @@ def run_dist_map(args, rank, world, local_rank):
             "data": "synthetic (seeded metaball blob of Kuhn cubes, twist displacement)",
             "config": {"workload": f"C3 (BASELINE configs[2]): StVK force+stiffness map, blob of {T_global} tets "
                                    f"(n={n}), fp32, split over {world} GPU(s) by the O4 owner maps with ghost tets; "
-                                   "a step = the u halo (NCCL) + the map of the local tets",
-                       "tets": T_global, "parallelism": f"domain decomposition x{world} (NCCL position halo)",
+                                   f"a step = the u halo ({args.dist_halo}) + the map of the local tets",
+                       "tets": T_global, "transport": transport,
+                       "parallelism": f"domain decomposition x{world} ({args.dist_halo} position halo)",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "roofline": {"kernel": "k_tet_map_seg (local tets of this rank)", "bound": "hbm",
                          "achieved": b_map / (map_us * 1e-6) / 1e9, "peak": peak, "unit": "GB/s",
@@ -854,6 +863,9 @@ def run_dist_map(args, rank, world, local_rank):
                            "partition_setup_s": t_part}}
     if rank == 0:
         emit(line)
+    if halo is not None:
+        dist.barrier()
+        halo.close()
     ctx.close()
 
 
@@ -873,6 +885,8 @@ def main():
                     help="PCG driver of the multi-GPU path (peer: ONE fused kernel per solve, halos and scalar "
                          "sums over peer memory; single: per-iteration phases with one fused NCCL allreduce; "
                          "saad: two allreduces per iteration)")
+    ap.add_argument("--dist-halo", default="peer", choices=["peer", "nccl"],
+                    help="position halo of the --map-only multi-GPU path (peer: one push kernel over peer memory)")
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU (domain decomposition) path even with one rank (smoke test)")
     args = ap.parse_args()

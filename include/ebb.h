@@ -554,13 +554,34 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
  * */
 ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_stream s);
 
+/* Halo of a vertex field over peer memory (SURVEY §8(e) "halo exchange of
+ * vertex positions", without NCCL): owners store the rows [0, n_owned) that
+ * peers hold as ghosts straight into the peers' copies of `field` (the send
+ * lists of ebb_peer_send_csr), then one mailbox exchange; when
+ * ebb_peer_halo_push ends on a rank (stream order) its ghost rows are
+ * current.  The mailbox may be the one of the rank's fused PCG group (one
+ * epoch counter; every rank must issue the same sequence of pushes and PCG
+ * steps).  field: element-major (AOS or scalar), any non-key dtype, rows a
+ * multiple of 4 bytes.  peer_field[q]: device address, valid on this rank's
+ * device, of rank q's copy; [rank] unused.  bind: synchronous, validates;
+ * push: stream-ordered, graph-capturable, a cooperative launch. */
+typedef struct {
+    int32_t nranks, rank;
+    uint64_t n_owned;
+    ebb_field field, send_off, send_dst, mbox;
+    uint64_t peer_field[EBB_MAX_RANKS], peer_mbox[EBB_MAX_RANKS];
+} ebb_peer_halo;
+ebb_status ebb_peer_halo_bind(ebb_ctx ctx, int32_t nlocal, const ebb_peer_halo* descs, int32_t* group_out);
+ebb_status ebb_peer_halo_push(ebb_ctx ctx, int32_t group, ebb_stream s);
+
 typedef struct {
     ebb_field f, mass, mask;  /* mask: verts U8 (1 = free) or EBB_NONE        */
     ebb_field u, vel;         /* verts vec3 (read-write)                      */
     double h;
     double g[3];
 } ebb_explicit_desc;
-/* O8: a = (f + m g)/m; u += v h + a h^2/2; v += a h on free vertices. */
+/* O8 (the update of P:376-377): a = (f + m g)/m;
+ * u += v h + a h^2/2; v += a h on free vertices. */
 ebb_status ebb_explicit_update(ebb_ctx ctx, const ebb_explicit_desc* d, ebb_stream s);
 /* O9 implicit state update (P:941 backward Euler):
  * vel += dv; u += h vel.  dv, u, vel: AOS vec3 fields of one dtype on the

@@ -100,6 +100,13 @@ class PeerCG(C.Structure):
                 ("peer_mbox", C.c_uint64 * MAX_RANKS)]
 
 
+class PeerHalo(C.Structure):
+    """ebb_peer_halo (include/ebb.h)."""
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("n_owned", C.c_uint64), ("field", u32),
+                ("send_off", u32), ("send_dst", u32), ("mbox", u32),
+                ("peer_field", C.c_uint64 * MAX_RANKS), ("peer_mbox", C.c_uint64 * MAX_RANKS)]
+
+
 class ExplicitDesc(C.Structure):
     _fields_ = [("f", u32), ("mass", u32), ("mask", u32), ("u", u32), ("vel", u32), ("h", C.c_double),
                 ("g", C.c_double * 3)]
@@ -193,6 +200,8 @@ SIGS = {
     "ebb_ipc_close": (S, [ctx_t, C.c_uint64]),
     "ebb_cg_peer_bind": (S, [ctx_t, C.c_int32, C.POINTER(CG), C.POINTER(PeerCG), C.POINTER(C.c_int32)]),
     "ebb_cg_peer_step": (S, [ctx_t, C.c_int32, C.c_int32, stream_t]),
+    "ebb_peer_halo_bind": (S, [ctx_t, C.c_int32, C.POINTER(PeerHalo), C.POINTER(C.c_int32)]),
+    "ebb_peer_halo_push": (S, [ctx_t, C.c_int32, stream_t]),
 }
 
 _lib = None

@@ -1437,9 +1437,9 @@ __device__ __forceinline__ void rank_barrier(unsigned int* bar, unsigned int nbl
 // exchange number `epoch` of (d, g) between the ranks; returns the sums over
 // ranks in rank order (every CTA, every rank: the same values).  Call after a
 // rank_barrier that follows this CTA's last read of the previous exchange.
-__device__ __forceinline__ void peer_exchange(const PeerRankArgs& a, unsigned bid, uint64_t epoch, double d,
-                                              double g, double* sm2, unsigned long long* err, double& dsum,
-                                              double& gsum) {
+template <typename ARGS>   // PeerRankArgs or HaloRankArgs: rank, nranks, mbox, peer_mbox
+__device__ __forceinline__ void peer_exchange(const ARGS& a, unsigned bid, uint64_t epoch, double d, double g,
+                                              double* sm2, unsigned long long* err, double& dsum, double& gsum) {
     const unsigned slot = (unsigned)(epoch & 1u);
     const unsigned long long seq = epoch + 1;
     const unsigned q = threadIdx.x;
@@ -2066,6 +2066,52 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), PEER_MINB)
     const unsigned lr = blockIdx.x / G;
     if constexpr (SAAD) cg_saad_peer_body<R>(ranks[lr], lr, blockIdx.x - lr * G, G, err, iters, tol2);
     else cg1_peer_body<R>(ranks[lr], lr, blockIdx.x - lr * G, G, err, iters, tol2);
+}
+
+// ---------------------------------------------------------------------------
+// Halo of a vertex field over peer memory (ebb_peer_halo_push; SURVEY §8(e)
+// "halo exchange of vertex positions"): the owners store the rows peers hold
+// as ghosts straight into the peers' copies of the field, then one mailbox
+// exchange (the same mailboxes and epoch counter as the fused PCG) tells
+// every rank that its ghost rows have arrived; when the kernel ends on a rank
+// its ghosts are current.  Rows are moved as 4-byte words (any dtype / shape
+// of an element-major field).
+struct HaloRankArgs {
+    const uint32_t* src;               // the field (row r at src + r * wpr)
+    uint64_t n_owned;
+    uint32_t wpr, pad;                 // 4-byte words per row
+    const uint32_t* send_off;
+    const uint2* send_dst;
+    unsigned long long* mbox;
+    unsigned int* bar;
+    uint32_t* peer_dst[kPeerMax];
+    unsigned long long* peer_mbox[kPeerMax];
+    int rank, nranks;
+};
+
+__global__ void __launch_bounds__(256) k_peer_halo(const HaloRankArgs* __restrict__ recs, unsigned G,
+                                                   unsigned long long* __restrict__ err) {
+    __shared__ double sm2[2];
+    const unsigned lr = blockIdx.x / G, bid = blockIdx.x - lr * G;
+    const HaloRankArgs& a = recs[lr];
+    const uint64_t epoch = a.mbox[kMbEpoch];
+    const uint32_t wpr = a.wpr;
+    bool sent = false;
+    for (uint64_t v = (uint64_t)bid * blockDim.x + threadIdx.x; v < a.n_owned; v += (uint64_t)G * blockDim.x) {
+        const uint32_t s0 = a.send_off[v], s1 = a.send_off[v + 1];
+        if (s0 == s1) continue;
+        const uint32_t* row = a.src + v * wpr;
+        for (uint32_t k = s0; k < s1; ++k) {
+            const uint2 d = a.send_dst[k];
+            uint32_t* dst = a.peer_dst[d.x] + (uint64_t)d.y * wpr;
+            for (uint32_t w = 0; w < wpr; ++w) dst[w] = row[w];
+        }
+        sent = true;
+    }
+    rank_barrier(a.bar, G, sent);
+    double x0, x1;
+    peer_exchange(a, bid, epoch, 0.0, 0.0, sm2, err, x0, x1);
+    if (bid == 0 && threadIdx.x == 0) a.mbox[kMbEpoch] = epoch + 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -2758,6 +2804,8 @@ struct PeerGroup {
     PeerRankArgs* d_args = nullptr;
     PeerRankArgs one;                  // nlocal == 1: the record passed as a kernel parameter
     std::vector<ebb_field> fields;     // every field a record points into (checked at each step)
+    HaloRankArgs* d_halo = nullptr;    // halo groups (ebb_peer_halo_bind): the records of k_peer_halo
+    bool noop = false;                 // halo group of a one-rank job
     double* d_part = nullptr;
     unsigned int* d_bar = nullptr;
 };
@@ -2793,6 +2841,7 @@ void peer_release(Ctx* c) {
         cudaFree(P->d_args);
         cudaFree(P->d_part);
         cudaFree(P->d_bar);
+        if (P->d_halo) cudaFree(P->d_halo);
         delete P;
     }
     c->peer_groups.clear();
@@ -3291,6 +3340,7 @@ ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_strea
         return fail(c, EBB_E_ARG, "peer_step: bad group %d", group);
     if (iters < 0) return fail(c, EBB_E_ARG, "negative iteration count");
     PeerGroup* P = (PeerGroup*)c->peer_groups[group];
+    if (P->d_halo) return fail(c, EBB_E_ARG, "peer_step: group %d is a halo group", group);
     for (ebb_field f : P->fields)
         if (!get_field(c, f)) return fail(c, EBB_E_STATE, "peer_step: a field of group %d was freed", group);
     cudaStream_t s = (cudaStream_t)stream;
@@ -3314,6 +3364,102 @@ ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_strea
     void* one_args[] = {(void*)&P->one, (void*)&err, (void*)&it, (void*)&tol2};
     void* multi_args[] = {(void*)&recs, (void*)&G, (void*)&err, (void*)&it, (void*)&tol2};
     EBB_CUDA(c, cudaLaunchKernelExC(&cfg, k, P->nlocal == 1 ? one_args : multi_args));
+    return EBB_OK;
+}
+
+ebb_status ebb_peer_halo_bind(ebb_ctx ctx, int32_t nlocal, const ebb_peer_halo* descs, int32_t* group_out) {
+    Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
+    if (!c || !descs || !group_out) return fail(c, EBB_E_ARG, "null argument");
+    if (nlocal < 1 || nlocal > EBB_MAX_RANKS) return fail(c, EBB_E_ARG, "halo_bind: nlocal must be 1..%d", EBB_MAX_RANKS);
+    std::vector<HaloRankArgs> h(nlocal);
+    std::vector<ebb_field> used;
+    for (int i = 0; i < nlocal; ++i) {
+        const ebb_peer_halo* d = &descs[i];
+        if (d->nranks < 1 || d->nranks > EBB_MAX_RANKS || d->rank < 0 || d->rank >= d->nranks ||
+            d->nranks != descs[0].nranks)
+            return fail(c, EBB_E_ARG, "halo_bind: rank %d: bad rank / nranks (%d / %d)", i, d->rank, d->nranks);
+        for (int j = 0; j < i; ++j)
+            if (descs[j].rank == d->rank) return fail(c, EBB_E_ARG, "halo_bind: rank %d bound twice", d->rank);
+        Field* F = get_field(c, d->field);
+        if (!F || F->dtype == EBB_KEY || (F->layout != EBB_AOS && F->comps() != 1))
+            return fail(c, EBB_E_TYPE, "halo_bind: the field must be an element-major, non-key field");
+        const size_t rb = F->comps() * dtype_size(F->dtype);
+        if (rb % 4) return fail(c, EBB_E_TYPE, "halo_bind: rows must be a multiple of 4 bytes");
+        if (d->n_owned > c->rels[F->rel].size) return fail(c, EBB_E_SIZE, "halo_bind: n_owned exceeds the rows");
+        Field* SO = get_field(c, d->send_off);
+        Field* SD = get_field(c, d->send_dst);
+        Field* MB = get_field(c, d->mbox);
+        if (!SO || SO->dtype != EBB_U32 || SO->comps() != 1 || c->rels[SO->rel].size != d->n_owned + 1)
+            return fail(c, EBB_E_TYPE, "halo_bind: send_off must be a U32 field of n_owned + 1 rows");
+        if (!SD || SD->dtype != EBB_U32 || SD->comps() != 2)
+            return fail(c, EBB_E_TYPE, "halo_bind: send_dst must be a U32 2x1 field");
+        if (!MB || MB->dtype != EBB_F64 || MB->comps() != 1 || c->rels[MB->rel].size < EBB_PEER_MBOX_WORDS)
+            return fail(c, EBB_E_TYPE, "halo_bind: mbox must be an F64 field of >= %d rows", EBB_PEER_MBOX_WORDS);
+        for (int q = 0; q < d->nranks; ++q)
+            if (q != d->rank && (!d->peer_field[q] || !d->peer_mbox[q]))
+                return fail(c, EBB_E_ARG, "halo_bind: rank %d: missing buffer address of peer %d", d->rank, q);
+        HaloRankArgs& a = h[i];
+        memset(&a, 0, sizeof(a));
+        a.src = (const uint32_t*)F->ptr;
+        a.n_owned = d->n_owned;
+        a.wpr = (uint32_t)(rb / 4);
+        a.send_off = (const uint32_t*)SO->ptr;
+        a.send_dst = (const uint2*)SD->ptr;
+        a.mbox = (unsigned long long*)MB->ptr;
+        for (int q = 0; q < d->nranks; ++q) {
+            a.peer_dst[q] = (uint32_t*)(uintptr_t)d->peer_field[q];
+            a.peer_mbox[q] = (unsigned long long*)(uintptr_t)d->peer_mbox[q];
+        }
+        a.rank = d->rank;
+        a.nranks = d->nranks;
+        for (ebb_field f : {d->field, d->send_off, d->send_dst, d->mbox}) used.push_back(f);
+    }
+    int nb = 0;
+    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_peer_halo, 256, 0));
+    unsigned G = (unsigned)c->num_sms;                 // one CTA per SM and rank: a light copy kernel
+    if ((uint64_t)G * nlocal > (uint64_t)nb * c->num_sms) G = (unsigned)((uint64_t)nb * c->num_sms / nlocal);
+    if (G < 1) return fail(c, EBB_E_SIZE, "halo_bind: %d ranks cannot all be resident", nlocal);
+    PeerGroup* P = new PeerGroup();
+    P->nlocal = nlocal;
+    P->G = G;
+    P->fields = used;
+    P->noop = descs[0].nranks == 1;    // a one-rank job has no peer and no ghost row
+    c->peer_groups.push_back(P);
+    EBB_CUDA(c, cudaMalloc(&P->d_halo, sizeof(HaloRankArgs) * nlocal));
+    EBB_CUDA(c, cudaMalloc(&P->d_bar, sizeof(unsigned int) * 2 * nlocal));
+    EBB_CUDA(c, cudaMemset(P->d_bar, 0, sizeof(unsigned int) * 2 * nlocal));
+    for (int i = 0; i < nlocal; ++i) h[i].bar = P->d_bar + 2 * i;
+    EBB_CUDA(c, cudaMemcpy(P->d_halo, h.data(), sizeof(HaloRankArgs) * nlocal, cudaMemcpyHostToDevice));
+    *group_out = (int32_t)(c->peer_groups.size() - 1);
+    return EBB_OK;
+}
+
+ebb_status ebb_peer_halo_push(ebb_ctx ctx, int32_t group, ebb_stream stream) {
+    Ctx* c = (Ctx*)ctx;
+    EBB_DEVICE_GUARD(c);
+    if (!c) return EBB_E_ARG;
+    if (group < 0 || (size_t)group >= c->peer_groups.size() || !c->peer_groups[group] ||
+        !((PeerGroup*)c->peer_groups[group])->d_halo)
+        return fail(c, EBB_E_ARG, "halo_push: bad halo group %d", group);
+    PeerGroup* P = (PeerGroup*)c->peer_groups[group];
+    for (ebb_field f : P->fields)
+        if (!get_field(c, f)) return fail(c, EBB_E_STATE, "halo_push: a field of group %d was freed", group);
+    if (P->noop) return EBB_OK;        // one rank: nothing to move, no launch
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P->G * (unsigned)P->nlocal);
+    cfg.blockDim = dim3(256);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const HaloRankArgs* recs = P->d_halo;
+    unsigned G = P->G;
+    unsigned long long* err = c->d_err;
+    c->launches++;
+    EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_peer_halo, recs, G, err));
     return EBB_OK;
 }
 

@@ -161,15 +161,20 @@ def _map_assemble(ranks, transport, model, h, alpha, beta, g):
         R.assemble(h, alpha, beta, g)
 
 
-def map_step(ranks, transport, model="stvk"):
+def map_step(ranks, transport, model="stvk", halo=None):
     """The distributed element map alone (BASELINE configs[2]: the force +
     stiffness map with halo exchange): the owners' displacements go to their
     ghost copies (the position halo, owners -> ghosts), then every rank maps
     its tets -- with the reverse-add variant the partial f / K rows of ghost
-    tails are added into their owners afterwards."""
-    for R in ranks:
-        R.set_halo("disp")
-    transport.exchange(ranks)
+    tails are added into their owners afterwards.  halo: a ``PeerHalo`` of
+    the displacements -- the position halo as one peer-memory push kernel
+    instead of the transport's pack / send / unpack."""
+    if halo is not None:
+        halo.push()
+    else:
+        for R in ranks:
+            R.set_halo("disp")
+        transport.exchange(ranks)
     for R in ranks:
         R.map_forces(model)
     if getattr(ranks[0], "map_variant", "overlap") == "reverse":
@@ -507,7 +512,7 @@ class GpuRank:
                                                       self.fem.vel.h, _stream(self.stream)))
 
     # -- fused PCG over peer memory (PeerPCG)
-    def peer_export(self, ipc):
+    def peer_export(self, ipc, extra=None):
         """What peers need of this rank: its recv rows per peer (numpy), its
         local vertex count, send-list lengths, and its ghost-row targets
         (cg.u, cg.u2, cg.x = dv, cg.z, the mailbox) as device addresses
@@ -520,6 +525,7 @@ class GpuRank:
             self.mbox = rel.field("mbox", "f64", init=np.zeros(A.PEER_MBOX_WORDS))
         cg = self.fem.cg
         handles = {"u": cg.u, "u2": cg.u2, "x": cg.x, "z": cg.z, "mbox": self.mbox.h}
+        handles.update(extra or {})
         buf = {}
         for name, fh in handles.items():
             if ipc:
@@ -610,7 +616,7 @@ class GpuRank:
 PEER_BUFFERS = ("u", "u2", "x", "z", "mbox")
 
 
-def peer_tables(infos, local_ranks, nranks):
+def peer_tables(infos, local_ranks, nranks, names=PEER_BUFFERS):
     """What each local rank needs of its peers for ebb_cg_peer_bind, from the
     peers' exported infos (``GpuRank.peer_export``): per local rank r, the
     sorted send peers q with r's remote rows on q (q's recv rows from r: the
@@ -628,7 +634,7 @@ def peer_tables(infos, local_ranks, nranks):
                 raise ValueError(f"rank {r} sends {me['send'][q]} rows to {q}, which expects {rows.size}")
             remote.append(rows)
             peer_nv.append(int(infos[q]["nv"]))
-        bufs = {name: [infos[q]["buf"][name] if q != r else None for q in range(nranks)] for name in PEER_BUFFERS}
+        bufs = {name: [infos[q]["buf"][name] if q != r else None for q in range(nranks)] for name in names}
         out[r] = dict(peers=peers, remote=remote, peer_nv=peer_nv, bufs=bufs)
     return out
 
@@ -661,18 +667,7 @@ class PeerPCG:
         self.ranks, self.ctx, self.stream = list(ranks), ranks[0].ctx, stream
         ctx = self.ctx
         ipc = comm is not None
-        if ipc:
-            import torch.distributed as tdist
-            nranks = tdist.get_world_size(comm)
-            (R0,) = self.ranks
-            gathered = [None] * nranks
-            tdist.all_gather_object(gathered, R0.peer_export(ipc=True), group=comm)
-            infos = {d["rank"]: d for d in gathered}
-        else:
-            nranks = len(self.ranks)
-            infos = {R.rank: R.peer_export(ipc=False) for R in self.ranks}
-        if sorted(infos) != list(range(nranks)):
-            raise ValueError(f"peer ranks {sorted(infos)} are not 0..{nranks - 1}")
+        infos, nranks = _gather_infos(self.ranks, comm, lambda R: None)
         if variant == "auto":                 # the same choice on every rank: from the gathered sizes
             variant = "single" if max(d["nv"] for d in infos.values()) <= self.AUTO_SINGLE_MAX_VERTS else "saad"
         self.variant = variant
@@ -685,7 +680,9 @@ class PeerPCG:
         pcs = (A.PeerCG * len(self.ranks))()
         for i, R in enumerate(self.ranks):
             t = tables[R.rank]
-            off, dst = R.peer_send_csr(t["peers"], t["remote"], t["peer_nv"])
+            if getattr(R, "peer_off", None) is None:      # one send CSR per rank (a property of the partition)
+                R.peer_send_csr(t["peers"], t["remote"], t["peer_nv"])
+            off, dst = R.peer_off, R.peer_dst
             pc = pcs[i]
             pc.nranks, pc.rank, pc.n_owned = nranks, R.rank, R.n_owned
             pc.send_off, pc.send_dst, pc.mbox = off.h, dst.h, R.mbox.h
@@ -719,6 +716,81 @@ class PeerPCG:
         """Unmap the peers' buffers (one process per GPU); the binding is
         unusable afterwards.  Every rank must have finished its last step
         first (a barrier), or a peer could still be storing into us."""
+        for a in self._opened:
+            self.ctx.check(self.ctx.L.ebb_ipc_close(self.ctx.h, a))
+        self._opened = []
+        self.group = None
+
+
+def _gather_infos(ranks, comm, extra):
+    """Every rank's peer infos (local: direct; one process per GPU: through
+    all_gather_object) and the job's rank count."""
+    ipc = comm is not None
+    if ipc:
+        import torch.distributed as tdist
+        nranks = tdist.get_world_size(comm)
+        (R0,) = ranks
+        gathered = [None] * nranks
+        tdist.all_gather_object(gathered, R0.peer_export(ipc=True, extra=extra(R0)), group=comm)
+        infos = {d["rank"]: d for d in gathered}
+    else:
+        nranks = len(ranks)
+        infos = {R.rank: R.peer_export(ipc=False, extra=extra(R)) for R in ranks}
+    if sorted(infos) != list(range(nranks)):
+        raise ValueError(f"peer ranks {sorted(infos)} are not 0..{nranks - 1}")
+    return infos, nranks
+
+
+class PeerHalo:
+    """The ghost rows of a vertex field over peer memory
+    (``ebb_peer_halo_bind`` / ``ebb_peer_halo_push``, SURVEY §8(e) "halo
+    exchange of vertex positions"): owners store their boundary rows into
+    the peers' copies, one mailbox exchange (shared with the ranks' PeerPCG
+    epoch counter) ends the push.  which: a key of ``GpuRank.halo_fields``
+    ("disp" = the displacement u).  comm as for ``PeerPCG``."""
+
+    def __init__(self, ranks, which="disp", comm=None, stream=None):
+        import ctypes as C
+
+        from . import _abi as A
+        self.ranks, self.ctx, self.stream = list(ranks), ranks[0].ctx, stream
+        ctx = self.ctx
+        ipc = comm is not None
+        infos, nranks = _gather_infos(self.ranks, comm, lambda R: {"halo": R.halo_fields[which].h})
+        tables = peer_tables(infos, [R.rank for R in self.ranks], nranks, names=("halo", "mbox"))
+        self._opened = []
+        ds = (A.PeerHalo * len(self.ranks))()
+        for i, R in enumerate(self.ranks):
+            t = tables[R.rank]
+            if getattr(R, "peer_off", None) is None:
+                R.peer_send_csr(t["peers"], t["remote"], t["peer_nv"])
+            d = ds[i]
+            d.nranks, d.rank, d.n_owned = nranks, R.rank, R.n_owned
+            d.field, d.send_off, d.send_dst, d.mbox = R.halo_fields[which].h, R.peer_off.h, R.peer_dst.h, R.mbox.h
+            for name, arr in (("halo", d.peer_field), ("mbox", d.peer_mbox)):
+                for q, b in enumerate(t["bufs"][name]):
+                    if b is None:
+                        continue
+                    if ipc:
+                        addr = C.c_uint64()
+                        ctx.check(ctx.L.ebb_ipc_open(ctx.h, bytes(b), C.byref(addr)))
+                        self._opened.append(addr.value)
+                        b = addr.value
+                    arr[q] = int(b)
+        g = C.c_int32()
+        ctx.check(ctx.L.ebb_peer_halo_bind(ctx.h, len(self.ranks), ds, C.byref(g)))
+        self.group = g.value
+        if ipc:
+            import torch.distributed as tdist
+            tdist.barrier(group=comm)
+
+    def push(self):
+        from .ebb import _stream
+        if self.group is None:
+            raise RuntimeError("PeerHalo.push after close()")
+        self.ctx.check(self.ctx.L.ebb_peer_halo_push(self.ctx.h, self.group, _stream(self.stream)))
+
+    def close(self):
         for a in self._opened:
             self.ctx.check(self.ctx.L.ebb_ipc_close(self.ctx.h, a))
         self._opened = []

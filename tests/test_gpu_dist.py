@@ -240,16 +240,19 @@ def test_reverse_add_maps_every_tet_once(ctx, P):
     assert rel_l2(dv[order], ref["dv"]) <= 1e-8
 
 
+@pytest.mark.parametrize("halo", ["transport", "peer"])
 @pytest.mark.parametrize("map_variant", ["overlap", "reverse"])
 @pytest.mark.parametrize("model,dtype", [("stvk", "f64"), ("nh", "f64"), ("stvk", "f32")])
 @pytest.mark.parametrize("P", [2, 3])
-def test_distributed_map_step(ctx, P, model, dtype, map_variant):
+def test_distributed_map_step(ctx, P, model, dtype, map_variant, halo):
     """BASELINE configs[2]'s distributed map: after the position halo and the
     map (plus the reverse add), every owned force row and every owned
     stiffness row equals the single-domain oracle's: f directly, K through
     K p for a seeded global p (each owned row of K p uses the whole row).
     The ranks start from stale ghost displacements (zeros), so the halo
-    exchange is what makes the ghost tets right."""
+    exchange is what makes the ghost tets right.  halo="peer": the position
+    halo as the peer-memory push kernel (ebb_peer_halo_push), the ranks
+    emulated in one cooperative launch."""
     from paper_1506_07577_b200 import dist
     case = Case(n=5, model=model, spread=0.1)
     if dtype == "f32":
@@ -263,16 +266,18 @@ def test_distributed_map_step(ctx, P, model, dtype, map_variant):
     Kp = oracle.edge_matvec(m.row_ptr, m.head, K, p_in[order])  # stored order
     ranks = []
     for r in range(P):
-        part = dist.partition_rank(ctx, case.X, case.tets, P, r, name=f"dm{P}{model}{dtype}{map_variant}p{r}")
+        part = dist.partition_rank(ctx, case.X, case.tets, P, r, name=f"dm{P}{model}{dtype}{map_variant}{halo}p{r}")
         u_stale = case.u.copy()
         R = dist.GpuRank(ctx, r, part, case.X, case.free, u_stale, case.vel, case.mu, case.lam, dtype=dtype,
-                         name=f"dm{P}{model}{dtype}{map_variant}r{r}", map_variant=map_variant, nranks=P)
+                         name=f"dm{P}{model}{dtype}{map_variant}{halo}r{r}", map_variant=map_variant, nranks=P)
         ghost = ~R.owned_stored
         uu = R.fem.u.read()
         uu[ghost] = 0.0                                         # stale ghosts: the halo must refresh them
         R.fem.u.write(uu)
         ranks.append(R)
-    dist.map_step(ranks, dist.LocalTransport(), model)
+    ph = dist.PeerHalo(ranks) if halo == "peer" else None
+    dist.map_step(ranks, dist.LocalTransport(), model, halo=ph)
+    assert ctx.error_counts()["peer_timeouts"] == 0
     tol = 1e-12 if dtype == "f64" else 1e-5
     f_in = np.full((m.nv, 3), np.nan)
     kp_in = np.full((m.nv, 3), np.nan)

@@ -101,7 +101,20 @@ def main():
             t_init = _time(lambda: [R.cg_init(single=sr) for R in ranks], a.reps, flush)
             peer_ms[var] = _time(run_peer, a.reps, flush) - t_init
             peer.close()
+        # the position halo of the displacements: one peer push kernel for all
+        # ranks vs the transport's pack / copy / unpack per peer
+        halo = dist.PeerHalo(ranks, "disp")
+        T = dist.LocalTransport()
+
+        def run_transport():
+            for R in ranks:
+                R.set_halo("disp")
+            T.exchange(ranks)
+        halo_us = {"peer_push": 1e3 * _time(halo.push, a.reps, flush),
+                   "transport": 1e3 * _time(run_transport, a.reps, flush)}
+        halo.close()
         line = {"P": P, "n": n, "global_tets": int(tets.shape[0]), "global_verts": int(nv_g),
+                "position_halo_us_all_ranks": halo_us,
                 "owned_verts": [int(R.n_owned) for R in ranks], "local_verts": [int(R.fem.nv) for R in ranks],
                 "send_rows": [int(sum(len(r_) for r_ in R.part_send.values())) for R in ranks],
                 "iters": a.iters, "peer_ms": peer_ms,

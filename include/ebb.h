@@ -286,6 +286,14 @@ ebb_status ebb_tetmesh_consistent_mass(ebb_ctx ctx, ebb_field tets_e, ebb_field 
                                    EBB_E_RANGE if one row gets blocks from
                                    more than 128 tiles or more than 248
                                    blocks from one tile.                     */
+#define EBB_SCATTER_CHUNK_RED 7 /* SURVEY §8(a) "+=" strategy (i): the CHUNK
+                                   tiles (each tet once, rows summed on chip
+                                   per tile), rows only one tile feeds stored
+                                   once, rows several tiles feed zeroed first
+                                   and then added to with red.global.add
+                                    -- no messages, no waits between
+                                   tiles; not bitwise run-to-run
+                                   deterministic (RED order).               */
 typedef struct {
     int32_t model;         /* EBB_STVK | EBB_NH                                */
     int32_t scatter;       /* EBB_SCATTER_*                                    */

@@ -26,6 +26,7 @@ AOS, SOA = 0, 1
 STVK, NH = 0, 1
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILED, SCATTER_GATHER, SCATTER_SEGMENTED, SCATTER_COLOR, SCATTER_CHUNK = \
     0, 1, 2, 3, 4, 5, 6
+SCATTER_CHUNK_RED = 7
 RED_SUM, RED_DOT, RED_MAX, RED_MIN = 0, 1, 2, 3
 CG_DIR, CG_MATVEC, CG_UPDATE, CG_SR_PHASE = 0, 1, 2, 3
 K_TET_MAP, K_EDGE_MATVEC, K_CG_UPDATE, K_CG_DIR, K_ASSEMBLE, K_CG_SOLVE, K_SPRING, K_EBE_MATVEC, K_GRID = \

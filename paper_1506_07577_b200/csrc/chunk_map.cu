@@ -155,13 +155,39 @@ __device__ __forceinline__ void chunk_store(uint32_t kind, uint32_t row, uint32_
 }
 
 
+// RED mode: the same destinations as chunk_store, added with red.global.add
+// (the row was zeroed before the map: k_chunk_zero_shared)
+template <typename R>
+__device__ __forceinline__ void chunk_red(uint32_t kind, uint32_t row, uint32_t row2, R a9[9], R* __restrict__ f,
+                                          R* __restrict__ K, uint64_t ne) {
+    if (kind == 1) {
+        R* df = f + 3ull * row2;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) atomicAdd(df + a, a9[6 + a]);
+        const R dd[6] = {a9[0], a9[1], a9[2], a9[3], a9[4], a9[5]};
+        a9[0] = dd[0]; a9[1] = dd[1]; a9[2] = dd[2];
+        a9[3] = dd[1]; a9[4] = dd[3]; a9[5] = dd[4];
+        a9[6] = dd[2]; a9[7] = dd[4]; a9[8] = dd[5];
+    }
+    R* dst = K + row;
+#pragma unroll
+    for (int q = 0; q < 9; ++q, dst += ne) atomicAdd(dst, a9[q]);
+    if (kind == 0) {
+        dst = K + row2;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int c = 0; c < 3; ++c, dst += ne) atomicAdd(dst, a9[3 * c + a]);
+    }
+}
+
 #ifdef CHUNK_PROF
 __device__ unsigned long long g_chunk_prof[16];
 #endif
 template <typename R, int NT>
 constexpr int chunk_min_blocks() { return NT <= 256 ? 2 : 1; }   // NT <= 128: no register cap
 
-template <typename R, int MODEL, bool WANT_E, int NT>
+template <typename R, int MODEL, bool WANT_E, int NT, bool RED>
 __global__ void __launch_bounds__(NT, chunk_min_blocks<R, NT>()) k_tet_map_chunk(
     uint32_t ntiles, const uint4* __restrict__ tdesc, const uint32_t* __restrict__ expect,
     const uint32_t* __restrict__ recv, uint32_t* __restrict__ cnt, uint32_t* __restrict__ ticket,
@@ -285,15 +311,19 @@ __global__ void __launch_bounds__(NT, chunk_min_blocks<R, NT>()) k_tet_map_chunk
             chunk_walk<R, MODEL, NT>(st, E, it.x, a9);
             chunk_combine<R>(it.x, a9);
             if (it_pos(it.x) == 0 && it.y != 0xFFFFFFFFu) {
-                R* mm = msg + (size_t)it.w * MW;
+                if constexpr (RED) {
+                    chunk_red<R>(it_kind(it.x), it.y, it.z, a9, f, K, ne);   // strategy (i): no message
+                } else {
+                    R* mm = msg + (size_t)it.w * MW;
 #pragma unroll
-                for (int q = 0; q < 9; ++q) mm[q] = a9[q];
+                    for (int q = 0; q < 9; ++q) mm[q] = a9[q];
+                }
             }
         }
-        __syncthreads();   // every message of this tile written (CTA scope)
+        if constexpr (!RED) __syncthreads();   // every message of this tile written (CTA scope)
         CP_MARK(2);
         // ---- signal the receivers, wait for the senders
-        if (tid == 0) {
+        if (!RED && tid == 0) {
             if (r1 > d.w) {
                 red_release_add(cnt + __ldg(recv + d.w), 1u);   // MEMBAR.ALL.GPU once, then the RED
                 for (uint32_t r = d.w + 1; r < r1; ++r) atomicAdd(cnt + __ldg(recv + r), 1u);
@@ -306,7 +336,7 @@ __global__ void __launch_bounds__(NT, chunk_min_blocks<R, NT>()) k_tet_map_chunk
             }
         }
         CP_MARK(3);
-        __syncthreads();
+        if constexpr (!RED) __syncthreads();
         CP_MARK(4);
         // ---- phase 2b: owned segments + their incoming messages (L2 loads)
         for (uint32_t base = 0; base < d.z; base += NT) {
@@ -319,12 +349,18 @@ __global__ void __launch_bounds__(NT, chunk_min_blocks<R, NT>()) k_tet_map_chunk
             chunk_combine<R>(it.x, a9);
             if (it_pos(it.x) == 0 && it.y != 0xFFFFFFFFu) {
                 const uint32_t nm = it_nmsg(it.x);
-                for (uint32_t k = 0; k < nm; ++k) {
-                    const R* mm = msg + (size_t)(it.w + k) * MW;
+                if constexpr (RED) {
+                    // a row other tiles also feed: added; a row only this tile feeds: stored
+                    if (nm) chunk_red<R>(it_kind(it.x), it.y, it.z, a9, f, K, ne);
+                    else chunk_store<R>(it_kind(it.x), it.y, it.z, a9, f, K, ne, accumulate);
+                } else {
+                    for (uint32_t k = 0; k < nm; ++k) {
+                        const R* mm = msg + (size_t)(it.w + k) * MW;
 #pragma unroll
-                    for (int q = 0; q < 9; ++q) a9[q] += __ldcg(mm + q);
+                        for (int q = 0; q < 9; ++q) a9[q] += __ldcg(mm + q);
+                    }
+                    chunk_store<R>(it_kind(it.x), it.y, it.z, a9, f, K, ne, accumulate);
                 }
-                chunk_store<R>(it_kind(it.x), it.y, it.z, a9, f, K, ne, accumulate);
             }
         }
         CP_MARK(5);
@@ -364,6 +400,21 @@ __global__ void k_chunk_zero(const uint32_t* __restrict__ zrows, uint64_t nz, co
         for (int q = 0; q < 9; ++q) K[q * ne + zrows[i]] = R(0);
     if (i < nzv)
         for (int a = 0; a < 3; ++a) f[3ull * zverts[i] + a] = R(0);
+}
+
+// RED mode: the rows more than one tile feeds (and their transposes / the
+// vertex forces of self rows) start from zero -- every contribution is a RED
+template <typename R>
+__global__ void k_chunk_zero_shared(const uint32_t* __restrict__ srows, uint64_t n, const uint32_t* __restrict__ tval,
+                                    R* __restrict__ K, uint64_t ne, R* __restrict__ f) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t r = srows[i], t = tval[2 * i], v = tval[2 * i + 1];
+    for (int q = 0; q < 9; ++q) K[q * ne + r] = R(0);
+    if (t != r)
+        for (int q = 0; q < 9; ++q) K[q * ne + t] = R(0);
+    else
+        for (int a = 0; a < 3; ++a) f[3ull * v + a] = R(0);
 }
 
 // ------------------------------------------------------------------ plan (device)
@@ -525,7 +576,7 @@ __device__ uint32_t layout_tile(const SegView& S, uint32_t tile, uint32_t L, boo
             const uint32_t sz = cnt / nc + (cc < cnt % nc ? 1 : 0);
             if (emit) {
                 uint4 it;
-                if (cls < 2) it = make_uint4(0, 0, 0, S.slot_of_seg[s]);
+                if (cls < 2) it = make_uint4(0, row, row2, S.slot_of_seg[s]);   // row, row2: the RED mode
                 else it = make_uint4(nm << 25, row, row2, S.mstart[row]);
                 it.x |= beg | (sz << 13) | (cc << 18) | ((nc - 1) << 21) | (kind << 24);
                 out[n] = it;
@@ -623,6 +674,18 @@ __global__ void kp_rowinfo(uint64_t nv, const uint32_t* __restrict__ index, cons
     }
 }
 
+// rows with incoming messages (fed by more than one tile): (row) and (transpose or self, vertex)
+__global__ void kp_shared_rows(uint64_t ne, const uint32_t* __restrict__ nout, const uint32_t* __restrict__ tval,
+                               const uint32_t* __restrict__ rvert, uint32_t* __restrict__ srows,
+                               uint32_t* __restrict__ sinfo, uint32_t* __restrict__ ns) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= ne || nout[r] == 0) return;
+    const uint32_t k = atomicAdd(ns, 1u);
+    srows[k] = (uint32_t)r;
+    sinfo[2 * k] = tval[r];
+    sinfo[2 * k + 1] = rvert[r];
+}
+
 int bits_for(uint64_t n) {
     int b = 1;
     while ((1ull << b) < n) ++b;
@@ -642,8 +705,9 @@ struct DevBuf {
 void ChunkPlan::release() {
     cudaFree(tdesc); cudaFree(expect); cudaFree(recv); cudaFree(cnt); cudaFree(ticket);
     cudaFree(items); cudaFree(ents); cudaFree(msg); cudaFree(zrows); cudaFree(zverts); cudaFree(tile_e);
+    cudaFree(srows);
     tdesc = nullptr; items = nullptr; tile_e = nullptr;
-    expect = recv = cnt = ticket = ents = zrows = zverts = nullptr;
+    expect = recv = cnt = ticket = ents = zrows = zverts = srows = nullptr;
     msg = nullptr;
 }
 
@@ -825,6 +889,15 @@ ebb_status build_chunk_plan(Ctx* c, ebb_field vf, ebb_field ef, int NT, ChunkPla
     if (nv) kp_rowinfo<<<grid_for(nv, B), B, 0, s>>>(nv, index, head, owner.as<int>(), tval.as<uint32_t>(),
                                                      rvert.as<uint32_t>(), P->zrows, zcnt.as<uint32_t>(), P->zverts,
                                                      zcnt.as<uint32_t>() + 1);
+    // 6b. rows fed by several tiles (the RED mode zeroes them first): the row
+    // list, then (transpose or self, vertex) per entry, in one allocation
+    DevBuf nsr;
+    CP_CUDA(nsr.alloc(4));
+    CP_CUDA(cudaMemsetAsync(nsr.p, 0, 4, s));
+    CP_CUDA(cudaMalloc(&P->srows, ne * 12 + 16));
+    if (ne) kp_shared_rows<<<grid_for(ne, B), B, 0, s>>>(ne, nout.as<uint32_t>(), tval.as<uint32_t>(),
+                                                         rvert.as<uint32_t>(), P->srows, P->srows + ne,
+                                                         nsr.as<uint32_t>());
     // 7. item layout per tile
     SegView S;
     S.ukey = ukey;
@@ -856,7 +929,8 @@ ebb_status build_chunk_plan(Ctx* c, ebb_field vf, ebb_field ef, int NT, ChunkPla
         CP_CUDA(cub::DeviceScan::ExclusiveSum(tmp8.p, tb8, nitems.as<uint32_t>(), item0.as<uint32_t>(),
                                               (int64_t)(ntiles + 1), s));
     }
-    uint32_t nit = 0, zc[3] = {0, 0, 0};
+    uint32_t nit = 0, zc[3] = {0, 0, 0}, nsr_h = 0;
+    CP_CUDA(cudaMemcpyAsync(&nsr_h, nsr.p, 4, cudaMemcpyDeviceToHost, s));
     CP_CUDA(cudaMemcpyAsync(&nit, item0.as<uint32_t>() + ntiles, 4, cudaMemcpyDeviceToHost, s));
     CP_CUDA(cudaMemcpyAsync(zc, zcnt.p, 12, cudaMemcpyDeviceToHost, s));
     CP_CUDA(cudaStreamSynchronize(s));
@@ -884,6 +958,7 @@ ebb_status build_chunk_plan(Ctx* c, ebb_field vf, ebb_field ef, int NT, ChunkPla
     P->nitems = nit;
     P->nzrows = zc[0];
     P->nzverts = zc[1];
+    P->nsrows = nsr_h;
     P->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     c->chunkplans.push_back(P);
     *out = P;
@@ -892,13 +967,14 @@ ebb_status build_chunk_plan(Ctx* c, ebb_field vf, ebb_field ef, int NT, ChunkPla
 
 namespace {
 
-template <typename R, int MODEL, int NT>
+template <typename R, int MODEL, int NT, bool RED>
 ebb_status launch_chunk_t(Ctx* c, const ChunkPlan& P, bool want_e, int accumulate, uint64_t nt, const Field* V,
                           const Field* U, const Field* D, const Field* W, const Field* MU, const Field* LA,
                           const Field* Fo, const Field* Ko, uint64_t ne, const Field* En, cudaStream_t s) {
     const size_t smem = (size_t)SegState<MODEL>::SW * NT * sizeof(R) + 2ull * 10 * NT * 4;
     if (smem > 227 * 1024)
         return fail(c, EBB_E_RANGE, "chunk map: %zu B of shared memory needed (> 227 KB)", smem);
+    KernelTimer kt(c, EBB_K_TET_MAP, s);   // the whole map: the zero passes included
     if (!accumulate && (P.nzrows || P.nzverts)) {
         const uint64_t n = std::max(P.nzrows, P.nzverts);
         k_chunk_zero<R><<<grid_for(n, 256), 256, 0, s>>>(P.zrows, P.nzrows, P.zverts, P.nzverts, (R*)Ko->ptr, ne,
@@ -906,8 +982,15 @@ ebb_status launch_chunk_t(Ctx* c, const ChunkPlan& P, bool want_e, int accumulat
         EBB_CUDA(c, cudaGetLastError());
         c->launches++;
     }
+    if (RED && !accumulate && P.nsrows) {
+        // the srows allocation holds the rows (ne entries) then (tval, vertex) pairs
+        k_chunk_zero_shared<R><<<grid_for(P.nsrows, 256), 256, 0, s>>>(P.srows, P.nsrows, P.srows + ne, (R*)Ko->ptr,
+                                                                       ne, (R*)Fo->ptr);
+        EBB_CUDA(c, cudaGetLastError());
+        c->launches++;
+    }
     if (P.ntiles == 0) return EBB_OK;
-    auto kern = want_e ? k_tet_map_chunk<R, MODEL, true, NT> : k_tet_map_chunk<R, MODEL, false, NT>;
+    auto kern = want_e ? k_tet_map_chunk<R, MODEL, true, NT, RED> : k_tet_map_chunk<R, MODEL, false, NT, RED>;
     static thread_local size_t configured_dev[kMaxDevices][2] = {};
     size_t* const configured = configured_dev[c->device % kMaxDevices];
     if (smem > configured[want_e]) {
@@ -917,7 +1000,6 @@ ebb_status launch_chunk_t(Ctx* c, const ChunkPlan& P, bool want_e, int accumulat
     unsigned grid = occ_grid(c, kern, NT, smem, (uint64_t)P.ntiles * NT);
     const char* eg = getenv("EBB_CHUNK_GRID");   // test knob: fewer CTAs
     if (eg && atoi(eg) > 0 && (unsigned)atoi(eg) < grid) grid = (unsigned)atoi(eg);
-    KernelTimer kt(c, EBB_K_TET_MAP, s);
     kern<<<grid, NT, smem, s>>>(P.ntiles, P.tdesc, P.expect, P.recv, P.cnt, P.ticket, P.items, P.ents, (R*)P.msg, nt,
                                 (const uint4*)V->ptr, (const R*)U->ptr, (const R*)D->ptr, (const R*)W->ptr,
                                 (const R*)MU->ptr, (const R*)LA->ptr, (R*)Fo->ptr, (R*)Ko->ptr, ne, accumulate,
@@ -964,20 +1046,25 @@ ebb_status chunk_plan_probe(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, in
 ebb_status chunk_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
                             const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                             const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool red) {
     const ebb_dtype dt = U->dtype;
     const int NT = chunk_threads(dt, model);
     ChunkPlan* P;
     EBB_TRY(build_chunk_plan(c, vf, ef, NT, &P));
 #define EBB_CARGS c, *P, want_e, accumulate, nt, V, U, D, W, MU, LA, Fo, Ko, ne, En, s
-#define EBB_CDISPATCH(R, MODEL)                                             \
+#define EBB_CDISPATCH2(R, MODEL, RD)                                        \
     do {                                                                    \
-        if (NT == 128) return launch_chunk_t<R, MODEL, 128>(EBB_CARGS);     \
-        if (NT == 256) return launch_chunk_t<R, MODEL, 256>(EBB_CARGS);     \
-        if (NT == 384) return launch_chunk_t<R, MODEL, 384>(EBB_CARGS);     \
+        if (NT == 128) return launch_chunk_t<R, MODEL, 128, RD>(EBB_CARGS); \
+        if (NT == 256) return launch_chunk_t<R, MODEL, 256, RD>(EBB_CARGS); \
+        if (NT == 384) return launch_chunk_t<R, MODEL, 384, RD>(EBB_CARGS); \
         if constexpr (!(sizeof(R) == 8 && MODEL == EBB_STVK))               \
-            return launch_chunk_t<R, MODEL, 512>(EBB_CARGS);                \
+            return launch_chunk_t<R, MODEL, 512, RD>(EBB_CARGS);            \
         return fail(c, EBB_E_ARG, "chunk map: bad thread count %d", NT);   \
+    } while (0)
+#define EBB_CDISPATCH(R, MODEL)                  \
+    do {                                         \
+        if (red) EBB_CDISPATCH2(R, MODEL, true); \
+        EBB_CDISPATCH2(R, MODEL, false);         \
     } while (0)
     if (dt == EBB_F64) {
         if (model == EBB_NH) EBB_CDISPATCH(double, EBB_NH);
@@ -986,6 +1073,7 @@ ebb_status chunk_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool 
     if (model == EBB_NH) EBB_CDISPATCH(float, EBB_NH);
     EBB_CDISPATCH(float, EBB_STVK);
 #undef EBB_CDISPATCH
+#undef EBB_CDISPATCH2
 #undef EBB_CARGS
 }
 

@@ -104,6 +104,8 @@ struct ChunkPlan {
     void* msg = nullptr;              // nmsg x 128 B
     uint32_t* zrows = nullptr;        // rows no tet contributes to
     uint32_t* zverts = nullptr;       // vertices in no tet
+    uint32_t* srows = nullptr;        // canonical rows fed by more than one tile (zeroed before a RED-mode map)
+    uint64_t nsrows = 0;
     void release();
 };
 
@@ -247,7 +249,7 @@ ebb_status build_chunk_plan(Ctx* c, ebb_field vf, ebb_field ef, int NT, ChunkPla
 ebb_status chunk_map_launch(Ctx* c, ebb_field vf, ebb_field ef, int model, bool want_e, int accumulate, uint64_t nt,
                             const Field* V, const Field* U, const Field* D, const Field* W, const Field* MU,
                             const Field* LA, const Field* Fo, const Field* Ko, uint64_t ne, const Field* En,
-                            cudaStream_t s);
+                            cudaStream_t s, bool red);
 // build the SEGMENTED / CHUNK plan for (v, e) if absent (EBB_E_RANGE: refused)
 ebb_status seg_plan_probe(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, int model);
 ebb_status chunk_plan_probe(Ctx* c, ebb_field vf, ebb_field ef, ebb_dtype dt, int model);

@@ -136,7 +136,7 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
     EBB_DEVICE_GUARD(c);
     if (!c || !d) return fail(c, EBB_E_ARG, "null argument");
     if (d->model != EBB_STVK && d->model != EBB_NH) return fail(c, EBB_E_ARG, "unknown model %d", d->model);
-    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_CHUNK)
+    if (d->scatter < EBB_SCATTER_AUTO || d->scatter > EBB_SCATTER_CHUNK_RED)
         return fail(c, EBB_E_ARG, "unknown scatter strategy %d", d->scatter);
     Field* V = get_field(c, d->v);
     Field* U = get_field(c, d->u);
@@ -222,11 +222,13 @@ extern "C" ebb_status ebb_map_tet_forces(ebb_ctx ctx, const ebb_tet_map_desc* d,
         }
         return color_map_launch(c, d->v, d->model, En != nullptr, nt, V, Ef, U, D, W, MU, LA, Fo, Ko, ne, En, s);
     }
-    if (Ko && strat == EBB_SCATTER_CHUNK) {
-        // every K row and f row is written exactly once: zero_outputs means overwrite
+    if (Ko && (strat == EBB_SCATTER_CHUNK || strat == EBB_SCATTER_CHUNK_RED)) {
+        // CHUNK: every K row and f row is written exactly once (zero_outputs
+        // means overwrite); CHUNK_RED: rows fed by several tiles are zeroed,
+        // then added to with red.global.add
         if (d->zero_outputs && En) EBB_CUDA(c, cudaMemsetAsync(En->ptr, 0, dtype_size(dt), s));
         return chunk_map_launch(c, d->v, d->e, d->model, En != nullptr, d->zero_outputs ? 0 : 1, nt, V, U, D, W, MU,
-                                LA, Fo, Ko, ne, En, s);
+                                LA, Fo, Ko, ne, En, s, strat == EBB_SCATTER_CHUNK_RED);
     }
     if (Ko && strat == EBB_SCATTER_SEGMENTED) {
         // every K row and f row is written exactly once: zero_outputs means overwrite

@@ -21,7 +21,7 @@ from synth import state as S
 
 pytestmark = pytest.mark.gpu
 
-SCATTERS = {"atomic": 1, "segmented": 4, "color": 5, "chunk": 6}
+SCATTERS = {"atomic": 1, "segmented": 4, "color": 5, "chunk": 6, "chunk_red": 7}
 
 
 @pytest.fixture(scope="module")
@@ -102,7 +102,7 @@ def test_small_blob(ctx, model, scatter):
     assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
 
 
-@pytest.mark.parametrize("scatter", ["segmented", "chunk"])
+@pytest.mark.parametrize("scatter", ["segmented", "chunk", "chunk_red"])
 def test_without_renumbering(ctx, scatter):
     """Scrambled vertex order (no SFC renumbering): tiles are ragged and
     tiny, the plan still covers every row exactly once."""
@@ -233,9 +233,10 @@ def test_chunk_hub_vertex(ctx, nt, monkeypatch):
     for k in ((200, 300) if nt == "128" else (200,)):
         X, tets = _fan(k)
         fem, m, f, K, en = _fem_and_oracle(ctx, X, tets, "nh", f"fanchunk{nt}_{k}")
-        fem.map_forces("nh", scatter=SCATTERS["chunk"])
-        assert rel_l2(fem.f.read(), f) <= 1e-12 and rel_l2(fem.K.read(), K) <= 1e-12
-        assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
+        for sc in ("chunk", "chunk_red"):          # messages / red.global.add into the hub's rows
+            fem.map_forces("nh", scatter=SCATTERS[sc])
+            assert rel_l2(fem.f.read(), f) <= 1e-12 and rel_l2(fem.K.read(), K) <= 1e-12
+            assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)
     monkeypatch.setenv("EBB_CHUNK_NT", "512")
     X3, tets3 = _fan(300)
     fem3, *_ = _fem_and_oracle(ctx, X3, tets3, "nh", f"fanchunk300s_{nt}")

@@ -30,10 +30,10 @@ def _oracle_map(case, m, order, tet_src, model, u=None):
                               e=m.e, ne=m.ne)
 
 
-SCATTERS = {"atomic": 1, "segmented": 4, "color": 5, "chunk": 6}
+SCATTERS = {"atomic": 1, "segmented": 4, "color": 5, "chunk": 6, "chunk_red": 7}
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "segmented", "color", "chunk"])
+@pytest.mark.parametrize("scatter", ["atomic", "segmented", "color", "chunk", "chunk_red"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 @pytest.mark.parametrize("n,mesh", [(4, "kuhn6"), (9, "kuhn6"), (4, "alt5")])
 def test_map_fp64(ctx, model, n, mesh, scatter):
@@ -48,7 +48,7 @@ def test_map_fp64(ctx, model, n, mesh, scatter):
     assert ctx.error_counts(reset=True)["inverted"] == 0
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "segmented", "color", "chunk"])
+@pytest.mark.parametrize("scatter", ["atomic", "segmented", "color", "chunk", "chunk_red"])
 @pytest.mark.parametrize("model", ["stvk", "nh"])
 def test_map_fp32_displacement_form(ctx, model, scatter):
     case = Case(n=8, model=model, spread=0.1)
@@ -105,7 +105,7 @@ def test_map_energy_deterministic(ctx):
     assert fem.energy.get() == e1
 
 
-@pytest.mark.parametrize("scatter", ["atomic", "segmented", "color", "chunk"])
+@pytest.mark.parametrize("scatter", ["atomic", "segmented", "color", "chunk", "chunk_red"])
 def test_map_accumulates_without_zeroing(ctx, scatter):
     """zero_outputs = 0 is the paper's `+=` into existing fields."""
     case = Case(n=4, model="stvk")
@@ -187,9 +187,10 @@ def test_chunk_map_is_bitwise_deterministic(ctx):
         assert fem.energy.get() == e1
 
 
+@pytest.mark.parametrize("scatter", ["chunk", "chunk_red"])
 @pytest.mark.parametrize("nt", ["128", "256", "384", "512"])
 @pytest.mark.parametrize("model,dtype", [("nh", "f64"), ("stvk", "f64"), ("nh", "f32"), ("stvk", "f32")])
-def test_chunk_tile_sizes(ctx, nt, model, dtype, monkeypatch):
+def test_chunk_tile_sizes(ctx, nt, model, dtype, monkeypatch, scatter):
     """Every tile size (tets per CTA) gives the oracle's result: n=9 -> 4374
     tets over 9..35 tiles, the last one ragged, rows spanning many tiles."""
     monkeypatch.setenv("EBB_CHUNK_NT", nt)
@@ -198,10 +199,10 @@ def test_chunk_tile_sizes(ctx, nt, model, dtype, monkeypatch):
         case.u = case.u.astype(np.float32).astype(np.float64)
         case.mu = case.mu.astype(np.float32).astype(np.float64)
         case.lam = case.lam.astype(np.float32).astype(np.float64)
-    fem = gpu_fem(ctx, case, dtype=dtype, name=f"mchunk{nt}{model}{dtype}")
+    fem = gpu_fem(ctx, case, dtype=dtype, name=f"mchunk{nt}{model}{dtype}{scatter}")
     m, new_of_old, tet_src, order = oracle_renumbered(case)
     f, K, en, inv = _oracle_map(case, m, order, tet_src, model)
-    fem.map_forces(model, scatter=SCATTERS["chunk"])
+    fem.map_forces(model, scatter=SCATTERS[scatter])
     tol = 1e-12 if dtype == "f64" else 1e-5
     assert rel_l2(fem.f.read(), f) <= tol
     assert rel_l2(fem.K.read(), K) <= tol
@@ -287,3 +288,23 @@ def test_retired_strategies_refused(ctx, sid):
     fem = gpu_fem(ctx, Case(n=3), name=f"retired{sid}")
     with pytest.raises(EbbError, match="EBB_E_ARG"):
         fem.map_forces("nh", scatter=sid)
+
+
+@pytest.mark.parametrize("grid", ["1", "3"])
+def test_chunk_red_few_ctas_and_repeat(ctx, grid, monkeypatch):
+    """The RED mode of the chunk map (SURVEY strategy (i): rows fed by several
+    tiles zeroed, then red.global.add) on one and three CTAs and on the full
+    grid, twice in a row (the shared rows are re-zeroed every launch): the
+    oracle's result each time (no bitwise claim: RED order varies)."""
+    case = Case(n=12, model="nh", spread=0.1)
+    fem = gpu_fem(ctx, case, name=f"mchunkred{grid}")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    f, K, en, inv = _oracle_map(case, m, order, tet_src, "nh")
+    for env in (None, grid):
+        if env:
+            monkeypatch.setenv("EBB_CHUNK_GRID", env)
+        for _ in range(2):
+            fem.map_forces("nh", scatter=SCATTERS["chunk_red"])
+            assert rel_l2(fem.f.read(), f) <= 1e-12
+            assert rel_l2(fem.K.read(), K) <= 1e-12
+            assert abs(fem.energy.get() - en) <= 1e-12 * abs(en)

@@ -70,7 +70,7 @@ def run_c3(reps, dtypes=("f32", "f64"), models=("stvk", "nh"), target=10_000_000
         bf = 4 if dt == "f32" else 8
         for model in models:
             ids = {"segmented": A.SCATTER_SEGMENTED, "atomic": A.SCATTER_ATOMIC, "color": A.SCATTER_COLOR,
-                   "chunk": A.SCATTER_CHUNK}
+                   "chunk": A.SCATTER_CHUNK, "chunk_red": A.SCATTER_CHUNK_RED}
             for scat in scatters:
                 sid = ids[scat]
                 fem.map_forces(model, scatter=sid)

@@ -41,7 +41,7 @@ def main():
     from synth import state as S
 
     scat = {"atomic": A.SCATTER_ATOMIC, "segmented": A.SCATTER_SEGMENTED, "color": A.SCATTER_COLOR,
-            "chunk": A.SCATTER_CHUNK}
+            "chunk": A.SCATTER_CHUNK, "chunk_red": A.SCATTER_CHUNK_RED}
     ctx = ebb.Context(0)
     for n in ([] if a.peer_only else [int(x) for x in a.sizes.split(",")]):
         X, tets = M.kuhn6(n)

@@ -59,19 +59,38 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def _ncu_traffic(kernel, workload):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full
-    capture of this bench's workload (tools/ncu_traffic.py), else None."""
+def _ncu_entry(kernel, workload):
+    """The committed ncu --set full capture of `kernel` at this bench's
+    workload (profiles/ncu_traffic.json, tools/ncu_traffic.py), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
         e = d.get(f"{workload}:{kernel}") or d[kernel]
         if e.get("workload") == workload:
-            return float(e["dram_bytes_per_launch"])
+            return e
     except Exception:
         pass
     return None
+
+
+def _ncu_traffic(kernel, workload):
+    """DRAM bytes per launch of `kernel` from that capture, else None."""
+    e = _ncu_entry(kernel, workload)
+    return float(e["dram_bytes_per_launch"]) if e else None
+
+
+def _ncu_extra(kernel, workload):
+    """SURVEY §8(d)'s other ncu figures of the same capture: L2 hit rate, L2
+    red / atom sectors, fp64-pipe utilisation (whatever the capture has)."""
+    e = _ncu_entry(kernel, workload)
+    if not e:
+        return None
+    keys = ("l2_hit_rate_pct", "l2_red_sectors", "l2_atom_sectors", "fp64_pipe_pct", "fp64_pipe_inst_pct")
+    out = {k: e[k] for k in keys if k in e}
+    if out:
+        out["capture"] = e.get("capture")
+    return out or None
 
 
 class ClockSampler:
@@ -233,6 +252,20 @@ def _e2e_pipelined(ctx, fem, stream, flush, run_step, u_h, v_h, steps, dev):
     return t0.elapsed_time(t1)
 
 
+def _host_cpu():
+    """The host the oracle ran on (report nproc and the CPU model)."""
+    model = "?"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(steps=CPU_BASELINE_STEPS):
     """The oracle, as it stands, on a bounded sample of the workload (1 thread)."""
     import numpy as np
@@ -251,7 +284,7 @@ def cpu_baseline(steps=CPU_BASELINE_STEPS):
             "sample": f"{steps} full implicit NH step(s) (map + assembly + 50 PCG iterations) of the same "
                       f"recipe on the 1/10-size Kuhn-6 n={SAMPLE_N} cube ({T} tets: the C2 workload); "
                       f"single-threaded C oracle (gcc -O2, generic 4th-order stiffness tensor)",
-            "seconds": dt}
+            "seconds": dt, **_host_cpu()}
 
 
 def run_reference(args, rank, world):
@@ -275,7 +308,7 @@ def run_reference(args, rank, world):
     val = T * args.steps / dt
     cb = {"value": val, "unit": "tets/s", "cores": 1, "kind": "oracle",
           "sample": f"each step = one implicit NH step (map + assembly + 50 PCG its) of the same recipe on the "
-                    f"1/10-size Kuhn-6 n={SAMPLE_N} cube ({T} tets); single-threaded C oracle"}
+                    f"1/10-size Kuhn-6 n={SAMPLE_N} cube ({T} tets); single-threaded C oracle", **_host_cpu()}
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tets/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -423,10 +456,14 @@ def _components(fem, w, kt, t_ms, peak, workload_name):
     if dram is not None and cs["launches"]:
         cg["dram_bytes_per_iter"] = dram / iters
         cg["hbm_frac_dram"] = dram / (cs["avg_us"] * 1e-6) / 1e9 / peak
+    cg_ncu = _ncu_extra("cg_solve", workload_name)
+    if cg_ncu:
+        cg["ncu"] = cg_ncu
+    map_ncu = _ncu_extra("tet_map", workload_name)
     return {
         "map": {"tets_per_s": T / (mp["avg_us"] * 1e-6), "avg_us": mp["avg_us"],
                 "hbm_frac": b_map / (mp["avg_us"] * 1e-6) / 1e9 / peak, "bytes": b_map,
-                "kernel": "k_tet_map_seg (SEGMENTED)"},
+                "kernel": "k_tet_map_seg (SEGMENTED)", **({"ncu": map_ncu} if map_ncu else {})},
         "cg": cg,
         "ms_per_step": t_ms,
     }

@@ -35,7 +35,18 @@ def main():
                 for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     u = units[h.index(m)]
                     b += float(d[m].replace(",", "")) * scale.get(u, 1)
-                acc[key].append((b, name, float(d["gpu__time_duration.sum"].replace(",", ""))))
+                extra = {}
+                for m, k in (("lts__t_sector_hit_rate.pct", "l2_hit_rate_pct"),
+                             ("lts__t_sectors_op_red.sum", "l2_red_sectors"),
+                             ("lts__t_sectors_op_atom.sum", "l2_atom_sectors"),
+                             ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_pct"),
+                             ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64_pipe_inst_pct")):
+                    if m in d and d[m] not in ("", "n/a"):
+                        try:
+                            extra[k] = float(d[m].replace(",", ""))
+                        except ValueError:
+                            pass
+                acc[key].append((b, name, float(d["gpu__time_duration.sum"].replace(",", "")), extra))
     res = {}
     for key, v in acc.items():
         if key == "edge_matvec":
@@ -45,6 +56,7 @@ def main():
         res[f"{workload}:{key}"] = {"workload": workload, "dram_bytes_per_launch": sum(x[0] for x in v) / len(v),
                     "launches_captured": len(v), "ncu_kernel": v[0][1][:100], "capture": os.path.basename(path),
                     "ncu_duration_each": [x[2] for x in v],
+                    **{k: sum(x[3].get(k, 0.0) for x in v) / len(v) for k in v[0][3]},
                     "note": "ncu --set full --clock-control none (replayed, cold cache per pass)"}
     dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
     old = {}

@@ -243,3 +243,38 @@ def test_peer_bind_refuses_bad_arguments(ctx):
     ranks[1].mbox.free()
     with pytest.raises(EbbError, match="EBB_E_STATE"):
         peer.step(1)
+
+
+@pytest.mark.parametrize("variant", ["single", "saad"])
+def test_peer_pcg_blob_mesh(ctx, variant):
+    """The C3 blob (irregular boundary, ragged partitions, vertices of very
+    different degree) over 3 emulated ranks: two consecutive steps equal the
+    single-domain oracle on owned and ghost rows."""
+    from synth import mesh as M
+    from synth import state as S
+
+    from paper_1506_07577_b200 import dist
+    X, tets, n = M.blob(target_T=6_000)
+    free = S.fixed_mask(X, n)
+    u = S.twist_u(X, n, 6, free=free)
+    mu, lam = S.materials(tets.shape[0], 2e5, 0.3, spread=0.1)
+    vel = np.zeros_like(X)
+    new_of_old, tet_src, tets_new = oracle.renumber(X, tets)
+    order = np.argsort(new_of_old)
+    m = oracle.Mesh(X[order], tets_new)
+    uo, vo = u[order], vel[order]
+    for _ in range(2):
+        ref = oracle.implicit_step(m, "nh", uo, vo, mu[tet_src], lam[tet_src], free[order], 1e-2, iters=50)
+        uo, vo = ref["u"], ref["v"]
+    u_ref = np.empty_like(uo)
+    u_ref[order] = uo
+    ranks = []
+    for r in range(3):
+        part = dist.partition_rank(ctx, X, tets, 3, r, name=f"ppblob{variant}p{r}")
+        ranks.append(dist.GpuRank(ctx, r, part, X, free, u, vel, mu, lam, name=f"ppblob{variant}r{r}", nranks=3))
+    peer = dist.PeerPCG(ranks, variant=variant)
+    for _ in range(2):
+        dist.implicit_step(ranks, None, "nh", h=1e-2, iters=50, variant="peer", peer=peer)
+    for R in ranks:
+        ids, gu = R.local_values(R.fem.u)
+        assert rel_l2(gu, u_ref[ids]) <= 1e-8

@@ -520,6 +520,10 @@ typedef struct {
     uint64_t peer_u[EBB_MAX_RANKS], peer_u2[EBB_MAX_RANKS], peer_x[EBB_MAX_RANKS],
              peer_z[EBB_MAX_RANKS], peer_mbox[EBB_MAX_RANKS];
 } ebb_peer_cg;
+/* Mailbox layout (u64 words): [slot 0..1][sender rank 0..15][4] = (d, g,
+ * sequence, unused), then word 128 = this rank's exchange count (epoch).
+ * Exchange k of a rank writes slot k & 1 of every peer's mailbox and
+ * releases its sequence word with k + 1. */
 /* Per-owned-vertex send lists for the fused PCG, built on the device: for
  * each peer k (npeers of them, ranks peers[k]) send_rows[k] (U32 local rows,
  * all < n_owned, e.g. ebb_partition_local's send rows of that peer) and
@@ -553,9 +557,10 @@ ebb_status ebb_ipc_close(ebb_ctx ctx, uint64_t dev_addr);
  * (the PCG of P:946, Jacobi-preconditioned) */
 ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, const ebb_peer_cg* peers,
                             int32_t* group_out);
-/* `iters` single-reduction iterations of every rank of the group in one
- * cooperative launch (the first call after ebb_cg_init adds the z_0 halo,
- * the r.z sum and the w_0 = A z_0 prologue).  Every rank of the job must
+/* `iters` PCG iterations (the bound body) of every rank of the group in one
+ * cooperative launch (the first call after ebb_cg_init adds the r.z sum and
+ * the z_0 halo, and for the single-reduction body the w_0 = A z_0
+ * prologue).  Every rank of the job must
  * call it with the same iters, in the same order.  Stream-ordered,
  * graph-capturable; the bound tol is honoured (the same stop on every
  * rank).  EBB_E_STATE if a field of the group was freed since the bind.

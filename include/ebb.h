@@ -553,7 +553,9 @@ ebb_status ebb_ipc_close(ebb_ctx ctx, uint64_t dev_addr);
  * peers[i].  Validates and uploads the
  * per-rank launch records once (synchronous, not capturable); *group_out is
  * the group id.  ebb_cg.tol is taken here.  EBB_E_SIZE if the ranks' CTAs
- * cannot all be resident.
+ * cannot all be resident or a rank's TMA ring (sized by its largest
+ * 16-vertex chunk of edge rows) does not fit in shared memory -- hub meshes
+ * then use the per-phase driver (ebb_cg_phase), which has unstaged paths.
  * (the PCG of P:946, Jacobi-preconditioned) */
 ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, const ebb_peer_cg* peers,
                             int32_t* group_out);

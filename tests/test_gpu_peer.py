@@ -278,3 +278,27 @@ def test_peer_pcg_blob_mesh(ctx, variant):
     for R in ranks:
         ids, gu = R.local_values(R.fem.u)
         assert rel_l2(gu, u_ref[ids]) <= 1e-8
+
+
+def test_peer_pcg_twenty_steps_track_the_single_domain_solve(ctx):
+    """Long run: 20 consecutive distributed steps (3 emulated ranks, the
+    fused peer PCG, auto body) stay on the single-domain GPU trajectory
+    (TetFEM.implicit_step, the bench's single-GPU path) on every local row --
+    ghost state that drifted a little each step would show up here."""
+    from helpers import gpu_fem
+
+    from paper_1506_07577_b200 import dist
+    case = Case(n=6, model="nh", vel_amp=0.05)
+    fem = gpu_fem(ctx, case, name="pp20ref")
+    ranks = _ranks(ctx, case, 3, "pp20")
+    peer = dist.PeerPCG(ranks)
+    for _ in range(20):
+        fem.implicit_step("nh", h=1e-2, iters=50)
+        dist.implicit_step(ranks, None, "nh", h=1e-2, iters=50, variant="peer", peer=peer)
+    u_ref = fem.to_input_order(fem.u.read())
+    v_ref = fem.to_input_order(fem.vel.read())
+    for R in ranks:
+        ids, gu = R.local_values(R.fem.u)
+        _, gv = R.local_values(R.fem.vel)
+        assert rel_l2(gu, u_ref[ids]) <= 1e-8
+        assert rel_l2(gv, v_ref[ids]) <= 1e-8

@@ -524,9 +524,11 @@ typedef struct {
  * sequence, unused), then word 128 = this rank's exchange count (epoch).
  * Exchange k of a rank writes slot k & 1 of every peer's mailbox and
  * releases its sequence word with k + 1. */
-/* Per-owned-vertex send lists for the fused PCG, built on the device: for
- * each peer k (npeers of them, ranks peers[k]) send_rows[k] (U32 local rows,
- * all < n_owned, e.g. ebb_partition_local's send rows of that peer) and
+/* Per-source-row send lists for the fused PCG and the peer halos, built on
+ * the device: for each peer k (npeers of them, ranks peers[k]) send_rows[k]
+ * (U32 local rows, all < n_owned -- the source rows: owned vertices for the
+ * PCG and COPY halos, every row of the relation for an ADD halo --, e.g.
+ * ebb_partition_local's send rows of that peer) and
  * remote_rows[k] (U32, the same length: the row of each of them in the
  * peer's local numbering, i.e. the peer's recv rows from this rank, which
  * list the same vertices in the same order), each < peer_nv[k].  Creates
@@ -569,23 +571,39 @@ ebb_status ebb_cg_peer_bind(ebb_ctx ctx, int32_t nlocal, const ebb_cg* cgs, cons
  * */
 ebb_status ebb_cg_peer_step(ebb_ctx ctx, int32_t group, int32_t iters, ebb_stream s);
 
-/* Halo of a vertex field over peer memory (SURVEY §8(e) "halo exchange of
- * vertex positions", without NCCL): owners store the rows [0, n_owned) that
- * peers hold as ghosts straight into the peers' copies of `field` (the send
- * lists of ebb_peer_send_csr), then one mailbox exchange; when
- * ebb_peer_halo_push ends on a rank (stream order) its ghost rows are
- * current.  The mailbox may be the one of the rank's fused PCG group (one
- * epoch counter; every rank must issue the same sequence of pushes and PCG
- * steps).  field: element-major (AOS or scalar), any non-key dtype, rows a
- * multiple of 4 bytes.  peer_field[q]: device address, valid on this rank's
- * device, of rank q's copy; [rank] unused.  bind: synchronous, validates;
- * push: stream-ordered, graph-capturable, a cooperative launch. */
+/* Halo of a field over peer memory ("halo exchange of vertex
+ * positions and of the partial force sums", without NCCL).  Two modes:
+ *   EBB_HALO_COPY  owners store the rows [0, n_src) that peers hold as
+ *                  ghosts into the peers' copies of `field` (positions:
+ *                  owners -> ghosts; send lists of ebb_peer_send_csr);
+ *   EBB_HALO_ADD   each rank adds the partial rows it computed for rows
+ *                  another rank owns into the owners' rows with
+ *                  red.global.add over peer memory (the reverse add of
+ *                  partial f / K rows; lists of ebb_partition_reverse made
+ *                  into a send CSR over all rows, n_src = the relation's
+ *                  rows); F32 / F64 fields.
+ * One mailbox exchange first (every rank has reached the push: no peer still
+ * reads a ghost row a COPY overwrites, every owner has written the rows an
+ * ADD adds into), then the stores / REDs, one exchange more: when
+ * ebb_peer_halo_push ends on a rank (stream order) its rows are current.
+ * The mailbox may be the one of the rank's fused PCG group (one epoch
+ * counter; every rank issues the same sequence of pushes and PCG steps).
+ * field: any non-key dtype of 4 / 8-byte elements, element-major or
+ * component-planar (SOA: one element per plane; peer_rows[q] = rank q's
+ * relation rows, its plane stride).  peer_field[q]: device address, valid
+ * on this rank's device, of rank q's copy; [rank] unused.  bind:
+ * synchronous, validates; push: stream-ordered, graph-capturable, a
+ * cooperative launch (no launch for a one-rank job). */
+#define EBB_HALO_COPY 0
+#define EBB_HALO_ADD 1
 typedef struct {
     int32_t nranks, rank;
-    uint64_t n_owned;
+    uint64_t n_src;           /* source rows [0, n_src) (owned vertices for COPY) */
     ebb_field field, send_off, send_dst, mbox;
-    uint64_t peer_field[EBB_MAX_RANKS], peer_mbox[EBB_MAX_RANKS];
+    int32_t mode;             /* EBB_HALO_COPY | EBB_HALO_ADD                    */
+    uint64_t peer_field[EBB_MAX_RANKS], peer_mbox[EBB_MAX_RANKS], peer_rows[EBB_MAX_RANKS];
 } ebb_peer_halo;
+/* (the field reductions of P:885 across ranks) */
 ebb_status ebb_peer_halo_bind(ebb_ctx ctx, int32_t nlocal, const ebb_peer_halo* descs, int32_t* group_out);
 ebb_status ebb_peer_halo_push(ebb_ctx ctx, int32_t group, ebb_stream s);
 

@@ -101,11 +101,15 @@ class PeerCG(C.Structure):
                 ("peer_mbox", C.c_uint64 * MAX_RANKS)]
 
 
+HALO_COPY, HALO_ADD = 0, 1      # EBB_HALO_*
+
+
 class PeerHalo(C.Structure):
     """ebb_peer_halo (include/ebb.h)."""
-    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("n_owned", C.c_uint64), ("field", u32),
-                ("send_off", u32), ("send_dst", u32), ("mbox", u32),
-                ("peer_field", C.c_uint64 * MAX_RANKS), ("peer_mbox", C.c_uint64 * MAX_RANKS)]
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("n_src", C.c_uint64), ("field", u32),
+                ("send_off", u32), ("send_dst", u32), ("mbox", u32), ("mode", C.c_int32),
+                ("peer_field", C.c_uint64 * MAX_RANKS), ("peer_mbox", C.c_uint64 * MAX_RANKS),
+                ("peer_rows", C.c_uint64 * MAX_RANKS)]
 
 
 class ExplicitDesc(C.Structure):

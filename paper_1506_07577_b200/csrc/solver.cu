@@ -16,6 +16,7 @@
 // CG work vectors are padded 4-component records (32 B fp64 / 16 B fp32) so a
 // vertex is one 256-/128-bit access.
 #include <cstdlib>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
@@ -2069,25 +2070,52 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), PEER_MINB)
 }
 
 // ---------------------------------------------------------------------------
-// Halo of a vertex field over peer memory (ebb_peer_halo_push; SURVEY §8(e)
-// "halo exchange of vertex positions"): the owners store the rows peers hold
-// as ghosts straight into the peers' copies of the field, then one mailbox
-// exchange (the same mailboxes and epoch counter as the fused PCG) tells
-// every rank that its ghost rows have arrived; when the kernel ends on a rank
-// its ghosts are current.  Rows are moved as 4-byte words (any dtype / shape
-// of an element-major field).
+// Halo of a field over peer memory (ebb_peer_halo_push; SURVEY §8(e) "halo
+// exchange of vertex positions and of the partial force sums"):
+//   COPY  the owners store the rows peers hold as ghosts straight into the
+//         peers' copies of the field (positions: owners -> ghosts);
+//   ADD   the partial rows this rank computed for rows another rank owns are
+//         added into the owners' rows with red.global.add over peer memory
+//         (the reverse add of partial f / K rows: ghost tails -> owners).
+// One mailbox exchange first (every rank has reached the push, so no peer
+// still reads the ghost rows a COPY overwrites, and every owner has written
+// the rows an ADD adds into), the stores / REDs, a rank barrier, one
+// exchange more: when the kernel ends on a rank its rows are current.  The
+// same mailboxes and epoch counter as the fused PCG.  Element-major fields
+// move rows of `comps` elements; component-planar (SOA) fields one element
+// per plane (plane stride = the relation's rows, the peer's for its copy).
 struct HaloRankArgs {
-    const uint32_t* src;               // the field (row r at src + r * wpr)
-    uint64_t n_owned;
-    uint32_t wpr, pad;                 // 4-byte words per row
+    const void* src;
+    uint64_t n_src;                    // source rows [0, n_src) may send (CSR rows)
+    uint64_t n_rows;                   // rows of the source relation (SOA plane stride)
+    uint32_t comps, esize;             // elements per row, bytes per element (4 | 8)
+    int soa, add, is_f64, pad;
     const uint32_t* send_off;
     const uint2* send_dst;
     unsigned long long* mbox;
     unsigned int* bar;
-    uint32_t* peer_dst[kPeerMax];
+    void* peer_dst[kPeerMax];
+    uint64_t peer_rows[kPeerMax];      // the peers' relation rows (their SOA plane stride)
     unsigned long long* peer_mbox[kPeerMax];
     int rank, nranks;
 };
+
+template <typename T>
+__device__ __forceinline__ void halo_move(const HaloRankArgs& a, const T* src, uint64_t v, const uint2 d) {
+    T* dst = (T*)a.peer_dst[d.x];
+    const uint64_t pr = a.peer_rows[d.x];
+    for (uint32_t c = 0; c < a.comps; ++c) {
+        const T x = a.soa ? src[c * a.n_rows + v] : src[v * a.comps + c];
+        T* p = a.soa ? dst + c * pr + d.y : dst + (uint64_t)d.y * a.comps + c;
+        if constexpr (sizeof(T) == 8 && !std::is_same<T, double>::value) {
+            *p = x;
+        } else if constexpr (sizeof(T) == 4 && !std::is_same<T, float>::value) {
+            *p = x;
+        } else {
+            atomicAdd(p, x);   // float / double: ADD mode only (COPY moves integer words)
+        }
+    }
+}
 
 __global__ void __launch_bounds__(256) k_peer_halo(const HaloRankArgs* __restrict__ recs, unsigned G,
                                                    unsigned long long* __restrict__ err) {
@@ -2095,23 +2123,28 @@ __global__ void __launch_bounds__(256) k_peer_halo(const HaloRankArgs* __restric
     const unsigned lr = blockIdx.x / G, bid = blockIdx.x - lr * G;
     const HaloRankArgs& a = recs[lr];
     const uint64_t epoch = a.mbox[kMbEpoch];
-    const uint32_t wpr = a.wpr;
+    double x0, x1;
+    peer_exchange(a, bid, epoch, 0.0, 0.0, sm2, err, x0, x1);   // every rank is here
     bool sent = false;
-    for (uint64_t v = (uint64_t)bid * blockDim.x + threadIdx.x; v < a.n_owned; v += (uint64_t)G * blockDim.x) {
+    for (uint64_t v = (uint64_t)bid * blockDim.x + threadIdx.x; v < a.n_src; v += (uint64_t)G * blockDim.x) {
         const uint32_t s0 = a.send_off[v], s1 = a.send_off[v + 1];
         if (s0 == s1) continue;
-        const uint32_t* row = a.src + v * wpr;
         for (uint32_t k = s0; k < s1; ++k) {
             const uint2 d = a.send_dst[k];
-            uint32_t* dst = a.peer_dst[d.x] + (uint64_t)d.y * wpr;
-            for (uint32_t w = 0; w < wpr; ++w) dst[w] = row[w];
+            if (!a.add) {
+                if (a.esize == 8) halo_move<unsigned long long>(a, (const unsigned long long*)a.src, v, d);
+                else halo_move<uint32_t>(a, (const uint32_t*)a.src, v, d);
+            } else if (a.is_f64) {
+                halo_move<double>(a, (const double*)a.src, v, d);
+            } else {
+                halo_move<float>(a, (const float*)a.src, v, d);
+            }
         }
         sent = true;
     }
     rank_barrier(a.bar, G, sent);
-    double x0, x1;
-    peer_exchange(a, bid, epoch, 0.0, 0.0, sm2, err, x0, x1);
-    if (bid == 0 && threadIdx.x == 0) a.mbox[kMbEpoch] = epoch + 1;
+    peer_exchange(a, bid, epoch + 1, 0.0, 0.0, sm2, err, x0, x1);   // every rank's rows have landed
+    if (bid == 0 && threadIdx.x == 0) a.mbox[kMbEpoch] = epoch + 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -3382,33 +3415,42 @@ ebb_status ebb_peer_halo_bind(ebb_ctx ctx, int32_t nlocal, const ebb_peer_halo* 
         for (int j = 0; j < i; ++j)
             if (descs[j].rank == d->rank) return fail(c, EBB_E_ARG, "halo_bind: rank %d bound twice", d->rank);
         Field* F = get_field(c, d->field);
-        if (!F || F->dtype == EBB_KEY || (F->layout != EBB_AOS && F->comps() != 1))
-            return fail(c, EBB_E_TYPE, "halo_bind: the field must be an element-major, non-key field");
-        const size_t rb = F->comps() * dtype_size(F->dtype);
-        if (rb % 4) return fail(c, EBB_E_TYPE, "halo_bind: rows must be a multiple of 4 bytes");
-        if (d->n_owned > c->rels[F->rel].size) return fail(c, EBB_E_SIZE, "halo_bind: n_owned exceeds the rows");
+        if (!F || F->dtype == EBB_KEY) return fail(c, EBB_E_TYPE, "halo_bind: bad or key field");
+        const size_t es = dtype_size(F->dtype);
+        if (es != 4 && es != 8) return fail(c, EBB_E_TYPE, "halo_bind: elements must be 4 or 8 bytes");
+        if (d->mode != EBB_HALO_COPY && d->mode != EBB_HALO_ADD) return fail(c, EBB_E_ARG, "halo_bind: bad mode");
+        if (d->mode == EBB_HALO_ADD && F->dtype != EBB_F64 && F->dtype != EBB_F32)
+            return fail(c, EBB_E_TYPE, "halo_bind: EBB_HALO_ADD needs an F32 / F64 field");
+        if (d->n_src > c->rels[F->rel].size) return fail(c, EBB_E_SIZE, "halo_bind: n_src exceeds the rows");
         Field* SO = get_field(c, d->send_off);
         Field* SD = get_field(c, d->send_dst);
         Field* MB = get_field(c, d->mbox);
-        if (!SO || SO->dtype != EBB_U32 || SO->comps() != 1 || c->rels[SO->rel].size != d->n_owned + 1)
-            return fail(c, EBB_E_TYPE, "halo_bind: send_off must be a U32 field of n_owned + 1 rows");
+        if (!SO || SO->dtype != EBB_U32 || SO->comps() != 1 || c->rels[SO->rel].size != d->n_src + 1)
+            return fail(c, EBB_E_TYPE, "halo_bind: send_off must be a U32 field of n_src + 1 rows");
         if (!SD || SD->dtype != EBB_U32 || SD->comps() != 2)
             return fail(c, EBB_E_TYPE, "halo_bind: send_dst must be a U32 2x1 field");
         if (!MB || MB->dtype != EBB_F64 || MB->comps() != 1 || c->rels[MB->rel].size < EBB_PEER_MBOX_WORDS)
             return fail(c, EBB_E_TYPE, "halo_bind: mbox must be an F64 field of >= %d rows", EBB_PEER_MBOX_WORDS);
         for (int q = 0; q < d->nranks; ++q)
-            if (q != d->rank && (!d->peer_field[q] || !d->peer_mbox[q]))
-                return fail(c, EBB_E_ARG, "halo_bind: rank %d: missing buffer address of peer %d", d->rank, q);
+            if (q != d->rank && (!d->peer_field[q] || !d->peer_mbox[q] ||
+                                 (F->layout == EBB_SOA && F->comps() > 1 && !d->peer_rows[q])))
+                return fail(c, EBB_E_ARG, "halo_bind: rank %d: missing buffer address / rows of peer %d", d->rank, q);
         HaloRankArgs& a = h[i];
         memset(&a, 0, sizeof(a));
-        a.src = (const uint32_t*)F->ptr;
-        a.n_owned = d->n_owned;
-        a.wpr = (uint32_t)(rb / 4);
+        a.src = F->ptr;
+        a.n_src = d->n_src;
+        a.n_rows = c->rels[F->rel].size;
+        a.comps = F->comps();
+        a.esize = (uint32_t)es;
+        a.soa = F->layout == EBB_SOA && F->comps() > 1;
+        a.add = d->mode == EBB_HALO_ADD;
+        a.is_f64 = F->dtype == EBB_F64;
         a.send_off = (const uint32_t*)SO->ptr;
         a.send_dst = (const uint2*)SD->ptr;
         a.mbox = (unsigned long long*)MB->ptr;
         for (int q = 0; q < d->nranks; ++q) {
-            a.peer_dst[q] = (uint32_t*)(uintptr_t)d->peer_field[q];
+            a.peer_dst[q] = (void*)(uintptr_t)d->peer_field[q];
+            a.peer_rows[q] = d->peer_rows[q];
             a.peer_mbox[q] = (unsigned long long*)(uintptr_t)d->peer_mbox[q];
         }
         a.rank = d->rank;

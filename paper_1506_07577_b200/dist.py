@@ -146,22 +146,33 @@ class LocalTransport:
 
 
 # ----------------------------------------------------------------------------- driver
-def _map_assemble(ranks, transport, model, h, alpha, beta, g):
+def _reverse_add(ranks, transport, peer_rev):
+    """The partial f and K rows of ghost tails into their owners: the peer
+    RED pushes (``peer_rev`` = (PeerHalo "rf", PeerHalo "rK")) or two
+    transport exchanges."""
+    if peer_rev is not None:
+        for hp in peer_rev:
+            hp.push()
+        return
+    for which in ("rf", "rK"):
+        for R in ranks:
+            R.set_halo(which)
+        transport.exchange(ranks)
+
+
+def _map_assemble(ranks, transport, model, h, alpha, beta, g, peer_rev=None):
     """The element map on every rank; with the reverse-add variant the partial
-    f and K rows of ghost tails are added into their owners (two exchanges)
-    before the assembly reads them."""
+    f and K rows of ghost tails are added into their owners before the
+    assembly reads them."""
     for R in ranks:
         R.map_forces(model)
     if getattr(ranks[0], "map_variant", "overlap") == "reverse":
-        for which in ("rf", "rK"):
-            for R in ranks:
-                R.set_halo(which)
-            transport.exchange(ranks)
+        _reverse_add(ranks, transport, peer_rev)
     for R in ranks:
         R.assemble(h, alpha, beta, g)
 
 
-def map_step(ranks, transport, model="stvk", halo=None):
+def map_step(ranks, transport, model="stvk", halo=None, peer_rev=None):
     """The distributed element map alone (BASELINE configs[2]: the force +
     stiffness map with halo exchange): the owners' displacements go to their
     ghost copies (the position halo, owners -> ghosts), then every rank maps
@@ -178,14 +189,11 @@ def map_step(ranks, transport, model="stvk", halo=None):
     for R in ranks:
         R.map_forces(model)
     if getattr(ranks[0], "map_variant", "overlap") == "reverse":
-        for which in ("rf", "rK"):
-            for R in ranks:
-                R.set_halo(which)
-            transport.exchange(ranks)
+        _reverse_add(ranks, transport, peer_rev)
 
 
 def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, beta=0.0, g=(0.0, -9.81, 0.0),
-                  variant="saad", peer=None):
+                  variant="saad", peer=None, peer_rev=None):
     """One distributed implicit step (O9 + O10) over `ranks` (the local ones).
 
     variant="saad": per iteration DIR, MATVEC, [sum p.q], UPDATE, [sum r.z,
@@ -207,7 +215,7 @@ def implicit_step(ranks, transport, model="nh", h=1e-2, iters=50, alpha=0.0, bet
     x (and z_0) into their peers' ghost rows and the two scalars go through
     peer mailboxes inside the kernel -- no host loop, no NCCL call, no
     transport (``transport`` is used only by the reverse-add map)."""
-    _map_assemble(ranks, transport, model, h, alpha, beta, g)
+    _map_assemble(ranks, transport, model, h, alpha, beta, g, peer_rev)
     if variant == "peer":
         # the fused multi-GPU PCG: one kernel for every iteration (and the
         # z_0 / u / x halos and the scalar sums inside it); `peer` is the
@@ -435,6 +443,7 @@ class GpuRank:
             lists.append(d)
         self._make_lists("rf", fem.verts.name + ".rev", lists[0], lists[1], (3,))
         self._make_lists("rK", fem.verts.name + ".rev", lists[2], lists[3], (9,))
+        self.rev_lists = {"rf": (lists[0], lists[1]), "rK": (lists[2], lists[3])}   # (send, recv) rows per peer
         # the own-tet subset: its own relation with keys into the local verts / edges
         sel = np.nonzero(own)[0]
         self.n_map_tets = int(sel.size)
@@ -512,7 +521,15 @@ class GpuRank:
                                                       self.fem.vel.h, _stream(self.stream)))
 
     # -- fused PCG over peer memory (PeerPCG)
-    def peer_export(self, ipc, extra=None):
+    def _list_rows(self, lists):
+        """(send, recv) rows per peer and the relation rows of a list set:
+        "fwd" (vertex halo), "rf" / "rK" (reverse add of forces / K rows)."""
+        if lists == "fwd":
+            return self.part_send, self.part_recv, int(self.fem.nv)
+        send, recv = self.rev_lists[lists]
+        return send, recv, int(self.fem.nv if lists == "rf" else self.fem.ne)
+
+    def peer_export(self, ipc, extra=None, lists="fwd"):
         """What peers need of this rank: its recv rows per peer (numpy), its
         local vertex count, send-list lengths, and its ghost-row targets
         (cg.u, cg.u2, cg.x = dv, cg.z, the mailbox) as device addresses
@@ -536,12 +553,13 @@ class GpuRank:
                 v = A.View()
                 self.ctx.check(self.ctx.L.ebb_field_view(self.ctx.h, int(fh), C.byref(v)))
                 buf[name] = int(v.data)
-        return dict(rank=self.rank, nv=int(self.fem.nv), send={q: int(len(r)) for q, r in self.part_send.items()},
-                    recv={q: np.asarray(r, np.int64) for q, r in self.part_recv.items()}, buf=buf)
+        send, recv, nrows = self._list_rows(lists)
+        return dict(rank=self.rank, nv=nrows, send={q: int(len(r)) for q, r in send.items()},
+                    recv={q: np.asarray(r, np.int64) for q, r in recv.items()}, buf=buf)
 
-    def peer_send_csr(self, peers, remote, peer_nv):
-        """ebb_peer_send_csr over this rank's send lists (fields of the halo
-        lists) and the peers' rows of the same vertices."""
+    def peer_send_csr(self, peers, remote, peer_nv, lists="fwd"):
+        """ebb_peer_send_csr over this rank's send lists of a list set (fields
+        of the halo lists) and the peers' rows of the same rows."""
         import ctypes as C
 
         from . import _abi as A
@@ -554,18 +572,24 @@ class GpuRank:
             rel = self.ctx.relation(f"{tag}.remote{q}", max(len(rows), 1))
             self._remote_rels.append(rel)
             rf.append(rel.field("rows", "u32", init=np.asarray(rows, np.uint32)).h)
-            sf.append(self._lists["fwd"]["send"][q][0].h)
+            sf.append(self._lists[lists]["send"][q][0].h)
         off, dst = C.c_uint32(), C.c_uint32()
+        n_src = self.n_owned if lists == "fwd" else self._list_rows(lists)[2]
         self.ctx.check(self.ctx.L.ebb_peer_send_csr(
-            self.ctx.h, self.n_owned, n, (C.c_int32 * max(n, 1))(*peers), (A.u32 * max(n, 1))(*sf),
+            self.ctx.h, n_src, n, (C.c_int32 * max(n, 1))(*peers), (A.u32 * max(n, 1))(*sf),
             (A.u32 * max(n, 1))(*rf), (C.c_uint64 * max(n, 1))(*peer_nv), tag.encode(),
             C.byref(off), C.byref(dst)))
         from .ebb import Field
-        self.peer_off = Field(self.ctx, off.value, None, "off", "u32", (1, 1), A.AOS)
-        self.peer_off.count = self.n_owned + 1
-        self.peer_dst = Field(self.ctx, dst.value, None, "dst", "u32", (2, 1), A.AOS)
-        self.peer_dst.count = max(sum(len(r) for r in remote), 1)
-        return self.peer_off, self.peer_dst
+        po = Field(self.ctx, off.value, None, "off", "u32", (1, 1), A.AOS)
+        po.count = n_src + 1
+        pd = Field(self.ctx, dst.value, None, "dst", "u32", (2, 1), A.AOS)
+        pd.count = max(sum(len(r) for r in remote), 1)
+        if not hasattr(self, "peer_csr"):
+            self.peer_csr = {}
+        self.peer_csr[lists] = (po, pd, n_src)
+        if lists == "fwd":
+            self.peer_off, self.peer_dst = po, pd
+        return po, pd
 
     # -- transport hooks
     def scal_tensor(self):
@@ -680,7 +704,7 @@ class PeerPCG:
         pcs = (A.PeerCG * len(self.ranks))()
         for i, R in enumerate(self.ranks):
             t = tables[R.rank]
-            if getattr(R, "peer_off", None) is None:      # one send CSR per rank (a property of the partition)
+            if "fwd" not in getattr(R, "peer_csr", {}):   # one send CSR per rank (a property of the partition)
                 R.peer_send_csr(t["peers"], t["remote"], t["peer_nv"])
             off, dst = R.peer_off, R.peer_dst
             pc = pcs[i]
@@ -722,7 +746,7 @@ class PeerPCG:
         self.group = None
 
 
-def _gather_infos(ranks, comm, extra):
+def _gather_infos(ranks, comm, extra, lists="fwd"):
     """Every rank's peer infos (local: direct; one process per GPU: through
     all_gather_object) and the job's rank count."""
     ipc = comm is not None
@@ -731,23 +755,25 @@ def _gather_infos(ranks, comm, extra):
         nranks = tdist.get_world_size(comm)
         (R0,) = ranks
         gathered = [None] * nranks
-        tdist.all_gather_object(gathered, R0.peer_export(ipc=True, extra=extra(R0)), group=comm)
+        tdist.all_gather_object(gathered, R0.peer_export(ipc=True, extra=extra(R0), lists=lists), group=comm)
         infos = {d["rank"]: d for d in gathered}
     else:
         nranks = len(ranks)
-        infos = {R.rank: R.peer_export(ipc=False, extra=extra(R)) for R in ranks}
+        infos = {R.rank: R.peer_export(ipc=False, extra=extra(R), lists=lists) for R in ranks}
     if sorted(infos) != list(range(nranks)):
         raise ValueError(f"peer ranks {sorted(infos)} are not 0..{nranks - 1}")
     return infos, nranks
 
 
 class PeerHalo:
-    """The ghost rows of a vertex field over peer memory
-    (``ebb_peer_halo_bind`` / ``ebb_peer_halo_push``, SURVEY §8(e) "halo
-    exchange of vertex positions"): owners store their boundary rows into
-    the peers' copies, one mailbox exchange (shared with the ranks' PeerPCG
-    epoch counter) ends the push.  which: a key of ``GpuRank.halo_fields``
-    ("disp" = the displacement u).  comm as for ``PeerPCG``."""
+    """A halo of a field over peer memory (``ebb_peer_halo_bind`` /
+    ``ebb_peer_halo_push``, SURVEY §8(e) "halo exchange of vertex positions
+    and of the partial force sums").  which = "disp" (the displacements u,
+    owners -> ghosts, copy), or "rf" / "rK" (map_variant="reverse": the
+    partial force / stiffness rows of ghost tails added into their owners
+    with red.global.add over peer memory).  One mailbox exchange before and
+    one after the stores (shared with the ranks' PeerPCG epoch counter).
+    comm as for ``PeerPCG``."""
 
     def __init__(self, ranks, which="disp", comm=None, stream=None):
         import ctypes as C
@@ -756,17 +782,26 @@ class PeerHalo:
         self.ranks, self.ctx, self.stream = list(ranks), ranks[0].ctx, stream
         ctx = self.ctx
         ipc = comm is not None
-        infos, nranks = _gather_infos(self.ranks, comm, lambda R: {"halo": R.halo_fields[which].h})
+        add = which in ("rf", "rK")
+        lists = which if add else "fwd"
+        field_of = (lambda R: R.fem.f) if which == "rf" else (lambda R: R.fem.K) if which == "rK" else \
+            (lambda R: R.halo_fields[which])
+        infos, nranks = _gather_infos(self.ranks, comm, lambda R: {"halo": field_of(R).h}, lists=lists)
         tables = peer_tables(infos, [R.rank for R in self.ranks], nranks, names=("halo", "mbox"))
         self._opened = []
         ds = (A.PeerHalo * len(self.ranks))()
         for i, R in enumerate(self.ranks):
             t = tables[R.rank]
-            if getattr(R, "peer_off", None) is None:
-                R.peer_send_csr(t["peers"], t["remote"], t["peer_nv"])
+            if lists not in getattr(R, "peer_csr", {}):
+                R.peer_send_csr(t["peers"], t["remote"], t["peer_nv"], lists=lists)
+            off, dst, n_src = R.peer_csr[lists]
             d = ds[i]
-            d.nranks, d.rank, d.n_owned = nranks, R.rank, R.n_owned
-            d.field, d.send_off, d.send_dst, d.mbox = R.halo_fields[which].h, R.peer_off.h, R.peer_dst.h, R.mbox.h
+            d.nranks, d.rank, d.n_src = nranks, R.rank, n_src
+            d.field, d.send_off, d.send_dst, d.mbox = field_of(R).h, off.h, dst.h, R.mbox.h
+            d.mode = A.HALO_ADD if add else A.HALO_COPY
+            for q in range(nranks):
+                if q != R.rank:
+                    d.peer_rows[q] = int(infos[q]["nv"])
             for name, arr in (("halo", d.peer_field), ("mbox", d.peer_mbox)):
                 for q, b in enumerate(t["bufs"][name]):
                     if b is None:

@@ -251,7 +251,9 @@ def test_distributed_map_step(ctx, P, model, dtype, map_variant, halo):
     K p for a seeded global p (each owned row of K p uses the whole row).
     The ranks start from stale ghost displacements (zeros), so the halo
     exchange is what makes the ghost tets right.  halo="peer": the position
-    halo as the peer-memory push kernel (ebb_peer_halo_push), the ranks
+    halo as the peer-memory push kernel (ebb_peer_halo_push, COPY) and, for
+    the reverse variant, the partial f / K rows added into their owners with
+    red.global.add over peer memory (ADD) -- no transport at all; the ranks
     emulated in one cooperative launch."""
     from paper_1506_07577_b200 import dist
     case = Case(n=5, model=model, spread=0.1)
@@ -276,7 +278,9 @@ def test_distributed_map_step(ctx, P, model, dtype, map_variant, halo):
         R.fem.u.write(uu)
         ranks.append(R)
     ph = dist.PeerHalo(ranks) if halo == "peer" else None
-    dist.map_step(ranks, dist.LocalTransport(), model, halo=ph)
+    prev = (dist.PeerHalo(ranks, "rf"), dist.PeerHalo(ranks, "rK")) if halo == "peer" and map_variant == "reverse" \
+        else None                                               # the reverse add as peer-memory REDs
+    dist.map_step(ranks, None if halo == "peer" else dist.LocalTransport(), model, halo=ph, peer_rev=prev)
     assert ctx.error_counts()["peer_timeouts"] == 0
     tol = 1e-12 if dtype == "f64" else 1e-5
     f_in = np.full((m.nv, 3), np.nan)

@@ -87,11 +87,13 @@ def test_peer_pcg_three_steps_owned_and_ghost_rows(ctx, P, map_variant, variant)
         u, v = ref["u"], ref["v"]
     ranks = _ranks(ctx, case, P, f"pp3{P}{map_variant}{variant}", map_variant)
     peer = dist.PeerPCG(ranks, variant=variant)
-    transport = dist.LocalTransport()            # the reverse-add map's exchange only
+    # reverse variant: the partial f / K rows of ghost tails go to their
+    # owners as peer-memory REDs (PeerHalo ADD) -- no transport anywhere
+    prev = (dist.PeerHalo(ranks, "rf"), dist.PeerHalo(ranks, "rK")) if map_variant == "reverse" else None
     u_in, v_in = np.empty_like(u), np.empty_like(v)
     u_in[order], v_in[order] = u, v
     for _ in range(steps):
-        dist.implicit_step(ranks, transport, "nh", h=h, iters=iters, variant="peer", peer=peer)
+        dist.implicit_step(ranks, None, "nh", h=h, iters=iters, variant="peer", peer=peer, peer_rev=prev)
     nghost = 0
     for R in ranks:
         ids, gu = R.local_values(R.fem.u)

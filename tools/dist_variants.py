@@ -55,7 +55,7 @@ def main():
                 R.map_forces(w["model"])
             torch.cuda.synchronize()
             ctx.timing(True)
-            map_us, ex_us = [], 0.0
+            map_us, ex_us, peer_rev_us = [], 0.0, None
             for R in ranks:
                 ctx.timing_read(A.K_TET_MAP, reset=True)
                 for _ in range(a.reps):
@@ -81,6 +81,20 @@ def main():
                     ev[1].synchronize()
                     tot += ev[0].elapsed_time(ev[1])
                 ex_us = 1e3 * tot / a.reps / P      # all P ranks' exchanges run one after the other here
+                # the same reverse add as peer-memory REDs (PeerHalo ADD, all ranks in one launch per list)
+                prev = (dist.PeerHalo(ranks, "rf"), dist.PeerHalo(ranks, "rK"))
+                for hp in prev:
+                    hp.push()                     # warm-up
+                tot = 0.0
+                for _ in range(a.reps):
+                    flush.zero_()
+                    ev[0].record()
+                    for hp in prev:
+                        hp.push()
+                    ev[1].record()
+                    ev[1].synchronize()
+                    tot += ev[0].elapsed_time(ev[1])
+                peer_rev_us = 1e3 * tot / a.reps
             ctx.timing(False)
             # one whole distributed implicit step (map, reverse add, assembly,
             # 50 PCG iterations, halos, allreduces) per PCG driver; all P ranks
@@ -98,6 +112,25 @@ def main():
                     ev[1].synchronize()
                     tot += ev[0].elapsed_time(ev[1])
                 step_ms[cg] = tot / 2 / P
+            # the transport-free step: the fused peer PCG (+ the peer RED
+            # reverse add); the PCG of all ranks is ONE launch here
+            pcg = dist.PeerPCG(ranks)
+            prv = (dist.PeerHalo(ranks, "rf"), dist.PeerHalo(ranks, "rK")) if variant == "reverse" else None
+
+            def peer_step():
+                dist.implicit_step(ranks, None, w["model"], h=w["h"], iters=w["cg_iters"], variant="peer", peer=pcg,
+                                   peer_rev=prv)
+            peer_step()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            tot = 0.0
+            for _ in range(2):
+                flush.zero_()
+                ev[0].record()
+                peer_step()
+                ev[1].record()
+                ev[1].synchronize()
+                tot += ev[0].elapsed_time(ev[1])
+            peer_step_ms_total = tot / 2
             bf = 8
             halo_rows = [sum(b[1][3][1].shape[0] for b in R._lists["fwd"]["send"].values()) for R in ranks]
             line = {"P": P, "variant": variant, "global_tets": int(tets.shape[0]), "n": n,
@@ -107,7 +140,9 @@ def main():
                     "reverse_bytes_per_rank": [int(R.rev_bytes["rf"] + R.rev_bytes["rK"]) for R in ranks]
                     if variant == "reverse" else None,
                     "reverse_exchange_us_per_rank": ex_us if variant == "reverse" else None,
+                    "reverse_add_peer_red_us_all_ranks": peer_rev_us if variant == "reverse" else None,
                     "step_ms_per_rank": step_ms,
+                    "peer_step_ms_all_ranks": peer_step_ms_total, "peer_pcg_body": pcg.variant,
                     "pcg_iter_us_per_rank_incl_halo": {k: 1e3 * v / w["cg_iters"] for k, v in step_ms.items()},
                     "fwd_halo_rows_per_rank": halo_rows,
                     "fwd_halo_bytes_per_iteration_per_rank": [r_ * 4 * bf for r_ in halo_rows],

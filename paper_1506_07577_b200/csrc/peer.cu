@@ -1,8 +1,9 @@
 // peer.cu -- host side of the fused multi-GPU PCG over peer memory (SURVEY
 // §8(e): the halo of the gathered CG operand and the allreduce of the CG
-// scalars without NCCL on the iteration path; the kernel is k_cg1_peer in
-// solver.cu): the per-owned-vertex send lists (a CSR over the owned rows,
-// built on the device from the per-peer halo lists of ebb_partition_local)
+// scalars without NCCL on the iteration path; the kernels are in
+// peer_cg.cu): the per-source-row send lists (a CSR over the source rows,
+// built on the device from the per-peer halo lists of ebb_partition_local /
+// ebb_partition_reverse)
 // and CUDA IPC of library fields (one process per GPU maps its peers'
 // buffers; ranks emulated on one device use the fields' own addresses).
 #include <cub/cub.cuh>

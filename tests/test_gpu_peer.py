@@ -240,6 +240,15 @@ def test_peer_bind_refuses_bad_arguments(ctx):
     q = sorted(R.part_send)[0]
     with pytest.raises(EbbError, match="EBB_E_RANGE"):
         R.peer_send_csr([q], [np.full(len(R.part_send[q]), 10 ** 6)], [ranks[q].fem.nv])
+    with pytest.raises(EbbError, match="EBB_E_SIZE"):          # remote list of another length
+        R.peer_send_csr([q], [np.zeros(len(R.part_send[q]) + 1, np.int64)], [ranks[q].fem.nv])
+    # a halo group is not a PCG group and vice versa
+    halo = dist.PeerHalo(ranks)
+    with pytest.raises(EbbError, match="EBB_E_ARG"):
+        ctx.check(L.ebb_cg_peer_step(h, halo.group, 1, None))
+    pcg = dist.PeerPCG(ranks)
+    with pytest.raises(EbbError, match="EBB_E_ARG"):
+        ctx.check(L.ebb_peer_halo_push(h, pcg.group, None))
     # a group whose field was freed refuses to launch
     peer = dist.PeerPCG(ranks)
     ranks[1].mbox.free()

@@ -40,10 +40,17 @@ __device__ __forceinline__ void seg_load(uint32_t t, uint4 v, uint64_t nt, const
                                          const R* __restrict__ mu_t, const R* __restrict__ lam_t, SegIn<R>& in) {
     if (t == 0xFFFFFFFFu) return;
     const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#ifdef SEG_NO_GATHER   // measurement-only build: no u gathers (wrong results)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) in.uu[k][a] = R(1e-4) * (R)((vv[k] + a) & 15);
+#else
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int a = 0; a < 3; ++a) in.uu[k][a] = __ldg(u + 3ull * vv[k] + a);
+#endif
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll

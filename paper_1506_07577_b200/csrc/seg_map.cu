@@ -320,6 +320,9 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
                 R* dst = K + item.y;
 #pragma unroll
                 for (int q = 0; q < 9; ++q, dst += ne) *dst = accumulate ? *dst + a9[q] : a9[q];
+#ifdef SEG_NO_KSTORE_T   // measurement-only build: the transposed-row stores alone skipped
+                if (kind == 0 && a9[0] == R(12345.678)) K[item.z] = a9[1];
+#else
                 if (kind == 0) {
                     dst = K + item.z;
 #pragma unroll
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
 #pragma unroll
                         for (int c = 0; c < 3; ++c, dst += ne) *dst = accumulate ? *dst + a9[3 * c + a] : a9[3 * c + a];
                 }
+#endif
 #endif
             }
         }

@@ -316,6 +316,19 @@ __global__ void __launch_bounds__(NT, seg_min_blocks<R, NT>()) k_tet_map_seg(
                 }
 #ifdef SEG_NO_KSTORE   // measurement-only build: the cost of the scattered K row stores
                 if (a9[0] == R(12345.678)) K[item.y] = a9[1];
+#elif defined(SEG_KAOS_PROBE)   // measurement-only build: K rows element-major (72 contiguous bytes)
+                {
+                    R* dst = K + 9ull * item.y;
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) dst[q] = a9[q];
+                    if (kind == 0) {
+                        dst = K + 9ull * item.z;
+#pragma unroll
+                        for (int a = 0; a < 3; ++a)
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) dst[3 * a + c] = a9[3 * c + a];
+                    }
+                }
 #else
                 R* dst = K + item.y;
 #pragma unroll

@@ -996,11 +996,13 @@ __global__ void k_compress_upper(uint64_t nu, uint64_t ne, const uint32_t* __res
 // of each vertex applies every recurrence as it finishes the vertex's row.
 // Only u is read by neighbours (double-buffered); the rest is owner-local.
 // The first call after ebb_cg_init runs one extra matvec (w_0 = A z_0).
-// (no min-blocks in the launch bounds: ptxas then keeps 72 registers, 3 CTAs
-// per SM; an explicit min-blocks of 1 let it take 148 and ran 1.5x slower)
+// The body is shared by two kernels that differ only in their launch bounds
+// (measured, profiles/r02_cg1_launch_bounds.jsonl): fp64 with min 3 CTAs per
+// SM (72 registers, no spills; without a min-blocks ptxas keeps 72 but
+// spills 56 bytes and runs 2.7 % slower at C2; min 1 takes 146 and runs
+// 1.45x slower), fp32 without one (72 registers, no spills).
 template <typename R>
-__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
-    k_cg1_persistent(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
+__device__ __forceinline__ void cg1_persistent_body(uint64_t nv, const uint32_t* __restrict__ index, const uint32_t* __restrict__ head,
                      const R* __restrict__ A, uint64_t ne, const R* __restrict__ dinv, R* __restrict__ x,
                      R* __restrict__ r, const R* __restrict__ z0, R* __restrict__ p, R* __restrict__ sv,
                      R* __restrict__ yv, R* __restrict__ wv, R* ub0, R* ub1, const uint8_t* __restrict__ mask,
@@ -1264,6 +1266,34 @@ __global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1))
         scal[S_FIRST] = first ? 1.0 : 0.0;
         scal[S_PAR] = par ? 1.0 : 0.0;
     }
+}
+
+#define EBB_CG1_PARAMS                                                                                              \
+    uint64_t nv, const uint32_t *__restrict__ index, const uint32_t *__restrict__ head, const R *__restrict__ A,  \
+        uint64_t ne, const R *__restrict__ dinv, R *__restrict__ x, R *__restrict__ r, const R *__restrict__ z0,    \
+        R *__restrict__ p, R *__restrict__ sv, R *__restrict__ yv, R *__restrict__ wv, R *ub0, R *ub1,              \
+        const uint8_t *__restrict__ mask, double *__restrict__ part_g, double *__restrict__ part_d,                  \
+        unsigned int *__restrict__ bar_count, unsigned int *__restrict__ bar_gen, double *__restrict__ scal,        \
+        double *__restrict__ rho_user, unsigned long long *__restrict__ err, uint32_t cap, int iters, double tol2,   \
+        int dist
+#define EBB_CG1_ARGS                                                                                                \
+    nv, index, head, A, ne, dinv, x, r, z0, p, sv, yv, wv, ub0, ub1, mask, part_g, part_d, bar_count, bar_gen,     \
+        scal, rho_user, err, cap, iters, tol2, dist
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1), 3) k_cg1_persistent_f64(EBB_CG1_PARAMS) {
+    cg1_persistent_body<R>(EBB_CG1_ARGS);
+}
+template <typename R>
+__global__ void __launch_bounds__(32 * (TMA_CONSUMERS + 1)) k_cg1_persistent_f32(EBB_CG1_PARAMS) {
+    cg1_persistent_body<R>(EBB_CG1_ARGS);
+}
+#undef EBB_CG1_PARAMS
+#undef EBB_CG1_ARGS
+// the kernel of a dtype
+template <typename R>
+constexpr auto cg1_kernel() {
+    if constexpr (sizeof(R) == 8) return k_cg1_persistent_f64<R>;
+    else return k_cg1_persistent_f32<R>;
 }
 
 // ---------------------------------------------------------------------------
@@ -1778,12 +1808,12 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     static thread_local size_t configured_dev[kMaxDevices] = {};
     size_t& configured = configured_dev[c->device % kMaxDevices];
     if (smem > configured) {
-        EBB_CUDA(c, cudaFuncSetAttribute(k_cg1_persistent<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        EBB_CUDA(c, cudaFuncSetAttribute(cg1_kernel<R>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
     const int block = 32 * (TMA_CONSUMERS + 1);
     int nb = 0;
-    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cg1_persistent<R>, block, smem));
+    EBB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cg1_kernel<R>(), block, smem));
     if (nb < 1) return fail(c, EBB_E_CUDA, "cg: persistent kernel does not fit on an SM");
     const uint64_t nch = (G.nv + TMA_VCH - 1) / TMA_VCH;
     uint64_t grid = (uint64_t)nb * c->num_sms;
@@ -1800,7 +1830,7 @@ ebb_status cg1_launch(Ctx* c, const ebb_cg* cg, const EdgeGraph& G, int iters, c
     cfg.attrs = at;
     cfg.numAttrs = 1;
     KernelTimer kt(c, EBB_K_CG_SOLVE, s);
-    EBB_CUDA(c, cudaLaunchKernelEx(&cfg, k_cg1_persistent<R>, G.nv, G.index, G.head, (const R*)c->fields[cg->A].ptr,
+    EBB_CUDA(c, cudaLaunchKernelEx(&cfg, cg1_kernel<R>(), G.nv, G.index, G.head, (const R*)c->fields[cg->A].ptr,
                                    G.ne, (const R*)c->fields[cg->dinv].ptr, F(cg->x), F(cg->r), (const R*)F(cg->z),
                                    F(cg->p), F(cg->s), F(cg->y), F(cg->w), F(cg->u), F(cg->u2), mask, c->d_partials,
                                    c->d_partials + 4096, c->d_counter + 10, c->d_counter + 11,

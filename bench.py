@@ -696,6 +696,10 @@ def run_dist(args, rank, world, local_rank):
     dist.barrier()
     launches = ctx.launch_count(reset=True)
     errs = ctx.error_counts(reset=True)
+    if errs.get("peer_timeouts"):
+        # a peer never arrived at a mailbox exchange: the numbers would be
+        # those of an abandoned solve -- fail loudly instead of reporting them
+        raise RuntimeError(f"rank {rank}: {errs['peer_timeouts']} peer waits abandoned (error word [3])")
     t_ms = sum(a.elapsed_time(b) for a, b in evs)
     mv_ms, mv_n = ctx.timing_read(kmv)
     mp_ms, mp_n = ctx.timing_read(A.K_TET_MAP, reset=True)

@@ -876,6 +876,8 @@ def run_dist_map(args, rank, world, local_rank):
             mp_n += n_
         torch.cuda.synchronize()
     dist.barrier()
+    if ctx.error_counts()["peer_timeouts"]:
+        raise RuntimeError(f"rank {rank}: peer waits of the position halo abandoned (error word [3])")
     t_ms = sum(a_.elapsed_time(b_) for a_, b_ in evs)
     tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)

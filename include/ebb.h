@@ -526,17 +526,17 @@ typedef struct {
  * releases its sequence word with k + 1. */
 /* Per-source-row send lists for the fused PCG and the peer halos, built on
  * the device: for each peer k (npeers of them, ranks peers[k]) send_rows[k]
- * (U32 local rows, all < n_owned -- the source rows: owned vertices for the
+ * (U32 local rows, all < n_src -- the source rows: owned vertices for the
  * PCG and COPY halos, every row of the relation for an ADD halo --, e.g.
  * ebb_partition_local's send rows of that peer) and
  * remote_rows[k] (U32, the same length: the row of each of them in the
  * peer's local numbering, i.e. the peer's recv rows from this rank, which
  * list the same vertices in the same order), each < peer_nv[k].  Creates
- * relations <name>.off (n_owned + 1 rows, U32 "off") and <name>.dst (one row
+ * relations <name>.off (n_src + 1 rows, U32 "off") and <name>.dst (one row
  * per entry, U32 2x1 "dst" = (peer, remote row)), entries of a vertex in
  * peers[] order.  EBB_E_RANGE on a row out of bounds.  Synchronous.
  * (SURVEY §8(e) halo lists; P:1014 for the paper's single device) */
-ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_owned, int32_t npeers, const int32_t* peers,
+ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_src, int32_t npeers, const int32_t* peers,
                              const ebb_field* send_rows, const ebb_field* remote_rows, const uint64_t* peer_nv,
                              const char* name, ebb_field* send_off, ebb_field* send_dst);
 /* CUDA IPC of a library-allocated field (one process per GPU): the 64-byte

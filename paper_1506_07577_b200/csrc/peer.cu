@@ -27,20 +27,20 @@ struct Buf {
 // entries of peer k: key = local row, value = (peer rank, remote row); rows
 // out of range raise bad[0]
 __global__ void kpe_fill(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ remote, uint64_t n,
-                         uint32_t peer, uint64_t n_owned, uint64_t peer_nv, uint32_t* __restrict__ key,
+                         uint32_t peer, uint64_t n_src, uint64_t peer_nv, uint32_t* __restrict__ key,
                          uint64_t* __restrict__ val, unsigned int* __restrict__ bad) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t r = rows[i], q = remote[i];
-    if (r >= n_owned || q >= peer_nv) atomicAdd(bad, 1u);
+    if (r >= n_src || q >= peer_nv) atomicAdd(bad, 1u);
     key[i] = r;
     val[i] = ((uint64_t)q << 32) | peer;   // uint2 (peer, remote row) in little-endian order
 }
 
-// off[v] = first entry with key >= v (keys sorted), v in [0, n_owned]
-__global__ void kpe_offsets(const uint32_t* __restrict__ key, uint64_t n, uint64_t n_owned, uint32_t* __restrict__ off) {
+// off[v] = first entry with key >= v (keys sorted), v in [0, n_src]
+__global__ void kpe_offsets(const uint32_t* __restrict__ key, uint64_t n, uint64_t n_src, uint32_t* __restrict__ off) {
     const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (v > n_owned) return;
+    if (v > n_src) return;
     uint64_t lo = 0, hi = n;
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
@@ -57,12 +57,12 @@ using namespace ebb;
 
 extern "C" {
 
-ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_owned, int32_t npeers, const int32_t* peers,
+ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_src, int32_t npeers, const int32_t* peers,
                              const ebb_field* send_rows, const ebb_field* remote_rows, const uint64_t* peer_nv,
                              const char* name, ebb_field* send_off, ebb_field* send_dst) {
     Ctx* c = (Ctx*)ctx;
     EBB_DEVICE_GUARD(c);
-    if (!c || !send_off || !send_dst || npeers < 0 || npeers > EBB_MAX_RANKS || n_owned >= 0xffffffffull)
+    if (!c || !send_off || !send_dst || npeers < 0 || npeers > EBB_MAX_RANKS || n_src >= 0xffffffffull)
         return EBB_E_ARG;
     if (npeers > 0 && (!peers || !send_rows || !remote_rows || !peer_nv)) return EBB_E_ARG;
     const std::string nm = name ? name : "peer";
@@ -81,7 +81,7 @@ ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_owned, int32_t npeers, cons
     }
     if (n >= 0xffffffffull) return fail(c, EBB_E_SIZE, "peer_send_csr: too many entries");
     ebb_rel roff, rdst;
-    EBB_TRY(ebb_relation_new(ctx, (nm + ".off").c_str(), n_owned + 1, &roff));
+    EBB_TRY(ebb_relation_new(ctx, (nm + ".off").c_str(), n_src + 1, &roff));
     EBB_TRY(new_internal_field(c, roff, "off", EBB_U32, 1, 1, EBB_AOS, send_off));
     EBB_TRY(ebb_relation_new(ctx, (nm + ".dst").c_str(), n ? n : 1, &rdst));
     EBB_TRY(new_internal_field(c, rdst, "dst", EBB_U32, 2, 1, EBB_AOS, send_dst));
@@ -99,7 +99,7 @@ ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_owned, int32_t npeers, cons
         const uint64_t m = c->rels[S->rel].size;
         if (m == 0) continue;
         kpe_fill<<<grid_for(m, B), B>>>((const uint32_t*)S->ptr, (const uint32_t*)Q->ptr, m, (uint32_t)peers[k],
-                                        n_owned, peer_nv[k], key.as<uint32_t>() + at, val.as<uint64_t>() + at,
+                                        n_src, peer_nv[k], key.as<uint32_t>() + at, val.as<uint64_t>() + at,
                                         bad.as<unsigned int>());
         EBB_CUDA(c, cudaGetLastError());
         at += m;
@@ -114,12 +114,12 @@ ebb_status ebb_peer_send_csr(ebb_ctx ctx, uint64_t n_owned, int32_t npeers, cons
         EBB_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.as<uint32_t>(), key2.as<uint32_t>(),
                                                     val.as<uint64_t>(), dst, (int)n, 0, 32));
     }
-    kpe_offsets<<<grid_for(n_owned + 1, B), B>>>(key2.as<uint32_t>(), n, n_owned,
+    kpe_offsets<<<grid_for(n_src + 1, B), B>>>(key2.as<uint32_t>(), n, n_src,
                                                  (uint32_t*)c->fields[*send_off].ptr);
     EBB_CUDA(c, cudaGetLastError());
     unsigned int hb = 0;
     EBB_CUDA(c, cudaMemcpy(&hb, bad.p, 4, cudaMemcpyDeviceToHost));
-    if (hb) return fail(c, EBB_E_RANGE, "peer_send_csr: %u rows out of range (local rows < n_owned, remote < peer_nv)", hb);
+    if (hb) return fail(c, EBB_E_RANGE, "peer_send_csr: %u rows out of range (local rows < n_src, remote < peer_nv)", hb);
     return EBB_OK;
 }
 

@@ -280,7 +280,8 @@ def partition_rank(ctx, X, tets, nranks, rank, name="part", mode="overlap", debu
     read back the local-size arrays, free every global relation.
 
     Returns dict(vert_src, tet_src: the local vertices / tets as rows of the
-    INPUT X / tets; tets: the local tets in local vertex ids; n_owned: local
+    INPUT X / tets; vert_gid: the local vertices' global (renumbered, O3)
+    ids; tets: the local tets in local vertex ids; n_owned: local
     vertices [0, n_owned) are owned; send / recv: {peer: local vertex rows};
     owner_v: the global owner map in stored order (tests); vert_order /
     tet_order: stored -> input rows of the global mesh (tests))."""
@@ -319,6 +320,7 @@ def partition_rank(ctx, X, tets, nranks, rank, name="part", mode="overlap", debu
     ctx.check(L.ebb_rows_gather(h, vid.h, info.vert_gid, vsrc.h, None))
     ctx.check(L.ebb_rows_gather(h, tid.h, info.tet_gid, tsrc.h, None))
     out = dict(vert_src=vsrc.read().astype(np.int64), tet_src=tsrc.read().astype(np.int64),
+               vert_gid=Field(ctx, info.vert_gid, LV, "gid", "u32", (1, 1), A.AOS).read().astype(np.int64),
                tets=Field(ctx, info.v, LT, "v", "key", (4, 1), A.AOS).read().astype(np.int64),
                n_owned=int(info.n_owned), send={}, recv={})
     for kind, rel, rows, ptr in (("send", info.send, info.send_rows, sp), ("recv", info.recv, info.recv_rows, rp)):
@@ -369,6 +371,7 @@ class GpuRank:
         self.dtype = dtype
         self.tdt = torch.float64 if dtype == "f64" else torch.float32
         self.verts_g = vs                              # input row of every local vertex
+        self.vert_gid = part.get("vert_gid")           # global (renumbered) id of every local vertex
         owned = np.arange(vs.size) < n_owned
         mask = (np.asarray(free)[vs].astype(bool) & owned).astype(np.uint8)
         self.fem = TetFEM(ctx, np.asarray(X)[vs], part["tets"], dtype=dtype, mu=np.asarray(mu)[ts],
@@ -422,7 +425,10 @@ class GpuRank:
         owner = np.full(fem.nv, self.rank, dtype=np.int32)
         for q, rows in part["recv"].items():
             owner[rows] = q
-        gid = fem.verts.field("gid", "u32", init=np.asarray(self.verts_g).astype(np.uint32))
+        # the global ids of O4 (the renumbered order every rank shares): the
+        # computing rank of a tet is the owner of its lowest-id vertex
+        gids = self.vert_gid if self.vert_gid is not None else self.verts_g
+        gid = fem.verts.field("gid", "u32", init=np.asarray(gids).astype(np.uint32))
         own_f = fem.verts.field("owner", "i32", init=owner)
         info = A.ReverseInfo()
         ptr = (C.c_uint64 * (4 * (nranks + 1)))()

@@ -229,7 +229,9 @@ def test_reverse_add_maps_every_tet_once(ctx, P):
     ranks = _ranks(ctx, case, P, f"rv1{P}", "reverse")
     assert sum(R.n_map_tets for R in ranks) == m.nt
     assert sum(R.fem.nt for R in ranks) > m.nt                       # the overlap's ghost tets
-    assert all(R.rev_bytes["rK"] > 0 for R in ranks)
+    assert any(R.rev_bytes["rK"] > 0 for R in ranks)                 # the reverse add has work
+    # (with O4's renumbered ids a rank may have no foreign-tail rows to send:
+    # at P = 2 the owner of a tet's lowest vertex tends to own all four)
     ref = oracle.implicit_step(m, "nh", case.u[order], case.vel[order], case.mu[tet_src], case.lam[tet_src],
                                case.free[order], 1e-2, iters=50)
     dist.implicit_step(ranks, dist.LocalTransport(), "nh", h=1e-2, iters=50, variant="single")
@@ -330,3 +332,34 @@ def test_partition_and_halo_entry_points_refuse_bad_arguments(ctx):
     ptr = (C.c_uint64 * 12)()
     with pytest.raises(EbbError, match="EBB_E_TYPE"):
         ctx.check(ctx.L.ebb_partition_reverse(ctx.h, v.h, v.h, rows.h, ov.h, 2, 0, b"badrev", C.byref(rinfo), ptr))
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_partition_reverse_matches_oracle(ctx, P):
+    """ebb_partition_reverse (device) == oracle.partition_reverse bit-exact
+    for every rank and peer, in global ids: the force rows sent and received
+    (vertex ids) and the stiffness rows sent and received ((tail, head) of
+    the local edge rows), each in the order both ends derive."""
+    case = Case(n=5, model="nh")
+    m, new_of_old, tet_src, order = oracle_renumbered(case)
+    ref = oracle.partition_reverse(m.nv, m.tets, P)
+    st_v = np.empty_like(order)
+    st_v[order] = np.arange(order.size)                 # input row -> stored (global) id
+    ranks = _ranks(ctx, case, P, f"prv{P}", "reverse")
+    none = np.zeros(0, np.int64)
+    for R in ranks:
+        g = st_v[R.verts_g]                              # local vertex row -> global id
+        index = R.fem.index.read().astype(np.int64)
+        head = R.fem.head.read().astype(np.int64)
+        tail = np.repeat(np.arange(R.fem.nv), np.diff(index))
+        fsend, frecv = R.rev_lists["rf"]
+        ksend, krecv = R.rev_lists["rK"]
+        pairs = lambda rows: np.stack([g[tail[rows]], g[head[rows]]], axis=1) if len(rows) else \
+            np.zeros((0, 2), np.int64)                  # noqa: E731
+        for q in range(P):
+            if q == R.rank:
+                continue
+            assert np.array_equal(g[np.asarray(fsend.get(q, none))], ref["fsend"][R.rank][q])
+            assert np.array_equal(g[np.asarray(frecv.get(q, none))], ref["fsend"][q][R.rank])
+            assert np.array_equal(pairs(np.asarray(ksend.get(q, none))), ref["ksend"][R.rank][q])
+            assert np.array_equal(pairs(np.asarray(krecv.get(q, none))), ref["ksend"][q][R.rank])

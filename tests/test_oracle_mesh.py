@@ -12,6 +12,7 @@ import pytest
 
 import oracle
 from synth import mesh as M
+from synth import state as S
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -242,3 +243,48 @@ def test_partition_overlap_invariants(P):
         assert on == set(ov[m.tets[t]].tolist())
     if P == 1:
         assert part["ghosts"][0].size == 0 and part["ltets"][0].size == m.nt
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_partition_reverse_lists_carry_every_foreign_partial_row(P):
+    """oracle.partition_reverse pinned by the reverse-add semantics, with the
+    oracle's element map (its own edge relation) instead of the pair
+    enumeration: map each rank's computing tets alone; every force row and
+    every stiffness row with a nonzero partial sum whose vertex / tail
+    another rank q owns must be in the rank's list for q, and every listed
+    row must be one its tets touch; every tet has exactly one computing rank,
+    the owner of its lowest vertex, and the ranks' partial sums add up to the
+    single-domain map."""
+    X, tets = M.kuhn6(4)
+    X, tets = M.permute_vertices(X, tets, 2)
+    m = oracle.Mesh(X, tets)
+    u = S.stretch_noise_u(X, 4, 1)
+    mu, lam = S.materials(m.nt, 2e5, 0.3)
+    rv = oracle.partition_reverse(m.nv, m.tets, P)
+    ov, comp = rv["owner_v"], rv["comp"]
+    assert np.array_equal(comp, ov[m.tets.min(axis=1)])
+    f_all, K_all, _, _ = oracle.element_map("nh", m.X, u, m.tets, m.Dminv, m.W, mu, lam, e=m.e, ne=m.ne)
+    f_sum, K_sum = np.zeros_like(f_all), np.zeros_like(K_all)
+    for r in range(P):
+        sel = comp == r
+        f_r, K_r, _, _ = oracle.element_map("nh", m.X, u, m.tets[sel], m.Dminv[sel], m.W[sel], mu[sel], lam[sel],
+                                            e=m.e[sel], ne=m.ne)
+        f_sum += f_r
+        K_sum += K_r
+        touched_v = np.unique(m.tets[sel].ravel())
+        for q in range(P):
+            if q == r:
+                continue
+            fv = rv["fsend"][r][q]
+            nz_v = np.nonzero(np.abs(f_r).sum(axis=1) > 0)[0]
+            want_v = np.intersect1d(touched_v, np.nonzero(ov == q)[0])
+            assert np.array_equal(fv, want_v)                     # the touched vertices q owns
+            assert set(nz_v[ov[nz_v] == q]) <= set(fv.tolist())   # every nonzero partial force row
+            rows = {(int(m.tail[e]), int(m.head[e])) for e in range(m.ne)
+                    if ov[m.tail[e]] == q and np.abs(K_r[e]).sum() > 0}
+            listed = {tuple(x) for x in rv["ksend"][r][q].tolist()}
+            assert rows <= listed                                 # every nonzero partial stiffness row
+            assert all(ov[a] == q for a, _ in listed)
+            assert rv["ksend"][r][q].tolist() == sorted(rv["ksend"][r][q].tolist())
+    assert np.allclose(f_sum, f_all, rtol=0, atol=1e-9 * np.abs(f_all).max())
+    assert np.allclose(K_sum, K_all, rtol=0, atol=1e-9 * np.abs(K_all).max())

@@ -188,26 +188,29 @@ def partition(nv, tets, P, tail=None, mode="own"):
     return out
 
 
-def partition_reverse(nv, tets, P):
+def partition_reverse(nv, tets, P, key=None):
     """O4, reverse-add reading (SURVEY §8(e) "halo exchange ...
     of the partial force sums"): every tet is computed by ONE rank, the
-    owner (O4 owner_v) of its lowest-id vertex; a rank sends the partial
-    rows whose tail it does not own to the tail's owner.  Plain loops:
+    owner (O4 owner_v) of its vertex of lowest key (key = a global vertex
+    numbering every rank shares, default the vertex id); a rank sends the
+    partial rows whose tail it does not own to the tail's owner.  Plain loops:
       comp[t]        computing rank of tet t
-      fsend[r][q]    ids of the vertices owned by q that r's tets touch (the
-                     force rows r adds into q), ascending
+      fsend[r][q]    the vertices owned by q that r's tets touch (the force
+                     rows r adds into q), ascending by key
       ksend[r][q]    (tail, head) of the edge rows -- every ordered pair of
                      vertices of one of r's tets, self pairs included --
-                     whose tail q owns, ascending by (tail, head)
+                     whose tail q owns, ascending by (key[tail], key[head])
     r receives from q exactly what q sends to r (frecv[r][q] = fsend[q][r])."""
     tets = _i64(tets)
+    key = np.arange(nv, dtype=np.int64) if key is None else _i64(key)
     owner_v = partition(nv, tets, P, mode="overlap")["owner_v"]
     T = tets.shape[0]
     comp = np.empty(T, np.int64)
     fs = [[set() for _ in range(P)] for _ in range(P)]
     ks = [[set() for _ in range(P)] for _ in range(P)]
     for t in range(T):
-        r = int(owner_v[min(tets[t])])
+        lo = min(tets[t], key=lambda v: key[v])
+        r = int(owner_v[lo])
         comp[t] = r
         for a in tets[t]:
             q = int(owner_v[a])
@@ -216,8 +219,9 @@ def partition_reverse(nv, tets, P):
             fs[r][q].add(int(a))
             for b in tets[t]:
                 ks[r][q].add((int(a), int(b)))
-    fsend = [[np.array(sorted(fs[r][q]), np.int64) for q in range(P)] for r in range(P)]
-    ksend = [[np.array(sorted(ks[r][q]), np.int64).reshape(-1, 2) for q in range(P)] for r in range(P)]
+    fsend = [[np.array(sorted(fs[r][q], key=lambda v: key[v]), np.int64) for q in range(P)] for r in range(P)]
+    ksend = [[np.array(sorted(ks[r][q], key=lambda e: (key[e[0]], key[e[1]])), np.int64).reshape(-1, 2)
+              for q in range(P)] for r in range(P)]
     return dict(owner_v=owner_v, comp=comp, fsend=fsend, ksend=ksend)
 
 

@@ -425,10 +425,13 @@ class GpuRank:
         owner = np.full(fem.nv, self.rank, dtype=np.int32)
         for q, rows in part["recv"].items():
             owner[rows] = q
-        # the global ids of O4 (the renumbered order every rank shares): the
-        # computing rank of a tet is the owner of its lowest-id vertex
-        gids = self.vert_gid if self.vert_gid is not None else self.verts_g
-        gid = fem.verts.field("gid", "u32", init=np.asarray(gids).astype(np.uint32))
+        # the key every rank shares for "the tet's lowest vertex" and the list
+        # order: the INPUT row ids (scrambled w.r.t. the SFC order, so the
+        # computing ranks stay balanced; with the renumbered ids the lowest
+        # vertex's owner is biased towards the lower ranks -- measured: the
+        # last rank computes no foreign rows and the map's slowest rank is
+        # 3-10 % slower, profiles/r02_dist_variants_renumbered_key.jsonl)
+        gid = fem.verts.field("gid", "u32", init=np.asarray(self.verts_g).astype(np.uint32))
         own_f = fem.verts.field("owner", "i32", init=owner)
         info = A.ReverseInfo()
         ptr = (C.c_uint64 * (4 * (nranks + 1)))()

@@ -260,9 +260,11 @@ def test_partition_reverse_lists_carry_every_foreign_partial_row(P):
     m = oracle.Mesh(X, tets)
     u = S.stretch_noise_u(X, 4, 1)
     mu, lam = S.materials(m.nt, 2e5, 0.3)
-    rv = oracle.partition_reverse(m.nv, m.tets, P)
+    key = np.random.default_rng(3).permutation(m.nv)         # any shared global numbering
+    rv = oracle.partition_reverse(m.nv, m.tets, P, key=key)
     ov, comp = rv["owner_v"], rv["comp"]
-    assert np.array_equal(comp, ov[m.tets.min(axis=1)])
+    lo = m.tets[np.arange(m.nt), np.argmin(key[m.tets], axis=1)]
+    assert np.array_equal(comp, ov[lo])
     f_all, K_all, _, _ = oracle.element_map("nh", m.X, u, m.tets, m.Dminv, m.W, mu, lam, e=m.e, ne=m.ne)
     f_sum, K_sum = np.zeros_like(f_all), np.zeros_like(K_all)
     for r in range(P):
@@ -278,13 +280,15 @@ def test_partition_reverse_lists_carry_every_foreign_partial_row(P):
             fv = rv["fsend"][r][q]
             nz_v = np.nonzero(np.abs(f_r).sum(axis=1) > 0)[0]
             want_v = np.intersect1d(touched_v, np.nonzero(ov == q)[0])
-            assert np.array_equal(fv, want_v)                     # the touched vertices q owns
+            assert np.array_equal(np.sort(fv), want_v)            # the touched vertices q owns
+            assert np.array_equal(key[fv], np.sort(key[fv]))      # in key order
             assert set(nz_v[ov[nz_v] == q]) <= set(fv.tolist())   # every nonzero partial force row
             rows = {(int(m.tail[e]), int(m.head[e])) for e in range(m.ne)
                     if ov[m.tail[e]] == q and np.abs(K_r[e]).sum() > 0}
             listed = {tuple(x) for x in rv["ksend"][r][q].tolist()}
             assert rows <= listed                                 # every nonzero partial stiffness row
             assert all(ov[a] == q for a, _ in listed)
-            assert rv["ksend"][r][q].tolist() == sorted(rv["ksend"][r][q].tolist())
+            kl = [(key[a], key[b]) for a, b in rv["ksend"][r][q].tolist()]
+            assert kl == sorted(kl) and len(set(kl)) == len(kl)
     assert np.allclose(f_sum, f_all, rtol=0, atol=1e-9 * np.abs(f_all).max())
     assert np.allclose(K_sum, K_all, rtol=0, atol=1e-9 * np.abs(K_all).max())

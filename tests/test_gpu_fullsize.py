@@ -236,3 +236,38 @@ def test_t10m_peer_pcg_two_ranks(ctx, t10m, body):
     assert not np.isnan(dv).any()
     assert rel_l2(dv, dv_ref) <= 1e-8                           # north_star's CG-iterate bar
     assert rel_l2(u, u_ref) <= 1e-8
+
+
+def test_t10m_transport_free_reverse_add_step(ctx, t10m):
+    """The whole transport-free distributed step at full size with north_star's
+    reverse add: T10M over 2 emulated ranks, each tet mapped once, the
+    partial f / K rows of ghost tails added into their owners with
+    red.global.add over peer memory (PeerHalo ADD), the fused peer PCG
+    (Saad body): dv and u on every local row equal the single-domain step's
+    (north_star's 1e-8 CG bar)."""
+    from paper_1506_07577_b200 import dist
+    from paper_1506_07577_b200.tetfem import TetFEM
+    d = t10m
+    w = d["w"]
+    v0 = np.zeros_like(d["u"])
+    ranks = []
+    for r in range(2):
+        part = dist.partition_rank(ctx, d["X"], d["tets"], 2, r, name=f"t10mrv{r}")
+        ranks.append(dist.GpuRank(ctx, r, part, d["X"], d["free"], d["u"], v0, d["mu"], d["lam"], rho=w["rho"],
+                                  name=f"t10mrvr{r}", map_variant="reverse", nranks=2))
+    assert sum(R.n_map_tets for R in ranks) == d["tets"].shape[0]     # every tet mapped once
+    peer = dist.PeerPCG(ranks, variant="saad")
+    prev = (dist.PeerHalo(ranks, "rf"), dist.PeerHalo(ranks, "rK"))
+    dist.implicit_step(ranks, None, w["model"], h=w["h"], iters=w["cg_iters"], variant="peer", peer=peer,
+                       peer_rev=prev)
+    assert ctx.error_counts()["peer_timeouts"] == 0
+    fem = TetFEM(ctx, d["X"], d["tets"], dtype="f64", mu=d["mu"], lam=d["lam"], rho=w["rho"], free=d["free"],
+                 u=d["u"], name="t10mrvref")
+    fem.implicit_step(w["model"], h=w["h"], iters=w["cg_iters"])
+    dv_ref = fem.to_input_order(fem.dv.read())
+    u_ref = fem.to_input_order(fem.u.read())
+    for R in ranks:
+        ids, dv = R.local_values(R.fem.dv)
+        _, u = R.local_values(R.fem.u)
+        assert rel_l2(dv, dv_ref[ids]) <= 1e-8
+        assert rel_l2(u, u_ref[ids]) <= 1e-8
